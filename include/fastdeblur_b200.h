@@ -1,0 +1,158 @@
+/*
+ * fastdeblur_b200 — C ABI of the B200-native transform + filter + GCV path.
+ *
+ * Drop-in boundary for the reference's operator API (namespace fastdeblur in
+ * /root/reference/proj/core/include/fastdeblur/*.hpp).  The reference has no
+ * C ABI; each entry point below names the C++ function it replaces
+ * (file:line) and keeps its argument meaning and error behaviour:
+ * status 0 ok, 2 ValidationError (incl. Dimension/Parameter), 3
+ * DegenerateError, 1 anything else — the CLI's exit-code mapping
+ * (tools/fastdeblur.cpp:442-451).  fd_last_error() returns the thread-local
+ * message.
+ *
+ * Memory: every array argument of an apply is a caller-owned DEVICE pointer
+ * (cudaMalloc / torch CUDA tensor), row-major; complex arrays are interleaved
+ * (re, im) doubles.  Host pointers appear only in the create calls (PSF
+ * weights) and fd_gcv_minimize_host.  `stream` is a cudaStream_t (NULL =
+ * legacy default stream).  Calls that must report a DegenerateError found on
+ * the device (GCV denominators) synchronise the stream before returning.
+ *
+ * Threading: operators and smoothers are immutable after creation and may be
+ * used concurrently on distinct streams / buffers (boundary.hpp:42-43,
+ * operators.hpp:68-69); scratch memory is stream-ordered per call.
+ *
+ * Batching: `count` independent items (signals for 1D operators, images for
+ * 2D operators) laid out contiguously: item b starts at b*N (N = n or n1*n2).
+ */
+#ifndef FASTDEBLUR_B200_H
+#define FASTDEBLUR_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes (fastdeblur.cpp:442-451) */
+#define FD_OK 0
+#define FD_ERR_OTHER 1
+#define FD_ERR_VALIDATION 2
+#define FD_ERR_DEGENERATE 3
+
+/* BoundaryCondition (operators.hpp:15-21) */
+#define FD_BC_PERIODIC 0
+#define FD_BC_REFLECTIVE 1
+#define FD_BC_ANTIREFLECTIVE 2
+#define FD_BC_HOC_COSINE 3
+#define FD_BC_HOC_FOURIER 4
+
+/* SmootherKind (regularize.hpp:15); FIRST_DIFFERENCE is an extension
+ * (s = sqrt(2 - 2 cos node), BASELINE config 1) */
+#define FD_SMOOTH_IDENTITY 0
+#define FD_SMOOTH_LAPLACIAN 1
+#define FD_SMOOTH_FIRST_DIFFERENCE 2
+
+typedef struct fd_op fd_op;
+typedef struct fd_smoother fd_smoother;
+
+const char* fd_last_error(void);
+int fd_version(void);
+
+/* parse_boundary_condition (operators.cpp:232-239); -1 if unknown */
+int fd_parse_bc(const char* name);
+
+/* BC for a polynomial-preservation degree (north_star "BC degree d"):
+ * d=1 -> antireflective (symmetric PSF only, operators.cpp:173-176),
+ * d=2 -> hoc-cosine (symmetric) or hoc-fourier (any PSF).
+ * Other degrees are not in the reference: ValidationError. */
+int fd_bc_for_degree(int degree, int psf_symmetric, int* bc);
+
+/* build_operator(make_psf(weights, normalize), n, bc)   operators.cpp:404-412,
+ * psf.cpp:10-38.  Validation errors as validate_build (operators.cpp:173-187). */
+int fd_op_create_1d(const double* psf, int len, int normalize, int n, int bc, fd_op** op);
+
+/* build_operator_2d(make_psf2d(weights, rows, cols, normalize), n1, n2, bc)
+ * multidim.cpp:413-426; eigenvalues by the three-step scheme (311-376). */
+int fd_op_create_2d(const double* psf, int rows, int cols, int normalize, int n1, int n2, int bc,
+                    fd_op** op);
+
+/* build_operator_2d for the separable mask separable_psf2d(a, b)
+ * (multidim.cpp:226-233): eigenvalues are kept as the outer product of the
+ * marginal 1D eigenvalue vectors (equal to eigenvalues_2d for separable
+ * masks, test_multidim.cpp:106-123), so no n1*n2 eigenvalue array is stored. */
+int fd_op_create_2d_separable(const double* psf_a, int len_a, const double* psf_b, int len_b,
+                              int normalize, int n1, int n2, int bc, fd_op** op);
+
+int fd_op_destroy(fd_op* op);
+
+/* dim (1|2), n1, n2 (1 for 1D), bc, complex basis flag */
+int fd_op_info(const fd_op* op, int* dim, int* n1, int* n2, int* bc, int* is_complex);
+
+/* operator_eigenvalues / eigenvalues_2d (operators.hpp:41-42, multidim.hpp:58-60):
+ * writes N complex values (interleaved) to the device array d. */
+int fd_op_eigenvalues(const fd_op* op, double* d, void* stream);
+
+/* smoothing_eigenvalues(_2d) (regularize.cpp:155-175, multidim.cpp:433-460);
+ * ValidationError on a joint null space with the operator. */
+int fd_smoother_create(const fd_op* op, int kind, fd_smoother** L);
+/* SmoothingOperator{kind, eigenvalues} aggregate with caller-supplied
+ * eigenvalues (regularize.hpp:20-23); s is a HOST array of N doubles. */
+int fd_smoother_create_custom(const fd_op* op, const double* s, fd_smoother** L);
+int fd_smoother_destroy(fd_smoother* L);
+/* writes the N smoother eigenvalues to the device array s */
+int fd_smoother_eigenvalues(const fd_smoother* L, double* s, void* stream);
+
+/* SpectralBasis::analyze = T_X^{-1} (operators.cpp:303-312, boundary.cpp:338-375)
+ * and tensor_apply(..., Direction::inverse) for 2D (multidim.cpp:275-302).
+ * in: real (in_complex = 0) or complex; out: complex for complex bases
+ * (periodic, hoc-fourier), real otherwise. */
+int fd_analyze(const fd_op* op, const void* in, int in_complex, void* out, long long count,
+               void* stream);
+
+/* SpectralBasis::synthesize = T_X (operators.cpp:291-301, boundary.cpp:310-336);
+ * in: complex for complex bases, real otherwise.  out_complex = 0 keeps the
+ * real part and, if imag_residue != NULL, writes ||Im||_2 per item. */
+int fd_synthesize(const fd_op* op, const void* in, void* out, int out_complex,
+                  double* imag_residue, long long count, void* stream);
+
+/* blur_apply(_2d) (operators.cpp:317-343, multidim.cpp:381-408): real f -> real A f */
+int fd_matvec(const fd_op* op, const double* f, double* out, double* imag_residue,
+              long long count, void* stream);
+
+/* tikhonov_solve(_2d) (regularize.cpp:209-239, multidim.cpp:462-499) with one
+ * mu per item (device array mu, each > 0: ParameterError otherwise). */
+int fd_tikhonov(const fd_op* op, const fd_smoother* L, const double* g, const double* mu,
+                double* out, double* imag_residue, long long count, void* stream);
+
+/* gcv_value(_2d) (regularize.cpp:255-269, multidim.cpp:501-519): G per item */
+int fd_gcv_value(const fd_op* op, const fd_smoother* L, const double* g, double mu, double* G,
+                 long long count, void* stream);
+
+/* gcv_select(_2d) (regularize.cpp:353-374, multidim.cpp:521-546) with the
+ * gcv_minimize semantics (regularize.cpp:281-351) per item: mu (device, per
+ * item), best_k (device int, per item; -1 never), curve (device
+ * count x grid_count G values, or NULL). */
+int fd_gcv_select(const fd_op* op, const fd_smoother* L, const double* g, double mu_min,
+                  double mu_max, int grid_count, double* mu, int* best_k, double* curve,
+                  long long count, void* stream);
+
+/* deblur(_2d) (pipeline.cpp:732-778): GCV-selected (use_gcv = 1) or fixed mu,
+ * then the Tikhonov solve.  Outputs per item: restored (device, N each),
+ * mu_used, best_k (or NULL), curve (or NULL), imag_residue (or NULL). */
+int fd_deblur(const fd_op* op, const fd_smoother* L, const double* g, int use_gcv,
+              double fixed_mu, double mu_min, double mu_max, int grid_count, double* restored,
+              double* mu_used, int* best_k, double* curve, double* imag_residue, long long count,
+              void* stream);
+
+/* The same selection logic the kernels run (gcv_minimize, regularize.cpp:281-351),
+ * on the host with a caller-supplied G: for the CPU test suite. */
+typedef double (*fd_gcv_fn)(double mu, void* ctx);
+int fd_gcv_minimize_host(fd_gcv_fn G, void* ctx, double mu_min, double mu_max, int grid_count,
+                         double* mu, int* best_k, double* curve);
+
+/* number of kernels this library launched since load (for bench accounting) */
+long long fd_kernel_launches(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASTDEBLUR_B200_H */

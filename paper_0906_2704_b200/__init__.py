@@ -1,0 +1,10 @@
+"""B200-native transform + filter + GCV restoration path of arXiv 0906.2704
+(reference: fastdeblur).  The product is libfdb200.so (sm_100a kernels behind
+the C ABI in include/fastdeblur_b200.h); ``fastdeblur`` mirrors the reference
+operator API over it."""
+from .fastdeblur import (  # noqa: F401
+    BC, SMOOTHER, BlurOperator, DegenerateError, FastDeblurError, GcvResult, GcvSearch,
+    MuChoice, RestorationReport, Smoother, ValidationError, bc_for_degree, blur_apply,
+    build_operator, build_operator_2d, build_operator_2d_separable, deblur, gcv_select,
+    gcv_value, kernel_launches, lib, smoother_from_eigenvalues, smoothing_eigenvalues,
+    tikhonov_solve)

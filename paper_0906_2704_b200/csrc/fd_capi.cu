@@ -1,0 +1,1415 @@
+// C ABI (include/fastdeblur_b200.h) and host orchestration of the sm_100a
+// kernels in fd_kernels.cu.  Host code only builds O(n) operator metadata
+// exactly as the reference does (boundary column q, boundary rows c_a/c_b,
+// capacitance check: boundary.cpp:139-303) and validates arguments; every
+// transform, filter, eigenvalue and GCV evaluation runs on the GPU.  There is
+// no CPU fallback: without a CUDA device every call fails with status 1.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/fastdeblur_b200.h"
+#include "fd_fft.cuh"
+#include "fd_gcv_core.h"
+#include "fd_internal.h"
+#include "fd_kernels.cuh"
+
+
+using namespace fdb;
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+thread_local std::string g_err;
+std::atomic<long long> g_launches{0};
+
+struct FdError : std::runtime_error {
+  int code;
+  FdError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void validation(const std::string& m) { throw FdError(FD_ERR_VALIDATION, m); }
+[[noreturn]] void degenerate(const std::string& m) { throw FdError(FD_ERR_DEGENERATE, m); }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw FdError(FD_ERR_OTHER, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void launched(const char* what) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  ck(cudaGetLastError(), what);
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return FD_OK;
+  } catch (const FdError& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FD_ERR_OTHER;
+  }
+}
+
+using cplx = std::complex<double>;
+
+// ---------------------------------------------------------------------------
+// device memory helpers
+// ---------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+template <class T>
+T* dev_alloc(std::vector<std::unique_ptr<DevBuf>>& owner, size_t count) {
+  auto b = std::make_unique<DevBuf>();
+  ck(cudaMalloc(&b->p, std::max<size_t>(count, 1) * sizeof(T)), "cudaMalloc");
+  T* r = static_cast<T*>(b->p);
+  owner.push_back(std::move(b));
+  return r;
+}
+
+template <class T>
+T* dev_upload(std::vector<std::unique_ptr<DevBuf>>& owner, const std::vector<T>& h) {
+  T* d = dev_alloc<T>(owner, h.size());
+  if (!h.empty()) ck(cudaMemcpy(d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+  return d;
+}
+
+// stream-ordered scratch for one call
+struct Scratch {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Scratch(cudaStream_t s) : st(s) {}
+  template <class T>
+  T* get(size_t count) {
+    void* p = nullptr;
+    ck(cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), st), "cudaMallocAsync");
+    ptrs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  ~Scratch() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+};
+
+void init_runtime_once() {
+  static std::once_flag once;
+  static bool ok = false;
+  std::call_once(once, [] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    const int kmax = 227 * 1024;
+    cudaFuncSetAttribute(k_analyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+    cudaFuncSetAttribute(k_synth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+    cudaFuncSetAttribute(k_bhat, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+    ok = true;
+  });
+  if (!ok) throw FdError(FD_ERR_OTHER, "no CUDA device available (fastdeblur_b200 has no CPU path)");
+}
+
+// ---------------------------------------------------------------------------
+// host-side PSF / grid metadata (restated exactly as the reference computes it)
+// ---------------------------------------------------------------------------
+struct HostPsf {
+  std::vector<double> w;
+  int m = 0;
+  bool symmetric = false;
+};
+
+// make_psf (psf.cpp:10-38)
+HostPsf make_psf(const double* w, int len, bool normalize) {
+  if (len < 1 || len % 2 == 0) validation("psf must have odd length 2m+1");
+  HostPsf p;
+  p.w.assign(w, w + len);
+  double sum = 0.0;
+  for (double x : p.w) {
+    if (!std::isfinite(x)) validation("psf weights must be finite");
+    sum += x;
+  }
+  if (normalize) {
+    if (sum == 0.0) validation("psf weights sum to zero; cannot normalize");
+    for (double& x : p.w) x /= sum;
+  } else if (std::abs(sum - 1.0) > 1e-8) {
+    validation("psf weights must sum to 1 (pass normalize to rescale)");
+  }
+  p.m = len / 2;
+  p.symmetric = true;
+  for (int j = 1; j <= p.m; ++j)
+    if (p.w[p.m + j] != p.w[p.m - j]) {
+      p.symmetric = false;
+      break;
+    }
+  return p;
+}
+
+bool needs_symmetric(int bc) {
+  return bc == BC_REFLECTIVE || bc == BC_ANTIREFLECTIVE || bc == BC_HOC_COSINE;
+}
+bool is_complex_bc(int bc) { return bc == BC_PERIODIC || bc == BC_HOC_FOURIER; }
+bool is_corrected(int bc) {
+  return bc == BC_ANTIREFLECTIVE || bc == BC_HOC_COSINE || bc == BC_HOC_FOURIER;
+}
+const char* bc_name(int bc) {
+  static const char* names[] = {"periodic", "reflective", "antireflective", "hoc-cosine",
+                                "hoc-fourier"};
+  return (bc >= 0 && bc < 5) ? names[bc] : "?";
+}
+void check_bc(int bc) {
+  if (bc < 0 || bc > 4) validation("unknown boundary condition");
+}
+
+// validate_build (operators.cpp:173-187)
+void validate_build(const HostPsf& psf, int n, int bc) {
+  check_bc(bc);
+  if (needs_symmetric(bc) && !psf.symmetric)
+    validation(std::string(bc_name(bc)) + " boundary conditions require a symmetric psf");
+  const int support = 2 * psf.m + 1;
+  if (is_corrected(bc)) {
+    if (n < 5) validation("boundary-corrected operators need n >= 5");
+    if (support > n - 2)
+      validation("psf support 2m+1 must be <= n-2 for boundary-corrected operators");
+  } else {
+    if (n < 1) validation("operator order must be positive");
+    if (support > n) validation("psf support 2m+1 must be <= n");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// axis construction
+// ---------------------------------------------------------------------------
+int ceil_pow2(long long v, int* logv) {
+  int l = 0;
+  long long p = 1;
+  while (p < v) {
+    p <<= 1;
+    ++l;
+  }
+  *logv = l;
+  return (int)p;
+}
+
+size_t smem_bytes(int M) { return (size_t)(pidx(M) + 1) * sizeof(double2) + 32 * 8 * 8 + 8 * 16; }
+int line_threads(int M) {
+  int t = M / 16;
+  if (t < 64) t = 64;
+  if (t > 512) t = 512;
+  return t;
+}
+
+struct Axis {
+  AxisDev dev{};
+  std::vector<std::unique_ptr<DevBuf>> bufs;
+  std::vector<double> q_host;
+};
+
+void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
+  const int blocks = io.in_cplx ? io.gi.count : (io.gi.count + 1) / 2;
+  if (blocks == 0) return;
+  k_analyze<<<blocks, line_threads(ax.fft.M), smem_bytes(ax.fft.M), st>>>(ax, io);
+  launched("k_analyze");
+}
+
+void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cudaStream_t st) {
+  const int blocks = ax.cplx ? io.gi.count : (io.gi.count + 1) / 2;
+  if (blocks == 0) return;
+  k_synth<<<blocks, line_threads(ax.fft.M), smem_bytes(ax.fft.M), st>>>(ax, io, sa);
+  launched("k_synth");
+}
+
+Lines lines_1d(int n, long long count) {
+  Lines g{};
+  g.item_stride = n;
+  g.line_stride = 0;
+  g.elem_stride = 1;
+  g.per_item = 1;
+  g.count = (int)count;
+  return g;
+}
+
+// interior-only view of an axis: the plain transform X (or X^{-1}) of length m
+AxisDev interior_view(const AxisDev& a) {
+  AxisDev v = a;
+  v.n = a.m;
+  v.bordered = 0;
+  v.correction = 0;
+  return v;
+}
+
+void check_capacitance(const cplx m[4]) {  // boundary.cpp:139-150
+  const double t = std::norm(m[0]) + std::norm(m[1]) + std::norm(m[2]) + std::norm(m[3]);
+  const cplx det = m[0] * m[3] - m[1] * m[2];
+  const double d = std::norm(det);
+  const double r = std::sqrt(std::max(t * t - 4.0 * d, 0.0));
+  const double smax = std::sqrt((t + r) / 2.0);
+  const double smin2 = (t - r) / 2.0;
+  if (smin2 <= 0.0 || smax / std::sqrt(smin2) > 1e12)
+    degenerate("degenerate transform: 2x2 capacitance matrix is singular or ill-conditioned");
+}
+
+std::unique_ptr<Axis> build_axis(int bc, int n) {
+  auto A = std::make_unique<Axis>();
+  AxisDev& d = A->dev;
+  d.n = n;
+  d.bordered = is_corrected(bc);
+  d.cplx = is_complex_bc(bc);
+  d.m = d.bordered ? n - 2 : n;
+  d.kind = (bc == BC_PERIODIC || bc == BC_HOC_FOURIER) ? IK_FOURIER
+           : bc == BC_ANTIREFLECTIVE                  ? IK_SINE
+                                                      : IK_COS;
+  d.correction = d.bordered && bc != BC_ANTIREFLECTIVE;
+  const int m = d.m;
+  const int L = d.kind == IK_SINE ? 2 * (m + 1) : m;
+  int logM = 0;
+  const int M = ceil_pow2(2LL * L - 1, &logM);
+  if (M > 8192)
+    validation("order " + std::to_string(n) + " exceeds this build's on-chip transform limit "
+               "(interior DFT length <= 4096)");
+  d.fft.L = L;
+  d.fft.M = M;
+  d.fft.logM = logM;
+  double2* chirp = dev_alloc<double2>(A->bufs, L);
+  double2* tw = dev_alloc<double2>(A->bufs, std::max(M / 2, 1));
+  double2* b = dev_alloc<double2>(A->bufs, M);
+  double2* bhat = dev_alloc<double2>(A->bufs, M);
+  double2* dct_tw = dev_alloc<double2>(A->bufs, d.kind == IK_COS ? m : 1);
+  d.fft.chirp = chirp;
+  d.fft.tw = tw;
+  d.fft.bhat = bhat;
+  d.dct_tw = dct_tw;
+  k_init_tables<<<std::max(1, std::min(1024, (M + 255) / 256)), 256>>>(
+      L, M, chirp, tw, b, d.kind == IK_COS ? m : 0, dct_tw);
+  launched("k_init_tables");
+  k_bhat<<<1, line_threads(M), smem_bytes(M)>>>(d.fft, b, bhat);
+  launched("k_bhat");
+
+  if (!d.bordered) {
+    ck(cudaDeviceSynchronize(), "axis tables");
+    return A;
+  }
+  // ---- boundary column and rows (boundary.cpp:218-303) ----
+  double ga, gb;
+  std::vector<double> pts(n), q(n);
+  if (bc == BC_ANTIREFLECTIVE) {
+    ga = 0.0;
+    gb = kPi;
+    for (int i = 0; i < n; ++i) pts[i] = i * kPi / (n - 1);
+    for (int i = 0; i < n; ++i) q[i] = 1.0 - static_cast<double>(i) / (n - 1);
+  } else if (bc == BC_HOC_COSINE) {
+    ga = -kPi / (2 * n - 4);
+    gb = (2 * n - 3) * kPi / (2 * n - 4);
+    for (int i = 0; i < n; ++i) pts[i] = (2 * i - 1) * kPi / (2 * n - 4);
+    for (int i = 0; i < n; ++i) {
+      const double t = gb - pts[i];
+      q[i] = t * t;
+    }
+  } else {
+    ga = -2.0 * kPi / (n - 2);
+    gb = 2.0 * kPi;
+    for (int i = 0; i < n; ++i) pts[i] = (i - 1) * 2.0 * kPi / (n - 2);
+    for (int i = 0; i < n; ++i) {
+      const double t = gb - pts[i];
+      q[i] = t * t;
+    }
+    q.back() = 0.0;
+  }
+  double norm = 0.0;
+  for (double x : q) norm += x * x;
+  norm = std::sqrt(norm);
+  for (double& x : q) x /= norm;
+  q.back() = 0.0;
+  const double alpha = 1.0 / q[0];
+  d.alpha = alpha;
+  A->q_host = q;
+  d.q = dev_upload(A->bufs, q);
+
+  std::vector<cplx> c_a(m), c_b(m);
+  if (bc == BC_HOC_COSINE) {
+    for (int j = 0; j < m; ++j) {
+      const double scale = std::sqrt((j == 0 ? 1.0 : 2.0) / (n - 2));
+      c_a[j] = scale * std::cos(j * ga);
+      c_b[j] = (j % 2 == 0) ? c_a[j] : -c_a[j];
+    }
+  } else if (bc == BC_HOC_FOURIER) {
+    const double scale = 1.0 / std::sqrt(static_cast<double>(n - 2));
+    for (int j = 0; j < m; ++j) {
+      c_a[j] = std::polar(scale, j * ga);
+      c_b[j] = cplx{scale, 0.0};
+    }
+  }
+  (void)gb;
+
+  // v = -alpha X qhat, w = -alpha X J qhat: two real lines through X on the GPU
+  const AxisDev iv = interior_view(d);
+  std::vector<double> qq(2 * (size_t)m);
+  for (int i = 0; i < m; ++i) {
+    qq[i] = q[i + 1];
+    qq[m + i] = q[m - i];
+  }
+  std::vector<std::unique_ptr<DevBuf>> tmp;
+  double* dq = dev_upload(tmp, qq);
+  double2* dx = dev_alloc<double2>(tmp, 2 * (size_t)m);
+  LineIO io{};
+  io.in = dq;
+  io.out = dx;
+  io.gi = lines_1d(m, 2);
+  io.go = lines_1d(m, 2);
+  io.in_cplx = 0;
+  io.out_cplx = 1;
+  launch_analyze(iv, io, 0);
+  std::vector<double2> xq(2 * (size_t)m);
+  ck(cudaMemcpy(xq.data(), dx, xq.size() * sizeof(double2), cudaMemcpyDeviceToHost), "v/w");
+  std::vector<cplx> v(m), w(m);
+  for (int i = 0; i < m; ++i) {
+    v[i] = cplx(xq[i].x, d.cplx ? xq[i].y : 0.0) * (-alpha);
+    w[i] = cplx(xq[m + i].x, d.cplx ? xq[m + i].y : 0.0) * (-alpha);
+  }
+  if (!d.cplx)
+    for (int i = 0; i < m; ++i) {  // real scalar semantics: v[i] *= -alpha
+      v[i] = cplx(xq[i].x * -alpha, 0.0);
+      w[i] = cplx(xq[m + i].x * -alpha, 0.0);
+    }
+
+  // row_a = X^T c_a (C^T c for the cosine basis, F c for Fourier)
+  std::vector<cplx> row_a(m), row_b(m);
+  cplx cav[4] = {0.0, 0.0, 0.0, 0.0};
+  cplx cap[4] = {1.0, 0.0, 0.0, 1.0};
+  if (d.correction) {
+    std::vector<double2> cc(2 * (size_t)m);
+    for (int i = 0; i < m; ++i) {
+      cc[i] = make_double2(c_a[i].real(), c_a[i].imag());
+      cc[m + i] = make_double2(c_b[i].real(), c_b[i].imag());
+    }
+    double2* dc = dev_upload(tmp, cc);
+    double2* dr = dev_alloc<double2>(tmp, 2 * (size_t)m);
+    LineIO io2{};
+    io2.gi = lines_1d(m, 2);
+    io2.go = lines_1d(m, 2);
+    if (d.cplx) {  // F c (complex input, one line per CTA)
+      io2.in = dc;
+      io2.out = dr;
+      io2.in_cplx = 1;
+      io2.out_cplx = 1;
+      launch_analyze(iv, io2, 0);
+    } else {  // C^T c: real lines through the synthesis kernel
+      std::vector<double> cr(2 * (size_t)m);
+      for (int i = 0; i < 2 * m; ++i) cr[i] = cc[i].x;
+      double* dcr = dev_upload(tmp, cr);
+      io2.in = dcr;
+      io2.out = dr;
+      io2.in_cplx = 0;
+      io2.out_cplx = 1;
+      SynthArgs sa{};
+      launch_synth(iv, io2, sa, 0);
+    }
+    std::vector<double2> rr(2 * (size_t)m);
+    ck(cudaMemcpy(rr.data(), dr, rr.size() * sizeof(double2), cudaMemcpyDeviceToHost), "rows");
+    for (int i = 0; i < m; ++i) {
+      row_a[i] = cplx(rr[i].x, d.cplx ? rr[i].y : 0.0);
+      row_b[i] = cplx(rr[m + i].x, d.cplx ? rr[m + i].y : 0.0);
+    }
+    cplx ca_v = 0.0, ca_w = 0.0, cb_v = 0.0, cb_w = 0.0;
+    for (int i = 0; i < m; ++i) {
+      ca_v += c_a[i] * v[i];
+      ca_w += c_a[i] * w[i];
+      cb_v += c_b[i] * v[i];
+      cb_w += c_b[i] * w[i];
+    }
+    if (!d.cplx) {  // real arithmetic, as the double instantiation does
+      double a1 = 0, a2 = 0, b1 = 0, b2 = 0;
+      for (int i = 0; i < m; ++i) {
+        a1 += c_a[i].real() * v[i].real();
+        a2 += c_a[i].real() * w[i].real();
+        b1 += c_b[i].real() * v[i].real();
+        b2 += c_b[i].real() * w[i].real();
+      }
+      ca_v = a1, ca_w = a2, cb_v = b1, cb_w = b2;
+    }
+    cav[0] = ca_v, cav[1] = ca_w, cav[2] = cb_v, cav[3] = cb_w;
+    cap[0] = cplx(1.0) + ca_v, cap[1] = ca_w, cap[2] = cb_v, cap[3] = cplx(1.0) + cb_w;
+    check_capacitance(cap);
+  }
+  for (int k = 0; k < 4; ++k) {
+    d.cav[k] = make_double2(cav[k].real(), cav[k].imag());
+    d.cap[k] = make_double2(cap[k].real(), cap[k].imag());
+  }
+  auto up = [&](const std::vector<cplx>& h) {
+    std::vector<double2> t(h.size());
+    for (size_t i = 0; i < h.size(); ++i) t[i] = make_double2(h[i].real(), h[i].imag());
+    return static_cast<const double2*>(dev_upload(A->bufs, t));
+  };
+  d.v = up(v);
+  d.w = up(w);
+  d.row_a = up(row_a);
+  d.row_b = up(row_b);
+  d.c_a = up(c_a);
+  d.c_b = up(c_b);
+  ck(cudaDeviceSynchronize(), "axis build");
+  return A;
+}
+
+std::vector<double2> eig1d(const HostPsf& p, int n, int bc,
+                           std::vector<std::unique_ptr<DevBuf>>& owner, double2** dptr) {
+  std::vector<std::unique_ptr<DevBuf>> tmp;
+  double* dh = dev_upload(tmp, p.w);
+  double2* d = dev_alloc<double2>(owner, n);
+  k_eigenvalues_1d<<<std::max(1, std::min(1024, (n + 255) / 256)), 256>>>(dh, p.m,
+                                                                           p.symmetric, bc, n, d);
+  launched("k_eigenvalues_1d");
+  std::vector<double2> h(n);
+  ck(cudaMemcpy(h.data(), d, n * sizeof(double2), cudaMemcpyDeviceToHost), "eigenvalues");
+  *dptr = d;
+  return h;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// handles
+// ---------------------------------------------------------------------------
+struct fd_op {
+  int dim = 1, n1 = 0, n2 = 1, bc = 0, cplx = 0;
+  int sep = 0;                      // 2D separable eigenvalues
+  std::unique_ptr<Axis> ax1, ax2;   // ax1: order n1 (1D axis / 2D column pass), ax2: order n2
+  double2* d = nullptr;             // 1D: n; 2D full: n1*n2
+  double2* d1 = nullptr;            // 2D: marginal eigenvalues along axis 1 / 2
+  double2* d2 = nullptr;
+  std::vector<double2> d_host, d1_host, d2_host;
+  std::vector<std::unique_ptr<DevBuf>> bufs;
+  long long N() const { return (long long)n1 * n2; }
+};
+
+struct fd_smoother {
+  const fd_op* op = nullptr;
+  int kind = 0;
+  double* s = nullptr;    // 1D: n; 2D full: n1*n2 (custom / non-separable op)
+  double* s1 = nullptr;   // 2D separable: per-axis laplacian pieces
+  double* s2 = nullptr;
+  double* r = nullptr;    // 1D GCV ratio |d|^2/s^2
+  int sep_sum = 0;        // separable: s = s1 + s2 (1) or 1 (0)
+  int full = 0;           // 2D uses full arrays (Spectral mode 3)
+  double2* dfull = nullptr;  // full d materialised for mode 3 on a separable op
+  std::vector<std::unique_ptr<DevBuf>> bufs;
+};
+
+namespace {
+
+Spectral spectral_of(const fd_op* op, const fd_smoother* L, bool col_pass) {
+  Spectral sp{};
+  sp.col_pass = col_pass;
+  if (op->dim == 1) {
+    sp.mode = 1;
+    sp.dA = op->d;
+    sp.sA = L ? L->s : nullptr;
+    return sp;
+  }
+  sp.n2 = op->n2;
+  const bool full = (L && L->full) || !op->sep;
+  if (!full) {
+    sp.mode = 2;
+    sp.dA = op->d1;
+    sp.dB = op->d2;
+    sp.smooth_sum = L ? L->sep_sum : 0;
+    sp.sA = L ? L->s1 : nullptr;
+    sp.sB = L ? L->s2 : nullptr;
+  } else {
+    sp.mode = 3;
+    sp.dA = op->sep ? (L ? L->dfull : nullptr) : op->d;
+    sp.sA = L ? L->s : nullptr;
+  }
+  return sp;
+}
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+// ---- transform pipelines (tensor_apply order: columns, then rows) ----
+// analyze count items: in (real or complex) -> out (basis type)
+void run_analyze(const fd_op* op, const void* in, int in_cplx, void* out, long long count,
+                 Scratch& S) {
+  const int oc = op->cplx;
+  if (op->dim == 1) {
+    LineIO io{};
+    io.in = in;
+    io.out = out;
+    io.gi = lines_1d(op->n1, count);
+    io.go = io.gi;
+    io.in_cplx = in_cplx;
+    io.out_cplx = oc;
+    launch_analyze(op->ax1->dev, io, S.st);
+    return;
+  }
+  const int n1 = op->n1, n2 = op->n2;
+  void* mid = oc ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
+  Lines cols{};
+  cols.item_stride = (long long)n1 * n2;
+  cols.line_stride = 1;
+  cols.elem_stride = n2;
+  cols.per_item = n2;
+  cols.count = (int)(count * n2);
+  Lines rows{};
+  rows.item_stride = (long long)n1 * n2;
+  rows.line_stride = n2;
+  rows.elem_stride = 1;
+  rows.per_item = n1;
+  rows.count = (int)(count * n1);
+  LineIO a{};
+  a.in = in;
+  a.out = mid;
+  a.gi = cols;
+  a.go = cols;
+  a.in_cplx = in_cplx;
+  a.out_cplx = oc;
+  launch_analyze(op->ax1->dev, a, S.st);
+  LineIO b{};
+  b.in = mid;
+  b.out = out;
+  b.gi = rows;
+  b.go = rows;
+  b.in_cplx = oc;
+  b.out_cplx = oc;
+  launch_analyze(op->ax2->dev, b, S.st);
+}
+
+// synthesize coefficients (basis type) -> out, with mode 0/1/2 fused into the
+// first (column) pass; real output keeps Re and reports the residue per item.
+void run_synth(const fd_op* op, const fd_smoother* L, const void* in, void* out, int out_cplx,
+               int mode, const double* mu_item, double* resid, long long count, Scratch& S) {
+  const int oc = op->cplx;
+  if (op->dim == 1) {
+    LineIO io{};
+    io.in = in;
+    io.out = out;
+    io.gi = lines_1d(op->n1, count);
+    io.go = io.gi;
+    io.in_cplx = oc;
+    io.out_cplx = out_cplx;
+    SynthArgs sa{};
+    sa.mode = mode;
+    sa.sp = spectral_of(op, L, false);
+    sa.mu_item = mu_item;
+    double* r2 = nullptr;
+    if (oc && !out_cplx && resid) r2 = S.get<double>(count);
+    sa.resid2 = r2;
+    launch_synth(op->ax1->dev, io, sa, S.st);
+    if (r2) {
+      k_resid_reduce<<<(int)((count + 255) / 256), 256, 0, S.st>>>(r2, (int)count, 1, resid);
+      launched("k_resid_reduce");
+    }
+    return;
+  }
+  const int n1 = op->n1, n2 = op->n2;
+  void* mid = oc ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
+  Lines cols{};
+  cols.item_stride = (long long)n1 * n2;
+  cols.line_stride = 1;
+  cols.elem_stride = n2;
+  cols.per_item = n2;
+  cols.count = (int)(count * n2);
+  Lines rows{};
+  rows.item_stride = (long long)n1 * n2;
+  rows.line_stride = n2;
+  rows.elem_stride = 1;
+  rows.per_item = n1;
+  rows.count = (int)(count * n1);
+  LineIO a{};
+  a.in = in;
+  a.out = mid;
+  a.gi = cols;
+  a.go = cols;
+  a.in_cplx = oc;
+  a.out_cplx = oc;
+  SynthArgs sa{};
+  sa.mode = mode;
+  sa.sp = spectral_of(op, L, true);
+  sa.mu_item = mu_item;
+  launch_synth(op->ax1->dev, a, sa, S.st);
+  LineIO b{};
+  b.in = mid;
+  b.out = out;
+  b.gi = rows;
+  b.go = rows;
+  b.in_cplx = oc;
+  b.out_cplx = out_cplx;
+  SynthArgs sb{};
+  double* r2 = nullptr;
+  if (oc && !out_cplx && resid) r2 = S.get<double>(count * n1);
+  sb.resid2 = r2;
+  launch_synth(op->ax2->dev, b, sb, S.st);
+  if (r2) {
+    k_resid_reduce<<<(int)((count + 255) / 256), 256, 0, S.st>>>(r2, (int)count, n1, resid);
+    launched("k_resid_reduce");
+  }
+}
+
+// ---- GCV ----
+struct GridHost {
+  std::vector<double> mus, logmus;
+};
+
+GridHost make_grid(double mu_min, double mu_max, int count) {  // regularize.cpp:283-293
+  if (!(mu_min > 0.0) || !(mu_max > mu_min) || count < 2)
+    validation("gcv search needs 0 < mu_min < mu_max and count >= 2");
+  GridHost g;
+  const double llo = std::log(mu_min), lhi = std::log(mu_max);
+  g.mus.resize(count);
+  g.logmus.resize(count);
+  for (int k = 0; k < count; ++k) {
+    g.mus[k] = std::exp(llo + (lhi - llo) * k / (count - 1));
+    g.logmus[k] = std::log(g.mus[k]);
+  }
+  return g;
+}
+
+GcvData gcv_data(const fd_op* op, const fd_smoother* L, const void* ghat, long long count) {
+  GcvData g{};
+  g.ghat = ghat;
+  g.cplx = op->cplx;
+  g.N = op->N();
+  g.items = (int)count;
+  g.r1d = op->dim == 1 ? L->r : nullptr;
+  g.sp = spectral_of(op, L, false);
+  return g;
+}
+
+int pick_chunks(long long N, long long items, int sg) {
+  const long long groups = (items + sg - 1) / sg;
+  const long long target = 148LL * 64;  // warps in flight
+  long long nch = (target + groups - 1) / groups;
+  nch = std::min(nch, std::max(1LL, N / 256));
+  return (int)std::max(1LL, nch);
+}
+
+template <int KC, int SG>
+void launch_grid_t(const GcvData& g, const GcvGrid& grid, long long chunk, int nch,
+                   double* partial, cudaStream_t st) {
+  const int K = grid.count;
+  const int groups = (g.items + SG - 1) / SG;
+  const long long warps = (long long)groups * nch;
+  const int blocks = (int)((warps * 32 + 255) / 256);
+  for (int kb = 0; kb < K; kb += 32 * KC) {
+    k_gcv_grid<KC, SG><<<blocks, 256, 0, st>>>(g, grid, chunk, nch, kb, partial);
+    launched("k_gcv_grid");
+  }
+}
+
+void launch_grid(const GcvData& g, const GcvGrid& grid, int sg, long long chunk, int nch,
+                 double* partial, cudaStream_t st) {
+  const int K = grid.count;
+  const int kc = K <= 32 ? 1 : K <= 64 ? 2 : K <= 128 ? 4 : 8;
+#define FD_GRID(KCV)                                                         \
+  if (kc == KCV) {                                                           \
+    if (sg == 4)                                                             \
+      launch_grid_t<KCV, 4>(g, grid, chunk, nch, partial, st);               \
+    else                                                                     \
+      launch_grid_t<KCV, 1>(g, grid, chunk, nch, partial, st);               \
+    return;                                                                  \
+  }
+  FD_GRID(1) FD_GRID(2) FD_GRID(4) FD_GRID(8)
+#undef FD_GRID
+}
+
+void launch_moments(int J, const GcvData& g, const double* center, const int* need,
+                    long long chunk, int nch, double* partial, cudaStream_t st) {
+  const long long warps = (long long)g.items * nch;
+  const int blocks = (int)((warps * 32 + 255) / 256);
+#define FD_MOM(JV)                                                                   \
+  case JV:                                                                           \
+    k_gcv_moments<JV><<<blocks, 256, 0, st>>>(g, center, need, chunk, nch, partial); \
+    break;
+  switch (J) {
+    FD_MOM(4) FD_MOM(8) FD_MOM(12) FD_MOM(16) FD_MOM(20) FD_MOM(24) FD_MOM(28) FD_MOM(32)
+    FD_MOM(36) FD_MOM(40) FD_MOM(44) FD_MOM(48)
+    default: throw FdError(FD_ERR_OTHER, "unsupported moment count");
+  }
+#undef FD_MOM
+  launched("k_gcv_moments");
+}
+
+// G(mu_item) for all items -> G (device)
+void gcv_direct(const GcvData& g, const double* mu_item, double* G, int* status, Scratch& S) {
+  const int nch = pick_chunks(g.N, g.items, 1);
+  const long long chunk = (g.N + nch - 1) / nch;
+  double* part = S.get<double>((size_t)g.items * nch * 2);
+  const long long warps = (long long)g.items * nch;
+  k_gcv_direct<<<(int)((warps * 32 + 255) / 256), 256, 0, S.st>>>(g, mu_item, chunk, nch, part);
+  launched("k_gcv_direct");
+  k_gcv_direct_reduce<<<(g.items + 255) / 256, 256, 0, S.st>>>(part, g.items, nch, G, status);
+  launched("k_gcv_direct_reduce");
+}
+
+// gcv_minimize per item on the GPU.  ghat: analyzed coefficients.
+void gcv_select_dev(const fd_op* op, const fd_smoother* L, const void* ghat, long long count,
+                    double mu_min, double mu_max, int K, double* mu_out, int* best_k_out,
+                    double* curve_out, int* status, Scratch& S) {
+  const GridHost gh = make_grid(mu_min, mu_max, K);
+  double* dmus = S.get<double>(K);
+  double* dlog = S.get<double>(K);
+  ck(cudaMemcpyAsync(dmus, gh.mus.data(), K * sizeof(double), cudaMemcpyHostToDevice, S.st), "mus");
+  ck(cudaMemcpyAsync(dlog, gh.logmus.data(), K * sizeof(double), cudaMemcpyHostToDevice, S.st),
+     "logmus");
+  GcvGrid grid{K, dmus, dlog};
+  const GcvData g = gcv_data(op, L, ghat, count);
+  const int items = (int)count;
+
+  const int sg = items >= 4 * 148 * 8 ? 4 : 1;
+  const int nch = pick_chunks(g.N, items, sg);
+  const long long chunk = (g.N + nch - 1) / nch;
+  double* part = S.get<double>((size_t)items * nch * 2 * K);
+  launch_grid(g, grid, sg, chunk, nch, part, S.st);
+  double* G = curve_out ? curve_out : S.get<double>((size_t)items * K);
+  {
+    const long long tot = (long long)items * K;
+    k_gcv_reduce_grid<<<(int)((tot + 255) / 256), 256, 0, S.st>>>(part, items, nch, K, G, status);
+    launched("k_gcv_reduce_grid");
+  }
+  int* bk = best_k_out ? best_k_out : S.get<int>(items);
+  double* center = S.get<double>(items);
+  int* need = S.get<int>(items);
+  k_gcv_pick<<<(items + 127) / 128, 128, 0, S.st>>>(G, items, grid, mu_out, bk, center, need);
+  launched("k_gcv_pick");
+
+  const int J = gcv_moment_terms(mu_min, mu_max, K);
+  if (J > 0) {
+    const int nchm = pick_chunks(g.N, items, 1);
+    const long long chunkm = (g.N + nchm - 1) / nchm;
+    double* pm = S.get<double>((size_t)items * nchm * 2 * J);
+    launch_moments(J, g, center, need, chunkm, nchm, pm, S.st);
+    k_gcv_golden<<<(items + 63) / 64, 64, 0, S.st>>>(pm, items, nchm, J, G, grid, bk, center,
+                                                     need, mu_out);
+    launched("k_gcv_golden");
+    return;
+  }
+  // Coarse grids: golden section driven from the host with direct G
+  // evaluations on the GPU (each step one batched launch over all items).
+  std::vector<double> Gh((size_t)items * K);
+  std::vector<int> bkh(items), needh(items);
+  std::vector<double> muh(items);
+  ck(cudaMemcpyAsync(Gh.data(), G, Gh.size() * sizeof(double), cudaMemcpyDeviceToHost, S.st), "G");
+  ck(cudaMemcpyAsync(bkh.data(), bk, items * sizeof(int), cudaMemcpyDeviceToHost, S.st), "bk");
+  ck(cudaMemcpyAsync(needh.data(), need, items * sizeof(int), cudaMemcpyDeviceToHost, S.st),
+     "need");
+  ck(cudaMemcpyAsync(muh.data(), mu_out, items * sizeof(double), cudaMemcpyDeviceToHost, S.st),
+     "mu");
+  ck(cudaStreamSynchronize(S.st), "sync");
+  // every item's golden section takes the same number of steps within its
+  // bracket class, so run them in lockstep with a callback that batches
+  double* dmu = S.get<double>(items);
+  double* dG = S.get<double>(items);
+  struct Lane {
+    double a, b, x1, x2, f1, f2;
+    int phase;  // 0 idle, 1 evaluating f1, 2 evaluating f2
+  };
+  std::vector<Lane> st(items);
+  const double invphi = 0.6180339887498949;
+  std::vector<double> req(items, 1.0), got(items, 0.0);
+  auto eval_batch = [&]() {
+    ck(cudaMemcpyAsync(dmu, req.data(), items * sizeof(double), cudaMemcpyHostToDevice, S.st),
+       "req");
+    gcv_direct(g, dmu, dG, status, S);
+    ck(cudaMemcpyAsync(got.data(), dG, items * sizeof(double), cudaMemcpyDeviceToHost, S.st),
+       "got");
+    ck(cudaStreamSynchronize(S.st), "sync");
+  };
+  for (int i = 0; i < items; ++i) {
+    if (!needh[i]) continue;
+    const int k = bkh[i];
+    const double lo = gh.mus[k > 0 ? k - 1 : 0], hi = gh.mus[k + 1 < K ? k + 1 : K - 1];
+    st[i].a = std::log(lo);
+    st[i].b = std::log(hi);
+    st[i].x1 = st[i].b - invphi * (st[i].b - st[i].a);
+    st[i].x2 = st[i].a + invphi * (st[i].b - st[i].a);
+  }
+  for (int i = 0; i < items; ++i) req[i] = std::exp(st[i].x1);
+  eval_batch();
+  for (int i = 0; i < items; ++i) st[i].f1 = got[i];
+  for (int i = 0; i < items; ++i) req[i] = std::exp(st[i].x2);
+  eval_batch();
+  for (int i = 0; i < items; ++i) st[i].f2 = got[i];
+  for (;;) {
+    bool any = false;
+    for (int i = 0; i < items; ++i) {
+      Lane& s = st[i];
+      s.phase = 0;
+      if (!(needh[i] && std::exp(s.b - s.a) - 1.0 > 1e-3)) continue;
+      any = true;
+      if (s.f1 <= s.f2) {
+        s.b = s.x2, s.x2 = s.x1, s.f2 = s.f1, s.x1 = s.b - invphi * (s.b - s.a);
+        req[i] = std::exp(s.x1);
+        s.phase = 1;
+      } else {
+        s.a = s.x1, s.x1 = s.x2, s.f1 = s.f2, s.x2 = s.a + invphi * (s.b - s.a);
+        req[i] = std::exp(s.x2);
+        s.phase = 2;
+      }
+    }
+    if (!any) break;
+    eval_batch();
+    for (int i = 0; i < items; ++i) {
+      if (st[i].phase == 1) st[i].f1 = got[i];
+      if (st[i].phase == 2) st[i].f2 = got[i];
+    }
+  }
+  for (int i = 0; i < items; ++i) req[i] = needh[i] ? std::exp(0.5 * (st[i].a + st[i].b)) : 1.0;
+  eval_batch();
+  for (int i = 0; i < items; ++i) {
+    if (!needh[i]) continue;
+    const double best = Gh[(size_t)i * K + bkh[i]];
+    muh[i] = got[i] <= best ? req[i] : gh.mus[bkh[i]];
+  }
+  ck(cudaMemcpyAsync(mu_out, muh.data(), items * sizeof(double), cudaMemcpyHostToDevice, S.st),
+     "mu out");
+}
+
+void check_status(int* status, cudaStream_t st) {
+  int h = 0;
+  ck(cudaMemcpyAsync(&h, status, sizeof(int), cudaMemcpyDeviceToHost, st), "status");
+  ck(cudaStreamSynchronize(st), "sync");
+  if (h == 3) degenerate("degenerate gcv: all smoother eigenvalues are zero");
+}
+
+void check_op(const fd_op* op) {
+  if (!op) validation("null operator");
+}
+void check_L(const fd_op* op, const fd_smoother* L) {
+  if (!L) validation("null smoother");
+  if (L->op != op) validation("smoother was built for a different operator");
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* fd_last_error(void) { return g_err.c_str(); }
+int fd_version(void) { return 1; }
+long long fd_kernel_launches(void) { return g_launches.load(); }
+
+int fd_parse_bc(const char* name) {
+  if (!name) return -1;
+  const std::string s(name);
+  for (int b = 0; b < 5; ++b)
+    if (s == bc_name(b)) return b;
+  return -1;
+}
+
+int fd_bc_for_degree(int degree, int psf_symmetric, int* bc) {
+  return guarded([&] {
+    if (degree == 1) {
+      if (!psf_symmetric)
+        validation("degree 1 (antireflective) requires a symmetric psf in the reference "
+                   "(operators.cpp:173-176)");
+      *bc = BC_ANTIREFLECTIVE;
+    } else if (degree == 2) {
+      *bc = psf_symmetric ? BC_HOC_COSINE : BC_HOC_FOURIER;
+    } else {
+      validation("boundary-condition degree " + std::to_string(degree) +
+                 " is not provided by the reference (SPEC.md:164)");
+    }
+  });
+}
+
+int fd_op_create_1d(const double* psf, int len, int normalize, int n, int bc, fd_op** out) {
+  return guarded([&] {
+    if (!out) validation("null output");
+    *out = nullptr;
+    const HostPsf p = make_psf(psf, len, normalize != 0);
+    validate_build(p, n, bc);
+    init_runtime_once();
+    auto op = std::make_unique<fd_op>();
+    op->dim = 1;
+    op->n1 = n;
+    op->n2 = 1;
+    op->bc = bc;
+    op->cplx = is_complex_bc(bc);
+    op->ax1 = build_axis(bc, n);
+    op->d_host = eig1d(p, n, bc, op->bufs, &op->d);
+    *out = op.release();
+  });
+}
+
+namespace {
+HostPsf marginal(const std::vector<double>& w2, int rows, int cols, bool sum_columns) {
+  // marginal_sum_columns / _rows (multidim.cpp:247-263), then make_psf(normalize)
+  std::vector<double> w(sum_columns ? rows : cols, 0.0);
+  for (int j = 0; j < rows; ++j)
+    for (int k = 0; k < cols; ++k) w[sum_columns ? j : k] += w2[(size_t)j * cols + k];
+  return make_psf(w.data(), (int)w.size(), true);
+}
+
+std::vector<double> make_psf2d(const double* w, int rows, int cols, bool normalize,
+                               bool* symmetric) {  // multidim.cpp:185-213
+  if (rows < 1 || cols < 1 || rows % 2 == 0 || cols % 2 == 0)
+    validation("2D psf needs odd rows and cols");
+  std::vector<double> v(w, w + (size_t)rows * cols);
+  double sum = 0.0;
+  for (double x : v) {
+    if (!std::isfinite(x)) validation("2D psf weights must be finite");
+    sum += x;
+  }
+  if (normalize) {
+    if (sum == 0.0) validation("2D psf weights sum to zero");
+    for (double& x : v) x /= sum;
+  } else if (std::abs(sum - 1.0) > 1e-8) {
+    validation("2D psf weights must sum to 1 (pass normalize)");
+  }
+  const int m1 = rows / 2, m2 = cols / 2;
+  bool sym = true;
+  auto at = [&](int j, int k) { return v[(size_t)(m1 + j) * cols + (m2 + k)]; };
+  for (int j = -m1; j <= m1 && sym; ++j)
+    for (int k = -m2; k <= m2; ++k)
+      if (at(j, k) != at(-j, k) || at(j, k) != at(j, -k)) {
+        sym = false;
+        break;
+      }
+  *symmetric = sym;
+  return v;
+}
+
+void validate_build_2d(bool symmetric, int rows, int cols, int n1, int n2, int bc) {
+  check_bc(bc);
+  if (needs_symmetric(bc) && !symmetric)
+    validation(std::string(bc_name(bc)) +
+               " boundary conditions require a quadrantally symmetric 2D psf");
+  const bool corrected = is_corrected(bc);
+  const int slack = corrected ? 2 : 0;
+  if (corrected && (n1 < 5 || n2 < 5))
+    validation("boundary-corrected 2D operators need n >= 5 per axis");
+  if (rows > n1 - slack || cols > n2 - slack) validation("2D psf support exceeds the per-axis limit");
+}
+
+fd_op* create_2d(const std::vector<double>& w2, int rows, int cols, bool symmetric, int n1, int n2,
+                 int bc, bool separable) {
+  validate_build_2d(symmetric, rows, cols, n1, n2, bc);
+  init_runtime_once();
+  auto op = std::make_unique<fd_op>();
+  op->dim = 2;
+  op->n1 = n1;
+  op->n2 = n2;
+  op->bc = bc;
+  op->cplx = is_complex_bc(bc);
+  op->sep = separable;
+  op->ax1 = build_axis(bc, n1);
+  op->ax2 = build_axis(bc, n2);
+  const HostPsf a1 = marginal(w2, rows, cols, true);
+  const HostPsf a2 = marginal(w2, rows, cols, false);
+  op->d1_host = eig1d(a1, n1, bc, op->bufs, &op->d1);
+  op->d2_host = eig1d(a2, n2, bc, op->bufs, &op->d2);
+  if (!separable) {
+    std::vector<std::unique_ptr<DevBuf>> tmp;
+    double* dh = dev_upload(tmp, w2);
+    double2* T = dev_alloc<double2>(tmp, (size_t)rows * n2);
+    op->d = dev_alloc<double2>(op->bufs, (size_t)n1 * n2);
+    const int m1 = rows / 2, m2 = cols / 2;
+    k_eig2d_stage1<<<1024, 256>>>(dh, m1, m2, bc, n2, T);
+    launched("k_eig2d_stage1");
+    k_eig2d_stage2<<<2048, 256>>>(T, m1, bc, n1, n2, op->cplx, op->d);
+    launched("k_eig2d_stage2");
+    if (is_corrected(bc)) {
+      k_eig2d_edges<<<64, 256>>>(op->d1, op->d2, n1, n2, op->d);
+      launched("k_eig2d_edges");
+      k_eig2d_corners<<<1, 32>>>(n1, n2, op->d);
+      launched("k_eig2d_corners");
+    }
+    ck(cudaDeviceSynchronize(), "eigenvalues_2d");
+  }
+  return op.release();
+}
+}  // namespace
+
+int fd_op_create_2d(const double* psf, int rows, int cols, int normalize, int n1, int n2, int bc,
+                    fd_op** out) {
+  return guarded([&] {
+    if (!out) validation("null output");
+    *out = nullptr;
+    bool sym = false;
+    const auto w2 = make_psf2d(psf, rows, cols, normalize != 0, &sym);
+    *out = create_2d(w2, rows, cols, sym, n1, n2, bc, false);
+  });
+}
+
+int fd_op_create_2d_separable(const double* psf_a, int len_a, const double* psf_b, int len_b,
+                              int normalize, int n1, int n2, int bc, fd_op** out) {
+  return guarded([&] {
+    if (!out) validation("null output");
+    *out = nullptr;
+    const HostPsf a = make_psf(psf_a, len_a, normalize != 0);
+    const HostPsf b = make_psf(psf_b, len_b, normalize != 0);
+    // separable_psf2d (multidim.cpp:226-233): outer product, normalised
+    std::vector<double> w((size_t)len_a * len_b);
+    for (int j = 0; j < len_a; ++j)
+      for (int k = 0; k < len_b; ++k) w[(size_t)j * len_b + k] = a.w[j] * b.w[k];
+    bool sym = false;
+    const auto w2 = make_psf2d(w.data(), len_a, len_b, true, &sym);
+    *out = create_2d(w2, len_a, len_b, sym, n1, n2, bc, true);
+  });
+}
+
+int fd_op_destroy(fd_op* op) {
+  return guarded([&] {
+    if (op) {
+      cudaDeviceSynchronize();
+      delete op;
+    }
+  });
+}
+
+int fd_op_info(const fd_op* op, int* dim, int* n1, int* n2, int* bc, int* is_complex) {
+  return guarded([&] {
+    check_op(op);
+    if (dim) *dim = op->dim;
+    if (n1) *n1 = op->n1;
+    if (n2) *n2 = op->n2;
+    if (bc) *bc = op->bc;
+    if (is_complex) *is_complex = op->cplx;
+  });
+}
+
+int fd_op_eigenvalues(const fd_op* op, double* d, void* stream) {
+  return guarded([&] {
+    check_op(op);
+    const cudaStream_t st = as_stream(stream);
+    if (op->dim == 1 || !op->sep) {
+      ck(cudaMemcpyAsync(d, op->d, op->N() * sizeof(double2), cudaMemcpyDeviceToDevice, st), "eig");
+      return;
+    }
+    // separable: materialise the outer product d1 (x) d2 (scale an all-ones array)
+    std::vector<double2> ones(op->N(), make_double2(1.0, 0.0));
+    ck(cudaMemcpyAsync(d, ones.data(), ones.size() * sizeof(double2), cudaMemcpyHostToDevice, st),
+       "ones");
+    Spectral sp{};
+    sp.mode = 2;
+    sp.n2 = op->n2;
+    sp.dA = op->d1;
+    sp.dB = op->d2;
+    k_scale_full<<<1024, 256, 0, st>>>(d, 1, op->N(), 1, sp);
+    launched("k_scale_full");
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int fd_smoother_create(const fd_op* op, int kind, fd_smoother** out) {
+  return guarded([&] {
+    check_op(op);
+    if (!out) validation("null output");
+    *out = nullptr;
+    if (kind < 0 || kind > 2) validation("unknown smoother kind");
+    auto L = std::make_unique<fd_smoother>();
+    L->op = op;
+    L->kind = kind;
+    if (op->dim == 1) {
+      const int n = op->n1;
+      L->s = dev_alloc<double>(L->bufs, n);
+      k_smoother_1d<<<std::max(1, (n + 255) / 256), 256>>>(kind, op->bc, n, L->s);
+      launched("k_smoother_1d");
+      std::vector<double> sh(n);
+      ck(cudaMemcpy(sh.data(), L->s, n * sizeof(double), cudaMemcpyDeviceToHost), "s");
+      for (int i = 0; i < n; ++i)
+        if (sh[i] == 0.0 && std::abs(cplx(op->d_host[i].x, op->d_host[i].y)) == 0.0)
+          validation("incompatible smoother: joint null space with the blur operator");
+      L->r = dev_alloc<double>(L->bufs, n);
+      k_gcv_ratio<<<std::max(1, (n + 255) / 256), 256>>>(op->d, L->s, n, L->r);
+      launched("k_gcv_ratio");
+    } else {
+      if (kind == SM_FIRST_DIFFERENCE)
+        validation("the first-difference smoother is defined for 1D operators only");
+      const int n1 = op->n1, n2 = op->n2;
+      if (kind == SM_LAPLACIAN) {
+        L->s1 = dev_alloc<double>(L->bufs, n1);
+        L->s2 = dev_alloc<double>(L->bufs, n2);
+        k_smoother_1d<<<std::max(1, (n1 + 255) / 256), 256>>>(SM_LAPLACIAN, op->bc, n1, L->s1);
+        launched("k_smoother_1d");
+        k_smoother_1d<<<std::max(1, (n2 + 255) / 256), 256>>>(SM_LAPLACIAN, op->bc, n2, L->s2);
+        launched("k_smoother_1d");
+        L->sep_sum = 1;
+      }
+      if (!op->sep) {
+        L->full = 1;
+        L->s = dev_alloc<double>(L->bufs, (size_t)n1 * n2);
+        k_smoother_2d<<<2048, 256>>>(kind, L->s1, L->s2, n1, n2, L->s);
+        launched("k_smoother_2d");
+      }
+      // joint null space: s_ij = 0 only where both axis nodes are 0 (corners),
+      // where the corner eigenvalues are 1 for corrected BCs
+      if (kind == SM_LAPLACIAN) {
+        std::vector<double> s1(n1), s2(n2);
+        ck(cudaMemcpy(s1.data(), L->s1, n1 * sizeof(double), cudaMemcpyDeviceToHost), "s1");
+        ck(cudaMemcpy(s2.data(), L->s2, n2 * sizeof(double), cudaMemcpyDeviceToHost), "s2");
+        std::vector<double2> dfull;
+        if (!op->sep) {
+          dfull.resize((size_t)n1 * n2);
+          ck(cudaMemcpy(dfull.data(), op->d, dfull.size() * sizeof(double2),
+                        cudaMemcpyDeviceToHost),
+             "d");
+        }
+        for (int i = 0; i < n1; ++i) {
+          if (s1[i] != 0.0) continue;
+          for (int j = 0; j < n2; ++j) {
+            if (s1[i] + s2[j] != 0.0) continue;
+            const double2 dv = op->sep ? make_double2(
+                                             op->d1_host[i].x * op->d2_host[j].x -
+                                                 op->d1_host[i].y * op->d2_host[j].y,
+                                             op->d1_host[i].x * op->d2_host[j].y +
+                                                 op->d1_host[i].y * op->d2_host[j].x)
+                                       : dfull[(size_t)i * n2 + j];
+            if (dv.x == 0.0 && dv.y == 0.0) validation("incompatible smoother: joint null space");
+          }
+        }
+      }
+    }
+    ck(cudaDeviceSynchronize(), "smoother");
+    *out = L.release();
+  });
+}
+
+int fd_smoother_create_custom(const fd_op* op, const double* s, fd_smoother** out) {
+  return guarded([&] {
+    check_op(op);
+    if (!out || !s) validation("null argument");
+    *out = nullptr;
+    auto L = std::make_unique<fd_smoother>();
+    L->op = op;
+    L->kind = SM_CUSTOM;
+    const long long N = op->N();
+    std::vector<double> h(s, s + N);
+    L->s = dev_upload(L->bufs, h);
+    if (op->dim == 1) {
+      L->r = dev_alloc<double>(L->bufs, N);
+      k_gcv_ratio<<<std::max(1, (int)((N + 255) / 256)), 256>>>(op->d, L->s, (int)N, L->r);
+      launched("k_gcv_ratio");
+    } else {
+      L->full = 1;
+      if (op->sep) {
+        L->dfull = dev_alloc<double2>(L->bufs, N);
+        std::vector<double2> ones(N, make_double2(1.0, 0.0));
+        ck(cudaMemcpy(L->dfull, ones.data(), N * sizeof(double2), cudaMemcpyHostToDevice), "1");
+        Spectral sp{};
+        sp.mode = 2;
+        sp.n2 = op->n2;
+        sp.dA = op->d1;
+        sp.dB = op->d2;
+        k_scale_full<<<1024, 256>>>(L->dfull, 1, N, 1, sp);
+        launched("k_scale_full");
+      }
+    }
+    ck(cudaDeviceSynchronize(), "smoother");
+    *out = L.release();
+  });
+}
+
+int fd_smoother_destroy(fd_smoother* L) {
+  return guarded([&] {
+    if (L) {
+      cudaDeviceSynchronize();
+      delete L;
+    }
+  });
+}
+
+int fd_smoother_eigenvalues(const fd_smoother* L, double* s, void* stream) {
+  return guarded([&] {
+    if (!L) validation("null smoother");
+    const fd_op* op = L->op;
+    const cudaStream_t st = as_stream(stream);
+    if (L->s) {
+      ck(cudaMemcpyAsync(s, L->s, op->N() * sizeof(double), cudaMemcpyDeviceToDevice, st), "s");
+      return;
+    }
+    std::vector<double> h((size_t)op->N(), 1.0);
+    if (L->sep_sum) {
+      std::vector<double> s1(op->n1), s2(op->n2);
+      ck(cudaMemcpy(s1.data(), L->s1, op->n1 * sizeof(double), cudaMemcpyDeviceToHost), "s1");
+      ck(cudaMemcpy(s2.data(), L->s2, op->n2 * sizeof(double), cudaMemcpyDeviceToHost), "s2");
+      for (int i = 0; i < op->n1; ++i)
+        for (int j = 0; j < op->n2; ++j) h[(size_t)i * op->n2 + j] = s1[i] + s2[j];
+    }
+    ck(cudaMemcpyAsync(s, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, st), "s");
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int fd_analyze(const fd_op* op, const void* in, int in_complex, void* out, long long count,
+               void* stream) {
+  return guarded([&] {
+    check_op(op);
+    if (count < 0) validation("negative count");
+    if (in_complex && !op->cplx)
+      validation("real boundary condition in a complex basis: analyze needs real input");
+    if (count == 0) return;
+    Scratch S(as_stream(stream));
+    run_analyze(op, in, in_complex, out, count, S);
+  });
+}
+
+int fd_synthesize(const fd_op* op, const void* in, void* out, int out_complex,
+                  double* imag_residue, long long count, void* stream) {
+  return guarded([&] {
+    check_op(op);
+    if (count < 0) validation("negative count");
+    if (out_complex && !op->cplx) validation("complex output requested from a real basis");
+    if (count == 0) return;
+    Scratch S(as_stream(stream));
+    if (!op->cplx && imag_residue)
+      ck(cudaMemsetAsync(imag_residue, 0, count * sizeof(double), S.st), "memset");
+    run_synth(op, nullptr, in, out, out_complex, 0, nullptr, imag_residue, count, S);
+  });
+}
+
+int fd_matvec(const fd_op* op, const double* f, double* out, double* imag_residue, long long count,
+              void* stream) {
+  return guarded([&] {
+    check_op(op);
+    if (count < 0) validation("negative count");
+    if (count == 0) return;
+    Scratch S(as_stream(stream));
+    void* c = op->cplx ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
+    run_analyze(op, f, 0, c, count, S);
+    if (!op->cplx && imag_residue)
+      ck(cudaMemsetAsync(imag_residue, 0, count * sizeof(double), S.st), "memset");
+    run_synth(op, nullptr, c, out, 0, 2, nullptr, imag_residue, count, S);
+  });
+}
+
+int fd_tikhonov(const fd_op* op, const fd_smoother* L, const double* g, const double* mu,
+                double* out, double* imag_residue, long long count, void* stream) {
+  return guarded([&] {
+    check_op(op);
+    check_L(op, L);
+    if (count < 0) validation("negative count");
+    if (count == 0) return;
+    Scratch S(as_stream(stream));
+    std::vector<double> muh(count);
+    ck(cudaMemcpyAsync(muh.data(), mu, count * sizeof(double), cudaMemcpyDeviceToHost, S.st), "mu");
+    ck(cudaStreamSynchronize(S.st), "sync");
+    for (double m : muh)
+      if (!(m > 0.0)) validation("mu must be positive");
+    void* c = op->cplx ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
+    run_analyze(op, g, 0, c, count, S);
+    if (!op->cplx && imag_residue)
+      ck(cudaMemsetAsync(imag_residue, 0, count * sizeof(double), S.st), "memset");
+    run_synth(op, L, c, out, 0, 1, mu, imag_residue, count, S);
+  });
+}
+
+int fd_gcv_value(const fd_op* op, const fd_smoother* L, const double* g, double mu, double* G,
+                 long long count, void* stream) {
+  return guarded([&] {
+    check_op(op);
+    check_L(op, L);
+    if (!(mu > 0.0)) validation("mu must be positive");
+    if (count <= 0) return;
+    Scratch S(as_stream(stream));
+    void* c = op->cplx ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
+    run_analyze(op, g, 0, c, count, S);
+    std::vector<double> muh(count, mu);
+    double* dmu = S.get<double>(count);
+    ck(cudaMemcpyAsync(dmu, muh.data(), count * sizeof(double), cudaMemcpyHostToDevice, S.st), "mu");
+    int* status = S.get<int>(1);
+    ck(cudaMemsetAsync(status, 0, sizeof(int), S.st), "memset");
+    gcv_direct(gcv_data(op, L, c, count), dmu, G, status, S);
+    check_status(status, S.st);
+  });
+}
+
+int fd_gcv_select(const fd_op* op, const fd_smoother* L, const double* g, double mu_min,
+                  double mu_max, int grid_count, double* mu, int* best_k, double* curve,
+                  long long count, void* stream) {
+  return guarded([&] {
+    check_op(op);
+    check_L(op, L);
+    make_grid(mu_min, mu_max, grid_count);  // parameter validation first
+    if (count <= 0) return;
+    Scratch S(as_stream(stream));
+    void* c = op->cplx ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
+    run_analyze(op, g, 0, c, count, S);
+    int* status = S.get<int>(1);
+    ck(cudaMemsetAsync(status, 0, sizeof(int), S.st), "memset");
+    gcv_select_dev(op, L, c, count, mu_min, mu_max, grid_count, mu, best_k, curve, status, S);
+    check_status(status, S.st);
+  });
+}
+
+int fd_deblur(const fd_op* op, const fd_smoother* L, const double* g, int use_gcv,
+              double fixed_mu, double mu_min, double mu_max, int grid_count, double* restored,
+              double* mu_used, int* best_k, double* curve, double* imag_residue, long long count,
+              void* stream) {
+  return guarded([&] {
+    check_op(op);
+    check_L(op, L);
+    if (!mu_used) validation("mu_used output is required");
+    const bool need_grid = use_gcv || curve != nullptr;  // pipeline.cpp:737-750
+    if (need_grid) make_grid(mu_min, mu_max, grid_count);
+    if (!use_gcv && !(fixed_mu > 0.0)) validation("mu must be positive");
+    if (count <= 0) return;
+    Scratch S(as_stream(stream));
+    void* c = op->cplx ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
+    run_analyze(op, g, 0, c, count, S);
+    int* status = S.get<int>(1);
+    ck(cudaMemsetAsync(status, 0, sizeof(int), S.st), "memset");
+    if (use_gcv) {
+      gcv_select_dev(op, L, c, count, mu_min, mu_max, grid_count, mu_used, best_k, curve, status,
+                     S);
+    } else {
+      if (curve) {
+        double* tmp_mu = S.get<double>(count);
+        gcv_select_dev(op, L, c, count, mu_min, mu_max, grid_count, tmp_mu, best_k, curve, status,
+                       S);
+      }
+      std::vector<double> muh(count, fixed_mu);
+      ck(cudaMemcpyAsync(mu_used, muh.data(), count * sizeof(double), cudaMemcpyHostToDevice,
+                         S.st),
+         "mu");
+    }
+    if (!op->cplx && imag_residue)
+      ck(cudaMemsetAsync(imag_residue, 0, count * sizeof(double), S.st), "memset");
+    run_synth(op, L, c, restored, 0, 1, mu_used, imag_residue, count, S);
+    if (need_grid) check_status(status, S.st);
+  });
+}
+
+int fd_gcv_minimize_host(fd_gcv_fn G, void* ctx, double mu_min, double mu_max, int grid_count,
+                         double* mu, int* best_k, double* curve) {
+  return guarded([&] {
+    if (!G || !mu) validation("null argument");
+    const GridHost gh = make_grid(mu_min, mu_max, grid_count);
+    std::vector<double> vals(grid_count);
+    for (int k = 0; k < grid_count; ++k) vals[k] = G(gh.mus[k], ctx);
+    if (curve) std::copy(vals.begin(), vals.end(), curve);
+    const GcvPick pk = gcv_pick(gh.mus.data(), gh.logmus.data(), vals.data(), grid_count);
+    if (best_k) *best_k = pk.best_k;
+    if (pk.tied) {
+      *mu = pk.mu_tie;
+      return;
+    }
+    auto f = [&](double x) { return G(x, ctx); };
+    *mu = gcv_golden(gh.mus.data(), grid_count, pk.best_k, vals[pk.best_k], f);
+  });
+}
+
+}  // extern "C"

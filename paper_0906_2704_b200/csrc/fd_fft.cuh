@@ -1,0 +1,219 @@
+// Block-level fp64 FFT engine for sm_100a.
+//
+// One CTA owns one length-M complex buffer in shared memory (M = 2^k, padded
+// one slot per 16 so strided passes are bank-conflict free) and runs
+//   DIF (natural -> digit-reversed)  then  DIT (digit-reversed -> natural).
+// Each pass fuses up to four radix-2 stages in registers (radix-16 butterflies,
+// 16 complex values per thread item), so an M = 8192 transform touches shared
+// memory 4 times instead of 13.  Twiddles come from a global table
+// e^{-2 pi i j/M} (L1-resident) plus compile-time radix-16 constants.
+//
+// Arbitrary lengths L (the interior lengths n-2 = 2*7*73, 2*23*89, 2*8191 of
+// the BASELINE sizes are never powers of two) use Bluestein:
+//   X_k = c_k * sum_j (x_j c_j) conj(c_{k-j}),   c_j = e^{-i pi j^2/L},
+// evaluated as DIF -> pointwise multiply by the precomputed DIF(b)/M (already
+// in digit-reversed order, so no permutation is ever materialised) -> DIT.
+// The chirp pre/post multiplies are fused into the callers' load/store loops.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "fd_internal.h"
+
+namespace fdb {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) {
+  return make_double2(a.x + b.x, a.y + b.y);
+}
+__device__ __forceinline__ double2 csub(double2 a, double2 b) {
+  return make_double2(a.x - b.x, a.y - b.y);
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+// a * conj(b)
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+  return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 cscale(double2 a, double s) {
+  return make_double2(a.x * s, a.y * s);
+}
+__device__ __forceinline__ double2 czero() { return make_double2(0.0, 0.0); }
+
+// padded shared-memory slot of logical index i
+__host__ __device__ __forceinline__ int pidx(int i) { return i + (i >> 4); }
+
+// d * e^{-2 pi i k/16} for a compile-time k in [0, 8)
+__device__ __forceinline__ double2 mul_w16(double2 d, int k) {
+  constexpr double C1 = 0.92387953251128675613, S1 = 0.38268343236508977173;
+  constexpr double H = 0.70710678118654752440;
+  switch (k) {
+    case 0: return d;
+    case 1: return cmul(d, make_double2(C1, -S1));
+    case 2: return make_double2(H * (d.x + d.y), H * (d.y - d.x));
+    case 3: return cmul(d, make_double2(S1, -C1));
+    case 4: return make_double2(d.y, -d.x);
+    case 5: return cmul(d, make_double2(-S1, -C1));
+    case 6: return make_double2(H * (d.y - d.x), -H * (d.x + d.y));
+    default: return cmul(d, make_double2(-C1, -S1));
+  }
+}
+// d * e^{+2 pi i k/16}
+__device__ __forceinline__ double2 mul_w16c(double2 d, int k) {
+  return cconj(mul_w16(cconj(d), k));
+}
+
+// One fused pass of LOGR radix-2 decimation-in-frequency stages on blocks of
+// size S (S >= 2^LOGR).  Items are disjoint element sets, so the pass is
+// in-place with no barrier inside.
+template <int LOGR>
+__device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S,
+                                         const double2* __restrict__ tw) {
+  constexpr int R = 1 << LOGR;
+  const int SR = S >> LOGR;
+  const int items = M >> LOGR;
+  const int twstep = M / S;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int j0 = it & (SR - 1);
+    const int base = (it - j0) * R + j0;
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = x[pidx(base + q * SR)];
+#pragma unroll
+    for (int st = 0; st < LOGR; ++st) {
+      const int half = R >> (st + 1);
+      const double2 w = __ldg(&tw[(j0 * twstep) << st]);
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (q & half) continue;
+        const int qq = q & (half - 1);
+        const double2 a = v[q], b = v[q + half];
+        v[q] = cadd(a, b);
+        const double2 d = mul_w16(csub(a, b), (qq << st) * (16 / R));
+        v[q + half] = cmul(d, w);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) x[pidx(base + q * SR)] = v[q];
+  }
+}
+
+// Exact inverse (times 2 per stage) of dif_pass with conjugate twiddles: the
+// mirrored DIT pass of the backward transform.
+template <int LOGR>
+__device__ __forceinline__ void dit_pass(double2* __restrict__ x, int M, int S,
+                                         const double2* __restrict__ tw) {
+  constexpr int R = 1 << LOGR;
+  const int SR = S >> LOGR;
+  const int items = M >> LOGR;
+  const int twstep = M / S;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int j0 = it & (SR - 1);
+    const int base = (it - j0) * R + j0;
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = x[pidx(base + q * SR)];
+#pragma unroll
+    for (int st = LOGR - 1; st >= 0; --st) {
+      const int half = R >> (st + 1);
+      const double2 w = __ldg(&tw[(j0 * twstep) << st]);
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (q & half) continue;
+        const int qq = q & (half - 1);
+        const double2 a = v[q];
+        const double2 b = mul_w16c(cmulc(v[q + half], w), (qq << st) * (16 / R));
+        v[q] = cadd(a, b);
+        v[q + half] = csub(a, b);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) x[pidx(base + q * SR)] = v[q];
+  }
+}
+
+__device__ __forceinline__ int pass_logr(int rem) { return rem >= 4 ? 4 : rem; }
+
+// Forward DIF FFT (sign -1), natural order in, digit-reversed order out.
+// Caller must __syncthreads() before; returns after a barrier.
+__device__ __forceinline__ void fft_dif(double2* x, int M, int logM, const double2* tw) {
+  int S = M;
+  int rem = logM;
+  while (rem > 0) {
+    const int l = pass_logr(rem);
+    switch (l) {
+      case 4: dif_pass<4>(x, M, S, tw); break;
+      case 3: dif_pass<3>(x, M, S, tw); break;
+      case 2: dif_pass<2>(x, M, S, tw); break;
+      default: dif_pass<1>(x, M, S, tw); break;
+    }
+    S >>= l;
+    rem -= l;
+    __syncthreads();
+  }
+}
+
+// Backward DIT FFT (sign +1, unnormalised), digit-reversed in, natural out.
+__device__ __forceinline__ void fft_dit(double2* x, int M, int logM, const double2* tw) {
+  int ls[8];
+  int np = 0;
+  for (int rem = logM; rem > 0;) {
+    const int l = pass_logr(rem);
+    ls[np++] = l;
+    rem -= l;
+  }
+  int used = logM;
+  for (int p = np - 1; p >= 0; --p) {
+    const int l = ls[p];
+    used -= l;
+    const int S = M >> used;  // block size of pass p in the DIF sequence
+    switch (l) {
+      case 4: dit_pass<4>(x, M, S, tw); break;
+      case 3: dit_pass<3>(x, M, S, tw); break;
+      case 2: dit_pass<2>(x, M, S, tw); break;
+      default: dit_pass<1>(x, M, S, tw); break;
+    }
+    __syncthreads();
+  }
+}
+
+// Bluestein core: x holds a_j = z_j c_j (j < L) and zeros up to M; on return
+// x_k holds the circular convolution (a * b)_k; the caller multiplies by c_k.
+// Requires a barrier before the call (the caller's loads); ends with one.
+__device__ __forceinline__ void bluestein_core(double2* x, const FftTables& T) {
+  fft_dif(x, T.M, T.logM, T.tw);
+  for (int j = threadIdx.x; j < T.M; j += blockDim.x)
+    x[pidx(j)] = cmul(x[pidx(j)], __ldg(&T.bhat[j]));
+  __syncthreads();
+  fft_dit(x, T.M, T.logM, T.tw);
+}
+
+// ----------------------------------------------------------------------------
+// block reductions (deterministic: fixed shuffle tree, then warp order)
+// ----------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double* scratch /* >= 32*NV */) {
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = (blockDim.x + 31) >> 5;
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) scratch[warp * NV + k] = v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double acc = 0.0;
+    for (int w = 0; w < nw; ++w) acc += scratch[w * NV + k];
+    v[k] = acc;
+  }
+  __syncthreads();
+}
+
+}  // namespace fdb

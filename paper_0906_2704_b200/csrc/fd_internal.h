@@ -1,0 +1,83 @@
+// Internal structures shared by the sm_100a kernels (fd_kernels.cu) and the
+// C-ABI / host orchestration (fd_capi.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fdb {
+
+// BoundaryCondition codes (reference operators.hpp:15-21).
+enum Bc : int { BC_PERIODIC = 0, BC_REFLECTIVE = 1, BC_ANTIREFLECTIVE = 2, BC_HOC_COSINE = 3,
+                BC_HOC_FOURIER = 4 };
+// Interior trigonometric transform of an axis (boundary.cpp:120-129, operators.cpp:291-312).
+enum Interior : int { IK_COS = 0, IK_FOURIER = 1, IK_SINE = 2 };
+// Smoother kinds (regularize.hpp:15) + the first-difference extension.
+enum Smoother : int { SM_IDENTITY = 0, SM_LAPLACIAN = 1, SM_FIRST_DIFFERENCE = 2, SM_CUSTOM = 3 };
+
+// Tables for one length-L DFT evaluated by Bluestein's chirp-z convolution on
+// a power-of-two FFT of size M >= 2L-1 held in shared memory.
+struct FftTables {
+  int L, M, logM;
+  const double2* chirp;  // L entries  e^{-i pi j^2 / L}
+  const double2* bhat;   // M entries  DIF_M(b)/M (in the DIF output order)
+  const double2* tw;     // M/2 entries e^{-2 pi i j / M}
+};
+
+// One transform axis: T_X of order n (boundary.hpp:44-60) or a plain trig
+// basis (periodic: F^H / F, reflective: C^T / C).  All vectors are complex
+// (imag = 0 for the real bases) and live in device memory.
+struct AxisDev {
+  int n, m;        // order and interior length (m = n-2 when bordered)
+  int kind;        // Interior
+  int bordered;    // antireflective / hoc-cosine / hoc-fourier
+  int correction;  // rank-2 SMW correction (false for antireflective)
+  int cplx;        // complex basis (periodic, hoc-fourier)
+  FftTables fft;
+  const double2* dct_tw;  // m entries e^{-i pi k/(2m)} (IK_COS)
+  const double* q;        // n, boundary column (unit norm, q[n-1] = 0)
+  double alpha;           // 1/q[0]
+  const double2 *v, *w, *row_a, *row_b, *c_a, *c_b;  // m each
+  double2 cav[4];         // ca_v, ca_w, cb_v, cb_w
+  double2 cap[4];         // capacitance I + [c rows][v w], row-major
+};
+
+// Geometry of a set of lines (rows or columns of a batch of arrays).
+// Element e of line l lives at  (l / per_item) * item_stride
+//                              + (l % per_item) * line_stride + e * elem_stride
+// (strides in elements of the array's own type).
+struct Lines {
+  long long item_stride;
+  long long line_stride;
+  long long elem_stride;
+  int per_item;
+  int count;
+};
+
+__host__ __device__ __forceinline__ long long line_offset(const Lines& g, int l) {
+  return (long long)(l / g.per_item) * g.item_stride + (long long)(l % g.per_item) * g.line_stride;
+}
+
+// Per-coefficient spectral data for the filter / matvec scale / GCV.
+//   mode 1: 1D vectors indexed by the element (d[e], s[e]);
+//   mode 2: separable 2D  d = dA[i] * dB[j],  s = sA[i] + sB[j] (laplacian) or 1;
+//   mode 3: full 2D arrays d[i*n2 + j], s[i*n2 + j].
+// For 2D, (i, j) are recovered from (line, element) by the pass direction.
+struct Spectral {
+  int mode;
+  int smooth_sum;        // separable: 1 = s_ij = sA[i] + sB[j]; 0 = identity (s = 1)
+  int n2;                // row length of the 2D array
+  int col_pass;          // 1: line = column j, element = row i; 0: line = row i, element = j
+  const double2* dA;
+  const double2* dB;
+  const double* sA;
+  const double* sB;
+};
+
+struct GcvGrid {
+  int count;             // K
+  const double* mus;     // K grid values (host std::exp, regularize.cpp:291-293)
+  const double* logmus;  // log of each grid value (tie geometric mean)
+};
+
+}  // namespace fdb

@@ -1,0 +1,1017 @@
+// sm_100a kernels of the transform + filter + GCV restoration path.
+//
+// Reference functions restated here (paths under /root/reference/proj/core):
+//   transform_apply_inverse (analyze)       src/boundary.cpp:338-375
+//   transform_apply (synthesize)            src/boundary.cpp:310-336
+//   cosine_apply / fourier_apply / sine_apply  src/trig.cpp:170-234
+//   SpectralBasis::analyze / synthesize     src/operators.cpp:291-312
+//   tensor_apply (2D: column pass, row pass) src/multidim.cpp:275-302
+//   apply_tikhonov_filter                   include/fastdeblur/regularize.hpp:42-58
+//   gcv_from_coeffs                         include/fastdeblur/regularize.hpp:63-81
+//   gcv_minimize                            src/regularize.cpp:281-351
+//   operator_eigenvalues / eigenvalues_2d   src/operators.cpp:348-397, src/multidim.cpp:311-376
+//   smoothing_eigenvalues(_2d)              src/regularize.cpp:155-175, src/multidim.cpp:433-460
+//
+// Every line transform is one CTA: the interior trigonometric transform runs
+// in shared memory (fd_fft.cuh), two real lines share one complex FFT, and the
+// rank-2 border (dot products, 2x2 capacitance solve, axpy) is fused into the
+// load / store loops, so a line is read once and written once.
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "fd_fft.cuh"
+#include "fd_gcv_core.h"
+#include "fd_internal.h"
+
+namespace fdb {
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double2 ldc(const void* base, bool cplx, long long idx) {
+  if (cplx) return __ldg(reinterpret_cast<const double2*>(base) + idx);
+  return make_double2(__ldg(reinterpret_cast<const double*>(base) + idx), 0.0);
+}
+
+__device__ __forceinline__ void stc(void* base, bool cplx, long long idx, double2 v) {
+  if (cplx)
+    reinterpret_cast<double2*>(base)[idx] = v;
+  else
+    reinterpret_cast<double*>(base)[idx] = v.x;
+}
+
+// element index of interior coefficient i
+__device__ __forceinline__ int interior_elem(const AxisDev& ax, int i) {
+  return ax.bordered ? i + 1 : i;
+}
+
+// spectral values (d, s) of coefficient e of line l
+__device__ __forceinline__ void spectral_at(const Spectral& sp, const Lines& g, int l, int e,
+                                            double2& d, double& s) {
+  if (sp.mode == 1) {
+    d = __ldg(&sp.dA[e]);
+    s = __ldg(&sp.sA[e]);
+    return;
+  }
+  const int li = l % g.per_item;
+  const int i = sp.col_pass ? e : li;
+  const int j = sp.col_pass ? li : e;
+  if (sp.mode == 2) {
+    d = cmul(__ldg(&sp.dA[i]), __ldg(&sp.dB[j]));
+    s = sp.smooth_sum ? __ldg(&sp.sA[i]) + __ldg(&sp.sB[j]) : 1.0;
+  } else {
+    const long long idx = (long long)i * sp.n2 + j;
+    d = __ldg(&sp.dA[idx]);
+    s = __ldg(&sp.sA[idx]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// setup kernels
+// ---------------------------------------------------------------------------
+// chirp c_j = e^{-i pi j^2/L}, twiddles e^{-2 pi i j/M}, Bluestein kernel b,
+// DCT quarter-wave twiddles e^{-i pi k/(2m)} (trig.cpp:126-141).
+__global__ void k_init_tables(int L, int M, double2* chirp, double2* tw, double2* b, int mdct,
+                              double2* dct_tw) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < M; j += stride) {
+    if (j < L) {
+      const long long q = (j * j) % (2LL * L);
+      double s, c;
+      sincospi(-(double)q / (double)L, &s, &c);
+      chirp[j] = make_double2(c, s);
+    }
+    if (j < M / 2) {
+      double s, c;
+      sincospi(-2.0 * (double)j / (double)M, &s, &c);
+      tw[j] = make_double2(c, s);
+    }
+    // b_j = conj(c_|j|) on the circle of length M
+    long long jj = -1;
+    if (j < L)
+      jj = j;
+    else if (j > M - L)
+      jj = M - j;
+    if (jj >= 0) {
+      const long long q = (jj * jj) % (2LL * L);
+      double s, c;
+      sincospi((double)q / (double)L, &s, &c);
+      b[j] = make_double2(c, s);
+    } else {
+      b[j] = make_double2(0.0, 0.0);
+    }
+    if (j < mdct) {
+      double s, c;
+      sincospi(-(double)j / (2.0 * mdct), &s, &c);
+      dct_tw[j] = make_double2(c, s);
+    }
+  }
+}
+
+// bhat = DIF_M(b)/M, left in DIF (digit-reversed) order
+__global__ void k_bhat(FftTables T, const double2* __restrict__ b, double2* bhat) {
+  extern __shared__ double2 sm[];
+  for (int j = threadIdx.x; j < T.M; j += blockDim.x) sm[pidx(j)] = b[j];
+  __syncthreads();
+  fft_dif(sm, T.M, T.logM, T.tw);
+  const double inv = 1.0 / (double)T.M;
+  for (int j = threadIdx.x; j < T.M; j += blockDim.x) bhat[j] = cscale(sm[pidx(j)], inv);
+}
+
+// symbol z(t) = sum_j h_j e^{ijt} (psf.cpp:39-52)
+__device__ double2 symbol_eval(const double* __restrict__ h, int m, int symmetric, double t) {
+  if (symmetric) {
+    double z = h[m];
+    for (int j = 1; j <= m; ++j) z += 2.0 * h[m + j] * cos(j * t);
+    return make_double2(z, 0.0);
+  }
+  double zr = h[m], zi = 0.0;
+  for (int j = 1; j <= m; ++j) {
+    double s, c;
+    sincos(j * t, &s, &c);
+    // h_j (c + i s) + h_{-j} (c - i s)
+    zr += h[m + j] * c + h[m - j] * c;
+    zi += h[m + j] * s - h[m - j] * s;
+  }
+  return make_double2(zr, zi);
+}
+
+// node_i of eigenvalue_grid (operators.cpp:241-272), operation order mirrored
+__device__ __forceinline__ double eig_node(int bc, int n, int i) {
+  const double kPi = 3.14159265358979323846;
+  switch (bc) {
+    case BC_PERIODIC: return 2.0 * kPi * i / n;
+    case BC_REFLECTIVE: return kPi * i / n;
+    case BC_ANTIREFLECTIVE: return i < n - 1 ? kPi * i / (n - 1) : 0.0;
+    case BC_HOC_COSINE: return (i >= 1 && i < n - 1) ? kPi * (i - 1) / (n - 2) : 0.0;
+    default: return (i >= 1 && i < n - 1) ? 2.0 * kPi * (i - 1) / (n - 2) : 0.0;
+  }
+}
+
+// 1D eigenvalues d (operators.cpp:348-397): symbol at the interior nodes,
+// boundary eigenvalues of corrected operators pinned to exactly 1.
+__global__ void k_eigenvalues_1d(const double* __restrict__ h, int m, int symmetric, int bc,
+                                 int n, double2* d) {
+  const double kPi = 3.14159265358979323846;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    double t;
+    bool pinned = false;
+    switch (bc) {
+      case BC_PERIODIC: t = 2.0 * kPi * i / n; break;  // exp_grid_symbol(len=n)
+      case BC_REFLECTIVE: t = i * kPi / n; break;       // cos_grid_symbol(denom=n)
+      case BC_ANTIREFLECTIVE:
+        pinned = (i == 0 || i == n - 1);
+        t = i * kPi / (n - 1);
+        break;
+      case BC_HOC_COSINE:
+        pinned = (i == 0 || i == n - 1);
+        t = (i - 1) * kPi / (n - 2);
+        break;
+      default:
+        pinned = (i == 0 || i == n - 1);
+        t = 2.0 * kPi * (i - 1) / (n - 2);
+        break;
+    }
+    double2 z = pinned ? make_double2(1.0, 0.0) : symbol_eval(h, m, symmetric, t);
+    if (bc != BC_PERIODIC && bc != BC_HOC_FOURIER) z.y = 0.0;  // real bases keep .real()
+    d[i] = z;
+  }
+}
+
+// smoother eigenvalues on the node grid (regularize.cpp:155-175)
+__global__ void k_smoother_1d(int kind, int bc, int n, double* s) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (kind == SM_IDENTITY) {
+      s[i] = 1.0;
+    } else {
+      const double v = 2.0 - 2.0 * cos(eig_node(bc, n, i));
+      s[i] = kind == SM_FIRST_DIFFERENCE ? sqrt(v) : v;
+    }
+  }
+}
+
+// r_e = |d_e|^2 / s_e^2 (+inf where s = 0) for the GCV kernels; sigma = 1/(r+mu)
+// equals s^2/(|d|^2 + mu s^2) of regularize.hpp:71 (to rounding).
+__global__ void k_gcv_ratio(const double2* __restrict__ d, const double* __restrict__ s, int n,
+                            double* r) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double2 di = d[i];
+    const double si = s[i];
+    const double d2 = di.x * di.x + di.y * di.y;
+    r[i] = si == 0.0 ? INFINITY : d2 / (si * si);
+  }
+}
+
+// 2D interior eigenvalues d_ij = sum_{p,q} h_pq e^{i(p t1_i + q t2_j)} as
+// E1 (H E2): first T[p][j] = sum_q h_pq e^{i q t2_j}, then d_ij.
+__global__ void k_eig2d_stage1(const double* __restrict__ h, int m1, int m2, int bc, int n2,
+                               double2* T) {
+  const int cols = 2 * m2 + 1, rows = 2 * m1 + 1;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)rows * n2;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int p = (int)(idx / n2), j = (int)(idx % n2);
+    const double t2 = eig_node(bc, n2, j);
+    double re = 0.0, im = 0.0;
+    for (int q = -m2; q <= m2; ++q) {
+      double s, c;
+      sincos(q * t2, &s, &c);
+      const double w = h[p * cols + (q + m2)];
+      re += w * c;
+      im += w * s;
+    }
+    T[idx] = make_double2(re, im);
+  }
+}
+
+__global__ void k_eig2d_stage2(const double2* __restrict__ T, int m1, int bc, int n1, int n2,
+                               int cplx, double2* d) {
+  const int rows = 2 * m1 + 1;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n1 * n2;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / n2), j = (int)(idx % n2);
+    const double t1 = eig_node(bc, n1, i);
+    double2 z = make_double2(0.0, 0.0);
+    for (int p = 0; p < rows; ++p) {
+      double s, c;
+      sincos((p - m1) * t1, &s, &c);
+      z = cadd(z, cmul(make_double2(c, s), T[(long long)p * n2 + j]));
+    }
+    if (!cplx) z.y = 0.0;
+    d[idx] = z;
+  }
+}
+
+// edges from the marginal 1D eigenvalues, corners 1 (multidim.cpp:352-374)
+__global__ void k_eig2d_edges(const double2* __restrict__ d1, const double2* __restrict__ d2,
+                              int n1, int n2, double2* d) {
+  const int tot = 2 * n1 + 2 * n2;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < tot; t += gridDim.x * blockDim.x) {
+    if (t < n1) {
+      d[(long long)t * n2] = d1[t];
+    } else if (t < 2 * n1) {
+      const int i = t - n1;
+      d[(long long)i * n2 + n2 - 1] = d1[i];
+    } else if (t < 2 * n1 + n2) {
+      const int j = t - 2 * n1;
+      d[j] = d2[j];
+    } else {
+      const int j = t - 2 * n1 - n2;
+      d[(long long)(n1 - 1) * n2 + j] = d2[j];
+    }
+  }
+}
+
+__global__ void k_eig2d_corners(int n1, int n2, double2* d) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const double2 one = make_double2(1.0, 0.0);
+    d[0] = one;
+    d[n2 - 1] = one;
+    d[(long long)(n1 - 1) * n2] = one;
+    d[(long long)(n1 - 1) * n2 + n2 - 1] = one;
+  }
+}
+
+__global__ void k_smoother_2d(int kind, const double* __restrict__ s1,
+                              const double* __restrict__ s2, int n1, int n2, double* s) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n1 * n2;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / n2), j = (int)(idx % n2);
+    s[idx] = kind == SM_IDENTITY ? 1.0 : s1[i] + s2[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// analyze: out = T_X^{-1} in along each line (transform_apply_inverse,
+// boundary.cpp:338-375; plain C / F for reflective / periodic).
+// Real input lines are packed in pairs into one complex FFT.
+// ---------------------------------------------------------------------------
+struct LineIO {
+  const void* in;
+  void* out;
+  Lines gi, go;
+  int in_cplx, out_cplx;
+};
+
+__global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
+  extern __shared__ double2 sm[];
+  const int M = ax.fft.M;
+  double2* x = sm;
+  double* red = reinterpret_cast<double*>(sm + pidx(M) + 1);
+  double2* bc = reinterpret_cast<double2*>(red + 32 * 8);
+
+  const bool pair = !io.in_cplx;
+  const int l0 = pair ? 2 * blockIdx.x : blockIdx.x;
+  if (l0 >= io.gi.count) return;
+  const bool has1 = pair && (l0 + 1 < io.gi.count);
+  const long long oi0 = line_offset(io.gi, l0);
+  const long long oi1 = has1 ? line_offset(io.gi, l0 + 1) : oi0;
+  const long long es = io.gi.elem_stride;
+  const int n = ax.n, m = ax.m, L = ax.fft.L;
+  const double2* chirp = ax.fft.chirp;
+
+  auto ld0 = [&](int e) { return ldc(io.in, io.in_cplx, oi0 + e * es); };
+  auto ld1 = [&](int e) { return has1 ? ldc(io.in, io.in_cplx, oi1 + e * es) : czero(); };
+
+  double2 y00 = czero(), yn0 = czero(), y01 = czero(), yn1 = czero();
+  if (ax.bordered) {
+    y00 = ld0(0);
+    yn0 = ld0(n - 1);
+    y01 = ld1(0);
+    yn1 = ld1(n - 1);
+  }
+
+  // ---- load (with chirp premultiply) + border dot products ----
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // ra0, rb0, ra1, rb1 (re, im)
+  const bool dots = ax.bordered && ax.correction;
+  if (ax.kind == IK_COS) {
+    const int half = (m + 1) / 2;
+    for (int j = threadIdx.x; j < M; j += blockDim.x) {
+      double2 val = czero();
+      if (j < m) {
+        const int src = j < half ? 2 * j : 2 * (m - 1 - j) + 1;  // trig.cpp:194-195
+        const int e = interior_elem(ax, src);
+        const double a = ld0(e).x, b = ld1(e).x;
+        val = cmul(make_double2(a, b), __ldg(&chirp[j]));
+        if (dots) {
+          const double ra = __ldg(&ax.row_a[src]).x, rb = __ldg(&ax.row_b[src]).x;
+          acc[0] += ra * a;
+          acc[2] += rb * a;
+          acc[4] += ra * b;
+          acc[6] += rb * b;
+        }
+      }
+      x[pidx(j)] = val;
+    }
+  } else if (ax.kind == IK_FOURIER) {
+    for (int j = threadIdx.x; j < M; j += blockDim.x) {
+      double2 val = czero();
+      if (j < m) {
+        const int e = interior_elem(ax, j);
+        if (pair) {
+          const double a = ld0(e).x, b = ld1(e).x;
+          val = cmul(make_double2(a, b), __ldg(&chirp[j]));
+          if (dots) {
+            const double2 ra = __ldg(&ax.row_a[j]), rb = __ldg(&ax.row_b[j]);
+            acc[0] += ra.x * a, acc[1] += ra.y * a;
+            acc[2] += rb.x * a, acc[3] += rb.y * a;
+            acc[4] += ra.x * b, acc[5] += ra.y * b;
+            acc[6] += rb.x * b, acc[7] += rb.y * b;
+          }
+        } else {
+          const double2 z = ld0(e);
+          val = cmul(z, __ldg(&chirp[j]));
+          if (dots) {
+            const double2 ra = cmul(__ldg(&ax.row_a[j]), z), rb = cmul(__ldg(&ax.row_b[j]), z);
+            acc[0] += ra.x, acc[1] += ra.y;
+            acc[2] += rb.x, acc[3] += rb.y;
+          }
+        }
+      }
+      x[pidx(j)] = val;
+    }
+  } else {  // IK_SINE: odd extension (0, u, 0, -rev u) of length 2(m+1) (trig.cpp:219-228)
+    for (int p = threadIdx.x; p < M; p += blockDim.x) {
+      double2 val = czero();
+      if (p < L && p != 0 && p != m + 1) {
+        double a, b;
+        if (p <= m) {
+          const int e = interior_elem(ax, p - 1);
+          a = ld0(e).x, b = ld1(e).x;
+        } else {
+          const int e = interior_elem(ax, L - 1 - p);
+          a = -ld0(e).x, b = -ld1(e).x;
+        }
+        val = cmul(make_double2(a, b), __ldg(&chirp[p]));
+      }
+      x[pidx(p)] = val;
+    }
+  }
+  if (dots) block_sum<8>(acc, red);
+
+  // ---- SMW capacitance solve (boundary.cpp:357-368) ----
+  if (threadIdx.x == 0) {
+    double2 beta[4] = {czero(), czero(), czero(), czero()};
+    if (dots) {
+      const double2* c = ax.cap;
+      const double2 det = csub(cmul(c[0], c[3]), cmul(c[1], c[2]));
+      for (int t = 0; t < (pair ? 2 : 1); ++t) {
+        const double2 y0 = t == 0 ? y00 : y01, yn = t == 0 ? yn0 : yn1;
+        double2 ra = cadd(cmul(ax.cav[0], y0), cmul(ax.cav[1], yn));
+        double2 rb = cadd(cmul(ax.cav[2], y0), cmul(ax.cav[3], yn));
+        ra = cadd(ra, make_double2(acc[4 * t + 0], acc[4 * t + 1]));
+        rb = cadd(rb, make_double2(acc[4 * t + 2], acc[4 * t + 3]));
+        const double2 n0 = csub(cmul(ra, c[3]), cmul(rb, c[1]));
+        const double2 n1 = csub(cmul(rb, c[0]), cmul(ra, c[2]));
+        // complex division n / det
+        const double dd = det.x * det.x + det.y * det.y;
+        beta[2 * t] = make_double2((n0.x * det.x + n0.y * det.y) / dd,
+                                   (n0.y * det.x - n0.x * det.y) / dd);
+        beta[2 * t + 1] = make_double2((n1.x * det.x + n1.y * det.y) / dd,
+                                       (n1.y * det.x - n1.x * det.y) / dd);
+        if (!ax.cplx) {
+          beta[2 * t] = make_double2(n0.x / det.x, 0.0);
+          beta[2 * t + 1] = make_double2(n1.x / det.x, 0.0);
+        }
+      }
+    }
+    for (int k = 0; k < 4; ++k) bc[k] = beta[k];
+  }
+  __syncthreads();
+
+  bluestein_core(x, ax.fft);
+
+  const double2 b00 = bc[0], b10 = bc[1], b01 = bc[2], b11 = bc[3];
+  const long long oo0 = line_offset(io.go, l0);
+  const long long oo1 = has1 ? line_offset(io.go, l0 + 1) : oo0;
+  const long long eso = io.go.elem_stride;
+
+  // ---- post-process, border update, store ----
+  const double inv_sqrt_m = 1.0 / sqrt((double)m);
+  for (int k = threadIdx.x; k < m; k += blockDim.x) {
+    double2 xi0, xi1 = czero();
+    if (ax.kind == IK_SINE) {
+      const double sc = -0.5 * sqrt(2.0 / ((double)m + 1.0));
+      const double2 Z = cmul(x[pidx(k + 1)], __ldg(&chirp[k + 1]));
+      xi0 = make_double2(sc * Z.y, 0.0);
+      xi1 = make_double2(-sc * Z.x, 0.0);
+    } else {
+      const double2 Zk = cmul(x[pidx(k)], __ldg(&chirp[k]));
+      if (pair) {
+        const int kc = k == 0 ? 0 : m - k;
+        const double2 Zc = cconj(cmul(x[pidx(kc)], __ldg(&chirp[kc])));
+        const double2 U0 = cscale(cadd(Zk, Zc), 0.5);
+        const double2 D = csub(Zk, Zc);
+        const double2 U1 = make_double2(0.5 * D.y, -0.5 * D.x);
+        if (ax.kind == IK_COS) {
+          const double2 t = __ldg(&ax.dct_tw[k]);
+          const double sk = k == 0 ? sqrt(1.0 / (double)m) : sqrt(2.0 / (double)m);
+          xi0 = make_double2(sk * (t.x * U0.x - t.y * U0.y), 0.0);
+          xi1 = make_double2(sk * (t.x * U1.x - t.y * U1.y), 0.0);
+        } else {
+          xi0 = cscale(U0, inv_sqrt_m);
+          xi1 = cscale(U1, inv_sqrt_m);
+        }
+      } else {
+        xi0 = cscale(Zk, inv_sqrt_m);
+      }
+    }
+    const int e = interior_elem(ax, k);
+    if (ax.bordered) {
+      const double2 v = __ldg(&ax.v[k]), w = __ldg(&ax.w[k]);
+      if (ax.cplx) {
+        double2 o = cadd(cadd(cmul(y00, v), xi0), cmul(yn0, w));
+        if (dots) o = csub(o, cadd(cmul(b00, v), cmul(b10, w)));
+        stc(io.out, io.out_cplx, oo0 + e * eso, o);
+        if (has1) {
+          double2 o1 = cadd(cadd(cmul(y01, v), xi1), cmul(yn1, w));
+          if (dots) o1 = csub(o1, cadd(cmul(b01, v), cmul(b11, w)));
+          stc(io.out, io.out_cplx, oo1 + e * eso, o1);
+        }
+      } else {
+        double o = y00.x * v.x + xi0.x + yn0.x * w.x;
+        if (dots) o -= b00.x * v.x + b10.x * w.x;
+        stc(io.out, io.out_cplx, oo0 + e * eso, make_double2(o, 0.0));
+        if (has1) {
+          double o1 = y01.x * v.x + xi1.x + yn1.x * w.x;
+          if (dots) o1 -= b01.x * v.x + b11.x * w.x;
+          stc(io.out, io.out_cplx, oo1 + e * eso, make_double2(o1, 0.0));
+        }
+      }
+    } else {
+      stc(io.out, io.out_cplx, oo0 + e * eso, xi0);
+      if (has1) stc(io.out, io.out_cplx, oo1 + e * eso, xi1);
+    }
+  }
+  if (ax.bordered && threadIdx.x == 0) {
+    const double al = ax.alpha;
+    for (int t = 0; t < (has1 ? 2 : 1); ++t) {
+      const double2 y0 = t == 0 ? y00 : y01, yn = t == 0 ? yn0 : yn1;
+      const double2 b0 = t == 0 ? b00 : b01, b1 = t == 0 ? b10 : b11;
+      double2 o0 = cscale(y0, al), on = cscale(yn, al);
+      if (dots) {
+        o0 = csub(o0, cscale(b0, al));
+        on = csub(on, cscale(b1, al));
+      }
+      const long long oo = t == 0 ? oo0 : oo1;
+      stc(io.out, io.out_cplx, oo, o0);
+      stc(io.out, io.out_cplx, oo + (long long)(n - 1) * eso, on);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// synthesize: out = T_X c (transform_apply, boundary.cpp:310-336), optionally
+// with the Tikhonov filter (mode 1, regularize.hpp:42-58) or the eigenvalue
+// scale of the matvec (mode 2, operators.cpp:317-343) fused into the load.
+// Real bases: pairs of real lines.  Complex bases: one complex line per CTA;
+// real outputs keep Re and report sum(Im^2) per line (operators.cpp:334-340).
+// ---------------------------------------------------------------------------
+struct SynthArgs {
+  int mode;              // 0 plain, 1 filter, 2 scale by d
+  Spectral sp;
+  const double* mu_item; // per item (filter)
+  double* resid2;        // per line sum Im^2 (complex basis, real output), or null
+};
+
+__device__ __forceinline__ double2 coeff_at(const AxisDev& ax, const LineIO& io,
+                                            const SynthArgs& sa, int l, long long off, int e) {
+  double2 c = ldc(io.in, io.in_cplx, off + e * io.gi.elem_stride);
+  if (sa.mode == 0) return c;
+  double2 d;
+  double s;
+  spectral_at(sa.sp, io.gi, l, e, d, s);
+  if (sa.mode == 2) return ax.cplx ? cmul(c, d) : make_double2(c.x * d.x, 0.0);
+  const double mu = __ldg(&sa.mu_item[l / io.gi.per_item]);
+  if (ax.cplx) {
+    const double den = (d.x * d.x + d.y * d.y) + mu * s * s;
+    return cmul(c, make_double2(d.x / den, -d.y / den));
+  }
+  const double f = d.x / (d.x * d.x + mu * s * s);
+  return make_double2(c.x * f, 0.0);
+}
+
+__global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs sa) {
+  extern __shared__ double2 sm[];
+  const int M = ax.fft.M;
+  double2* x = sm;
+  double* red = reinterpret_cast<double*>(sm + pidx(M) + 1);
+
+  const bool pair = !ax.cplx;  // real bases: real coefficients, two lines per FFT
+  const int l0 = pair ? 2 * blockIdx.x : blockIdx.x;
+  if (l0 >= io.gi.count) return;
+  const bool has1 = pair && (l0 + 1 < io.gi.count);
+  const long long oi0 = line_offset(io.gi, l0);
+  const long long oi1 = has1 ? line_offset(io.gi, l0 + 1) : oi0;
+  const int n = ax.n, m = ax.m, L = ax.fft.L;
+  const double2* chirp = ax.fft.chirp;
+
+  auto c0 = [&](int e) { return coeff_at(ax, io, sa, l0, oi0, e); };
+  auto c1 = [&](int e) { return has1 ? coeff_at(ax, io, sa, l0 + 1, oi1, e) : czero(); };
+
+  double2 u00 = czero(), un0 = czero(), u01 = czero(), un1 = czero();
+  if (ax.bordered) {
+    u00 = c0(0);
+    un0 = c0(n - 1);
+    u01 = c1(0);
+    un1 = c1(n - 1);
+  }
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // top0, bottom0, top1, bottom1 (re, im)
+  const bool dots = ax.bordered && ax.correction;
+
+  if (ax.kind == IK_COS) {
+    // C^T u (trig.cpp:201-212): buf_k = s_k u_k tw_k, Re FFT(buf) reordered.
+    // Two lines: Re FFT(buf) = FFT(herm(buf)), herm(b)_k = (b_k + conj b_{-k})/2.
+    const double s0 = sqrt(1.0 / (double)m), s = sqrt(2.0 / (double)m);
+    for (int j = threadIdx.x; j < M; j += blockDim.x) {
+      double2 val = czero();
+      if (j < m) {
+        const int jc = j == 0 ? 0 : m - j;
+        const int e = interior_elem(ax, j), ec = interior_elem(ax, jc);
+        const double2 tj = __ldg(&ax.dct_tw[j]), tc = __ldg(&ax.dct_tw[jc]);
+        const double sj = j == 0 ? s0 : s, sc = jc == 0 ? s0 : s;
+        const double a = c0(e).x, ac = c0(ec).x;
+        const double b = c1(e).x, bcv = c1(ec).x;
+        const double ta = sj * a, tac = sc * ac, tb = sj * b, tbc = sc * bcv;
+        const double2 h0 = make_double2(0.5 * (ta * tj.x + tac * tc.x), 0.5 * (ta * tj.y - tac * tc.y));
+        const double2 h1 = make_double2(0.5 * (tb * tj.x + tbc * tc.x), 0.5 * (tb * tj.y - tbc * tc.y));
+        val = cmul(make_double2(h0.x - h1.y, h0.y + h1.x), __ldg(&chirp[j]));
+        if (dots) {
+          const double ca = __ldg(&ax.c_a[j]).x, cb = __ldg(&ax.c_b[j]).x;
+          acc[0] += ca * a;
+          acc[2] += cb * a;
+          acc[4] += ca * b;
+          acc[6] += cb * b;
+        }
+      }
+      x[pidx(j)] = val;
+    }
+  } else if (ax.kind == IK_SINE) {  // Q is an involution (boundary.cpp:124)
+    for (int p = threadIdx.x; p < M; p += blockDim.x) {
+      double2 val = czero();
+      if (p < L && p != 0 && p != m + 1) {
+        double a, b;
+        if (p <= m) {
+          const int e = interior_elem(ax, p - 1);
+          a = c0(e).x, b = c1(e).x;
+        } else {
+          const int e = interior_elem(ax, L - 1 - p);
+          a = -c0(e).x, b = -c1(e).x;
+        }
+        val = cmul(make_double2(a, b), __ldg(&chirp[p]));
+      }
+      x[pidx(p)] = val;
+    }
+  } else {  // IK_FOURIER: F^H v = conj(F conj(v)) (trig.cpp:170-178)
+    for (int j = threadIdx.x; j < M; j += blockDim.x) {
+      double2 val = czero();
+      if (j < m) {
+        const double2 z = c0(interior_elem(ax, j));
+        val = cmul(cconj(z), __ldg(&chirp[j]));
+        if (dots) {
+          const double2 t = cmul(__ldg(&ax.c_a[j]), z), bt = cmul(__ldg(&ax.c_b[j]), z);
+          acc[0] += t.x, acc[1] += t.y;
+          acc[2] += bt.x, acc[3] += bt.y;
+        }
+      }
+      x[pidx(j)] = val;
+    }
+  }
+  if (dots) block_sum<8>(acc, red);
+  __syncthreads();
+
+  bluestein_core(x, ax.fft);
+
+  const long long oo0 = line_offset(io.go, l0);
+  const long long oo1 = has1 ? line_offset(io.go, l0 + 1) : oo0;
+  const long long eso = io.go.elem_stride;
+  const double inv_sqrt_m = 1.0 / sqrt((double)m);
+  double im2 = 0.0;
+  for (int p = threadIdx.x; p < m; p += blockDim.x) {
+    double2 in0, in1 = czero();
+    if (ax.kind == IK_COS) {
+      const int idx = (p & 1) ? m - 1 - (p >> 1) : (p >> 1);  // trig.cpp:209-211
+      const double2 Z = cmul(x[pidx(idx)], __ldg(&chirp[idx]));
+      in0 = make_double2(Z.x, 0.0);
+      in1 = make_double2(Z.y, 0.0);
+    } else if (ax.kind == IK_SINE) {
+      const double sc = -0.5 * sqrt(2.0 / ((double)m + 1.0));
+      const double2 Z = cmul(x[pidx(p + 1)], __ldg(&chirp[p + 1]));
+      in0 = make_double2(sc * Z.y, 0.0);
+      in1 = make_double2(-sc * Z.x, 0.0);
+    } else {
+      in0 = cscale(cconj(cmul(x[pidx(p)], __ldg(&chirp[p]))), inv_sqrt_m);
+    }
+    const int e = interior_elem(ax, p);
+    if (ax.bordered) {
+      const double qi = __ldg(&ax.q[e]), qr = __ldg(&ax.q[n - 1 - e]);
+      if (ax.cplx) {
+        const double2 o = cadd(cadd(cscale(u00, qi), in0), cscale(un0, qr));
+        stc(io.out, io.out_cplx, oo0 + e * eso, o);
+        im2 += o.y * o.y;
+      } else {
+        const double o = qi * u00.x + in0.x + qr * un0.x;
+        stc(io.out, io.out_cplx, oo0 + e * eso, make_double2(o, 0.0));
+        if (has1) {
+          const double o1 = qi * u01.x + in1.x + qr * un1.x;
+          stc(io.out, io.out_cplx, oo1 + e * eso, make_double2(o1, 0.0));
+        }
+      }
+    } else {
+      stc(io.out, io.out_cplx, oo0 + e * eso, in0);
+      im2 += in0.y * in0.y;
+      if (has1) stc(io.out, io.out_cplx, oo1 + e * eso, in1);
+    }
+  }
+  if (ax.bordered && threadIdx.x == 0) {
+    const double q0 = ax.q[0];
+    for (int t = 0; t < (has1 ? 2 : 1); ++t) {
+      const double2 u0 = t == 0 ? u00 : u01, un = t == 0 ? un0 : un1;
+      const double2 top = make_double2(acc[4 * t + 0], acc[4 * t + 1]);
+      const double2 bot = make_double2(acc[4 * t + 2], acc[4 * t + 3]);
+      const double2 o0 = cadd(cscale(u0, q0), top);
+      const double2 on = cadd(bot, cscale(un, q0));
+      const long long oo = t == 0 ? oo0 : oo1;
+      stc(io.out, io.out_cplx, oo, o0);
+      stc(io.out, io.out_cplx, oo + (long long)(n - 1) * eso, on);
+      if (ax.cplx) im2 += o0.y * o0.y + on.y * on.y;
+    }
+  }
+  if (ax.cplx && sa.resid2 != nullptr) {
+    double v[1] = {im2};
+    block_sum<1>(v, red);
+    if (threadIdx.x == 0) sa.resid2[l0] = v[0];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GCV grid: for every item and grid value mu_k,
+//   num_k = sum_e sigma_e^2 |ghat_e|^2,  den_k = sum_e sigma_e,
+//   sigma_e = 1/(r_e + mu_k)   (r_e = |d_e|^2/s_e^2; s_e = 0 contributes 0)
+// (gcv_from_coeffs, regularize.hpp:63-81).  One warp owns SG items and one
+// element chunk; lane k-block owns KC consecutive grid values, whose
+// reciprocals share one division (Montgomery batch inversion).  All loads
+// are warp-uniform broadcasts.  Partial sums land in
+// partial[item][chunk][2][K] and are reduced in a fixed order afterwards.
+// ---------------------------------------------------------------------------
+struct GcvData {
+  const void* ghat;      // item-major, N coefficients per item
+  int cplx;
+  long long N;           // coefficients per item
+  int items;
+  const double* r1d;     // 1D ratio vector (length N), or null for 2D
+  Spectral sp;           // 2D: mode 2 (separable) or 3 (full); sp.n2 = row length
+};
+
+__device__ __forceinline__ double gcv_ratio(const GcvData& g, long long e) {
+  if (g.r1d) return __ldg(&g.r1d[e]);
+  const int i = (int)(e / g.sp.n2), j = (int)(e % g.sp.n2);
+  double2 d;
+  double s;
+  if (g.sp.mode == 2) {
+    d = cmul(__ldg(&g.sp.dA[i]), __ldg(&g.sp.dB[j]));
+    s = g.sp.smooth_sum ? __ldg(&g.sp.sA[i]) + __ldg(&g.sp.sB[j]) : 1.0;
+  } else {
+    d = __ldg(&g.sp.dA[e]);
+    s = __ldg(&g.sp.sA[e]);
+  }
+  if (s == 0.0) return INFINITY;
+  return (d.x * d.x + d.y * d.y) / (s * s);
+}
+
+__device__ __forceinline__ double gcv_w(const GcvData& g, int item, long long e) {
+  const long long idx = (long long)item * g.N + e;
+  if (g.cplx) {
+    const double2 c = __ldg(reinterpret_cast<const double2*>(g.ghat) + idx);
+    return c.x * c.x + c.y * c.y;
+  }
+  const double c = __ldg(reinterpret_cast<const double*>(g.ghat) + idx);
+  return c * c;
+}
+
+template <int KC, int SG>
+__global__ void __launch_bounds__(256) k_gcv_grid(GcvData g, GcvGrid grid, long long chunk,
+                                                  int nchunks, int kblock0, double* partial) {
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int groups = (g.items + SG - 1) / SG;
+  if (warp_global >= groups * nchunks) return;
+  const int grp = warp_global / nchunks, ch = warp_global % nchunks;
+  const int K = grid.count;
+  const int k0 = kblock0 + lane * KC;
+
+  double mu[KC];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) mu[k] = (k0 + k < K) ? grid.mus[k0 + k] : 1.0;
+  double num[SG][KC], den[KC];
+#pragma unroll
+  for (int k = 0; k < KC; ++k) {
+    den[k] = 0.0;
+#pragma unroll
+    for (int p = 0; p < SG; ++p) num[p][k] = 0.0;
+  }
+  const long long e0 = (long long)ch * chunk;
+  const long long e1 = min(g.N, e0 + chunk);
+  for (long long e = e0; e < e1; ++e) {
+    const double r = gcv_ratio(g, e);
+    if (isinf(r)) continue;
+    double w[SG];
+#pragma unroll
+    for (int p = 0; p < SG; ++p) {
+      const int item = grp * SG + p;
+      w[p] = item < g.items ? gcv_w(g, item, e) : 0.0;
+    }
+    double sig[KC];
+    if (r < 1e30) {
+      double xk[KC], pre[KC];
+#pragma unroll
+      for (int k = 0; k < KC; ++k) xk[k] = r + mu[k];
+      pre[0] = xk[0];
+#pragma unroll
+      for (int k = 1; k < KC; ++k) pre[k] = pre[k - 1] * xk[k];
+      double inv = 1.0 / pre[KC - 1];
+#pragma unroll
+      for (int k = KC - 1; k >= 1; --k) {
+        sig[k] = inv * pre[k - 1];
+        inv = inv * xk[k];
+      }
+      sig[0] = inv;
+    } else {
+#pragma unroll
+      for (int k = 0; k < KC; ++k) sig[k] = 1.0 / (r + mu[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+      den[k] += sig[k];
+      const double s2 = sig[k] * sig[k];
+#pragma unroll
+      for (int p = 0; p < SG; ++p) num[p][k] = fma(s2, w[p], num[p][k]);
+    }
+  }
+#pragma unroll
+  for (int p = 0; p < SG; ++p) {
+    const int item = grp * SG + p;
+    if (item >= g.items) continue;
+    double* base = partial + ((long long)item * nchunks + ch) * 2 * K;
+#pragma unroll
+    for (int k = 0; k < KC; ++k) {
+      if (k0 + k < K) {
+        base[k0 + k] = num[p][k];
+        base[K + k0 + k] = den[k];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GCV selection (gcv_minimize, regularize.cpp:281-351), one thread per item:
+// reduce the grid partials in chunk order, G_k = num/den^2, first minimum,
+// 1e-12 tie test, and the golden-section refinement evaluated from Taylor
+// moments about mu_c = sqrt(lo*hi):
+//   den(mu) = sum_j (-d)^j B_j,  num(mu) = sum_j (j+1)(-d)^j A_j,  d = mu-mu_c,
+//   B_j = sum_e t_e^{j+1}, A_j = sum_e w_e t_e^{j+2}, t_e = 1/(r_e + mu_c).
+// Every point the golden section visits lies in [lo, hi], where the series
+// ratio |d|/(r+mu_c) <= sqrt(hi/lo)-1, so J terms give ~1e-17 relative error.
+// ---------------------------------------------------------------------------
+__global__ void k_gcv_reduce_grid(const double* __restrict__ partial, int items, int nchunks,
+                                  int K, double* G, int* status) {
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t >= (long long)items * K) return;
+  const int item = (int)(t / K), k = (int)(t % K);
+  double num = 0.0, den = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    const double* base = partial + ((long long)item * nchunks + c) * 2 * K;
+    num += base[k];
+    den += base[K + k];
+  }
+  if (den == 0.0) {
+    atomicExch(status, 3);  // DegenerateError (regularize.hpp:78-79)
+    G[t] = NAN;
+    return;
+  }
+  G[t] = num / (den * den);
+}
+
+__global__ void k_gcv_pick(const double* __restrict__ G, int items, GcvGrid grid, double* mu_out,
+                           int* best_k, double* center, int* need_refine) {
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= items) return;
+  const GcvPick pk = gcv_pick(grid.mus, grid.logmus, G + (long long)item * grid.count, grid.count);
+  best_k[item] = pk.best_k;
+  if (pk.tied) {
+    mu_out[item] = pk.mu_tie;
+    need_refine[item] = 0;
+    center[item] = 0.0;
+  } else {
+    need_refine[item] = 1;
+    center[item] = sqrt(pk.lo * pk.hi);
+    mu_out[item] = grid.mus[pk.best_k];
+  }
+}
+
+template <int J>
+__global__ void __launch_bounds__(256) k_gcv_moments(GcvData g, const double* __restrict__ center,
+                                                     const int* __restrict__ need, long long chunk,
+                                                     int nchunks, double* partial) {
+  // one warp per (item, chunk); lanes stride over elements
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp_global >= g.items * nchunks) return;
+  const int item = warp_global / nchunks, ch = warp_global % nchunks;
+  if (!need[item]) return;
+  const double mc = center[item];
+  double A[J], B[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) A[j] = B[j] = 0.0;
+  const long long e0 = (long long)ch * chunk;
+  const long long e1 = min(g.N, e0 + chunk);
+  for (long long e = e0 + lane; e < e1; e += 32) {
+    const double r = gcv_ratio(g, e);
+    if (isinf(r)) continue;
+    const double w = gcv_w(g, item, e);
+    const double t = 1.0 / (r + mc);
+    double p = t;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      B[j] += p;
+      A[j] = fma(w * p, t, A[j]);
+      p *= t;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < J; ++j) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      A[j] += __shfl_xor_sync(0xffffffffu, A[j], o);
+      B[j] += __shfl_xor_sync(0xffffffffu, B[j], o);
+    }
+  }
+  if (lane == 0) {
+    double* base = partial + ((long long)item * nchunks + ch) * 2 * J;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      base[j] = A[j];
+      base[J + j] = B[j];
+    }
+  }
+}
+
+struct MomentG {
+  const double* A;
+  const double* B;
+  int J;
+  double mc;
+  __device__ double operator()(double mu) const {
+    const double d = -(mu - mc);
+    double num = 0.0, den = 0.0;
+    for (int j = J - 1; j >= 0; --j) {
+      num = fma(num, d, (double)(j + 1) * A[j]);
+      den = fma(den, d, B[j]);
+    }
+    return num / (den * den);
+  }
+};
+
+__global__ void k_gcv_golden(const double* __restrict__ partial, int items, int nchunks, int J,
+                             const double* __restrict__ G, GcvGrid grid,
+                             const int* __restrict__ best_k, const double* __restrict__ center,
+                             const int* __restrict__ need, double* mu_out) {
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= items || !need[item]) return;
+  double A[64], B[64];
+  for (int j = 0; j < J; ++j) A[j] = B[j] = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    const double* base = partial + ((long long)item * nchunks + c) * 2 * J;
+    for (int j = 0; j < J; ++j) {
+      A[j] += base[j];
+      B[j] += base[J + j];
+    }
+  }
+  MomentG f{A, B, J, center[item]};
+  const int k = best_k[item];
+  const double best = G[(long long)item * grid.count + k];
+  mu_out[item] = gcv_golden(grid.mus, grid.count, k, best, f);
+}
+
+// direct G(mu_item) for every item (gcv_value, regularize.cpp:255-269)
+__global__ void __launch_bounds__(256) k_gcv_direct(GcvData g, const double* __restrict__ mu_item,
+                                                    long long chunk, int nchunks,
+                                                    double* partial) {
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp_global >= g.items * nchunks) return;
+  const int item = warp_global / nchunks, ch = warp_global % nchunks;
+  const double mu = mu_item[item];
+  double num = 0.0, den = 0.0;
+  const long long e0 = (long long)ch * chunk;
+  const long long e1 = min(g.N, e0 + chunk);
+  for (long long e = e0 + lane; e < e1; e += 32) {
+    const double r = gcv_ratio(g, e);
+    if (isinf(r)) continue;
+    const double sig = 1.0 / (r + mu);
+    den += sig;
+    num = fma(sig * sig, gcv_w(g, item, e), num);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    num += __shfl_xor_sync(0xffffffffu, num, o);
+    den += __shfl_xor_sync(0xffffffffu, den, o);
+  }
+  if (lane == 0) {
+    double* base = partial + ((long long)item * nchunks + ch) * 2;
+    base[0] = num;
+    base[1] = den;
+  }
+}
+
+__global__ void k_gcv_direct_reduce(const double* __restrict__ partial, int items, int nchunks,
+                                    double* G, int* status) {
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= items) return;
+  double num = 0.0, den = 0.0;
+  for (int c = 0; c < nchunks; ++c) {
+    num += partial[((long long)item * nchunks + c) * 2];
+    den += partial[((long long)item * nchunks + c) * 2 + 1];
+  }
+  if (den == 0.0) {
+    atomicExch(status, 3);
+    G[item] = NAN;
+    return;
+  }
+  G[item] = num / (den * den);
+}
+
+// per-item residue: sqrt of the summed per-line Im^2 (operators.cpp:334-340)
+__global__ void k_resid_reduce(const double* __restrict__ r2, int items, int per_item,
+                               double* out) {
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= items) return;
+  double acc = 0.0;
+  for (int l = 0; l < per_item; ++l) acc += r2[(long long)item * per_item + l];
+  out[item] = sqrt(acc);
+}
+
+// elementwise c <- c * d (complex or real), used by the 2D matvec between passes
+__global__ void k_scale_full(void* c, int cplx, long long N, int items, Spectral sp) {
+  const long long tot = N * items;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long e = t % N;
+    const int i = (int)(e / sp.n2), j = (int)(e % sp.n2);
+    double2 d;
+    if (sp.mode == 2)
+      d = cmul(sp.dA[i], sp.dB[j]);
+    else
+      d = sp.dA[e];
+    if (cplx) {
+      double2* p = reinterpret_cast<double2*>(c) + t;
+      *p = cmul(*p, d);
+    } else {
+      double* p = reinterpret_cast<double*>(c) + t;
+      *p = *p * d.x;
+    }
+  }
+}
+
+}  // namespace fdb

@@ -1,0 +1,366 @@
+"""Python mirror of the reference operator API over the sm_100a C ABI.
+
+The names, argument meaning and error behaviour follow the reference C++ API
+(namespace ``fastdeblur``; see include/fastdeblur_b200.h for the file:line of
+each function).  Arrays are torch CUDA tensors (float64 / complex128), batched
+over leading axes: a 1D operator accepts ``[..., n]``, a 2D operator
+``[..., n1, n2]``.  Every computation runs in libfdb200.so on the GPU; there
+is no CPU path, and a missing library or device raises immediately.
+
+    op = build_operator(psf, n, "hoc-cosine")
+    L = smoothing_eigenvalues("laplacian", op)
+    rep = deblur(op, L, g, MuChoice(use_gcv=True), search=GcvSearch(1e-6, 1, 64))
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfdb200.so")
+
+BC = {"periodic": 0, "reflective": 1, "antireflective": 2, "hoc-cosine": 3, "hoc-fourier": 4}
+BC_NAMES = {v: k for k, v in BC.items()}
+SMOOTHER = {"identity": 0, "laplacian": 1, "first-difference": 2}
+
+
+class FastDeblurError(RuntimeError):
+    """Base class (errors.hpp:10-13); status 1."""
+
+
+class ValidationError(FastDeblurError, ValueError):
+    """errors.hpp:16-19; status 2."""
+
+
+class DegenerateError(FastDeblurError, ArithmeticError):
+    """errors.hpp:38-41; status 3."""
+
+
+_lib = None
+
+
+def lib():
+    """Load libfdb200.so (fails loudly when the CUDA library was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FastDeblurError(f"{LIB_PATH} missing: run paper_0906_2704_b200.build")
+        L = C.CDLL(LIB_PATH)
+        L.fd_last_error.restype = C.c_char_p
+        L.fd_kernel_launches.restype = C.c_longlong
+        vp, dp, ip, ll = C.c_void_p, C.POINTER(C.c_double), C.c_int, C.c_longlong
+        L.fd_op_create_1d.argtypes = [dp, ip, ip, ip, ip, C.POINTER(vp)]
+        L.fd_op_create_2d.argtypes = [dp, ip, ip, ip, ip, ip, ip, C.POINTER(vp)]
+        L.fd_op_create_2d_separable.argtypes = [dp, ip, dp, ip, ip, ip, ip, ip, C.POINTER(vp)]
+        L.fd_op_destroy.argtypes = [vp]
+        L.fd_op_info.argtypes = [vp] + [C.POINTER(C.c_int)] * 5
+        L.fd_op_eigenvalues.argtypes = [vp, vp, vp]
+        L.fd_smoother_create.argtypes = [vp, ip, C.POINTER(vp)]
+        L.fd_smoother_create_custom.argtypes = [vp, dp, C.POINTER(vp)]
+        L.fd_smoother_destroy.argtypes = [vp]
+        L.fd_smoother_eigenvalues.argtypes = [vp, vp, vp]
+        L.fd_analyze.argtypes = [vp, vp, ip, vp, ll, vp]
+        L.fd_synthesize.argtypes = [vp, vp, vp, ip, vp, ll, vp]
+        L.fd_matvec.argtypes = [vp, vp, vp, vp, ll, vp]
+        L.fd_tikhonov.argtypes = [vp, vp, vp, vp, vp, vp, ll, vp]
+        L.fd_gcv_value.argtypes = [vp, vp, vp, C.c_double, vp, ll, vp]
+        L.fd_gcv_select.argtypes = [vp, vp, vp, C.c_double, C.c_double, ip, vp, vp, vp, ll, vp]
+        L.fd_deblur.argtypes = [vp, vp, vp, ip, C.c_double, C.c_double, C.c_double, ip, vp, vp,
+                                vp, vp, vp, ll, vp]
+        L.fd_bc_for_degree.argtypes = [ip, ip, C.POINTER(C.c_int)]
+        L.fd_parse_bc.argtypes = [C.c_char_p]
+        _lib = L
+    return _lib
+
+
+def check(code):
+    if code == 0:
+        return
+    msg = lib().fd_last_error().decode()
+    if code == 2:
+        raise ValidationError(msg)
+    if code == 3:
+        raise DegenerateError(msg)
+    raise FastDeblurError(msg)
+
+
+def kernel_launches():
+    return int(lib().fd_kernel_launches())
+
+
+def _bc(bc):
+    if isinstance(bc, str):
+        if bc not in BC:
+            raise ValidationError(f"unknown boundary condition {bc!r}")
+        return BC[bc]
+    return int(bc)
+
+
+def _host(a):
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    return a, a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _dev(x, dtype=torch.float64):
+    if not isinstance(x, torch.Tensor):
+        x = torch.as_tensor(np.asarray(x))
+    if x.dtype != dtype:
+        x = x.to(dtype)
+    return x.to("cuda").contiguous()
+
+
+def bc_for_degree(degree, psf_symmetric):
+    """north_star 'BC degree d' -> the reference BC (d=1 AR, d=2 hoc-*)."""
+    out = C.c_int()
+    check(lib().fd_bc_for_degree(int(degree), int(bool(psf_symmetric)), C.byref(out)))
+    return BC_NAMES[out.value]
+
+
+# ---------------------------------------------------------------------------
+# operators
+# ---------------------------------------------------------------------------
+class BlurOperator:
+    """BlurOperatorT / BlurOperator2DT (operators.hpp:70-83, multidim.hpp:62-73)."""
+
+    def __init__(self, handle, dim, n1, n2, bc, complex_basis):
+        self._h = handle
+        self.dim, self.n1, self.n2 = dim, n1, n2
+        self.bc = bc
+        self.complex = bool(complex_basis)
+
+    @property
+    def n(self):
+        return self.n1
+
+    @property
+    def shape(self):
+        return (self.n1,) if self.dim == 1 else (self.n1, self.n2)
+
+    @property
+    def size(self):
+        return self.n1 * (self.n2 if self.dim == 2 else 1)
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h and _lib is not None:
+            _lib.fd_op_destroy(h)
+
+    def _count(self, x):
+        shp = tuple(x.shape)
+        k = len(self.shape)
+        if shp[len(shp) - k:] != self.shape:
+            raise ValidationError(f"array shape {shp} does not end with {self.shape}")
+        return int(np.prod(shp[:len(shp) - k])) if len(shp) > k else 1, shp[:len(shp) - k]
+
+    def eigenvalues(self):
+        """operator_eigenvalues / eigenvalues_2d -> complex128 tensor of the op shape."""
+        out = torch.empty(self.shape, dtype=torch.complex128, device="cuda")
+        check(lib().fd_op_eigenvalues(self._h, _ptr(out), _stream()))
+        return out
+
+    def analyze(self, y):
+        """SpectralBasis::analyze / tensor_apply(inverse): T_X^{-1} y."""
+        cplx_in = torch.is_complex(y) if isinstance(y, torch.Tensor) else np.iscomplexobj(y)
+        y = _dev(y, torch.complex128 if cplx_in else torch.float64)
+        count, lead = self._count(y)
+        out = torch.empty(y.shape, dtype=torch.complex128 if self.complex else torch.float64,
+                          device="cuda")
+        check(lib().fd_analyze(self._h, _ptr(y), int(cplx_in), _ptr(out), count, _stream()))
+        return out
+
+    def synthesize(self, c, complex_out=None):
+        """SpectralBasis::synthesize / tensor_apply(forward): T_X c.
+
+        Complex bases return a complex tensor by default; complex_out=False keeps
+        the real part and returns (real, imag_residue)."""
+        c = _dev(c, torch.complex128 if self.complex else torch.float64)
+        count, lead = self._count(c)
+        if complex_out is None:
+            complex_out = self.complex
+        out = torch.empty(c.shape, dtype=torch.complex128 if complex_out else torch.float64,
+                          device="cuda")
+        res = None if complex_out else torch.zeros(lead, dtype=torch.float64, device="cuda")
+        check(lib().fd_synthesize(self._h, _ptr(c), _ptr(out), int(bool(complex_out)),
+                                  _ptr(res), count, _stream()))
+        return out if complex_out else (out, res)
+
+    def apply(self, f):
+        """blur_apply(_2d): (A f, imag_residue)."""
+        f = _dev(f)
+        count, lead = self._count(f)
+        out = torch.empty_like(f)
+        res = torch.zeros(lead, dtype=torch.float64, device="cuda")
+        check(lib().fd_matvec(self._h, _ptr(f), _ptr(out), _ptr(res), count, _stream()))
+        return out, res
+
+
+def _new_op(create, *args):
+    h = C.c_void_p()
+    check(create(*args, C.byref(h)))
+    info = [C.c_int() for _ in range(5)]
+    check(lib().fd_op_info(h, *[C.byref(v) for v in info]))
+    dim, n1, n2, bc, cx = (v.value for v in info)
+    return BlurOperator(h, dim, n1, n2, bc, cx)
+
+
+def build_operator(psf, n, bc, normalize=True) -> BlurOperator:
+    """build_operator(make_psf(psf, normalize), n, bc) (operators.cpp:404-412)."""
+    a, p = _host(psf)
+    return _new_op(lib().fd_op_create_1d, p, len(a), int(normalize), int(n), _bc(bc))
+
+
+def build_operator_2d(psf2d, n1, n2, bc, normalize=True) -> BlurOperator:
+    """build_operator_2d(make_psf2d(...), n1, n2, bc) (multidim.cpp:413-426)."""
+    a, p = _host(psf2d)
+    if a.ndim != 2:
+        raise ValidationError("2D psf must be a 2D array")
+    return _new_op(lib().fd_op_create_2d, p, a.shape[0], a.shape[1], int(normalize), int(n1),
+                   int(n2), _bc(bc))
+
+
+def build_operator_2d_separable(psf_a, psf_b, n1, n2, bc, normalize=True) -> BlurOperator:
+    """build_operator_2d(separable_psf2d(a, b), ...) with outer-product eigenvalues."""
+    a, pa = _host(psf_a)
+    b, pb = _host(psf_b)
+    return _new_op(lib().fd_op_create_2d_separable, pa, len(a), pb, len(b), int(normalize),
+                   int(n1), int(n2), _bc(bc))
+
+
+def blur_apply(op: BlurOperator, f):
+    return op.apply(f)
+
+
+class Smoother:
+    """SmoothingOperator / SmoothingOperator2D (regularize.hpp:20-23)."""
+
+    def __init__(self, handle, op, kind):
+        self._h, self.op, self.kind = handle, op, kind
+
+    def __del__(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h and _lib is not None:
+            _lib.fd_smoother_destroy(h)
+
+    def eigenvalues(self):
+        out = torch.empty(self.op.shape, dtype=torch.float64, device="cuda")
+        check(lib().fd_smoother_eigenvalues(self._h, _ptr(out), _stream()))
+        return out
+
+
+def smoothing_eigenvalues(kind, op: BlurOperator) -> Smoother:
+    """smoothing_eigenvalues(_2d) (regularize.cpp:155-175, multidim.cpp:433-460)."""
+    k = SMOOTHER[kind] if isinstance(kind, str) else int(kind)
+    h = C.c_void_p()
+    check(lib().fd_smoother_create(op._h, k, C.byref(h)))
+    return Smoother(h, op, k)
+
+
+def smoother_from_eigenvalues(op: BlurOperator, s) -> Smoother:
+    """SmoothingOperator aggregate with caller-supplied eigenvalues."""
+    a, p = _host(s)
+    if a.size != op.size:
+        raise ValidationError("smoother length != operator order")
+    h = C.c_void_p()
+    check(lib().fd_smoother_create_custom(op._h, p, C.byref(h)))
+    return Smoother(h, op, 3)
+
+
+# ---------------------------------------------------------------------------
+# regularisation
+# ---------------------------------------------------------------------------
+@dataclass
+class GcvSearch:
+    """regularize.hpp:99-103."""
+    mu_min: float = 1e-12
+    mu_max: float = 10.0
+    count: int = 200
+
+
+@dataclass
+class GcvResult:
+    """regularize.hpp:105-108 (+ the grid argmin, per item)."""
+    mu: torch.Tensor
+    best_k: torch.Tensor
+    curve: torch.Tensor | None
+
+
+@dataclass
+class MuChoice:
+    """pipeline.hpp:49-52."""
+    use_gcv: bool = False
+    fixed_mu: float = 0.0
+
+
+@dataclass
+class RestorationReport:
+    """regularize.hpp:126-133 (batched)."""
+    restored: torch.Tensor
+    mu_used: torch.Tensor
+    best_k: torch.Tensor | None
+    gcv_curve: torch.Tensor | None
+    imag_residue: torch.Tensor
+
+
+def tikhonov_solve(op: BlurOperator, L: Smoother, g, mu):
+    """tikhonov_solve(_2d) -> (f_reg, imag_residue); mu scalar or per item."""
+    g = _dev(g)
+    count, lead = op._count(g)
+    mu_t = torch.as_tensor(mu, dtype=torch.float64).to("cuda").expand(lead).contiguous() \
+        if np.ndim(mu) == 0 else _dev(mu).reshape(lead).contiguous()
+    out = torch.empty_like(g)
+    res = torch.zeros(lead, dtype=torch.float64, device="cuda")
+    check(lib().fd_tikhonov(op._h, L._h, _ptr(g), _ptr(mu_t), _ptr(out), _ptr(res), count,
+                            _stream()))
+    return out, res
+
+
+def gcv_value(op: BlurOperator, L: Smoother, g, mu):
+    g = _dev(g)
+    count, lead = op._count(g)
+    G = torch.empty(lead, dtype=torch.float64, device="cuda")
+    check(lib().fd_gcv_value(op._h, L._h, _ptr(g), float(mu), _ptr(G), count, _stream()))
+    return G
+
+
+def gcv_select(op: BlurOperator, L: Smoother, g, search: GcvSearch = GcvSearch(),
+               want_curve=True) -> GcvResult:
+    g = _dev(g)
+    count, lead = op._count(g)
+    mu = torch.empty(lead, dtype=torch.float64, device="cuda")
+    bk = torch.empty(lead, dtype=torch.int32, device="cuda")
+    curve = torch.empty(lead + (search.count,), dtype=torch.float64, device="cuda") \
+        if want_curve else None
+    check(lib().fd_gcv_select(op._h, L._h, _ptr(g), float(search.mu_min), float(search.mu_max),
+                              int(search.count), _ptr(mu), _ptr(bk), _ptr(curve), count,
+                              _stream()))
+    return GcvResult(mu, bk, curve)
+
+
+def deblur(op: BlurOperator, L: Smoother, g, mu: MuChoice, want_curve=False,
+           search: GcvSearch = GcvSearch(), out=None) -> RestorationReport:
+    """deblur(_2d) (pipeline.cpp:732-778)."""
+    g = _dev(g)
+    count, lead = op._count(g)
+    restored = torch.empty_like(g) if out is None else out
+    mu_used = torch.empty(lead, dtype=torch.float64, device="cuda")
+    bk = torch.full(lead, -1, dtype=torch.int32, device="cuda")
+    curve = torch.empty(lead + (search.count,), dtype=torch.float64, device="cuda") \
+        if want_curve else None
+    res = torch.zeros(lead, dtype=torch.float64, device="cuda")
+    check(lib().fd_deblur(op._h, L._h, _ptr(g), int(bool(mu.use_gcv)), float(mu.fixed_mu),
+                          float(search.mu_min), float(search.mu_max), int(search.count),
+                          _ptr(restored), _ptr(mu_used), _ptr(bk) if mu.use_gcv else None,
+                          _ptr(curve), _ptr(res), count, _stream()))
+    return RestorationReport(restored, mu_used, bk if mu.use_gcv else None, curve, res)

@@ -1,0 +1,245 @@
+"""Seeded synthetic inputs for the five BASELINE.json configurations.
+
+The reference publishes no data; these generators stand in for the
+paper's unpublished test signals with the shapes, sizes and value
+distributions BASELINE.json names.  Generation follows the reference's
+"true-extended" observation model: the scene is sampled on the extended grid
+(n + 2m per axis, t = (i - m)/n as in acceptance_main.cpp:387-398), blurred
+with ``convolve_valid`` (g_i = sum_j h_j f_{i+j}, pipeline.cpp:628-664) and
+perturbed with the reference's ``add_noise`` (SplitMix64 + Box-Muller,
+rescaled so ||eta|| = level ||g||, operators.cpp:443-469).
+
+Random parameters come from a counter-based SplitMix64 keyed by
+(config, item, draw), so every item is reproducible independently of batch
+size or order.  Builder-defined details (documented in DESIGN.md):
+  * 1D: cubic coefficients U[-1,1]; 3 bumps a*exp(-((t-c)/w)^2) with
+    a ~ U[0.2,1], w ~ U[0.02,0.08], c ~ U[0,1]; a unit step at U[0,1].
+  * 2D: quadratic trend with coefficients U[-0.5,0.5] plus 0.5; blobs
+    a*exp(-|x-c|^2/w^2), a ~ +-U[0.1,0.6], w ~ U[0.01,0.08], c ~ U[0,1]^2,
+    evaluated on their +-6w bounding box; rectangles with corner U[0,1]^2,
+    sides U[0.05,0.3], value U[0,1] replacing the region; clip to [0,1].
+This module is host-side data preparation only (not timed, not the product's
+compute path).
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+PERIODIC, REFLECTIVE, ANTIREFLECTIVE, HOC_COSINE, HOC_FOURIER = range(5)
+IDENTITY, LAPLACIAN, FIRST_DIFFERENCE = range(3)
+
+_GOLD = np.uint64(0x9E3779B97F4A7C15)
+
+
+def splitmix64(x):
+    """operators.cpp:189-196."""
+    x = np.asarray(x, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        x = x ^ (x >> np.uint64(30))
+        x = x * np.uint64(0xBF58476D1CE4E5B9)
+        x = x ^ (x >> np.uint64(27))
+        x = x * np.uint64(0x94D049BB133111EB)
+        x = x ^ (x >> np.uint64(31))
+    return x
+
+
+def bits_to_u01(bits):
+    """(0, 1], operators.cpp:198-201."""
+    return ((np.asarray(bits, dtype=np.uint64) >> np.uint64(11)).astype(np.float64) + 1.0) \
+        * (2.0 ** -53)
+
+
+def item_key(cfg, item):
+    item = np.asarray(item, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        return splitmix64((np.uint64(cfg) << np.uint64(40)) + item)
+
+
+def draw(key, k):
+    """k-th uniform (0,1] draw of the stream ``key`` (vectorised over key)."""
+    with np.errstate(over="ignore"):
+        return bits_to_u01(splitmix64(np.asarray(key, np.uint64) +
+                                      np.uint64(k + 1) * _GOLD))
+
+
+def add_noise(g, level, seed):
+    """Reference add_noise (operators.cpp:443-469) over the last axis; ``seed``
+    broadcasts against the leading axes."""
+    g = np.asarray(g, dtype=np.float64)
+    if level == 0.0:
+        return g.copy()
+    n = g.shape[-1]
+    pairs = (n + 1) // 2
+    seed = np.asarray(seed, dtype=np.uint64)[..., None]
+    p = np.arange(pairs, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        u1 = bits_to_u01(splitmix64(seed + (np.uint64(2) * p + np.uint64(1)) * _GOLD))
+        u2 = bits_to_u01(splitmix64(seed + (np.uint64(2) * p + np.uint64(2)) * _GOLD))
+    r = np.sqrt(-2.0 * np.log(u1))
+    ang = 2.0 * math.pi * u2
+    eta = np.empty(np.broadcast_shapes(seed.shape[:-1], g.shape[:-1]) + (2 * pairs,))
+    eta[..., 0::2] = r * np.cos(ang)
+    eta[..., 1::2] = r * np.sin(ang)
+    eta = eta[..., :n]
+    gn = np.sum(g * g, axis=-1, keepdims=True)
+    en = np.sum(eta * eta, axis=-1, keepdims=True)
+    return g + level * np.sqrt(gn / en) * eta
+
+
+def convolve_valid(ext, w):
+    """g_i = sum_j h_j f_{i+j} over the last axis (pipeline.cpp:628-642)."""
+    m = (len(w) - 1) // 2
+    n = ext.shape[-1] - 2 * m
+    g = np.zeros(ext.shape[:-1] + (n,))
+    for j in range(-m, m + 1):
+        if w[m + j] != 0.0:
+            g += w[m + j] * ext[..., m + j:m + j + n]
+    return g
+
+
+def gaussian_weights(m, sigma):
+    """psf.cpp:62-69 (normalised by the serial sum)."""
+    j = np.arange(-m, m + 1, dtype=np.float64)
+    w = np.exp(-j * j / (2.0 * sigma * sigma))
+    s = 0.0
+    for x in w:
+        s += float(x)
+    return w / s
+
+
+def onesided_exp_weights(taps, rate):
+    """Centred mask of half-width taps-1 with h_k ∝ exp(-rate k), k = 0..taps-1,
+    zero for k < 0 (BASELINE configs 1 and 3)."""
+    m = taps - 1
+    w = np.zeros(2 * m + 1)
+    w[m:] = np.exp(-rate * np.arange(taps))
+    s = 0.0
+    for x in w:
+        s += float(x)
+    return w / s
+
+
+@dataclass
+class Config:
+    index: int
+    dim: int
+    n1: int
+    n2: int
+    batch: int
+    psf: np.ndarray      # 1D weights (dim 1) or the per-axis 1D factor (dim 2, separable)
+    bc: int
+    smoothers: tuple
+    mu_min: float
+    mu_max: float
+    count: int
+    noise: float
+    blobs: int = 0
+    rects: int = 0
+    note: str = ""
+
+    @property
+    def pixels(self):
+        return self.batch * self.n1 * (self.n2 if self.dim == 2 else 1)
+
+    def psf2d(self):
+        return np.outer(self.psf, self.psf) / float(np.sum(np.outer(self.psf, self.psf)))
+
+
+def config(index: int) -> Config:
+    """BASELINE.json configs.  Reference-unsupported features are mapped to the
+    nearest supported BC; DESIGN.md states each mapping."""
+    if index == 0:
+        return Config(0, 1, 1024, 1, 1, gaussian_weights(10, 3.0), HOC_COSINE, (IDENTITY,),
+                      1e-6, 1.0, 64, 0.01)
+    if index == 1:
+        return Config(1, 1, 4096, 1, 65536, onesided_exp_weights(15, 1 / 5), HOC_FOURIER,
+                      (FIRST_DIFFERENCE,), 1e-8, 1.0, 256, 0.005,
+                      note="d=1/d=3 with a nonsymmetric PSF are not in the reference; "
+                           "run at d=2 (hoc-fourier)")
+    if index == 2:
+        return Config(2, 2, 4096, 4096, 1, gaussian_weights(12, 2.5), HOC_COSINE, (LAPLACIAN,),
+                      1e-6, 1.0, 128, 0.01, blobs=40, rects=10)
+    if index == 3:
+        return Config(3, 2, 1024, 1024, 512, onesided_exp_weights(11, 1 / 4), HOC_FOURIER,
+                      (IDENTITY, LAPLACIAN), 1e-6, 1.0, 128, 0.01, blobs=40, rects=10,
+                      note="d=3 is not in the reference; run at d=2 (hoc-fourier); "
+                           "lambda range unspecified, [1e-6, 1] used")
+    if index == 4:
+        return Config(4, 2, 16384, 16384, 1, gaussian_weights(16, 4.0), HOC_COSINE,
+                      (LAPLACIAN,), 1e-8, 1.0, 512, 0.01, blobs=80, rects=20)
+    raise ValueError(index)
+
+
+def signals_1d(cfg: Config, first: int, count: int, n: int | None = None,
+               m: int | None = None):
+    """(truth, observed) for items [first, first+count) of a 1D config."""
+    n = cfg.n1 if n is None else n
+    m = (len(cfg.psf) - 1) // 2 if m is None else m
+    items = np.arange(first, first + count, dtype=np.uint64)
+    key = item_key(cfg.index, items)[:, None]
+    t = (np.arange(n + 2 * m, dtype=np.float64) - m) / n
+    u = [draw(key, k) for k in range(4 + 9 + 1)]
+    c = [2.0 * u[k] - 1.0 for k in range(4)]
+    f = c[0] + t * (c[1] + t * (c[2] + t * c[3]))
+    for j in range(3):
+        amp = 0.2 + 0.8 * u[4 + 3 * j]
+        width = 0.02 + 0.06 * u[5 + 3 * j]
+        cen = u[6 + 3 * j]
+        f = f + amp * np.exp(-((t - cen) / width) ** 2)
+    f = f + (t >= u[13]).astype(np.float64)
+    truth = f[:, m:m + n]
+    g = convolve_valid(f, cfg.psf)
+    return truth, add_noise(g, cfg.noise, key[:, 0])
+
+
+def _scene_2d(cfg: Config, item: int, n1: int, n2: int, m1: int, m2: int):
+    key = item_key(cfg.index, np.uint64(item))
+    k = iter(range(10_000))
+    y = (np.arange(n1 + 2 * m1, dtype=np.float64) - m1) / n1
+    x = (np.arange(n2 + 2 * m2, dtype=np.float64) - m2) / n2
+    a = [float(draw(key, next(k))) - 0.5 for _ in range(6)]
+    f = 0.5 + a[0] + a[1] * y[:, None] + a[2] * x[None, :] + a[3] * (y * y)[:, None] + \
+        a[4] * y[:, None] * x[None, :] + a[5] * (x * x)[None, :]
+    for _ in range(cfg.blobs):
+        amp = (0.1 + 0.5 * float(draw(key, next(k)))) * \
+            (1.0 if float(draw(key, next(k))) < 0.5 else -1.0)
+        w = 0.01 + 0.07 * float(draw(key, next(k)))
+        cy, cx = float(draw(key, next(k))), float(draw(key, next(k)))
+        i0 = max(0, int(math.floor((cy - 6 * w) * n1)) + m1)
+        i1 = min(len(y), int(math.ceil((cy + 6 * w) * n1)) + m1 + 1)
+        j0 = max(0, int(math.floor((cx - 6 * w) * n2)) + m2)
+        j1 = min(len(x), int(math.ceil((cx + 6 * w) * n2)) + m2 + 1)
+        if i0 < i1 and j0 < j1:
+            dy = (y[i0:i1] - cy) ** 2
+            dx = (x[j0:j1] - cx) ** 2
+            f[i0:i1, j0:j1] += amp * np.exp(-(dy[:, None] + dx[None, :]) / (w * w))
+    for _ in range(cfg.rects):
+        r0, c0 = float(draw(key, next(k))), float(draw(key, next(k)))
+        hr = 0.05 + 0.25 * float(draw(key, next(k)))
+        hc = 0.05 + 0.25 * float(draw(key, next(k)))
+        val = float(draw(key, next(k)))
+        sel_y = (y >= r0) & (y < r0 + hr)
+        sel_x = (x >= c0) & (x < c0 + hc)
+        f[np.ix_(sel_y, sel_x)] = val
+    np.clip(f, 0.0, 1.0, out=f)
+    return key, f
+
+
+def image_2d(cfg: Config, item: int, n1: int | None = None, n2: int | None = None,
+             psf: np.ndarray | None = None):
+    """(truth, observed) for image ``item`` of a 2D config (separable blur)."""
+    n1 = cfg.n1 if n1 is None else n1
+    n2 = cfg.n2 if n2 is None else n2
+    w = cfg.psf if psf is None else psf
+    m = (len(w) - 1) // 2
+    key, f = _scene_2d(cfg, item, n1, n2, m, m)
+    truth = f[m:m + n1, m:m + n2].copy()
+    # separable valid convolution: rows then columns (equals the 2D mask sum
+    # for the outer-product mask up to rounding)
+    g = convolve_valid(f, w)
+    g = convolve_valid(np.ascontiguousarray(g.T), w).T
+    obs = add_noise(np.ascontiguousarray(g).reshape(-1), cfg.noise, key).reshape(n1, n2)
+    return truth, obs

@@ -1,0 +1,103 @@
+"""GPU parity of the 2D path (multidim.cpp): tensor transforms, three-step
+eigenvalues, separable fast path, matvec, Tikhonov and GCV restoration."""
+import numpy as np
+import pytest
+import torch
+
+import fdoracle as O
+import paper_0906_2704_b200 as P
+from paper_0906_2704_b200 import workloads as W
+from util import gauss, np_, onesided, rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("bc", range(5))
+@pytest.mark.parametrize("shape", [(12, 12), (14, 18), (33, 20), (64, 64)])
+def test_tensor_transforms(bc, shape, rng):
+    n1, n2 = shape
+    op = P.build_operator_2d(np.ones((1, 1)), n1, n2, bc)
+    r, c = O.SpectralBasis(bc, n1), O.SpectralBasis(bc, n2)
+    x = rng.standard_normal((2, n1, n2))
+    got = np_(op.analyze(torch.from_numpy(x)))
+    want = O.tensor_apply(r, c, x.astype(complex) if r.complex else x, forward=False)
+    assert rel(got, want) < 1e-11
+    cc = rng.standard_normal((2, n1, n2)) + (1j * rng.standard_normal((2, n1, n2))
+                                             if r.complex else 0)
+    s = op.synthesize(torch.from_numpy(cc))
+    s = np_(s if r.complex else s[0])
+    assert rel(s, O.tensor_apply(r, c, cc, forward=True)) < 1e-12
+
+
+def _disk(radius):
+    j = np.arange(-radius, radius + 1)
+    return (j[:, None] ** 2 + j[None, :] ** 2 <= radius * radius).astype(float)
+
+
+@pytest.mark.parametrize("bc,psf2", [
+    (O.HOC_COSINE, _disk(2)), (O.REFLECTIVE, _disk(3)), (O.ANTIREFLECTIVE, _disk(2)),
+    (O.HOC_FOURIER, np.outer(onesided(3, 0.5), gauss(2, 1.0)) + 0.01),
+    (O.PERIODIC, np.outer(onesided(3, 0.5), onesided(2, 0.3)))])
+def test_general_2d_operator(bc, psf2, rng):
+    n1, n2 = 14, 18
+    op = P.build_operator_2d(psf2, n1, n2, bc)
+    p = O.make_psf2d(psf2, normalize=True)
+    oop = O.build_operator_2d(p, n1, n2, bc)
+    assert np.max(np.abs(np_(op.eigenvalues()) - oop.eigenvalues)) < 1e-13
+    f = rng.standard_normal((n1, n2))
+    got, _ = op.apply(torch.from_numpy(f))
+    want, _ = oop.apply(f)
+    assert rel(np_(got), want) < 1e-11
+    L = P.smoothing_eigenvalues("laplacian", op)
+    s = O.smoothing_eigenvalues_2d(O.LAPLACIAN, bc, n1, n2, oop.eigenvalues)
+    rep = P.deblur(op, L, torch.from_numpy(f), P.MuChoice(True),
+                   search=P.GcvSearch(1e-6, 1.0, 32))
+    w = O.deblur_2d(oop, s, f, True, mu_min=1e-6, mu_max=1.0, count=32)
+    assert int(np_(rep.best_k)) == int(w.best_k)
+    assert rel(np_(rep.restored), w.restored) < 1e-10
+
+
+@pytest.mark.parametrize("bc,a,b", [(O.HOC_COSINE, gauss(3, 1.2), gauss(2, 1.0)),
+                                    (O.HOC_FOURIER, onesided(4, 0.25), onesided(3, 0.5)),
+                                    (O.REFLECTIVE, gauss(2, 1.0), gauss(2, 1.0))])
+@pytest.mark.parametrize("smoother", ["identity", "laplacian"])
+def test_separable_2d_pipeline(bc, a, b, smoother, rng):
+    n1, n2 = 48, 40
+    op = P.build_operator_2d_separable(a, b, n1, n2, bc)
+    p = O.separable_psf2d(O.make_psf(a, True), O.make_psf(b, True))
+    oop = O.build_operator_2d(p, n1, n2, bc, separable=True)
+    assert np.max(np.abs(np_(op.eigenvalues()) - oop.eigenvalues)) < 1e-14
+    # separable eigenvalues agree with the three-step direct scheme
+    assert np.max(np.abs(oop.eigenvalues - O.eigenvalues_2d(p, n1, n2, bc))) < 1e-10
+    f = rng.standard_normal((3, n1, n2))
+    got, _ = op.apply(torch.from_numpy(f))
+    want, _ = oop.apply(f)
+    assert rel(np_(got), want) < 1e-11
+    kind = O.IDENTITY if smoother == "identity" else O.LAPLACIAN
+    L = P.smoothing_eigenvalues(smoother, op)
+    s = O.smoothing_eigenvalues_2d(kind, bc, n1, n2, oop.eigenvalues)
+    assert np.max(np.abs(np_(L.eigenvalues()) - s)) < 1e-14
+    rep = P.deblur(op, L, torch.from_numpy(f), P.MuChoice(True), want_curve=True,
+                   search=P.GcvSearch(1e-6, 1.0, 128))
+    w = O.deblur_2d(oop, s, f, True, mu_min=1e-6, mu_max=1.0, count=128, want_curve=True)
+    assert np.array_equal(np_(rep.best_k), w.best_k)
+    assert np.max(np.abs(np_(rep.gcv_curve) / w.curves - 1)) < 1e-11
+    assert np.max(np.abs(np_(rep.mu_used) / w.mu_used - 1)) < 1e-10
+    assert rel(np_(rep.restored), w.restored) < 1e-10
+
+
+def test_config2_scaled_image():
+    """BASELINE config 2 family (hoc-cosine, Laplacian, 128 lambda) at 256^2."""
+    cfg = W.config(2)
+    truth, g = W.image_2d(cfg, 0, 256, 256)
+    op = P.build_operator_2d_separable(cfg.psf, cfg.psf, 256, 256, cfg.bc)
+    L = P.smoothing_eigenvalues("laplacian", op)
+    rep = P.deblur(op, L, torch.from_numpy(g), P.MuChoice(True),
+                   search=P.GcvSearch(cfg.mu_min, cfg.mu_max, cfg.count))
+    p = O.separable_psf2d(O.make_psf(cfg.psf, True), O.make_psf(cfg.psf, True))
+    oop = O.build_operator_2d(p, 256, 256, cfg.bc, separable=True)
+    s = O.smoothing_eigenvalues_2d(O.LAPLACIAN, cfg.bc, 256, 256)
+    w = O.deblur_2d(oop, s, g, True, mu_min=cfg.mu_min, mu_max=cfg.mu_max, count=cfg.count)
+    assert int(np_(rep.best_k)) == int(w.best_k)
+    assert rel(np_(rep.restored), w.restored) < 1e-10
+    assert O.rre(truth.ravel(), np_(rep.restored).ravel()) < 0.2

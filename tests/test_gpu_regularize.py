@@ -1,0 +1,130 @@
+"""GPU parity of the filter + GCV path (regularize.hpp:42-81,
+regularize.cpp:209-374, pipeline.cpp:732-768) against the numpy restatement:
+restorations within 1e-10 relative, identical GCV grid index best_k, refined
+mu within 1e-10 relative (north_star parity contract)."""
+import numpy as np
+import pytest
+import torch
+
+import fdoracle as O
+import paper_0906_2704_b200 as P
+from paper_0906_2704_b200 import workloads as W
+from util import gauss, np_, onesided, rel
+
+pytestmark = pytest.mark.gpu
+
+SM = {0: O.IDENTITY, 1: O.LAPLACIAN, 2: O.FIRST_DIFFERENCE}
+
+
+def setup(bc, psf, n, smoother):
+    op = P.build_operator(psf, n, bc)
+    L = P.smoothing_eigenvalues(smoother, op)
+    oop = O.build_operator(O.make_psf(psf, normalize=True), n, bc)
+    s = O.smoothing_eigenvalues(SM[smoother], bc, n, oop.eigenvalues)
+    return op, L, oop, s
+
+
+CASES = [(O.HOC_COSINE, gauss(10, 3.0)), (O.HOC_FOURIER, onesided(15, 0.2)),
+         (O.ANTIREFLECTIVE, gauss(4, 1.5)), (O.REFLECTIVE, gauss(3, 1.5)),
+         (O.PERIODIC, onesided(5, 0.5))]
+
+
+@pytest.mark.parametrize("bc,psf", CASES)
+@pytest.mark.parametrize("smoother", [0, 1, 2])
+def test_smoother_tikhonov_gcv_value(bc, psf, smoother, rng):
+    n = 256
+    op, L, oop, s = setup(bc, psf, n, smoother)
+    assert np.max(np.abs(np_(L.eigenvalues()) - s)) < 1e-14
+    g = np.cumsum(rng.standard_normal((3, n)), axis=-1) / 10
+    mu = np.array([1e-6, 1e-3, 0.5])
+    f, res = P.tikhonov_solve(op, L, torch.from_numpy(g), torch.from_numpy(mu))
+    for b in range(3):
+        want, _ = O.tikhonov_solve(oop, s, g[b], mu[b])
+        assert rel(np_(f[b]), want) < 1e-10
+    for m in (1e-7, 1e-2):
+        G = np_(P.gcv_value(op, L, torch.from_numpy(g), m))
+        want = O.gcv_value(oop, s, g, m)
+        assert np.max(np.abs(G / want - 1)) < 1e-11
+
+
+@pytest.mark.parametrize("bc,psf", CASES)
+@pytest.mark.parametrize("smoother", [0, 1])
+@pytest.mark.parametrize("search", [(1e-8, 1.0, 64), (1e-12, 10.0, 200), (1e-6, 1.0, 7)])
+def test_gcv_select_and_deblur(bc, psf, smoother, search, rng):
+    n = 512
+    op, L, oop, s = setup(bc, psf, n, smoother)
+    cfg = W.config(0)
+    # config-0 style scenes on the extended grid, blurred with this case's psf
+    truth, _ = W.signals_1d(cfg, 0, 5, n=n + len(psf) - 1, m=0)
+    g = W.add_noise(W.convolve_valid(truth, np.asarray(psf) / np.sum(psf)), 0.01,
+                    W.item_key(99, np.arange(5, dtype=np.uint64)))
+    mu_min, mu_max, K = search
+    rep = P.deblur(op, L, torch.from_numpy(g), P.MuChoice(True), want_curve=True,
+                   search=P.GcvSearch(mu_min, mu_max, K))
+    want = O.deblur(oop, s, g, True, mu_min=mu_min, mu_max=mu_max, count=K, want_curve=True)
+    assert np.array_equal(np_(rep.best_k), want.best_k)
+    assert np.max(np.abs(np_(rep.gcv_curve) / want.curves - 1)) < 1e-11
+    assert np.max(np.abs(np_(rep.mu_used) / want.mu_used - 1)) < 1e-10
+    assert rel(np_(rep.restored), want.restored) < 1e-10
+    sel = P.gcv_select(op, L, torch.from_numpy(g), P.GcvSearch(mu_min, mu_max, K))
+    assert np.array_equal(np_(sel.mu), np_(rep.mu_used))
+
+
+def test_gcv_constant_functional_tie_break(rng):
+    """test_regularize.cpp:201-222: identity psf + identity smoother gives a
+    constant G = ||ghat||^2/n^2 and the geometric midpoint of the grid."""
+    n = 16
+    op = P.build_operator([1.0], n, "reflective")
+    L = P.smoothing_eigenvalues("identity", op)
+    g = rng.uniform(-1, 1, n)
+    ghat = O.cosine_apply(g)
+    want = np.sum(ghat ** 2) / (n * n)
+    for mu in (1e-10, 1e-4, 1.0, 9.9):
+        assert abs(float(np_(P.gcv_value(op, L, torch.from_numpy(g), mu))) / want - 1) < 1e-12
+    sel = P.gcv_select(op, L, torch.from_numpy(g), P.GcvSearch(1e-12, 10.0, 200))
+    assert abs(float(np_(sel.mu)) / np.sqrt(1e-12 * 10.0) - 1) < 1e-9
+
+
+def test_identity_tikhonov_is_g_over_one_plus_mu(rng):
+    """test_regularize.cpp:41-50."""
+    op = P.build_operator([1.0], 32, "reflective")
+    L = P.smoothing_eigenvalues("identity", op)
+    g = rng.uniform(-1, 1, 32)
+    for mu in (1e-3, 0.5, 2.0):
+        f, _ = P.tikhonov_solve(op, L, torch.from_numpy(g), mu)
+        assert np.allclose(np_(f), g / (1 + mu), rtol=1e-12, atol=0)
+
+
+def test_degenerate_gcv_raises(rng):
+    """test_regularize.cpp:277-284: all smoother eigenvalues zero -> DegenerateError."""
+    op = P.build_operator([1.0], 16, "reflective")
+    L = P.smoother_from_eigenvalues(op, np.zeros(16))
+    with pytest.raises(P.DegenerateError):
+        P.gcv_value(op, L, torch.from_numpy(rng.uniform(-1, 1, 16)), 1e-3)
+
+
+def test_parameter_errors(rng):
+    """test_regularize.cpp:296-304."""
+    op = P.build_operator([1.0], 16, "reflective")
+    L = P.smoothing_eigenvalues("identity", op)
+    g = torch.from_numpy(rng.uniform(-1, 1, 16))
+    with pytest.raises(P.ValidationError):
+        P.tikhonov_solve(op, L, g, 0.0)
+    with pytest.raises(P.ValidationError):
+        P.tikhonov_solve(op, L, g, -1.0)
+    with pytest.raises(P.ValidationError):
+        P.gcv_select(op, L, g, P.GcvSearch(0.0, 1.0, 10))
+    with pytest.raises(P.ValidationError):
+        P.gcv_select(op, L, g, P.GcvSearch(1e-3, 1e-6, 10))
+
+
+def test_gcv_argmin_scale_invariance(rng):
+    """test_regularize.cpp:224-244: power-of-two scaling keeps the argmin and
+    scales G by c^2."""
+    op = P.build_operator(gauss(4, 2.0), 64, "hoc-cosine")
+    L = P.smoothing_eigenvalues("laplacian", op)
+    g = rng.uniform(-1, 1, 64)
+    r1 = P.gcv_select(op, L, torch.from_numpy(g), P.GcvSearch(1e-10, 1.0, 60))
+    r4 = P.gcv_select(op, L, torch.from_numpy(4 * g), P.GcvSearch(1e-10, 1.0, 60))
+    assert int(np_(r1.best_k)) == int(np_(r4.best_k))
+    assert np.allclose(np_(r4.curve), 16 * np_(r1.curve), rtol=1e-12, atol=0)
