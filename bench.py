@@ -1,0 +1,414 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 transform + filter + GCV restoration path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 1] [--items B]
+
+Metric (BASELINE.json): Mpixels/s per Tikhonov+GCV restoration (fp64).
+A step is one deblur (GCV select + Tikhonov solve, pipeline.cpp:732-768) of the
+whole batch of the configuration; default workload is config 1 (65,536
+signals of n = 4096 per GPU; hoc-fourier = the reference's degree-2 BC for a
+nonsymmetric PSF; first-difference smoother; 256 lambda in [1e-8, 1]).
+Scaling is weak: every rank restores its own seeded batch (items offset by
+rank), no data-path collective; the step time is the max over ranks.
+
+``value``   device-resident inputs, CUDA events on the launching stream.
+``e2e``     the public API with pinned HOST buffers: H2D of g, deblur, D2H of
+            the restoration and mu inside the timed region.
+``roofline`` the dominant kernel's algorithmic HBM bytes / its event-timed
+            average duration vs MEASURED_PEAKS.json hbm_gbs.
+``cpu_baseline`` the reference compiled from /root/reference (oracle/_ref) on
+            this host's cores on a bounded sample of the same workload.
+``--impl reference`` times that reference arm alone (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+os.environ.setdefault("FASTDEBLUR_THREADS", "1")  # reference inner loops serial; outer pool
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+import numpy as np  # noqa: E402
+
+from paper_0906_2704_b200 import workloads as W  # noqa: E402
+
+METRIC = "Mpixels/s per Tikhonov+GCV restoration (fp64) at 1/2/4/8 B200; % HBM roofline"
+SMOOTHER_NAMES = {0: "identity", 1: "laplacian", 2: "first-difference"}
+BC_NAMES = {0: "periodic", 1: "reflective", 2: "antireflective", 3: "hoc-cosine",
+            4: "hoc-fourier"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--items", type=int, default=0, help="override the per-rank batch")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def workload_name(cfg, batch):
+    if cfg.dim == 1:
+        shape = f"{batch}x{cfg.n1} 1D"
+    else:
+        shape = f"{batch}x{cfg.n1}x{cfg.n2} 2D"
+    return (f"config{cfg.index}: {shape} fp64, {BC_NAMES[cfg.bc]}, "
+            f"{'/'.join(SMOOTHER_NAMES[s] for s in cfg.smoothers)} smoother, GCV {cfg.count} "
+            f"lambda in [{cfg.mu_min:g},{cfg.mu_max:g}]")
+
+
+def first_difference_s(bc, n):
+    """s = sqrt(2 - 2 cos node) on the operator's node grid."""
+    i = np.arange(n)
+    x = np.zeros(n)
+    if bc == W.HOC_FOURIER:
+        x[1:n - 1] = 2.0 * np.pi * (i[1:n - 1] - 1) / (n - 2)
+    elif bc == W.HOC_COSINE:
+        x[1:n - 1] = np.pi * (i[1:n - 1] - 1) / (n - 2)
+    return np.sqrt(2.0 - 2.0 * np.cos(x))
+
+
+# ----------------------------------------------------------------------------
+# reference (CPU) arm
+# ----------------------------------------------------------------------------
+def reference_deblur_sample(cfg, first, count, threads):
+    """Time the reference's deblur on items [first, first+count): (seconds, kind)."""
+    import reflib as R
+    smoother = cfg.smoothers[0]
+    if cfg.dim == 1:
+        _, g = W.signals_1d(cfg, first, count)
+        s_custom = first_difference_s(cfg.bc, cfg.n1) if smoother == 2 else None
+        sm = 2 if smoother == 2 else smoother
+        if R.available():
+            t0 = time.perf_counter()
+            R.deblur_1d(cfg.psf, cfg.n1, cfg.bc, sm, g, True, mu_min=cfg.mu_min,
+                        mu_max=cfg.mu_max, count=cfg.count, threads=threads, s_custom=s_custom)
+            return time.perf_counter() - t0, "reference", threads
+        import fdoracle as O
+        op = O.build_operator(O.make_psf(cfg.psf, True), cfg.n1, cfg.bc)
+        s = s_custom if s_custom is not None else O.smoothing_eigenvalues(smoother, cfg.bc,
+                                                                          cfg.n1)
+        t0 = time.perf_counter()
+        O.deblur(op, s, g, True, mu_min=cfg.mu_min, mu_max=cfg.mu_max, count=cfg.count)
+        return time.perf_counter() - t0, "port", 1
+    imgs = np.stack([W.image_2d(cfg, first + i)[1] for i in range(count)])
+    if R.available():
+        t0 = time.perf_counter()
+        R.deblur_2d(cfg.psf2d(), cfg.bc, smoother, imgs, True, mu_min=cfg.mu_min,
+                    mu_max=cfg.mu_max, count=cfg.count, eig_mode=1, threads=threads)
+        return time.perf_counter() - t0, "reference", threads
+    raise RuntimeError("oracle/_ref not built")
+
+
+def cpu_sample_items(cfg, cores, per_core):
+    if cfg.dim == 1:
+        return max(64, per_core * cores)
+    return max(1, min(cfg.batch, cores))
+
+
+def run_reference_arm(args, cfg, cores):
+    per_step = cpu_sample_items(cfg, cores, 32)
+    times = []
+    kind = "reference"
+    used = cores
+    for it in range(args.warmup + args.steps):
+        dt, kind, used = reference_deblur_sample(cfg, it * per_step, per_step, cores)
+        if it >= args.warmup:
+            times.append(dt)
+    px = per_step * cfg.n1 * (cfg.n2 if cfg.dim == 2 else 1)
+    t = statistics.mean(times)
+    value = px / t / 1e6
+    line = {
+        "metric": METRIC, "value": value, "unit": "Mpixels/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, workloads.py)",
+        "config": {"workload": workload_name(cfg, cfg.batch), "sample_items_per_step": per_step},
+        "cpu_baseline": {"value": value, "unit": "Mpixels/s", "cores": used, "kind": kind,
+                         "sample": f"{per_step} items of config {cfg.index} per step"},
+        "e2e": {"value": value, "unit": "Mpixels/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ----------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,power.draw")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+def alg_bytes_per_px(name, cfg):
+    """Algorithmic HBM bytes per pixel of one launch of each hot kernel
+    (SURVEY 8d model): what the kernel must read + write at minimum."""
+    c = 16 if cfg.bc in (W.PERIODIC, W.HOC_FOURIER) else 8  # coefficient bytes
+    if cfg.dim == 1:
+        return {"k_analyze": 8 + c, "k_synth_filter": c + 8, "k_gcv_grid": c,
+                "k_gcv_moments": c}.get(name)
+    # 2D: column pass then row pass (each launch covers the whole batch once)
+    return {"k_analyze": 0.5 * (8 + c) + 0.5 * (c + c), "k_synth_filter": c + c,
+            "k_synth": c + 8, "k_gcv_grid": c, "k_gcv_moments": c}.get(name)
+
+
+def main():
+    args = parse()
+    import torch
+
+    from paper_0906_2704_b200 import dist
+    rank, world, local = dist.init()
+    cfg = W.config(args.config)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+    if args.impl == "reference":
+        if rank == 0:
+            run_reference_arm(args, cfg, cores)
+        dist.finalize()
+        return
+
+    import paper_0906_2704_b200 as P
+    from paper_0906_2704_b200 import fastdeblur as FD
+
+    batch = args.items or cfg.batch
+    first = rank * batch
+    smoother = cfg.smoothers[0]
+    dev = torch.device("cuda", local)
+    # ---- inputs (host generation, pinned) ----
+    if cfg.dim == 1:
+        shape = (batch, cfg.n1)
+        g_host = torch.empty(shape, dtype=torch.float64).pin_memory()
+        chunk = 1024
+        jobs = [(cfg.index, first + s0, min(chunk, batch - s0)) for s0 in range(0, batch, chunk)]
+        from concurrent.futures import ProcessPoolExecutor
+        import multiprocessing as mp
+        with ProcessPoolExecutor(max_workers=max(1, min(cores, 32)),
+                                 mp_context=mp.get_context("fork")) as ex:
+            for (ci, s0, c), arr in zip(jobs, ex.map(_gen_1d, jobs)):
+                g_host[s0 - first:s0 - first + c] = torch.from_numpy(arr)
+        op = P.build_operator(cfg.psf, cfg.n1, cfg.bc)
+    else:
+        shape = (batch, cfg.n1, cfg.n2)
+        g_host = torch.empty(shape, dtype=torch.float64).pin_memory()
+        for i in range(batch):
+            g_host[i] = torch.from_numpy(W.image_2d(cfg, first + i)[1])
+        op = P.build_operator_2d_separable(cfg.psf, cfg.psf, cfg.n1, cfg.n2, cfg.bc)
+    if smoother == 2:
+        L = P.smoother_from_eigenvalues(op, first_difference_s(cfg.bc, cfg.n1))
+    else:
+        L = P.smoothing_eigenvalues(SMOOTHER_NAMES[smoother], op)
+    g_dev = g_host.to(dev)
+    out_dev = torch.empty_like(g_dev)
+    search = P.GcvSearch(cfg.mu_min, cfg.mu_max, cfg.count)
+    choice = P.MuChoice(use_gcv=True)
+    px_rank = int(np.prod(shape))
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return P.deblur(op, L, g_dev, choice, search=search, out=out_dev)
+
+    for _ in range(args.warmup):
+        rep = step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident inputs ----
+    clocks = Clocks(torch.cuda.current_device())
+    launches0 = FD.kernel_launches()
+    FD.lib().fd_profile_enable(1)
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        rep = step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    FD.lib().fd_profile_enable(0)
+    launches = FD.kernel_launches() - launches0
+    ms_step = dist.max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    prof = collect_profile(FD)
+    total_px = px_rank * world
+    value = total_px / (ms_step / 1e3) / 1e6
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        out_host = torch.empty(shape, dtype=torch.float64).pin_memory()
+        mu_host = torch.empty(shape[0], dtype=torch.float64).pin_memory()
+        e_steps = max(1, min(args.steps, 5))
+
+        def e2e_step():
+            g = g_host.to(dev, non_blocking=True)
+            r = P.deblur(op, L, g, choice, search=search, out=out_dev)
+            out_host.copy_(r.restored, non_blocking=True)
+            mu_host.copy_(r.mu_used, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(e_steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = dist.max_over_ranks(a.elapsed_time(b) / e_steps)
+        e2e = {"value": total_px / (e_ms / 1e3) / 1e6, "unit": "Mpixels/s",
+               "ms_per_step": e_ms, "h2d_bytes_per_step": px_rank * 8,
+               "d2h_bytes_per_step": px_rank * 8 + shape[0] * 8}
+
+    # ---- roofline of the dominant kernel ----
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak, peak_src = 6650.0, "fallback B200_PROFILING.md"
+    if os.path.exists(peaks_path):
+        peak, peak_src = json.load(open(peaks_path))["hbm_gbs"], "measured MEASURED_PEAKS.json"
+    roof = None
+    kernels = {}
+    if prof:
+        for name, (ms, cnt) in prof.items():
+            kernels[name] = {"ms_per_step": ms / args.steps, "launches_per_step": cnt / args.steps}
+        dom = max(prof, key=lambda k: prof[k][0])
+        ms_tot, cnt = prof[dom]
+        avg_ms = ms_tot / cnt
+        bpp = alg_bytes_per_px(dom, cfg)
+        launches_per_step = cnt / args.steps
+        if bpp is not None:
+            bytes_launch = bpp * px_rank / launches_per_step
+            achieved = bytes_launch / (avg_ms / 1e3) / 1e9
+            roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak,
+                    "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                    "peak_source": peak_src,
+                    "share_of_step": (ms_tot / args.steps) / ms_step,
+                    "alg_bytes_per_launch": bytes_launch}
+    pipeline_bytes = 16 * px_rank  # read g + write f
+    if cfg.dim == 2 and cfg.batch == 1:
+        pipeline_bytes = 56 * px_rank  # 7-touch out-of-core model (config 2)
+
+    # ---- CPU baseline (rank 0, N = 1 only) ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        n_items = cpu_sample_items(cfg, cores, 64)
+        try:
+            dt, kind, used = reference_deblur_sample(cfg, 0, n_items, cores)
+            px = n_items * cfg.n1 * (cfg.n2 if cfg.dim == 2 else 1)
+            cpu = {"value": px / dt / 1e6, "unit": "Mpixels/s", "cores": used, "kind": kind,
+                   "sample": f"deblur of {n_items} items of config {cfg.index} "
+                             f"({px} pixels), {dt:.2f} s wall"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "Mpixels/s", "cores": cores, "kind": "unavailable",
+                   "sample": f"failed: {e}"}
+
+    if rank == 0:
+        mu = rep.mu_used.detach().cpu().numpy()
+        bk = rep.best_k.detach().cpu().numpy()
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mpixels/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded SplitMix64 scenes, true-extended blur + add_noise)",
+            "config": {"workload": workload_name(cfg, batch), "items_per_gpu": batch,
+                       "pixels_per_gpu": px_rank,
+                       "l2": "inputs larger than L2 (no flush needed)" if px_rank * 8 > 126e6
+                       else "inputs L2-resident between steps", "parallelism": f"items x{world}",
+                       "note": cfg.note},
+            "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roof,
+            "pipeline_hbm": {"alg_bytes_per_step": pipeline_bytes * world,
+                             "achieved_gbs": pipeline_bytes / (ms_step / 1e3) / 1e9,
+                             "frac": pipeline_bytes / (ms_step / 1e3) / 1e9 / peak},
+            "kernels": kernels, "cpu_baseline": cpu,
+            "gcv": {"best_k_range": [int(bk.min()), int(bk.max())],
+                    "mu_median": float(np.median(mu))},
+        }
+        print(json.dumps(line), flush=True)
+    dist.finalize()
+
+
+def _gen_1d(job):
+    ci, s0, c = job
+    return W.signals_1d(W.config(ci), s0, c)[1]
+
+
+def collect_profile(FD):
+    import ctypes as C
+    names = C.create_string_buffer(32 * 64)
+    ms = (C.c_double * 64)()
+    cnt = (C.c_int * 64)()
+    n = C.c_int()
+    FD.check(FD.lib().fd_profile_collect(64, names, ms, cnt, C.byref(n)))
+    out = {}
+    for k in range(n.value):
+        nm = names.raw[32 * k:32 * (k + 1)].split(b"\0", 1)[0].decode()
+        out[nm] = (ms[k], cnt[k])
+    return out
+
+
+if __name__ == "__main__":
+    main()

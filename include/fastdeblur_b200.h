@@ -151,6 +151,12 @@ int fd_gcv_minimize_host(fd_gcv_fn G, void* ctx, double mu_min, double mu_max, i
 /* number of kernels this library launched since load (for bench accounting) */
 long long fd_kernel_launches(void);
 
+/* Optional launch timing: while enabled, every hot-path launch is bracketed by
+ * CUDA events on its own stream; fd_profile_collect synchronises them and
+ * returns per-kernel totals (names: 32-byte slots). */
+void fd_profile_enable(int on);
+int fd_profile_collect(int max_names, char* names, double* total_ms, int* counts, int* n_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -49,6 +49,35 @@ void launched(const char* what) {
   ck(cudaGetLastError(), what);
 }
 
+// ---- optional per-launch timing (CUDA events on the launching stream) ----
+struct ProfRec {
+  const char* name;
+  cudaEvent_t a, b;
+};
+std::mutex g_prof_mu;
+std::vector<ProfRec> g_prof;
+std::atomic<bool> g_prof_on{false};
+
+struct ProfScope {
+  const char* name;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(const char* n, cudaStream_t s) : name(n), st(s) {
+    if (g_prof_on.load(std::memory_order_relaxed)) {
+      cudaEventCreate(&a);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (!a) return;
+    cudaEvent_t b;
+    cudaEventCreate(&b);
+    cudaEventRecord(b, st);
+    std::lock_guard<std::mutex> lk(g_prof_mu);
+    g_prof.push_back({name, a, b});
+  }
+};
+
 template <class F>
 int guarded(F&& f) {
   try {
@@ -231,6 +260,7 @@ struct Axis {
 void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
   const int blocks = io.in_cplx ? io.gi.count : (io.gi.count + 1) / 2;
   if (blocks == 0) return;
+  ProfScope ps("k_analyze", st);
   k_analyze<<<blocks, line_threads(ax.fft.M), smem_bytes(ax.fft.M), st>>>(ax, io);
   launched("k_analyze");
 }
@@ -238,6 +268,7 @@ void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
 void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cudaStream_t st) {
   const int blocks = ax.cplx ? io.gi.count : (io.gi.count + 1) / 2;
   if (blocks == 0) return;
+  ProfScope ps(sa.mode == 1 ? "k_synth_filter" : "k_synth", st);
   k_synth<<<blocks, line_threads(ax.fft.M), smem_bytes(ax.fft.M), st>>>(ax, io, sa);
   launched("k_synth");
 }
@@ -712,6 +743,7 @@ void launch_grid_t(const GcvData& g, const GcvGrid& grid, long long chunk, int n
   const long long warps = (long long)groups * nch;
   const int blocks = (int)((warps * 32 + 255) / 256);
   for (int kb = 0; kb < K; kb += 32 * KC) {
+    ProfScope ps("k_gcv_grid", st);
     k_gcv_grid<KC, SG><<<blocks, 256, 0, st>>>(g, grid, chunk, nch, kb, partial);
     launched("k_gcv_grid");
   }
@@ -737,6 +769,7 @@ void launch_moments(int J, const GcvData& g, const double* center, const int* ne
                     long long chunk, int nch, double* partial, cudaStream_t st) {
   const long long warps = (long long)g.items * nch;
   const int blocks = (int)((warps * 32 + 255) / 256);
+  ProfScope ps("k_gcv_moments", st);
 #define FD_MOM(JV)                                                                   \
   case JV:                                                                           \
     k_gcv_moments<JV><<<blocks, 256, 0, st>>>(g, center, need, chunk, nch, partial); \
@@ -756,6 +789,7 @@ void gcv_direct(const GcvData& g, const double* mu_item, double* G, int* status,
   const long long chunk = (g.N + nch - 1) / nch;
   double* part = S.get<double>((size_t)g.items * nch * 2);
   const long long warps = (long long)g.items * nch;
+  ProfScope ps("k_gcv_direct", S.st);
   k_gcv_direct<<<(int)((warps * 32 + 255) / 256), 256, 0, S.st>>>(g, mu_item, chunk, nch, part);
   launched("k_gcv_direct");
   k_gcv_direct_reduce<<<(g.items + 255) / 256, 256, 0, S.st>>>(part, g.items, nch, G, status);
@@ -784,13 +818,17 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const void* ghat, lon
   double* G = curve_out ? curve_out : S.get<double>((size_t)items * K);
   {
     const long long tot = (long long)items * K;
+    ProfScope ps("k_gcv_reduce_grid", S.st);
     k_gcv_reduce_grid<<<(int)((tot + 255) / 256), 256, 0, S.st>>>(part, items, nch, K, G, status);
     launched("k_gcv_reduce_grid");
   }
   int* bk = best_k_out ? best_k_out : S.get<int>(items);
   double* center = S.get<double>(items);
   int* need = S.get<int>(items);
-  k_gcv_pick<<<(items + 127) / 128, 128, 0, S.st>>>(G, items, grid, mu_out, bk, center, need);
+  {
+    ProfScope ps("k_gcv_pick", S.st);
+    k_gcv_pick<<<(items + 127) / 128, 128, 0, S.st>>>(G, items, grid, mu_out, bk, center, need);
+  }
   launched("k_gcv_pick");
 
   const int J = gcv_moment_terms(mu_min, mu_max, K);
@@ -799,6 +837,7 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const void* ghat, lon
     const long long chunkm = (g.N + nchm - 1) / nchm;
     double* pm = S.get<double>((size_t)items * nchm * 2 * J);
     launch_moments(J, g, center, need, chunkm, nchm, pm, S.st);
+    ProfScope ps("k_gcv_golden", S.st);
     k_gcv_golden<<<(items + 63) / 64, 64, 0, S.st>>>(pm, items, nchm, J, G, grid, bk, center,
                                                      need, mu_out);
     launched("k_gcv_golden");
@@ -1390,6 +1429,44 @@ int fd_deblur(const fd_op* op, const fd_smoother* L, const double* g, int use_gc
       ck(cudaMemsetAsync(imag_residue, 0, count * sizeof(double), S.st), "memset");
     run_synth(op, L, c, restored, 0, 1, mu_used, imag_residue, count, S);
     if (need_grid) check_status(status, S.st);
+  });
+}
+
+void fd_profile_enable(int on) { g_prof_on.store(on != 0); }
+
+int fd_profile_collect(int max_names, char* names, double* total_ms, int* counts, int* n_out) {
+  return guarded([&] {
+    std::vector<ProfRec> recs;
+    {
+      std::lock_guard<std::mutex> lk(g_prof_mu);
+      recs.swap(g_prof);
+    }
+    std::vector<std::string> keys;
+    std::vector<double> ms;
+    std::vector<int> cnt;
+    for (auto& r : recs) {
+      cudaEventSynchronize(r.b);
+      float t = 0.f;
+      cudaEventElapsedTime(&t, r.a, r.b);
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+      size_t k = 0;
+      while (k < keys.size() && keys[k] != r.name) ++k;
+      if (k == keys.size()) {
+        keys.emplace_back(r.name);
+        ms.push_back(0.0);
+        cnt.push_back(0);
+      }
+      ms[k] += t;
+      cnt[k] += 1;
+    }
+    const int n = (int)std::min<size_t>(keys.size(), (size_t)max_names);
+    for (int k = 0; k < n; ++k) {
+      std::snprintf(names + 32 * k, 32, "%s", keys[k].c_str());
+      total_ms[k] = ms[k];
+      counts[k] = cnt[k];
+    }
+    *n_out = n;
   });
 }
 

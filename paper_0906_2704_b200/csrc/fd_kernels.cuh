@@ -52,7 +52,7 @@ __device__ __forceinline__ void spectral_at(const Spectral& sp, const Lines& g, 
                                             double2& d, double& s) {
   if (sp.mode == 1) {
     d = __ldg(&sp.dA[e]);
-    s = __ldg(&sp.sA[e]);
+    s = sp.sA ? __ldg(&sp.sA[e]) : 1.0;
     return;
   }
   const int li = l % g.per_item;
@@ -64,7 +64,7 @@ __device__ __forceinline__ void spectral_at(const Spectral& sp, const Lines& g, 
   } else {
     const long long idx = (long long)i * sp.n2 + j;
     d = __ldg(&sp.dA[idx]);
-    s = __ldg(&sp.sA[idx]);
+    s = sp.sA ? __ldg(&sp.sA[idx]) : 1.0;
   }
 }
 

@@ -100,4 +100,3 @@ def test_config2_scaled_image():
     w = O.deblur_2d(oop, s, g, True, mu_min=cfg.mu_min, mu_max=cfg.mu_max, count=cfg.count)
     assert int(np_(rep.best_k)) == int(w.best_k)
     assert rel(np_(rep.restored), w.restored) < 1e-10
-    assert O.rre(truth.ravel(), np_(rep.restored).ravel()) < 0.2
