@@ -266,7 +266,8 @@ void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
 }
 
 void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cudaStream_t st) {
-  const int blocks = ax.cplx ? io.gi.count : (io.gi.count + 1) / 2;
+  const bool hpack = ax.cplx && !io.out_cplx && sa.resid2 == nullptr;
+  const int blocks = (ax.cplx && !hpack) ? io.gi.count : (io.gi.count + 1) / 2;
   if (blocks == 0) return;
   ProfScope ps(sa.mode == 1 ? "k_synth_filter" : "k_synth", st);
   k_synth<<<blocks, line_threads(ax.fft.M), smem_bytes(ax.fft.M), st>>>(ax, io, sa);
@@ -765,6 +766,39 @@ void launch_grid(const GcvData& g, const GcvGrid& grid, int sg, long long chunk,
 #undef FD_GRID
 }
 
+size_t gemm_smem(int nj) { return (size_t)(64 * 32 + 32 * 32 * nj + 32 + 256) * sizeof(double); }
+
+template <int NJ>
+void launch_gemm_t(const GcvData& g, const GcvGrid& grid, long long echunk, int nch,
+                   double* partial, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    ck(cudaFuncSetAttribute(k_gcv_gemm<NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)gemm_smem(NJ)),
+       "gemm attr");
+    attr = true;
+  }
+  const dim3 blocks((g.items + 63) / 64, nch);
+  for (int kb = 0; kb < grid.count; kb += 32 * NJ) {
+    ProfScope ps("k_gcv_grid", st);
+    k_gcv_gemm<NJ><<<blocks, 256, gemm_smem(NJ), st>>>(g, grid, kb, echunk, nch, partial);
+    launched("k_gcv_gemm");
+  }
+}
+
+void launch_gemm(const GcvData& g, const GcvGrid& grid, long long echunk, int nch,
+                 double* partial, cudaStream_t st) {
+  const int K = grid.count;
+  if (K <= 32)
+    launch_gemm_t<1>(g, grid, echunk, nch, partial, st);
+  else if (K <= 64)
+    launch_gemm_t<2>(g, grid, echunk, nch, partial, st);
+  else if (K <= 128)
+    launch_gemm_t<4>(g, grid, echunk, nch, partial, st);
+  else
+    launch_gemm_t<8>(g, grid, echunk, nch, partial, st);
+}
+
 void launch_moments(int J, const GcvData& g, const double* center, const int* need,
                     long long chunk, int nch, double* partial, cudaStream_t st) {
   const long long warps = (long long)g.items * nch;
@@ -810,11 +844,24 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const void* ghat, lon
   const GcvData g = gcv_data(op, L, ghat, count);
   const int items = (int)count;
 
-  const int sg = items >= 4 * 148 * 8 ? 4 : 1;
-  const int nch = pick_chunks(g.N, items, sg);
-  const long long chunk = (g.N + nch - 1) / nch;
-  double* part = S.get<double>((size_t)items * nch * 2 * K);
-  launch_grid(g, grid, sg, chunk, nch, part, S.st);
+  int nch;
+  double* part;
+  if (items >= 32) {
+    // shared-operator batch: fp64 GEMM form (k_gcv_gemm)
+    const int sblocks = (items + 63) / 64;
+    nch = (int)std::max(1LL, std::min((296LL + sblocks - 1) / sblocks, g.N / 256));
+    long long echunk = (g.N + nch - 1) / nch;
+    echunk = (echunk + 31) / 32 * 32;
+    nch = (int)((g.N + echunk - 1) / echunk);
+    part = S.get<double>((size_t)items * nch * 2 * K);
+    launch_gemm(g, grid, echunk, nch, part, S.st);
+  } else {
+    const int sg = 1;
+    nch = pick_chunks(g.N, items, sg);
+    const long long chunk = (g.N + nch - 1) / nch;
+    part = S.get<double>((size_t)items * nch * 2 * K);
+    launch_grid(g, grid, sg, chunk, nch, part, S.st);
+  }
   double* G = curve_out ? curve_out : S.get<double>((size_t)items * K);
   {
     const long long tot = (long long)items * K;

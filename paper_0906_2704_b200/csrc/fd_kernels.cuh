@@ -538,7 +538,13 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
   double2* x = sm;
   double* red = reinterpret_cast<double*>(sm + pidx(M) + 1);
 
-  const bool pair = !ax.cplx;  // real bases: real coefficients, two lines per FFT
+  // Real bases: real coefficients, two lines per FFT.  Complex bases with a
+  // real output and no residue request: the real part of T_X c only depends
+  // on the Hermitian part of the interior coefficients (F^H of the
+  // anti-Hermitian part is purely imaginary), so two lines share one FFT as
+  // z = herm(c0) + i herm(c1).
+  const bool hpack = ax.cplx && !io.out_cplx && sa.resid2 == nullptr;
+  const bool pair = !ax.cplx || hpack;
   const int l0 = pair ? 2 * blockIdx.x : blockIdx.x;
   if (l0 >= io.gi.count) return;
   const bool has1 = pair && (l0 + 1 < io.gi.count);
@@ -603,6 +609,27 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
       }
       x[pidx(p)] = val;
     }
+  } else if (hpack) {  // IK_FOURIER, two Hermitian-projected lines per FFT
+    for (int j = threadIdx.x; j < M; j += blockDim.x) {
+      double2 val = czero();
+      if (j < m) {
+        const int jc = j == 0 ? 0 : m - j;
+        const int e = interior_elem(ax, j), ec = interior_elem(ax, jc);
+        const double2 z0 = c0(e), z0c = c0(ec), z1 = c1(e), z1c = c1(ec);
+        const double2 h0 = cscale(cadd(z0, cconj(z0c)), 0.5);
+        const double2 h1 = cscale(cadd(z1, cconj(z1c)), 0.5);
+        const double2 z = make_double2(h0.x - h1.y, h0.y + h1.x);
+        val = cmul(cconj(z), __ldg(&chirp[j]));
+        if (dots) {
+          const double2 ca = __ldg(&ax.c_a[j]), cb = __ldg(&ax.c_b[j]);
+          const double2 t0 = cmul(ca, z0), b0 = cmul(cb, z0);
+          const double2 t1 = cmul(ca, z1), b1 = cmul(cb, z1);
+          acc[0] += t0.x, acc[1] += t0.y, acc[2] += b0.x, acc[3] += b0.y;
+          acc[4] += t1.x, acc[5] += t1.y, acc[6] += b1.x, acc[7] += b1.y;
+        }
+      }
+      x[pidx(j)] = val;
+    }
   } else {  // IK_FOURIER: F^H v = conj(F conj(v)) (trig.cpp:170-178)
     for (int j = threadIdx.x; j < M; j += blockDim.x) {
       double2 val = czero();
@@ -640,13 +667,17 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
       const double2 Z = cmul(x[pidx(p + 1)], __ldg(&chirp[p + 1]));
       in0 = make_double2(sc * Z.y, 0.0);
       in1 = make_double2(-sc * Z.x, 0.0);
+    } else if (hpack) {
+      const double2 Z = cconj(cmul(x[pidx(p)], __ldg(&chirp[p])));
+      in0 = make_double2(Z.x * inv_sqrt_m, 0.0);
+      in1 = make_double2(Z.y * inv_sqrt_m, 0.0);
     } else {
       in0 = cscale(cconj(cmul(x[pidx(p)], __ldg(&chirp[p]))), inv_sqrt_m);
     }
     const int e = interior_elem(ax, p);
     if (ax.bordered) {
       const double qi = __ldg(&ax.q[e]), qr = __ldg(&ax.q[n - 1 - e]);
-      if (ax.cplx) {
+      if (ax.cplx && !hpack) {
         const double2 o = cadd(cadd(cscale(u00, qi), in0), cscale(un0, qr));
         stc(io.out, io.out_cplx, oo0 + e * eso, o);
         im2 += o.y * o.y;
@@ -660,7 +691,7 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
       }
     } else {
       stc(io.out, io.out_cplx, oo0 + e * eso, in0);
-      im2 += in0.y * in0.y;
+      if (!hpack) im2 += in0.y * in0.y;
       if (has1) stc(io.out, io.out_cplx, oo1 + e * eso, in1);
     }
   }
@@ -675,7 +706,7 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
       const long long oo = t == 0 ? oo0 : oo1;
       stc(io.out, io.out_cplx, oo, o0);
       stc(io.out, io.out_cplx, oo + (long long)(n - 1) * eso, on);
-      if (ax.cplx) im2 += o0.y * o0.y + on.y * on.y;
+      if (ax.cplx && !hpack) im2 += o0.y * o0.y + on.y * on.y;
     }
   }
   if (ax.cplx && sa.resid2 != nullptr) {
@@ -799,6 +830,121 @@ __global__ void __launch_bounds__(256) k_gcv_grid(GcvData g, GcvGrid grid, long 
       if (k0 + k < K) {
         base[k0 + k] = num[p][k];
         base[K + k0 + k] = den[k];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GCV grid for batches sharing one operator, as a register-tiled fp64 GEMM
+// (SURVEY H3(a)): num[b][k] = sum_e w[b][e] * sigma[e][k]^2.  Per element
+// chunk of 32, the CTA generates sigma^2 for its 32*NJ grid values once in
+// shared memory (one reciprocal per 4 elements by batch inversion) and every
+// thread accumulates an 8-signal x NJ-mu micro-tile from shared memory, so
+// sigma generation is amortised over 64 signals instead of repeated per
+// signal.  den[k] = sum_e sigma is item independent and produced by the same
+// pass.  Grid: x = signal blocks of 64, y = element ranges.
+// ---------------------------------------------------------------------------
+template <int NJ>
+__global__ void __launch_bounds__(256) k_gcv_gemm(GcvData g, GcvGrid grid, int kb0,
+                                                  long long echunk, int nch, double* partial) {
+  constexpr int BS = 64, E = 32, BK = 32 * NJ, GP = 256 / BK;
+  extern __shared__ double gsm[];
+  double* Wt = gsm;              // [BS][E]
+  double* Sg = gsm + BS * E;     // [E][BK]
+  double* Rt = Sg + E * BK;      // [E]
+  double* Dn = Rt + E;           // [256] den partials
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int item0 = blockIdx.x * BS;
+  const int er = blockIdx.y;
+  const long long eb = (long long)er * echunk;
+  const long long ee = min(g.N, eb + echunk);
+  const int K = grid.count;
+  const int kk = tid % BK, part = tid / BK;
+  const double mu = (kb0 + kk < K) ? grid.mus[kb0 + kk] : 1.0;
+  double acc[8][NJ];
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[s][j] = 0.0;
+  double den = 0.0;
+  for (long long e0 = eb; e0 < ee; e0 += E) {
+#pragma unroll
+    for (int q = 0; q < BS * E / 256; ++q) {
+      const int idx = tid + 256 * q;
+      const int sidx = idx >> 5, e = idx & 31;
+      const int item = item0 + sidx;
+      Wt[idx] = (item < g.items && e0 + e < ee) ? gcv_w(g, item, e0 + e) : 0.0;
+    }
+    if (tid < E) Rt[tid] = (e0 + tid < ee) ? gcv_ratio(g, e0 + tid) : INFINITY;
+    __syncthreads();
+    // sigma^2 for (element e, grid value kk); GP threads share one grid value
+    constexpr int EPT = E / GP;
+#pragma unroll
+    for (int e4 = 0; e4 < EPT; e4 += 4) {
+      const int eb4 = part * EPT + e4;
+      double x[4], pre[4], sg[4];
+      bool dead[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const double r = Rt[eb4 + t];
+        dead[t] = !(r < 1e30);  // s = 0 (inf) or absurdly large: handled below
+        x[t] = dead[t] ? 1.0 : r + mu;
+      }
+      pre[0] = x[0];
+#pragma unroll
+      for (int t = 1; t < 4; ++t) pre[t] = pre[t - 1] * x[t];
+      double inv = 1.0 / pre[3];
+#pragma unroll
+      for (int t = 3; t >= 1; --t) {
+        sg[t] = inv * pre[t - 1];
+        inv *= x[t];
+      }
+      sg[0] = inv;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (dead[t]) {
+          const double r = Rt[eb4 + t];
+          sg[t] = isinf(r) ? 0.0 : 1.0 / (r + mu);
+        }
+        den += sg[t];
+        Sg[(eb4 + t) * BK + kk] = sg[t] * sg[t];
+      }
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int e = 0; e < E; ++e) {
+      double a[8], b[NJ];
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) a[s2] = Wt[(ty * 8 + s2) * E + e];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) b[j] = Sg[e * BK + tx + 32 * j];
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc[s2][j] = fma(a[s2], b[j], acc[s2][j]);
+    }
+    __syncthreads();
+  }
+  Dn[tid] = den;
+  __syncthreads();
+  if (tid < BK) {
+    double dsum = 0.0;
+    for (int p = 0; p < GP; ++p) dsum += Dn[p * BK + tid];
+    Dn[tid] = dsum;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int s2 = 0; s2 < 8; ++s2) {
+    const int item = item0 + ty * 8 + s2;
+    if (item >= g.items) continue;
+    double* base = partial + ((long long)item * nch + er) * 2 * K;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int k = kb0 + tx + 32 * j;
+      if (k < K) {
+        base[k] = acc[s2][j];
+        base[K + k] = Dn[tx + 32 * j];
       }
     }
   }

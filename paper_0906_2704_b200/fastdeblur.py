@@ -313,14 +313,19 @@ class RestorationReport:
     imag_residue: torch.Tensor
 
 
-def tikhonov_solve(op: BlurOperator, L: Smoother, g, mu):
-    """tikhonov_solve(_2d) -> (f_reg, imag_residue); mu scalar or per item."""
+def tikhonov_solve(op: BlurOperator, L: Smoother, g, mu, want_imag_residue=False):
+    """tikhonov_solve(_2d) -> (f_reg, imag_residue); mu scalar or per item.
+
+    The imaginary residue of complex bases is a diagnostic (operators.cpp:334-340);
+    requesting it runs the exact one-line-per-FFT synthesis, otherwise two real
+    lines share each FFT and imag_residue is None."""
     g = _dev(g)
     count, lead = op._count(g)
     mu_t = torch.as_tensor(mu, dtype=torch.float64).to("cuda").expand(lead).contiguous() \
         if np.ndim(mu) == 0 else _dev(mu).reshape(lead).contiguous()
     out = torch.empty_like(g)
-    res = torch.zeros(lead, dtype=torch.float64, device="cuda")
+    res = torch.zeros(lead, dtype=torch.float64, device="cuda") \
+        if (want_imag_residue or not op.complex) else None
     check(lib().fd_tikhonov(op._h, L._h, _ptr(g), _ptr(mu_t), _ptr(out), _ptr(res), count,
                             _stream()))
     return out, res
@@ -349,8 +354,9 @@ def gcv_select(op: BlurOperator, L: Smoother, g, search: GcvSearch = GcvSearch()
 
 
 def deblur(op: BlurOperator, L: Smoother, g, mu: MuChoice, want_curve=False,
-           search: GcvSearch = GcvSearch(), out=None) -> RestorationReport:
-    """deblur(_2d) (pipeline.cpp:732-778)."""
+           search: GcvSearch = GcvSearch(), out=None,
+           want_imag_residue=False) -> RestorationReport:
+    """deblur(_2d) (pipeline.cpp:732-778).  imag_residue as in tikhonov_solve."""
     g = _dev(g)
     count, lead = op._count(g)
     restored = torch.empty_like(g) if out is None else out
@@ -358,7 +364,8 @@ def deblur(op: BlurOperator, L: Smoother, g, mu: MuChoice, want_curve=False,
     bk = torch.full(lead, -1, dtype=torch.int32, device="cuda")
     curve = torch.empty(lead + (search.count,), dtype=torch.float64, device="cuda") \
         if want_curve else None
-    res = torch.zeros(lead, dtype=torch.float64, device="cuda")
+    res = torch.zeros(lead, dtype=torch.float64, device="cuda") \
+        if (want_imag_residue or not op.complex) else None
     check(lib().fd_deblur(op._h, L._h, _ptr(g), int(bool(mu.use_gcv)), float(mu.fixed_mu),
                           float(search.mu_min), float(search.mu_max), int(search.count),
                           _ptr(restored), _ptr(mu_used), _ptr(bk) if mu.use_gcv else None,

@@ -128,3 +128,44 @@ def test_gcv_argmin_scale_invariance(rng):
     r4 = P.gcv_select(op, L, torch.from_numpy(4 * g), P.GcvSearch(1e-10, 1.0, 60))
     assert int(np_(r1.best_k)) == int(np_(r4.best_k))
     assert np.allclose(np_(r4.curve), 16 * np_(r1.curve), rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("bc,psf,smoother,search", [
+    (O.HOC_FOURIER, onesided(15, 0.2), 2, (1e-8, 1.0, 256)),
+    (O.HOC_COSINE, gauss(10, 3.0), 0, (1e-6, 1.0, 64)),
+    (O.HOC_COSINE, gauss(6, 2.0), 1, (1e-6, 1.0, 128)),
+    (O.PERIODIC, onesided(5, 0.5), 1, (1e-10, 1.0, 300))])
+def test_batched_gemm_gcv_path(bc, psf, smoother, search):
+    """Batches of >= 32 signals take the GEMM-form GCV grid (k_gcv_gemm)."""
+    n, B = 1024, 97
+    op, L, oop, s = setup(bc, psf, n, smoother)
+    cfg = W.config(1)
+    truth, _ = W.signals_1d(cfg, 100, B, n=n + len(psf) - 1, m=0)
+    g = W.add_noise(W.convolve_valid(truth, np.asarray(psf) / np.sum(psf)), 0.005,
+                    W.item_key(98, np.arange(B, dtype=np.uint64)))
+    mu_min, mu_max, K = search
+    rep = P.deblur(op, L, torch.from_numpy(g), P.MuChoice(True), want_curve=True,
+                   search=P.GcvSearch(mu_min, mu_max, K))
+    want = O.deblur(oop, s, g, True, mu_min=mu_min, mu_max=mu_max, count=K, want_curve=True)
+    assert np.array_equal(np_(rep.best_k), want.best_k)
+    assert np.max(np.abs(np_(rep.gcv_curve) / want.curves - 1)) < 1e-11
+    assert np.max(np.abs(np_(rep.mu_used) / want.mu_used - 1)) < 1e-10
+    assert rel(np_(rep.restored), want.restored) < 1e-10
+
+
+@pytest.mark.parametrize("bc", [O.HOC_FOURIER, O.PERIODIC])
+def test_hermitian_packed_synthesis(bc, rng):
+    """Real outputs of complex bases: two Hermitian-projected lines per FFT give
+    Re(T c) of the exact one-line path."""
+    n = 4096
+    psf = onesided(15, 0.2)
+    op, L, oop, s = setup(bc, psf, n, 1)
+    g = np.cumsum(rng.standard_normal((5, n)), axis=-1) / 30
+    mu = np.array([1e-6, 1e-4, 1e-3, 1e-2, 1.0])
+    f_fast, r_fast = P.tikhonov_solve(op, L, torch.from_numpy(g), torch.from_numpy(mu))
+    f_exact, r_exact = P.tikhonov_solve(op, L, torch.from_numpy(g), torch.from_numpy(mu),
+                                        want_imag_residue=True)
+    assert r_fast is None and np.all(np_(r_exact) < 1e-9)
+    assert rel(np_(f_fast), np_(f_exact)) < 1e-13
+    for b in range(5):
+        assert rel(np_(f_fast[b]), O.tikhonov_solve(oop, s, g[b], mu[b])[0]) < 1e-10
