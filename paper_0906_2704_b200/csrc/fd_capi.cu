@@ -157,6 +157,8 @@ void init_runtime_once() {
     cudaFuncSetAttribute(k_analyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
     cudaFuncSetAttribute(k_synth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
     cudaFuncSetAttribute(k_bhat, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+    cudaFuncSetAttribute(k_ranalyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+    cudaFuncSetAttribute(k_rsynth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
     ok = true;
   });
   if (!ok) throw FdError(FD_ERR_OTHER, "no CUDA device available (fastdeblur_b200 has no CPU path)");
@@ -243,7 +245,9 @@ int ceil_pow2(long long v, int* logv) {
   return (int)p;
 }
 
-size_t smem_bytes(int M) { return (size_t)(pidx(M) + 1) * sizeof(double2) + 32 * 8 * 8 + 8 * 16; }
+size_t smem_bytes(int M) {
+  return (size_t)(pidx(M) + 1 + kTwSlots) * sizeof(double2) + 32 * 8 * 8 + 8 * 16;
+}
 int line_threads(int M) {
   int t = M / 16;
   if (t < 64) t = 64;
@@ -258,14 +262,31 @@ struct Axis {
 };
 
 void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
+  if (io.gi.count == 0) return;
+  if (!io.in_cplx && ax.rhalf) {  // one real line per CTA, half-length DFT
+    ProfScope ps("k_analyze", st);
+    k_ranalyze<<<io.gi.count, std::min(256, line_threads(ax.hfft.M)), smem_bytes(ax.hfft.M),
+                 st>>>(ax, io);
+    launched("k_ranalyze");
+    return;
+  }
+  if (!ax.fft.M) validation("complex lines of this order exceed the on-chip transform limit");
   const int blocks = io.in_cplx ? io.gi.count : (io.gi.count + 1) / 2;
-  if (blocks == 0) return;
   ProfScope ps("k_analyze", st);
   k_analyze<<<blocks, line_threads(ax.fft.M), smem_bytes(ax.fft.M), st>>>(ax, io);
   launched("k_analyze");
 }
 
 void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cudaStream_t st) {
+  if (io.gi.count == 0) return;
+  if (!io.out_cplx && ax.rhalf && (!ax.cplx || sa.resid2 == nullptr)) {
+    ProfScope ps(sa.mode == 1 ? "k_synth_filter" : "k_synth", st);
+    k_rsynth<<<io.gi.count, std::min(256, line_threads(ax.hfft.M)), smem_bytes(ax.hfft.M),
+               st>>>(ax, io, sa);
+    launched("k_rsynth");
+    return;
+  }
+  if (!ax.fft.M) validation("complex lines of this order exceed the on-chip transform limit");
   const bool hpack = ax.cplx && !io.out_cplx && sa.resid2 == nullptr;
   const int blocks = (ax.cplx && !hpack) ? io.gi.count : (io.gi.count + 1) / 2;
   if (blocks == 0) return;
@@ -304,6 +325,33 @@ void check_capacitance(const cplx m[4]) {  // boundary.cpp:139-150
     degenerate("degenerate transform: 2x2 capacitance matrix is singular or ill-conditioned");
 }
 
+constexpr int kMaxOnChipM = 8192;  // 139 KB of complex fp64 in shared memory
+
+FftTables make_fft_tables(int L, std::vector<std::unique_ptr<DevBuf>>& owner, int mdct,
+                          double2* dct_tw) {
+  FftTables T{};
+  int logM = 0;
+  const int M = ceil_pow2(std::max(2LL * L - 1, 2LL), &logM);
+  T.L = L;
+  T.M = M;
+  T.logM = logM;
+  double2* chirp = dev_alloc<double2>(owner, L);
+  double2* tw = dev_alloc<double2>(owner, std::max(M / 2, 1));
+  std::vector<std::unique_ptr<DevBuf>> tmp;
+  double2* b = dev_alloc<double2>(tmp, M);
+  double2* bhat = dev_alloc<double2>(owner, M);
+  T.chirp = chirp;
+  T.tw = tw;
+  T.bhat = bhat;
+  k_init_tables<<<std::max(1, std::min(1024, (M + 255) / 256)), 256>>>(L, M, chirp, tw, b, mdct,
+                                                                       dct_tw);
+  launched("k_init_tables");
+  k_bhat<<<1, line_threads(M), smem_bytes(M)>>>(T, b, bhat);
+  launched("k_bhat");
+  ck(cudaDeviceSynchronize(), "fft tables");
+  return T;
+}
+
 std::unique_ptr<Axis> build_axis(int bc, int n) {
   auto A = std::make_unique<Axis>();
   AxisDev& d = A->dev;
@@ -317,28 +365,30 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
   d.correction = d.bordered && bc != BC_ANTIREFLECTIVE;
   const int m = d.m;
   const int L = d.kind == IK_SINE ? 2 * (m + 1) : m;
-  int logM = 0;
-  const int M = ceil_pow2(2LL * L - 1, &logM);
-  if (M > 8192)
-    validation("order " + std::to_string(n) + " exceeds this build's on-chip transform limit "
-               "(interior DFT length <= 4096)");
-  d.fft.L = L;
-  d.fft.M = M;
-  d.fft.logM = logM;
-  double2* chirp = dev_alloc<double2>(A->bufs, L);
-  double2* tw = dev_alloc<double2>(A->bufs, std::max(M / 2, 1));
-  double2* b = dev_alloc<double2>(A->bufs, M);
-  double2* bhat = dev_alloc<double2>(A->bufs, M);
   double2* dct_tw = dev_alloc<double2>(A->bufs, d.kind == IK_COS ? m : 1);
-  d.fft.chirp = chirp;
-  d.fft.tw = tw;
-  d.fft.bhat = bhat;
   d.dct_tw = dct_tw;
-  k_init_tables<<<std::max(1, std::min(1024, (M + 255) / 256)), 256>>>(
-      L, M, chirp, tw, b, d.kind == IK_COS ? m : 0, dct_tw);
-  launched("k_init_tables");
-  k_bhat<<<1, line_threads(M), smem_bytes(M)>>>(d.fft, b, bhat);
-  launched("k_bhat");
+  // full-length tables (complex lines / line pairs); only built when they fit on chip
+  {
+    int logM = 0;
+    const int M = ceil_pow2(std::max(2LL * L - 1, 2LL), &logM);
+    if (M <= kMaxOnChipM) d.fft = make_fft_tables(L, A->bufs, d.kind == IK_COS ? m : 0, dct_tw);
+  }
+  // half-length real path (R even)
+  d.rhalf = (L % 2 == 0) && L >= 2;
+  if (d.rhalf) {
+    int logM = 0;
+    const int M = ceil_pow2(std::max((long long)L - 1, 2LL), &logM);
+    if (M > kMaxOnChipM) d.rhalf = 0;
+  }
+  if (d.rhalf) {
+    d.hfft = make_fft_tables(L / 2, A->bufs, d.fft.M ? 0 : (d.kind == IK_COS ? m : 0), dct_tw);
+    double2* rtw = dev_alloc<double2>(A->bufs, L / 2);
+    k_init_rtw<<<std::max(1, std::min(1024, (L / 2 + 255) / 256)), 256>>>(L, rtw);
+    launched("k_init_rtw");
+    d.rtw = rtw;
+  }
+  if (!d.fft.M && !d.rhalf)
+    validation("order " + std::to_string(n) + " exceeds this build's on-chip transform limit");
 
   if (!d.bordered) {
     ck(cudaDeviceSynchronize(), "axis tables");
@@ -543,6 +593,11 @@ struct fd_smoother {
   double* s1 = nullptr;   // 2D separable: per-axis laplacian pieces
   double* s2 = nullptr;
   double* r = nullptr;    // 1D GCV ratio |d|^2/s^2
+  // 1D complex bases: Hermitian pairing of the coefficients of real data
+  // (element e of the reduced set sums the pair pair[e]); r_red = r at pair.x
+  int2* pair = nullptr;
+  double* r_red = nullptr;
+  long long n_red = 0;
   int sep_sum = 0;        // separable: s = s1 + s2 (1) or 1 (0)
   int full = 0;           // 2D uses full arrays (Spectral mode 3)
   double2* dfull = nullptr;  // full d materialised for mode 3 on a separable op
@@ -722,10 +777,38 @@ GcvData gcv_data(const fd_op* op, const fd_smoother* L, const void* ghat, long l
   g.ghat = ghat;
   g.cplx = op->cplx;
   g.N = op->N();
+  g.stride = op->N();
   g.items = (int)count;
   g.r1d = op->dim == 1 ? L->r : nullptr;
   g.sp = spectral_of(op, L, false);
+  if (L->pair) {  // analyzed real data in a complex basis: Hermitian pairs
+    g.pair = L->pair;
+    g.r1d = L->r_red;
+    g.N = L->n_red;
+  }
   return g;
+}
+
+// Hermitian pairs of the coefficient vector of a real signal in a complex
+// basis (periodic: k <-> n-k; hoc-fourier: interior k <-> m-k, borders alone).
+void build_pairs(fd_smoother* L, const fd_op* op) {
+  const int n = op->n1;
+  std::vector<int2> pairs;
+  const int off = op->bc == BC_HOC_FOURIER ? 1 : 0;
+  const int R = op->bc == BC_HOC_FOURIER ? n - 2 : n;
+  if (off) pairs.push_back(make_int2(0, -1));
+  for (int k = 0; k <= R / 2; ++k) {
+    const int kc = (R - k) % R;
+    pairs.push_back(make_int2(off + k, kc == k ? -1 : off + kc));
+  }
+  if (off) pairs.push_back(make_int2(n - 1, -1));
+  std::vector<double> r(n);
+  ck(cudaMemcpy(r.data(), L->r, n * sizeof(double), cudaMemcpyDeviceToHost), "r");
+  std::vector<double> rr(pairs.size());
+  for (size_t i = 0; i < pairs.size(); ++i) rr[i] = r[pairs[i].x];
+  L->pair = dev_upload(L->bufs, pairs);
+  L->r_red = dev_upload(L->bufs, rr);
+  L->n_red = (long long)pairs.size();
 }
 
 int pick_chunks(long long N, long long items, int sg) {
@@ -766,7 +849,9 @@ void launch_grid(const GcvData& g, const GcvGrid& grid, int sg, long long chunk,
 #undef FD_GRID
 }
 
-size_t gemm_smem(int nj) { return (size_t)(64 * 32 + 32 * 32 * nj + 32 + 256) * sizeof(double); }
+size_t gemm_smem(int nj) {
+  return (size_t)(64 * 32 + 32 * 32 * nj + 32 + 32 + 256) * sizeof(double);
+}
 
 template <int NJ>
 void launch_gemm_t(const GcvData& g, const GcvGrid& grid, long long echunk, int nch,
@@ -1222,6 +1307,7 @@ int fd_smoother_create(const fd_op* op, int kind, fd_smoother** out) {
       L->r = dev_alloc<double>(L->bufs, n);
       k_gcv_ratio<<<std::max(1, (n + 255) / 256), 256>>>(op->d, L->s, n, L->r);
       launched("k_gcv_ratio");
+      if (op->cplx) build_pairs(L.get(), op);
     } else {
       if (kind == SM_FIRST_DIFFERENCE)
         validation("the first-difference smoother is defined for 1D operators only");
@@ -1289,6 +1375,15 @@ int fd_smoother_create_custom(const fd_op* op, const double* s, fd_smoother** ou
       L->r = dev_alloc<double>(L->bufs, N);
       k_gcv_ratio<<<std::max(1, (int)((N + 255) / 256)), 256>>>(op->d, L->s, (int)N, L->r);
       launched("k_gcv_ratio");
+      ck(cudaDeviceSynchronize(), "ratio");
+      if (op->cplx) {
+        // pairing needs a symmetric custom smoother (s_e = s_{R-e}); check it
+        const int n = op->n1, off = op->bc == BC_HOC_FOURIER ? 1 : 0;
+        const int R = op->bc == BC_HOC_FOURIER ? n - 2 : n;
+        bool sym = true;
+        for (int k = 1; k < R && sym; ++k) sym = h[off + k] == h[off + R - k];
+        if (sym) build_pairs(L.get(), op);
+      }
     } else {
       L->full = 1;
       if (op->sep) {

@@ -5,8 +5,8 @@
 //   DIF (natural -> digit-reversed)  then  DIT (digit-reversed -> natural).
 // Each pass fuses up to four radix-2 stages in registers (radix-16 butterflies,
 // 16 complex values per thread item), so an M = 8192 transform touches shared
-// memory 4 times instead of 13.  Twiddles come from a global table
-// e^{-2 pi i j/M} (L1-resident) plus compile-time radix-16 constants.
+// memory 4 times instead of 13.  Twiddles come from two small shared-memory
+// tables (TwSm) plus compile-time radix-16 constants.
 //
 // Arbitrary lengths L (the interior lengths n-2 = 2*7*73, 2*23*89, 2*8191 of
 // the BASELINE sizes are never powers of two) use Bluestein:
@@ -64,12 +64,37 @@ __device__ __forceinline__ double2 mul_w16c(double2 d, int k) {
   return cconj(mul_w16(cconj(d), k));
 }
 
+// Twiddles e^{-2 pi i j/M} from two small shared-memory tables,
+// W^j = hi[j >> lob] * lo[j & (2^lob - 1)]: exact table entries, one complex
+// multiply (<= 2 ulp), and no L2 round trip inside the barrier-separated passes.
+struct TwSm {
+  const double2* lo;
+  const double2* hi;
+  int lob;
+  __device__ __forceinline__ double2 operator()(int j) const {
+    return cmul(hi[j >> lob], lo[j & ((1 << lob) - 1)]);
+  }
+};
+
+constexpr int kTwSlots = 256;  // lo + hi entries (M <= 2^16)
+
+// fill the two tables from the global table of M/2 entries; returns the view
+__device__ __forceinline__ TwSm load_twiddles(double2* slots, const FftTables& T) {
+  const int b = T.logM > 1 ? T.logM - 1 : 0;
+  const int lob = (b + 1) / 2;
+  const int nlo = 1 << lob, nhi = 1 << (b - lob);
+  double2* lo = slots;
+  double2* hi = slots + nlo;
+  for (int i = threadIdx.x; i < nlo; i += blockDim.x) lo[i] = T.tw[i];
+  for (int i = threadIdx.x; i < nhi; i += blockDim.x) hi[i] = T.tw[(long long)i << lob];
+  return TwSm{lo, hi, lob};
+}
+
 // One fused pass of LOGR radix-2 decimation-in-frequency stages on blocks of
 // size S (S >= 2^LOGR).  Items are disjoint element sets, so the pass is
 // in-place with no barrier inside.
 template <int LOGR>
-__device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S,
-                                         const double2* __restrict__ tw) {
+__device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S, const TwSm& tw) {
   constexpr int R = 1 << LOGR;
   const int SR = S >> LOGR;
   const int items = M >> LOGR;
@@ -83,7 +108,7 @@ __device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S,
 #pragma unroll
     for (int st = 0; st < LOGR; ++st) {
       const int half = R >> (st + 1);
-      const double2 w = __ldg(&tw[(j0 * twstep) << st]);
+      const double2 w = tw((j0 * twstep) << st);
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         if (q & half) continue;
@@ -102,8 +127,7 @@ __device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S,
 // Exact inverse (times 2 per stage) of dif_pass with conjugate twiddles: the
 // mirrored DIT pass of the backward transform.
 template <int LOGR>
-__device__ __forceinline__ void dit_pass(double2* __restrict__ x, int M, int S,
-                                         const double2* __restrict__ tw) {
+__device__ __forceinline__ void dit_pass(double2* __restrict__ x, int M, int S, const TwSm& tw) {
   constexpr int R = 1 << LOGR;
   const int SR = S >> LOGR;
   const int items = M >> LOGR;
@@ -117,7 +141,7 @@ __device__ __forceinline__ void dit_pass(double2* __restrict__ x, int M, int S,
 #pragma unroll
     for (int st = LOGR - 1; st >= 0; --st) {
       const int half = R >> (st + 1);
-      const double2 w = __ldg(&tw[(j0 * twstep) << st]);
+      const double2 w = tw((j0 * twstep) << st);
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         if (q & half) continue;
@@ -137,7 +161,7 @@ __device__ __forceinline__ int pass_logr(int rem) { return rem >= 4 ? 4 : rem; }
 
 // Forward DIF FFT (sign -1), natural order in, digit-reversed order out.
 // Caller must __syncthreads() before; returns after a barrier.
-__device__ __forceinline__ void fft_dif(double2* x, int M, int logM, const double2* tw) {
+__device__ __forceinline__ void fft_dif(double2* x, int M, int logM, const TwSm& tw) {
   int S = M;
   int rem = logM;
   while (rem > 0) {
@@ -155,7 +179,7 @@ __device__ __forceinline__ void fft_dif(double2* x, int M, int logM, const doubl
 }
 
 // Backward DIT FFT (sign +1, unnormalised), digit-reversed in, natural out.
-__device__ __forceinline__ void fft_dit(double2* x, int M, int logM, const double2* tw) {
+__device__ __forceinline__ void fft_dit(double2* x, int M, int logM, const TwSm& tw) {
   int ls[8];
   int np = 0;
   for (int rem = logM; rem > 0;) {
@@ -181,12 +205,12 @@ __device__ __forceinline__ void fft_dit(double2* x, int M, int logM, const doubl
 // Bluestein core: x holds a_j = z_j c_j (j < L) and zeros up to M; on return
 // x_k holds the circular convolution (a * b)_k; the caller multiplies by c_k.
 // Requires a barrier before the call (the caller's loads); ends with one.
-__device__ __forceinline__ void bluestein_core(double2* x, const FftTables& T) {
-  fft_dif(x, T.M, T.logM, T.tw);
+__device__ __forceinline__ void bluestein_core(double2* x, const FftTables& T, const TwSm& tw) {
+  fft_dif(x, T.M, T.logM, tw);
   for (int j = threadIdx.x; j < T.M; j += blockDim.x)
     x[pidx(j)] = cmul(x[pidx(j)], __ldg(&T.bhat[j]));
   __syncthreads();
-  fft_dit(x, T.M, T.logM, T.tw);
+  fft_dit(x, T.M, T.logM, tw);
 }
 
 // ----------------------------------------------------------------------------

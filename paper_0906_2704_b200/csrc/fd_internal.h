@@ -33,7 +33,13 @@ struct AxisDev {
   int bordered;    // antireflective / hoc-cosine / hoc-fourier
   int correction;  // rank-2 SMW correction (false for antireflective)
   int cplx;        // complex basis (periodic, hoc-fourier)
-  FftTables fft;
+  FftTables fft;          // full-length interior DFT (complex lines, line pairs)
+  // Half-length real path: a real line of even length R (R = m, or 2(m+1) for
+  // the DST-I odd extension) as a complex DFT of length R/2 (fd_kernels.cuh,
+  // k_ranalyze / k_rsynth); rhalf = 0 when R is odd.
+  int rhalf;
+  FftTables hfft;         // DFT of length R/2
+  const double2* rtw;     // R/2 entries e^{-2 pi i k/R}
   const double2* dct_tw;  // m entries e^{-i pi k/(2m)} (IK_COS)
   const double* q;        // n, boundary column (unit norm, q[n-1] = 0)
   double alpha;           // 1/q[0]

@@ -110,12 +110,23 @@ __global__ void k_init_tables(int L, int M, double2* chirp, double2* tw, double2
   }
 }
 
+// real-FFT twiddles e^{-2 pi i k/R}, k < R/2
+__global__ void k_init_rtw(int R, double2* rtw) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < R / 2; k += gridDim.x * blockDim.x) {
+    double s, c;
+    sincospi(-2.0 * (double)k / (double)R, &s, &c);
+    rtw[k] = make_double2(c, s);
+  }
+}
+
 // bhat = DIF_M(b)/M, left in DIF (digit-reversed) order
-__global__ void k_bhat(FftTables T, const double2* __restrict__ b, double2* bhat) {
+__global__ void __launch_bounds__(512) k_bhat(FftTables T, const double2* __restrict__ b,
+                                              double2* bhat) {
   extern __shared__ double2 sm[];
+  const TwSm tw = load_twiddles(sm + pidx(T.M) + 1, T);
   for (int j = threadIdx.x; j < T.M; j += blockDim.x) sm[pidx(j)] = b[j];
   __syncthreads();
-  fft_dif(sm, T.M, T.logM, T.tw);
+  fft_dif(sm, T.M, T.logM, tw);
   const double inv = 1.0 / (double)T.M;
   for (int j = threadIdx.x; j < T.M; j += blockDim.x) bhat[j] = cscale(sm[pidx(j)], inv);
 }
@@ -298,7 +309,8 @@ __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
   extern __shared__ double2 sm[];
   const int M = ax.fft.M;
   double2* x = sm;
-  double* red = reinterpret_cast<double*>(sm + pidx(M) + 1);
+  const TwSm tw = load_twiddles(sm + pidx(M) + 1, ax.fft);
+  double* red = reinterpret_cast<double*>(sm + pidx(M) + 1 + kTwSlots);
   double2* bc = reinterpret_cast<double2*>(red + 32 * 8);
 
   const bool pair = !io.in_cplx;
@@ -420,7 +432,7 @@ __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
   }
   __syncthreads();
 
-  bluestein_core(x, ax.fft);
+  bluestein_core(x, ax.fft, tw);
 
   const double2 b00 = bc[0], b10 = bc[1], b01 = bc[2], b11 = bc[3];
   const long long oo0 = line_offset(io.go, l0);
@@ -536,7 +548,8 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
   extern __shared__ double2 sm[];
   const int M = ax.fft.M;
   double2* x = sm;
-  double* red = reinterpret_cast<double*>(sm + pidx(M) + 1);
+  const TwSm tw = load_twiddles(sm + pidx(M) + 1, ax.fft);
+  double* red = reinterpret_cast<double*>(sm + pidx(M) + 1 + kTwSlots);
 
   // Real bases: real coefficients, two lines per FFT.  Complex bases with a
   // real output and no residue request: the real part of T_X c only depends
@@ -648,7 +661,7 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
   if (dots) block_sum<8>(acc, red);
   __syncthreads();
 
-  bluestein_core(x, ax.fft);
+  bluestein_core(x, ax.fft, tw);
 
   const long long oo0 = line_offset(io.go, l0);
   const long long oo1 = has1 ? line_offset(io.go, l0 + 1) : oo0;
@@ -717,6 +730,290 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
 }
 
 // ---------------------------------------------------------------------------
+// Real lines through the half-length complex DFT (one line per CTA).
+//   R2C (analyze):  X = DFT_R(x), x real, R even, h = R/2:
+//     z_j = x_{2j} + i x_{2j+1},  Z = DFT_h(z),
+//     E_k = (Z_k + conj Z_{-k})/2,  O_k = -i (Z_k - conj Z_{-k})/2,
+//     X_k = E_k + W_R^k O_k,  X_{k+h} = E_k - W_R^k O_k.
+//   C2R (synthesize):  x_j = sum_q X_q e^{+2 pi i jq/R} for Hermitian X:
+//     Zin_k = (X_k + X_{k+h}) + i (X_k - X_{k+h}) W_R^{-k},  z = IDFT_h(Zin),
+//     x_{2j} = Re z_j,  x_{2j+1} = Im z_j.
+// A real line of even length is exactly the interleaved complex buffer z, so
+// the Bluestein size drops from M >= 2R-1 to M >= R-1 (4096 at n = 4096): a
+// 70 KB buffer, several CTAs per SM.  The interior kinds map on this as
+//   cosine (DCT-II / III, trig.cpp:180-214): Makhoul reorder + quarter-wave twiddle,
+//     DCT-III via Re DFT(buf) = C2R(herm(conj buf));
+//   Fourier (F / F^H, real data): R2C / C2R of length m (Re F^H c = F^H herm(c));
+//   sine (DST-I, trig.cpp:216-234): R2C of the odd extension, R = 2(m+1).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int makhoul_src(int p, int m, int half) {
+  return p < half ? 2 * p : 2 * (m - 1 - p) + 1;  // trig.cpp:194-195
+}
+
+__global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io) {
+  extern __shared__ double2 sm[];
+  const FftTables& T = ax.hfft;
+  const int M = T.M, h = T.L;
+  double2* x = sm;
+  const TwSm tw = load_twiddles(sm + pidx(M) + 1, T);
+  double* red = reinterpret_cast<double*>(sm + pidx(M) + 1 + kTwSlots);
+  double2* bcs = reinterpret_cast<double2*>(red + 32 * 4);
+  const int l = blockIdx.x;
+  if (l >= io.gi.count) return;
+  const long long oi = line_offset(io.gi, l), es = io.gi.elem_stride;
+  const int n = ax.n, m = ax.m;
+  const double2* chirp = T.chirp;
+  const double* in = reinterpret_cast<const double*>(io.in);
+  auto ld = [&](int e) { return __ldg(in + oi + e * es); };
+  double y0 = 0.0, yn = 0.0;
+  if (ax.bordered) {
+    y0 = ld(0);
+    yn = ld(n - 1);
+  }
+  const bool dots = ax.bordered && ax.correction;
+  const int half = (m + 1) / 2;
+  double acc[4] = {0, 0, 0, 0};  // ra (re, im), rb (re, im)
+  for (int j = threadIdx.x; j < M; j += blockDim.x) {
+    double2 val = czero();
+    if (j < h) {
+      const int p0 = 2 * j, p1 = 2 * j + 1;
+      double a, b;
+      if (ax.kind == IK_SINE) {
+        const int R = 2 * (m + 1);
+        auto ext = [&](int p) -> double {
+          if (p == 0 || p == m + 1) return 0.0;
+          if (p <= m) return ld(interior_elem(ax, p - 1));
+          return -ld(interior_elem(ax, R - 1 - p));
+        };
+        a = ext(p0);
+        b = ext(p1);
+      } else {
+        const int s0 = ax.kind == IK_COS ? makhoul_src(p0, m, half) : p0;
+        const int s1 = ax.kind == IK_COS ? makhoul_src(p1, m, half) : p1;
+        a = ld(interior_elem(ax, s0));
+        b = ld(interior_elem(ax, s1));
+        if (dots) {
+          const double2 ra0 = __ldg(&ax.row_a[s0]), ra1 = __ldg(&ax.row_a[s1]);
+          const double2 rb0 = __ldg(&ax.row_b[s0]), rb1 = __ldg(&ax.row_b[s1]);
+          acc[0] += ra0.x * a + ra1.x * b;
+          acc[1] += ra0.y * a + ra1.y * b;
+          acc[2] += rb0.x * a + rb1.x * b;
+          acc[3] += rb0.y * a + rb1.y * b;
+        }
+      }
+      val = cmul(make_double2(a, b), __ldg(&chirp[j]));
+    }
+    x[pidx(j)] = val;
+  }
+  if (dots) block_sum<4>(acc, red);
+  if (threadIdx.x == 0) {
+    double2 b0 = czero(), b1 = czero();
+    if (dots) {  // boundary.cpp:357-368
+      const double2* c = ax.cap;
+      const double2 ra = cadd(cadd(cscale(ax.cav[0], y0), cscale(ax.cav[1], yn)),
+                              make_double2(acc[0], acc[1]));
+      const double2 rb = cadd(cadd(cscale(ax.cav[2], y0), cscale(ax.cav[3], yn)),
+                              make_double2(acc[2], acc[3]));
+      const double2 n0 = csub(cmul(ra, c[3]), cmul(rb, c[1]));
+      const double2 n1 = csub(cmul(rb, c[0]), cmul(ra, c[2]));
+      if (ax.cplx) {
+        const double2 det = csub(cmul(c[0], c[3]), cmul(c[1], c[2]));
+        const double dd = det.x * det.x + det.y * det.y;
+        b0 = make_double2((n0.x * det.x + n0.y * det.y) / dd, (n0.y * det.x - n0.x * det.y) / dd);
+        b1 = make_double2((n1.x * det.x + n1.y * det.y) / dd, (n1.y * det.x - n1.x * det.y) / dd);
+      } else {
+        const double det = c[0].x * c[3].x - c[1].x * c[2].x;
+        b0 = make_double2(n0.x / det, 0.0);
+        b1 = make_double2(n1.x / det, 0.0);
+      }
+    }
+    bcs[0] = b0;
+    bcs[1] = b1;
+  }
+  __syncthreads();
+
+  bluestein_core(x, T, tw);
+
+  const double2 b0 = bcs[0], b1 = bcs[1];
+  const long long oo = line_offset(io.go, l), eso = io.go.elem_stride;
+  const double inv_sqrt_m = 1.0 / sqrt((double)m);
+  const double s0 = sqrt(1.0 / (double)m), s1 = sqrt(2.0 / (double)m);
+  auto emit = [&](int i, double2 xi) {
+    const int e = interior_elem(ax, i);
+    if (!ax.bordered) {
+      stc(io.out, io.out_cplx, oo + e * eso, xi);
+      return;
+    }
+    const double2 v = __ldg(&ax.v[i]), w = __ldg(&ax.w[i]);
+    if (ax.cplx) {
+      double2 o = cadd(cadd(cscale(v, y0), xi), cscale(w, yn));
+      if (dots) o = csub(o, cadd(cmul(b0, v), cmul(b1, w)));
+      stc(io.out, io.out_cplx, oo + e * eso, o);
+    } else {
+      double o = y0 * v.x + xi.x + yn * w.x;
+      if (dots) o -= b0.x * v.x + b1.x * w.x;
+      stc(io.out, io.out_cplx, oo + e * eso, make_double2(o, 0.0));
+    }
+  };
+  for (int k = threadIdx.x; k < h; k += blockDim.x) {
+    const int kc = k == 0 ? 0 : h - k;
+    const double2 Zk = cmul(x[pidx(k)], __ldg(&chirp[k]));
+    const double2 Zc = cconj(cmul(x[pidx(kc)], __ldg(&chirp[kc])));
+    const double2 E = cscale(cadd(Zk, Zc), 0.5);
+    const double2 D = csub(Zk, Zc);
+    const double2 WO = cmul(__ldg(&ax.rtw[k]), make_double2(0.5 * D.y, -0.5 * D.x));
+    const double2 X0 = cadd(E, WO), X1 = csub(E, WO);  // X_k, X_{k+h}
+    if (ax.kind == IK_SINE) {
+      if (k >= 1) emit(k - 1, make_double2(-0.5 * sqrt(2.0 / ((double)m + 1.0)) * X0.y, 0.0));
+    } else if (ax.kind == IK_COS) {
+      const double2 t0 = __ldg(&ax.dct_tw[k]), t1 = __ldg(&ax.dct_tw[k + h]);
+      emit(k, make_double2((k == 0 ? s0 : s1) * (t0.x * X0.x - t0.y * X0.y), 0.0));
+      emit(k + h, make_double2(s1 * (t1.x * X1.x - t1.y * X1.y), 0.0));
+    } else {
+      emit(k, cscale(X0, inv_sqrt_m));
+      emit(k + h, cscale(X1, inv_sqrt_m));
+    }
+  }
+  if (ax.bordered && threadIdx.x == 0) {
+    const double al = ax.alpha;
+    double2 o0 = make_double2(al * y0, 0.0), on = make_double2(al * yn, 0.0);
+    if (dots) {
+      o0 = csub(o0, cscale(b0, al));
+      on = csub(on, cscale(b1, al));
+    }
+    stc(io.out, io.out_cplx, oo, o0);
+    stc(io.out, io.out_cplx, oo + (long long)(n - 1) * eso, on);
+  }
+}
+
+__global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthArgs sa) {
+  extern __shared__ double2 sm[];
+  const FftTables& T = ax.hfft;
+  const int M = T.M, h = T.L;
+  double2* x = sm;
+  const TwSm tw = load_twiddles(sm + pidx(M) + 1, T);
+  double* red = reinterpret_cast<double*>(sm + pidx(M) + 1 + kTwSlots);
+  const int l = blockIdx.x;
+  if (l >= io.gi.count) return;
+  const long long oi = line_offset(io.gi, l);
+  const int n = ax.n, m = ax.m;
+  const double2* chirp = T.chirp;
+  auto cf = [&](int e) { return coeff_at(ax, io, sa, l, oi, e); };
+  double2 u0 = czero(), un = czero();
+  if (ax.bordered) {
+    u0 = cf(0);
+    un = cf(n - 1);
+  }
+  const bool dots = ax.bordered && ax.correction;
+  double acc[4] = {0, 0, 0, 0};  // top (re, im), bottom (re, im)
+  if (ax.kind == IK_SINE) {  // Q c_mid: R2C of the odd extension (Q is an involution)
+    const int R = 2 * (m + 1);
+    for (int j = threadIdx.x; j < M; j += blockDim.x) {
+      double2 val = czero();
+      if (j < h) {
+        auto ext = [&](int p) -> double {
+          if (p == 0 || p == m + 1) return 0.0;
+          if (p <= m) return cf(interior_elem(ax, p - 1)).x;
+          return -cf(interior_elem(ax, R - 1 - p)).x;
+        };
+        val = cmul(make_double2(ext(2 * j), ext(2 * j + 1)), __ldg(&chirp[j]));
+      }
+      x[pidx(j)] = val;
+    }
+    __syncthreads();
+  } else {
+    // stage the (filtered) coefficients: cosine stores conj(buf_i) = s_i c_i conj(tw_i)
+    const double s0 = sqrt(1.0 / (double)m), s1 = sqrt(2.0 / (double)m);
+    for (int i = threadIdx.x; i < m; i += blockDim.x) {
+      const double2 c = cf(interior_elem(ax, i));
+      double2 val;
+      if (ax.kind == IK_COS) {
+        const double2 t = __ldg(&ax.dct_tw[i]);
+        const double ts = (i == 0 ? s0 : s1) * c.x;
+        val = make_double2(ts * t.x, -(ts * t.y));
+        if (dots) {
+          acc[0] += __ldg(&ax.c_a[i]).x * c.x;
+          acc[2] += __ldg(&ax.c_b[i]).x * c.x;
+        }
+      } else {
+        val = c;
+        if (dots) {
+          const double2 t0 = cmul(__ldg(&ax.c_a[i]), c), t1 = cmul(__ldg(&ax.c_b[i]), c);
+          acc[0] += t0.x, acc[1] += t0.y, acc[2] += t1.x, acc[3] += t1.y;
+        }
+      }
+      x[pidx(i)] = val;
+    }
+    __syncthreads();
+    // C2R pre-pass over the closed index groups {k, h-k}: X = herm(staged),
+    // Zin_k = (X_k + X_{k+h}) + i (X_k - X_{k+h}) W^{-k}; Bluestein input conj(Zin) c_k
+    auto herm = [&](int q) {
+      const int qc = q == 0 ? 0 : m - q;
+      return cscale(cadd(x[pidx(q)], cconj(x[pidx(qc)])), 0.5);
+    };
+    auto zin = [&](int k) {
+      const double2 Xa = herm(k), Xb = herm(k + h);
+      const double2 Od = cmulc(csub(Xa, Xb), __ldg(&ax.rtw[k]));
+      const double2 Ev = cadd(Xa, Xb);
+      return make_double2(Ev.x - Od.y, Ev.y + Od.x);
+    };
+    for (int k = threadIdx.x; k <= h / 2; k += blockDim.x) {
+      const int kp = k == 0 ? 0 : h - k;
+      const double2 za = zin(k);
+      const double2 zb = zin(kp);
+      x[pidx(k)] = cmul(cconj(za), __ldg(&chirp[k]));
+      if (kp != k) x[pidx(kp)] = cmul(cconj(zb), __ldg(&chirp[kp]));
+    }
+    __syncthreads();
+    for (int j = h + threadIdx.x; j < M; j += blockDim.x) x[pidx(j)] = czero();
+    __syncthreads();
+  }
+  if (dots) block_sum<4>(acc, red);
+
+  bluestein_core(x, T, tw);
+
+  const long long oo = line_offset(io.go, l), eso = io.go.elem_stride;
+  auto put = [&](int p, double val) {  // interior position p of the output line
+    const int e = interior_elem(ax, p);
+    double o = val;
+    if (ax.bordered) o = __ldg(&ax.q[e]) * u0.x + val + __ldg(&ax.q[n - 1 - e]) * un.x;
+    stc(io.out, 0, oo + e * eso, make_double2(o, 0.0));
+  };
+  if (ax.kind == IK_SINE) {
+    const double sc = -0.5 * sqrt(2.0 / ((double)m + 1.0));
+    for (int k = 1 + threadIdx.x; k < h; k += blockDim.x) {
+      const int kc = h - k;
+      const double2 Zk = cmul(x[pidx(k)], __ldg(&chirp[k]));
+      const double2 Zc = cconj(cmul(x[pidx(kc)], __ldg(&chirp[kc])));
+      const double2 E = cscale(cadd(Zk, Zc), 0.5);
+      const double2 D = csub(Zk, Zc);
+      const double2 WO = cmul(__ldg(&ax.rtw[k]), make_double2(0.5 * D.y, -0.5 * D.x));
+      put(k - 1, sc * (E.y + WO.y));
+    }
+  } else {
+    const double inv_sqrt_m = 1.0 / sqrt((double)m);
+    const int half = (m + 1) / 2;
+    for (int j = threadIdx.x; j < h; j += blockDim.x) {
+      const double2 z = cconj(cmul(x[pidx(j)], __ldg(&chirp[j])));
+      if (ax.kind == IK_COS) {  // spec[p] -> out[2p] (p < half) or out[2(m-1-p)+1]
+        const int p0 = 2 * j, p1 = 2 * j + 1;
+        put(p0 < half ? 2 * p0 : 2 * (m - 1 - p0) + 1, z.x);
+        put(p1 < half ? 2 * p1 : 2 * (m - 1 - p1) + 1, z.y);
+      } else {
+        put(2 * j, z.x * inv_sqrt_m);
+        put(2 * j + 1, z.y * inv_sqrt_m);
+      }
+    }
+  }
+  if (ax.bordered && threadIdx.x == 0) {
+    const double q0 = ax.q[0];
+    const double2 top = make_double2(acc[0], acc[1]), bot = make_double2(acc[2], acc[3]);
+    stc(io.out, 0, oo, make_double2(q0 * u0.x + top.x, 0.0));
+    stc(io.out, 0, oo + (long long)(n - 1) * eso, make_double2(bot.x + q0 * un.x, 0.0));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // GCV grid: for every item and grid value mu_k,
 //   num_k = sum_e sigma_e^2 |ghat_e|^2,  den_k = sum_e sigma_e,
 //   sigma_e = 1/(r_e + mu_k)   (r_e = |d_e|^2/s_e^2; s_e = 0 contributes 0)
@@ -727,11 +1024,13 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
 // partial[item][chunk][2][K] and are reduced in a fixed order afterwards.
 // ---------------------------------------------------------------------------
 struct GcvData {
-  const void* ghat;      // item-major, N coefficients per item
+  const void* ghat;      // item-major coefficients, `stride` per item
   int cplx;
-  long long N;           // coefficients per item
+  long long N;           // GCV elements per item
+  long long stride;      // coefficients per item in ghat
   int items;
   const double* r1d;     // 1D ratio vector (length N), or null for 2D
+  const int2* pair;      // optional: element e sums |ghat|^2 at pair[e].x and pair[e].y (>= 0)
   Spectral sp;           // 2D: mode 2 (separable) or 3 (full); sp.n2 = row length
 };
 
@@ -751,14 +1050,31 @@ __device__ __forceinline__ double gcv_ratio(const GcvData& g, long long e) {
   return (d.x * d.x + d.y * d.y) / (s * s);
 }
 
-__device__ __forceinline__ double gcv_w(const GcvData& g, int item, long long e) {
-  const long long idx = (long long)item * g.N + e;
+__device__ __forceinline__ double gcv_w1(const GcvData& g, long long idx) {
   if (g.cplx) {
     const double2 c = __ldg(reinterpret_cast<const double2*>(g.ghat) + idx);
     return c.x * c.x + c.y * c.y;
   }
   const double c = __ldg(reinterpret_cast<const double*>(g.ghat) + idx);
   return c * c;
+}
+
+// |ghat_e|^2, or the sum over a Hermitian pair (e, R-e) of a real signal's
+// coefficients in a complex basis: both share r_e (d_{R-e} = conj d_e,
+// s_{R-e} = s_e), so sigma^2 w summed over the pair is one term.
+// multiplicity of element e in sum_e sigma_e (2 for a Hermitian pair)
+__device__ __forceinline__ double gcv_mult(const GcvData& g, long long e) {
+  return (g.pair && __ldg(&g.pair[e]).y >= 0) ? 2.0 : 1.0;
+}
+
+__device__ __forceinline__ double gcv_w(const GcvData& g, int item, long long e) {
+  const long long base = (long long)item * g.stride;
+  if (g.pair) {
+    const int2 p = __ldg(&g.pair[e]);
+    const double w = gcv_w1(g, base + p.x);
+    return p.y >= 0 ? w + gcv_w1(g, base + p.y) : w;
+  }
+  return gcv_w1(g, base + e);
 }
 
 template <int KC, int SG>
@@ -787,6 +1103,7 @@ __global__ void __launch_bounds__(256) k_gcv_grid(GcvData g, GcvGrid grid, long 
   for (long long e = e0; e < e1; ++e) {
     const double r = gcv_ratio(g, e);
     if (isinf(r)) continue;
+    const double mult = gcv_mult(g, e);
     double w[SG];
 #pragma unroll
     for (int p = 0; p < SG; ++p) {
@@ -814,7 +1131,7 @@ __global__ void __launch_bounds__(256) k_gcv_grid(GcvData g, GcvGrid grid, long 
     }
 #pragma unroll
     for (int k = 0; k < KC; ++k) {
-      den[k] += sig[k];
+      den[k] = fma(mult, sig[k], den[k]);
       const double s2 = sig[k] * sig[k];
 #pragma unroll
       for (int p = 0; p < SG; ++p) num[p][k] = fma(s2, w[p], num[p][k]);
@@ -853,7 +1170,8 @@ __global__ void __launch_bounds__(256) k_gcv_gemm(GcvData g, GcvGrid grid, int k
   double* Wt = gsm;              // [BS][E]
   double* Sg = gsm + BS * E;     // [E][BK]
   double* Rt = Sg + E * BK;      // [E]
-  double* Dn = Rt + E;           // [256] den partials
+  double* Mt = Rt + E;           // [E] multiplicities
+  double* Dn = Mt + E;           // [256] den partials
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   const int item0 = blockIdx.x * BS;
   const int er = blockIdx.y;
@@ -868,16 +1186,34 @@ __global__ void __launch_bounds__(256) k_gcv_gemm(GcvData g, GcvGrid grid, int k
 #pragma unroll
     for (int j = 0; j < NJ; ++j) acc[s][j] = 0.0;
   double den = 0.0;
-  for (long long e0 = eb; e0 < ee; e0 += E) {
+  // software pipeline: the next tile's global loads are in flight while this
+  // tile's sigma^2 generation and micro-GEMM run
+  constexpr int NQ = BS * E / 256;
+  double wreg[NQ];
+  double rreg = INFINITY, mreg = 1.0;
+  auto fetch = [&](long long e0) {
 #pragma unroll
-    for (int q = 0; q < BS * E / 256; ++q) {
+    for (int q = 0; q < NQ; ++q) {
       const int idx = tid + 256 * q;
       const int sidx = idx >> 5, e = idx & 31;
       const int item = item0 + sidx;
-      Wt[idx] = (item < g.items && e0 + e < ee) ? gcv_w(g, item, e0 + e) : 0.0;
+      wreg[q] = (item < g.items && e0 + e < ee) ? gcv_w(g, item, e0 + e) : 0.0;
     }
-    if (tid < E) Rt[tid] = (e0 + tid < ee) ? gcv_ratio(g, e0 + tid) : INFINITY;
+    if (tid < E) {
+      rreg = (e0 + tid < ee) ? gcv_ratio(g, e0 + tid) : INFINITY;
+      mreg = (e0 + tid < ee) ? gcv_mult(g, e0 + tid) : 1.0;
+    }
+  };
+  if (eb < ee) fetch(eb);
+  for (long long e0 = eb; e0 < ee; e0 += E) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) Wt[tid + 256 * q] = wreg[q];
+    if (tid < E) {
+      Rt[tid] = rreg;
+      Mt[tid] = mreg;
+    }
     __syncthreads();
+    if (e0 + E < ee) fetch(e0 + E);
     // sigma^2 for (element e, grid value kk); GP threads share one grid value
     constexpr int EPT = E / GP;
 #pragma unroll
@@ -907,7 +1243,7 @@ __global__ void __launch_bounds__(256) k_gcv_gemm(GcvData g, GcvGrid grid, int k
           const double r = Rt[eb4 + t];
           sg[t] = isinf(r) ? 0.0 : 1.0 / (r + mu);
         }
-        den += sg[t];
+        den = fma(Mt[eb4 + t], sg[t], den);
         Sg[(eb4 + t) * BK + kk] = sg[t] * sg[t];
       }
     }
@@ -1016,11 +1352,12 @@ __global__ void __launch_bounds__(256) k_gcv_moments(GcvData g, const double* __
     const double r = gcv_ratio(g, e);
     if (isinf(r)) continue;
     const double w = gcv_w(g, item, e);
+    const double mult = gcv_mult(g, e);
     const double t = 1.0 / (r + mc);
     double p = t;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-      B[j] += p;
+      B[j] = fma(mult, p, B[j]);
       A[j] = fma(w * p, t, A[j]);
       p *= t;
     }
@@ -1096,7 +1433,7 @@ __global__ void __launch_bounds__(256) k_gcv_direct(GcvData g, const double* __r
     const double r = gcv_ratio(g, e);
     if (isinf(r)) continue;
     const double sig = 1.0 / (r + mu);
-    den += sig;
+    den = fma(gcv_mult(g, e), sig, den);
     num = fma(sig * sig, gcv_w(g, item, e), num);
   }
 #pragma unroll

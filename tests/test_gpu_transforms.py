@@ -22,7 +22,7 @@ SIZES = [5, 6, 7, 8, 33, 64, 101, 128, 1024, 2049, 4096]
 
 
 def _max_n(bc):
-    return 2049 if bc == O.ANTIREFLECTIVE else 4098
+    return 4098
 
 
 @pytest.mark.parametrize("bc", range(5))
