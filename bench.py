@@ -258,10 +258,7 @@ def main():
         for i in range(batch):
             g_host[i] = torch.from_numpy(W.image_2d(cfg, first + i)[1])
         op = P.build_operator_2d_separable(cfg.psf, cfg.psf, cfg.n1, cfg.n2, cfg.bc)
-    if smoother == 2:
-        L = P.smoother_from_eigenvalues(op, first_difference_s(cfg.bc, cfg.n1))
-    else:
-        L = P.smoothing_eigenvalues(SMOOTHER_NAMES[smoother], op)
+    L = P.smoothing_eigenvalues(SMOOTHER_NAMES[smoother], op)
     g_dev = g_host.to(dev)
     out_dev = torch.empty_like(g_dev)
     search = P.GcvSearch(cfg.mu_min, cfg.mu_max, cfg.count)

@@ -637,7 +637,7 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 // ---- transform pipelines (tensor_apply order: columns, then rows) ----
 // analyze count items: in (real or complex) -> out (basis type)
 void run_analyze(const fd_op* op, const void* in, int in_cplx, void* out, long long count,
-                 Scratch& S) {
+                 Scratch& S, double* wout = nullptr, long long wstride = 0, long long wn = 0) {
   const int oc = op->cplx;
   if (op->dim == 1) {
     LineIO io{};
@@ -647,6 +647,9 @@ void run_analyze(const fd_op* op, const void* in, int in_cplx, void* out, long l
     io.go = io.gi;
     io.in_cplx = in_cplx;
     io.out_cplx = oc;
+    io.wout = wout;
+    io.wstride = wstride;
+    io.wn = wn;
     launch_analyze(op->ax1->dev, io, S.st);
     return;
   }
@@ -772,6 +775,29 @@ GridHost make_grid(double mu_min, double mu_max, int count) {  // regularize.cpp
   return g;
 }
 
+// analyze for the GCV path: coefficients (for the solve) and, for 1D
+// operators on the half-length real path, the compact weights |ghat|^2
+// (Hermitian pairs pre-summed) that the GCV kernels stream contiguously.
+struct Analyzed {
+  void* ghat = nullptr;
+  double* w = nullptr;
+  long long wn = 0, wstride = 0;
+};
+
+Analyzed analyze_for_gcv(const fd_op* op, const fd_smoother* L, const double* g, long long count,
+                         Scratch& S) {
+  Analyzed a;
+  a.ghat = op->cplx ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
+  const bool use_w = op->dim == 1 && op->ax1->dev.rhalf && (!op->cplx || L->pair);
+  if (use_w) {
+    a.wn = op->cplx ? L->n_red : op->N();
+    a.wstride = (a.wn + 31) / 32 * 32;
+    a.w = S.get<double>((size_t)count * a.wstride);
+  }
+  run_analyze(op, g, 0, a.ghat, count, S, a.w, a.wstride, a.wn);
+  return a;
+}
+
 GcvData gcv_data(const fd_op* op, const fd_smoother* L, const void* ghat, long long count) {
   GcvData g{};
   g.ghat = ghat;
@@ -785,6 +811,15 @@ GcvData gcv_data(const fd_op* op, const fd_smoother* L, const void* ghat, long l
     g.pair = L->pair;
     g.r1d = L->r_red;
     g.N = L->n_red;
+  }
+  return g;
+}
+
+GcvData gcv_data(const fd_op* op, const fd_smoother* L, const Analyzed& a, long long count) {
+  GcvData g = gcv_data(op, L, a.ghat, count);
+  if (a.w) {
+    g.wred = a.w;
+    g.wstride = a.wstride;
   }
   return g;
 }
@@ -884,6 +919,44 @@ void launch_gemm(const GcvData& g, const GcvGrid& grid, long long echunk, int nc
     launch_gemm_t<8>(g, grid, echunk, nch, partial, st);
 }
 
+size_t gemm2_smem(int nj) { return (size_t)2 * (64 * 32 + 32 * 32 * nj) * 8 + 16; }
+
+template <int NJ>
+void launch_gemm2_t(const GcvData& g, const GcvGrid& grid, int nch, long long echunk,
+                    double* partial, Scratch& S) {
+  static bool attr = false;
+  if (!attr) {
+    ck(cudaFuncSetAttribute(k_gcv_gemm2<NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)gemm2_smem(NJ)),
+       "gemm2 attr");
+    attr = true;
+  }
+  constexpr int BK = 32 * NJ;
+  const int K = grid.count;
+  const int Kp = (K + BK - 1) / BK * BK;
+  const long long Np = g.wstride;
+  double* S2 = S.get<double>((size_t)Np * Kp);
+  double* den = S.get<double>(K);
+  {
+    ProfScope ps("k_gcv_s2", S.st);
+    k_gcv_s2<<<(int)std::min<long long>(4096, (Np * Kp + 255) / 256), 256, 0, S.st>>>(g, grid, Np,
+                                                                                   Kp, S2);
+    launched("k_gcv_s2");
+  }
+  {
+    ProfScope ps("k_gcv_den", S.st);
+    k_gcv_den<<<K, 256, 0, S.st>>>(g, grid, den);
+    launched("k_gcv_den");
+  }
+  const dim3 blocks((g.items + 63) / 64, nch);
+  for (int kb = 0; kb < K; kb += BK) {
+    ProfScope ps("k_gcv_grid", S.st);
+    k_gcv_gemm2<NJ><<<blocks, 256, gemm2_smem(NJ), S.st>>>(g.wred, Np, g.items, S2, Kp, K, kb,
+                                                           echunk, nch, den, partial);
+    launched("k_gcv_gemm2");
+  }
+}
+
 void launch_moments(int J, const GcvData& g, const double* center, const int* need,
                     long long chunk, int nch, double* partial, cudaStream_t st) {
   const long long warps = (long long)g.items * nch;
@@ -916,7 +989,7 @@ void gcv_direct(const GcvData& g, const double* mu_item, double* G, int* status,
 }
 
 // gcv_minimize per item on the GPU.  ghat: analyzed coefficients.
-void gcv_select_dev(const fd_op* op, const fd_smoother* L, const void* ghat, long long count,
+void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, long long count,
                     double mu_min, double mu_max, int K, double* mu_out, int* best_k_out,
                     double* curve_out, int* status, Scratch& S) {
   const GridHost gh = make_grid(mu_min, mu_max, K);
@@ -926,12 +999,28 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const void* ghat, lon
   ck(cudaMemcpyAsync(dlog, gh.logmus.data(), K * sizeof(double), cudaMemcpyHostToDevice, S.st),
      "logmus");
   GcvGrid grid{K, dmus, dlog};
-  const GcvData g = gcv_data(op, L, ghat, count);
+  const GcvData g = gcv_data(op, L, an, count);
   const int items = (int)count;
 
   int nch;
   double* part;
-  if (items >= 32) {
+  if (items >= 32 && g.wred) {
+    // shared-operator batch with compact weights: sigma^2 table + pipelined GEMM
+    const int sblocks = (items + 63) / 64;
+    nch = (int)std::max(1LL, std::min((296LL + sblocks - 1) / sblocks, g.wstride / 256));
+    long long echunk = (g.wstride + nch - 1) / nch;
+    echunk = (echunk + 31) / 32 * 32;
+    nch = (int)((g.wstride + echunk - 1) / echunk);
+    part = S.get<double>((size_t)items * nch * 2 * K);
+    if (K <= 32)
+      launch_gemm2_t<1>(g, grid, nch, echunk, part, S);
+    else if (K <= 64)
+      launch_gemm2_t<2>(g, grid, nch, echunk, part, S);
+    else if (K <= 128)
+      launch_gemm2_t<4>(g, grid, nch, echunk, part, S);
+    else
+      launch_gemm2_t<8>(g, grid, nch, echunk, part, S);
+  } else if (items >= 32) {
     // shared-operator batch: fp64 GEMM form (k_gcv_gemm)
     const int sblocks = (items + 63) / 64;
     nch = (int)std::max(1LL, std::min((296LL + sblocks - 1) / sblocks, g.N / 256));
@@ -1381,7 +1470,8 @@ int fd_smoother_create_custom(const fd_op* op, const double* s, fd_smoother** ou
         const int n = op->n1, off = op->bc == BC_HOC_FOURIER ? 1 : 0;
         const int R = op->bc == BC_HOC_FOURIER ? n - 2 : n;
         bool sym = true;
-        for (int k = 1; k < R && sym; ++k) sym = h[off + k] == h[off + R - k];
+        for (int k = 1; k < R && sym; ++k)  // symmetric to rounding
+          sym = std::abs(h[off + k] - h[off + R - k]) <= 1e-13 * std::abs(h[off + k]);
         if (sym) build_pairs(L.get(), op);
       }
     } else {
@@ -1506,14 +1596,13 @@ int fd_gcv_value(const fd_op* op, const fd_smoother* L, const double* g, double 
     if (!(mu > 0.0)) validation("mu must be positive");
     if (count <= 0) return;
     Scratch S(as_stream(stream));
-    void* c = op->cplx ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
-    run_analyze(op, g, 0, c, count, S);
+    const Analyzed an = analyze_for_gcv(op, L, g, count, S);
     std::vector<double> muh(count, mu);
     double* dmu = S.get<double>(count);
     ck(cudaMemcpyAsync(dmu, muh.data(), count * sizeof(double), cudaMemcpyHostToDevice, S.st), "mu");
     int* status = S.get<int>(1);
     ck(cudaMemsetAsync(status, 0, sizeof(int), S.st), "memset");
-    gcv_direct(gcv_data(op, L, c, count), dmu, G, status, S);
+    gcv_direct(gcv_data(op, L, an, count), dmu, G, status, S);
     check_status(status, S.st);
   });
 }
@@ -1527,11 +1616,10 @@ int fd_gcv_select(const fd_op* op, const fd_smoother* L, const double* g, double
     make_grid(mu_min, mu_max, grid_count);  // parameter validation first
     if (count <= 0) return;
     Scratch S(as_stream(stream));
-    void* c = op->cplx ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
-    run_analyze(op, g, 0, c, count, S);
+    const Analyzed an = analyze_for_gcv(op, L, g, count, S);
     int* status = S.get<int>(1);
     ck(cudaMemsetAsync(status, 0, sizeof(int), S.st), "memset");
-    gcv_select_dev(op, L, c, count, mu_min, mu_max, grid_count, mu, best_k, curve, status, S);
+    gcv_select_dev(op, L, an, count, mu_min, mu_max, grid_count, mu, best_k, curve, status, S);
     check_status(status, S.st);
   });
 }
@@ -1549,18 +1637,18 @@ int fd_deblur(const fd_op* op, const fd_smoother* L, const double* g, int use_gc
     if (!use_gcv && !(fixed_mu > 0.0)) validation("mu must be positive");
     if (count <= 0) return;
     Scratch S(as_stream(stream));
-    void* c = op->cplx ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
-    run_analyze(op, g, 0, c, count, S);
+    const Analyzed an = analyze_for_gcv(op, L, g, count, S);
+    void* c = an.ghat;
     int* status = S.get<int>(1);
     ck(cudaMemsetAsync(status, 0, sizeof(int), S.st), "memset");
     if (use_gcv) {
-      gcv_select_dev(op, L, c, count, mu_min, mu_max, grid_count, mu_used, best_k, curve, status,
+      gcv_select_dev(op, L, an, count, mu_min, mu_max, grid_count, mu_used, best_k, curve, status,
                      S);
     } else {
       if (curve) {
         double* tmp_mu = S.get<double>(count);
-        gcv_select_dev(op, L, c, count, mu_min, mu_max, grid_count, tmp_mu, best_k, curve, status,
-                       S);
+        gcv_select_dev(op, L, an, count, mu_min, mu_max, grid_count, tmp_mu, best_k, curve,
+                       status, S);
       }
       std::vector<double> muh(count, fixed_mu);
       ck(cudaMemcpyAsync(mu_used, muh.data(), count * sizeof(double), cudaMemcpyHostToDevice,

@@ -303,6 +303,12 @@ struct LineIO {
   void* out;
   Lines gi, go;
   int in_cplx, out_cplx;
+  // optional GCV weights of 1D analyze (k_ranalyze): w[l * wstride + i] = |ghat|^2,
+  // Hermitian pairs pre-summed for complex bases (reduced index order of
+  // build_pairs in fd_capi.cu)
+  double* wout;
+  long long wstride;
+  long long wn;  // weights actually written; [wn, wstride) is zero-filled
 };
 
 __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
@@ -838,40 +844,83 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io) {
   const long long oo = line_offset(io.go, l), eso = io.go.elem_stride;
   const double inv_sqrt_m = 1.0 / sqrt((double)m);
   const double s0 = sqrt(1.0 / (double)m), s1 = sqrt(2.0 / (double)m);
-  auto emit = [&](int i, double2 xi) {
+  double* wl = io.wout ? io.wout + (long long)l * io.wstride : nullptr;
+  if (wl)
+    for (long long i = io.wn + threadIdx.x; i < io.wstride; i += blockDim.x) wl[i] = 0.0;
+  // final coefficient of interior index i (border terms applied), stored;
+  // returns the value for the GCV weights
+  auto emit = [&](int i, double2 xi) -> double2 {
     const int e = interior_elem(ax, i);
-    if (!ax.bordered) {
-      stc(io.out, io.out_cplx, oo + e * eso, xi);
-      return;
+    double2 o = xi;
+    if (ax.bordered) {
+      const double2 v = __ldg(&ax.v[i]), w = __ldg(&ax.w[i]);
+      if (ax.cplx) {
+        o = cadd(cadd(cscale(v, y0), xi), cscale(w, yn));
+        if (dots) o = csub(o, cadd(cmul(b0, v), cmul(b1, w)));
+      } else {
+        double r = y0 * v.x + xi.x + yn * w.x;
+        if (dots) r -= b0.x * v.x + b1.x * w.x;
+        o = make_double2(r, 0.0);
+      }
     }
-    const double2 v = __ldg(&ax.v[i]), w = __ldg(&ax.w[i]);
-    if (ax.cplx) {
-      double2 o = cadd(cadd(cscale(v, y0), xi), cscale(w, yn));
-      if (dots) o = csub(o, cadd(cmul(b0, v), cmul(b1, w)));
-      stc(io.out, io.out_cplx, oo + e * eso, o);
-    } else {
-      double o = y0 * v.x + xi.x + yn * w.x;
-      if (dots) o -= b0.x * v.x + b1.x * w.x;
-      stc(io.out, io.out_cplx, oo + e * eso, make_double2(o, 0.0));
-    }
+    stc(io.out, io.out_cplx, oo + e * eso, o);
+    if (wl && !ax.cplx) wl[e] = o.x * o.x;
+    return o;
   };
-  for (int k = threadIdx.x; k < h; k += blockDim.x) {
-    const int kc = k == 0 ? 0 : h - k;
-    const double2 Zk = cmul(x[pidx(k)], __ldg(&chirp[k]));
-    const double2 Zc = cconj(cmul(x[pidx(kc)], __ldg(&chirp[kc])));
-    const double2 E = cscale(cadd(Zk, Zc), 0.5);
-    const double2 D = csub(Zk, Zc);
-    const double2 WO = cmul(__ldg(&ax.rtw[k]), make_double2(0.5 * D.y, -0.5 * D.x));
-    const double2 X0 = cadd(E, WO), X1 = csub(E, WO);  // X_k, X_{k+h}
-    if (ax.kind == IK_SINE) {
-      if (k >= 1) emit(k - 1, make_double2(-0.5 * sqrt(2.0 / ((double)m + 1.0)) * X0.y, 0.0));
-    } else if (ax.kind == IK_COS) {
-      const double2 t0 = __ldg(&ax.dct_tw[k]), t1 = __ldg(&ax.dct_tw[k + h]);
-      emit(k, make_double2((k == 0 ? s0 : s1) * (t0.x * X0.x - t0.y * X0.y), 0.0));
-      emit(k + h, make_double2(s1 * (t1.x * X1.x - t1.y * X1.y), 0.0));
-    } else {
-      emit(k, cscale(X0, inv_sqrt_m));
-      emit(k + h, cscale(X1, inv_sqrt_m));
+  auto nrm = [](double2 a) { return a.x * a.x + a.y * a.y; };
+  if (ax.kind == IK_FOURIER) {
+    // groups {k, h-k}: both Hermitian partners of each coefficient come out of
+    // the same pair (Z_k, Z_{h-k}), so the GCV weights |g_k|^2 + |g_{m-k}|^2
+    // are formed in registers
+    const int off = ax.bordered ? 1 : 0;
+    for (int k = threadIdx.x; k <= h / 2; k += blockDim.x) {
+      const int kp = k == 0 ? 0 : h - k;
+      const double2 Zk = cmul(x[pidx(k)], __ldg(&chirp[k]));
+      const double2 Zp = cmul(x[pidx(kp)], __ldg(&chirp[kp]));
+      const double2 E = cscale(cadd(Zk, cconj(Zp)), 0.5);
+      const double2 D = csub(Zk, cconj(Zp));
+      const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
+      const double2 WO = cmul(__ldg(&ax.rtw[k]), O);
+      const double2 ok = emit(k, cscale(cadd(E, WO), inv_sqrt_m));
+      const double2 okh = emit(k + h, cscale(csub(E, WO), inv_sqrt_m));
+      if (kp != k) {
+        const double2 WOp = cmul(__ldg(&ax.rtw[kp]), cconj(O));
+        const double2 okp = emit(kp, cscale(cadd(cconj(E), WOp), inv_sqrt_m));
+        const double2 okph = emit(kp + h, cscale(csub(cconj(E), WOp), inv_sqrt_m));
+        if (wl) {
+          if (k == 0) {
+            wl[off] = nrm(ok);
+            wl[off + h] = nrm(okh);
+          } else {
+            wl[off + k] = nrm(ok) + nrm(okph);   // pair (k, m-k = kp+h)
+            wl[off + kp] = nrm(okp) + nrm(okh);  // pair (kp, m-kp = k+h)
+          }
+        }
+      } else if (wl) {
+        if (k == 0) {  // singleton group {0}: self pairs 0 and h
+          wl[off] = nrm(ok);
+          wl[off + h] = nrm(okh);
+        } else {
+          wl[off + k] = nrm(ok) + nrm(okh);  // k = h/2: pair (k, k+h)
+        }
+      }
+    }
+  } else {
+    for (int k = threadIdx.x; k < h; k += blockDim.x) {
+      const int kc = k == 0 ? 0 : h - k;
+      const double2 Zk = cmul(x[pidx(k)], __ldg(&chirp[k]));
+      const double2 Zc = cconj(cmul(x[pidx(kc)], __ldg(&chirp[kc])));
+      const double2 E = cscale(cadd(Zk, Zc), 0.5);
+      const double2 D = csub(Zk, Zc);
+      const double2 WO = cmul(__ldg(&ax.rtw[k]), make_double2(0.5 * D.y, -0.5 * D.x));
+      const double2 X0 = cadd(E, WO), X1 = csub(E, WO);  // X_k, X_{k+h}
+      if (ax.kind == IK_SINE) {
+        if (k >= 1) emit(k - 1, make_double2(-0.5 * sqrt(2.0 / ((double)m + 1.0)) * X0.y, 0.0));
+      } else {
+        const double2 t0 = __ldg(&ax.dct_tw[k]), t1 = __ldg(&ax.dct_tw[k + h]);
+        emit(k, make_double2((k == 0 ? s0 : s1) * (t0.x * X0.x - t0.y * X0.y), 0.0));
+        emit(k + h, make_double2(s1 * (t1.x * X1.x - t1.y * X1.y), 0.0));
+      }
     }
   }
   if (ax.bordered && threadIdx.x == 0) {
@@ -883,6 +932,15 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io) {
     }
     stc(io.out, io.out_cplx, oo, o0);
     stc(io.out, io.out_cplx, oo + (long long)(n - 1) * eso, on);
+    if (wl) {
+      if (ax.cplx) {
+        wl[0] = nrm(o0);
+        wl[h + 2] = nrm(on);
+      } else {
+        wl[0] = o0.x * o0.x;
+        wl[n - 1] = on.x * on.x;
+      }
+    }
   }
 }
 
@@ -1031,6 +1089,8 @@ struct GcvData {
   int items;
   const double* r1d;     // 1D ratio vector (length N), or null for 2D
   const int2* pair;      // optional: element e sums |ghat|^2 at pair[e].x and pair[e].y (>= 0)
+  const double* wred;    // optional: precomputed weights w[item * wstride + e] (k_ranalyze wout)
+  long long wstride;
   Spectral sp;           // 2D: mode 2 (separable) or 3 (full); sp.n2 = row length
 };
 
@@ -1068,6 +1128,7 @@ __device__ __forceinline__ double gcv_mult(const GcvData& g, long long e) {
 }
 
 __device__ __forceinline__ double gcv_w(const GcvData& g, int item, long long e) {
+  if (g.wred) return __ldg(&g.wred[(long long)item * g.wstride + e]);
   const long long base = (long long)item * g.stride;
   if (g.pair) {
     const int2 p = __ldg(&g.pair[e]);
@@ -1281,6 +1342,154 @@ __global__ void __launch_bounds__(256) k_gcv_gemm(GcvData g, GcvGrid grid, int k
       if (k < K) {
         base[k] = acc[s2][j];
         base[K + k] = Dn[tx + 32 * j];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GCV grid, GEMM form with a precomputed sigma^2 table (batches sharing one
+// operator, 1D).  sigma depends only on (operator, smoother, grid), so
+//   S2[e][k] = sigma_e(mu_k)^2  (N x Kp, L2-resident),  den[k] = sum_e mult_e sigma_e(mu_k)
+// are formed once per call; the GEMM num = W S2 then streams 32-element tiles
+// of the weights W (|ghat|^2 written by k_ranalyze, pairs pre-summed) and of S2
+// into shared memory with cp.async.bulk + mbarrier, double buffered, so the
+// copy engine fills stage c+1 while the DFMA micro-tiles consume stage c.
+// ---------------------------------------------------------------------------
+__global__ void k_gcv_s2(GcvData g, GcvGrid grid, long long Np, int Kp, double* S2) {
+  const long long tot = Np * Kp;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long e = t / Kp;
+    const int kk = (int)(t % Kp);
+    double v = 0.0;
+    if (e < g.N && kk < grid.count) {
+      const double r = gcv_ratio(g, e);
+      if (!isinf(r)) {
+        const double s = 1.0 / (r + grid.mus[kk]);
+        v = s * s;
+      }
+    }
+    S2[t] = v;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_gcv_den(GcvData g, GcvGrid grid, double* den) {
+  __shared__ double red[32];
+  const int kk = blockIdx.x;
+  const double mu = grid.mus[kk];
+  double acc[1] = {0.0};
+  for (long long e = threadIdx.x; e < g.N; e += blockDim.x) {
+    const double r = gcv_ratio(g, e);
+    if (!isinf(r)) acc[0] = fma(gcv_mult(g, e), 1.0 / (r + mu), acc[0]);
+  }
+  block_sum<1>(acc, red);
+  if (threadIdx.x == 0) den[kk] = acc[0];
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// bulk global -> shared copy (TMA engine, UBLKCP), completion on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int NJ>
+__global__ void __launch_bounds__(256) k_gcv_gemm2(const double* __restrict__ W, long long Np,
+                                                   int items, const double* __restrict__ S2,
+                                                   int Kp, int K, int kb0, long long echunk,
+                                                   int nch, const double* __restrict__ den,
+                                                   double* partial) {
+  constexpr int BS = 64, E = 32, BK = 32 * NJ;
+  constexpr int STAGE = BS * E + E * BK;  // doubles per stage
+  extern __shared__ __align__(128) double gsm2[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(gsm2 + 2 * STAGE);
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  const int item0 = blockIdx.x * BS;
+  const int rows = min(BS, items - item0);
+  const long long eb = (long long)blockIdx.y * echunk;
+  const long long ee = min(Np, eb + echunk);
+  const int nck = (int)((ee - eb + E - 1) / E);
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t bytes = (uint32_t)(rows * E + E * BK) * 8u;
+  auto issue = [&](int c) {  // warp 0 fills stage c & 1 with chunk c
+    double* st = gsm2 + (c & 1) * STAGE;
+    const long long e0 = eb + (long long)c * E;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (tx == 0) mbar_expect_tx(&bars[c & 1], bytes);
+    __syncwarp();
+    for (int s = tx; s < rows; s += 32)
+      bulk_g2s(st + s * E, W + (long long)(item0 + s) * Np + e0, E * 8, &bars[c & 1]);
+    if (BK == Kp) {
+      if (tx == 0) bulk_g2s(st + BS * E, S2 + e0 * Kp, E * BK * 8, &bars[c & 1]);
+    } else {
+      bulk_g2s(st + BS * E + tx * BK, S2 + (e0 + tx) * Kp + kb0, BK * 8, &bars[c & 1]);
+    }
+  };
+  double acc[8][NJ];
+#pragma unroll
+  for (int s = 0; s < 8; ++s)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[s][j] = 0.0;
+  if (ty == 0 && nck > 0) issue(0);
+  for (int c = 0; c < nck; ++c) {
+    if (ty == 0 && c + 1 < nck) issue(c + 1);
+    mbar_wait(&bars[c & 1], (c >> 1) & 1);
+    const double* Wt = gsm2 + (c & 1) * STAGE;
+    const double* St = Wt + BS * E;
+#pragma unroll 4
+    for (int e = 0; e < E; ++e) {
+      double a[8], b[NJ];
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2) a[s2] = Wt[(ty * 8 + s2) * E + e];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) b[j] = St[e * BK + tx + 32 * j];
+#pragma unroll
+      for (int s2 = 0; s2 < 8; ++s2)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc[s2][j] = fma(a[s2], b[j], acc[s2][j]);
+    }
+    __syncthreads();  // stage (c & 1) is refilled by iteration c + 1's issue(c + 2)
+  }
+#pragma unroll
+  for (int s2 = 0; s2 < 8; ++s2) {
+    const int item = item0 + ty * 8 + s2;
+    if (item >= items) continue;
+    double* base = partial + ((long long)item * nch + blockIdx.y) * 2 * K;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      const int kk = kb0 + tx + 32 * j;
+      if (kk < K) {
+        base[kk] = acc[s2][j];
+        base[K + kk] = blockIdx.y == 0 ? den[kk] : 0.0;
       }
     }
   }
