@@ -202,15 +202,106 @@ __device__ __forceinline__ void fft_dit(double2* x, int M, int logM, const TwSm&
   }
 }
 
+// The innermost DIF pass, the pointwise multiply by DIF(b)/M and the
+// outermost DIT pass act on the same disjoint element groups (blocks of S
+// consecutive positions, S = 2^LOGR), so they run as one register pass: load
+// the group and its bhat values, LOGR DIF stages, multiply, LOGR DIT stages,
+// store.  Saves two shared-memory round trips per Bluestein convolution.
+template <int LOGR>
+__device__ __forceinline__ void mid_pass(double2* __restrict__ x, int M,
+                                         const double2* __restrict__ bhat, const TwSm& tw) {
+  constexpr int R = 1 << LOGR;
+  const int items = M >> LOGR;
+  const int twstep = M / R;
+  for (int it = threadIdx.x; it < items; it += blockDim.x) {
+    const int base = it * R;  // S = R: SR = 1, j0 = 0
+    double2 v[R], bh[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) bh[q] = __ldg(&bhat[base + q]);
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = x[pidx(base + q)];
+    (void)twstep;
+    // DIF stages with j0 = 0: every twiddle is a radix-16 constant
+#pragma unroll
+    for (int st = 0; st < LOGR; ++st) {
+      const int half = R >> (st + 1);
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (q & half) continue;
+        const int qq = q & (half - 1);
+        const double2 a = v[q], b = v[q + half];
+        v[q] = cadd(a, b);
+        v[q + half] = mul_w16(csub(a, b), (qq << st) * (16 / R));
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = cmul(v[q], bh[q]);
+#pragma unroll
+    for (int st = LOGR - 1; st >= 0; --st) {
+      const int half = R >> (st + 1);
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (q & half) continue;
+        const int qq = q & (half - 1);
+        const double2 a = v[q];
+        const double2 b = mul_w16c(v[q + half], (qq << st) * (16 / R));
+        v[q] = cadd(a, b);
+        v[q + half] = csub(a, b);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) x[pidx(base + q)] = v[q];
+  }
+  (void)tw;
+}
+
 // Bluestein core: x holds a_j = z_j c_j (j < L) and zeros up to M; on return
 // x_k holds the circular convolution (a * b)_k; the caller multiplies by c_k.
 // Requires a barrier before the call (the caller's loads); ends with one.
 __device__ __forceinline__ void bluestein_core(double2* x, const FftTables& T, const TwSm& tw) {
-  fft_dif(x, T.M, T.logM, tw);
-  for (int j = threadIdx.x; j < T.M; j += blockDim.x)
-    x[pidx(j)] = cmul(x[pidx(j)], __ldg(&T.bhat[j]));
+  const int M = T.M, logM = T.logM;
+  if (logM == 0) {
+    if (threadIdx.x == 0) x[0] = cmul(x[0], __ldg(&T.bhat[0]));
+    __syncthreads();
+    return;
+  }
+  int ls[8];
+  int np = 0;
+  for (int rem = logM; rem > 0;) {
+    const int l = pass_logr(rem);
+    ls[np++] = l;
+    rem -= l;
+  }
+  // DIF passes 0 .. np-2
+  int S = M;
+  for (int p = 0; p < np - 1; ++p) {
+    switch (ls[p]) {
+      case 4: dif_pass<4>(x, M, S, tw); break;
+      case 3: dif_pass<3>(x, M, S, tw); break;
+      case 2: dif_pass<2>(x, M, S, tw); break;
+      default: dif_pass<1>(x, M, S, tw); break;
+    }
+    S >>= ls[p];
+    __syncthreads();
+  }
+  switch (ls[np - 1]) {  // S == 2^ls[np-1] here
+    case 4: mid_pass<4>(x, M, T.bhat, tw); break;
+    case 3: mid_pass<3>(x, M, T.bhat, tw); break;
+    case 2: mid_pass<2>(x, M, T.bhat, tw); break;
+    default: mid_pass<1>(x, M, T.bhat, tw); break;
+  }
   __syncthreads();
-  fft_dit(x, T.M, T.logM, tw);
+  // DIT passes np-2 .. 0
+  for (int p = np - 2; p >= 0; --p) {
+    S <<= ls[p];
+    switch (ls[p]) {
+      case 4: dit_pass<4>(x, M, S, tw); break;
+      case 3: dit_pass<3>(x, M, S, tw); break;
+      case 2: dit_pass<2>(x, M, S, tw); break;
+      default: dit_pass<1>(x, M, S, tw); break;
+    }
+    __syncthreads();
+  }
 }
 
 // ----------------------------------------------------------------------------

@@ -779,9 +779,11 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io) {
   const bool dots = ax.bordered && ax.correction;
   const int half = (m + 1) / 2;
   double acc[4] = {0, 0, 0, 0};  // ra (re, im), rb (re, im)
-  for (int j = threadIdx.x; j < M; j += blockDim.x) {
+  for (int j = h + threadIdx.x; j < M; j += blockDim.x) x[pidx(j)] = czero();
+#pragma unroll 4
+  for (int j = threadIdx.x; j < h; j += blockDim.x) {
     double2 val = czero();
-    if (j < h) {
+    {
       const int p0 = 2 * j, p1 = 2 * j + 1;
       double a, b;
       if (ax.kind == IK_SINE) {
@@ -982,6 +984,7 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
   } else {
     // stage the (filtered) coefficients: cosine stores conj(buf_i) = s_i c_i conj(tw_i)
     const double s0 = sqrt(1.0 / (double)m), s1 = sqrt(2.0 / (double)m);
+#pragma unroll 4
     for (int i = threadIdx.x; i < m; i += blockDim.x) {
       const double2 c = cf(interior_elem(ax, i));
       double2 val;
