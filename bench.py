@@ -302,11 +302,8 @@ def main():
         mu_host = torch.empty(shape[0], dtype=torch.float64).pin_memory()
         e_steps = max(1, min(args.steps, 5))
 
-        def e2e_step():
-            g = g_host.to(dev, non_blocking=True)
-            r = P.deblur(op, L, g, choice, search=search, out=out_dev)
-            out_host.copy_(r.restored, non_blocking=True)
-            mu_host.copy_(r.mu_used, non_blocking=True)
+        def e2e_step():  # public host-buffer API: chunked H2D | deblur | D2H pipeline
+            P.deblur_host(op, L, g_host, choice, search=search, out=out_host)
 
         e2e_step()
         torch.cuda.synchronize()

@@ -142,6 +142,16 @@ int fd_deblur(const fd_op* op, const fd_smoother* L, const double* g, int use_gc
               double* mu_used, int* best_k, double* curve, double* imag_residue, long long count,
               void* stream);
 
+/* deblur for HOST buffers (pinned memory recommended): the batch is split
+ * into chunks of `chunk` items (0 = count/16, at least 256) that flow through a three-stage
+ * pipeline -- H2D copy, deblur in place, D2H copy -- on separate streams, so
+ * both PCIe directions overlap each other and the kernels.  g, restored:
+ * count*N doubles; mu_used: count doubles; best_k: count ints or NULL. */
+int fd_deblur_host(const fd_op* op, const fd_smoother* L, const double* g, int use_gcv,
+                   double fixed_mu, double mu_min, double mu_max, int grid_count,
+                   double* restored, double* mu_used, int* best_k, long long count,
+                   long long chunk, void* stream);
+
 /* The same selection logic the kernels run (gcv_minimize, regularize.cpp:281-351),
  * on the host with a caller-supplied G: for the CPU test suite. */
 typedef double (*fd_gcv_fn)(double mu, void* ctx);

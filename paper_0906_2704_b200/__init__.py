@@ -4,7 +4,7 @@ the C ABI in include/fastdeblur_b200.h); ``fastdeblur`` mirrors the reference
 operator API over it."""
 from .fastdeblur import (  # noqa: F401
     BC, SMOOTHER, BlurOperator, DegenerateError, FastDeblurError, GcvResult, GcvSearch,
-    MuChoice, RestorationReport, Smoother, ValidationError, bc_for_degree, blur_apply,
+    MuChoice, RestorationReport, Smoother, ValidationError, bc_for_degree, blur_apply, deblur_host,
     build_operator, build_operator_2d, build_operator_2d_separable, deblur, gcv_select,
     gcv_value, kernel_launches, lib, smoother_from_eigenvalues, smoothing_eigenvalues,
     tikhonov_solve)

@@ -989,16 +989,29 @@ void gcv_direct(const GcvData& g, const double* mu_item, double* G, int* status,
 }
 
 // gcv_minimize per item on the GPU.  ghat: analyzed coefficients.
+// the log-spaced grid (regularize.cpp:283-293) on the host with the
+// reference's libm, uploaded once per API call (a pageable upload would
+// synchronise the stream, so it must not sit inside a pipelined loop)
+struct DevGrid {
+  GridHost h;
+  GcvGrid d{};
+  DevGrid(double mu_min, double mu_max, int K, Scratch& S) : h(make_grid(mu_min, mu_max, K)) {
+    double* buf = S.get<double>(2 * (size_t)K);
+    std::vector<double> tmp(h.mus);
+    tmp.insert(tmp.end(), h.logmus.begin(), h.logmus.end());
+    ck(cudaMemcpyAsync(buf, tmp.data(), tmp.size() * sizeof(double), cudaMemcpyHostToDevice,
+                       S.st),
+       "grid");
+    d = GcvGrid{K, buf, buf + K};
+  }
+};
+
 void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, long long count,
-                    double mu_min, double mu_max, int K, double* mu_out, int* best_k_out,
-                    double* curve_out, int* status, Scratch& S) {
-  const GridHost gh = make_grid(mu_min, mu_max, K);
-  double* dmus = S.get<double>(K);
-  double* dlog = S.get<double>(K);
-  ck(cudaMemcpyAsync(dmus, gh.mus.data(), K * sizeof(double), cudaMemcpyHostToDevice, S.st), "mus");
-  ck(cudaMemcpyAsync(dlog, gh.logmus.data(), K * sizeof(double), cudaMemcpyHostToDevice, S.st),
-     "logmus");
-  GcvGrid grid{K, dmus, dlog};
+                    const DevGrid& dg, double mu_min, double mu_max, double* mu_out,
+                    int* best_k_out, double* curve_out, int* status, Scratch& S) {
+  const GridHost& gh = dg.h;
+  const int K = dg.d.count;
+  GcvGrid grid = dg.d;
   const GcvData g = gcv_data(op, L, an, count);
   const int items = (int)count;
 
@@ -1143,6 +1156,46 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
   }
   ck(cudaMemcpyAsync(mu_out, muh.data(), items * sizeof(double), cudaMemcpyHostToDevice, S.st),
      "mu out");
+}
+
+__global__ void k_fill(double* p, long long n, double v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+void check_deblur_args(const fd_op* op, const fd_smoother* L, int use_gcv, double fixed_mu,
+                       double mu_min, double mu_max, int grid_count, const double* mu_used,
+                       const double* curve) {
+  if (!op) validation("null operator");
+  if (!L) validation("null smoother");
+  if (L->op != op) validation("smoother was built for a different operator");
+  if (!mu_used) validation("mu_used output is required");
+  if (use_gcv || curve) make_grid(mu_min, mu_max, grid_count);  // pipeline.cpp:737-750
+  if (!use_gcv && !(fixed_mu > 0.0)) validation("mu must be positive");
+}
+
+// deblur (pipeline.cpp:732-768) of `count` device-resident items; a GCV
+// degeneracy is flagged in *status (checked by the caller after a sync).
+void deblur_dev(const fd_op* op, const fd_smoother* L, const double* g, int use_gcv,
+                double fixed_mu, double mu_min, double mu_max, const DevGrid* dg,
+                double* restored, double* mu_used, int* best_k, double* curve,
+                double* imag_residue, long long count, int* status, Scratch& S) {
+  const Analyzed an = analyze_for_gcv(op, L, g, count, S);
+  if (use_gcv) {
+    gcv_select_dev(op, L, an, count, *dg, mu_min, mu_max, mu_used, best_k, curve, status, S);
+  } else {
+    if (curve) {
+      double* tmp_mu = S.get<double>(count);
+      gcv_select_dev(op, L, an, count, *dg, mu_min, mu_max, tmp_mu, best_k, curve, status, S);
+    }
+    k_fill<<<(int)std::min<long long>(1024, (count + 255) / 256), 256, 0, S.st>>>(mu_used, count,
+                                                                                fixed_mu);
+    launched("k_fill");
+  }
+  if (!op->cplx && imag_residue)
+    ck(cudaMemsetAsync(imag_residue, 0, count * sizeof(double), S.st), "memset");
+  run_synth(op, L, an.ghat, restored, 0, 1, mu_used, imag_residue, count, S);
 }
 
 void check_status(int* status, cudaStream_t st) {
@@ -1619,7 +1672,8 @@ int fd_gcv_select(const fd_op* op, const fd_smoother* L, const double* g, double
     const Analyzed an = analyze_for_gcv(op, L, g, count, S);
     int* status = S.get<int>(1);
     ck(cudaMemsetAsync(status, 0, sizeof(int), S.st), "memset");
-    gcv_select_dev(op, L, an, count, mu_min, mu_max, grid_count, mu, best_k, curve, status, S);
+    const DevGrid dg(mu_min, mu_max, grid_count, S);
+    gcv_select_dev(op, L, an, count, dg, mu_min, mu_max, mu, best_k, curve, status, S);
     check_status(status, S.st);
   });
 }
@@ -1629,36 +1683,122 @@ int fd_deblur(const fd_op* op, const fd_smoother* L, const double* g, int use_gc
               double* mu_used, int* best_k, double* curve, double* imag_residue, long long count,
               void* stream) {
   return guarded([&] {
-    check_op(op);
-    check_L(op, L);
-    if (!mu_used) validation("mu_used output is required");
-    const bool need_grid = use_gcv || curve != nullptr;  // pipeline.cpp:737-750
-    if (need_grid) make_grid(mu_min, mu_max, grid_count);
-    if (!use_gcv && !(fixed_mu > 0.0)) validation("mu must be positive");
+    check_deblur_args(op, L, use_gcv, fixed_mu, mu_min, mu_max, grid_count, mu_used, curve);
     if (count <= 0) return;
     Scratch S(as_stream(stream));
-    const Analyzed an = analyze_for_gcv(op, L, g, count, S);
-    void* c = an.ghat;
     int* status = S.get<int>(1);
     ck(cudaMemsetAsync(status, 0, sizeof(int), S.st), "memset");
-    if (use_gcv) {
-      gcv_select_dev(op, L, an, count, mu_min, mu_max, grid_count, mu_used, best_k, curve, status,
-                     S);
-    } else {
-      if (curve) {
-        double* tmp_mu = S.get<double>(count);
-        gcv_select_dev(op, L, an, count, mu_min, mu_max, grid_count, tmp_mu, best_k, curve,
-                       status, S);
-      }
-      std::vector<double> muh(count, fixed_mu);
-      ck(cudaMemcpyAsync(mu_used, muh.data(), count * sizeof(double), cudaMemcpyHostToDevice,
-                         S.st),
-         "mu");
+    std::unique_ptr<DevGrid> dg;
+    if (use_gcv || curve) dg = std::make_unique<DevGrid>(mu_min, mu_max, grid_count, S);
+    deblur_dev(op, L, g, use_gcv, fixed_mu, mu_min, mu_max, dg.get(), restored, mu_used, best_k,
+               curve, imag_residue, count, status, S);
+    if (use_gcv || curve) check_status(status, S.st);
+  });
+}
+
+int fd_deblur_host(const fd_op* op, const fd_smoother* L, const double* g, int use_gcv,
+                   double fixed_mu, double mu_min, double mu_max, int grid_count,
+                   double* restored, double* mu_used, int* best_k, long long count,
+                   long long chunk, void* stream) {
+  return guarded([&] {
+    check_deblur_args(op, L, use_gcv, fixed_mu, mu_min, mu_max, grid_count, mu_used, nullptr);
+    if (count <= 0) return;
+    if (!g || !restored) validation("null host buffer");
+    const long long N = op->N();
+    if (chunk <= 0) chunk = std::max(std::min(count, 256LL), (count + 15) / 16);
+    chunk = std::min(chunk, count);
+    const long long nchunks = (count + chunk - 1) / chunk;
+    const cudaStream_t sc = as_stream(stream);
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev_in[2], ev_comp[2], ev_out[2];
+    ck(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "stream");
+    for (int k = 0; k < 2; ++k) {
+      ck(cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&ev_comp[k], cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming), "event");
     }
-    if (!op->cplx && imag_residue)
-      ck(cudaMemsetAsync(imag_residue, 0, count * sizeof(double), S.st), "memset");
-    run_synth(op, L, c, restored, 0, 1, mu_used, imag_residue, count, S);
-    if (need_grid) check_status(status, S.st);
+    struct Cleanup {
+      cudaStream_t a, b;
+      cudaEvent_t* e[3];
+      ~Cleanup() {
+        cudaStreamSynchronize(a);
+        cudaStreamSynchronize(b);
+        for (auto* ev : e)
+          for (int k = 0; k < 2; ++k) cudaEventDestroy(ev[k]);
+        cudaStreamDestroy(a);
+        cudaStreamDestroy(b);
+      }
+    } cleanup{s_in, s_out, {ev_in, ev_comp, ev_out}};
+    // Async copies need page-locked host memory; pageable g / restored are
+    // registered for the duration of the call (a copy into pageable memory
+    // would block the issuing thread and serialise the pipeline).
+    struct HostPin {
+      std::vector<void*> regs;
+      void pin(const void* p, size_t bytes) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, p) == cudaSuccess && at.type == cudaMemoryTypeHost)
+          return;
+        cudaGetLastError();
+        if (cudaHostRegister(const_cast<void*>(p), bytes, cudaHostRegisterDefault) == cudaSuccess)
+          regs.push_back(const_cast<void*>(p));
+        else
+          cudaGetLastError();
+      }
+      ~HostPin() {
+        for (void* p : regs) cudaHostUnregister(p);
+      }
+    } pins;
+    pins.pin(g, (size_t)count * N * sizeof(double));
+    pins.pin(restored, (size_t)count * N * sizeof(double));
+    double* slot[2];
+    double* dmu = nullptr;
+    int* dbk = nullptr;
+    int* status = nullptr;
+    ck(cudaMallocAsync(&status, sizeof(int), sc), "alloc");
+    ck(cudaMemsetAsync(status, 0, sizeof(int), sc), "memset");
+    ck(cudaMallocAsync(&dmu, (size_t)count * sizeof(double), sc), "alloc");
+    ck(cudaMallocAsync(&dbk, (size_t)count * sizeof(int), sc), "alloc");
+    for (int k = 0; k < 2; ++k)
+      ck(cudaMallocAsync(&slot[k], (size_t)chunk * N * sizeof(double), sc), "alloc");
+    Scratch SG(sc);
+    std::unique_ptr<DevGrid> dg;
+    if (use_gcv) dg = std::make_unique<DevGrid>(mu_min, mu_max, grid_count, SG);
+    ck(cudaStreamSynchronize(sc), "alloc sync");
+    // three-stage pipeline: H2D (s_in) | deblur in place (sc) | D2H (s_out)
+    for (long long i = 0; i < nchunks; ++i) {
+      const int k = (int)(i & 1);
+      const long long b0 = i * chunk, nb = std::min(chunk, count - b0);
+      if (i >= 2) ck(cudaStreamWaitEvent(s_in, ev_out[k], 0), "wait");
+      ck(cudaMemcpyAsync(slot[k], g + b0 * N, (size_t)nb * N * sizeof(double),
+                         cudaMemcpyHostToDevice, s_in),
+         "h2d");
+      ck(cudaEventRecord(ev_in[k], s_in), "record");
+      ck(cudaStreamWaitEvent(sc, ev_in[k], 0), "wait");
+      {
+        Scratch S(sc);
+        deblur_dev(op, L, slot[k], use_gcv, fixed_mu, mu_min, mu_max, dg.get(), slot[k],
+                   dmu + b0, dbk + b0, nullptr, nullptr, nb, status, S);
+      }
+      ck(cudaEventRecord(ev_comp[k], sc), "record");
+      ck(cudaStreamWaitEvent(s_out, ev_comp[k], 0), "wait");
+      ck(cudaMemcpyAsync(restored + b0 * N, slot[k], (size_t)nb * N * sizeof(double),
+                         cudaMemcpyDeviceToHost, s_out),
+         "d2h");
+      ck(cudaEventRecord(ev_out[k], s_out), "record");
+    }
+    ck(cudaStreamSynchronize(s_out), "sync");
+    ck(cudaStreamSynchronize(sc), "sync");
+    int h = 0;
+    ck(cudaMemcpy(&h, status, sizeof(int), cudaMemcpyDeviceToHost), "status");
+    ck(cudaMemcpy(mu_used, dmu, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost), "mu");
+    if (best_k && use_gcv)
+      ck(cudaMemcpy(best_k, dbk, (size_t)count * sizeof(int), cudaMemcpyDeviceToHost), "best_k");
+    for (int k = 0; k < 2; ++k) cudaFreeAsync(slot[k], sc);
+    cudaFreeAsync(dmu, sc);
+    cudaFreeAsync(dbk, sc);
+    cudaFreeAsync(status, sc);
+    if (h == 3) degenerate("degenerate gcv: all smoother eigenvalues are zero");
   });
 }
 

@@ -217,7 +217,7 @@ __device__ __forceinline__ void mid_pass(double2* __restrict__ x, int M,
     const int base = it * R;  // S = R: SR = 1, j0 = 0
     double2 v[R], bh[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) bh[q] = __ldg(&bhat[base + q]);
+    for (int q = 0; q < R; ++q) bh[q] = bhat[base + q];  // global or shared
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = x[pidx(base + q)];
     (void)twstep;

@@ -71,6 +71,8 @@ def lib():
         L.fd_gcv_select.argtypes = [vp, vp, vp, C.c_double, C.c_double, ip, vp, vp, vp, ll, vp]
         L.fd_deblur.argtypes = [vp, vp, vp, ip, C.c_double, C.c_double, C.c_double, ip, vp, vp,
                                 vp, vp, vp, ll, vp]
+        L.fd_deblur_host.argtypes = [vp, vp, vp, ip, C.c_double, C.c_double, C.c_double, ip,
+                                     vp, vp, vp, ll, ll, vp]
         L.fd_bc_for_degree.argtypes = [ip, ip, C.POINTER(C.c_int)]
         L.fd_parse_bc.argtypes = [C.c_char_p]
         _lib = L
@@ -371,3 +373,25 @@ def deblur(op: BlurOperator, L: Smoother, g, mu: MuChoice, want_curve=False,
                           _ptr(restored), _ptr(mu_used), _ptr(bk) if mu.use_gcv else None,
                           _ptr(curve), _ptr(res), count, _stream()))
     return RestorationReport(restored, mu_used, bk if mu.use_gcv else None, curve, res)
+
+
+def deblur_host(op: BlurOperator, L: Smoother, g, mu: MuChoice, search: GcvSearch = GcvSearch(),
+                out=None, chunk=0):
+    """deblur for HOST arrays (the end-to-end entry point): chunks of the batch
+    stream through H2D copy -> deblur -> D2H copy on separate CUDA streams
+    (fd_deblur_host).  g: CPU float64 tensor [..., shape] (pinned for overlap).
+    Returns (restored, mu_used, best_k) as CPU tensors."""
+    if not isinstance(g, torch.Tensor):
+        g = torch.from_numpy(np.ascontiguousarray(np.asarray(g, dtype=np.float64)))
+    if g.is_cuda or g.dtype != torch.float64 or not g.is_contiguous():
+        raise ValidationError("deblur_host needs a contiguous CPU float64 tensor")
+    count, lead = op._count(g)
+    pin = g.is_pinned()
+    restored = torch.empty(g.shape, dtype=torch.float64, pin_memory=pin) if out is None else out
+    mu_used = torch.empty(lead, dtype=torch.float64, pin_memory=pin)
+    bk = torch.full(lead, -1, dtype=torch.int32)
+    check(lib().fd_deblur_host(op._h, L._h, _ptr(g), int(bool(mu.use_gcv)), float(mu.fixed_mu),
+                               float(search.mu_min), float(search.mu_max), int(search.count),
+                               _ptr(restored), _ptr(mu_used), _ptr(bk), count, int(chunk),
+                               _stream()))
+    return restored, mu_used, bk
