@@ -33,7 +33,6 @@ import sys
 import threading
 import time
 
-os.environ.setdefault("FASTDEBLUR_THREADS", "1")  # reference inner loops serial; outer pool
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -225,6 +224,10 @@ def main():
     rank, world, local = dist.init()
     cfg = W.config(args.config)
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    # reference threads: batched configs run an outer pool over
+    # items with serial inner loops; single-item configs use the library's own
+    # row/column and lambda-grid parallel_for with every core
+    os.environ.setdefault("FASTDEBLUR_THREADS", "1" if cfg.batch > 1 else str(cores))
 
     if args.impl == "reference":
         if rank == 0:

@@ -984,7 +984,15 @@ void gcv_direct(const GcvData& g, const double* mu_item, double* G, int* status,
   ProfScope ps("k_gcv_direct", S.st);
   k_gcv_direct<<<(int)((warps * 32 + 255) / 256), 256, 0, S.st>>>(g, mu_item, chunk, nch, part);
   launched("k_gcv_direct");
-  k_gcv_direct_reduce<<<(g.items + 255) / 256, 256, 0, S.st>>>(part, g.items, nch, G, status);
+  int nred = nch;
+  if (nch > 1) {
+    double* sums = S.get<double>((size_t)g.items * 2);
+    k_reduce_partials<<<dim3(g.items, 1), 256, 0, S.st>>>(part, nch, 2, sums);
+    launched("k_reduce_partials");
+    part = sums;
+    nred = 1;
+  }
+  k_gcv_direct_reduce<<<(g.items + 255) / 256, 256, 0, S.st>>>(part, g.items, nred, G, status);
   launched("k_gcv_direct_reduce");
 }
 
@@ -1050,6 +1058,14 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
     launch_grid(g, grid, sg, chunk, nch, part, S.st);
   }
   double* G = curve_out ? curve_out : S.get<double>((size_t)items * K);
+  if (nch > 1) {  // many element chunks per item: parallel fixed-order reduction first
+    double* sums = S.get<double>((size_t)items * 2 * K);
+    ProfScope ps("k_gcv_reduce_grid", S.st);
+    k_reduce_partials<<<dim3(items, (2 * K + 31) / 32), 256, 0, S.st>>>(part, nch, 2 * K, sums);
+    launched("k_reduce_partials");
+    part = sums;
+    nch = 1;
+  }
   {
     const long long tot = (long long)items * K;
     ProfScope ps("k_gcv_reduce_grid", S.st);
@@ -1067,10 +1083,18 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
 
   const int J = gcv_moment_terms(mu_min, mu_max, K);
   if (J > 0) {
-    const int nchm = pick_chunks(g.N, items, 1);
+    int nchm = pick_chunks(g.N, items, 1);
     const long long chunkm = (g.N + nchm - 1) / nchm;
     double* pm = S.get<double>((size_t)items * nchm * 2 * J);
     launch_moments(J, g, center, need, chunkm, nchm, pm, S.st);
+    if (nchm > 1) {
+      double* sums = S.get<double>((size_t)items * 2 * J);
+      ProfScope ps("k_gcv_moments", S.st);
+      k_reduce_partials<<<dim3(items, (2 * J + 31) / 32), 256, 0, S.st>>>(pm, nchm, 2 * J, sums);
+      launched("k_reduce_partials");
+      pm = sums;
+      nchm = 1;
+    }
     ProfScope ps("k_gcv_golden", S.st);
     k_gcv_golden<<<(items + 63) / 64, 64, 0, S.st>>>(pm, items, nchm, J, G, grid, bk, center,
                                                      need, mu_out);

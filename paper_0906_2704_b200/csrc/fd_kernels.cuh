@@ -1527,6 +1527,30 @@ __global__ void k_gcv_reduce_grid(const double* __restrict__ partial, int items,
   G[t] = num / (den * den);
 }
 
+// out[item][w] = sum_c partial[item][c][w], c = 0..nch-1, in a fixed order:
+// a CTA owns (item, 32 consecutive w); lane = w, warp = chunk residue mod 8,
+// then the 8 warp partials are added in warp order.  Coalesced over w.
+__global__ void __launch_bounds__(256) k_reduce_partials(const double* __restrict__ partial,
+                                                         int nch, int width, double* out) {
+  __shared__ double sm[8][33];
+  const int item = blockIdx.x;
+  const int w0 = blockIdx.y * 32;
+  const int lane = threadIdx.x & 31, cg = threadIdx.x >> 5;
+  const int w = w0 + lane;
+  double acc = 0.0;
+  if (w < width)
+    for (int c = cg; c < nch; c += 8)
+      acc += partial[((long long)item * nch + c) * width + w];
+  sm[cg][lane] = acc;
+  __syncthreads();
+  if (cg == 0 && w < width) {
+    double s = 0.0;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) s += sm[g][lane];
+    out[(long long)item * width + w] = s;
+  }
+}
+
 __global__ void k_gcv_pick(const double* __restrict__ G, int items, GcvGrid grid, double* mu_out,
                            int* best_k, double* center, int* need_refine) {
   const int item = blockIdx.x * blockDim.x + threadIdx.x;
