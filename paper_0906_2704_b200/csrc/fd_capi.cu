@@ -854,34 +854,32 @@ int pick_chunks(long long N, long long items, int sg) {
   return (int)std::max(1LL, nch);
 }
 
-template <int KC, int SG>
+template <int KC>
 void launch_grid_t(const GcvData& g, const GcvGrid& grid, long long chunk, int nch,
                    double* partial, cudaStream_t st) {
   const int K = grid.count;
-  const int groups = (g.items + SG - 1) / SG;
-  const long long warps = (long long)groups * nch;
+  const long long warps = (long long)g.items * nch;
   const int blocks = (int)((warps * 32 + 255) / 256);
   for (int kb = 0; kb < K; kb += 32 * KC) {
     ProfScope ps("k_gcv_grid", st);
-    k_gcv_grid<KC, SG><<<blocks, 256, 0, st>>>(g, grid, chunk, nch, kb, partial);
+    k_gcv_grid<KC><<<blocks, 256, 0, st>>>(g, grid, chunk, nch, kb, partial);
     launched("k_gcv_grid");
   }
 }
 
-void launch_grid(const GcvData& g, const GcvGrid& grid, int sg, long long chunk, int nch,
+void launch_grid(const GcvData& g, const GcvGrid& grid, long long chunk, int nch,
                  double* partial, cudaStream_t st) {
   const int K = grid.count;
-  const int kc = K <= 32 ? 1 : K <= 64 ? 2 : K <= 128 ? 4 : 8;
-#define FD_GRID(KCV)                                                         \
-  if (kc == KCV) {                                                           \
-    if (sg == 4)                                                             \
-      launch_grid_t<KCV, 4>(g, grid, chunk, nch, partial, st);               \
-    else                                                                     \
-      launch_grid_t<KCV, 1>(g, grid, chunk, nch, partial, st);               \
-    return;                                                                  \
-  }
-  FD_GRID(1) FD_GRID(2) FD_GRID(4) FD_GRID(8)
-#undef FD_GRID
+  if (K <= 32)
+    launch_grid_t<1>(g, grid, chunk, nch, partial, st);
+  else if (K <= 64)
+    launch_grid_t<2>(g, grid, chunk, nch, partial, st);
+  else if (K <= 128)
+    launch_grid_t<4>(g, grid, chunk, nch, partial, st);
+  else if (K <= 256)
+    launch_grid_t<8>(g, grid, chunk, nch, partial, st);
+  else
+    launch_grid_t<16>(g, grid, chunk, nch, partial, st);
 }
 
 size_t gemm_smem(int nj) {
@@ -1051,11 +1049,10 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
     part = S.get<double>((size_t)items * nch * 2 * K);
     launch_gemm(g, grid, echunk, nch, part, S.st);
   } else {
-    const int sg = 1;
-    nch = pick_chunks(g.N, items, sg);
+    nch = pick_chunks(g.N, items, 1);
     const long long chunk = (g.N + nch - 1) / nch;
     part = S.get<double>((size_t)items * nch * 2 * K);
-    launch_grid(g, grid, sg, chunk, nch, part, S.st);
+    launch_grid(g, grid, chunk, nch, part, S.st);
   }
   double* G = curve_out ? curve_out : S.get<double>((size_t)items * K);
   if (nch > 1) {  // many element chunks per item: parallel fixed-order reduction first

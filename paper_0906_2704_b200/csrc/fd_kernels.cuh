@@ -1171,77 +1171,87 @@ __device__ __forceinline__ double gcv_w(const GcvData& g, int item, long long e)
   return gcv_w1(g, base + e);
 }
 
-template <int KC, int SG>
+// 1/x for positive normal x: MUFU reciprocal seed + two Newton steps (<= 1 ulp)
+__device__ __forceinline__ double rcp_pos(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+// Single items / small batches: one warp per (item, element chunk); each lane
+// owns KC grid values.  Elements stream in tiles of 32 -- lane t loads and
+// forms (r, w) of element e0+t (coalesced, one division per element) -- and
+// are broadcast by shuffle; each lane's KC reciprocals share one reciprocal
+// (batch inversion).
+template <int KC>
 __global__ void __launch_bounds__(256) k_gcv_grid(GcvData g, GcvGrid grid, long long chunk,
-                                                  int nchunks, int kblock0, double* partial) {
+                                                  int nch, int kblock0, double* partial) {
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const int groups = (g.items + SG - 1) / SG;
-  if (warp_global >= groups * nchunks) return;
-  const int grp = warp_global / nchunks, ch = warp_global % nchunks;
+  if (warp_global >= g.items * nch) return;
+  const int item = warp_global / nch, ch = warp_global % nch;
   const int K = grid.count;
   const int k0 = kblock0 + lane * KC;
-
-  double mu[KC];
-#pragma unroll
-  for (int k = 0; k < KC; ++k) mu[k] = (k0 + k < K) ? grid.mus[k0 + k] : 1.0;
-  double num[SG][KC], den[KC];
+  double mu[KC], num[KC], den[KC];
 #pragma unroll
   for (int k = 0; k < KC; ++k) {
-    den[k] = 0.0;
-#pragma unroll
-    for (int p = 0; p < SG; ++p) num[p][k] = 0.0;
+    mu[k] = (k0 + k < K) ? grid.mus[k0 + k] : 1.0;
+    num[k] = den[k] = 0.0;
   }
   const long long e0 = (long long)ch * chunk;
   const long long e1 = min(g.N, e0 + chunk);
-  for (long long e = e0; e < e1; ++e) {
-    const double r = gcv_ratio(g, e);
-    if (isinf(r)) continue;
-    const double mult = gcv_mult(g, e);
-    double w[SG];
-#pragma unroll
-    for (int p = 0; p < SG; ++p) {
-      const int item = grp * SG + p;
-      w[p] = item < g.items ? gcv_w(g, item, e) : 0.0;
+  for (long long et = e0; et < e1; et += 32) {
+    const long long e = et + lane;
+    double rl = INFINITY, wl = 0.0, ml = 1.0;
+    if (e < e1) {
+      rl = gcv_ratio(g, e);
+      wl = gcv_w(g, item, e);
+      ml = gcv_mult(g, e);
     }
-    double sig[KC];
-    if (r < 1e30) {
-      double xk[KC], pre[KC];
+    const int cnt = (int)min(32LL, e1 - et);
+    for (int t = 0; t < cnt; ++t) {
+      const double r = __shfl_sync(0xffffffffu, rl, t);
+      const double w = __shfl_sync(0xffffffffu, wl, t);
+      const double mult = __shfl_sync(0xffffffffu, ml, t);
+      if (!(r < 1e30)) {
+        if (isinf(r)) continue;  // s = 0: sigma = 0
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+          const double s = 1.0 / (r + mu[k]);
+          den[k] = fma(mult, s, den[k]);
+          num[k] = fma(s * s, w, num[k]);
+        }
+        continue;
+      }
+      double xk[KC], pre[KC], sig[KC];
 #pragma unroll
       for (int k = 0; k < KC; ++k) xk[k] = r + mu[k];
       pre[0] = xk[0];
 #pragma unroll
       for (int k = 1; k < KC; ++k) pre[k] = pre[k - 1] * xk[k];
-      double inv = 1.0 / pre[KC - 1];
+      double inv = rcp_pos(pre[KC - 1]);
 #pragma unroll
       for (int k = KC - 1; k >= 1; --k) {
         sig[k] = inv * pre[k - 1];
-        inv = inv * xk[k];
+        inv *= xk[k];
       }
       sig[0] = inv;
-    } else {
 #pragma unroll
-      for (int k = 0; k < KC; ++k) sig[k] = 1.0 / (r + mu[k]);
-    }
-#pragma unroll
-    for (int k = 0; k < KC; ++k) {
-      den[k] = fma(mult, sig[k], den[k]);
-      const double s2 = sig[k] * sig[k];
-#pragma unroll
-      for (int p = 0; p < SG; ++p) num[p][k] = fma(s2, w[p], num[p][k]);
+      for (int k = 0; k < KC; ++k) {
+        den[k] = fma(mult, sig[k], den[k]);
+        num[k] = fma(sig[k] * sig[k], w, num[k]);
+      }
     }
   }
+  double* base = partial + ((long long)item * nch + ch) * 2 * K;
 #pragma unroll
-  for (int p = 0; p < SG; ++p) {
-    const int item = grp * SG + p;
-    if (item >= g.items) continue;
-    double* base = partial + ((long long)item * nchunks + ch) * 2 * K;
-#pragma unroll
-    for (int k = 0; k < KC; ++k) {
-      if (k0 + k < K) {
-        base[k0 + k] = num[p][k];
-        base[K + k0 + k] = den[k];
-      }
+  for (int k = 0; k < KC; ++k) {
+    if (k0 + k < K) {
+      base[k0 + k] = num[k];
+      base[K + k0 + k] = den[k];
     }
   }
 }
@@ -1324,7 +1334,7 @@ __global__ void __launch_bounds__(256) k_gcv_gemm(GcvData g, GcvGrid grid, int k
       pre[0] = x[0];
 #pragma unroll
       for (int t = 1; t < 4; ++t) pre[t] = pre[t - 1] * x[t];
-      double inv = 1.0 / pre[3];
+      double inv = rcp_pos(pre[3]);
 #pragma unroll
       for (int t = 3; t >= 1; --t) {
         sg[t] = inv * pre[t - 1];
@@ -1589,7 +1599,7 @@ __global__ void __launch_bounds__(256) k_gcv_moments(GcvData g, const double* __
     if (isinf(r)) continue;
     const double w = gcv_w(g, item, e);
     const double mult = gcv_mult(g, e);
-    const double t = 1.0 / (r + mc);
+    const double t = rcp_pos(r + mc);
     double p = t;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
