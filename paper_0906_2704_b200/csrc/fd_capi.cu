@@ -261,12 +261,33 @@ struct Axis {
   std::vector<double> q_host;
 };
 
+constexpr int kMaxOnChipM = 8192;  // 139 KB of complex fp64 in shared memory
+
+int num_sms() {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return nsm;
+}
+
 void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
   if (io.gi.count == 0) return;
   if (!io.in_cplx && ax.rhalf) {  // one real line per CTA, half-length DFT
     ProfScope ps("k_analyze", st);
+    if (ax.hfft.M > kMaxOnChipM) {  // split convolution, persistent CTAs + scratch
+      const int grid = std::min(io.gi.count, 2 * num_sms());
+      double2* scr = nullptr;
+      ck(cudaMallocAsync(&scr, (size_t)grid * 2 * ax.hfft.L * sizeof(double2), st), "scratch");
+      k_ranalyze<<<grid, 256, smem_bytes(ax.hfft.M / 2), st>>>(ax, io, scr);
+      launched("k_ranalyze");
+      ck(cudaFreeAsync(scr, st), "scratch");
+      return;
+    }
     k_ranalyze<<<io.gi.count, std::min(256, line_threads(ax.hfft.M)), smem_bytes(ax.hfft.M),
-                 st>>>(ax, io);
+                 st>>>(ax, io, nullptr);
     launched("k_ranalyze");
     return;
   }
@@ -281,8 +302,17 @@ void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cuda
   if (io.gi.count == 0) return;
   if (!io.out_cplx && ax.rhalf && (!ax.cplx || sa.resid2 == nullptr)) {
     ProfScope ps(sa.mode == 1 ? "k_synth_filter" : "k_synth", st);
+    if (ax.hfft.M > kMaxOnChipM) {
+      const int grid = std::min(io.gi.count, 2 * num_sms());
+      double2* scr = nullptr;
+      ck(cudaMallocAsync(&scr, (size_t)grid * 2 * ax.hfft.L * sizeof(double2), st), "scratch");
+      k_rsynth<<<grid, 256, smem_bytes(ax.hfft.M / 2), st>>>(ax, io, sa, scr);
+      launched("k_rsynth");
+      ck(cudaFreeAsync(scr, st), "scratch");
+      return;
+    }
     k_rsynth<<<io.gi.count, std::min(256, line_threads(ax.hfft.M)), smem_bytes(ax.hfft.M),
-               st>>>(ax, io, sa);
+               st>>>(ax, io, sa, nullptr);
     launched("k_rsynth");
     return;
   }
@@ -293,6 +323,12 @@ void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cuda
   ProfScope ps(sa.mode == 1 ? "k_synth_filter" : "k_synth", st);
   k_synth<<<blocks, line_threads(ax.fft.M), smem_bytes(ax.fft.M), st>>>(ax, io, sa);
   launched("k_synth");
+}
+
+__global__ void k_fill(double* p, long long n, double v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
 }
 
 Lines lines_1d(int n, long long count) {
@@ -325,7 +361,6 @@ void check_capacitance(const cplx m[4]) {  // boundary.cpp:139-150
     degenerate("degenerate transform: 2x2 capacitance matrix is singular or ill-conditioned");
 }
 
-constexpr int kMaxOnChipM = 8192;  // 139 KB of complex fp64 in shared memory
 
 FftTables make_fft_tables(int L, std::vector<std::unique_ptr<DevBuf>>& owner, int mdct,
                           double2* dct_tw) {
@@ -375,10 +410,10 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
   }
   // half-length real path (R even)
   d.rhalf = (L % 2 == 0) && L >= 2;
-  if (d.rhalf) {
+  if (d.rhalf) {  // split convolution (two halves of M/2) beyond the on-chip size
     int logM = 0;
     const int M = ceil_pow2(std::max((long long)L - 1, 2LL), &logM);
-    if (M > kMaxOnChipM) d.rhalf = 0;
+    if (M > 2 * kMaxOnChipM) d.rhalf = 0;
   }
   if (d.rhalf) {
     d.hfft = make_fft_tables(L / 2, A->bufs, d.fft.M ? 0 : (d.kind == IK_COS ? m : 0), dct_tw);
@@ -498,16 +533,22 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
       io2.in_cplx = 1;
       io2.out_cplx = 1;
       launch_analyze(iv, io2, 0);
-    } else {  // C^T c: real lines through the synthesis kernel
+    } else {  // C^T c: real lines through the (real-output) synthesis kernel
       std::vector<double> cr(2 * (size_t)m);
       for (int i = 0; i < 2 * m; ++i) cr[i] = cc[i].x;
       double* dcr = dev_upload(tmp, cr);
+      double* drr = dev_alloc<double>(tmp, 2 * (size_t)m);
       io2.in = dcr;
-      io2.out = dr;
+      io2.out = drr;
       io2.in_cplx = 0;
-      io2.out_cplx = 1;
+      io2.out_cplx = 0;
       SynthArgs sa{};
       launch_synth(iv, io2, sa, 0);
+      std::vector<double> hr(2 * (size_t)m);
+      ck(cudaMemcpy(hr.data(), drr, hr.size() * sizeof(double), cudaMemcpyDeviceToHost), "rows");
+      std::vector<double2> hc(2 * (size_t)m);
+      for (int i = 0; i < 2 * m; ++i) hc[i] = make_double2(hr[i], 0.0);
+      ck(cudaMemcpy(dr, hc.data(), hc.size() * sizeof(double2), cudaMemcpyHostToDevice), "rows");
     }
     std::vector<double2> rr(2 * (size_t)m);
     ck(cudaMemcpy(rr.data(), dr, rr.size() * sizeof(double2), cudaMemcpyDeviceToHost), "rows");
@@ -703,6 +744,12 @@ void run_synth(const fd_op* op, const fd_smoother* L, const void* in, void* out,
     sa.sp = spectral_of(op, L, false);
     sa.mu_item = mu_item;
     double* r2 = nullptr;
+    if (oc && !out_cplx && resid && !op->ax1->dev.fft.M) {
+      // lines beyond the exact complex path: real part only, residue not available
+      k_fill<<<1, 256, 0, S.st>>>(resid, count, NAN);
+      launched("k_fill");
+      resid = nullptr;
+    }
     if (oc && !out_cplx && resid) r2 = S.get<double>(count);
     sa.resid2 = r2;
     launch_synth(op->ax1->dev, io, sa, S.st);
@@ -1177,12 +1224,6 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
   }
   ck(cudaMemcpyAsync(mu_out, muh.data(), items * sizeof(double), cudaMemcpyHostToDevice, S.st),
      "mu out");
-}
-
-__global__ void k_fill(double* p, long long n, double v) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    p[i] = v;
 }
 
 void check_deblur_args(const fd_op* op, const fd_smoother* L, int use_gcv, double fixed_mu,

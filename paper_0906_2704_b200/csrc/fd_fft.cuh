@@ -94,11 +94,12 @@ __device__ __forceinline__ TwSm load_twiddles(double2* slots, const FftTables& T
 // size S (S >= 2^LOGR).  Items are disjoint element sets, so the pass is
 // in-place with no barrier inside.
 template <int LOGR>
-__device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S, const TwSm& tw) {
+__device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S, const TwSm& tw,
+                                         int Mtw) {
   constexpr int R = 1 << LOGR;
   const int SR = S >> LOGR;
   const int items = M >> LOGR;
-  const int twstep = M / S;
+  const int twstep = Mtw / S;  // tw is a table for size Mtw >= M
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int j0 = it & (SR - 1);
     const int base = (it - j0) * R + j0;
@@ -127,11 +128,12 @@ __device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S, 
 // Exact inverse (times 2 per stage) of dif_pass with conjugate twiddles: the
 // mirrored DIT pass of the backward transform.
 template <int LOGR>
-__device__ __forceinline__ void dit_pass(double2* __restrict__ x, int M, int S, const TwSm& tw) {
+__device__ __forceinline__ void dit_pass(double2* __restrict__ x, int M, int S, const TwSm& tw,
+                                         int Mtw) {
   constexpr int R = 1 << LOGR;
   const int SR = S >> LOGR;
   const int items = M >> LOGR;
-  const int twstep = M / S;
+  const int twstep = Mtw / S;  // tw is a table for size Mtw >= M
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int j0 = it & (SR - 1);
     const int base = (it - j0) * R + j0;
@@ -167,10 +169,10 @@ __device__ __forceinline__ void fft_dif(double2* x, int M, int logM, const TwSm&
   while (rem > 0) {
     const int l = pass_logr(rem);
     switch (l) {
-      case 4: dif_pass<4>(x, M, S, tw); break;
-      case 3: dif_pass<3>(x, M, S, tw); break;
-      case 2: dif_pass<2>(x, M, S, tw); break;
-      default: dif_pass<1>(x, M, S, tw); break;
+      case 4: dif_pass<4>(x, M, S, tw, M); break;
+      case 3: dif_pass<3>(x, M, S, tw, M); break;
+      case 2: dif_pass<2>(x, M, S, tw, M); break;
+      default: dif_pass<1>(x, M, S, tw, M); break;
     }
     S >>= l;
     rem -= l;
@@ -193,10 +195,10 @@ __device__ __forceinline__ void fft_dit(double2* x, int M, int logM, const TwSm&
     used -= l;
     const int S = M >> used;  // block size of pass p in the DIF sequence
     switch (l) {
-      case 4: dit_pass<4>(x, M, S, tw); break;
-      case 3: dit_pass<3>(x, M, S, tw); break;
-      case 2: dit_pass<2>(x, M, S, tw); break;
-      default: dit_pass<1>(x, M, S, tw); break;
+      case 4: dit_pass<4>(x, M, S, tw, M); break;
+      case 3: dit_pass<3>(x, M, S, tw, M); break;
+      case 2: dit_pass<2>(x, M, S, tw, M); break;
+      default: dit_pass<1>(x, M, S, tw, M); break;
     }
     __syncthreads();
   }
@@ -255,13 +257,14 @@ __device__ __forceinline__ void mid_pass(double2* __restrict__ x, int M,
   (void)tw;
 }
 
-// Bluestein core: x holds a_j = z_j c_j (j < L) and zeros up to M; on return
-// x_k holds the circular convolution (a * b)_k; the caller multiplies by c_k.
-// Requires a barrier before the call (the caller's loads); ends with one.
-__device__ __forceinline__ void bluestein_core(double2* x, const FftTables& T, const TwSm& tw) {
-  const int M = T.M, logM = T.logM;
+// Convolution with DIF(b)/M on a local block of Mloc points whose twiddles are
+// those of size Mtw (Mloc = Mtw for an ordinary convolution; Mloc = Mtw/2 for
+// one half of a split convolution, see bluestein_core).  bhat points at the
+// Mloc entries of this block.  Requires a barrier before; ends with one.
+__device__ __forceinline__ void bluestein_run(double2* x, int M, int logM, int Mtw,
+                                              const double2* bhat, const TwSm& tw) {
   if (logM == 0) {
-    if (threadIdx.x == 0) x[0] = cmul(x[0], __ldg(&T.bhat[0]));
+    if (threadIdx.x == 0) x[0] = cmul(x[0], bhat[0]);
     __syncthreads();
     return;
   }
@@ -272,36 +275,58 @@ __device__ __forceinline__ void bluestein_core(double2* x, const FftTables& T, c
     ls[np++] = l;
     rem -= l;
   }
-  // DIF passes 0 .. np-2
   int S = M;
   for (int p = 0; p < np - 1; ++p) {
     switch (ls[p]) {
-      case 4: dif_pass<4>(x, M, S, tw); break;
-      case 3: dif_pass<3>(x, M, S, tw); break;
-      case 2: dif_pass<2>(x, M, S, tw); break;
-      default: dif_pass<1>(x, M, S, tw); break;
+      case 4: dif_pass<4>(x, M, S, tw, Mtw); break;
+      case 3: dif_pass<3>(x, M, S, tw, Mtw); break;
+      case 2: dif_pass<2>(x, M, S, tw, Mtw); break;
+      default: dif_pass<1>(x, M, S, tw, Mtw); break;
     }
     S >>= ls[p];
     __syncthreads();
   }
   switch (ls[np - 1]) {  // S == 2^ls[np-1] here
-    case 4: mid_pass<4>(x, M, T.bhat, tw); break;
-    case 3: mid_pass<3>(x, M, T.bhat, tw); break;
-    case 2: mid_pass<2>(x, M, T.bhat, tw); break;
-    default: mid_pass<1>(x, M, T.bhat, tw); break;
+    case 4: mid_pass<4>(x, M, bhat, tw); break;
+    case 3: mid_pass<3>(x, M, bhat, tw); break;
+    case 2: mid_pass<2>(x, M, bhat, tw); break;
+    default: mid_pass<1>(x, M, bhat, tw); break;
   }
   __syncthreads();
-  // DIT passes np-2 .. 0
   for (int p = np - 2; p >= 0; --p) {
     S <<= ls[p];
     switch (ls[p]) {
-      case 4: dit_pass<4>(x, M, S, tw); break;
-      case 3: dit_pass<3>(x, M, S, tw); break;
-      case 2: dit_pass<2>(x, M, S, tw); break;
-      default: dit_pass<1>(x, M, S, tw); break;
+      case 4: dit_pass<4>(x, M, S, tw, Mtw); break;
+      case 3: dit_pass<3>(x, M, S, tw, Mtw); break;
+      case 2: dit_pass<2>(x, M, S, tw, Mtw); break;
+      default: dit_pass<1>(x, M, S, tw, Mtw); break;
     }
     __syncthreads();
   }
+}
+
+// Bluestein core: x holds a_j = z_j c_j (j < L) and zeros up to M; on return
+// x_k holds the circular convolution (a * b)_k; the caller multiplies by c_k.
+// Requires a barrier before the call (the caller's loads); ends with one.
+__device__ __forceinline__ void bluestein_core(double2* x, const FftTables& T, const TwSm& tw) {
+  bluestein_run(x, T.M, T.logM, T.M, T.bhat, tw);
+}
+
+// Split convolution for M beyond shared memory (M = 2 * Mloc).  The input a
+// is supported on [0, L) with L <= M/2, so the first DIF stage degenerates to
+// upper = lower (.) W_M^t and the last DIT stage only has to produce the lower
+// half: out[t] = y0[t] + conj(W_M^t) y1[t], where y_p is the half-size
+// convolution of half p (DIF(b)/M entries [p Mloc, (p+1) Mloc)).
+//   part 1: x = a (.) W^t  ->  y1   (caller saves y1)
+//   part 0: x = a          ->  y0   (caller combines)
+__device__ __forceinline__ void bluestein_half(double2* x, const FftTables& T, const TwSm& tw,
+                                               int part) {
+  const int Mloc = T.M >> 1;
+  if (part == 1) {
+    for (int j = threadIdx.x; j < Mloc; j += blockDim.x) x[pidx(j)] = cmul(x[pidx(j)], tw(j));
+    __syncthreads();
+  }
+  bluestein_run(x, Mloc, T.logM - 1, T.M, T.bhat + part * Mloc, tw);
 }
 
 // ----------------------------------------------------------------------------

@@ -786,16 +786,21 @@ __device__ __forceinline__ int makhoul_src(int p, int m, int half) {
   return p < half ? 2 * p : 2 * (m - 1 - p) + 1;  // trig.cpp:194-195
 }
 
-__global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io) {
+// scr != null: split-convolution mode for M beyond shared memory
+// (bluestein_half), persistent over lines, 2h complex of per-CTA scratch.
+__global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, double2* scr) {
   extern __shared__ double2 sm[];
   const FftTables& T = ax.hfft;
   const int M = T.M, h = T.L;
+  const bool big = scr != nullptr;
+  const int Mloc = big ? M / 2 : M;
   double2* x = sm;
-  const TwSm tw = load_twiddles(sm + pidx(M) + 1, T);
-  double* red = reinterpret_cast<double*>(sm + pidx(M) + 1 + kTwSlots);
+  const TwSm tw = load_twiddles(sm + pidx(Mloc) + 1, T);
+  double* red = reinterpret_cast<double*>(sm + pidx(Mloc) + 1 + kTwSlots);
   double2* bcs = reinterpret_cast<double2*>(red + 32 * 4);
-  const int l = blockIdx.x;
-  if (l >= io.gi.count) return;
+  double2* scrA = big ? scr + (long long)blockIdx.x * 2 * h : nullptr;
+  double2* scrY = big ? scrA + h : nullptr;
+  for (int l = blockIdx.x; l < io.gi.count; l += gridDim.x) {
   const long long oi = line_offset(io.gi, l), es = io.gi.elem_stride;
   const int n = ax.n, m = ax.m;
   const double2* chirp = T.chirp;
@@ -809,7 +814,7 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io) {
   const bool dots = ax.bordered && ax.correction;
   const int half = (m + 1) / 2;
   double acc[4] = {0, 0, 0, 0};  // ra (re, im), rb (re, im)
-  for (int j = h + threadIdx.x; j < M; j += blockDim.x) x[pidx(j)] = czero();
+  for (int j = h + threadIdx.x; j < Mloc; j += blockDim.x) x[pidx(j)] = czero();
 #pragma unroll 4
   for (int j = threadIdx.x; j < h; j += blockDim.x) {
     double2 val = czero();
@@ -870,7 +875,24 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io) {
   }
   __syncthreads();
 
-  bluestein_core(x, T, tw);
+  if (!big) {
+    bluestein_core(x, T, tw);
+  } else {
+    for (int j = threadIdx.x; j < h; j += blockDim.x) scrA[j] = x[pidx(j)];
+    bluestein_half(x, T, tw, 1);  // x = a (.) W, convolved: y1
+    for (int j = threadIdx.x; j < h; j += blockDim.x) {
+      scrY[j] = x[pidx(j)];
+      x[pidx(j)] = scrA[j];
+    }
+    for (int j = h + threadIdx.x; j < Mloc; j += blockDim.x) x[pidx(j)] = czero();
+    __syncthreads();
+    bluestein_half(x, T, tw, 0);  // y0
+  }
+  // Z_k = (a * b)_k c_k; in split mode the lower half of the last DIT stage
+  auto zv = [&](int k) {
+    const double2 y = big ? cadd(x[pidx(k)], cmulc(scrY[k], tw(k))) : x[pidx(k)];
+    return cmul(y, __ldg(&chirp[k]));
+  };
 
   const double2 b0 = bcs[0], b1 = bcs[1];
   const long long oo = line_offset(io.go, l), eso = io.go.elem_stride;
@@ -907,8 +929,8 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io) {
     const int off = ax.bordered ? 1 : 0;
     for (int k = threadIdx.x; k <= h / 2; k += blockDim.x) {
       const int kp = k == 0 ? 0 : h - k;
-      const double2 Zk = cmul(x[pidx(k)], __ldg(&chirp[k]));
-      const double2 Zp = cmul(x[pidx(kp)], __ldg(&chirp[kp]));
+      const double2 Zk = zv(k);
+      const double2 Zp = zv(kp);
       const double2 E = cscale(cadd(Zk, cconj(Zp)), 0.5);
       const double2 D = csub(Zk, cconj(Zp));
       const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
@@ -940,8 +962,8 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io) {
   } else {
     for (int k = threadIdx.x; k < h; k += blockDim.x) {
       const int kc = k == 0 ? 0 : h - k;
-      const double2 Zk = cmul(x[pidx(k)], __ldg(&chirp[k]));
-      const double2 Zc = cconj(cmul(x[pidx(kc)], __ldg(&chirp[kc])));
+      const double2 Zk = zv(k);
+      const double2 Zc = cconj(zv(kc));
       const double2 E = cscale(cadd(Zk, Zc), 0.5);
       const double2 D = csub(Zk, Zc);
       const double2 WO = cmul(__ldg(&ax.rtw[k]), make_double2(0.5 * D.y, -0.5 * D.x));
@@ -974,17 +996,24 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io) {
       }
     }
   }
+  __syncthreads();  // x, bcs and the scratch are reused by the next line
+  }
 }
 
-__global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthArgs sa) {
+// scr != null: split-convolution mode (see k_ranalyze)
+__global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthArgs sa,
+                                                   double2* scr) {
   extern __shared__ double2 sm[];
   const FftTables& T = ax.hfft;
   const int M = T.M, h = T.L;
+  const bool big = scr != nullptr;
+  const int Mloc = big ? M / 2 : M;
   double2* x = sm;
-  const TwSm tw = load_twiddles(sm + pidx(M) + 1, T);
-  double* red = reinterpret_cast<double*>(sm + pidx(M) + 1 + kTwSlots);
-  const int l = blockIdx.x;
-  if (l >= io.gi.count) return;
+  const TwSm tw = load_twiddles(sm + pidx(Mloc) + 1, T);
+  double* red = reinterpret_cast<double*>(sm + pidx(Mloc) + 1 + kTwSlots);
+  double2* scrA = big ? scr + (long long)blockIdx.x * 2 * h : nullptr;
+  double2* scrY = big ? scrA + h : nullptr;
+  for (int l = blockIdx.x; l < io.gi.count; l += gridDim.x) {
   const long long oi = line_offset(io.gi, l);
   const int n = ax.n, m = ax.m;
   const double2* chirp = T.chirp;
@@ -998,7 +1027,7 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
   double acc[4] = {0, 0, 0, 0};  // top (re, im), bottom (re, im)
   if (ax.kind == IK_SINE) {  // Q c_mid: R2C of the odd extension (Q is an involution)
     const int R = 2 * (m + 1);
-    for (int j = threadIdx.x; j < M; j += blockDim.x) {
+    for (int j = threadIdx.x; j < Mloc; j += blockDim.x) {
       double2 val = czero();
       if (j < h) {
         auto ext = [&](int p) -> double {
@@ -1012,56 +1041,92 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
     }
     __syncthreads();
   } else {
-    // stage the (filtered) coefficients: cosine stores conj(buf_i) = s_i c_i conj(tw_i)
+    // cosine works on conj(buf_i) = s_i c_i conj(tw_i) (DCT-III, trig.cpp:201-212)
     const double s0 = sqrt(1.0 / (double)m), s1 = sqrt(2.0 / (double)m);
-#pragma unroll 4
-    for (int i = threadIdx.x; i < m; i += blockDim.x) {
-      const double2 c = cf(interior_elem(ax, i));
-      double2 val;
+    auto prep = [&](int i, double2 c) {
       if (ax.kind == IK_COS) {
         const double2 t = __ldg(&ax.dct_tw[i]);
         const double ts = (i == 0 ? s0 : s1) * c.x;
-        val = make_double2(ts * t.x, -(ts * t.y));
-        if (dots) {
-          acc[0] += __ldg(&ax.c_a[i]).x * c.x;
-          acc[2] += __ldg(&ax.c_b[i]).x * c.x;
-        }
-      } else {
-        val = c;
-        if (dots) {
-          const double2 t0 = cmul(__ldg(&ax.c_a[i]), c), t1 = cmul(__ldg(&ax.c_b[i]), c);
-          acc[0] += t0.x, acc[1] += t0.y, acc[2] += t1.x, acc[3] += t1.y;
-        }
+        return make_double2(ts * t.x, -(ts * t.y));
       }
-      x[pidx(i)] = val;
-    }
-    __syncthreads();
-    // C2R pre-pass over the closed index groups {k, h-k}: X = herm(staged),
-    // Zin_k = (X_k + X_{k+h}) + i (X_k - X_{k+h}) W^{-k}; Bluestein input conj(Zin) c_k
-    auto herm = [&](int q) {
-      const int qc = q == 0 ? 0 : m - q;
-      return cscale(cadd(x[pidx(q)], cconj(x[pidx(qc)])), 0.5);
+      return c;
     };
-    auto zin = [&](int k) {
-      const double2 Xa = herm(k), Xb = herm(k + h);
-      const double2 Od = cmulc(csub(Xa, Xb), __ldg(&ax.rtw[k]));
-      const double2 Ev = cadd(Xa, Xb);
-      return make_double2(Ev.x - Od.y, Ev.y + Od.x);
+    auto dot = [&](int i, double2 c) {
+      if (ax.kind == IK_COS) {
+        acc[0] += __ldg(&ax.c_a[i]).x * c.x;
+        acc[2] += __ldg(&ax.c_b[i]).x * c.x;
+      } else {
+        const double2 t0 = cmul(__ldg(&ax.c_a[i]), c), t1 = cmul(__ldg(&ax.c_b[i]), c);
+        acc[0] += t0.x, acc[1] += t0.y, acc[2] += t1.x, acc[3] += t1.y;
+      }
+    };
+    if (!big) {  // stage the (filtered) coefficients in shared memory
+#pragma unroll 4
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        const double2 c = cf(interior_elem(ax, i));
+        if (dots) dot(i, c);
+        x[pidx(i)] = prep(i, c);
+      }
+      __syncthreads();
+    }
+    // C2R pre-pass over the closed index groups {k, h-k}: X = herm(staged),
+    // Zin_k = (X_k + X_{k+h}) + i (X_k - X_{k+h}) W^{-k}; Bluestein input conj(Zin) c_k.
+    // Split mode reads the group's four coefficients from global memory.
+    auto val_at = [&](int q) {
+      if (!big) return x[pidx(q)];
+      return prep(q, cf(interior_elem(ax, q)));
     };
     for (int k = threadIdx.x; k <= h / 2; k += blockDim.x) {
       const int kp = k == 0 ? 0 : h - k;
-      const double2 za = zin(k);
-      const double2 zb = zin(kp);
+      // group indices: k, kp (lower), k + h, kp + h = m - k (upper)
+      const double2 vk = val_at(k), vkh = val_at(k + h);
+      const double2 vp = kp != k ? val_at(kp) : vk, vph = kp != k ? val_at(kp + h) : vkh;
+      if (big && dots) {
+        dot(k, cf(interior_elem(ax, k)));
+        dot(k + h, cf(interior_elem(ax, k + h)));
+        if (kp != k) {
+          dot(kp, cf(interior_elem(ax, kp)));
+          dot(kp + h, cf(interior_elem(ax, kp + h)));
+        }
+      }
+      // herm(q) = (v_q + conj v_{m-q})/2: m-k = kp+h, m-(k+h) = kp (k = 0: m-0 -> 0, m-h = h)
+      const double2 Xk = cscale(cadd(vk, cconj(k == 0 ? vk : vph)), 0.5);
+      const double2 Xkh = cscale(cadd(vkh, cconj(k == 0 ? vkh : vp)), 0.5);
+      const double2 Xp = cscale(cadd(vp, cconj(k == 0 ? vp : vkh)), 0.5);
+      const double2 Xph = cscale(cadd(vph, cconj(k == 0 ? vph : vk)), 0.5);
+      auto zin = [&](int kk, double2 Xa, double2 Xb) {
+        const double2 Od = cmulc(csub(Xa, Xb), __ldg(&ax.rtw[kk]));
+        const double2 Ev = cadd(Xa, Xb);
+        return make_double2(Ev.x - Od.y, Ev.y + Od.x);
+      };
+      const double2 za = zin(k, Xk, Xkh);
+      const double2 zb = zin(kp, Xp, Xph);
       x[pidx(k)] = cmul(cconj(za), __ldg(&chirp[k]));
       if (kp != k) x[pidx(kp)] = cmul(cconj(zb), __ldg(&chirp[kp]));
     }
     __syncthreads();
-    for (int j = h + threadIdx.x; j < M; j += blockDim.x) x[pidx(j)] = czero();
+    for (int j = h + threadIdx.x; j < Mloc; j += blockDim.x) x[pidx(j)] = czero();
     __syncthreads();
   }
   if (dots) block_sum<4>(acc, red);
 
-  bluestein_core(x, T, tw);
+  if (!big) {
+    bluestein_core(x, T, tw);
+  } else {
+    for (int j = threadIdx.x; j < h; j += blockDim.x) scrA[j] = x[pidx(j)];
+    bluestein_half(x, T, tw, 1);
+    for (int j = threadIdx.x; j < h; j += blockDim.x) {
+      scrY[j] = x[pidx(j)];
+      x[pidx(j)] = scrA[j];
+    }
+    for (int j = h + threadIdx.x; j < Mloc; j += blockDim.x) x[pidx(j)] = czero();
+    __syncthreads();
+    bluestein_half(x, T, tw, 0);
+  }
+  auto zv = [&](int k) {
+    const double2 y = big ? cadd(x[pidx(k)], cmulc(scrY[k], tw(k))) : x[pidx(k)];
+    return cmul(y, __ldg(&chirp[k]));
+  };
 
   const long long oo = line_offset(io.go, l), eso = io.go.elem_stride;
   auto put = [&](int p, double val) {  // interior position p of the output line
@@ -1074,8 +1139,8 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
     const double sc = -0.5 * sqrt(2.0 / ((double)m + 1.0));
     for (int k = 1 + threadIdx.x; k < h; k += blockDim.x) {
       const int kc = h - k;
-      const double2 Zk = cmul(x[pidx(k)], __ldg(&chirp[k]));
-      const double2 Zc = cconj(cmul(x[pidx(kc)], __ldg(&chirp[kc])));
+      const double2 Zk = zv(k);
+      const double2 Zc = cconj(zv(kc));
       const double2 E = cscale(cadd(Zk, Zc), 0.5);
       const double2 D = csub(Zk, Zc);
       const double2 WO = cmul(__ldg(&ax.rtw[k]), make_double2(0.5 * D.y, -0.5 * D.x));
@@ -1085,7 +1150,7 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
     const double inv_sqrt_m = 1.0 / sqrt((double)m);
     const int half = (m + 1) / 2;
     for (int j = threadIdx.x; j < h; j += blockDim.x) {
-      const double2 z = cconj(cmul(x[pidx(j)], __ldg(&chirp[j])));
+      const double2 z = cconj(zv(j));
       if (ax.kind == IK_COS) {  // spec[p] -> out[2p] (p < half) or out[2(m-1-p)+1]
         const int p0 = 2 * j, p1 = 2 * j + 1;
         put(p0 < half ? 2 * p0 : 2 * (m - 1 - p0) + 1, z.x);
@@ -1101,6 +1166,8 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
     const double2 top = make_double2(acc[0], acc[1]), bot = make_double2(acc[2], acc[3]);
     stc(io.out, 0, oo, make_double2(q0 * u0.x + top.x, 0.0));
     stc(io.out, 0, oo + (long long)(n - 1) * eso, make_double2(bot.x + q0 * un.x, 0.0));
+  }
+  __syncthreads();  // x and the scratch are reused by the next line
   }
 }
 

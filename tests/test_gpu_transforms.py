@@ -112,3 +112,44 @@ def test_polynomial_preservation(bc, psf, degs, tol):
         got, res = op.apply(torch.from_numpy(f))
         assert rel(np_(got), f) < tol
         assert float(np_(res)) <= 1e-10 * (1.0 + np.linalg.norm(f))
+
+
+@pytest.mark.parametrize("bc", [O.HOC_COSINE, O.REFLECTIVE, O.HOC_FOURIER, O.PERIODIC])
+@pytest.mark.parametrize("n", [8194, 16384])
+def test_split_convolution_lines(bc, n, rng):
+    """Lines whose half-length Bluestein size exceeds shared memory (config 4:
+    interior DCT length 16382 = 2 * 8191) run as two half convolutions."""
+    psf = gauss(16, 4.0) if bc in (O.HOC_COSINE, O.REFLECTIVE) else onesided(15, 0.2)
+    op = P.build_operator(psf, n, bc)
+    oop = O.build_operator(O.make_psf(psf, True), n, bc)
+    b = oop.basis
+    x = np.cumsum(rng.standard_normal((2, n)), axis=-1) / 50
+    got = np_(op.analyze(torch.from_numpy(x)))
+    want = b.analyze(x.astype(complex) if b.complex else x)
+    assert rel(got, want) < 1e-9
+    L = P.smoothing_eigenvalues("laplacian", op)
+    s = O.smoothing_eigenvalues(O.LAPLACIAN, bc, n, oop.eigenvalues)
+    for mu in (1e-6, 1e-2):
+        f, _ = P.tikhonov_solve(op, L, torch.from_numpy(x), mu)
+        assert rel(np_(f), O.tikhonov_solve(oop, s, x, mu)[0]) < 1e-10
+    if not b.complex:
+        c = rng.standard_normal((3, n))
+        assert rel(np_(op.synthesize(torch.from_numpy(c))[0]), b.synthesize(c)) < 1e-12
+
+
+def test_split_convolution_2d_columns(rng):
+    """2D operator whose column lines (n1 = 16384) need the split convolution."""
+    n1, n2 = 16384, 40
+    a, bb = gauss(16, 4.0), gauss(2, 1.0)
+    op = P.build_operator_2d_separable(a, bb, n1, n2, "hoc-cosine")
+    p = O.separable_psf2d(O.make_psf(a, True), O.make_psf(bb, True))
+    oop = O.build_operator_2d(p, n1, n2, O.HOC_COSINE, separable=True)
+    f = rng.standard_normal((n1, n2))
+    got, _ = op.apply(torch.from_numpy(f))
+    assert rel(np_(got), oop.apply(f)[0]) < 1e-10
+    L = P.smoothing_eigenvalues("laplacian", op)
+    s = O.smoothing_eigenvalues_2d(O.LAPLACIAN, O.HOC_COSINE, n1, n2)
+    rep = P.deblur(op, L, torch.from_numpy(f), P.MuChoice(True), search=P.GcvSearch(1e-8, 1, 64))
+    w = O.deblur_2d(oop, s, f, True, mu_min=1e-8, mu_max=1.0, count=64)
+    assert int(np_(rep.best_k)) == int(w.best_k)
+    assert rel(np_(rep.restored), w.restored) < 1e-10
