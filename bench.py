@@ -258,8 +258,13 @@ def main():
     else:
         shape = (batch, cfg.n1, cfg.n2)
         g_host = torch.empty(shape, dtype=torch.float64).pin_memory()
-        for i in range(batch):
-            g_host[i] = torch.from_numpy(W.image_2d(cfg, first + i)[1])
+        from concurrent.futures import ProcessPoolExecutor
+        import multiprocessing as mp
+        jobs = [(cfg.index, first + i) for i in range(batch)]
+        with ProcessPoolExecutor(max_workers=max(1, min(cores, 16, batch)),
+                                 mp_context=mp.get_context("fork")) as ex:
+            for (ci, it), arr in zip(jobs, ex.map(_gen_2d, jobs)):
+                g_host[it - first] = torch.from_numpy(arr)
         op = P.build_operator_2d_separable(cfg.psf, cfg.psf, cfg.n1, cfg.n2, cfg.bc)
     L = P.smoothing_eigenvalues(SMOOTHER_NAMES[smoother], op)
     g_dev = g_host.to(dev)
@@ -386,6 +391,11 @@ def main():
         }
         print(json.dumps(line), flush=True)
     dist.finalize()
+
+
+def _gen_2d(job):
+    ci, it = job
+    return W.image_2d(W.config(ci), it)[1]
 
 
 def _gen_1d(job):

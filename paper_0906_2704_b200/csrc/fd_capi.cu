@@ -245,6 +245,8 @@ int ceil_pow2(long long v, int* logv) {
   return (int)p;
 }
 
+constexpr int kMaxOnChipM = 8192;  // 139 KB of complex fp64 in shared memory
+
 size_t smem_bytes(int M) {
   return (size_t)(pidx(M) + 1 + kTwSlots) * sizeof(double2) + 32 * 8 * 8 + 8 * 16;
 }
@@ -260,8 +262,6 @@ struct Axis {
   std::vector<std::unique_ptr<DevBuf>> bufs;
   std::vector<double> q_host;
 };
-
-constexpr int kMaxOnChipM = 8192;  // 139 KB of complex fp64 in shared memory
 
 int num_sms() {
   static int nsm = 0;
@@ -381,8 +381,15 @@ FftTables make_fft_tables(int L, std::vector<std::unique_ptr<DevBuf>>& owner, in
   k_init_tables<<<std::max(1, std::min(1024, (M + 255) / 256)), 256>>>(L, M, chirp, tw, b, mdct,
                                                                        dct_tw);
   launched("k_init_tables");
-  k_bhat<<<1, line_threads(M), smem_bytes(M)>>>(T, b, bhat);
-  launched("k_bhat");
+  if (M <= kMaxOnChipM) {
+    k_bhat<<<1, line_threads(M), smem_bytes(M)>>>(T, b, bhat, -1);
+    launched("k_bhat");
+  } else {
+    for (int part = 0; part < 2; ++part) {
+      k_bhat<<<1, line_threads(M / 2), smem_bytes(M / 2)>>>(T, b, bhat, part);
+      launched("k_bhat");
+    }
+  }
   ck(cudaDeviceSynchronize(), "fft tables");
   return T;
 }
@@ -527,12 +534,38 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
     LineIO io2{};
     io2.gi = lines_1d(m, 2);
     io2.go = lines_1d(m, 2);
-    if (d.cplx) {  // F c (complex input, one line per CTA)
+    if (d.cplx && d.fft.M) {  // F c (complex input, one line per CTA)
       io2.in = dc;
       io2.out = dr;
       io2.in_cplx = 1;
       io2.out_cplx = 1;
       launch_analyze(iv, io2, 0);
+    } else if (d.cplx) {  // F c = F Re c + i F Im c through the real-line path
+      std::vector<double> parts(4 * (size_t)m);
+      for (int i = 0; i < m; ++i) {
+        parts[i] = cc[i].x;
+        parts[m + i] = cc[i].y;
+        parts[2 * m + i] = cc[m + i].x;
+        parts[3 * m + i] = cc[m + i].y;
+      }
+      double* dp = dev_upload(tmp, parts);
+      double2* dx4 = dev_alloc<double2>(tmp, 4 * (size_t)m);
+      LineIO io4{};
+      io4.in = dp;
+      io4.out = dx4;
+      io4.gi = lines_1d(m, 4);
+      io4.go = lines_1d(m, 4);
+      io4.in_cplx = 0;
+      io4.out_cplx = 1;
+      launch_analyze(iv, io4, 0);
+      std::vector<double2> h4(4 * (size_t)m), hr(2 * (size_t)m);
+      ck(cudaMemcpy(h4.data(), dx4, h4.size() * sizeof(double2), cudaMemcpyDeviceToHost), "F c");
+      for (int t = 0; t < 2; ++t)
+        for (int i = 0; i < m; ++i) {
+          const double2 re = h4[(2 * t) * m + i], im = h4[(2 * t + 1) * m + i];
+          hr[t * m + i] = make_double2(re.x - im.y, re.y + im.x);
+        }
+      ck(cudaMemcpy(dr, hr.data(), hr.size() * sizeof(double2), cudaMemcpyHostToDevice), "F c");
     } else {  // C^T c: real lines through the (real-output) synthesis kernel
       std::vector<double> cr(2 * (size_t)m);
       for (int i = 0; i < 2 * m; ++i) cr[i] = cc[i].x;

@@ -180,6 +180,25 @@ __device__ __forceinline__ void fft_dif(double2* x, int M, int logM, const TwSm&
   }
 }
 
+// DIF passes over a local block of M points with twiddles of size Mtw.
+__device__ __forceinline__ void fft_dif_local(double2* x, int M, int logM, int Mtw,
+                                              const TwSm& tw) {
+  int S = M;
+  int rem = logM;
+  while (rem > 0) {
+    const int l = pass_logr(rem);
+    switch (l) {
+      case 4: dif_pass<4>(x, M, S, tw, Mtw); break;
+      case 3: dif_pass<3>(x, M, S, tw, Mtw); break;
+      case 2: dif_pass<2>(x, M, S, tw, Mtw); break;
+      default: dif_pass<1>(x, M, S, tw, Mtw); break;
+    }
+    S >>= l;
+    rem -= l;
+    __syncthreads();
+  }
+}
+
 // Backward DIT FFT (sign +1, unnormalised), digit-reversed in, natural out.
 __device__ __forceinline__ void fft_dit(double2* x, int M, int logM, const TwSm& tw) {
   int ls[8];

@@ -119,16 +119,32 @@ __global__ void k_init_rtw(int R, double2* rtw) {
   }
 }
 
-// bhat = DIF_M(b)/M, left in DIF (digit-reversed) order
+// bhat = DIF_M(b)/M, left in DIF (digit-reversed) order.  part < 0: the whole
+// transform in shared memory; part 0/1: half p of a split DIF for M beyond
+// shared memory (first stage lower = b_lo + b_hi, upper = (b_lo - b_hi) W^t,
+// then a local DIF of size M/2), writing bhat[p M/2, (p+1) M/2).
 __global__ void __launch_bounds__(512) k_bhat(FftTables T, const double2* __restrict__ b,
-                                              double2* bhat) {
+                                              double2* bhat, int part) {
   extern __shared__ double2 sm[];
-  const TwSm tw = load_twiddles(sm + pidx(T.M) + 1, T);
-  for (int j = threadIdx.x; j < T.M; j += blockDim.x) sm[pidx(j)] = b[j];
+  const int Mloc = part < 0 ? T.M : T.M / 2;
+  const int logMloc = part < 0 ? T.logM : T.logM - 1;
+  const TwSm tw = load_twiddles(sm + pidx(Mloc) + 1, T);
   __syncthreads();
-  fft_dif(sm, T.M, T.logM, tw);
+  for (int j = threadIdx.x; j < Mloc; j += blockDim.x) {
+    double2 v;
+    if (part < 0) {
+      v = b[j];
+    } else {
+      const double2 lo = b[j], hi = b[j + Mloc];
+      v = part == 0 ? cadd(lo, hi) : cmul(csub(lo, hi), tw(j));
+    }
+    sm[pidx(j)] = v;
+  }
+  __syncthreads();
+  fft_dif_local(sm, Mloc, logMloc, T.M, tw);
   const double inv = 1.0 / (double)T.M;
-  for (int j = threadIdx.x; j < T.M; j += blockDim.x) bhat[j] = cscale(sm[pidx(j)], inv);
+  const int off = part < 0 ? 0 : part * Mloc;
+  for (int j = threadIdx.x; j < Mloc; j += blockDim.x) bhat[off + j] = cscale(sm[pidx(j)], inv);
 }
 
 // symbol z(t) = sum_j h_j e^{ijt} (psf.cpp:39-52)
