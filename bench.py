@@ -104,7 +104,10 @@ def reference_deblur_sample(cfg, first, count, threads):
         t0 = time.perf_counter()
         O.deblur(op, s, g, True, mu_min=cfg.mu_min, mu_max=cfg.mu_max, count=cfg.count)
         return time.perf_counter() - t0, "port", 1
-    imgs = np.stack([W.image_2d(cfg, first + i)[1] for i in range(count)])
+    if cfg.n1 * cfg.n2 >= 1 << 26:
+        imgs = np.stack([W.image_2d_large(cfg.index, first + i) for i in range(count)])
+    else:
+        imgs = np.stack([W.image_2d(cfg, first + i)[1] for i in range(count)])
     if R.available():
         t0 = time.perf_counter()
         R.deblur_2d(cfg.psf2d(), cfg.bc, smoother, imgs, True, mu_min=cfg.mu_min,
@@ -261,6 +264,10 @@ def main():
         from concurrent.futures import ProcessPoolExecutor
         import multiprocessing as mp
         jobs = [(cfg.index, first + i) for i in range(batch)]
+        if cfg.n1 * cfg.n2 >= 1 << 26:  # config 4: band-parallel generator
+            for i, (ci, it) in enumerate(jobs):
+                g_host[i] = torch.from_numpy(W.image_2d_large(ci, it, workers=max(1, cores)))
+            jobs = []
         with ProcessPoolExecutor(max_workers=max(1, min(cores, 16, batch)),
                                  mp_context=mp.get_context("fork")) as ex:
             for (ci, it), arr in zip(jobs, ex.map(_gen_2d, jobs)):

@@ -195,33 +195,38 @@ def signals_1d(cfg: Config, first: int, count: int, n: int | None = None,
     return truth, add_noise(g, cfg.noise, key[:, 0])
 
 
-def _scene_2d(cfg: Config, item: int, n1: int, n2: int, m1: int, m2: int):
+def _scene_2d(cfg: Config, item: int, n1: int, n2: int, m1: int, m2: int,
+              r0: int = 0, r1: int | None = None):
+    """Extended scene (n1+2m1) x (n2+2m2); rows [r0, r1) of it when given (every
+    value is elementwise, so a row band equals the same rows of the whole)."""
     key = item_key(cfg.index, np.uint64(item))
     k = iter(range(10_000))
     y = (np.arange(n1 + 2 * m1, dtype=np.float64) - m1) / n1
     x = (np.arange(n2 + 2 * m2, dtype=np.float64) - m2) / n2
+    r1 = len(y) if r1 is None else r1
+    yy = y[r0:r1]
     a = [float(draw(key, next(k))) - 0.5 for _ in range(6)]
-    f = 0.5 + a[0] + a[1] * y[:, None] + a[2] * x[None, :] + a[3] * (y * y)[:, None] + \
-        a[4] * y[:, None] * x[None, :] + a[5] * (x * x)[None, :]
+    f = 0.5 + a[0] + a[1] * yy[:, None] + a[2] * x[None, :] + a[3] * (yy * yy)[:, None] + \
+        a[4] * yy[:, None] * x[None, :] + a[5] * (x * x)[None, :]
     for _ in range(cfg.blobs):
         amp = (0.1 + 0.5 * float(draw(key, next(k)))) * \
             (1.0 if float(draw(key, next(k))) < 0.5 else -1.0)
         w = 0.01 + 0.07 * float(draw(key, next(k)))
         cy, cx = float(draw(key, next(k))), float(draw(key, next(k)))
-        i0 = max(0, int(math.floor((cy - 6 * w) * n1)) + m1)
-        i1 = min(len(y), int(math.ceil((cy + 6 * w) * n1)) + m1 + 1)
+        i0 = max(r0, int(math.floor((cy - 6 * w) * n1)) + m1)
+        i1 = min(r1, int(math.ceil((cy + 6 * w) * n1)) + m1 + 1)
         j0 = max(0, int(math.floor((cx - 6 * w) * n2)) + m2)
         j1 = min(len(x), int(math.ceil((cx + 6 * w) * n2)) + m2 + 1)
         if i0 < i1 and j0 < j1:
             dy = (y[i0:i1] - cy) ** 2
             dx = (x[j0:j1] - cx) ** 2
-            f[i0:i1, j0:j1] += amp * np.exp(-(dy[:, None] + dx[None, :]) / (w * w))
+            f[i0 - r0:i1 - r0, j0:j1] += amp * np.exp(-(dy[:, None] + dx[None, :]) / (w * w))
     for _ in range(cfg.rects):
-        r0, c0 = float(draw(key, next(k))), float(draw(key, next(k)))
+        rr, c0 = float(draw(key, next(k))), float(draw(key, next(k)))
         hr = 0.05 + 0.25 * float(draw(key, next(k)))
         hc = 0.05 + 0.25 * float(draw(key, next(k)))
         val = float(draw(key, next(k)))
-        sel_y = (y >= r0) & (y < r0 + hr)
+        sel_y = (yy >= rr) & (yy < rr + hr)
         sel_x = (x >= c0) & (x < c0 + hc)
         f[np.ix_(sel_y, sel_x)] = val
     np.clip(f, 0.0, 1.0, out=f)
@@ -243,3 +248,80 @@ def image_2d(cfg: Config, item: int, n1: int | None = None, n2: int | None = Non
     g = convolve_valid(np.ascontiguousarray(g.T), w).T
     obs = add_noise(np.ascontiguousarray(g).reshape(-1), cfg.noise, key).reshape(n1, n2)
     return truth, obs
+
+
+# ---------------------------------------------------------------------------
+# Large images (config 4, 16384^2): the same scene / blur / noise, generated in
+# fixed bands of SLAB rows by worker processes into shared memory.  Band
+# boundaries do not depend on the worker count, so the image is deterministic;
+# the noise norm is the band partial sums added in band order.
+SLAB = 256
+
+
+def _noise_band(key, e0, e1):
+    """Gaussian field of add_noise for flat positions [e0, e1) of the image."""
+    p = np.arange(e0 // 2, (e1 + 1) // 2, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        u1 = bits_to_u01(splitmix64(np.uint64(key) + (np.uint64(2) * p + np.uint64(1)) * _GOLD))
+        u2 = bits_to_u01(splitmix64(np.uint64(key) + (np.uint64(2) * p + np.uint64(2)) * _GOLD))
+    r = np.sqrt(-2.0 * np.log(u1))
+    ang = 2.0 * math.pi * u2
+    eta = np.empty(2 * len(p))
+    eta[0::2] = r * np.cos(ang)
+    eta[1::2] = r * np.sin(ang)
+    s = e0 - 2 * (e0 // 2)
+    return eta[s:s + (e1 - e0)]
+
+
+def _band_job(args):
+    from multiprocessing import shared_memory
+    phase, ci, item, n1, n2, b0, b1, name, scale = args
+    cfg = config(ci)
+    w = cfg.psf
+    m = (len(w) - 1) // 2
+    shm = shared_memory.SharedMemory(name=name)
+    try:
+        out = np.ndarray((n1, n2), dtype=np.float64, buffer=shm.buf)
+        key = item_key(ci, np.uint64(item))
+        if phase == 0:
+            _, f = _scene_2d(cfg, item, n1, n2, m, m, b0, b1 + 2 * m)
+            g = convolve_valid(f, w)                 # rows
+            h = np.zeros((b1 - b0, n2))
+            for j in range(-m, m + 1):               # columns, same term order
+                if w[m + j] != 0.0:
+                    h += w[m + j] * g[m + j:m + j + (b1 - b0)]
+            out[b0:b1] = h
+            eta = _noise_band(key, b0 * n2, b1 * n2)
+            return float(np.sum(h * h)), float(np.sum(eta * eta))
+        eta = _noise_band(key, b0 * n2, b1 * n2).reshape(b1 - b0, n2)
+        out[b0:b1] += scale * eta
+        return 0.0, 0.0
+    finally:
+        shm.close()
+
+
+def image_2d_large(ci: int, item: int, workers: int | None = None, n1: int | None = None,
+                   n2: int | None = None) -> np.ndarray:
+    """Observed image ``item`` of 2D config ``ci`` built band-parallel (the
+    scene, separable valid blur and add_noise of image_2d)."""
+    import os
+    from concurrent.futures import ProcessPoolExecutor
+    from multiprocessing import shared_memory
+    cfg = config(ci)
+    n1 = cfg.n1 if n1 is None else n1
+    n2 = cfg.n2 if n2 is None else n2
+    shm = shared_memory.SharedMemory(create=True, size=n1 * n2 * 8)
+    try:
+        bands = [(b, min(b + SLAB, n1)) for b in range(0, n1, SLAB)]
+        workers = workers or os.cpu_count() or 1
+        with ProcessPoolExecutor(workers) as ex:
+            parts = list(ex.map(_band_job, [(0, ci, item, n1, n2, b0, b1, shm.name, 0.0)
+                                           for b0, b1 in bands]))
+            gn = sum(p[0] for p in parts)
+            en = sum(p[1] for p in parts)
+            scale = cfg.noise * math.sqrt(gn / en)
+            list(ex.map(_band_job, [(1, ci, item, n1, n2, b0, b1, shm.name, scale) for b0, b1 in bands]))
+        return np.array(np.ndarray((n1, n2), dtype=np.float64, buffer=shm.buf))
+    finally:
+        shm.close()
+        shm.unlink()

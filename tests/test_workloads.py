@@ -69,3 +69,11 @@ def test_2d_scene_is_clipped_and_seeded():
     assert t1.min() >= 0.0 and t1.max() <= 1.0
     assert abs(np.linalg.norm(g1 - W.image_2d(W.Config(**{**c.__dict__, "noise": 0.0}), 3, 64,
                                                 64)[1]) / np.linalg.norm(g1) - 0.01) < 1e-3
+
+
+def test_image_2d_large_matches_serial():
+    """Band-parallel generator (config 4 path) = image_2d up to the noise-norm
+    summation order."""
+    _, g = W.image_2d(W.config(4), 1, 600, 300)
+    got = W.image_2d_large(4, 1, workers=3, n1=600, n2=300)
+    assert np.max(np.abs(got - g)) < 1e-14 * np.max(np.abs(g))
