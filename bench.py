@@ -212,8 +212,11 @@ def alg_bytes_per_px(name, cfg):
     (SURVEY 8d model): what the kernel must read + write at minimum."""
     c = 16 if cfg.bc in (W.PERIODIC, W.HOC_FOURIER) else 8  # coefficient bytes
     if cfg.dim == 1:
-        return {"k_analyze": 8 + c, "k_synth_filter": c + 8, "k_gcv_grid": c,
-                "k_gcv_moments": c}.get(name)
+        # real data: the coefficients are n reals (Hermitian-packed in a complex
+        # basis); GCV streams one weight per Hermitian pair (n/2) or per coefficient
+        wg = 4 if c == 16 else 8
+        return {"k_analyze": 8 + 8, "k_synth_filter": 8 + 8, "k_gcv_grid": wg,
+                "k_gcv_moments": wg}.get(name)
     # 2D: column pass then row pass (each launch covers the whole batch once)
     return {"k_analyze": 0.5 * (8 + c) + 0.5 * (c + c), "k_synth_filter": c + c,
             "k_synth": c + 8, "k_gcv_grid": c, "k_gcv_moments": c}.get(name)

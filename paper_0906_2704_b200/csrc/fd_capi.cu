@@ -250,6 +250,9 @@ constexpr int kMaxOnChipM = 8192;  // 139 KB of complex fp64 in shared memory
 size_t smem_bytes(int M) {
   return (size_t)(pidx(M) + 1 + kTwSlots) * sizeof(double2) + 32 * 8 * 8 + 8 * 16;
 }
+size_t rsmem_bytes(const AxisDev& ax, int Mloc) {
+  return (size_t)rline_slots(ax, Mloc) * sizeof(double2);
+}
 int line_threads(int M) {
   int t = M / 16;
   if (t < 64) t = 64;
@@ -281,13 +284,13 @@ void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
       const int grid = std::min(io.gi.count, 2 * num_sms());
       double2* scr = nullptr;
       ck(cudaMallocAsync(&scr, (size_t)grid * 2 * ax.hfft.L * sizeof(double2), st), "scratch");
-      k_ranalyze<<<grid, 256, smem_bytes(ax.hfft.M / 2), st>>>(ax, io, scr);
+      k_ranalyze<<<grid, 256, rsmem_bytes(ax, ax.hfft.M / 2), st>>>(ax, io, scr);
       launched("k_ranalyze");
       ck(cudaFreeAsync(scr, st), "scratch");
       return;
     }
-    k_ranalyze<<<io.gi.count, std::min(256, line_threads(ax.hfft.M)), smem_bytes(ax.hfft.M),
-                 st>>>(ax, io, nullptr);
+    k_ranalyze<<<io.gi.count, std::min(256, line_threads(ax.hfft.M)),
+                 rsmem_bytes(ax, ax.hfft.M), st>>>(ax, io, nullptr);
     launched("k_ranalyze");
     return;
   }
@@ -306,13 +309,13 @@ void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cuda
       const int grid = std::min(io.gi.count, 2 * num_sms());
       double2* scr = nullptr;
       ck(cudaMallocAsync(&scr, (size_t)grid * 2 * ax.hfft.L * sizeof(double2), st), "scratch");
-      k_rsynth<<<grid, 256, smem_bytes(ax.hfft.M / 2), st>>>(ax, io, sa, scr);
+      k_rsynth<<<grid, 256, rsmem_bytes(ax, ax.hfft.M / 2), st>>>(ax, io, sa, scr);
       launched("k_rsynth");
       ck(cudaFreeAsync(scr, st), "scratch");
       return;
     }
-    k_rsynth<<<io.gi.count, std::min(256, line_threads(ax.hfft.M)), smem_bytes(ax.hfft.M),
-               st>>>(ax, io, sa, nullptr);
+    k_rsynth<<<io.gi.count, std::min(256, line_threads(ax.hfft.M)),
+               rsmem_bytes(ax, ax.hfft.M), st>>>(ax, io, sa, nullptr);
     launched("k_rsynth");
     return;
   }
@@ -465,7 +468,7 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
   double norm = 0.0;
   for (double x : q) norm += x * x;
   norm = std::sqrt(norm);
-  for (double& x : q) x /= norm;
+  for (double& x : q) x /= norm;  // boundary.cpp:153-160
   q.back() = 0.0;
   const double alpha = 1.0 / q[0];
   d.alpha = alpha;
@@ -613,6 +616,37 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
   for (int k = 0; k < 4; ++k) {
     d.cav[k] = make_double2(cav[k].real(), cav[k].imag());
     d.cap[k] = make_double2(cap[k].real(), cap[k].imag());
+    d.cavr[k] = cav[k].real();
+    d.capr[k] = cap[k].real();
+  }
+  // closed forms used by the real-line kernels (AxisDev)
+  d.q0 = q[0];
+  d.q_inv = 1.0 / norm;
+  if (bc == BC_ANTIREFLECTIVE) {
+    d.qmode = 0;
+    d.q_s = 1.0 / (n - 1);
+  } else {
+    d.qmode = 1;
+    d.q_gb = gb;
+    d.q_s = bc == BC_HOC_COSINE ? 2.0 * kPi / (2 * n - 4) : 2.0 * kPi / (n - 2);
+    d.q_o = bc == BC_HOC_COSINE ? -kPi / (2 * n - 4) : -2.0 * kPi / (n - 2);
+  }
+  if (d.correction) {
+    auto impulse = [&](const std::vector<cplx>& r, int* at, double* val) {
+      int k = 0;
+      for (int i = 1; i < m; ++i)
+        if (std::abs(r[i]) > std::abs(r[k])) k = i;
+      for (int i = 0; i < m; ++i)
+        if (i != k && std::abs(r[i]) > 1e-12 * std::abs(r[k]))
+          throw FdError(FD_ERR_OTHER, "boundary row X^T c is not a unit impulse");
+      *at = k;
+      *val = r[k].real();
+    };
+    impulse(row_a, &d.ia, &d.ra1);
+    impulse(row_b, &d.ib, &d.rb1);
+    // c_a, c_b are rows of X^H at the mirrored end positions
+    d.top_i = bc == BC_HOC_COSINE ? 0 : m - 1;
+    d.bot_i = bc == BC_HOC_COSINE ? m - 1 : 0;
   }
   auto up = [&](const std::vector<cplx>& h) {
     std::vector<double2> t(h.size());
@@ -711,10 +745,12 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 // ---- transform pipelines (tensor_apply order: columns, then rows) ----
 // analyze count items: in (real or complex) -> out (basis type)
 void run_analyze(const fd_op* op, const void* in, int in_cplx, void* out, long long count,
-                 Scratch& S, double* wout = nullptr, long long wstride = 0, long long wn = 0) {
+                 Scratch& S, double* wout = nullptr, long long wstride = 0, long long wn = 0,
+                 int pack = 0) {
   const int oc = op->cplx;
   if (op->dim == 1) {
     LineIO io{};
+    io.pack = pack;
     io.in = in;
     io.out = out;
     io.gi = lines_1d(op->n1, count);
@@ -762,10 +798,12 @@ void run_analyze(const fd_op* op, const void* in, int in_cplx, void* out, long l
 // synthesize coefficients (basis type) -> out, with mode 0/1/2 fused into the
 // first (column) pass; real output keeps Re and reports the residue per item.
 void run_synth(const fd_op* op, const fd_smoother* L, const void* in, void* out, int out_cplx,
-               int mode, const double* mu_item, double* resid, long long count, Scratch& S) {
+               int mode, const double* mu_item, double* resid, long long count, Scratch& S,
+               int pack = 0) {
   const int oc = op->cplx;
   if (op->dim == 1) {
     LineIO io{};
+    io.pack = pack;
     io.in = in;
     io.out = out;
     io.gi = lines_1d(op->n1, count);
@@ -862,19 +900,23 @@ struct Analyzed {
   void* ghat = nullptr;
   double* w = nullptr;
   long long wn = 0, wstride = 0;
+  int pack = 0;  // ghat Hermitian-packed (n doubles per line), see k_ranalyze
 };
 
+// want_full: keep the full complex coefficients (imaginary residue requested)
 Analyzed analyze_for_gcv(const fd_op* op, const fd_smoother* L, const double* g, long long count,
-                         Scratch& S) {
+                         Scratch& S, bool want_full = false) {
   Analyzed a;
-  a.ghat = op->cplx ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
   const bool use_w = op->dim == 1 && op->ax1->dev.rhalf && (!op->cplx || L->pair);
+  a.pack = use_w && op->cplx && !want_full;
+  a.ghat = (op->cplx && !a.pack) ? (void*)S.get<double2>(count * op->N())
+                                 : (void*)S.get<double>(count * op->N());
   if (use_w) {
     a.wn = op->cplx ? L->n_red : op->N();
     a.wstride = (a.wn + 31) / 32 * 32;
     a.w = S.get<double>((size_t)count * a.wstride);
   }
-  run_analyze(op, g, 0, a.ghat, count, S, a.w, a.wstride, a.wn);
+  run_analyze(op, g, 0, a.ghat, count, S, a.w, a.wstride, a.wn, a.pack);
   return a;
 }
 
@@ -1276,7 +1318,7 @@ void deblur_dev(const fd_op* op, const fd_smoother* L, const double* g, int use_
                 double fixed_mu, double mu_min, double mu_max, const DevGrid* dg,
                 double* restored, double* mu_used, int* best_k, double* curve,
                 double* imag_residue, long long count, int* status, Scratch& S) {
-  const Analyzed an = analyze_for_gcv(op, L, g, count, S);
+  const Analyzed an = analyze_for_gcv(op, L, g, count, S, imag_residue != nullptr);
   if (use_gcv) {
     gcv_select_dev(op, L, an, count, *dg, mu_min, mu_max, mu_used, best_k, curve, status, S);
   } else {
@@ -1290,7 +1332,7 @@ void deblur_dev(const fd_op* op, const fd_smoother* L, const double* g, int use_
   }
   if (!op->cplx && imag_residue)
     ck(cudaMemsetAsync(imag_residue, 0, count * sizeof(double), S.st), "memset");
-  run_synth(op, L, an.ghat, restored, 0, 1, mu_used, imag_residue, count, S);
+  run_synth(op, L, an.ghat, restored, 0, 1, mu_used, imag_residue, count, S, an.pack);
 }
 
 void check_status(int* status, cudaStream_t st) {

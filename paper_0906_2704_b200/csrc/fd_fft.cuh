@@ -159,7 +159,18 @@ __device__ __forceinline__ void dit_pass(double2* __restrict__ x, int M, int S, 
   }
 }
 
-__device__ __forceinline__ int pass_logr(int rem) { return rem >= 4 ? 4 : rem; }
+__host__ __device__ __forceinline__ int pass_logr(int rem) { return rem >= 4 ? 4 : rem; }
+
+// radix (log2) of the last DIF pass of a size-2^logM transform (the mid pass)
+__host__ __device__ __forceinline__ int mid_logr(int logM) {
+  return logM <= 0 ? 0 : (logM % 4 == 0 ? 4 : logM % 4);
+}
+// storage slot of DIF-order entry j of a bhat block of M = 2^logM points
+__host__ __device__ __forceinline__ int bhat_store_index(int j, int logM) {
+  const int lr = mid_logr(logM);
+  const int items = (1 << logM) >> lr;
+  return (j & ((1 << lr) - 1)) * items + (j >> lr);
+}
 
 // Forward DIF FFT (sign -1), natural order in, digit-reversed order out.
 // Caller must __syncthreads() before; returns after a barrier.
@@ -228,6 +239,8 @@ __device__ __forceinline__ void fft_dit(double2* x, int M, int logM, const TwSm&
 // consecutive positions, S = 2^LOGR), so they run as one register pass: load
 // the group and its bhat values, LOGR DIF stages, multiply, LOGR DIT stages,
 // store.  Saves two shared-memory round trips per Bluestein convolution.
+// bhat is stored thread-major for this pass (bhat_store_index), so load q of
+// all threads in a warp is one contiguous 512-byte read.
 template <int LOGR>
 __device__ __forceinline__ void mid_pass(double2* __restrict__ x, int M,
                                          const double2* __restrict__ bhat, const TwSm& tw) {
@@ -238,7 +251,7 @@ __device__ __forceinline__ void mid_pass(double2* __restrict__ x, int M,
     const int base = it * R;  // S = R: SR = 1, j0 = 0
     double2 v[R], bh[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) bh[q] = bhat[base + q];  // global or shared
+    for (int q = 0; q < R; ++q) bh[q] = __ldg(&bhat[q * items + it]);
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = x[pidx(base + q)];
     (void)twstep;

@@ -46,6 +46,19 @@ struct AxisDev {
   const double2 *v, *w, *row_a, *row_b, *c_a, *c_b;  // m each
   double2 cav[4];         // ca_v, ca_w, cb_v, cb_w
   double2 cap[4];         // capacitance I + [c rows][v w], row-major
+  // Real-line kernels (k_ranalyze / k_rsynth) never touch v, w, row_a/b,
+  // c_a/b or q: for real data the correction is folded into the interior
+  // transform (see k_ranalyze), using
+  //   row_a = X^T c_a, row_b = X^T c_b  -- unit impulses at interior ia, ib
+  //                                        (values ra1, rb1; checked at build),
+  //   c_a . u = (X^H u)[top_i],  c_b . u = (X^H u)[bot_i],
+  //   q_e = (q_gb - (e q_s + q_o))^2 q_inv   (qmode 1), (1 - e q_s) q_inv (qmode 0),
+  // and the real parts of the 2x2 capacitance system (exactly real for real
+  // data; the imaginary parts of the hoc-fourier tables are rounding noise).
+  int ia, ib, top_i, bot_i, qmode;
+  double ra1, rb1, q0;
+  double q_gb, q_s, q_o, q_inv;
+  double cavr[4], capr[4];
 };
 
 // Geometry of a set of lines (rows or columns of a batch of arrays).

@@ -144,7 +144,8 @@ __global__ void __launch_bounds__(512) k_bhat(FftTables T, const double2* __rest
   fft_dif_local(sm, Mloc, logMloc, T.M, tw);
   const double inv = 1.0 / (double)T.M;
   const int off = part < 0 ? 0 : part * Mloc;
-  for (int j = threadIdx.x; j < Mloc; j += blockDim.x) bhat[off + j] = cscale(sm[pidx(j)], inv);
+  for (int j = threadIdx.x; j < Mloc; j += blockDim.x)
+    bhat[off + bhat_store_index(j, logMloc)] = cscale(sm[pidx(j)], inv);
 }
 
 // symbol z(t) = sum_j h_j e^{ijt} (psf.cpp:39-52)
@@ -325,6 +326,7 @@ struct LineIO {
   double* wout;
   long long wstride;
   long long wn;  // weights actually written; [wn, wstride) is zero-filled
+  int pack;      // Fourier lines of real data stored Hermitian-packed (k_ranalyze)
 };
 
 __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
@@ -549,21 +551,27 @@ struct SynthArgs {
   double* resid2;        // per line sum Im^2 (complex basis, real output), or null
 };
 
-__device__ __forceinline__ double2 coeff_at(const AxisDev& ax, const LineIO& io,
-                                            const SynthArgs& sa, int l, long long off, int e) {
-  double2 c = ldc(io.in, io.in_cplx, off + e * io.gi.elem_stride);
+// coefficient c of element e of line l after the synthesis mode's scaling
+// (apply_tikhonov_filter, regularize.hpp:42-58, for mode 1)
+__device__ __forceinline__ double2 coeff_filter(const AxisDev& ax, const SynthArgs& sa,
+                                                const Lines& g, int l, int e, double2 c) {
   if (sa.mode == 0) return c;
   double2 d;
   double s;
-  spectral_at(sa.sp, io.gi, l, e, d, s);
+  spectral_at(sa.sp, g, l, e, d, s);
   if (sa.mode == 2) return ax.cplx ? cmul(c, d) : make_double2(c.x * d.x, 0.0);
-  const double mu = __ldg(&sa.mu_item[l / io.gi.per_item]);
+  const double mu = __ldg(&sa.mu_item[l / g.per_item]);
   if (ax.cplx) {
     const double den = (d.x * d.x + d.y * d.y) + mu * s * s;
     return cmul(c, make_double2(d.x / den, -d.y / den));
   }
   const double f = d.x / (d.x * d.x + mu * s * s);
   return make_double2(c.x * f, 0.0);
+}
+
+__device__ __forceinline__ double2 coeff_at(const AxisDev& ax, const LineIO& io,
+                                            const SynthArgs& sa, int l, long long off, int e) {
+  return coeff_filter(ax, sa, io.gi, l, e, ldc(io.in, io.in_cplx, off + e * io.gi.elem_stride));
 }
 
 __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs sa) {
@@ -802,8 +810,76 @@ __device__ __forceinline__ int makhoul_src(int p, int m, int half) {
   return p < half ? 2 * p : 2 * (m - 1 - p) + 1;  // trig.cpp:194-195
 }
 
+// Two-level table of a twiddle sequence t_k (k < len) in shared memory:
+// t_k = hi[k >> 6] * lo[k & 63] (both exact entries of the global table).
+struct Tw2 {
+  const double2* lo;
+  const double2* hi;
+  __device__ __forceinline__ double2 operator()(int k) const {
+    return cmul(hi[k >> 6], lo[k & 63]);
+  }
+};
+__host__ __device__ __forceinline__ int tw2_slots(int len) {
+  return len > 0 ? 64 + ((len + 63) >> 6) : 0;
+}
+__device__ __forceinline__ Tw2 load_tw2(double2* slots, const double2* tab, int len) {
+  for (int i = threadIdx.x; i < 64; i += blockDim.x)
+    if (i < len) slots[i] = tab[i];
+  const int nhi = (len + 63) >> 6;
+  for (int i = threadIdx.x; i < nhi; i += blockDim.x) slots[64 + i] = tab[i << 6];
+  return Tw2{slots, slots + 64};
+}
+
+// boundary column q_e (boundary.cpp:218-303) in registers
+__device__ __forceinline__ double q_at(const AxisDev& ax, int e) {
+  if (ax.qmode == 0) return (1.0 - e * ax.q_s) * ax.q_inv;
+  const double t = ax.q_gb - fma((double)e, ax.q_s, ax.q_o);
+  return t * t * ax.q_inv;
+}
+
+// Border terms of T_X^{-1} y for a real line (transform_apply_inverse,
+// boundary.cpp:338-375).  row_a / row_b are unit impulses, so the two dot
+// products are two samples and every thread solves the 2x2 system itself; and
+//   y0 v + xi + yn w - (b0 v + b1 w) = X (x - o0 qhat - on J qhat),
+//   o0 = alpha y0 - alpha b0,  on = alpha yn - alpha b1  (v = -alpha X qhat,
+//   w = -alpha X J qhat), so the border enters as a correction of the
+// interior input and the output needs no v / w tables.
+struct Fold {
+  double o0, on;
+};
+template <class LD>
+__device__ __forceinline__ Fold fold_terms(const AxisDev& ax, LD ld) {
+  Fold f{0.0, 0.0};
+  if (!ax.bordered) return f;
+  const double y0 = ld(0), yn = ld(ax.n - 1);
+  double b0 = 0.0, b1 = 0.0;
+  if (ax.correction) {
+    const double xa = ld(ax.ia + 1), xb = ld(ax.ib + 1);
+    const double ra = (ax.cavr[0] * y0 + ax.cavr[1] * yn) + ax.ra1 * xa;
+    const double rb = (ax.cavr[2] * y0 + ax.cavr[3] * yn) + ax.rb1 * xb;
+    const double* c = ax.capr;
+    const double det = c[0] * c[3] - c[1] * c[2];
+    b0 = (ra * c[3] - rb * c[1]) / det;
+    b1 = (rb * c[0] - ra * c[2]) / det;
+  }
+  const double al = ax.alpha;
+  f.o0 = al * y0 - b0 * al;
+  f.on = al * yn - b1 * al;
+  return f;
+}
+
+// smem of the real-line kernels: buffer, FFT twiddles, rtw and DCT tables
+__host__ __device__ __forceinline__ int rline_slots(const AxisDev& ax, int Mloc) {
+  return pidx(Mloc) + 1 + kTwSlots + tw2_slots(ax.hfft.L) +
+         (ax.kind == IK_COS ? tw2_slots(ax.m) : 0);
+}
+
 // scr != null: split-convolution mode for M beyond shared memory
 // (bluestein_half), persistent over lines, 2h complex of per-CTA scratch.
+// io.pack (Fourier interior): the line is stored Hermitian-packed in n doubles
+//   [border0, border_n-1] [X_0, X_h] X_1 .. X_{h-1}   (double2 slots; the
+//   border slot only when bordered) -- the coefficients of real data in this
+//   basis are exactly Hermitian once the border is folded in.
 __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, double2* scr) {
   extern __shared__ double2 sm[];
   const FftTables& T = ax.hfft;
@@ -811,83 +887,48 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   const bool big = scr != nullptr;
   const int Mloc = big ? M / 2 : M;
   double2* x = sm;
-  const TwSm tw = load_twiddles(sm + pidx(Mloc) + 1, T);
-  double* red = reinterpret_cast<double*>(sm + pidx(Mloc) + 1 + kTwSlots);
-  double2* bcs = reinterpret_cast<double2*>(red + 32 * 4);
+  double2* slots = sm + pidx(Mloc) + 1;
+  const TwSm tw = load_twiddles(slots, T);
+  const Tw2 rtw = load_tw2(slots + kTwSlots, ax.rtw, h);
+  Tw2 dtw{nullptr, nullptr};
+  if (ax.kind == IK_COS) dtw = load_tw2(slots + kTwSlots + tw2_slots(h), ax.dct_tw, ax.m);
+  const bool pk = io.pack && ax.kind == IK_FOURIER;
   double2* scrA = big ? scr + (long long)blockIdx.x * 2 * h : nullptr;
   double2* scrY = big ? scrA + h : nullptr;
+  __syncthreads();
   for (int l = blockIdx.x; l < io.gi.count; l += gridDim.x) {
   const long long oi = line_offset(io.gi, l), es = io.gi.elem_stride;
   const int n = ax.n, m = ax.m;
   const double2* chirp = T.chirp;
   const double* in = reinterpret_cast<const double*>(io.in);
   auto ld = [&](int e) { return __ldg(in + oi + e * es); };
-  double y0 = 0.0, yn = 0.0;
-  if (ax.bordered) {
-    y0 = ld(0);
-    yn = ld(n - 1);
-  }
-  const bool dots = ax.bordered && ax.correction;
+  const Fold fd = fold_terms(ax, ld);
+  // folded interior sample s
+  auto xin = [&](int s) {
+    double v = ld(interior_elem(ax, s));
+    if (ax.bordered) v += -fd.o0 * q_at(ax, s + 1) - fd.on * q_at(ax, n - 2 - s);
+    return v;
+  };
   const int half = (m + 1) / 2;
-  double acc[4] = {0, 0, 0, 0};  // ra (re, im), rb (re, im)
   for (int j = h + threadIdx.x; j < Mloc; j += blockDim.x) x[pidx(j)] = czero();
 #pragma unroll 4
   for (int j = threadIdx.x; j < h; j += blockDim.x) {
-    double2 val = czero();
-    {
-      const int p0 = 2 * j, p1 = 2 * j + 1;
-      double a, b;
-      if (ax.kind == IK_SINE) {
-        const int R = 2 * (m + 1);
-        auto ext = [&](int p) -> double {
-          if (p == 0 || p == m + 1) return 0.0;
-          if (p <= m) return ld(interior_elem(ax, p - 1));
-          return -ld(interior_elem(ax, R - 1 - p));
-        };
-        a = ext(p0);
-        b = ext(p1);
-      } else {
-        const int s0 = ax.kind == IK_COS ? makhoul_src(p0, m, half) : p0;
-        const int s1 = ax.kind == IK_COS ? makhoul_src(p1, m, half) : p1;
-        a = ld(interior_elem(ax, s0));
-        b = ld(interior_elem(ax, s1));
-        if (dots) {
-          const double2 ra0 = __ldg(&ax.row_a[s0]), ra1 = __ldg(&ax.row_a[s1]);
-          const double2 rb0 = __ldg(&ax.row_b[s0]), rb1 = __ldg(&ax.row_b[s1]);
-          acc[0] += ra0.x * a + ra1.x * b;
-          acc[1] += ra0.y * a + ra1.y * b;
-          acc[2] += rb0.x * a + rb1.x * b;
-          acc[3] += rb0.y * a + rb1.y * b;
-        }
-      }
-      val = cmul(make_double2(a, b), __ldg(&chirp[j]));
+    const int p0 = 2 * j, p1 = 2 * j + 1;
+    double a, b;
+    if (ax.kind == IK_SINE) {
+      const int R = 2 * (m + 1);
+      auto ext = [&](int p) -> double {
+        if (p == 0 || p == m + 1) return 0.0;
+        if (p <= m) return xin(p - 1);
+        return -xin(R - 1 - p);
+      };
+      a = ext(p0);
+      b = ext(p1);
+    } else {
+      a = xin(ax.kind == IK_COS ? makhoul_src(p0, m, half) : p0);
+      b = xin(ax.kind == IK_COS ? makhoul_src(p1, m, half) : p1);
     }
-    x[pidx(j)] = val;
-  }
-  if (dots) block_sum<4>(acc, red);
-  if (threadIdx.x == 0) {
-    double2 b0 = czero(), b1 = czero();
-    if (dots) {  // boundary.cpp:357-368
-      const double2* c = ax.cap;
-      const double2 ra = cadd(cadd(cscale(ax.cav[0], y0), cscale(ax.cav[1], yn)),
-                              make_double2(acc[0], acc[1]));
-      const double2 rb = cadd(cadd(cscale(ax.cav[2], y0), cscale(ax.cav[3], yn)),
-                              make_double2(acc[2], acc[3]));
-      const double2 n0 = csub(cmul(ra, c[3]), cmul(rb, c[1]));
-      const double2 n1 = csub(cmul(rb, c[0]), cmul(ra, c[2]));
-      if (ax.cplx) {
-        const double2 det = csub(cmul(c[0], c[3]), cmul(c[1], c[2]));
-        const double dd = det.x * det.x + det.y * det.y;
-        b0 = make_double2((n0.x * det.x + n0.y * det.y) / dd, (n0.y * det.x - n0.x * det.y) / dd);
-        b1 = make_double2((n1.x * det.x + n1.y * det.y) / dd, (n1.y * det.x - n1.x * det.y) / dd);
-      } else {
-        const double det = c[0].x * c[3].x - c[1].x * c[2].x;
-        b0 = make_double2(n0.x / det, 0.0);
-        b1 = make_double2(n1.x / det, 0.0);
-      }
-    }
-    bcs[0] = b0;
-    bcs[1] = b1;
+    x[pidx(j)] = cmul(make_double2(a, b), __ldg(&chirp[j]));
   }
   __syncthreads();
 
@@ -910,39 +951,24 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
     return cmul(y, __ldg(&chirp[k]));
   };
 
-  const double2 b0 = bcs[0], b1 = bcs[1];
   const long long oo = line_offset(io.go, l), eso = io.go.elem_stride;
+  double2* P = reinterpret_cast<double2*>(reinterpret_cast<double*>(io.out) + oo);
+  const int off = ax.bordered ? 1 : 0;
   const double inv_sqrt_m = 1.0 / sqrt((double)m);
   const double s0 = sqrt(1.0 / (double)m), s1 = sqrt(2.0 / (double)m);
   double* wl = io.wout ? io.wout + (long long)l * io.wstride : nullptr;
   if (wl)
     for (long long i = io.wn + threadIdx.x; i < io.wstride; i += blockDim.x) wl[i] = 0.0;
-  // final coefficient of interior index i (border terms applied), stored;
-  // returns the value for the GCV weights
-  auto emit = [&](int i, double2 xi) -> double2 {
+  auto emit = [&](int i, double2 o) {
     const int e = interior_elem(ax, i);
-    double2 o = xi;
-    if (ax.bordered) {
-      const double2 v = __ldg(&ax.v[i]), w = __ldg(&ax.w[i]);
-      if (ax.cplx) {
-        o = cadd(cadd(cscale(v, y0), xi), cscale(w, yn));
-        if (dots) o = csub(o, cadd(cmul(b0, v), cmul(b1, w)));
-      } else {
-        double r = y0 * v.x + xi.x + yn * w.x;
-        if (dots) r -= b0.x * v.x + b1.x * w.x;
-        o = make_double2(r, 0.0);
-      }
-    }
     stc(io.out, io.out_cplx, oo + e * eso, o);
     if (wl && !ax.cplx) wl[e] = o.x * o.x;
-    return o;
   };
   auto nrm = [](double2 a) { return a.x * a.x + a.y * a.y; };
   if (ax.kind == IK_FOURIER) {
     // groups {k, h-k}: both Hermitian partners of each coefficient come out of
     // the same pair (Z_k, Z_{h-k}), so the GCV weights |g_k|^2 + |g_{m-k}|^2
     // are formed in registers
-    const int off = ax.bordered ? 1 : 0;
     for (int k = threadIdx.x; k <= h / 2; k += blockDim.x) {
       const int kp = k == 0 ? 0 : h - k;
       const double2 Zk = zv(k);
@@ -950,26 +976,34 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
       const double2 E = cscale(cadd(Zk, cconj(Zp)), 0.5);
       const double2 D = csub(Zk, cconj(Zp));
       const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
-      const double2 WO = cmul(__ldg(&ax.rtw[k]), O);
-      const double2 ok = emit(k, cscale(cadd(E, WO), inv_sqrt_m));
-      const double2 okh = emit(k + h, cscale(csub(E, WO), inv_sqrt_m));
-      if (kp != k) {
-        const double2 WOp = cmul(__ldg(&ax.rtw[kp]), cconj(O));
-        const double2 okp = emit(kp, cscale(cadd(cconj(E), WOp), inv_sqrt_m));
-        const double2 okph = emit(kp + h, cscale(csub(cconj(E), WOp), inv_sqrt_m));
-        if (wl) {
-          if (k == 0) {
-            wl[off] = nrm(ok);
-            wl[off + h] = nrm(okh);
-          } else {
-            wl[off + k] = nrm(ok) + nrm(okph);   // pair (k, m-k = kp+h)
-            wl[off + kp] = nrm(okp) + nrm(okh);  // pair (kp, m-kp = k+h)
-          }
+      const double2 WO = cmul(rtw(k), O);
+      const double2 ok = cscale(cadd(E, WO), inv_sqrt_m);
+      const double2 okh = cscale(csub(E, WO), inv_sqrt_m);
+      const double2 WOp = cmul(rtw(kp), cconj(O));
+      const double2 okp = cscale(cadd(cconj(E), WOp), inv_sqrt_m);
+      const double2 okph = cscale(csub(cconj(E), WOp), inv_sqrt_m);
+      if (pk) {
+        if (k == 0) {
+          P[off] = make_double2(ok.x, okh.x);
+        } else {
+          P[off + k] = ok;
+          if (kp != k) P[off + kp] = okp;
         }
-      } else if (wl) {
+      } else {
+        emit(k, ok);
+        emit(k + h, okh);
+        if (kp != k) {
+          emit(kp, okp);
+          emit(kp + h, okph);
+        }
+      }
+      if (wl) {
         if (k == 0) {  // singleton group {0}: self pairs 0 and h
           wl[off] = nrm(ok);
           wl[off + h] = nrm(okh);
+        } else if (kp != k) {
+          wl[off + k] = nrm(ok) + nrm(okph);   // pair (k, m-k = kp+h)
+          wl[off + kp] = nrm(okp) + nrm(okh);  // pair (kp, m-kp = k+h)
         } else {
           wl[off + k] = nrm(ok) + nrm(okh);  // k = h/2: pair (k, k+h)
         }
@@ -982,41 +1016,39 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
       const double2 Zc = cconj(zv(kc));
       const double2 E = cscale(cadd(Zk, Zc), 0.5);
       const double2 D = csub(Zk, Zc);
-      const double2 WO = cmul(__ldg(&ax.rtw[k]), make_double2(0.5 * D.y, -0.5 * D.x));
+      const double2 WO = cmul(rtw(k), make_double2(0.5 * D.y, -0.5 * D.x));
       const double2 X0 = cadd(E, WO), X1 = csub(E, WO);  // X_k, X_{k+h}
       if (ax.kind == IK_SINE) {
         if (k >= 1) emit(k - 1, make_double2(-0.5 * sqrt(2.0 / ((double)m + 1.0)) * X0.y, 0.0));
       } else {
-        const double2 t0 = __ldg(&ax.dct_tw[k]), t1 = __ldg(&ax.dct_tw[k + h]);
+        const double2 t0 = dtw(k), t1 = dtw(k + h);
         emit(k, make_double2((k == 0 ? s0 : s1) * (t0.x * X0.x - t0.y * X0.y), 0.0));
         emit(k + h, make_double2(s1 * (t1.x * X1.x - t1.y * X1.y), 0.0));
       }
     }
   }
   if (ax.bordered && threadIdx.x == 0) {
-    const double al = ax.alpha;
-    double2 o0 = make_double2(al * y0, 0.0), on = make_double2(al * yn, 0.0);
-    if (dots) {
-      o0 = csub(o0, cscale(b0, al));
-      on = csub(on, cscale(b1, al));
+    const double2 o0 = make_double2(fd.o0, 0.0), on = make_double2(fd.on, 0.0);
+    if (pk) {
+      P[0] = make_double2(fd.o0, fd.on);
+    } else {
+      stc(io.out, io.out_cplx, oo, o0);
+      stc(io.out, io.out_cplx, oo + (long long)(n - 1) * eso, on);
     }
-    stc(io.out, io.out_cplx, oo, o0);
-    stc(io.out, io.out_cplx, oo + (long long)(n - 1) * eso, on);
     if (wl) {
-      if (ax.cplx) {
-        wl[0] = nrm(o0);
-        wl[h + 2] = nrm(on);
-      } else {
-        wl[0] = o0.x * o0.x;
-        wl[n - 1] = on.x * on.x;
-      }
+      wl[0] = fd.o0 * fd.o0;
+      wl[ax.cplx ? h + 2 : n - 1] = fd.on * fd.on;
     }
   }
-  __syncthreads();  // x, bcs and the scratch are reused by the next line
+  __syncthreads();  // x and the scratch are reused by the next line
   }
 }
 
-// scr != null: split-convolution mode (see k_ranalyze)
+// Real output of T_X c (transform_apply, boundary.cpp:310-336) with the
+// filter of the restoration fused into the coefficient loads.  The two border
+// dots c_a . c_mid, c_b . c_mid are samples of the interior synthesis
+// (top_i, bot_i), written by the thread that produces them.
+// scr != null: split-convolution mode (see k_ranalyze); io.pack: packed input.
 __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthArgs sa,
                                                    double2* scr) {
   extern __shared__ double2 sm[];
@@ -1025,22 +1057,35 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
   const bool big = scr != nullptr;
   const int Mloc = big ? M / 2 : M;
   double2* x = sm;
-  const TwSm tw = load_twiddles(sm + pidx(Mloc) + 1, T);
-  double* red = reinterpret_cast<double*>(sm + pidx(Mloc) + 1 + kTwSlots);
+  double2* slots = sm + pidx(Mloc) + 1;
+  const TwSm tw = load_twiddles(slots, T);
+  const Tw2 rtw = load_tw2(slots + kTwSlots, ax.rtw, h);
+  Tw2 dtw{nullptr, nullptr};
+  if (ax.kind == IK_COS) dtw = load_tw2(slots + kTwSlots + tw2_slots(h), ax.dct_tw, ax.m);
+  const bool pk = io.pack && ax.kind == IK_FOURIER;
   double2* scrA = big ? scr + (long long)blockIdx.x * 2 * h : nullptr;
   double2* scrY = big ? scrA + h : nullptr;
+  __syncthreads();
   for (int l = blockIdx.x; l < io.gi.count; l += gridDim.x) {
   const long long oi = line_offset(io.gi, l);
   const int n = ax.n, m = ax.m;
   const double2* chirp = T.chirp;
-  auto cf = [&](int e) { return coeff_at(ax, io, sa, l, oi, e); };
-  double2 u0 = czero(), un = czero();
+  auto filt = [&](int e, double2 c) { return coeff_filter(ax, sa, io.gi, l, e, c); };
+  auto cf = [&](int e) { return filt(e, ldc(io.in, io.in_cplx, oi + e * io.gi.elem_stride)); };
+  const double2* Pin =
+      reinterpret_cast<const double2*>(reinterpret_cast<const double*>(io.in) + oi);
+  const int off = ax.bordered ? 1 : 0;
+  double u0 = 0.0, un = 0.0;
   if (ax.bordered) {
-    u0 = cf(0);
-    un = cf(n - 1);
+    if (pk) {
+      const double2 b = __ldg(Pin);
+      u0 = filt(0, make_double2(b.x, 0.0)).x;
+      un = filt(n - 1, make_double2(b.y, 0.0)).x;
+    } else {
+      u0 = cf(0).x;
+      un = cf(n - 1).x;
+    }
   }
-  const bool dots = ax.bordered && ax.correction;
-  double acc[4] = {0, 0, 0, 0};  // top (re, im), bottom (re, im)
   if (ax.kind == IK_SINE) {  // Q c_mid: R2C of the odd extension (Q is an involution)
     const int R = 2 * (m + 1);
     for (int j = threadIdx.x; j < Mloc; j += blockDim.x) {
@@ -1055,76 +1100,57 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
       }
       x[pidx(j)] = val;
     }
-    __syncthreads();
   } else {
     // cosine works on conj(buf_i) = s_i c_i conj(tw_i) (DCT-III, trig.cpp:201-212)
     const double s0 = sqrt(1.0 / (double)m), s1 = sqrt(2.0 / (double)m);
-    auto prep = [&](int i, double2 c) {
+    auto val_at = [&](int i) {
+      const double2 c = cf(interior_elem(ax, i));
       if (ax.kind == IK_COS) {
-        const double2 t = __ldg(&ax.dct_tw[i]);
+        const double2 t = dtw(i);
         const double ts = (i == 0 ? s0 : s1) * c.x;
         return make_double2(ts * t.x, -(ts * t.y));
       }
       return c;
     };
-    auto dot = [&](int i, double2 c) {
-      if (ax.kind == IK_COS) {
-        acc[0] += __ldg(&ax.c_a[i]).x * c.x;
-        acc[2] += __ldg(&ax.c_b[i]).x * c.x;
-      } else {
-        const double2 t0 = cmul(__ldg(&ax.c_a[i]), c), t1 = cmul(__ldg(&ax.c_b[i]), c);
-        acc[0] += t0.x, acc[1] += t0.y, acc[2] += t1.x, acc[3] += t1.y;
-      }
-    };
-    if (!big) {  // stage the (filtered) coefficients in shared memory
-#pragma unroll 4
-      for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        const double2 c = cf(interior_elem(ax, i));
-        if (dots) dot(i, c);
-        x[pidx(i)] = prep(i, c);
-      }
-      __syncthreads();
-    }
-    // C2R pre-pass over the closed index groups {k, h-k}: X = herm(staged),
+    // C2R pre-pass over the closed index groups {k, h-k}: X = herm(c),
     // Zin_k = (X_k + X_{k+h}) + i (X_k - X_{k+h}) W^{-k}; Bluestein input conj(Zin) c_k.
-    // Split mode reads the group's four coefficients from global memory.
-    auto val_at = [&](int q) {
-      if (!big) return x[pidx(q)];
-      return prep(q, cf(interior_elem(ax, q)));
-    };
+    // Each coefficient is read exactly once, straight from global memory.
     for (int k = threadIdx.x; k <= h / 2; k += blockDim.x) {
       const int kp = k == 0 ? 0 : h - k;
-      // group indices: k, kp (lower), k + h, kp + h = m - k (upper)
-      const double2 vk = val_at(k), vkh = val_at(k + h);
-      const double2 vp = kp != k ? val_at(kp) : vk, vph = kp != k ? val_at(kp + h) : vkh;
-      if (big && dots) {
-        dot(k, cf(interior_elem(ax, k)));
-        dot(k + h, cf(interior_elem(ax, k + h)));
-        if (kp != k) {
-          dot(kp, cf(interior_elem(ax, kp)));
-          dot(kp + h, cf(interior_elem(ax, kp + h)));
+      double2 Xk, Xkh, Xp, Xph;  // X at k, k+h, kp, kp+h
+      if (pk) {  // exactly Hermitian: X_{m-q} = conj X_q
+        if (k == 0) {
+          const double2 b = __ldg(Pin + off);
+          Xk = Xp = filt(interior_elem(ax, 0), make_double2(b.x, 0.0));
+          Xkh = Xph = filt(interior_elem(ax, h), make_double2(b.y, 0.0));
+        } else {
+          const double2 fk = filt(interior_elem(ax, k), __ldg(Pin + off + k));
+          const double2 fp = kp != k ? filt(interior_elem(ax, kp), __ldg(Pin + off + kp)) : fk;
+          Xk = fk;
+          Xp = fp;
+          Xkh = cconj(fp);  // m - (k+h) = kp
+          Xph = cconj(fk);
         }
+      } else {
+        // herm(q) = (v_q + conj v_{m-q})/2: m-k = kp+h, m-(k+h) = kp (k = 0: 0 and h)
+        const double2 vk = val_at(k), vkh = val_at(k + h);
+        const double2 vp = kp != k ? val_at(kp) : vk, vph = kp != k ? val_at(kp + h) : vkh;
+        Xk = cscale(cadd(vk, cconj(k == 0 ? vk : vph)), 0.5);
+        Xkh = cscale(cadd(vkh, cconj(k == 0 ? vkh : vp)), 0.5);
+        Xp = cscale(cadd(vp, cconj(k == 0 ? vp : vkh)), 0.5);
+        Xph = cscale(cadd(vph, cconj(k == 0 ? vph : vk)), 0.5);
       }
-      // herm(q) = (v_q + conj v_{m-q})/2: m-k = kp+h, m-(k+h) = kp (k = 0: m-0 -> 0, m-h = h)
-      const double2 Xk = cscale(cadd(vk, cconj(k == 0 ? vk : vph)), 0.5);
-      const double2 Xkh = cscale(cadd(vkh, cconj(k == 0 ? vkh : vp)), 0.5);
-      const double2 Xp = cscale(cadd(vp, cconj(k == 0 ? vp : vkh)), 0.5);
-      const double2 Xph = cscale(cadd(vph, cconj(k == 0 ? vph : vk)), 0.5);
       auto zin = [&](int kk, double2 Xa, double2 Xb) {
-        const double2 Od = cmulc(csub(Xa, Xb), __ldg(&ax.rtw[kk]));
+        const double2 Od = cmulc(csub(Xa, Xb), rtw(kk));
         const double2 Ev = cadd(Xa, Xb);
         return make_double2(Ev.x - Od.y, Ev.y + Od.x);
       };
-      const double2 za = zin(k, Xk, Xkh);
-      const double2 zb = zin(kp, Xp, Xph);
-      x[pidx(k)] = cmul(cconj(za), __ldg(&chirp[k]));
-      if (kp != k) x[pidx(kp)] = cmul(cconj(zb), __ldg(&chirp[kp]));
+      x[pidx(k)] = cmul(cconj(zin(k, Xk, Xkh)), __ldg(&chirp[k]));
+      if (kp != k) x[pidx(kp)] = cmul(cconj(zin(kp, Xp, Xph)), __ldg(&chirp[kp]));
     }
-    __syncthreads();
     for (int j = h + threadIdx.x; j < Mloc; j += blockDim.x) x[pidx(j)] = czero();
-    __syncthreads();
   }
-  if (dots) block_sum<4>(acc, red);
+  __syncthreads();
 
   if (!big) {
     bluestein_core(x, T, tw);
@@ -1145,11 +1171,16 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
   };
 
   const long long oo = line_offset(io.go, l), eso = io.go.elem_stride;
+  double* out = reinterpret_cast<double*>(io.out);
   auto put = [&](int p, double val) {  // interior position p of the output line
     const int e = interior_elem(ax, p);
     double o = val;
-    if (ax.bordered) o = __ldg(&ax.q[e]) * u0.x + val + __ldg(&ax.q[n - 1 - e]) * un.x;
-    stc(io.out, 0, oo + e * eso, make_double2(o, 0.0));
+    if (ax.bordered) o = q_at(ax, e) * u0 + val + q_at(ax, n - 1 - e) * un;
+    out[oo + e * eso] = o;
+    if (ax.correction) {  // out_0 = q_0 u_0 + c_a . c,  out_{n-1} = c_b . c + q_0 u_{n-1}
+      if (p == ax.top_i) out[oo] = ax.q0 * u0 + val;
+      if (p == ax.bot_i) out[oo + (long long)(n - 1) * eso] = val + ax.q0 * un;
+    }
   };
   if (ax.kind == IK_SINE) {
     const double sc = -0.5 * sqrt(2.0 / ((double)m + 1.0));
@@ -1159,7 +1190,7 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
       const double2 Zc = cconj(zv(kc));
       const double2 E = cscale(cadd(Zk, Zc), 0.5);
       const double2 D = csub(Zk, Zc);
-      const double2 WO = cmul(__ldg(&ax.rtw[k]), make_double2(0.5 * D.y, -0.5 * D.x));
+      const double2 WO = cmul(rtw(k), make_double2(0.5 * D.y, -0.5 * D.x));
       put(k - 1, sc * (E.y + WO.y));
     }
   } else {
@@ -1177,11 +1208,9 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
       }
     }
   }
-  if (ax.bordered && threadIdx.x == 0) {
-    const double q0 = ax.q[0];
-    const double2 top = make_double2(acc[0], acc[1]), bot = make_double2(acc[2], acc[3]);
-    stc(io.out, 0, oo, make_double2(q0 * u0.x + top.x, 0.0));
-    stc(io.out, 0, oo + (long long)(n - 1) * eso, make_double2(bot.x + q0 * un.x, 0.0));
+  if (ax.bordered && !ax.correction && threadIdx.x == 0) {
+    out[oo] = ax.q0 * u0;
+    out[oo + (long long)(n - 1) * eso] = ax.q0 * un;
   }
   __syncthreads();  // x and the scratch are reused by the next line
   }

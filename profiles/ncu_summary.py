@@ -2,6 +2,7 @@
 
     python profiles/ncu_summary.py gpurun_out/prof_rNN.ncu-rep > profiles/rNN_ncu_full.txt
     python profiles/ncu_summary.py --launches gpurun_out/launches_rNN.csv > profiles/rNN_launches.txt
+    python profiles/ncu_summary.py --source gpurun_out/prof_rNN.ncu-rep KERNEL_REGEX [TOP]
 """
 import collections
 import csv
@@ -73,8 +74,43 @@ def launches(path):
         print(f"{k:48s} {c:8d} {v:12.1f} {100 * v / tot:6.1f}%")
 
 
+def source(path, kernel, top=25):
+    """Per CUDA source line: share of warp-stall samples and its top reasons."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source",
+                          "cuda,sass", "-k", "regex:" + kernel], capture_output=True, text=True,
+                         check=True).stdout
+    fname, hdr, lines = "", None, []
+    for r in csv.reader(io.StringIO(raw)):
+        if not r:
+            continue
+        if r[0] == "File Path":
+            fname = r[1].split("/")[-1]
+        elif r[0] == "Line No":
+            hdr = r
+        elif hdr and r[0] not in ("", "Function Name"):
+            d = dict(zip(hdr, r))
+            try:
+                s = float(d["Warp Stall Sampling (All Samples)"])
+            except (KeyError, ValueError):
+                continue
+            reasons = []
+            for k in hdr:
+                if k.startswith("stall_") and not k.endswith("(Not Issued)"):
+                    try:
+                        reasons.append((float(d[k]), k[6:]))
+                    except ValueError:
+                        pass
+            lines.append((s, f"{fname}:{r[0]}", r[1].strip()[:70], sorted(reasons, reverse=True)[:3]))
+    tot = sum(x[0] for x in lines) or 1.0
+    for s, loc, src, rs in sorted(lines, reverse=True)[:top]:
+        why = ", ".join(f"{n} {100 * v / max(s, 1):.0f}%" for v, n in rs if v > 0)
+        print(f"{100 * s / tot:5.1f}%  {loc:22s} {src:70s} [{why}]")
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "--launches":
         launches(sys.argv[2])
+    elif sys.argv[1] == "--source":
+        source(sys.argv[2], sys.argv[3], int(sys.argv[4]) if len(sys.argv) > 4 else 25)
     else:
         full(sys.argv[1])
