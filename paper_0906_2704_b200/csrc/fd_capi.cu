@@ -251,7 +251,7 @@ size_t smem_bytes(int M) {
   return (size_t)(pidx(M) + 1 + kTwSlots) * sizeof(double2) + 32 * 8 * 8 + 8 * 16;
 }
 size_t rsmem_bytes(const AxisDev& ax, int Mloc) {
-  return (size_t)rline_slots(ax, Mloc) * sizeof(double2);
+  return (size_t)(rline_slots(ax, Mloc) + 1) * sizeof(double2);  // + mbarrier
 }
 int line_threads(int M) {
   int t = M / 16;
@@ -276,6 +276,15 @@ int num_sms() {
   return nsm;
 }
 
+// persistent grid of a real-line kernel: every CTA slot of the device, at most
+// one CTA per line
+template <class K>
+int persistent_grid(K kern, int threads, size_t smem, int count) {
+  int per_sm = 0;
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem), "occupancy");
+  return std::max(1, std::min(count, std::max(1, per_sm) * num_sms()));
+}
+
 void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
   if (io.gi.count == 0) return;
   if (!io.in_cplx && ax.rhalf) {  // one real line per CTA, half-length DFT
@@ -289,8 +298,10 @@ void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
       ck(cudaFreeAsync(scr, st), "scratch");
       return;
     }
-    k_ranalyze<<<io.gi.count, std::min(256, line_threads(ax.hfft.M)),
-                 rsmem_bytes(ax, ax.hfft.M), st>>>(ax, io, nullptr);
+    const int thr = std::min(256, line_threads(ax.hfft.M));
+    const size_t sm = rsmem_bytes(ax, ax.hfft.M);
+    k_ranalyze<<<persistent_grid(k_ranalyze, thr, sm, io.gi.count), thr, sm, st>>>(ax, io,
+                                                                                  nullptr);
     launched("k_ranalyze");
     return;
   }
@@ -314,8 +325,10 @@ void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cuda
       ck(cudaFreeAsync(scr, st), "scratch");
       return;
     }
-    k_rsynth<<<io.gi.count, std::min(256, line_threads(ax.hfft.M)),
-               rsmem_bytes(ax, ax.hfft.M), st>>>(ax, io, sa, nullptr);
+    const int thr = std::min(256, line_threads(ax.hfft.M));
+    const size_t sm = rsmem_bytes(ax, ax.hfft.M);
+    k_rsynth<<<persistent_grid(k_rsynth, thr, sm, io.gi.count), thr, sm, st>>>(ax, io, sa,
+                                                                              nullptr);
     launched("k_rsynth");
     return;
   }

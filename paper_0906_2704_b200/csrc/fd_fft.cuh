@@ -93,9 +93,11 @@ __device__ __forceinline__ TwSm load_twiddles(double2* slots, const FftTables& T
 // One fused pass of LOGR radix-2 decimation-in-frequency stages on blocks of
 // size S (S >= 2^LOGR).  Items are disjoint element sets, so the pass is
 // in-place with no barrier inside.
+// nvalid < M: entries [nvalid, M) are read as zero (first pass of a
+// zero-padded convolution; saves the padding stores and a barrier).
 template <int LOGR>
 __device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S, const TwSm& tw,
-                                         int Mtw) {
+                                         int Mtw, int nvalid) {
   constexpr int R = 1 << LOGR;
   const int SR = S >> LOGR;
   const int items = M >> LOGR;
@@ -105,7 +107,8 @@ __device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S, 
     const int base = (it - j0) * R + j0;
     double2 v[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) v[q] = x[pidx(base + q * SR)];
+    for (int q = 0; q < R; ++q)
+      v[q] = base + q * SR < nvalid ? x[pidx(base + q * SR)] : czero();
 #pragma unroll
     for (int st = 0; st < LOGR; ++st) {
       const int half = R >> (st + 1);
@@ -180,10 +183,10 @@ __device__ __forceinline__ void fft_dif(double2* x, int M, int logM, const TwSm&
   while (rem > 0) {
     const int l = pass_logr(rem);
     switch (l) {
-      case 4: dif_pass<4>(x, M, S, tw, M); break;
-      case 3: dif_pass<3>(x, M, S, tw, M); break;
-      case 2: dif_pass<2>(x, M, S, tw, M); break;
-      default: dif_pass<1>(x, M, S, tw, M); break;
+      case 4: dif_pass<4>(x, M, S, tw, M, M); break;
+      case 3: dif_pass<3>(x, M, S, tw, M, M); break;
+      case 2: dif_pass<2>(x, M, S, tw, M, M); break;
+      default: dif_pass<1>(x, M, S, tw, M, M); break;
     }
     S >>= l;
     rem -= l;
@@ -199,10 +202,10 @@ __device__ __forceinline__ void fft_dif_local(double2* x, int M, int logM, int M
   while (rem > 0) {
     const int l = pass_logr(rem);
     switch (l) {
-      case 4: dif_pass<4>(x, M, S, tw, Mtw); break;
-      case 3: dif_pass<3>(x, M, S, tw, Mtw); break;
-      case 2: dif_pass<2>(x, M, S, tw, Mtw); break;
-      default: dif_pass<1>(x, M, S, tw, Mtw); break;
+      case 4: dif_pass<4>(x, M, S, tw, Mtw, M); break;
+      case 3: dif_pass<3>(x, M, S, tw, Mtw, M); break;
+      case 2: dif_pass<2>(x, M, S, tw, Mtw, M); break;
+      default: dif_pass<1>(x, M, S, tw, Mtw, M); break;
     }
     S >>= l;
     rem -= l;
@@ -243,7 +246,8 @@ __device__ __forceinline__ void fft_dit(double2* x, int M, int logM, const TwSm&
 // all threads in a warp is one contiguous 512-byte read.
 template <int LOGR>
 __device__ __forceinline__ void mid_pass(double2* __restrict__ x, int M,
-                                         const double2* __restrict__ bhat, const TwSm& tw) {
+                                         const double2* __restrict__ bhat, const TwSm& tw,
+                                         int nvalid) {
   constexpr int R = 1 << LOGR;
   const int items = M >> LOGR;
   const int twstep = M / R;
@@ -253,7 +257,7 @@ __device__ __forceinline__ void mid_pass(double2* __restrict__ x, int M,
 #pragma unroll
     for (int q = 0; q < R; ++q) bh[q] = __ldg(&bhat[q * items + it]);
 #pragma unroll
-    for (int q = 0; q < R; ++q) v[q] = x[pidx(base + q)];
+    for (int q = 0; q < R; ++q) v[q] = base + q < nvalid ? x[pidx(base + q)] : czero();
     (void)twstep;
     // DIF stages with j0 = 0: every twiddle is a radix-16 constant
 #pragma unroll
@@ -294,9 +298,9 @@ __device__ __forceinline__ void mid_pass(double2* __restrict__ x, int M,
 // one half of a split convolution, see bluestein_core).  bhat points at the
 // Mloc entries of this block.  Requires a barrier before; ends with one.
 __device__ __forceinline__ void bluestein_run(double2* x, int M, int logM, int Mtw,
-                                              const double2* bhat, const TwSm& tw) {
+                                              const double2* bhat, const TwSm& tw, int nvalid) {
   if (logM == 0) {
-    if (threadIdx.x == 0) x[0] = cmul(x[0], bhat[0]);
+    if (threadIdx.x == 0) x[0] = nvalid > 0 ? cmul(x[0], bhat[0]) : czero();
     __syncthreads();
     return;
   }
@@ -309,20 +313,22 @@ __device__ __forceinline__ void bluestein_run(double2* x, int M, int logM, int M
   }
   int S = M;
   for (int p = 0; p < np - 1; ++p) {
+    const int nv = p == 0 ? nvalid : M;
     switch (ls[p]) {
-      case 4: dif_pass<4>(x, M, S, tw, Mtw); break;
-      case 3: dif_pass<3>(x, M, S, tw, Mtw); break;
-      case 2: dif_pass<2>(x, M, S, tw, Mtw); break;
-      default: dif_pass<1>(x, M, S, tw, Mtw); break;
+      case 4: dif_pass<4>(x, M, S, tw, Mtw, nv); break;
+      case 3: dif_pass<3>(x, M, S, tw, Mtw, nv); break;
+      case 2: dif_pass<2>(x, M, S, tw, Mtw, nv); break;
+      default: dif_pass<1>(x, M, S, tw, Mtw, nv); break;
     }
     S >>= ls[p];
     __syncthreads();
   }
+  const int nvm = np == 1 ? nvalid : M;
   switch (ls[np - 1]) {  // S == 2^ls[np-1] here
-    case 4: mid_pass<4>(x, M, bhat, tw); break;
-    case 3: mid_pass<3>(x, M, bhat, tw); break;
-    case 2: mid_pass<2>(x, M, bhat, tw); break;
-    default: mid_pass<1>(x, M, bhat, tw); break;
+    case 4: mid_pass<4>(x, M, bhat, tw, nvm); break;
+    case 3: mid_pass<3>(x, M, bhat, tw, nvm); break;
+    case 2: mid_pass<2>(x, M, bhat, tw, nvm); break;
+    default: mid_pass<1>(x, M, bhat, tw, nvm); break;
   }
   __syncthreads();
   for (int p = np - 2; p >= 0; --p) {
@@ -337,11 +343,13 @@ __device__ __forceinline__ void bluestein_run(double2* x, int M, int logM, int M
   }
 }
 
-// Bluestein core: x holds a_j = z_j c_j (j < L) and zeros up to M; on return
-// x_k holds the circular convolution (a * b)_k; the caller multiplies by c_k.
+// Bluestein core: x holds a_j = z_j c_j (j < nvalid <= L; entries beyond are
+// taken as zero, whatever the buffer holds); on return x_k holds the circular
+// convolution (a * b)_k; the caller multiplies by c_k.
 // Requires a barrier before the call (the caller's loads); ends with one.
-__device__ __forceinline__ void bluestein_core(double2* x, const FftTables& T, const TwSm& tw) {
-  bluestein_run(x, T.M, T.logM, T.M, T.bhat, tw);
+__device__ __forceinline__ void bluestein_core(double2* x, const FftTables& T, const TwSm& tw,
+                                               int nvalid) {
+  bluestein_run(x, T.M, T.logM, T.M, T.bhat, tw, nvalid);
 }
 
 // Split convolution for M beyond shared memory (M = 2 * Mloc).  The input a
@@ -352,13 +360,13 @@ __device__ __forceinline__ void bluestein_core(double2* x, const FftTables& T, c
 //   part 1: x = a (.) W^t  ->  y1   (caller saves y1)
 //   part 0: x = a          ->  y0   (caller combines)
 __device__ __forceinline__ void bluestein_half(double2* x, const FftTables& T, const TwSm& tw,
-                                               int part) {
+                                               int part, int nvalid) {
   const int Mloc = T.M >> 1;
   if (part == 1) {
-    for (int j = threadIdx.x; j < Mloc; j += blockDim.x) x[pidx(j)] = cmul(x[pidx(j)], tw(j));
+    for (int j = threadIdx.x; j < nvalid; j += blockDim.x) x[pidx(j)] = cmul(x[pidx(j)], tw(j));
     __syncthreads();
   }
-  bluestein_run(x, Mloc, T.logM - 1, T.M, T.bhat + part * Mloc, tw);
+  bluestein_run(x, Mloc, T.logM - 1, T.M, T.bhat + part * Mloc, tw, nvalid);
 }
 
 // ----------------------------------------------------------------------------

@@ -456,7 +456,7 @@ __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
   }
   __syncthreads();
 
-  bluestein_core(x, ax.fft, tw);
+  bluestein_core(x, ax.fft, tw, ax.fft.M);
 
   const double2 b00 = bc[0], b10 = bc[1], b01 = bc[2], b11 = bc[3];
   const long long oo0 = line_offset(io.go, l0);
@@ -691,7 +691,7 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
   if (dots) block_sum<8>(acc, red);
   __syncthreads();
 
-  bluestein_core(x, ax.fft, tw);
+  bluestein_core(x, ax.fft, tw, ax.fft.M);
 
   const long long oo0 = line_offset(io.go, l0);
   const long long oo1 = has1 ? line_offset(io.go, l0 + 1) : oo0;
@@ -868,10 +868,51 @@ __device__ __forceinline__ Fold fold_terms(const AxisDev& ax, LD ld) {
   return f;
 }
 
-// smem of the real-line kernels: buffer, FFT twiddles, rtw and DCT tables
+// smem of the real-line kernels: buffer, FFT twiddles, rtw and DCT tables,
+// then one mbarrier
 __host__ __device__ __forceinline__ int rline_slots(const AxisDev& ax, int Mloc) {
   return pidx(Mloc) + 1 + kTwSlots + tw2_slots(ax.hfft.L) +
          (ax.kind == IK_COS ? tw2_slots(ax.m) : 0);
+}
+
+// Input staging of the real-line kernels: the n doubles of the NEXT line are
+// bulk-copied (TMA engine) into the upper part of the FFT buffer, which is
+// free from the end of the convolution until the next line's first DIF pass
+// (the load phase writes only [0, h) and that pass reads the rest as zero).
+// A line is staged when its row is contiguous and 16-byte aligned.
+struct Stage {
+  double* buf;     // smem, >= n doubles
+  uint64_t* bar;   // mbarrier
+  bool on;         // kernel-level: layout allows staging
+  uint32_t phase;
+};
+__device__ __forceinline__ bool stage_line(const Stage& s, const LineIO& io, int l, int n) {
+  if (!s.on || l >= io.gi.count) return false;
+  const double* src = reinterpret_cast<const double*>(io.in) + line_offset(io.gi, l);
+  return (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+}
+// thread 0: start the copy of line l (after a barrier that ends all reads of
+// the region through the generic proxy)
+__device__ __forceinline__ void stage_issue(Stage& s, const LineIO& io, int l, int n) {
+  if (!stage_line(s, io, l, n)) return;
+  const double* src = reinterpret_cast<const double*>(io.in) + line_offset(io.gi, l);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_expect_tx(s.bar, (uint32_t)n * 8);
+  bulk_g2s(s.buf, src, (uint32_t)n * 8, s.bar);
+}
+__device__ __forceinline__ Stage stage_init(double2* x, int h, int Mloc, double2* after, int n,
+                                            const LineIO& io, bool big) {
+  Stage s;
+  s.buf = reinterpret_cast<double*>(x + pidx(h) + 1);
+  s.bar = reinterpret_cast<uint64_t*>(after);
+  s.phase = 0;
+  s.on = !big && io.gi.elem_stride == 1 && (n & 1) == 0 &&
+         2LL * (pidx(Mloc) - pidx(h)) >= (long long)n;
+  if (threadIdx.x == 0 && s.on) {
+    mbar_init(s.bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  return s;
 }
 
 // scr != null: split-convolution mode for M beyond shared memory
@@ -895,13 +936,21 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   const bool pk = io.pack && ax.kind == IK_FOURIER;
   double2* scrA = big ? scr + (long long)blockIdx.x * 2 * h : nullptr;
   double2* scrY = big ? scrA + h : nullptr;
+  Stage stg = stage_init(x, h, Mloc, sm + rline_slots(ax, Mloc), ax.n, io, big);
   __syncthreads();
+  if (threadIdx.x == 0) stage_issue(stg, io, blockIdx.x, ax.n);
   for (int l = blockIdx.x; l < io.gi.count; l += gridDim.x) {
   const long long oi = line_offset(io.gi, l), es = io.gi.elem_stride;
   const int n = ax.n, m = ax.m;
   const double2* chirp = T.chirp;
   const double* in = reinterpret_cast<const double*>(io.in);
-  auto ld = [&](int e) { return __ldg(in + oi + e * es); };
+  const bool st = stage_line(stg, io, l, n);
+  if (st) {
+    mbar_wait(stg.bar, stg.phase);
+    stg.phase ^= 1;
+  }
+  const double* sin_ = stg.buf;
+  auto ld = [&](int e) { return st ? sin_[e] : __ldg(in + oi + e * es); };
   const Fold fd = fold_terms(ax, ld);
   // folded interior sample s
   auto xin = [&](int s) {
@@ -910,7 +959,6 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
     return v;
   };
   const int half = (m + 1) / 2;
-  for (int j = h + threadIdx.x; j < Mloc; j += blockDim.x) x[pidx(j)] = czero();
 #pragma unroll 4
   for (int j = threadIdx.x; j < h; j += blockDim.x) {
     const int p0 = 2 * j, p1 = 2 * j + 1;
@@ -933,17 +981,18 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   __syncthreads();
 
   if (!big) {
-    bluestein_core(x, T, tw);
+    bluestein_core(x, T, tw, h);
+    // the post phase reads [0, h) only: stage the next line behind it
+    if (threadIdx.x == 0) stage_issue(stg, io, l + gridDim.x, n);
   } else {
     for (int j = threadIdx.x; j < h; j += blockDim.x) scrA[j] = x[pidx(j)];
-    bluestein_half(x, T, tw, 1);  // x = a (.) W, convolved: y1
+    bluestein_half(x, T, tw, 1, h);  // x = a (.) W, convolved: y1
     for (int j = threadIdx.x; j < h; j += blockDim.x) {
       scrY[j] = x[pidx(j)];
       x[pidx(j)] = scrA[j];
     }
-    for (int j = h + threadIdx.x; j < Mloc; j += blockDim.x) x[pidx(j)] = czero();
     __syncthreads();
-    bluestein_half(x, T, tw, 0);  // y0
+    bluestein_half(x, T, tw, 0, h);  // y0
   }
   // Z_k = (a * b)_k c_k; in split mode the lower half of the last DIT stage
   auto zv = [&](int k) {
@@ -1065,20 +1114,34 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
   const bool pk = io.pack && ax.kind == IK_FOURIER;
   double2* scrA = big ? scr + (long long)blockIdx.x * 2 * h : nullptr;
   double2* scrY = big ? scrA + h : nullptr;
+  // staging needs real (or packed) input lines of n doubles
+  Stage stg = stage_init(x, h, Mloc, sm + rline_slots(ax, Mloc), ax.n, io,
+                         big || (io.in_cplx && !pk));
   __syncthreads();
+  if (threadIdx.x == 0) stage_issue(stg, io, blockIdx.x, ax.n);
   for (int l = blockIdx.x; l < io.gi.count; l += gridDim.x) {
   const long long oi = line_offset(io.gi, l);
   const int n = ax.n, m = ax.m;
   const double2* chirp = T.chirp;
+  const bool st = stage_line(stg, io, l, n);
+  if (st) {
+    mbar_wait(stg.bar, stg.phase);
+    stg.phase ^= 1;
+  }
   auto filt = [&](int e, double2 c) { return coeff_filter(ax, sa, io.gi, l, e, c); };
-  auto cf = [&](int e) { return filt(e, ldc(io.in, io.in_cplx, oi + e * io.gi.elem_stride)); };
+  auto cf = [&](int e) {
+    return filt(e, st ? make_double2(stg.buf[e], 0.0)
+                      : ldc(io.in, io.in_cplx, oi + e * io.gi.elem_stride));
+  };
   const double2* Pin =
-      reinterpret_cast<const double2*>(reinterpret_cast<const double*>(io.in) + oi);
+      st ? reinterpret_cast<const double2*>(stg.buf)
+         : reinterpret_cast<const double2*>(reinterpret_cast<const double*>(io.in) + oi);
+  auto ldp = [&](int i) { return st ? Pin[i] : __ldg(Pin + i); };
   const int off = ax.bordered ? 1 : 0;
   double u0 = 0.0, un = 0.0;
   if (ax.bordered) {
     if (pk) {
-      const double2 b = __ldg(Pin);
+      const double2 b = ldp(0);
       u0 = filt(0, make_double2(b.x, 0.0)).x;
       un = filt(n - 1, make_double2(b.y, 0.0)).x;
     } else {
@@ -1088,17 +1151,13 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
   }
   if (ax.kind == IK_SINE) {  // Q c_mid: R2C of the odd extension (Q is an involution)
     const int R = 2 * (m + 1);
-    for (int j = threadIdx.x; j < Mloc; j += blockDim.x) {
-      double2 val = czero();
-      if (j < h) {
-        auto ext = [&](int p) -> double {
-          if (p == 0 || p == m + 1) return 0.0;
-          if (p <= m) return cf(interior_elem(ax, p - 1)).x;
-          return -cf(interior_elem(ax, R - 1 - p)).x;
-        };
-        val = cmul(make_double2(ext(2 * j), ext(2 * j + 1)), __ldg(&chirp[j]));
-      }
-      x[pidx(j)] = val;
+    for (int j = threadIdx.x; j < h; j += blockDim.x) {
+      auto ext = [&](int p) -> double {
+        if (p == 0 || p == m + 1) return 0.0;
+        if (p <= m) return cf(interior_elem(ax, p - 1)).x;
+        return -cf(interior_elem(ax, R - 1 - p)).x;
+      };
+      x[pidx(j)] = cmul(make_double2(ext(2 * j), ext(2 * j + 1)), __ldg(&chirp[j]));
     }
   } else {
     // cosine works on conj(buf_i) = s_i c_i conj(tw_i) (DCT-III, trig.cpp:201-212)
@@ -1120,12 +1179,12 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
       double2 Xk, Xkh, Xp, Xph;  // X at k, k+h, kp, kp+h
       if (pk) {  // exactly Hermitian: X_{m-q} = conj X_q
         if (k == 0) {
-          const double2 b = __ldg(Pin + off);
+          const double2 b = ldp(off);
           Xk = Xp = filt(interior_elem(ax, 0), make_double2(b.x, 0.0));
           Xkh = Xph = filt(interior_elem(ax, h), make_double2(b.y, 0.0));
         } else {
-          const double2 fk = filt(interior_elem(ax, k), __ldg(Pin + off + k));
-          const double2 fp = kp != k ? filt(interior_elem(ax, kp), __ldg(Pin + off + kp)) : fk;
+          const double2 fk = filt(interior_elem(ax, k), ldp(off + k));
+          const double2 fp = kp != k ? filt(interior_elem(ax, kp), ldp(off + kp)) : fk;
           Xk = fk;
           Xp = fp;
           Xkh = cconj(fp);  // m - (k+h) = kp
@@ -1148,22 +1207,21 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
       x[pidx(k)] = cmul(cconj(zin(k, Xk, Xkh)), __ldg(&chirp[k]));
       if (kp != k) x[pidx(kp)] = cmul(cconj(zin(kp, Xp, Xph)), __ldg(&chirp[kp]));
     }
-    for (int j = h + threadIdx.x; j < Mloc; j += blockDim.x) x[pidx(j)] = czero();
   }
   __syncthreads();
 
   if (!big) {
-    bluestein_core(x, T, tw);
+    bluestein_core(x, T, tw, h);
+    if (threadIdx.x == 0) stage_issue(stg, io, l + gridDim.x, n);
   } else {
     for (int j = threadIdx.x; j < h; j += blockDim.x) scrA[j] = x[pidx(j)];
-    bluestein_half(x, T, tw, 1);
+    bluestein_half(x, T, tw, 1, h);
     for (int j = threadIdx.x; j < h; j += blockDim.x) {
       scrY[j] = x[pidx(j)];
       x[pidx(j)] = scrA[j];
     }
-    for (int j = h + threadIdx.x; j < Mloc; j += blockDim.x) x[pidx(j)] = czero();
     __syncthreads();
-    bluestein_half(x, T, tw, 0);
+    bluestein_half(x, T, tw, 0, h);
   }
   auto zv = [&](int k) {
     const double2 y = big ? cadd(x[pidx(k)], cmulc(scrY[k], tw(k))) : x[pidx(k)];
