@@ -276,6 +276,15 @@ int num_sms() {
   return nsm;
 }
 
+// on-chip real-line kernels: shared memory, with the chirp copied in when it
+// still leaves room for two CTAs per SM (sets io.chirp_smem)
+size_t rline_smem(const AxisDev& ax, LineIO& io) {
+  const size_t base = rsmem_bytes(ax, ax.hfft.M);
+  const size_t with = base + (size_t)ax.hfft.L * sizeof(double2);
+  io.chirp_smem = with <= 112 * 1024;
+  return io.chirp_smem ? with : base;
+}
+
 // persistent grid of a real-line kernel: every CTA slot of the device, at most
 // one CTA per line
 template <class K>
@@ -299,8 +308,9 @@ void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
       return;
     }
     const int thr = std::min(256, line_threads(ax.hfft.M));
-    const size_t sm = rsmem_bytes(ax, ax.hfft.M);
-    k_ranalyze<<<persistent_grid(k_ranalyze, thr, sm, io.gi.count), thr, sm, st>>>(ax, io,
+    LineIO io2 = io;
+    const size_t sm = rline_smem(ax, io2);
+    k_ranalyze<<<persistent_grid(k_ranalyze, thr, sm, io.gi.count), thr, sm, st>>>(ax, io2,
                                                                                   nullptr);
     launched("k_ranalyze");
     return;
@@ -326,8 +336,9 @@ void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cuda
       return;
     }
     const int thr = std::min(256, line_threads(ax.hfft.M));
-    const size_t sm = rsmem_bytes(ax, ax.hfft.M);
-    k_rsynth<<<persistent_grid(k_rsynth, thr, sm, io.gi.count), thr, sm, st>>>(ax, io, sa,
+    LineIO io2 = io;
+    const size_t sm = rline_smem(ax, io2);
+    k_rsynth<<<persistent_grid(k_rsynth, thr, sm, io.gi.count), thr, sm, st>>>(ax, io2, sa,
                                                                               nullptr);
     launched("k_rsynth");
     return;

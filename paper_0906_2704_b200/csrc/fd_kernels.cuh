@@ -327,6 +327,7 @@ struct LineIO {
   long long wstride;
   long long wn;  // weights actually written; [wn, wstride) is zero-filled
   int pack;      // Fourier lines of real data stored Hermitian-packed (k_ranalyze)
+  int chirp_smem;  // real-line kernels: copy the Bluestein chirp to shared memory
 };
 
 __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
@@ -553,14 +554,15 @@ struct SynthArgs {
 
 // coefficient c of element e of line l after the synthesis mode's scaling
 // (apply_tikhonov_filter, regularize.hpp:42-58, for mode 1)
+// (mu: the line's regularisation parameter, read once per line by the caller)
 __device__ __forceinline__ double2 coeff_filter(const AxisDev& ax, const SynthArgs& sa,
-                                                const Lines& g, int l, int e, double2 c) {
+                                                const Lines& g, int l, int e, double2 c,
+                                                double mu) {
   if (sa.mode == 0) return c;
   double2 d;
   double s;
   spectral_at(sa.sp, g, l, e, d, s);
   if (sa.mode == 2) return ax.cplx ? cmul(c, d) : make_double2(c.x * d.x, 0.0);
-  const double mu = __ldg(&sa.mu_item[l / g.per_item]);
   if (ax.cplx) {
     const double den = (d.x * d.x + d.y * d.y) + mu * s * s;
     return cmul(c, make_double2(d.x / den, -d.y / den));
@@ -569,9 +571,40 @@ __device__ __forceinline__ double2 coeff_filter(const AxisDev& ax, const SynthAr
   return make_double2(c.x * f, 0.0);
 }
 
+// 1/x for positive normal x: MUFU reciprocal seed + two Newton steps (<= 1 ulp)
+__device__ __forceinline__ double rcp_pos(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+// coeff_filter of the real-line synthesis: the two quotients conj(d)/den share
+// one reciprocal (within 1 ulp of the reference's two divisions)
+__device__ __forceinline__ double2 coeff_filter_fast(const AxisDev& ax, const SynthArgs& sa,
+                                                     const Lines& g, int l, int e, double2 c,
+                                                     double mu) {
+  if (sa.mode != 1) return coeff_filter(ax, sa, g, l, e, c, mu);
+  double2 d;
+  double s;
+  spectral_at(sa.sp, g, l, e, d, s);
+  if (ax.cplx) {
+    const double r = rcp_pos((d.x * d.x + d.y * d.y) + mu * s * s);
+    return cmul(c, make_double2(d.x * r, -d.y * r));
+  }
+  return make_double2(c.x * (d.x * rcp_pos(d.x * d.x + mu * s * s)), 0.0);
+}
+
+__device__ __forceinline__ double line_mu(const SynthArgs& sa, const Lines& g, int l) {
+  return sa.mode == 1 ? __ldg(&sa.mu_item[l / g.per_item]) : 0.0;
+}
+
 __device__ __forceinline__ double2 coeff_at(const AxisDev& ax, const LineIO& io,
                                             const SynthArgs& sa, int l, long long off, int e) {
-  return coeff_filter(ax, sa, io.gi, l, e, ldc(io.in, io.in_cplx, off + e * io.gi.elem_stride));
+  return coeff_filter(ax, sa, io.gi, l, e, ldc(io.in, io.in_cplx, off + e * io.gi.elem_stride),
+                      line_mu(sa, io.gi, l));
 }
 
 __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs sa) {
@@ -937,12 +970,18 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   double2* scrA = big ? scr + (long long)blockIdx.x * 2 * h : nullptr;
   double2* scrY = big ? scrA + h : nullptr;
   Stage stg = stage_init(x, h, Mloc, sm + rline_slots(ax, Mloc), ax.n, io, big);
+  const double2* chirp = T.chirp;
+  if (io.chirp_smem) {  // persistent CTA: the chirp once per CTA in shared memory
+    double2* cs = sm + rline_slots(ax, Mloc) + 1;
+    for (int j = threadIdx.x; j < h; j += blockDim.x) cs[j] = T.chirp[j];
+    chirp = cs;
+  }
+  auto chirp_at = [&](int j) { return io.chirp_smem ? chirp[j] : __ldg(&chirp[j]); };
   __syncthreads();
   if (threadIdx.x == 0) stage_issue(stg, io, blockIdx.x, ax.n);
   for (int l = blockIdx.x; l < io.gi.count; l += gridDim.x) {
   const long long oi = line_offset(io.gi, l), es = io.gi.elem_stride;
   const int n = ax.n, m = ax.m;
-  const double2* chirp = T.chirp;
   const double* in = reinterpret_cast<const double*>(io.in);
   const bool st = stage_line(stg, io, l, n);
   if (st) {
@@ -976,7 +1015,7 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
       a = xin(ax.kind == IK_COS ? makhoul_src(p0, m, half) : p0);
       b = xin(ax.kind == IK_COS ? makhoul_src(p1, m, half) : p1);
     }
-    x[pidx(j)] = cmul(make_double2(a, b), __ldg(&chirp[j]));
+    x[pidx(j)] = cmul(make_double2(a, b), chirp_at(j));
   }
   __syncthreads();
 
@@ -997,7 +1036,7 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   // Z_k = (a * b)_k c_k; in split mode the lower half of the last DIT stage
   auto zv = [&](int k) {
     const double2 y = big ? cadd(x[pidx(k)], cmulc(scrY[k], tw(k))) : x[pidx(k)];
-    return cmul(y, __ldg(&chirp[k]));
+    return cmul(y, chirp_at(k));
   };
 
   const long long oo = line_offset(io.go, l), eso = io.go.elem_stride;
@@ -1117,18 +1156,25 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
   // staging needs real (or packed) input lines of n doubles
   Stage stg = stage_init(x, h, Mloc, sm + rline_slots(ax, Mloc), ax.n, io,
                          big || (io.in_cplx && !pk));
+  const double2* chirp = T.chirp;
+  if (io.chirp_smem) {  // persistent CTA: the chirp once per CTA in shared memory
+    double2* cs = sm + rline_slots(ax, Mloc) + 1;
+    for (int j = threadIdx.x; j < h; j += blockDim.x) cs[j] = T.chirp[j];
+    chirp = cs;
+  }
+  auto chirp_at = [&](int j) { return io.chirp_smem ? chirp[j] : __ldg(&chirp[j]); };
   __syncthreads();
   if (threadIdx.x == 0) stage_issue(stg, io, blockIdx.x, ax.n);
   for (int l = blockIdx.x; l < io.gi.count; l += gridDim.x) {
   const long long oi = line_offset(io.gi, l);
   const int n = ax.n, m = ax.m;
-  const double2* chirp = T.chirp;
   const bool st = stage_line(stg, io, l, n);
   if (st) {
     mbar_wait(stg.bar, stg.phase);
     stg.phase ^= 1;
   }
-  auto filt = [&](int e, double2 c) { return coeff_filter(ax, sa, io.gi, l, e, c); };
+  const double mu = line_mu(sa, io.gi, l);
+  auto filt = [&](int e, double2 c) { return coeff_filter_fast(ax, sa, io.gi, l, e, c, mu); };
   auto cf = [&](int e) {
     return filt(e, st ? make_double2(stg.buf[e], 0.0)
                       : ldc(io.in, io.in_cplx, oi + e * io.gi.elem_stride));
@@ -1157,7 +1203,7 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
         if (p <= m) return cf(interior_elem(ax, p - 1)).x;
         return -cf(interior_elem(ax, R - 1 - p)).x;
       };
-      x[pidx(j)] = cmul(make_double2(ext(2 * j), ext(2 * j + 1)), __ldg(&chirp[j]));
+      x[pidx(j)] = cmul(make_double2(ext(2 * j), ext(2 * j + 1)), chirp_at(j));
     }
   } else {
     // cosine works on conj(buf_i) = s_i c_i conj(tw_i) (DCT-III, trig.cpp:201-212)
@@ -1204,8 +1250,8 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
         const double2 Ev = cadd(Xa, Xb);
         return make_double2(Ev.x - Od.y, Ev.y + Od.x);
       };
-      x[pidx(k)] = cmul(cconj(zin(k, Xk, Xkh)), __ldg(&chirp[k]));
-      if (kp != k) x[pidx(kp)] = cmul(cconj(zin(kp, Xp, Xph)), __ldg(&chirp[kp]));
+      x[pidx(k)] = cmul(cconj(zin(k, Xk, Xkh)), chirp_at(k));
+      if (kp != k) x[pidx(kp)] = cmul(cconj(zin(kp, Xp, Xph)), chirp_at(kp));
     }
   }
   __syncthreads();
@@ -1225,7 +1271,7 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
   }
   auto zv = [&](int k) {
     const double2 y = big ? cadd(x[pidx(k)], cmulc(scrY[k], tw(k))) : x[pidx(k)];
-    return cmul(y, __ldg(&chirp[k]));
+    return cmul(y, chirp_at(k));
   };
 
   const long long oo = line_offset(io.go, l), eso = io.go.elem_stride;
@@ -1341,15 +1387,6 @@ __device__ __forceinline__ double gcv_w(const GcvData& g, int item, long long e)
   return gcv_w1(g, base + e);
 }
 
-// 1/x for positive normal x: MUFU reciprocal seed + two Newton steps (<= 1 ulp)
-__device__ __forceinline__ double rcp_pos(double x) {
-  double y;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double e = fma(-x, y, 1.0);
-  y = fma(y, e, y);
-  e = fma(-x, y, 1.0);
-  return fma(y, e, y);
-}
 
 // Single items / small batches: one warp per (item, element chunk); each lane
 // owns KC grid values.  Elements stream in tiles of 32 -- lane t loads and
