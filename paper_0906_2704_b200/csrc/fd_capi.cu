@@ -655,6 +655,13 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
     d.q_s = bc == BC_HOC_COSINE ? 2.0 * kPi / (2 * n - 4) : 2.0 * kPi / (n - 2);
     d.q_o = bc == BC_HOC_COSINE ? -kPi / (2 * n - 4) : -2.0 * kPi / (n - 2);
   }
+  if (d.qmode == 0) {
+    d.qa1 = 1.0 - d.q_s;
+    d.qa2 = 1.0 - (n - 2) * d.q_s;
+  } else {
+    d.qa1 = d.q_gb - d.q_o - d.q_s;
+    d.qa2 = d.q_gb - d.q_o - (n - 2) * d.q_s;
+  }
   if (d.correction) {
     auto impulse = [&](const std::vector<cplx>& r, int* at, double* val) {
       int k = 0;

@@ -95,20 +95,20 @@ __device__ __forceinline__ TwSm load_twiddles(double2* slots, const FftTables& T
 // in-place with no barrier inside.
 // nvalid < M: entries [nvalid, M) are read as zero (first pass of a
 // zero-padded convolution; saves the padding stores and a barrier).
-template <int LOGR>
+template <int LOGR, bool PAD = false>
 __device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S, const TwSm& tw,
                                          int Mtw, int nvalid) {
   constexpr int R = 1 << LOGR;
   const int SR = S >> LOGR;
   const int items = M >> LOGR;
-  const int twstep = Mtw / S;  // tw is a table for size Mtw >= M
+  const int twstep = Mtw >> (__ffs(S) - 1);  // Mtw / S: tw is a table for size Mtw >= M
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int j0 = it & (SR - 1);
     const int base = (it - j0) * R + j0;
     double2 v[R];
 #pragma unroll
     for (int q = 0; q < R; ++q)
-      v[q] = base + q * SR < nvalid ? x[pidx(base + q * SR)] : czero();
+      v[q] = (!PAD || base + q * SR < nvalid) ? x[pidx(base + q * SR)] : czero();
 #pragma unroll
     for (int st = 0; st < LOGR; ++st) {
       const int half = R >> (st + 1);
@@ -136,7 +136,7 @@ __device__ __forceinline__ void dit_pass(double2* __restrict__ x, int M, int S, 
   constexpr int R = 1 << LOGR;
   const int SR = S >> LOGR;
   const int items = M >> LOGR;
-  const int twstep = Mtw / S;  // tw is a table for size Mtw >= M
+  const int twstep = Mtw >> (__ffs(S) - 1);  // Mtw / S: tw is a table for size Mtw >= M
   for (int it = threadIdx.x; it < items; it += blockDim.x) {
     const int j0 = it & (SR - 1);
     const int base = (it - j0) * R + j0;
@@ -244,7 +244,7 @@ __device__ __forceinline__ void fft_dit(double2* x, int M, int logM, const TwSm&
 // store.  Saves two shared-memory round trips per Bluestein convolution.
 // bhat is stored thread-major for this pass (bhat_store_index), so load q of
 // all threads in a warp is one contiguous 512-byte read.
-template <int LOGR>
+template <int LOGR, bool PAD = false>
 __device__ __forceinline__ void mid_pass(double2* __restrict__ x, int M,
                                          const double2* __restrict__ bhat, const TwSm& tw,
                                          int nvalid) {
@@ -257,7 +257,7 @@ __device__ __forceinline__ void mid_pass(double2* __restrict__ x, int M,
 #pragma unroll
     for (int q = 0; q < R; ++q) bh[q] = __ldg(&bhat[q * items + it]);
 #pragma unroll
-    for (int q = 0; q < R; ++q) v[q] = base + q < nvalid ? x[pidx(base + q)] : czero();
+    for (int q = 0; q < R; ++q) v[q] = (!PAD || base + q < nvalid) ? x[pidx(base + q)] : czero();
     (void)twstep;
     // DIF stages with j0 = 0: every twiddle is a radix-16 constant
 #pragma unroll
@@ -313,22 +313,38 @@ __device__ __forceinline__ void bluestein_run(double2* x, int M, int logM, int M
   }
   int S = M;
   for (int p = 0; p < np - 1; ++p) {
-    const int nv = p == 0 ? nvalid : M;
-    switch (ls[p]) {
-      case 4: dif_pass<4>(x, M, S, tw, Mtw, nv); break;
-      case 3: dif_pass<3>(x, M, S, tw, Mtw, nv); break;
-      case 2: dif_pass<2>(x, M, S, tw, Mtw, nv); break;
-      default: dif_pass<1>(x, M, S, tw, Mtw, nv); break;
+    if (p == 0 && nvalid < M) {  // zero padding: only the first pass reads it
+      switch (ls[p]) {
+        case 4: dif_pass<4, true>(x, M, S, tw, Mtw, nvalid); break;
+        case 3: dif_pass<3, true>(x, M, S, tw, Mtw, nvalid); break;
+        case 2: dif_pass<2, true>(x, M, S, tw, Mtw, nvalid); break;
+        default: dif_pass<1, true>(x, M, S, tw, Mtw, nvalid); break;
+      }
+    } else {
+      switch (ls[p]) {
+        case 4: dif_pass<4>(x, M, S, tw, Mtw, M); break;
+        case 3: dif_pass<3>(x, M, S, tw, Mtw, M); break;
+        case 2: dif_pass<2>(x, M, S, tw, Mtw, M); break;
+        default: dif_pass<1>(x, M, S, tw, Mtw, M); break;
+      }
     }
     S >>= ls[p];
     __syncthreads();
   }
-  const int nvm = np == 1 ? nvalid : M;
-  switch (ls[np - 1]) {  // S == 2^ls[np-1] here
-    case 4: mid_pass<4>(x, M, bhat, tw, nvm); break;
-    case 3: mid_pass<3>(x, M, bhat, tw, nvm); break;
-    case 2: mid_pass<2>(x, M, bhat, tw, nvm); break;
-    default: mid_pass<1>(x, M, bhat, tw, nvm); break;
+  if (np == 1 && nvalid < M) {
+    switch (ls[0]) {
+      case 4: mid_pass<4, true>(x, M, bhat, tw, nvalid); break;
+      case 3: mid_pass<3, true>(x, M, bhat, tw, nvalid); break;
+      case 2: mid_pass<2, true>(x, M, bhat, tw, nvalid); break;
+      default: mid_pass<1, true>(x, M, bhat, tw, nvalid); break;
+    }
+  } else {
+    switch (ls[np - 1]) {  // S == 2^ls[np-1] here
+      case 4: mid_pass<4>(x, M, bhat, tw, M); break;
+      case 3: mid_pass<3>(x, M, bhat, tw, M); break;
+      case 2: mid_pass<2>(x, M, bhat, tw, M); break;
+      default: mid_pass<1>(x, M, bhat, tw, M); break;
+    }
   }
   __syncthreads();
   for (int p = np - 2; p >= 0; --p) {

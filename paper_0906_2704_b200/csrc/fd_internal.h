@@ -58,6 +58,11 @@ struct AxisDev {
   int ia, ib, top_i, bot_i, qmode;
   double ra1, rb1, q0;
   double q_gb, q_s, q_o, q_inv;
+  // q over the interior as polynomials in the interior index s:
+  //   q[s+1] = (qa1 - q_s s)^k q_inv,  q[n-2-s] = (qa2 + q_s s)^k q_inv,  k = 2 (qmode 1)
+  //   or 1 (qmode 0), so a border combination a q[s+1] + b q[n-2-s] is one
+  //   quadratic per line (border_poly).
+  double qa1, qa2;
   double cavr[4], capr[4];
 };
 
@@ -74,6 +79,7 @@ struct Lines {
 };
 
 __host__ __device__ __forceinline__ long long line_offset(const Lines& g, int l) {
+  if (g.per_item == 1) return (long long)l * g.item_stride;
   return (long long)(l / g.per_item) * g.item_stride + (long long)(l % g.per_item) * g.line_stride;
 }
 

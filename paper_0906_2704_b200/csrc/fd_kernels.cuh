@@ -870,6 +870,29 @@ __device__ __forceinline__ double q_at(const AxisDev& ax, int e) {
   return t * t * ax.q_inv;
 }
 
+// a q[s+1] + b q[n-2-s] over the interior index s, as c0 + s (c1 + s c2)
+struct BorderPoly {
+  double c0, c1, c2;
+  __device__ __forceinline__ double operator()(int s) const {
+    const double t = (double)s;
+    return fma(fma(c2, t, c1), t, c0);
+  }
+};
+__device__ __forceinline__ BorderPoly border_poly(const AxisDev& ax, double a, double b) {
+  BorderPoly p;
+  const double qs = ax.q_s, k = ax.q_inv;
+  if (ax.qmode == 0) {
+    p.c0 = k * (a * ax.qa1 + b * ax.qa2);
+    p.c1 = k * (qs * (b - a));
+    p.c2 = 0.0;
+  } else {
+    p.c0 = k * (a * ax.qa1 * ax.qa1 + b * ax.qa2 * ax.qa2);
+    p.c1 = k * (2.0 * qs * (b * ax.qa2 - a * ax.qa1));
+    p.c2 = k * (qs * qs * (a + b));
+  }
+  return p;
+}
+
 // Border terms of T_X^{-1} y for a real line (transform_apply_inverse,
 // boundary.cpp:338-375).  row_a / row_b are unit impulses, so the two dot
 // products are two samples and every thread solves the 2x2 system itself; and
@@ -991,10 +1014,11 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   const double* sin_ = stg.buf;
   auto ld = [&](int e) { return st ? sin_[e] : __ldg(in + oi + e * es); };
   const Fold fd = fold_terms(ax, ld);
+  const BorderPoly fp = border_poly(ax, -fd.o0, -fd.on);
   // folded interior sample s
   auto xin = [&](int s) {
     double v = ld(interior_elem(ax, s));
-    if (ax.bordered) v += -fd.o0 * q_at(ax, s + 1) - fd.on * q_at(ax, n - 2 - s);
+    if (ax.bordered) v += fp(s);
     return v;
   };
   const int half = (m + 1) / 2;
@@ -1276,10 +1300,11 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
 
   const long long oo = line_offset(io.go, l), eso = io.go.elem_stride;
   double* out = reinterpret_cast<double*>(io.out);
+  const BorderPoly bp = border_poly(ax, u0, un);  // q[e] u0 + q[n-1-e] un, e = p + 1
   auto put = [&](int p, double val) {  // interior position p of the output line
     const int e = interior_elem(ax, p);
     double o = val;
-    if (ax.bordered) o = q_at(ax, e) * u0 + val + q_at(ax, n - 1 - e) * un;
+    if (ax.bordered) o = val + bp(p);
     out[oo + e * eso] = o;
     if (ax.correction) {  // out_0 = q_0 u_0 + c_a . c,  out_{n-1} = c_b . c + q_0 u_{n-1}
       if (p == ax.top_i) out[oo] = ax.q0 * u0 + val;
