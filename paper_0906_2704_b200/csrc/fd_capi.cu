@@ -11,6 +11,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -777,7 +778,7 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 // analyze count items: in (real or complex) -> out (basis type)
 void run_analyze(const fd_op* op, const void* in, int in_cplx, void* out, long long count,
                  Scratch& S, double* wout = nullptr, long long wstride = 0, long long wn = 0,
-                 int pack = 0) {
+                 int pack = 0, float* wout32 = nullptr, float* wout32lo = nullptr) {
   const int oc = op->cplx;
   if (op->dim == 1) {
     LineIO io{};
@@ -789,6 +790,8 @@ void run_analyze(const fd_op* op, const void* in, int in_cplx, void* out, long l
     io.in_cplx = in_cplx;
     io.out_cplx = oc;
     io.wout = wout;
+    io.wout32 = wout32;
+    io.wout32lo = wout32lo;
     io.wstride = wstride;
     io.wn = wn;
     launch_analyze(op->ax1->dev, io, S.st);
@@ -930,13 +933,16 @@ GridHost make_grid(double mu_min, double mu_max, int count) {  // regularize.cpp
 struct Analyzed {
   void* ghat = nullptr;
   double* w = nullptr;
+  float* w32 = nullptr;    // TF32 split of w in screen tiles (tensor-core GCV screen)
+  float* w32lo = nullptr;
   long long wn = 0, wstride = 0;
   int pack = 0;  // ghat Hermitian-packed (n doubles per line), see k_ranalyze
 };
 
-// want_full: keep the full complex coefficients (imaginary residue requested)
+// want_full: keep the full complex coefficients (imaginary residue requested);
+// want_w32: also emit fp32 weights (tensor-core screen, see gcv_select_dev)
 Analyzed analyze_for_gcv(const fd_op* op, const fd_smoother* L, const double* g, long long count,
-                         Scratch& S, bool want_full = false) {
+                         Scratch& S, bool want_full = false, bool want_w32 = false) {
   Analyzed a;
   const bool use_w = op->dim == 1 && op->ax1->dev.rhalf && (!op->cplx || L->pair);
   a.pack = use_w && op->cplx && !want_full;
@@ -946,8 +952,13 @@ Analyzed analyze_for_gcv(const fd_op* op, const fd_smoother* L, const double* g,
     a.wn = op->cplx ? L->n_red : op->N();
     a.wstride = (a.wn + 31) / 32 * 32;
     a.w = S.get<double>((size_t)count * a.wstride);
+    if (want_w32) {  // items padded to whole 128-row tiles
+      const size_t rows = ((size_t)count + kTcBM - 1) / kTcBM * kTcBM;
+      a.w32 = S.get<float>(rows * a.wstride);
+      a.w32lo = S.get<float>(rows * a.wstride);
+    }
   }
-  run_analyze(op, g, 0, a.ghat, count, S, a.w, a.wstride, a.wn, a.pack);
+  run_analyze(op, g, 0, a.ghat, count, S, a.w, a.wstride, a.wn, a.pack, a.w32, a.w32lo);
   return a;
 }
 
@@ -1165,6 +1176,87 @@ struct DevGrid {
   }
 };
 
+// FASTDEBLUR_GCV_SCREEN=0 forces the all-fp64 grid (tests compare the two)
+bool screen_enabled() {
+  const char* e = std::getenv("FASTDEBLUR_GCV_SCREEN");
+  return !(e && e[0] == '0');
+}
+
+template <int BN>
+void launch_screen(const Analyzed& an, int items, const float* Sh, const float* Sl, int nkb, int K,
+                   const double* gscale, uint32_t* mask, int* flag, cudaStream_t st) {
+  constexpr bool SPLIT = true;
+  static bool attr = false;
+  if (!attr) {
+    ck(cudaFuncSetAttribute(k_gcv_screen<BN, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)tc_smem_bytes(BN, SPLIT)),
+       "screen attr");
+    attr = true;
+  }
+  ProfScope ps("k_gcv_screen", st);
+  k_gcv_screen<BN, SPLIT><<<(items + kTcBM - 1) / kTcBM, 128, tc_smem_bytes(BN, SPLIT), st>>>(
+      an.w32, an.w32lo, items, Sh, Sl, nkb, K, gscale, (float)screen_tau(32LL * nkb, SPLIT), mask,
+      flag);
+  launched("k_gcv_screen");
+}
+
+// G over the grid for a batch sharing one operator: tensor-core 3xTF32 screen
+// of num, exact fp64 G at the surviving candidates, +inf elsewhere (fd_tc.cuh)
+void gcv_screen_exact(const GcvData& g, const GcvGrid& grid, const Analyzed& an, double* G,
+                      int* status, Scratch& S) {
+  const int K = grid.count, items = g.items;
+  const int BN = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
+  const long long Ep = g.wstride;  // multiple of 32, zero-padded weights
+  const int nkb = (int)(Ep / 32);
+  double* rmin = S.get<double>(1);
+  double* den = S.get<double>(K);
+  double* gscale = S.get<double>(K);
+  float* Sh = S.get<float>((size_t)BN * Ep);
+  float* Sl = S.get<float>((size_t)BN * Ep);
+  uint32_t* mask = S.get<uint32_t>((size_t)items * 8);
+  int* flag = S.get<int>(items);
+  {
+    ProfScope ps("k_gcv_tables", S.st);
+    k_gcv_rmin<<<1, 256, 0, S.st>>>(g, rmin);
+    launched("k_gcv_rmin");
+    k_gcv_den<<<K, 256, 0, S.st>>>(g, grid, den);
+    launched("k_gcv_den");
+    k_gcv_s32<<<(int)std::min<long long>(4096, (BN * Ep + 255) / 256), 256, 0, S.st>>>(
+        g, grid, BN, Ep, rmin, Sh, Sl);
+    launched("k_gcv_s32");
+    k_gcv_gscale<<<(K + 127) / 128, 128, 0, S.st>>>(grid, den, rmin, gscale, status);
+    launched("k_gcv_gscale");
+  }
+  switch (BN) {
+    case 32: launch_screen<32>(an, items, Sh, Sl, nkb, K, gscale, mask, flag, S.st); break;
+    case 64: launch_screen<64>(an, items, Sh, Sl, nkb, K, gscale, mask, flag, S.st); break;
+    case 128: launch_screen<128>(an, items, Sh, Sl, nkb, K, gscale, mask, flag, S.st); break;
+    default: launch_screen<256>(an, items, Sh, Sl, nkb, K, gscale, mask, flag, S.st); break;
+  }
+  ProfScope ps("k_gcv_exact", S.st);
+  k_gcv_exact<<<(int)(((long long)items * 32 + 255) / 256), 256, 0, S.st>>>(g, grid, mask, flag,
+                                                                          den, G);
+  launched("k_gcv_exact");
+  if (const char* dbg = std::getenv("FASTDEBLUR_GCV_DEBUG"); dbg && dbg[0] == '1') {
+    std::vector<uint32_t> hm((size_t)items * 8);
+    std::vector<int> hf(items);
+    ck(cudaMemcpyAsync(hm.data(), mask, hm.size() * 4, cudaMemcpyDeviceToHost, S.st), "dbg");
+    ck(cudaMemcpyAsync(hf.data(), flag, hf.size() * 4, cudaMemcpyDeviceToHost, S.st), "dbg");
+    ck(cudaStreamSynchronize(S.st), "dbg");
+    long long tot = 0, nfl = 0;
+    int mx = 0;
+    for (int i = 0; i < items; ++i) {
+      int cnt = 0;
+      for (int w = 0; w < 8; ++w) cnt += __builtin_popcount(hm[(size_t)i * 8 + w]);
+      tot += cnt;
+      mx = std::max(mx, cnt);
+      nfl += hf[i];
+    }
+    std::fprintf(stderr, "gcv screen: %d items, candidates mean %.2f max %d, flagged %lld\n",
+                 items, (double)tot / items, mx, nfl);
+  }
+}
+
 void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, long long count,
                     const DevGrid& dg, double mu_min, double mu_max, double* mu_out,
                     int* best_k_out, double* curve_out, int* status, Scratch& S) {
@@ -1176,7 +1268,11 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
 
   int nch;
   double* part;
-  if (items >= 32 && g.wred) {
+  double* G = nullptr;
+  if (an.w32 && !curve_out && K <= 256 && screen_enabled()) {
+    G = S.get<double>((size_t)items * K);
+    gcv_screen_exact(g, grid, an, G, status, S);
+  } else if (items >= 32 && g.wred) {
     // shared-operator batch with compact weights: sigma^2 table + pipelined GEMM
     const int sblocks = (items + 63) / 64;
     nch = (int)std::max(1LL, std::min((296LL + sblocks - 1) / sblocks, g.wstride / 256));
@@ -1207,7 +1303,8 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
     part = S.get<double>((size_t)items * nch * 2 * K);
     launch_grid(g, grid, chunk, nch, part, S.st);
   }
-  double* G = curve_out ? curve_out : S.get<double>((size_t)items * K);
+  if (!G) {
+  G = curve_out ? curve_out : S.get<double>((size_t)items * K);
   if (nch > 1) {  // many element chunks per item: parallel fixed-order reduction first
     double* sums = S.get<double>((size_t)items * 2 * K);
     ProfScope ps("k_gcv_reduce_grid", S.st);
@@ -1221,6 +1318,7 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
     ProfScope ps("k_gcv_reduce_grid", S.st);
     k_gcv_reduce_grid<<<(int)((tot + 255) / 256), 256, 0, S.st>>>(part, items, nch, K, G, status);
     launched("k_gcv_reduce_grid");
+  }
   }
   int* bk = best_k_out ? best_k_out : S.get<int>(items);
   double* center = S.get<double>(items);
@@ -1349,7 +1447,8 @@ void deblur_dev(const fd_op* op, const fd_smoother* L, const double* g, int use_
                 double fixed_mu, double mu_min, double mu_max, const DevGrid* dg,
                 double* restored, double* mu_used, int* best_k, double* curve,
                 double* imag_residue, long long count, int* status, Scratch& S) {
-  const Analyzed an = analyze_for_gcv(op, L, g, count, S, imag_residue != nullptr);
+  const bool w32 = use_gcv && !curve && count >= 32 && dg && dg->d.count <= 256 && screen_enabled();
+  const Analyzed an = analyze_for_gcv(op, L, g, count, S, imag_residue != nullptr, w32);
   if (use_gcv) {
     gcv_select_dev(op, L, an, count, *dg, mu_min, mu_max, mu_used, best_k, curve, status, S);
   } else {

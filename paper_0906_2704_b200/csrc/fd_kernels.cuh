@@ -328,6 +328,8 @@ struct LineIO {
   long long wn;  // weights actually written; [wn, wstride) is zero-filled
   int pack;      // Fourier lines of real data stored Hermitian-packed (k_ranalyze)
   int chirp_smem;  // real-line kernels: copy the Bluestein chirp to shared memory
+  float* wout32;    // optional TF32 split of wout in screen tiles (fd_tc.cuh): hi
+  float* wout32lo;  // and lo parts
 };
 
 __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
@@ -839,6 +841,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  mbar_wait(bar, parity);
+}
+}  // namespace fdb
+#include "fd_tc.cuh"
+namespace fdb {
+
 __device__ __forceinline__ int makhoul_src(int p, int m, int half) {
   return p < half ? 2 * p : 2 * (m - 1 - p) + 1;  // trig.cpp:194-195
 }
@@ -1069,12 +1078,23 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   const double inv_sqrt_m = 1.0 / sqrt((double)m);
   const double s0 = sqrt(1.0 / (double)m), s1 = sqrt(2.0 / (double)m);
   double* wl = io.wout ? io.wout + (long long)l * io.wstride : nullptr;
+  const long long nkb32 = io.wstride >> 5;
+  auto wset = [&](long long i, double v) {  // GCV weight (and its TF32 split for the screen)
+    wl[i] = v;
+    if (io.wout32) {
+      float hi, lo;
+      tf32_split(v, hi, lo);
+      const long long t = tc_tile_index(l, i, kTcBM, nkb32);
+      io.wout32[t] = hi;
+      io.wout32lo[t] = lo;
+    }
+  };
   if (wl)
-    for (long long i = io.wn + threadIdx.x; i < io.wstride; i += blockDim.x) wl[i] = 0.0;
+    for (long long i = io.wn + threadIdx.x; i < io.wstride; i += blockDim.x) wset(i, 0.0);
   auto emit = [&](int i, double2 o) {
     const int e = interior_elem(ax, i);
     stc(io.out, io.out_cplx, oo + e * eso, o);
-    if (wl && !ax.cplx) wl[e] = o.x * o.x;
+    if (wl && !ax.cplx) wset(e, o.x * o.x);
   };
   auto nrm = [](double2 a) { return a.x * a.x + a.y * a.y; };
   if (ax.kind == IK_FOURIER) {
@@ -1111,13 +1131,13 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
       }
       if (wl) {
         if (k == 0) {  // singleton group {0}: self pairs 0 and h
-          wl[off] = nrm(ok);
-          wl[off + h] = nrm(okh);
+          wset(off, nrm(ok));
+          wset(off + h, nrm(okh));
         } else if (kp != k) {
-          wl[off + k] = nrm(ok) + nrm(okph);   // pair (k, m-k = kp+h)
-          wl[off + kp] = nrm(okp) + nrm(okh);  // pair (kp, m-kp = k+h)
+          wset(off + k, nrm(ok) + nrm(okph));   // pair (k, m-k = kp+h)
+          wset(off + kp, nrm(okp) + nrm(okh));  // pair (kp, m-kp = k+h)
         } else {
-          wl[off + k] = nrm(ok) + nrm(okh);  // k = h/2: pair (k, k+h)
+          wset(off + k, nrm(ok) + nrm(okh));  // k = h/2: pair (k, k+h)
         }
       }
     }
@@ -1148,8 +1168,8 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
       stc(io.out, io.out_cplx, oo + (long long)(n - 1) * eso, on);
     }
     if (wl) {
-      wl[0] = fd.o0 * fd.o0;
-      wl[ax.cplx ? h + 2 : n - 1] = fd.on * fd.on;
+      wset(0, fd.o0 * fd.o0);
+      wset(ax.cplx ? h + 2 : n - 1, fd.on * fd.on);
     }
   }
   __syncthreads();  // x and the scratch are reused by the next line
@@ -1660,6 +1680,163 @@ __global__ void __launch_bounds__(256) k_gcv_den(GcvData g, GcvGrid grid, double
   }
   block_sum<1>(acc, red);
   if (threadIdx.x == 0) den[kk] = acc[0];
+}
+
+// ---- tensor-core screening of the grid (fd_tc.cuh) and exact candidates ----
+// rmin = min over elements of the finite ratios r_e (one CTA)
+__global__ void __launch_bounds__(256) k_gcv_rmin(GcvData g, double* rmin) {
+  __shared__ double red[32];
+  double v = INFINITY;
+  for (long long e = threadIdx.x; e < g.N; e += blockDim.x) v = fmin(v, gcv_ratio(g, e));
+  for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmin(m, red[w]);
+    *rmin = m;
+  }
+}
+
+// S32[k][e] = ((rmin + mu_k) / (r_e + mu_k))^2 = S2[e][k] / S2max_k  (<= 1),
+// zero for padding rows k >= K and elements e >= N; written as the TF32 split
+// (hi, lo) in screen tiles of BN rows (tc_tile_index)
+__global__ void k_gcv_s32(GcvData g, GcvGrid grid, int BN, long long Ep,
+                          const double* __restrict__ rmin, float* S32h, float* S32l) {
+  const long long tot = (long long)BN * Ep;
+  const double r0 = *rmin;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(t / Ep);
+    const long long e = t % Ep;
+    double v = 0.0;
+    if (k < grid.count && e < g.N) {
+      const double r = gcv_ratio(g, e);
+      if (!isinf(r)) {
+        const double q = (r0 + grid.mus[k]) / (r + grid.mus[k]);
+        v = q * q;
+      }
+    }
+    float hi, lo;
+    tf32_split(v, hi, lo);
+    const long long d = tc_tile_index(k, e, BN, Ep >> 5);
+    S32h[d] = hi;
+    S32l[d] = lo;
+  }
+}
+
+// gscale_k = S2max_k / den_k^2 (G~ = num~ gscale); a zero den is the
+// degenerate case (regularize.hpp:78-79)
+__global__ void k_gcv_gscale(GcvGrid grid, const double* __restrict__ den,
+                             const double* __restrict__ rmin, double* gscale, int* status) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= grid.count) return;
+  const double d = den[k];
+  if (d == 0.0) {
+    atomicExch(status, 3);
+    gscale[k] = NAN;
+    return;
+  }
+  const double s = 1.0 / (*rmin + grid.mus[k]);
+  gscale[k] = (s * s) / (d * d);
+}
+
+// num at CH grid values (mu[i], i < nv; the rest padding) for one item:
+// warp-strided elements, the CH reciprocals of each element from one
+// division (batch inversion), shuffle-tree sum; lane i < nv returns num_i.
+template <int CH>
+__device__ __forceinline__ double exact_num(const GcvData& g, int item, const double (&mu)[CH],
+                                            int lane) {
+  double acc[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) acc[i] = 0.0;
+  for (long long e = lane; e < g.N; e += 32) {
+    const double r = gcv_ratio(g, e);
+    if (isinf(r)) continue;
+    const double w = gcv_w(g, item, e);
+    double a[CH], pre[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) a[i] = r + mu[i];
+    pre[0] = a[0];
+#pragma unroll
+    for (int i = 1; i < CH; ++i) pre[i] = pre[i - 1] * a[i];
+    if (pre[CH - 1] < 1e300 && pre[CH - 1] > 1e-300) {
+      double inv = rcp_pos(pre[CH - 1]);
+#pragma unroll
+      for (int i = CH - 1; i >= 1; --i) {
+        const double s = inv * pre[i - 1];
+        inv *= a[i];
+        acc[i] = fma(w, s * s, acc[i]);
+      }
+      acc[0] = fma(w, inv * inv, acc[0]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        const double s = 1.0 / a[i];
+        acc[i] = fma(w, s * s, acc[i]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < CH; ++i)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], o);
+  double v = acc[0];
+#pragma unroll
+  for (int i = 1; i < CH; ++i)
+    if (lane == i) v = acc[i];
+  return v;
+}
+
+// Exact G(mu_k) = num_k / den_k^2 at the screened candidates of each item
+// (every grid point when the item is flagged), +inf elsewhere.  One warp per
+// item; candidates in groups of up to 8 (exact_num).  Fixed lane order +
+// shuffle tree: deterministic.
+__global__ void __launch_bounds__(256) k_gcv_exact(GcvData g, GcvGrid grid,
+                                                   const uint32_t* __restrict__ mask,
+                                                   const int* __restrict__ flag,
+                                                   const double* __restrict__ den, double* G) {
+  __shared__ int lists[8][256];
+  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (item >= g.items) return;
+  const int K = grid.count;
+  double* Gi = G + (long long)item * K;
+  int* list = lists[wib];
+  const bool all = flag[item] != 0;
+  // candidate list (ascending k) in shared memory
+  int nc = 0;
+  for (int w0 = 0; w0 < 8; ++w0) {
+    const uint32_t bits = all ? 0xffffffffu : __ldg(&mask[(long long)item * 8 + w0]);
+    const int k = w0 * 32 + lane;
+    const bool on = k < K && ((bits >> lane) & 1u);
+    const uint32_t ball = __ballot_sync(0xffffffffu, on);
+    if (on) list[nc + __popc(ball & ((1u << lane) - 1u))] = k;
+    else if (k < K) Gi[k] = INFINITY;
+    nc += __popc(ball);
+  }
+  __syncwarp();
+  for (int c0 = 0; c0 < nc;) {
+    const int nv = min(8, nc - c0);
+    double v;
+    if (nv <= 4) {
+      double mu[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) mu[i] = i < nv ? grid.mus[list[c0 + i]] : 1.0;
+      v = exact_num<4>(g, item, mu, lane);
+    } else {
+      double mu[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mu[i] = i < nv ? grid.mus[list[c0 + i]] : 1.0;
+      v = exact_num<8>(g, item, mu, lane);
+    }
+    if (lane < nv) {
+      const int k = list[c0 + lane];
+      const double d = den[k];
+      Gi[k] = d == 0.0 ? NAN : v / (d * d);
+    }
+    c0 += nv;
+  }
 }
 
 template <int NJ>

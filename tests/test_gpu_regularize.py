@@ -187,3 +187,32 @@ def test_deblur_host_pipeline_matches_device(chunk):
     assert np.array_equal(bk.numpy(), np_(rep.best_k))
     assert np.max(np.abs(mu.numpy() / np_(rep.mu_used) - 1)) < 1e-12
     assert rel(rest.numpy(), np_(rep.restored)) < 1e-12
+
+
+@pytest.mark.parametrize("bc,psf,smoother,search", [
+    (O.HOC_FOURIER, onesided(15, 0.2), 2, (1e-8, 1.0, 256)),
+    (O.HOC_COSINE, gauss(10, 3.0), 1, (1e-6, 1.0, 100)),
+    (O.PERIODIC, onesided(5, 0.5), 1, (1e-10, 1.0, 64)),
+    (O.REFLECTIVE, gauss(6, 2.0), 0, (1e-8, 10.0, 256))])
+def test_tensor_core_gcv_screen(bc, psf, smoother, search, monkeypatch):
+    """Batches without a requested curve take the tcgen05 TF32 screen + exact
+    fp64 candidates (fd_tc.cuh): identical best_k and mu to the all-fp64 grid
+    and to the oracle; an all-zero item falls back to the exact grid."""
+    n, B = 1024, 300
+    op, L, oop, s = setup(bc, psf, n, smoother)
+    truth, _ = W.signals_1d(W.config(1), 500, B, n=n + len(psf) - 1, m=0)
+    g = W.add_noise(W.convolve_valid(truth, np.asarray(psf) / np.sum(psf)), 0.005,
+                    W.item_key(97, np.arange(B, dtype=np.uint64)))
+    g[17] = 0.0
+    mu_min, mu_max, K = search
+    sr = P.GcvSearch(mu_min, mu_max, K)
+    rep = P.deblur(op, L, torch.from_numpy(g), P.MuChoice(True), search=sr)
+    monkeypatch.setenv("FASTDEBLUR_GCV_SCREEN", "0")
+    ref = P.deblur(op, L, torch.from_numpy(g), P.MuChoice(True), search=sr)
+    assert np.array_equal(np_(rep.best_k), np_(ref.best_k))
+    assert np.max(np.abs(np_(rep.mu_used) / np_(ref.mu_used) - 1)) < 1e-12
+    assert rel(np_(rep.restored), np_(ref.restored)) < 1e-12
+    sel = [i for i in range(B) if i % 10 == 3] + [17]
+    want = O.deblur(oop, s, g[sel], True, mu_min=mu_min, mu_max=mu_max, count=K)
+    assert np.array_equal(np_(rep.best_k)[sel], want.best_k)
+    assert np.max(np.abs(np_(rep.mu_used)[sel] / want.mu_used - 1)) < 1e-10
