@@ -1119,13 +1119,15 @@ void launch_gemm2_t(const GcvData& g, const GcvGrid& grid, int nch, long long ec
   }
 }
 
-void launch_moments(int J, const GcvData& g, const double* center, const int* need,
-                    long long chunk, int nch, double* partial, cudaStream_t st) {
+void launch_moments(int J, const GcvData& g, const GcvGrid& grid, const double* center,
+                    const int* need, long long chunk, int nch, double* partial, double* Btab,
+                    cudaStream_t st) {
   const long long warps = (long long)g.items * nch;
   const int blocks = (int)((warps * 32 + 255) / 256);
   ProfScope ps("k_gcv_moments", st);
 #define FD_MOM(JV)                                                                   \
   case JV:                                                                           \
+    k_gcv_bmom<JV><<<grid.count, 256, 0, st>>>(g, grid, Btab);                       \
     k_gcv_moments<JV><<<blocks, 256, 0, st>>>(g, center, need, chunk, nch, partial); \
     break;
   switch (J) {
@@ -1134,6 +1136,7 @@ void launch_moments(int J, const GcvData& g, const double* center, const int* ne
     default: throw FdError(FD_ERR_OTHER, "unsupported moment count");
   }
 #undef FD_MOM
+  launched("k_gcv_bmom");
   launched("k_gcv_moments");
 }
 
@@ -1333,19 +1336,20 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
   if (J > 0) {
     int nchm = pick_chunks(g.N, items, 1);
     const long long chunkm = (g.N + nchm - 1) / nchm;
-    double* pm = S.get<double>((size_t)items * nchm * 2 * J);
-    launch_moments(J, g, center, need, chunkm, nchm, pm, S.st);
+    double* pm = S.get<double>((size_t)items * nchm * J);
+    double* Btab = S.get<double>((size_t)K * J);
+    launch_moments(J, g, grid, center, need, chunkm, nchm, pm, Btab, S.st);
     if (nchm > 1) {
-      double* sums = S.get<double>((size_t)items * 2 * J);
+      double* sums = S.get<double>((size_t)items * J);
       ProfScope ps("k_gcv_moments", S.st);
-      k_reduce_partials<<<dim3(items, (2 * J + 31) / 32), 256, 0, S.st>>>(pm, nchm, 2 * J, sums);
+      k_reduce_partials<<<dim3(items, (J + 31) / 32), 256, 0, S.st>>>(pm, nchm, J, sums);
       launched("k_reduce_partials");
       pm = sums;
       nchm = 1;
     }
     ProfScope ps("k_gcv_golden", S.st);
-    k_gcv_golden<<<(items + 63) / 64, 64, 0, S.st>>>(pm, items, nchm, J, G, grid, bk, center,
-                                                     need, mu_out);
+    k_gcv_golden<<<(items + 63) / 64, 64, 0, S.st>>>(pm, items, nchm, J, Btab, G, grid, bk,
+                                                     center, need, mu_out);
     launched("k_gcv_golden");
     return;
   }

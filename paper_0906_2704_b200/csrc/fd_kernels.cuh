@@ -1750,10 +1750,8 @@ __device__ __forceinline__ double exact_num(const GcvData& g, int item, const do
   double acc[CH];
 #pragma unroll
   for (int i = 0; i < CH; ++i) acc[i] = 0.0;
-  for (long long e = lane; e < g.N; e += 32) {
-    const double r = gcv_ratio(g, e);
-    if (isinf(r)) continue;
-    const double w = gcv_w(g, item, e);
+  auto one = [&](double r, double w) {
+    if (isinf(r)) return;
     double a[CH], pre[CH];
 #pragma unroll
     for (int i = 0; i < CH; ++i) a[i] = r + mu[i];
@@ -1776,7 +1774,16 @@ __device__ __forceinline__ double exact_num(const GcvData& g, int item, const do
         acc[i] = fma(w, s * s, acc[i]);
       }
     }
+  };
+  // two elements per lane and step: both loads in flight before either is used
+  long long e = lane;
+  for (; e + 32 < g.N; e += 64) {
+    const double r0 = gcv_ratio(g, e), r1 = gcv_ratio(g, e + 32);
+    const double w0 = gcv_w(g, item, e), w1 = gcv_w(g, item, e + 32);
+    one(r0, w0);
+    one(r1, w1);
   }
+  if (e < g.N) one(gcv_ratio(g, e), gcv_w(g, item, e));
 #pragma unroll
   for (int i = 0; i < CH; ++i)
 #pragma unroll
@@ -1987,6 +1994,13 @@ __global__ void k_gcv_pick(const double* __restrict__ G, int items, GcvGrid grid
   }
 }
 
+// Taylor moments of the golden-section refinement around the item's bracket
+// center mc = sqrt(mu_{k-1} mu_{k+1}) (k = best_k, clamped):
+//   num(mu) = sum_j (j+1) A_j (mc - mu)^j,  A_j = sum_e W_e t_e^{j+2},
+//   den(mu) = sum_j B_j (mc - mu)^j,        B_j = sum_e mult_e t_e^{j+1},
+// t_e = 1/(r_e + mc).  B depends on the item only through k, so it is one
+// table over the K grid points (k_gcv_bmom); the per-item pass accumulates A
+// with two operations per term.
 template <int J>
 __global__ void __launch_bounds__(256) k_gcv_moments(GcvData g, const double* __restrict__ center,
                                                      const int* __restrict__ need, long long chunk,
@@ -1998,40 +2012,66 @@ __global__ void __launch_bounds__(256) k_gcv_moments(GcvData g, const double* __
   const int item = warp_global / nchunks, ch = warp_global % nchunks;
   if (!need[item]) return;
   const double mc = center[item];
-  double A[J], B[J];
+  double A[J];
 #pragma unroll
-  for (int j = 0; j < J; ++j) A[j] = B[j] = 0.0;
+  for (int j = 0; j < J; ++j) A[j] = 0.0;
   const long long e0 = (long long)ch * chunk;
   const long long e1 = min(g.N, e0 + chunk);
   for (long long e = e0 + lane; e < e1; e += 32) {
     const double r = gcv_ratio(g, e);
     if (isinf(r)) continue;
     const double w = gcv_w(g, item, e);
-    const double mult = gcv_mult(g, e);
     const double t = rcp_pos(r + mc);
-    double p = t;
+    double p = (w * t) * t;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-      B[j] = fma(mult, p, B[j]);
-      A[j] = fma(w * p, t, A[j]);
+      A[j] += p;
       p *= t;
     }
   }
 #pragma unroll
   for (int j = 0; j < J; ++j) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      A[j] += __shfl_xor_sync(0xffffffffu, A[j], o);
-      B[j] += __shfl_xor_sync(0xffffffffu, B[j], o);
-    }
+    for (int o = 16; o > 0; o >>= 1) A[j] += __shfl_xor_sync(0xffffffffu, A[j], o);
   }
   if (lane == 0) {
-    double* base = partial + ((long long)item * nchunks + ch) * 2 * J;
+    double* base = partial + ((long long)item * nchunks + ch) * J;
+#pragma unroll
+    for (int j = 0; j < J; ++j) base[j] = A[j];
+  }
+}
+
+// center of grid point k's golden bracket (k_gcv_pick uses the same expression)
+__device__ __forceinline__ double bracket_center(const GcvGrid& grid, int k) {
+  const int K = grid.count;
+  return sqrt(grid.mus[k > 0 ? k - 1 : 0] * grid.mus[k + 1 < K ? k + 1 : K - 1]);
+}
+
+// Btab[k][j] = sum_e mult_e t_e^{j+1}, t_e = 1/(r_e + center_k); one CTA per k
+template <int J>
+__global__ void __launch_bounds__(256) k_gcv_bmom(GcvData g, GcvGrid grid, double* Btab) {
+  __shared__ double red[32 * J];
+  const int k = blockIdx.x;
+  const double mc = bracket_center(grid, k);
+  double B[J];
+#pragma unroll
+  for (int j = 0; j < J; ++j) B[j] = 0.0;
+  for (long long e = threadIdx.x; e < g.N; e += blockDim.x) {
+    const double r = gcv_ratio(g, e);
+    if (isinf(r)) continue;
+    const double t = rcp_pos(r + mc);
+    double p = gcv_mult(g, e) * t;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-      base[j] = A[j];
-      base[J + j] = B[j];
+      B[j] += p;
+      p *= t;
     }
+  }
+  block_sum<J>(B, red);
+  if (threadIdx.x < J) {
+#pragma unroll
+    for (int j = 0; j < J; ++j)
+      if (threadIdx.x == j) Btab[(long long)k * J + j] = B[j];
   }
 }
 
@@ -2052,22 +2092,23 @@ struct MomentG {
 };
 
 __global__ void k_gcv_golden(const double* __restrict__ partial, int items, int nchunks, int J,
-                             const double* __restrict__ G, GcvGrid grid,
-                             const int* __restrict__ best_k, const double* __restrict__ center,
-                             const int* __restrict__ need, double* mu_out) {
+                             const double* __restrict__ Btab, const double* __restrict__ G,
+                             GcvGrid grid, const int* __restrict__ best_k,
+                             const double* __restrict__ center, const int* __restrict__ need,
+                             double* mu_out) {
   const int item = blockIdx.x * blockDim.x + threadIdx.x;
   if (item >= items || !need[item]) return;
   double A[64], B[64];
-  for (int j = 0; j < J; ++j) A[j] = B[j] = 0.0;
+  const int k = best_k[item];
+  for (int j = 0; j < J; ++j) {
+    A[j] = 0.0;
+    B[j] = Btab[(long long)k * J + j];
+  }
   for (int c = 0; c < nchunks; ++c) {
-    const double* base = partial + ((long long)item * nchunks + c) * 2 * J;
-    for (int j = 0; j < J; ++j) {
-      A[j] += base[j];
-      B[j] += base[J + j];
-    }
+    const double* base = partial + ((long long)item * nchunks + c) * J;
+    for (int j = 0; j < J; ++j) A[j] += base[j];
   }
   MomentG f{A, B, J, center[item]};
-  const int k = best_k[item];
   const double best = G[(long long)item * grid.count + k];
   mu_out[item] = gcv_golden(grid.mus, grid.count, k, best, f);
 }
