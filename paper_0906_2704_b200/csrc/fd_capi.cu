@@ -1205,8 +1205,8 @@ void launch_screen(const Analyzed& an, int items, const float* Sh, const float* 
 
 // G over the grid for a batch sharing one operator: tensor-core 3xTF32 screen
 // of num, exact fp64 G at the surviving candidates, +inf elsewhere (fd_tc.cuh)
-void gcv_screen_exact(const GcvData& g, const GcvGrid& grid, const Analyzed& an, double* G,
-                      int* status, Scratch& S) {
+void gcv_screen_exact(const GcvData& g, const GcvGrid& grid, const Analyzed& an, double* mu_out,
+                      int* bk, double* center, int* need, double* bestG, int* status, Scratch& S) {
   const int K = grid.count, items = g.items;
   const int BN = K <= 32 ? 32 : K <= 64 ? 64 : K <= 128 ? 128 : 256;
   const long long Ep = g.wstride;  // multiple of 32, zero-padded weights
@@ -1237,8 +1237,8 @@ void gcv_screen_exact(const GcvData& g, const GcvGrid& grid, const Analyzed& an,
     default: launch_screen<256>(an, items, Sh, Sl, nkb, K, gscale, mask, flag, S.st); break;
   }
   ProfScope ps("k_gcv_exact", S.st);
-  k_gcv_exact<<<(int)(((long long)items * 32 + 255) / 256), 256, 0, S.st>>>(g, grid, mask, flag,
-                                                                          den, G);
+  k_gcv_exact<<<(int)(((long long)items * 32 + 255) / 256), 256, 0, S.st>>>(
+      g, grid, mask, flag, den, mu_out, bk, center, need, bestG, status);
   launched("k_gcv_exact");
   if (const char* dbg = std::getenv("FASTDEBLUR_GCV_DEBUG"); dbg && dbg[0] == '1') {
     std::vector<uint32_t> hm((size_t)items * 8);
@@ -1272,10 +1272,16 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
   int nch;
   double* part;
   double* G = nullptr;
-  if (an.w32 && !curve_out && K <= 256 && screen_enabled()) {
-    G = S.get<double>((size_t)items * K);
-    gcv_screen_exact(g, grid, an, G, status, S);
-  } else if (items >= 32 && g.wred) {
+  int* bk = best_k_out ? best_k_out : S.get<int>(items);
+  double* center = S.get<double>(items);
+  int* need = S.get<int>(items);
+  double* bestG = S.get<double>(items);
+  const int J = gcv_moment_terms(mu_min, mu_max, K);
+  if (J > 0 && an.w32 && !curve_out && K <= 256 && screen_enabled()) {
+    // tensor-core screen + exact candidates, pick fused (no full curve)
+    gcv_screen_exact(g, grid, an, mu_out, bk, center, need, bestG, status, S);
+  } else {
+  if (items >= 32 && g.wred) {
     // shared-operator batch with compact weights: sigma^2 table + pipelined GEMM
     const int sblocks = (items + 63) / 64;
     nch = (int)std::max(1LL, std::min((296LL + sblocks - 1) / sblocks, g.wstride / 256));
@@ -1323,16 +1329,14 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
     launched("k_gcv_reduce_grid");
   }
   }
-  int* bk = best_k_out ? best_k_out : S.get<int>(items);
-  double* center = S.get<double>(items);
-  int* need = S.get<int>(items);
   {
     ProfScope ps("k_gcv_pick", S.st);
-    k_gcv_pick<<<(items + 127) / 128, 128, 0, S.st>>>(G, items, grid, mu_out, bk, center, need);
+    k_gcv_pick<<<(items + 127) / 128, 128, 0, S.st>>>(G, items, grid, mu_out, bk, center, need,
+                                                      bestG);
   }
   launched("k_gcv_pick");
+  }
 
-  const int J = gcv_moment_terms(mu_min, mu_max, K);
   if (J > 0) {
     int nchm = pick_chunks(g.N, items, 1);
     const long long chunkm = (g.N + nchm - 1) / nchm;
@@ -1348,7 +1352,7 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
       nchm = 1;
     }
     ProfScope ps("k_gcv_golden", S.st);
-    k_gcv_golden<<<(items + 63) / 64, 64, 0, S.st>>>(pm, items, nchm, J, Btab, G, grid, bk,
+    k_gcv_golden<<<(items + 63) / 64, 64, 0, S.st>>>(pm, items, nchm, J, Btab, bestG, grid, bk,
                                                      center, need, mu_out);
     launched("k_gcv_golden");
     return;

@@ -1741,6 +1741,25 @@ __global__ void k_gcv_gscale(GcvGrid grid, const double* __restrict__ den,
   gscale[k] = (s * s) / (d * d);
 }
 
+// Stream the elements [e0, e1) of one item through f(r_e, W_e): lane-strided,
+// U elements per lane and step with all their loads issued before any use
+// (the weights stream from HBM; one load in flight per warp is latency-bound).
+template <int U, class F>
+__device__ __forceinline__ void gcv_stream(const GcvData& g, int item, long long e0, long long e1,
+                                           int lane, F&& f) {
+  for (long long e = e0 + lane; e < e1; e += 32 * U) {
+    double r[U], w[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long x = e + 32 * u;
+      r[u] = x < e1 ? gcv_ratio(g, x) : INFINITY;
+      w[u] = x < e1 ? gcv_w(g, item, x) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) f(r[u], w[u]);
+  }
+}
+
 // num at CH grid values (mu[i], i < nv; the rest padding) for one item:
 // warp-strided elements, the CH reciprocals of each element from one
 // division (batch inversion), shuffle-tree sum; lane i < nv returns num_i.
@@ -1775,15 +1794,7 @@ __device__ __forceinline__ double exact_num(const GcvData& g, int item, const do
       }
     }
   };
-  // two elements per lane and step: both loads in flight before either is used
-  long long e = lane;
-  for (; e + 32 < g.N; e += 64) {
-    const double r0 = gcv_ratio(g, e), r1 = gcv_ratio(g, e + 32);
-    const double w0 = gcv_w(g, item, e), w1 = gcv_w(g, item, e + 32);
-    one(r0, w0);
-    one(r1, w1);
-  }
-  if (e < g.N) one(gcv_ratio(g, e), gcv_w(g, item, e));
+  gcv_stream<4>(g, item, 0, g.N, lane, one);
 #pragma unroll
   for (int i = 0; i < CH; ++i)
 #pragma unroll
@@ -1796,20 +1807,25 @@ __device__ __forceinline__ double exact_num(const GcvData& g, int item, const do
 }
 
 // Exact G(mu_k) = num_k / den_k^2 at the screened candidates of each item
-// (every grid point when the item is flagged), +inf elsewhere.  One warp per
-// item; candidates in groups of up to 8 (exact_num).  Fixed lane order +
-// shuffle tree: deterministic.
+// (every grid point when the item is flagged) and gcv_pick over them -- the
+// other grid points are above the minimum by more than the screen's error, so
+// the first minimum, the 1e-12 ties and the bracket are those of the full
+// grid.  One warp per item; candidates in groups of up to 8 (exact_num).
+// Fixed lane order + shuffle tree: deterministic.
 __global__ void __launch_bounds__(256) k_gcv_exact(GcvData g, GcvGrid grid,
                                                    const uint32_t* __restrict__ mask,
                                                    const int* __restrict__ flag,
-                                                   const double* __restrict__ den, double* G) {
+                                                   const double* __restrict__ den, double* mu_out,
+                                                   int* best_k, double* center, int* need,
+                                                   double* bestG, int* status) {
   __shared__ int lists[8][256];
+  __shared__ double vals[8][256];
   const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int item = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (item >= g.items) return;
   const int K = grid.count;
-  double* Gi = G + (long long)item * K;
   int* list = lists[wib];
+  double* val = vals[wib];
   const bool all = flag[item] != 0;
   // candidate list (ascending k) in shared memory
   int nc = 0;
@@ -1819,7 +1835,6 @@ __global__ void __launch_bounds__(256) k_gcv_exact(GcvData g, GcvGrid grid,
     const bool on = k < K && ((bits >> lane) & 1u);
     const uint32_t ball = __ballot_sync(0xffffffffu, on);
     if (on) list[nc + __popc(ball & ((1u << lane) - 1u))] = k;
-    else if (k < K) Gi[k] = INFINITY;
     nc += __popc(ball);
   }
   __syncwarp();
@@ -1838,11 +1853,42 @@ __global__ void __launch_bounds__(256) k_gcv_exact(GcvData g, GcvGrid grid,
       v = exact_num<8>(g, item, mu, lane);
     }
     if (lane < nv) {
-      const int k = list[c0 + lane];
-      const double d = den[k];
-      Gi[k] = d == 0.0 ? NAN : v / (d * d);
+      const double d = den[list[c0 + lane]];
+      val[c0 + lane] = d == 0.0 ? NAN : v / (d * d);
     }
     c0 += nv;
+  }
+  __syncwarp();
+  if (lane == 0) {  // gcv_pick (fd_gcv_core.h) restricted to the candidates
+    int bi = 0;
+    double best = val[0];
+    for (int i = 1; i < nc; ++i)
+      if (val[i] < best) {
+        best = val[i];
+        bi = i;
+      }
+    int ntied = 0;
+    double mean_log = 0.0;
+    for (int i = 0; i < nc; ++i) {
+      const bool tie = best == 0.0 ? val[i] == 0.0 : val[i] <= best + 1e-12 * fabs(best);
+      if (tie) {
+        ++ntied;
+        mean_log += grid.logmus[list[i]];
+      }
+    }
+    if (isnan(best)) atomicExch(status, 3);
+    const int k = list[bi];
+    best_k[item] = k;
+    bestG[item] = best;
+    if (ntied > 1) {
+      mu_out[item] = exp(mean_log / (double)ntied);
+      need[item] = 0;
+      center[item] = 0.0;
+    } else {
+      need[item] = 1;
+      center[item] = sqrt(grid.mus[k > 0 ? k - 1 : 0] * grid.mus[k + 1 < K ? k + 1 : K - 1]);
+      mu_out[item] = grid.mus[k];
+    }
   }
 }
 
@@ -1978,11 +2024,12 @@ __global__ void __launch_bounds__(256) k_reduce_partials(const double* __restric
 }
 
 __global__ void k_gcv_pick(const double* __restrict__ G, int items, GcvGrid grid, double* mu_out,
-                           int* best_k, double* center, int* need_refine) {
+                           int* best_k, double* center, int* need_refine, double* bestG) {
   const int item = blockIdx.x * blockDim.x + threadIdx.x;
   if (item >= items) return;
   const GcvPick pk = gcv_pick(grid.mus, grid.logmus, G + (long long)item * grid.count, grid.count);
   best_k[item] = pk.best_k;
+  bestG[item] = G[(long long)item * grid.count + pk.best_k];
   if (pk.tied) {
     mu_out[item] = pk.mu_tie;
     need_refine[item] = 0;
@@ -2017,10 +2064,8 @@ __global__ void __launch_bounds__(256) k_gcv_moments(GcvData g, const double* __
   for (int j = 0; j < J; ++j) A[j] = 0.0;
   const long long e0 = (long long)ch * chunk;
   const long long e1 = min(g.N, e0 + chunk);
-  for (long long e = e0 + lane; e < e1; e += 32) {
-    const double r = gcv_ratio(g, e);
-    if (isinf(r)) continue;
-    const double w = gcv_w(g, item, e);
+  gcv_stream<4>(g, item, e0, e1, lane, [&](double r, double w) {
+    if (isinf(r)) return;
     const double t = rcp_pos(r + mc);
     double p = (w * t) * t;
 #pragma unroll
@@ -2028,7 +2073,7 @@ __global__ void __launch_bounds__(256) k_gcv_moments(GcvData g, const double* __
       A[j] += p;
       p *= t;
     }
-  }
+  });
 #pragma unroll
   for (int j = 0; j < J; ++j) {
 #pragma unroll
@@ -2092,7 +2137,7 @@ struct MomentG {
 };
 
 __global__ void k_gcv_golden(const double* __restrict__ partial, int items, int nchunks, int J,
-                             const double* __restrict__ Btab, const double* __restrict__ G,
+                             const double* __restrict__ Btab, const double* __restrict__ bestG,
                              GcvGrid grid, const int* __restrict__ best_k,
                              const double* __restrict__ center, const int* __restrict__ need,
                              double* mu_out) {
@@ -2109,7 +2154,7 @@ __global__ void k_gcv_golden(const double* __restrict__ partial, int items, int 
     for (int j = 0; j < J; ++j) A[j] += base[j];
   }
   MomentG f{A, B, J, center[item]};
-  const double best = G[(long long)item * grid.count + k];
+  const double best = bestG[item];
   mu_out[item] = gcv_golden(grid.mus, grid.count, k, best, f);
 }
 
