@@ -141,6 +141,12 @@ struct Scratch {
   }
 };
 
+template <int LOGM>
+void set_rline_attrs(int kmax) {
+  cudaFuncSetAttribute(k_ranalyze<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+  cudaFuncSetAttribute(k_rsynth<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+}
+
 void init_runtime_once() {
   static std::once_flag once;
   static bool ok = false;
@@ -158,8 +164,12 @@ void init_runtime_once() {
     cudaFuncSetAttribute(k_analyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
     cudaFuncSetAttribute(k_synth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
     cudaFuncSetAttribute(k_bhat, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
-    cudaFuncSetAttribute(k_ranalyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
-    cudaFuncSetAttribute(k_rsynth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+    set_rline_attrs<0>(kmax);
+    set_rline_attrs<9>(kmax);
+    set_rline_attrs<10>(kmax);
+    set_rline_attrs<11>(kmax);
+    set_rline_attrs<12>(kmax);
+    set_rline_attrs<13>(kmax);
     ok = true;
   });
   if (!ok) throw FdError(FD_ERR_OTHER, "no CUDA device available (fastdeblur_b200 has no CPU path)");
@@ -303,7 +313,7 @@ void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
       const int grid = std::min(io.gi.count, 2 * num_sms());
       double2* scr = nullptr;
       ck(cudaMallocAsync(&scr, (size_t)grid * 2 * ax.hfft.L * sizeof(double2), st), "scratch");
-      k_ranalyze<<<grid, 256, rsmem_bytes(ax, ax.hfft.M / 2), st>>>(ax, io, scr);
+      k_ranalyze<0><<<grid, 256, rsmem_bytes(ax, ax.hfft.M / 2), st>>>(ax, io, scr);
       launched("k_ranalyze");
       ck(cudaFreeAsync(scr, st), "scratch");
       return;
@@ -311,8 +321,18 @@ void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
     const int thr = std::min(256, line_threads(ax.hfft.M));
     LineIO io2 = io;
     const size_t sm = rline_smem(ax, io2);
-    k_ranalyze<<<persistent_grid(k_ranalyze, thr, sm, io.gi.count), thr, sm, st>>>(ax, io2,
-                                                                                  nullptr);
+#define FD_RA(L)                                                                             \
+  k_ranalyze<L><<<persistent_grid(k_ranalyze<L>, thr, sm, io.gi.count), thr, sm, st>>>(ax, io2, \
+                                                                                    nullptr)
+    switch (ax.hfft.logM) {
+      case 9: FD_RA(9); break;
+      case 10: FD_RA(10); break;
+      case 11: FD_RA(11); break;
+      case 12: FD_RA(12); break;
+      case 13: FD_RA(13); break;
+      default: FD_RA(0); break;
+    }
+#undef FD_RA
     launched("k_ranalyze");
     return;
   }
@@ -331,7 +351,7 @@ void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cuda
       const int grid = std::min(io.gi.count, 2 * num_sms());
       double2* scr = nullptr;
       ck(cudaMallocAsync(&scr, (size_t)grid * 2 * ax.hfft.L * sizeof(double2), st), "scratch");
-      k_rsynth<<<grid, 256, rsmem_bytes(ax, ax.hfft.M / 2), st>>>(ax, io, sa, scr);
+      k_rsynth<0><<<grid, 256, rsmem_bytes(ax, ax.hfft.M / 2), st>>>(ax, io, sa, scr);
       launched("k_rsynth");
       ck(cudaFreeAsync(scr, st), "scratch");
       return;
@@ -339,8 +359,18 @@ void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cuda
     const int thr = std::min(256, line_threads(ax.hfft.M));
     LineIO io2 = io;
     const size_t sm = rline_smem(ax, io2);
-    k_rsynth<<<persistent_grid(k_rsynth, thr, sm, io.gi.count), thr, sm, st>>>(ax, io2, sa,
-                                                                              nullptr);
+#define FD_RS(L)                                                                           \
+  k_rsynth<L><<<persistent_grid(k_rsynth<L>, thr, sm, io.gi.count), thr, sm, st>>>(ax, io2, sa, \
+                                                                                  nullptr)
+    switch (ax.hfft.logM) {
+      case 9: FD_RS(9); break;
+      case 10: FD_RS(10); break;
+      case 11: FD_RS(11); break;
+      case 12: FD_RS(12); break;
+      case 13: FD_RS(13); break;
+      default: FD_RS(0); break;
+    }
+#undef FD_RS
     launched("k_rsynth");
     return;
   }

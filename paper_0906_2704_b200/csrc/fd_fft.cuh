@@ -162,11 +162,20 @@ __device__ __forceinline__ void dit_pass(double2* __restrict__ x, int M, int S, 
   }
 }
 
-__host__ __device__ __forceinline__ int pass_logr(int rem) { return rem >= 4 ? 4 : rem; }
+// Pass sequence of a size-2^logM transform: the remainder radix first, then
+// radix-16 passes, so every pass but the innermost has a sub-block stride
+// SR >= 16 (padded addresses linear in q) and the innermost (mid) pass is
+// radix 16 whenever logM >= 4.  k_bhat, the generic and the specialised
+// Bluestein cores all use this sequence (bhat is stored in its DIF order).
+__host__ __device__ __forceinline__ int num_passes(int logM) { return (logM + 3) / 4; }
+__host__ __device__ __forceinline__ int pass_radix(int logM, int p) {
+  const int rem = logM % 4;
+  return (rem != 0 && p == 0) ? rem : 4;
+}
 
 // radix (log2) of the last DIF pass of a size-2^logM transform (the mid pass)
 __host__ __device__ __forceinline__ int mid_logr(int logM) {
-  return logM <= 0 ? 0 : (logM % 4 == 0 ? 4 : logM % 4);
+  return logM <= 0 ? 0 : (logM >= 4 ? 4 : logM);
 }
 // storage slot of DIF-order entry j of a bhat block of M = 2^logM points
 __host__ __device__ __forceinline__ int bhat_store_index(int j, int logM) {
@@ -175,32 +184,13 @@ __host__ __device__ __forceinline__ int bhat_store_index(int j, int logM) {
   return (j & ((1 << lr) - 1)) * items + (j >> lr);
 }
 
-// Forward DIF FFT (sign -1), natural order in, digit-reversed order out.
-// Caller must __syncthreads() before; returns after a barrier.
-__device__ __forceinline__ void fft_dif(double2* x, int M, int logM, const TwSm& tw) {
-  int S = M;
-  int rem = logM;
-  while (rem > 0) {
-    const int l = pass_logr(rem);
-    switch (l) {
-      case 4: dif_pass<4>(x, M, S, tw, M, M); break;
-      case 3: dif_pass<3>(x, M, S, tw, M, M); break;
-      case 2: dif_pass<2>(x, M, S, tw, M, M); break;
-      default: dif_pass<1>(x, M, S, tw, M, M); break;
-    }
-    S >>= l;
-    rem -= l;
-    __syncthreads();
-  }
-}
-
 // DIF passes over a local block of M points with twiddles of size Mtw.
 __device__ __forceinline__ void fft_dif_local(double2* x, int M, int logM, int Mtw,
                                               const TwSm& tw) {
   int S = M;
-  int rem = logM;
-  while (rem > 0) {
-    const int l = pass_logr(rem);
+  const int np = num_passes(logM);
+  for (int p = 0; p < np; ++p) {
+    const int l = pass_radix(logM, p);
     switch (l) {
       case 4: dif_pass<4>(x, M, S, tw, Mtw, M); break;
       case 3: dif_pass<3>(x, M, S, tw, Mtw, M); break;
@@ -208,31 +198,6 @@ __device__ __forceinline__ void fft_dif_local(double2* x, int M, int logM, int M
       default: dif_pass<1>(x, M, S, tw, Mtw, M); break;
     }
     S >>= l;
-    rem -= l;
-    __syncthreads();
-  }
-}
-
-// Backward DIT FFT (sign +1, unnormalised), digit-reversed in, natural out.
-__device__ __forceinline__ void fft_dit(double2* x, int M, int logM, const TwSm& tw) {
-  int ls[8];
-  int np = 0;
-  for (int rem = logM; rem > 0;) {
-    const int l = pass_logr(rem);
-    ls[np++] = l;
-    rem -= l;
-  }
-  int used = logM;
-  for (int p = np - 1; p >= 0; --p) {
-    const int l = ls[p];
-    used -= l;
-    const int S = M >> used;  // block size of pass p in the DIF sequence
-    switch (l) {
-      case 4: dit_pass<4>(x, M, S, tw, M); break;
-      case 3: dit_pass<3>(x, M, S, tw, M); break;
-      case 2: dit_pass<2>(x, M, S, tw, M); break;
-      default: dit_pass<1>(x, M, S, tw, M); break;
-    }
     __syncthreads();
   }
 }
@@ -305,12 +270,8 @@ __device__ __forceinline__ void bluestein_run(double2* x, int M, int logM, int M
     return;
   }
   int ls[8];
-  int np = 0;
-  for (int rem = logM; rem > 0;) {
-    const int l = pass_logr(rem);
-    ls[np++] = l;
-    rem -= l;
-  }
+  const int np = num_passes(logM);
+  for (int p = 0; p < np; ++p) ls[p] = pass_radix(logM, p);
   int S = M;
   for (int p = 0; p < np - 1; ++p) {
     if (p == 0 && nvalid < M) {  // zero padding: only the first pass reads it
@@ -383,6 +344,176 @@ __device__ __forceinline__ void bluestein_half(double2* x, const FftTables& T, c
     __syncthreads();
   }
   bluestein_run(x, Mloc, T.logM - 1, T.M, T.bhat + part * Mloc, tw, nvalid);
+}
+
+// ----------------------------------------------------------------------------
+// Size-specialised Bluestein core (LOGM known at compile time).  Same
+// arithmetic, pass sequence and bhat layout as bluestein_run, but the launch
+// uses exactly FftShape<LOGM>::NT threads, every pass is unrolled, and every
+// shared-memory address is one per-thread base plus compile-time offsets
+// (pidx(base + q SR) = pidx(base) + q (SR + SR/16) for SR a multiple of 16).
+template <int LOGM>
+struct FftShape {
+  static constexpr int M = 1 << LOGM;
+  static constexpr int NT = M / 16 >= 256 ? 256 : (M / 16 <= 64 ? 64 : M / 16);
+  static constexpr int NP = (LOGM + 3) / 4;
+  static constexpr int LOB = ((LOGM > 1 ? LOGM - 1 : 0) + 1) / 2;  // load_twiddles' split
+};
+
+template <int LOB>
+__device__ __forceinline__ double2 tw_t(const TwSm& tw, int j) {
+  return cmul(tw.hi[j >> LOB], tw.lo[j & ((1 << LOB) - 1)]);
+}
+
+template <int LOGM, int LR, int S, bool PAD>
+__device__ __forceinline__ void dif_pass_t(double2* __restrict__ x, const TwSm& tw, int nvalid) {
+  using F = FftShape<LOGM>;
+  constexpr int R = 1 << LR, SR = S >> LR, ITEMS = F::M >> LR;
+  constexpr int TWSTEP = F::M / S;
+  constexpr int QS = SR + SR / 16;
+  static_assert(SR % 16 == 0, "outer passes have SR >= 16");
+#pragma unroll
+  for (int i0 = 0; i0 < ITEMS; i0 += F::NT) {
+    const int it = i0 + threadIdx.x;
+    if (ITEMS < F::NT && it >= ITEMS) break;
+    const int j0 = it & (SR - 1);
+    const int base = (it - j0) * R + j0;
+    double2* xb = x + pidx(base);
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = (!PAD || base + q * SR < nvalid) ? xb[q * QS] : czero();
+#pragma unroll
+    for (int st = 0; st < LR; ++st) {
+      const int half = R >> (st + 1);
+      const double2 w = tw_t<F::LOB>(tw, (j0 * TWSTEP) << st);
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (q & half) continue;
+        const int qq = q & (half - 1);
+        const double2 a = v[q], b = v[q + half];
+        v[q] = cadd(a, b);
+        v[q + half] = cmul(mul_w16(csub(a, b), (qq << st) * (16 / R)), w);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) xb[q * QS] = v[q];
+  }
+}
+
+template <int LOGM, int LR, int S>
+__device__ __forceinline__ void dit_pass_t(double2* __restrict__ x, const TwSm& tw) {
+  using F = FftShape<LOGM>;
+  constexpr int R = 1 << LR, SR = S >> LR, ITEMS = F::M >> LR;
+  constexpr int TWSTEP = F::M / S;
+  constexpr int QS = SR + SR / 16;
+  static_assert(SR % 16 == 0, "outer passes have SR >= 16");
+#pragma unroll
+  for (int i0 = 0; i0 < ITEMS; i0 += F::NT) {
+    const int it = i0 + threadIdx.x;
+    if (ITEMS < F::NT && it >= ITEMS) break;
+    const int j0 = it & (SR - 1);
+    const int base = (it - j0) * R + j0;
+    double2* xb = x + pidx(base);
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = xb[q * QS];
+#pragma unroll
+    for (int st = LR - 1; st >= 0; --st) {
+      const int half = R >> (st + 1);
+      const double2 w = tw_t<F::LOB>(tw, (j0 * TWSTEP) << st);
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (q & half) continue;
+        const int qq = q & (half - 1);
+        const double2 a = v[q];
+        const double2 b = mul_w16c(cmulc(v[q + half], w), (qq << st) * (16 / R));
+        v[q] = cadd(a, b);
+        v[q + half] = csub(a, b);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) xb[q * QS] = v[q];
+  }
+}
+
+// innermost radix-16 pass: DIF stages, multiply by bhat, DIT stages
+template <int LOGM, bool PAD>
+__device__ __forceinline__ void mid_pass_t(double2* __restrict__ x,
+                                           const double2* __restrict__ bhat, int nvalid) {
+  using F = FftShape<LOGM>;
+  constexpr int R = 16, ITEMS = F::M / 16;
+#pragma unroll
+  for (int i0 = 0; i0 < ITEMS; i0 += F::NT) {
+    const int it = i0 + threadIdx.x;
+    if (ITEMS < F::NT && it >= ITEMS) break;
+    const int base = it * R;
+    double2* xb = x + pidx(base);
+    double2 v[R], bh[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) bh[q] = __ldg(&bhat[q * ITEMS + it]);
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = (!PAD || base + q < nvalid) ? xb[q] : czero();
+#pragma unroll
+    for (int st = 0; st < 4; ++st) {
+      const int half = R >> (st + 1);
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (q & half) continue;
+        const int qq = q & (half - 1);
+        const double2 a = v[q], b = v[q + half];
+        v[q] = cadd(a, b);
+        v[q + half] = mul_w16(csub(a, b), qq << st);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = cmul(v[q], bh[q]);
+#pragma unroll
+    for (int st = 3; st >= 0; --st) {
+      const int half = R >> (st + 1);
+#pragma unroll
+      for (int q = 0; q < R; ++q) {
+        if (q & half) continue;
+        const int qq = q & (half - 1);
+        const double2 a = v[q];
+        const double2 b = mul_w16c(v[q + half], qq << st);
+        v[q] = cadd(a, b);
+        v[q + half] = csub(a, b);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) xb[q] = v[q];
+  }
+}
+
+// pass P of the DIF sequence (block size S), the inner passes, then its DIT mirror
+template <int LOGM, int P, int S>
+__device__ __forceinline__ void bluestein_rec(double2* x, const double2* bhat, const TwSm& tw,
+                                              int nvalid) {
+  using F = FftShape<LOGM>;
+  if constexpr (P == F::NP - 1) {
+    if (P == 0 && nvalid < F::M)
+      mid_pass_t<LOGM, true>(x, bhat, nvalid);
+    else
+      mid_pass_t<LOGM, false>(x, bhat, nvalid);
+    __syncthreads();
+  } else {
+    constexpr int LR = (P == 0 && LOGM % 4 != 0) ? LOGM % 4 : 4;
+    if (P == 0 && nvalid < F::M)
+      dif_pass_t<LOGM, LR, S, true>(x, tw, nvalid);
+    else
+      dif_pass_t<LOGM, LR, S, false>(x, tw, nvalid);
+    __syncthreads();
+    bluestein_rec<LOGM, P + 1, (S >> LR)>(x, bhat, tw, nvalid);
+    dit_pass_t<LOGM, LR, S>(x, tw);
+    __syncthreads();
+  }
+}
+
+// bluestein_core for a compile-time size (LOGM >= 4), blockDim.x == FftShape<LOGM>::NT
+template <int LOGM>
+__device__ __forceinline__ void bluestein_t(double2* x, const FftTables& T, const TwSm& tw,
+                                            int nvalid) {
+  bluestein_rec<LOGM, 0, (1 << LOGM)>(x, T.bhat, tw, nvalid);
 }
 
 // ----------------------------------------------------------------------------

@@ -986,6 +986,8 @@ __device__ __forceinline__ Stage stage_init(double2* x, int h, int Mloc, double2
 //   [border0, border_n-1] [X_0, X_h] X_1 .. X_{h-1}   (double2 slots; the
 //   border slot only when bordered) -- the coefficients of real data in this
 //   basis are exactly Hermitian once the border is folded in.
+// LOGM > 0: size-specialised Bluestein core (bluestein_t), blockDim = FftShape<LOGM>::NT
+template <int LOGM>
 __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, double2* scr) {
   extern __shared__ double2 sm[];
   const FftTables& T = ax.hfft;
@@ -1053,7 +1055,10 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   __syncthreads();
 
   if (!big) {
-    bluestein_core(x, T, tw, h);
+    if constexpr (LOGM > 0)
+      bluestein_t<LOGM>(x, T, tw, h);
+    else
+      bluestein_core(x, T, tw, h);
     // the post phase reads [0, h) only: stage the next line behind it
     if (threadIdx.x == 0) stage_issue(stg, io, l + gridDim.x, n);
   } else {
@@ -1181,6 +1186,8 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
 // dots c_a . c_mid, c_b . c_mid are samples of the interior synthesis
 // (top_i, bot_i), written by the thread that produces them.
 // scr != null: split-convolution mode (see k_ranalyze); io.pack: packed input.
+// LOGM > 0: size-specialised Bluestein core (bluestein_t), blockDim = FftShape<LOGM>::NT
+template <int LOGM>
 __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthArgs sa,
                                                    double2* scr) {
   extern __shared__ double2 sm[];
@@ -1301,7 +1308,10 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
   __syncthreads();
 
   if (!big) {
-    bluestein_core(x, T, tw, h);
+    if constexpr (LOGM > 0)
+      bluestein_t<LOGM>(x, T, tw, h);
+    else
+      bluestein_core(x, T, tw, h);
     if (threadIdx.x == 0) stage_issue(stg, io, l + gridDim.x, n);
   } else {
     for (int j = threadIdx.x; j < h; j += blockDim.x) scrA[j] = x[pidx(j)];
