@@ -165,7 +165,6 @@ void init_runtime_once() {
     cudaFuncSetAttribute(k_synth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
     cudaFuncSetAttribute(k_bhat, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
     set_rline_attrs<0>(kmax);
-    set_rline_attrs<9>(kmax);
     set_rline_attrs<10>(kmax);
     set_rline_attrs<11>(kmax);
     set_rline_attrs<12>(kmax);
@@ -325,7 +324,6 @@ void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
   k_ranalyze<L><<<persistent_grid(k_ranalyze<L>, thr, sm, io.gi.count), thr, sm, st>>>(ax, io2, \
                                                                                     nullptr)
     switch (ax.hfft.logM) {
-      case 9: FD_RA(9); break;
       case 10: FD_RA(10); break;
       case 11: FD_RA(11); break;
       case 12: FD_RA(12); break;
@@ -363,7 +361,6 @@ void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cuda
   k_rsynth<L><<<persistent_grid(k_rsynth<L>, thr, sm, io.gi.count), thr, sm, st>>>(ax, io2, sa, \
                                                                                   nullptr)
     switch (ax.hfft.logM) {
-      case 9: FD_RS(9); break;
       case 10: FD_RS(10); break;
       case 11: FD_RS(11); break;
       case 12: FD_RS(12); break;
