@@ -1152,10 +1152,15 @@ void launch_moments(int J, const GcvData& g, const GcvGrid& grid, const double* 
   const long long warps = (long long)g.items * nch;
   const int blocks = (int)((warps * 32 + 255) / 256);
   ProfScope ps("k_gcv_moments", st);
-#define FD_MOM(JV)                                                                   \
-  case JV:                                                                           \
-    k_gcv_bmom<JV><<<grid.count, 256, 0, st>>>(g, grid, Btab);                       \
-    k_gcv_moments<JV><<<blocks, 256, 0, st>>>(g, center, need, chunk, nch, partial); \
+  // B table over the K grid points only pays when items outnumber grid points
+#define FD_MOM(JV)                                                                          \
+  case JV:                                                                                  \
+    if (Btab) {                                                                             \
+      k_gcv_bmom<JV><<<grid.count, 256, 0, st>>>(g, grid, Btab);                            \
+      k_gcv_moments<JV, false><<<blocks, 256, 0, st>>>(g, center, need, chunk, nch, partial); \
+    } else {                                                                                \
+      k_gcv_moments<JV, true><<<blocks, 256, 0, st>>>(g, center, need, chunk, nch, partial);  \
+    }                                                                                       \
     break;
   switch (J) {
     FD_MOM(4) FD_MOM(8) FD_MOM(12) FD_MOM(16) FD_MOM(20) FD_MOM(24) FD_MOM(28) FD_MOM(32)
@@ -1163,7 +1168,7 @@ void launch_moments(int J, const GcvData& g, const GcvGrid& grid, const double* 
     default: throw FdError(FD_ERR_OTHER, "unsupported moment count");
   }
 #undef FD_MOM
-  launched("k_gcv_bmom");
+  if (Btab) launched("k_gcv_bmom");
   launched("k_gcv_moments");
 }
 
@@ -1367,13 +1372,14 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
   if (J > 0) {
     int nchm = pick_chunks(g.N, items, 1);
     const long long chunkm = (g.N + nchm - 1) / nchm;
-    double* pm = S.get<double>((size_t)items * nchm * J);
-    double* Btab = S.get<double>((size_t)K * J);
+    double* Btab = K <= items ? S.get<double>((size_t)K * J) : nullptr;
+    const int wm = Btab ? J : 2 * J;
+    double* pm = S.get<double>((size_t)items * nchm * wm);
     launch_moments(J, g, grid, center, need, chunkm, nchm, pm, Btab, S.st);
     if (nchm > 1) {
-      double* sums = S.get<double>((size_t)items * J);
+      double* sums = S.get<double>((size_t)items * wm);
       ProfScope ps("k_gcv_moments", S.st);
-      k_reduce_partials<<<dim3(items, (J + 31) / 32), 256, 0, S.st>>>(pm, nchm, J, sums);
+      k_reduce_partials<<<dim3(items, (wm + 31) / 32), 256, 0, S.st>>>(pm, nchm, wm, sums);
       launched("k_reduce_partials");
       pm = sums;
       nchm = 1;

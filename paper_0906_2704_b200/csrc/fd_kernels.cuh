@@ -2058,7 +2058,9 @@ __global__ void k_gcv_pick(const double* __restrict__ G, int items, GcvGrid grid
 // t_e = 1/(r_e + mc).  B depends on the item only through k, so it is one
 // table over the K grid points (k_gcv_bmom); the per-item pass accumulates A
 // with two operations per term.
-template <int J>
+// WITH_B: also accumulate B per item (few large items: a B table over all K
+// grid points would cost K passes over the elements); partial holds [A | B].
+template <int J, bool WITH_B>
 __global__ void __launch_bounds__(256) k_gcv_moments(GcvData g, const double* __restrict__ center,
                                                      const int* __restrict__ need, long long chunk,
                                                      int nchunks, double* partial) {
@@ -2069,30 +2071,58 @@ __global__ void __launch_bounds__(256) k_gcv_moments(GcvData g, const double* __
   const int item = warp_global / nchunks, ch = warp_global % nchunks;
   if (!need[item]) return;
   const double mc = center[item];
-  double A[J];
+  constexpr int NB = WITH_B ? J : 1;
+  double A[J], B[NB];
 #pragma unroll
   for (int j = 0; j < J; ++j) A[j] = 0.0;
+#pragma unroll
+  for (int j = 0; j < NB; ++j) B[j] = 0.0;
   const long long e0 = (long long)ch * chunk;
   const long long e1 = min(g.N, e0 + chunk);
-  gcv_stream<4>(g, item, e0, e1, lane, [&](double r, double w) {
-    if (isinf(r)) return;
-    const double t = rcp_pos(r + mc);
-    double p = (w * t) * t;
+  if (WITH_B) {
+    for (long long e = e0 + lane; e < e1; e += 32) {
+      const double r = gcv_ratio(g, e);
+      if (isinf(r)) continue;
+      const double w = gcv_w(g, item, e);
+      const double t = rcp_pos(r + mc);
+      double pa = (w * t) * t, pb = gcv_mult(g, e) * t;
 #pragma unroll
-    for (int j = 0; j < J; ++j) {
-      A[j] += p;
-      p *= t;
+      for (int j = 0; j < J; ++j) {
+        A[j] += pa;
+        pa *= t;
+        if (WITH_B) {
+          B[j % NB] += pb;
+          pb *= t;
+        }
+      }
     }
-  });
+  } else {
+    gcv_stream<4>(g, item, e0, e1, lane, [&](double r, double w) {
+      if (isinf(r)) return;
+      const double t = rcp_pos(r + mc);
+      double p = (w * t) * t;
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        A[j] += p;
+        p *= t;
+      }
+    });
+  }
 #pragma unroll
   for (int j = 0; j < J; ++j) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) A[j] += __shfl_xor_sync(0xffffffffu, A[j], o);
+    if (WITH_B)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) B[j % NB] += __shfl_xor_sync(0xffffffffu, B[j % NB], o);
   }
   if (lane == 0) {
-    double* base = partial + ((long long)item * nchunks + ch) * J;
+    double* base = partial + ((long long)item * nchunks + ch) * (WITH_B ? 2 : 1) * J;
 #pragma unroll
-    for (int j = 0; j < J; ++j) base[j] = A[j];
+    for (int j = 0; j < J; ++j) {
+      base[j] = A[j];
+      if (WITH_B) base[J + j] = B[j % NB];
+    }
   }
 }
 
@@ -2155,13 +2185,16 @@ __global__ void k_gcv_golden(const double* __restrict__ partial, int items, int 
   if (item >= items || !need[item]) return;
   double A[64], B[64];
   const int k = best_k[item];
+  const int w = Btab ? J : 2 * J;  // per-item B follows A in partial when there is no table
   for (int j = 0; j < J; ++j) {
     A[j] = 0.0;
-    B[j] = Btab[(long long)k * J + j];
+    B[j] = Btab ? Btab[(long long)k * J + j] : 0.0;
   }
   for (int c = 0; c < nchunks; ++c) {
-    const double* base = partial + ((long long)item * nchunks + c) * J;
+    const double* base = partial + ((long long)item * nchunks + c) * w;
     for (int j = 0; j < J; ++j) A[j] += base[j];
+    if (!Btab)
+      for (int j = 0; j < J; ++j) B[j] += base[J + j];
   }
   MomentG f{A, B, J, center[item]};
   const double best = bestG[item];
