@@ -222,6 +222,25 @@ def alg_bytes_per_px(name, cfg):
             "k_synth": c + 8, "k_gcv_grid": c, "k_gcv_moments": c}.get(name)
 
 
+def bluestein_flops_per_line(n, bc):
+    """Algorithmic fp64 flops of one real line through the half-length Bluestein
+    transform: two complex FFTs of M points (5 M log2 M each), the pointwise
+    product with DIF(b)/M (6 M) and the two chirp products (6 h each)."""
+    m = n if bc in (W.PERIODIC, W.REFLECTIVE) else n - 2
+    h = m + 1 if bc == W.ANTIREFLECTIVE else m // 2
+    M = 1
+    while M < max(2 * h - 1, 2):
+        M *= 2
+    return 2 * 5 * M * math.log2(M) + 6 * M + 12 * h
+
+
+def fp64_peak():
+    p = os.path.join(ROOT, "profiles", "r01_measured_peaks_extra.json")
+    if os.path.exists(p):
+        return json.load(open(p))["fp64_fma_tflops"], "measured (tools/probe_peaks.cu)"
+    return 37.0, "B200 datasheet fp64"
+
+
 def main():
     args = parse()
     import torch
@@ -360,6 +379,23 @@ def main():
                     "peak_source": peak_src,
                     "share_of_step": (ms_tot / args.steps) / ms_step,
                     "alg_bytes_per_launch": bytes_launch}
+    # fp64 roofline of the transform kernels: Bluestein FFTs are fp64-bound on B200
+    croof = None
+    fft_kernels = [k for k in prof if k in ("k_analyze", "k_synth_filter", "k_synth")]
+    if fft_kernels:
+        fdom = max(fft_kernels, key=lambda k: prof[k][0])
+        ms_tot, cnt = prof[fdom]
+        # per step: every line of length n1 (1D; 2D column pass) and n2 (2D row pass)
+        fl_step = bluestein_flops_per_line(cfg.n1, cfg.bc) * px_rank / cfg.n1
+        if cfg.dim == 2:
+            fl_step += bluestein_flops_per_line(cfg.n2, cfg.bc) * px_rank / cfg.n2
+        fl = fl_step * args.steps / cnt  # per launch
+        tf = fl / (ms_tot / cnt / 1e3) / 1e12
+        pk, pks = fp64_peak()
+        croof = {"kernel": fdom, "bound": "fp64", "achieved": tf, "peak": pk, "unit": "TFLOP/s",
+                 "frac": tf / pk, "peak_source": pks,
+                 "alg_flops_per_launch": fl,
+                 "model": "2 x 5 M log2 M + 6 M + 12 h per line (half-length Bluestein)"}
     pipeline_bytes = 16 * px_rank  # read g + write f
     if cfg.dim == 2 and cfg.batch == 1:
         pipeline_bytes = 56 * px_rank  # 7-touch out-of-core model (config 2)
@@ -395,7 +431,7 @@ def main():
             "pipeline_hbm": {"alg_bytes_per_step": pipeline_bytes * world,
                              "achieved_gbs": pipeline_bytes / (ms_step / 1e3) / 1e9,
                              "frac": pipeline_bytes / (ms_step / 1e3) / 1e9 / peak},
-            "kernels": kernels, "cpu_baseline": cpu,
+            "kernels": kernels, "compute_roofline": croof, "cpu_baseline": cpu,
             "gcv": {"best_k_range": [int(bk.min()), int(bk.max())],
                     "mu_median": float(np.median(mu))},
         }
