@@ -167,6 +167,43 @@ long long fd_kernel_launches(void);
 void fd_profile_enable(int on);
 int fd_profile_collect(int max_names, char* names, double* total_ms, int* counts, int* n_out);
 
+/* ---- One 2D image split into row slabs across GPUs ----
+ * The reference runs one image on one host (tensor_apply, multidim.cpp:171-198;
+ * gcv_select_2d / tikhonov_solve_2d, multidim.cpp:358-442); these calls are the
+ * per-rank pieces of the same computation, for separable operators.  A rank
+ * holding rows [r0, r0+R) analyzes its rows (axis 2), the caller transposes to
+ * column slabs (C columns from col0, stored as contiguous lines of length n1),
+ * analyzes them (axis 1) and sums the GCV partials / moments over ranks; the
+ * selection then runs on the sums (identical on every rank), and the filtered
+ * column synthesis + transposed row synthesis rebuild the rows.  Rows-then-
+ * columns equals tensor_apply's columns-then-rows up to rounding. */
+int fd_slab_analyze(const fd_op* op, int axis, const void* in, int in_complex, void* out,
+                    long long nlines, void* stream);
+/* L != NULL: apply_tikhonov_filter (regularize.hpp:42-58) with `mu` fused into
+ * the column pass (axis 1, lines = columns col0 ..). */
+int fd_slab_synthesize(const fd_op* op, const fd_smoother* L, int axis, const void* in, void* out,
+                       int out_complex, long long nlines, long long col0, double mu,
+                       void* stream);
+/* gcv_from_coeffs partial sums (regularize.hpp:63-81) of a column slab on the
+ * log grid (mus == NULL) or on `grid_count` explicit mus: num_den[0..K) = sum
+ * sigma^2 |ghat|^2, num_den[K..2K) = sum sigma.  Synchronous (host output). */
+int fd_slab_gcv_partials(const fd_op* op, const fd_smoother* L, const void* ghat, long long ncols,
+                         long long col0, double mu_min, double mu_max, int grid_count,
+                         const double* mus, double* num_den, void* stream);
+/* Taylor moments [A_0..A_{J-1}, B_0..B_{J-1}] about `center` of a column slab
+ * (the golden-section series of k_gcv_moments).  Synchronous. */
+int fd_slab_gcv_moments(const fd_op* op, const fd_smoother* L, const void* ghat, long long ncols,
+                        long long col0, double center, int J, double* moments, void* stream);
+/* gcv_minimize (regularize.cpp:281-351) on summed partials, host only:
+ * moment count J (0: coarse grid, refine with direct evaluations), grid pick
+ * (first minimum, 1e-12 ties, bracket centre), golden section on the moments. */
+int fd_gcv_moment_terms(double mu_min, double mu_max, int grid_count, int* J);
+int fd_gcv_pick_from_sums(const double* num_den, double mu_min, double mu_max, int grid_count,
+                          double* G, int* best_k, int* need_refine, double* center, double* mu);
+int fd_gcv_golden_from_moments(const double* moments, int J, double center, double best_G,
+                               double mu_min, double mu_max, int grid_count, int best_k,
+                               double* mu);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,16 +28,20 @@ def needs_build():
     return any(os.path.getmtime(s) > t for s in sources() + [hdr])
 
 
-def build_library(force=False, verbose=False):
-    if not force and not needs_build():
+def build_library(force=False, verbose=False, out=None, defines=()):
+    """Compile fd_capi.cu (one translation unit) into `out` (default LIB);
+    `defines` adds -D flags (e.g. FD_PHASE_CLOCKS for a timing build)."""
+    out = out or LIB
+    if out == LIB and not defines and not force and not needs_build():
         return LIB
     nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
-    cmd = [nvcc, *ARCH, *FLAGS, os.path.join(CSRC, "fd_capi.cu"), "-o", LIB + ".tmp"]
+    cmd = [nvcc, *ARCH, *FLAGS, *("-D" + d for d in defines), os.path.join(CSRC, "fd_capi.cu"),
+           "-o", out + ".tmp"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":

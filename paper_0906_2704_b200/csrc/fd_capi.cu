@@ -1532,6 +1532,20 @@ const char* fd_last_error(void) { return g_err.c_str(); }
 int fd_version(void) { return 1; }
 long long fd_kernel_launches(void) { return g_launches.load(); }
 
+#ifdef FD_PHASE_CLOCKS
+// timing build only: accumulated SM clocks [kernel][phase] of the real-line
+// kernels (k_ranalyze = 0, k_rsynth = 1; load, convolution, post); reset = 1 zeroes
+int fd_phase_clocks(unsigned long long* out, int reset) {
+  return guarded([&] {
+    ck(cudaMemcpyFromSymbol(out, fdb::g_phase_clocks, sizeof(unsigned long long) * 8), "clk");
+    if (reset) {
+      unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      ck(cudaMemcpyToSymbol(fdb::g_phase_clocks, z, sizeof(z)), "clk");
+    }
+  });
+}
+#endif
+
 int fd_parse_bc(const char* name) {
   if (!name) return -1;
   const std::string s(name);
@@ -2164,6 +2178,237 @@ int fd_gcv_minimize_host(fd_gcv_fn G, void* ctx, double mu_min, double mu_max, i
     }
     auto f = [&](double x) { return G(x, ctx); };
     *mu = gcv_golden(gh.mus.data(), grid_count, pk.best_k, vals[pk.best_k], f);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// Row-slab distribution of one 2D image: a rank holds rows
+// [r0, r0 + R) of an n1 x n2 image.  Rows are transformed locally, an
+// all-to-all transposes to column slabs (C columns stored as contiguous lines of
+// length n1), the column pass, the GCV partial sums and the filtered column
+// synthesis run on the column slab, and the selection runs on the all-reduced
+// sums (identical on every rank).  Separable operators only: the spectral data
+// of a column slab is d2[c0 + l] d1[i], s2[c0 + l] + s1[i] -- the separable mode
+// with the factor roles swapped and offset by c0, so the kernels are unchanged.
+namespace {
+void check_slab(const fd_op* op, const fd_smoother* L, int axis) {
+  check_op(op);
+  if (op->dim != 2 || !op->sep) validation("slab passes need a separable 2D operator");
+  if (axis != 1 && axis != 2) validation("axis must be 1 (columns) or 2 (rows)");
+  if (L) {
+    check_L(op, L);
+    if (L->full) validation("slab passes need a separable smoother");
+  }
+}
+Spectral slab_spectral(const fd_op* op, const fd_smoother* L, long long col0) {
+  Spectral sp{};
+  sp.mode = 2;
+  sp.col_pass = 0;  // line l = column col0 + l, element = row i
+  sp.n2 = op->n1;
+  sp.dA = op->d2 + col0;
+  sp.dB = op->d1;
+  sp.smooth_sum = L ? L->sep_sum : 0;
+  sp.sA = (L && L->s2) ? L->s2 + col0 : nullptr;
+  sp.sB = L ? L->s1 : nullptr;
+  return sp;
+}
+GcvData slab_gcv_data(const fd_op* op, const fd_smoother* L, const void* ghat, long long ncols,
+                      long long col0) {
+  GcvData g{};
+  g.ghat = ghat;
+  g.cplx = op->cplx;
+  g.N = ncols * op->n1;
+  g.stride = g.N;
+  g.items = 1;
+  g.sp = slab_spectral(op, L, col0);
+  return g;
+}
+}  // namespace
+
+int fd_slab_analyze(const fd_op* op, int axis, const void* in, int in_complex, void* out,
+                    long long nlines, void* stream) {
+  return guarded([&] {
+    check_slab(op, nullptr, axis);
+    if (nlines <= 0) return;
+    Scratch S(as_stream(stream));
+    const Axis& ax = axis == 1 ? *op->ax1 : *op->ax2;
+    LineIO io{};
+    io.in = in;
+    io.out = out;
+    io.gi = lines_1d(ax.dev.n, nlines);
+    io.go = io.gi;
+    io.in_cplx = in_complex;
+    io.out_cplx = op->cplx;
+    launch_analyze(ax.dev, io, S.st);
+  });
+}
+
+int fd_slab_synthesize(const fd_op* op, const fd_smoother* L, int axis, const void* in, void* out,
+                       int out_complex, long long nlines, long long col0, double mu,
+                       void* stream) {
+  return guarded([&] {
+    check_slab(op, L, axis);
+    if (L && axis != 1) validation("the filter is fused into the column pass (axis 1)");
+    if (L && !(mu > 0.0)) validation("mu must be positive");
+    if (nlines <= 0) return;
+    Scratch S(as_stream(stream));
+    const Axis& ax = axis == 1 ? *op->ax1 : *op->ax2;
+    LineIO io{};
+    io.in = in;
+    io.out = out;
+    io.gi = lines_1d(ax.dev.n, nlines);
+    io.go = io.gi;
+    io.in_cplx = op->cplx;
+    io.out_cplx = out_complex;
+    SynthArgs sa{};
+    double* dmu = nullptr;
+    if (L) {
+      dmu = S.get<double>(1);
+      ck(cudaMemcpyAsync(dmu, &mu, sizeof(double), cudaMemcpyHostToDevice, S.st), "mu");
+      sa.mode = 1;
+      sa.sp = slab_spectral(op, L, col0);
+      sa.mu_item = dmu;
+      io.gi.per_item = (int)nlines;  // one item: every line reads mu_item[0]
+      io.gi.item_stride = 0;
+      io.gi.line_stride = ax.dev.n;
+      io.go = io.gi;
+    }
+    launch_synth(ax.dev, io, sa, S.st);
+    if (dmu) ck(cudaStreamSynchronize(S.st), "sync");  // mu is a stack value
+  });
+}
+
+int fd_slab_gcv_partials(const fd_op* op, const fd_smoother* L, const void* ghat, long long ncols,
+                         long long col0, double mu_min, double mu_max, int grid_count,
+                         const double* mus, double* num_den, void* stream) {
+  return guarded([&] {
+    check_slab(op, L, 1);
+    if (!num_den) validation("null output");
+    std::vector<double> hm, hl;
+    if (mus) {  // explicit grid (direct evaluations of the golden section)
+      if (grid_count < 1) validation("grid_count must be positive");
+      hm.assign(mus, mus + grid_count);
+      for (double m : hm) {
+        if (!(m > 0.0)) validation("mu must be positive");
+        hl.push_back(std::log(m));
+      }
+    } else {
+      const GridHost gh = make_grid(mu_min, mu_max, grid_count);
+      hm = gh.mus;
+      hl = gh.logmus;
+    }
+    const int K = grid_count;
+    if (ncols <= 0) {
+      std::fill(num_den, num_den + 2 * K, 0.0);
+      return;
+    }
+    Scratch S(as_stream(stream));
+    double* dg = S.get<double>(2 * (size_t)K);
+    std::vector<double> t(hm);
+    t.insert(t.end(), hl.begin(), hl.end());
+    ck(cudaMemcpyAsync(dg, t.data(), t.size() * sizeof(double), cudaMemcpyHostToDevice, S.st),
+       "grid");
+    const GcvGrid grid{K, dg, dg + K};
+    const GcvData g = slab_gcv_data(op, L, ghat, ncols, col0);
+    const int nch = pick_chunks(g.N, 1, 1);
+    const long long chunk = (g.N + nch - 1) / nch;
+    double* part = S.get<double>((size_t)nch * 2 * K);
+    launch_grid(g, grid, chunk, nch, part, S.st);
+    double* sums = part;
+    if (nch > 1) {
+      sums = S.get<double>(2 * (size_t)K);
+      k_reduce_partials<<<dim3(1, (2 * K + 31) / 32), 256, 0, S.st>>>(part, nch, 2 * K, sums);
+      launched("k_reduce_partials");
+    }
+    ck(cudaMemcpyAsync(num_den, sums, 2 * K * sizeof(double), cudaMemcpyDeviceToHost, S.st),
+       "sums");
+    ck(cudaStreamSynchronize(S.st), "sync");
+  });
+}
+
+int fd_slab_gcv_moments(const fd_op* op, const fd_smoother* L, const void* ghat, long long ncols,
+                        long long col0, double center, int J, double* moments, void* stream) {
+  return guarded([&] {
+    check_slab(op, L, 1);
+    if (!moments) validation("null output");
+    if (J < 4 || J > 48 || J % 4) validation("moment count must be 4..48 in steps of 4");
+    if (ncols <= 0) {
+      std::fill(moments, moments + 2 * J, 0.0);
+      return;
+    }
+    Scratch S(as_stream(stream));
+    const GcvData g = slab_gcv_data(op, L, ghat, ncols, col0);
+    double* dc = S.get<double>(1);
+    int* need = S.get<int>(1);
+    const int one = 1;
+    ck(cudaMemcpyAsync(dc, &center, sizeof(double), cudaMemcpyHostToDevice, S.st), "c");
+    ck(cudaMemcpyAsync(need, &one, sizeof(int), cudaMemcpyHostToDevice, S.st), "need");
+    const int nch = pick_chunks(g.N, 1, 1);
+    const long long chunk = (g.N + nch - 1) / nch;
+    double* part = S.get<double>((size_t)nch * 2 * J);
+    const GcvGrid nogrid{0, nullptr, nullptr};
+    launch_moments(J, g, nogrid, dc, need, chunk, nch, part, nullptr, S.st);
+    double* sums = part;
+    if (nch > 1) {
+      sums = S.get<double>(2 * (size_t)J);
+      k_reduce_partials<<<dim3(1, (2 * J + 31) / 32), 256, 0, S.st>>>(part, nch, 2 * J, sums);
+      launched("k_reduce_partials");
+    }
+    ck(cudaMemcpyAsync(moments, sums, 2 * J * sizeof(double), cudaMemcpyDeviceToHost, S.st),
+       "moments");
+    ck(cudaStreamSynchronize(S.st), "sync");
+  });
+}
+
+// ---- selection from all-reduced sums (host; gcv_minimize, regularize.cpp:281-351) ----
+int fd_gcv_moment_terms(double mu_min, double mu_max, int grid_count, int* J) {
+  return guarded([&] {
+    make_grid(mu_min, mu_max, grid_count);
+    *J = gcv_moment_terms(mu_min, mu_max, grid_count);
+  });
+}
+
+// G_k = num_k / den_k^2, first minimum, 1e-12 ties, bracket centre.  *mu is the
+// final answer when *need_refine == 0 (ties), else the grid value at best_k.
+int fd_gcv_pick_from_sums(const double* num_den, double mu_min, double mu_max, int grid_count,
+                          double* G, int* best_k, int* need_refine, double* center, double* mu) {
+  return guarded([&] {
+    if (!num_den || !best_k || !need_refine || !center || !mu) validation("null argument");
+    const GridHost gh = make_grid(mu_min, mu_max, grid_count);
+    const int K = grid_count;
+    std::vector<double> vals(K);
+    for (int k = 0; k < K; ++k) {
+      const double den = num_den[K + k];
+      if (den == 0.0) degenerate("degenerate gcv: all smoother eigenvalues are zero");
+      vals[k] = num_den[k] / (den * den);
+    }
+    if (G) std::copy(vals.begin(), vals.end(), G);
+    const GcvPick pk = gcv_pick(gh.mus.data(), gh.logmus.data(), vals.data(), K);
+    *best_k = pk.best_k;
+    *need_refine = pk.tied ? 0 : 1;
+    *center = pk.tied ? 0.0 : std::sqrt(pk.lo * pk.hi);
+    *mu = pk.tied ? pk.mu_tie : gh.mus[pk.best_k];
+  });
+}
+
+// golden section on the Taylor moments [A_0..A_{J-1}, B_0..B_{J-1}] about
+// `center` (the same series and control flow as k_gcv_golden)
+int fd_gcv_golden_from_moments(const double* moments, int J, double center, double best_G,
+                               double mu_min, double mu_max, int grid_count, int best_k,
+                               double* mu) {
+  return guarded([&] {
+    if (!moments || !mu) validation("null argument");
+    const GridHost gh = make_grid(mu_min, mu_max, grid_count);
+    auto Gm = [&](double x) {
+      const double d = -(x - center);
+      double num = 0.0, den = 0.0;
+      for (int j = J - 1; j >= 0; --j) {
+        num = std::fma(num, d, (double)(j + 1) * moments[j]);
+        den = std::fma(den, d, moments[J + j]);
+      }
+      return num / (den * den);
+    };
+    *mu = gcv_golden(gh.mus.data(), grid_count, best_k, best_G, Gm);
   });
 }
 

@@ -986,6 +986,22 @@ __device__ __forceinline__ Stage stage_init(double2* x, int h, int Mloc, double2
 //   [border0, border_n-1] [X_0, X_h] X_1 .. X_{h-1}   (double2 slots; the
 //   border slot only when bordered) -- the coefficients of real data in this
 //   basis are exactly Hermitian once the border is folded in.
+// Optional phase timing of the real-line kernels (build with -DFD_PHASE_CLOCKS):
+// thread 0 of every CTA adds the SM clocks of [line start, load done),
+// [load done, convolution done), [convolution done, line done) and the
+// staging wait at the line start, per kernel.
+#ifdef FD_PHASE_CLOCKS
+__device__ unsigned long long g_phase_clocks[2][4];
+#define FD_CLK(v) long long v = clock64()
+#define FD_CLK_SET(v) v = clock64()
+#define FD_CLK_ADD(k, i, a, b) \
+  if (threadIdx.x == 0) atomicAdd(&g_phase_clocks[k][i], (unsigned long long)((b) - (a)))
+#else
+#define FD_CLK(v)
+#define FD_CLK_SET(v)
+#define FD_CLK_ADD(k, i, a, b)
+#endif
+
 // LOGM > 0: size-specialised Bluestein core (bluestein_t), blockDim = FftShape<LOGM>::NT
 template <int LOGM>
 __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, double2* scr) {
@@ -1017,11 +1033,14 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   const long long oi = line_offset(io.gi, l), es = io.gi.elem_stride;
   const int n = ax.n, m = ax.m;
   const double* in = reinterpret_cast<const double*>(io.in);
+  FD_CLK(c0);
   const bool st = stage_line(stg, io, l, n);
   if (st) {
     mbar_wait(stg.bar, stg.phase);
     stg.phase ^= 1;
   }
+  FD_CLK(cw);
+  FD_CLK_ADD(0, 3, c0, cw);
   const double* sin_ = stg.buf;
   auto ld = [&](int e) { return st ? sin_[e] : __ldg(in + oi + e * es); };
   const Fold fd = fold_terms(ax, ld);
@@ -1054,6 +1073,8 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   }
   __syncthreads();
 
+  FD_CLK(c1);
+  FD_CLK(c2);
   if (!big) {
     if constexpr (LOGM > 0)
       bluestein_t<LOGM>(x, T, tw, h);
@@ -1061,6 +1082,9 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
       bluestein_core(x, T, tw, h);
     // the post phase reads [0, h) only: stage the next line behind it
     if (threadIdx.x == 0) stage_issue(stg, io, l + gridDim.x, n);
+    FD_CLK_SET(c2);
+    FD_CLK_ADD(0, 0, c0, c1);
+    FD_CLK_ADD(0, 1, c1, c2);
   } else {
     for (int j = threadIdx.x; j < h; j += blockDim.x) scrA[j] = x[pidx(j)];
     bluestein_half(x, T, tw, 1, h);  // x = a (.) W, convolved: y1
@@ -1178,6 +1202,12 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
     }
   }
   __syncthreads();  // x and the scratch are reused by the next line
+#ifdef FD_PHASE_CLOCKS
+  if (!big) {
+    FD_CLK(c3);
+    FD_CLK_ADD(0, 2, c2, c3);
+  }
+#endif
   }
 }
 
@@ -1219,11 +1249,14 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
   for (int l = blockIdx.x; l < io.gi.count; l += gridDim.x) {
   const long long oi = line_offset(io.gi, l);
   const int n = ax.n, m = ax.m;
+  FD_CLK(c0);
   const bool st = stage_line(stg, io, l, n);
   if (st) {
     mbar_wait(stg.bar, stg.phase);
     stg.phase ^= 1;
   }
+  FD_CLK(cw);
+  FD_CLK_ADD(1, 3, c0, cw);
   const double mu = line_mu(sa, io.gi, l);
   auto filt = [&](int e, double2 c) { return coeff_filter_fast(ax, sa, io.gi, l, e, c, mu); };
   auto cf = [&](int e) {
@@ -1307,12 +1340,17 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
   }
   __syncthreads();
 
+  FD_CLK(c1);
+  FD_CLK(c2);
   if (!big) {
     if constexpr (LOGM > 0)
       bluestein_t<LOGM>(x, T, tw, h);
     else
       bluestein_core(x, T, tw, h);
     if (threadIdx.x == 0) stage_issue(stg, io, l + gridDim.x, n);
+    FD_CLK_SET(c2);
+    FD_CLK_ADD(1, 0, c0, c1);
+    FD_CLK_ADD(1, 1, c1, c2);
   } else {
     for (int j = threadIdx.x; j < h; j += blockDim.x) scrA[j] = x[pidx(j)];
     bluestein_half(x, T, tw, 1, h);
@@ -1372,6 +1410,12 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
     out[oo + (long long)(n - 1) * eso] = ax.q0 * un;
   }
   __syncthreads();  // x and the scratch are reused by the next line
+#ifdef FD_PHASE_CLOCKS
+  if (!big) {
+    FD_CLK(c3);
+    FD_CLK_ADD(1, 2, c2, c3);
+  }
+#endif
   }
 }
 

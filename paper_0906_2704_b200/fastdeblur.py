@@ -21,7 +21,8 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfdb200.so")
+# FASTDEBLUR_LIB: an alternative in-tree build (e.g. the phase-timing variant)
+LIB_PATH = os.environ.get("FASTDEBLUR_LIB") or os.path.join(_HERE, "libfdb200.so")
 
 BC = {"periodic": 0, "reflective": 1, "antireflective": 2, "hoc-cosine": 3, "hoc-fourier": 4}
 BC_NAMES = {v: k for k, v in BC.items()}
@@ -57,6 +58,15 @@ def lib():
         L.fd_op_create_2d.argtypes = [dp, ip, ip, ip, ip, ip, ip, C.POINTER(vp)]
         L.fd_op_create_2d_separable.argtypes = [dp, ip, dp, ip, ip, ip, ip, ip, C.POINTER(vp)]
         L.fd_op_destroy.argtypes = [vp]
+        cd = C.c_double
+        L.fd_slab_analyze.argtypes = [vp, ip, vp, ip, vp, ll, vp]
+        L.fd_slab_synthesize.argtypes = [vp, vp, ip, vp, vp, ip, ll, ll, cd, vp]
+        L.fd_slab_gcv_partials.argtypes = [vp, vp, vp, ll, ll, cd, cd, ip, dp, dp, vp]
+        L.fd_slab_gcv_moments.argtypes = [vp, vp, vp, ll, ll, cd, ip, dp, vp]
+        L.fd_gcv_moment_terms.argtypes = [cd, cd, ip, C.POINTER(C.c_int)]
+        L.fd_gcv_pick_from_sums.argtypes = [dp, cd, cd, ip, dp, C.POINTER(C.c_int),
+                                            C.POINTER(C.c_int), dp, dp]
+        L.fd_gcv_golden_from_moments.argtypes = [dp, ip, cd, cd, cd, cd, ip, ip, dp]
         L.fd_op_info.argtypes = [vp] + [C.POINTER(C.c_int)] * 5
         L.fd_op_eigenvalues.argtypes = [vp, vp, vp]
         L.fd_smoother_create.argtypes = [vp, ip, C.POINTER(vp)]

@@ -275,13 +275,14 @@ def _noise_band(key, e0, e1):
 
 def _band_job(args):
     from multiprocessing import shared_memory
-    phase, ci, item, n1, n2, b0, b1, name, scale = args
+    phase, ci, item, n1, n2, b0, b1, name, scale, r0, rows = args
     cfg = config(ci)
     w = cfg.psf
     m = (len(w) - 1) // 2
     shm = shared_memory.SharedMemory(name=name)
     try:
-        out = np.ndarray((n1, n2), dtype=np.float64, buffer=shm.buf)
+        # the shared buffer holds image rows [r0, r0 + rows)
+        out = np.ndarray((rows, n2), dtype=np.float64, buffer=shm.buf)
         key = item_key(ci, np.uint64(item))
         if phase == 0:
             _, f = _scene_2d(cfg, item, n1, n2, m, m, b0, b1 + 2 * m)
@@ -290,11 +291,11 @@ def _band_job(args):
             for j in range(-m, m + 1):               # columns, same term order
                 if w[m + j] != 0.0:
                     h += w[m + j] * g[m + j:m + j + (b1 - b0)]
-            out[b0:b1] = h
+            out[b0 - r0:b1 - r0] = h
             eta = _noise_band(key, b0 * n2, b1 * n2)
             return float(np.sum(h * h)), float(np.sum(eta * eta))
         eta = _noise_band(key, b0 * n2, b1 * n2).reshape(b1 - b0, n2)
-        out[b0:b1] += scale * eta
+        out[b0 - r0:b1 - r0] += scale * eta
         return 0.0, 0.0
     finally:
         shm.close()
@@ -304,24 +305,39 @@ def image_2d_large(ci: int, item: int, workers: int | None = None, n1: int | Non
                    n2: int | None = None) -> np.ndarray:
     """Observed image ``item`` of 2D config ``ci`` built band-parallel (the
     scene, separable valid blur and add_noise of image_2d)."""
+    cfg = config(ci)
+    n1 = cfg.n1 if n1 is None else n1
+    return image_2d_rows(ci, item, 0, n1, workers, n1, n2)
+
+
+def image_2d_rows(ci: int, item: int, r0: int, r1: int, workers: int | None = None,
+                  n1: int | None = None, n2: int | None = None, reduce=None) -> np.ndarray:
+    """Rows [r0, r1) of image_2d_large (r0 a multiple of SLAB).  ``reduce`` sums
+    the noise-norm partials over the other holders of the image (the ranks of a
+    row-slab split); the whole-image norm is their sum."""
     import os
     from concurrent.futures import ProcessPoolExecutor
     from multiprocessing import shared_memory
     cfg = config(ci)
     n1 = cfg.n1 if n1 is None else n1
     n2 = cfg.n2 if n2 is None else n2
-    shm = shared_memory.SharedMemory(create=True, size=n1 * n2 * 8)
+    if r0 % SLAB:
+        raise ValueError("row ranges start on band boundaries")
+    rows = r1 - r0
+    shm = shared_memory.SharedMemory(create=True, size=max(rows, 1) * n2 * 8)
     try:
-        bands = [(b, min(b + SLAB, n1)) for b in range(0, n1, SLAB)]
+        bands = [(b, min(b + SLAB, r1)) for b in range(r0, r1, SLAB)]
         workers = workers or os.cpu_count() or 1
         with ProcessPoolExecutor(workers) as ex:
-            parts = list(ex.map(_band_job, [(0, ci, item, n1, n2, b0, b1, shm.name, 0.0)
+            parts = list(ex.map(_band_job, [(0, ci, item, n1, n2, b0, b1, shm.name, 0.0, r0, rows)
                                            for b0, b1 in bands]))
-            gn = sum(p[0] for p in parts)
-            en = sum(p[1] for p in parts)
-            scale = cfg.noise * math.sqrt(gn / en)
-            list(ex.map(_band_job, [(1, ci, item, n1, n2, b0, b1, shm.name, scale) for b0, b1 in bands]))
-        return np.array(np.ndarray((n1, n2), dtype=np.float64, buffer=shm.buf))
+            sums = np.array([sum(p[0] for p in parts), sum(p[1] for p in parts)])
+            if reduce is not None:
+                sums = np.asarray(reduce(sums), dtype=np.float64)
+            scale = cfg.noise * math.sqrt(sums[0] / sums[1])
+            list(ex.map(_band_job, [(1, ci, item, n1, n2, b0, b1, shm.name, scale, r0, rows)
+                                    for b0, b1 in bands]))
+        return np.array(np.ndarray((rows, n2), dtype=np.float64, buffer=shm.buf))
     finally:
         shm.close()
         shm.unlink()

@@ -77,3 +77,23 @@ def test_image_2d_large_matches_serial():
     _, g = W.image_2d(W.config(4), 1, 600, 300)
     got = W.image_2d_large(4, 1, workers=3, n1=600, n2=300)
     assert np.max(np.abs(got - g)) < 1e-14 * np.max(np.abs(g))
+
+
+def test_image_2d_rows_split():
+    """Row bands of a split image equal the whole image (the noise norm summed
+    over the bands' holders, as the ranks of a row-slab split do)."""
+    whole = W.image_2d_large(4, 2, workers=2, n1=768, n2=200)
+    parts = [W.image_2d_rows(4, 2, r0, r0 + 256, workers=2, n1=768, n2=200) for r0 in (0, 256, 512)]
+    # without a reduction each part normalises alone; with it they match
+    sums = []
+    import numpy as np
+    def collect(s):
+        sums.append(s)
+        return s
+    for r0 in (0, 256, 512):
+        W.image_2d_rows(4, 2, r0, r0 + 256, workers=2, n1=768, n2=200, reduce=collect)
+    tot = sum(sums)
+    got = np.concatenate([W.image_2d_rows(4, 2, r0, r0 + 256, workers=2, n1=768, n2=200,
+                                          reduce=lambda s: tot) for r0 in (0, 256, 512)])
+    assert np.max(np.abs(got - whole)) < 1e-14 * np.max(np.abs(whole))
+    assert parts[0].shape == (256, 200)
