@@ -167,6 +167,15 @@ long long fd_kernel_launches(void);
 void fd_profile_enable(int on);
 int fd_profile_collect(int max_names, char* names, double* total_ms, int* counts, int* n_out);
 
+/* sweep_mu / sweep_mu_2d (pipeline.cpp:55-115, BcSweep pipeline.hpp:23-45) for
+ * one signal or image g (device): curve_mu / curve_gcv / curve_rre get the K
+ * grid points, G(mu) and RRE(mu) (NaN without truth; HOST arrays of K), and
+ * summary = {min_rre, mu_opt, mu_gcv, rre_gcv} (host, 4).  truth: device array
+ * of the signal's shape, or NULL.  Synchronous. */
+int fd_sweep_mu(const fd_op* op, const fd_smoother* L, const double* g, const double* truth,
+                double mu_min, double mu_max, int grid_count, double* curve_mu,
+                double* curve_gcv, double* curve_rre, double* summary, void* stream);
+
 /* ---- One 2D image split into row slabs across GPUs ----
  * The reference runs one image on one host (tensor_apply, multidim.cpp:171-198;
  * gcv_select_2d / tikhonov_solve_2d, multidim.cpp:358-442); these calls are the

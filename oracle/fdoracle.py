@@ -887,6 +887,28 @@ def convolve_valid_2d(ext, p: Psf2D):
     return g
 
 
+def sweep_mu(op: BlurOperator, s, g, truth=None, mu_min=1e-12, mu_max=10.0, count=200):
+    """sweep_mu (pipeline.cpp:55-115): GCV selection, then for every grid mu a
+    Tikhonov solve and its rre; the first strict RRE minimum gives mu_opt.
+    -> (mus, G, rre, [min_rre, mu_opt, mu_gcv, rre_gcv]) (NaN rre without truth)."""
+    g = np.asarray(g, dtype=np.float64)
+    r = gcv_select(op, s, g, mu_min, mu_max, count)
+    mus = np.asarray(r.mus, dtype=np.float64)
+    G = np.asarray(r.vals, dtype=np.float64)
+    nan = float("nan")
+    if truth is None:
+        return mus, G, np.full(count, nan), np.array([nan, nan, r.mu, nan])
+    t = np.asarray(truth, dtype=np.float64)
+    if np.sum(t * t) == 0.0:
+        raise ValidationError("rre: zero ground truth")
+    rr = np.array([rre(t, tikhonov_solve(op, s, g, m)[0]) for m in mus])
+    best, mu_opt = np.inf, mus[0]
+    for k in range(count):
+        if rr[k] < best:
+            best, mu_opt = rr[k], mus[k]
+    return mus, G, rr, np.array([best, mu_opt, r.mu, rre(t, tikhonov_solve(op, s, g, r.mu)[0])])
+
+
 def rre(truth, restored):
     """regularize.cpp:386-397."""
     truth, restored = np.asarray(truth), np.asarray(restored)

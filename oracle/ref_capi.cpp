@@ -12,6 +12,7 @@
 //   tikhonov_solve(_2d), gcv_value(_2d)    regularize.cpp:209-279, multidim.cpp:462-519
 //   gcv_minimize, gcv_select(_2d)          regularize.cpp:281-384, multidim.cpp:521-546
 //   deblur(_2d)                            pipeline.cpp:760-778
+//   sweep_mu                               pipeline.cpp:55-115
 //   add_noise, convolve_valid(_2d)         operators.cpp:443-469, pipeline.cpp:628-664
 // Status codes follow the CLI mapping (fastdeblur.cpp:442-451):
 // 0 ok, 2 ValidationError, 3 DegenerateError, 1 anything else.
@@ -222,6 +223,34 @@ int ref_matvec_1d(const double* psf, int len, int n, int bc, const double* f, do
     const fd::BlurOperator op = fd::build_operator(psf_of(psf, len), n, bc_of(bc));
     const auto y = fd::blur_apply(op, std::span<const double>(f, n), imag_residue);
     std::copy(y.begin(), y.end(), out);
+  });
+}
+
+// sweep_mu (pipeline.cpp:55-115): curve (mu, G, rre) and summary
+// {min_rre, mu_opt, mu_gcv, rre_gcv}; truth may be null (NaN rre fields).
+int ref_sweep_mu_1d(const double* psf, int len, int n, int bc, int smoother,
+                    const double* s_custom, const double* g, const double* truth, double mu_min,
+                    double mu_max, int count, double* mus, double* G, double* rre,
+                    double* summary) {
+  return guarded([&] {
+    const fd::BlurOperator op = fd::build_operator(psf_of(psf, len), n, bc_of(bc));
+    const auto L = smoother_1d(smoother, s_custom, op);
+    fd::GcvSearch s;
+    s.mu_min = mu_min;
+    s.mu_max = mu_max;
+    s.count = count;
+    const fd::BcSweep sw =
+        fd::sweep_mu(op, L, std::span<const double>(g, n),
+                     truth ? std::span<const double>(truth, n) : std::span<const double>(), s);
+    for (size_t k = 0; k < sw.curve.size(); ++k) {
+      mus[k] = sw.curve[k].mu;
+      G[k] = sw.curve[k].gcv;
+      rre[k] = sw.curve[k].rre;
+    }
+    summary[0] = sw.min_rre;
+    summary[1] = sw.mu_opt;
+    summary[2] = sw.mu_gcv;
+    summary[3] = sw.rre_gcv;
   });
 }
 

@@ -95,6 +95,19 @@ def matvec_1d(psf, n, bc, f):
     return out, res.value
 
 
+def sweep_mu_1d(psf, n, bc, smoother, g, truth=None, mu_min=1e-12, mu_max=10.0, count=200,
+                s_custom=None):
+    """sweep_mu (pipeline.cpp:55-115) -> (mus, G, rre, [min_rre, mu_opt, mu_gcv, rre_gcv])."""
+    psf, g = _f64(psf), _f64(g)
+    t = None if truth is None else _f64(truth)
+    sc = None if s_custom is None else _f64(s_custom)
+    mus, G, rre, summ = np.empty(count), np.empty(count), np.empty(count), np.empty(4)
+    _chk(lib().ref_sweep_mu_1d(_p(psf), len(psf), n, bc, smoother, _p(sc), _p(g), _p(t),
+                               C.c_double(mu_min), C.c_double(mu_max), count, _p(mus), _p(G),
+                               _p(rre), _p(summ)))
+    return mus, G, rre, summ
+
+
 def gcv_value_1d(psf, n, bc, smoother, g, mu, s_custom=None):
     psf, g = _f64(psf), _f64(g)
     G = C.c_double()

@@ -858,9 +858,11 @@ void run_analyze(const fd_op* op, const void* in, int in_cplx, void* out, long l
 
 // synthesize coefficients (basis type) -> out, with mode 0/1/2 fused into the
 // first (column) pass; real output keeps Re and reports the residue per item.
+// shared_in: every item reads the same coefficients (input item stride 0:
+// one analysis, many mu -- the mu sweep)
 void run_synth(const fd_op* op, const fd_smoother* L, const void* in, void* out, int out_cplx,
                int mode, const double* mu_item, double* resid, long long count, Scratch& S,
-               int pack = 0) {
+               int pack = 0, bool shared_in = false) {
   const int oc = op->cplx;
   if (op->dim == 1) {
     LineIO io{};
@@ -868,7 +870,10 @@ void run_synth(const fd_op* op, const fd_smoother* L, const void* in, void* out,
     io.in = in;
     io.out = out;
     io.gi = lines_1d(op->n1, count);
-    io.go = io.gi;
+    if (shared_in) {  // line l = item l: per_item 1 keeps mu_item[l]
+      io.gi.item_stride = 0;
+    }
+    io.go = lines_1d(op->n1, count);
     io.in_cplx = oc;
     io.out_cplx = out_cplx;
     SynthArgs sa{};
@@ -909,6 +914,7 @@ void run_synth(const fd_op* op, const fd_smoother* L, const void* in, void* out,
   a.in = in;
   a.out = mid;
   a.gi = cols;
+  if (shared_in) a.gi.item_stride = 0;
   a.go = cols;
   a.in_cplx = oc;
   a.out_cplx = oc;
@@ -2178,6 +2184,98 @@ int fd_gcv_minimize_host(fd_gcv_fn G, void* ctx, double mu_min, double mu_max, i
     }
     auto f = [&](double x) { return G(x, ctx); };
     *mu = gcv_golden(gh.mus.data(), grid_count, pk.best_k, vals[pk.best_k], f);
+  });
+}
+
+// ---------------------------------------------------------------------------
+// mu sweep with RRE (sweep_mu / sweep_mu_2d, pipeline.cpp:55-115): the GCV curve
+// on the grid, a restoration per grid mu (one analysis, K filtered syntheses in
+// batches sharing the coefficients), rre against the truth, and the restoration
+// at the GCV choice.
+namespace {
+void rre_dev(const double* f, const double* truth, long long N, int items, double* rre,
+             Scratch& S) {
+  const int nch = (int)std::max(1LL, std::min(4096LL / std::max(items, 1), N / 4096));
+  const long long chunk = (N + nch - 1) / nch;
+  double* part = S.get<double>((size_t)items * nch * 2);
+  k_rre_partials<<<dim3(items, nch), 256, 0, S.st>>>(f, truth, N, chunk, part);
+  launched("k_rre_partials");
+  double* sums = part;
+  if (nch > 1) {
+    sums = S.get<double>((size_t)items * 2);
+    k_reduce_partials<<<dim3(items, 1), 256, 0, S.st>>>(part, nch, 2, sums);
+    launched("k_reduce_partials");
+  }
+  k_rre_final<<<(items + 127) / 128, 128, 0, S.st>>>(sums, items, rre);
+  launched("k_rre_final");
+}
+}  // namespace
+
+int fd_sweep_mu(const fd_op* op, const fd_smoother* L, const double* g, const double* truth,
+                double mu_min, double mu_max, int grid_count, double* curve_mu,
+                double* curve_gcv, double* curve_rre, double* summary, void* stream) {
+  return guarded([&] {
+    check_op(op);
+    check_L(op, L);
+    if (!curve_mu || !curve_gcv || !curve_rre || !summary) validation("null output");
+    make_grid(mu_min, mu_max, grid_count);
+    const int K = grid_count;
+    const long long N = op->N();
+    Scratch S(as_stream(stream));
+    int* status = S.get<int>(1);
+    ck(cudaMemsetAsync(status, 0, sizeof(int), S.st), "memset");
+    const DevGrid dg(mu_min, mu_max, K, S);
+    const Analyzed an = analyze_for_gcv(op, L, g, 1, S);
+    double* dmu = S.get<double>(1);
+    int* dbk = S.get<int>(1);
+    double* dcurve = S.get<double>(K);
+    gcv_select_dev(op, L, an, 1, dg, mu_min, mu_max, dmu, dbk, dcurve, status, S);
+    check_status(status, S.st);
+    double mu_gcv = 0.0;
+    ck(cudaMemcpyAsync(&mu_gcv, dmu, sizeof(double), cudaMemcpyDeviceToHost, S.st), "mu");
+    ck(cudaMemcpyAsync(curve_gcv, dcurve, K * sizeof(double), cudaMemcpyDeviceToHost, S.st),
+       "curve");
+    std::copy(dg.h.mus.begin(), dg.h.mus.end(), curve_mu);
+    const double nan = std::nan("");
+    double min_rre = nan, mu_opt = nan, rre_gcv = nan;
+    if (truth) {
+      // restorations in batches of mu (2D passes need two scratch images each)
+      const long long per = N * 8 * (op->dim == 2 ? 3 : 1);
+      const int ch = (int)std::max(1LL, std::min<long long>(K, 16LL * 1024 * 1024 * 1024 / per));
+      double* f = S.get<double>((size_t)ch * N);
+      double* drre = S.get<double>(K + 1);
+      for (int c0 = 0; c0 < K; c0 += ch) {
+        const int nk = std::min(ch, K - c0);
+        run_synth(op, L, an.ghat, f, 0, 1, dg.d.mus + c0, nullptr, nk, S, an.pack, true);
+        rre_dev(f, truth, N, nk, drre + c0, S);
+      }
+      run_synth(op, L, an.ghat, f, 0, 1, dmu, nullptr, 1, S, an.pack);
+      rre_dev(f, truth, N, 1, drre + K, S);
+      std::vector<double> hr(K + 1);
+      ck(cudaMemcpyAsync(hr.data(), drre, (K + 1) * sizeof(double), cudaMemcpyDeviceToHost,
+                         S.st),
+         "rre");
+      ck(cudaStreamSynchronize(S.st), "sync");
+      if (std::isnan(hr[K])) validation("rre: zero ground truth");  // regularize.cpp:258
+      double best = INFINITY;
+      mu_opt = dg.h.mus[0];
+      for (int k = 0; k < K; ++k) {  // first strict minimum (pipeline.cpp:70-81)
+        curve_rre[k] = hr[k];
+        if (hr[k] < best) {
+          best = hr[k];
+          mu_opt = dg.h.mus[k];
+        }
+      }
+      min_rre = best;
+      rre_gcv = hr[K];
+    } else {
+      ck(cudaStreamSynchronize(S.st), "sync");
+      std::fill(curve_rre, curve_rre + K, nan);
+    }
+    summary[0] = min_rre;
+    summary[1] = mu_opt;
+    summary[2] = mu_gcv;
+    summary[3] = rre_gcv;
   });
 }
 

@@ -2294,6 +2294,38 @@ __global__ void k_gcv_direct_reduce(const double* __restrict__ partial, int item
 }
 
 // per-item residue: sqrt of the summed per-line Im^2 (operators.cpp:334-340)
+// rre (regularize.cpp:249-260) partial sums of `items` restorations against
+// one truth: partial[item][chunk] = (sum t^2, sum (t - f)^2) over the chunk
+__global__ void __launch_bounds__(256) k_rre_partials(const double* __restrict__ f,
+                                                      const double* __restrict__ t, long long N,
+                                                      long long chunk, double* partial) {
+  __shared__ double red[64];
+  const int b = blockIdx.x, ch = blockIdx.y;
+  const long long e0 = (long long)ch * chunk, e1 = min(N, e0 + chunk);
+  double acc[2] = {0.0, 0.0};
+  const double* fb = f + (long long)b * N;
+  for (long long i = e0 + threadIdx.x; i < e1; i += blockDim.x) {
+    const double tv = __ldg(&t[i]);
+    const double e = tv - __ldg(&fb[i]);
+    acc[0] = fma(tv, tv, acc[0]);
+    acc[1] = fma(e, e, acc[1]);
+  }
+  block_sum<2>(acc, red);
+  if (threadIdx.x == 0) {
+    double* o = partial + ((long long)b * gridDim.y + ch) * 2;
+    o[0] = acc[0];
+    o[1] = acc[1];
+  }
+}
+
+// rre[item] = sqrt(en / tn) from the reduced sums; NaN flags a zero truth
+__global__ void k_rre_final(const double* __restrict__ sums, int items, double* rre) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= items) return;
+  const double tn = sums[2 * b], en = sums[2 * b + 1];
+  rre[b] = tn == 0.0 ? NAN : sqrt(en / tn);
+}
+
 __global__ void k_resid_reduce(const double* __restrict__ r2, int items, int per_item,
                                double* out) {
   const int item = blockIdx.x * blockDim.x + threadIdx.x;

@@ -59,6 +59,7 @@ def lib():
         L.fd_op_create_2d_separable.argtypes = [dp, ip, dp, ip, ip, ip, ip, ip, C.POINTER(vp)]
         L.fd_op_destroy.argtypes = [vp]
         cd = C.c_double
+        L.fd_sweep_mu.argtypes = [vp, vp, vp, vp, cd, cd, ip, dp, dp, dp, dp, vp]
         L.fd_slab_analyze.argtypes = [vp, ip, vp, ip, vp, ll, vp]
         L.fd_slab_synthesize.argtypes = [vp, vp, ip, vp, vp, ip, ll, ll, cd, vp]
         L.fd_slab_gcv_partials.argtypes = [vp, vp, vp, ll, ll, cd, cd, ip, dp, dp, vp]
@@ -383,6 +384,48 @@ def deblur(op: BlurOperator, L: Smoother, g, mu: MuChoice, want_curve=False,
                           _ptr(restored), _ptr(mu_used), _ptr(bk) if mu.use_gcv else None,
                           _ptr(curve), _ptr(res), count, _stream()))
     return RestorationReport(restored, mu_used, bk if mu.use_gcv else None, curve, res)
+
+
+@dataclass
+class SweepPoint:
+    """pipeline.hpp:23-28."""
+    mu: float
+    gcv: float
+    rre: float
+
+
+@dataclass
+class BcSweep:
+    """pipeline.hpp:30-38."""
+    bc: str
+    min_rre: float
+    mu_opt: float
+    mu_gcv: float
+    rre_gcv: float
+    curve: list
+
+
+def sweep_mu(op: BlurOperator, L: Smoother, g, truth=None,
+             search: GcvSearch = GcvSearch()) -> BcSweep:
+    """sweep_mu / sweep_mu_2d (pipeline.cpp:55-115) for one signal or image:
+    G and (with truth) the RRE of the Tikhonov solution at every grid mu, the
+    RRE-optimal grid mu and the RRE at the GCV choice."""
+    g = _dev(g)
+    if tuple(g.shape) != op.shape:
+        raise ValidationError(f"sweep_mu takes one item of shape {op.shape}")
+    t = None if truth is None else _dev(truth)
+    if t is not None and tuple(t.shape) != op.shape:
+        raise ValidationError("truth shape differs from the signal")
+    K = int(search.count)
+    mus, G, rr, summ = (np.empty(K), np.empty(K), np.empty(K), np.empty(4))
+    dp = C.POINTER(C.c_double)
+    check(lib().fd_sweep_mu(op._h, L._h, _ptr(g), _ptr(t), C.c_double(search.mu_min),
+                            C.c_double(search.mu_max), K, mus.ctypes.data_as(dp),
+                            G.ctypes.data_as(dp), rr.ctypes.data_as(dp), summ.ctypes.data_as(dp),
+                            _stream()))
+    pts = [SweepPoint(float(m), float(v), float(r)) for m, v, r in zip(mus, G, rr)]
+    return BcSweep(BC_NAMES.get(op.bc, op.bc), float(summ[0]), float(summ[1]), float(summ[2]),
+                   float(summ[3]), pts)
 
 
 def deblur_host(op: BlurOperator, L: Smoother, g, mu: MuChoice, search: GcvSearch = GcvSearch(),

@@ -216,3 +216,48 @@ def test_tensor_core_gcv_screen(bc, psf, smoother, search, monkeypatch):
     want = O.deblur(oop, s, g[sel], True, mu_min=mu_min, mu_max=mu_max, count=K)
     assert np.array_equal(np_(rep.best_k)[sel], want.best_k)
     assert np.max(np.abs(np_(rep.mu_used)[sel] / want.mu_used - 1)) < 1e-10
+
+
+@pytest.mark.parametrize("bc,psf,smoother", [(O.HOC_COSINE, gauss(10, 3.0), 0),
+                                             (O.HOC_FOURIER, onesided(15, 0.2), 2),
+                                             (O.ANTIREFLECTIVE, gauss(4, 1.5), 1)])
+def test_sweep_mu_matches_oracle(bc, psf, smoother):
+    """sweep_mu (pipeline.cpp:55-115): G curve, RRE at every grid mu (one
+    analysis, batched filtered syntheses), mu_opt, mu_gcv, rre_gcv."""
+    n = 1024
+    op, L, oop, s = setup(bc, psf, n, smoother)
+    truth, _ = W.signals_1d(W.config(1), 11, 1, n=n + len(psf) - 1, m=0)
+    m = len(psf) // 2
+    g = W.add_noise(W.convolve_valid(truth, np.asarray(psf) / np.sum(psf)), 0.01, 5)[0]
+    t = truth[0, m:m + n]
+    sr = P.GcvSearch(1e-6, 1.0, 40)
+    sw = P.sweep_mu(op, L, torch.from_numpy(g), torch.from_numpy(t), search=sr)
+    mus, G, rr, summ = O.sweep_mu(oop, s, g, t, 1e-6, 1.0, 40)
+    assert np.array_equal([p.mu for p in sw.curve], mus)
+    assert np.max(np.abs(np.array([p.gcv for p in sw.curve]) / G - 1)) < 1e-11
+    assert np.max(np.abs(np.array([p.rre for p in sw.curve]) / rr - 1)) < 1e-10
+    assert sw.mu_opt == summ[1]
+    assert abs(sw.min_rre / summ[0] - 1) < 1e-10
+    assert abs(sw.mu_gcv / summ[2] - 1) < 1e-10
+    assert abs(sw.rre_gcv / summ[3] - 1) < 1e-10
+    nt = P.sweep_mu(op, L, torch.from_numpy(g), search=sr)
+    assert np.isnan(nt.min_rre) and np.isnan(nt.curve[0].rre) and nt.mu_gcv == sw.mu_gcv
+    with pytest.raises(P.ValidationError):
+        P.sweep_mu(op, L, torch.from_numpy(g), torch.zeros(n, dtype=torch.float64), search=sr)
+
+
+def test_sweep_mu_2d_consistent():
+    """sweep_mu_2d: the RRE of every grid mu equals that of tikhonov_solve_2d."""
+    n1, n2 = 96, 128
+    psf = gauss(4, 1.5)
+    op = P.build_operator_2d_separable(psf, psf, n1, n2, "hoc-cosine")
+    L = P.smoothing_eigenvalues("laplacian", op)
+    truth, g = W.image_2d(W.config(2), 1, n1, n2)
+    sr = P.GcvSearch(1e-6, 1.0, 12)
+    sw = P.sweep_mu(op, L, torch.from_numpy(g), torch.from_numpy(truth), search=sr)
+    sel = P.gcv_select(op, L, torch.from_numpy(g), search=sr)
+    for p in sw.curve:
+        f, _ = P.tikhonov_solve(op, L, torch.from_numpy(g), p.mu)
+        want = np.linalg.norm(truth - np_(f)) / np.linalg.norm(truth)
+        assert abs(p.rre / want - 1) < 1e-12
+    assert abs(sw.mu_gcv / float(np_(sel.mu)) - 1) < 1e-14

@@ -11,7 +11,8 @@ import pytest
 
 import fdoracle as O
 import reflib as R
-from util import rel
+from util import gauss, onesided, rel
+from paper_0906_2704_b200 import workloads as W
 
 PI = math.pi
 G1 = np.load(__import__("os").path.join(__import__("os").path.dirname(__file__), "golden",
@@ -233,3 +234,28 @@ def test_live_reference_gcv_minimize_paths():
         r = O.gcv_minimize(G, 1e-9, 1.0, 40)
         assert abs(r.mu / mu_ref - 1) < 1e-14
         assert np.allclose(r.vals, curve, rtol=0, atol=0)
+
+
+@pytest.mark.skipif(not R.available(), reason="oracle/_ref not built")
+@pytest.mark.parametrize("bc,smoother", [(O.HOC_COSINE, O.IDENTITY), (O.HOC_FOURIER, O.LAPLACIAN),
+                                         (O.REFLECTIVE, O.LAPLACIAN)])
+def test_sweep_mu_pins_reference(bc, smoother):
+    """sweep_mu (pipeline.cpp:55-115): curve, RRE per grid mu, summary."""
+    psf = gauss(10, 3.0) if bc != O.HOC_FOURIER else onesided(15, 0.2)
+    n = 512
+    truth, g = W.signals_1d(W.config(0), 3, 1, n=n, m=len(psf) // 2)
+    g = W.add_noise(W.convolve_valid(np.pad(truth[0], len(psf) // 2, mode="edge"),
+                                     np.asarray(psf) / np.sum(psf)), 0.01, 7)
+    op = O.build_operator(O.make_psf(psf, True), n, bc)
+    s = O.smoothing_eigenvalues(smoother, bc, n, op.eigenvalues)
+    mus, G, rr, summ = O.sweep_mu(op, s, g, truth[0], 1e-6, 1.0, 24)
+    rm, rG, rrr, rsumm = R.sweep_mu_1d(psf, n, bc, smoother, g, truth[0], 1e-6, 1.0, 24)
+    assert np.array_equal(mus, rm)
+    assert np.max(np.abs(G / rG - 1)) < 1e-12
+    assert np.max(np.abs(rr / rrr - 1)) < 1e-11
+    assert summ[1] == rsumm[1]  # mu_opt: identical grid point
+    assert abs(summ[0] / rsumm[0] - 1) < 1e-11
+    assert abs(summ[2] / rsumm[2] - 1) < 1e-10
+    assert abs(summ[3] / rsumm[3] - 1) < 1e-10
+    _, _, rr0, s0 = R.sweep_mu_1d(psf, n, bc, smoother, g, None, 1e-6, 1.0, 24)
+    assert np.all(np.isnan(rr0)) and np.isnan(s0[0]) and np.isnan(s0[3])
