@@ -462,6 +462,10 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
   d.correction = d.bordered && bc != BC_ANTIREFLECTIVE;
   const int m = d.m;
   const int L = d.kind == IK_SINE ? 2 * (m + 1) : m;
+  d.inv_sqrt_m = 1.0 / std::sqrt((double)m);
+  d.dct_s0 = std::sqrt(1.0 / (double)m);
+  d.dct_s1 = std::sqrt(2.0 / (double)m);
+  d.dst_scale = -0.5 * std::sqrt(2.0 / ((double)m + 1.0));
   double2* dct_tw = dev_alloc<double2>(A->bufs, d.kind == IK_COS ? m : 1);
   d.dct_tw = dct_tw;
   // full-length tables (complex lines / line pairs); only built when they fit on chip

@@ -63,6 +63,8 @@ struct AxisDev {
   //   or 1 (qmode 0), so a border combination a q[s+1] + b q[n-2-s] is one
   //   quadratic per line (border_poly).
   double qa1, qa2;
+  // per-axis constants of the trig transforms (trig.cpp:170-234), host-computed
+  double inv_sqrt_m, dct_s0, dct_s1, dst_scale;
   double cavr[4], capr[4];
 };
 

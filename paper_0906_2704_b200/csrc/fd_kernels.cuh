@@ -1042,8 +1042,11 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   FD_CLK(cw);
   FD_CLK_ADD(0, 3, c0, cw);
   const double* sin_ = stg.buf;
-  auto ld = [&](int e) { return st ? sin_[e] : __ldg(in + oi + e * es); };
-  const Fold fd = fold_terms(ax, ld);
+  const double* gin = in + oi;
+  Fold fd;
+  // the load phase, instantiated for the staged (shared) and the global source
+  auto load_phase = [&](auto ld) {
+  fd = fold_terms(ax, ld);
   const BorderPoly fp = border_poly(ax, -fd.o0, -fd.on);
   // folded interior sample s
   auto xin = [&](int s) {
@@ -1071,6 +1074,13 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
     }
     x[pidx(j)] = cmul(make_double2(a, b), chirp_at(j));
   }
+  };
+  if (st)
+    load_phase([&](int e) { return sin_[e]; });
+  else if (es == 1)
+    load_phase([&](int e) { return __ldg(gin + e); });
+  else
+    load_phase([&](int e) { return __ldg(gin + (long long)e * es); });
   __syncthreads();
 
   FD_CLK(c1);
@@ -1104,8 +1114,8 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   const long long oo = line_offset(io.go, l), eso = io.go.elem_stride;
   double2* P = reinterpret_cast<double2*>(reinterpret_cast<double*>(io.out) + oo);
   const int off = ax.bordered ? 1 : 0;
-  const double inv_sqrt_m = 1.0 / sqrt((double)m);
-  const double s0 = sqrt(1.0 / (double)m), s1 = sqrt(2.0 / (double)m);
+  const double inv_sqrt_m = ax.inv_sqrt_m;
+  const double s0 = ax.dct_s0, s1 = ax.dct_s1;
   double* wl = io.wout ? io.wout + (long long)l * io.wstride : nullptr;
   const long long nkb32 = io.wstride >> 5;
   auto wset = [&](long long i, double v) {  // GCV weight (and its TF32 split for the screen)
@@ -1180,7 +1190,7 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
       const double2 WO = cmul(rtw(k), make_double2(0.5 * D.y, -0.5 * D.x));
       const double2 X0 = cadd(E, WO), X1 = csub(E, WO);  // X_k, X_{k+h}
       if (ax.kind == IK_SINE) {
-        if (k >= 1) emit(k - 1, make_double2(-0.5 * sqrt(2.0 / ((double)m + 1.0)) * X0.y, 0.0));
+        if (k >= 1) emit(k - 1, make_double2(ax.dst_scale * X0.y, 0.0));
       } else {
         const double2 t0 = dtw(k), t1 = dtw(k + h);
         emit(k, make_double2((k == 0 ? s0 : s1) * (t0.x * X0.x - t0.y * X0.y), 0.0));
@@ -1291,7 +1301,7 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
     }
   } else {
     // cosine works on conj(buf_i) = s_i c_i conj(tw_i) (DCT-III, trig.cpp:201-212)
-    const double s0 = sqrt(1.0 / (double)m), s1 = sqrt(2.0 / (double)m);
+    const double s0 = ax.dct_s0, s1 = ax.dct_s1;
     auto val_at = [&](int i) {
       const double2 c = cf(interior_elem(ax, i));
       if (ax.kind == IK_COS) {
@@ -1374,13 +1384,21 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
     double o = val;
     if (ax.bordered) o = val + bp(p);
     out[oo + e * eso] = o;
-    if (ax.correction) {  // out_0 = q_0 u_0 + c_a . c,  out_{n-1} = c_b . c + q_0 u_{n-1}
-      if (p == ax.top_i) out[oo] = ax.q0 * u0 + val;
-      if (p == ax.bot_i) out[oo + (long long)(n - 1) * eso] = val + ax.q0 * un;
+  };
+  // interior synthesis sample p (before the border terms), read back from x
+  auto interior_at = [&](int p) {
+    if (ax.kind == IK_COS) {  // inverse of the Makhoul placement below
+      const int half = (m + 1) / 2;
+      const int sp = (p % 2 == 0) ? p / 2 : m - 1 - (p - 1) / 2;
+      (void)half;
+      const double2 z = cconj(zv(sp >> 1));
+      return (sp & 1) ? z.y : z.x;
     }
+    const double2 z = cconj(zv(p >> 1));
+    return ((p & 1) ? z.y : z.x) * ax.inv_sqrt_m;
   };
   if (ax.kind == IK_SINE) {
-    const double sc = -0.5 * sqrt(2.0 / ((double)m + 1.0));
+    const double sc = ax.dst_scale;
     for (int k = 1 + threadIdx.x; k < h; k += blockDim.x) {
       const int kc = h - k;
       const double2 Zk = zv(k);
@@ -1391,7 +1409,7 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
       put(k - 1, sc * (E.y + WO.y));
     }
   } else {
-    const double inv_sqrt_m = 1.0 / sqrt((double)m);
+    const double inv_sqrt_m = ax.inv_sqrt_m;
     const int half = (m + 1) / 2;
     for (int j = threadIdx.x; j < h; j += blockDim.x) {
       const double2 z = cconj(zv(j));
@@ -1405,9 +1423,13 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
       }
     }
   }
-  if (ax.bordered && !ax.correction && threadIdx.x == 0) {
-    out[oo] = ax.q0 * u0;
-    out[oo + (long long)(n - 1) * eso] = ax.q0 * un;
+  if (ax.bordered && threadIdx.x == 0) {
+    // out_0 = q_0 u_0 + c_a . c,  out_{n-1} = c_b . c + q_0 u_{n-1}; the dots are
+    // the interior synthesis at top_i / bot_i (zero without correction)
+    const double top = ax.correction ? interior_at(ax.top_i) : 0.0;
+    const double bot = ax.correction ? interior_at(ax.bot_i) : 0.0;
+    out[oo] = ax.q0 * u0 + top;
+    out[oo + (long long)(n - 1) * eso] = bot + ax.q0 * un;
   }
   __syncthreads();  // x and the scratch are reused by the next line
 #ifdef FD_PHASE_CLOCKS
