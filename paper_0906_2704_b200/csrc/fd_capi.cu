@@ -1302,6 +1302,125 @@ void gcv_screen_exact(const GcvData& g, const GcvGrid& grid, const Analyzed& an,
   }
 }
 
+// Single large item: bin the elements by r (k_gcv_hist), bound G on every grid
+// point (k_gcv_bounds), evaluate exactly only the points whose lower bound is
+// below the smallest upper bound, and return G on the device with +inf
+// elsewhere -- the pick / tie / bracket logic then sees the full-grid answer.
+// Returns null (caller evaluates the whole grid) when the r range needs too
+// many bins or too many points survive.
+double* interval_screen(const GcvData& g, const GcvGrid& grid, const GridHost& gh, int* status,
+                        Scratch& S) {
+  const int K = grid.count;
+  if (g.pair) return nullptr;  // paired (1D complex-basis) items keep the full grid
+  const int rctas = 2 * num_sms();
+  double* mm = S.get<double>(2 * (size_t)rctas);
+  {
+    ProfScope ps("k_gcv_tables", S.st);
+    k_gcv_rrange<<<rctas, 256, 0, S.st>>>(g, mm);
+    launched("k_gcv_rrange");
+  }
+  std::vector<double> hmmv(2 * (size_t)rctas);
+  ck(cudaMemcpyAsync(hmmv.data(), mm, hmmv.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                     S.st),
+     "rrange");
+  ck(cudaStreamSynchronize(S.st), "sync");
+  double hmm[2] = {INFINITY, 0.0};
+  for (int i = 0; i < rctas; ++i) {
+    hmm[0] = std::min(hmm[0], hmmv[2 * i]);
+    hmm[1] = std::max(hmm[1], hmmv[2 * i + 1]);
+  }
+  auto key = [](double r) {
+    long long b;
+    std::memcpy(&b, &r, sizeof(b));
+    return b >> kHistShift;
+  };
+  const bool any_pos = std::isfinite(hmm[0]) && hmm[1] > 0.0;
+  const long long base = any_pos ? key(hmm[0]) : 0;
+  const long long top = any_pos ? key(hmm[1]) : 0;
+  const long long nb = any_pos ? top - base + 1 : 0;
+  const size_t hbytes = (size_t)2 * (nb + 1) * sizeof(double);
+  if (hbytes > 200 * 1024) return nullptr;  // r spans too many octaves for one SMEM histogram
+  static bool attr = false;
+  if (!attr) {
+    ck(cudaFuncSetAttribute(k_gcv_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+       "hist attr");
+    attr = true;
+  }
+  const int ctas = num_sms();
+  const int nw = (int)(2 * (nb + 1));
+  double* part = S.get<double>((size_t)ctas * nw);
+  double* hist = S.get<double>(nw);
+  double* bounds = S.get<double>(2 * (size_t)K);
+  {
+    ProfScope ps("k_gcv_screen", S.st);
+    k_gcv_hist<<<ctas, 512, hbytes, S.st>>>(g, base, (int)nb, part);
+    launched("k_gcv_hist");
+    k_reduce_partials<<<dim3(1, (nw + 31) / 32), 256, 0, S.st>>>(part, ctas, nw, hist);
+    launched("k_reduce_partials");
+    k_gcv_bounds<<<K, 256, 0, S.st>>>(hist, base, (int)nb, grid, bounds);
+    launched("k_gcv_bounds");
+  }
+  std::vector<double> hb(2 * (size_t)K);
+  ck(cudaMemcpyAsync(hb.data(), bounds, hb.size() * sizeof(double), cudaMemcpyDeviceToHost, S.st),
+     "bounds");
+  ck(cudaStreamSynchronize(S.st), "sync");
+  double min_hi = INFINITY;
+  for (int k = 0; k < K; ++k) min_hi = std::min(min_hi, hb[2 * k + 1]);
+  if (!std::isfinite(min_hi)) return nullptr;  // degenerate or overflow: exact grid decides
+  std::vector<int> cand;
+  for (int k = 0; k < K; ++k)
+    if (!(hb[2 * k] > min_hi)) cand.push_back(k);  // NaN bounds stay candidates
+  if (cand.empty() || (int)cand.size() > 64) return nullptr;
+  // exact fp64 G at the candidates, 8 per pass (k_gcv_cand)
+  const int C = (int)cand.size();
+  std::vector<double> cm(C);
+  for (int i = 0; i < C; ++i) cm[i] = gh.mus[cand[i]];
+  double* dcm = S.get<double>((size_t)C);
+  ck(cudaMemcpyAsync(dcm, cm.data(), C * sizeof(double), cudaMemcpyHostToDevice, S.st), "cands");
+  const int nch = pick_chunks(g.N, 1, 1);
+  const long long chunk = (g.N + nch - 1) / nch;
+  const int npass = (C + 7) / 8;
+  double* cpart = S.get<double>((size_t)nch * 16);
+  double* sums = S.get<double>((size_t)npass * 16);
+  {
+    ProfScope ps("k_gcv_exact", S.st);
+    for (int p = 0; p < npass; ++p) {
+      const int nc = std::min(8, C - 8 * p);
+      if (nc <= 4)
+        k_gcv_cand<4><<<(nch * 32 + 255) / 256, 256, 0, S.st>>>(g, dcm + 8 * p, nc, chunk, nch,
+                                                                cpart);
+      else
+        k_gcv_cand<8><<<(nch * 32 + 255) / 256, 256, 0, S.st>>>(g, dcm + 8 * p, nc, chunk, nch,
+                                                                cpart);
+      launched("k_gcv_cand");
+      const int w = nc <= 4 ? 8 : 16;
+      k_reduce_partials<<<dim3(1, 1), 256, 0, S.st>>>(cpart, nch, w, sums + 16 * p);
+      launched("k_reduce_partials");
+    }
+  }
+  std::vector<double> hs((size_t)npass * 16), Gh((size_t)K, INFINITY);
+  ck(cudaMemcpyAsync(hs.data(), sums, hs.size() * sizeof(double), cudaMemcpyDeviceToHost, S.st),
+     "sums");
+  ck(cudaStreamSynchronize(S.st), "sync");
+  for (int i = 0; i < C; ++i) {
+    const int p = i / 8, j = i % 8;
+    const int w = std::min(8, C - 8 * p) <= 4 ? 4 : 8;
+    const double num = hs[16 * p + j];
+    const double den = hs[16 * p + w + j];
+    if (den == 0.0) {
+      const int three = 3;
+      ck(cudaMemcpyAsync(status, &three, sizeof(int), cudaMemcpyHostToDevice, S.st), "status");
+      Gh[cand[i]] = NAN;
+    } else {
+      Gh[cand[i]] = num / (den * den);
+    }
+  }
+  double* G = S.get<double>(K);
+  ck(cudaMemcpyAsync(G, Gh.data(), K * sizeof(double), cudaMemcpyHostToDevice, S.st), "G");
+  ck(cudaStreamSynchronize(S.st), "sync");  // Gh is a stack vector
+  return G;
+}
+
 void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, long long count,
                     const DevGrid& dg, double mu_min, double mu_max, double* mu_out,
                     int* best_k_out, double* curve_out, int* status, Scratch& S) {
@@ -1348,6 +1467,9 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
     nch = (int)((g.N + echunk - 1) / echunk);
     part = S.get<double>((size_t)items * nch * 2 * K);
     launch_gemm(g, grid, echunk, nch, part, S.st);
+  } else if (items == 1 && !curve_out && g.N >= (1LL << 20) && screen_enabled() &&
+             (G = interval_screen(g, grid, dg.h, status, S)) != nullptr) {
+    // single large item: interval screen + exact candidates wrote G
   } else {
     nch = pick_chunks(g.N, items, 1);
     const long long chunk = (g.N + nch - 1) / nch;

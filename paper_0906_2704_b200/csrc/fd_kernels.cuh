@@ -1758,6 +1758,105 @@ __global__ void __launch_bounds__(256) k_gcv_den(GcvData g, GcvGrid grid, double
   if (threadIdx.x == 0) den[kk] = acc[0];
 }
 
+// ---- interval screen of the grid for single large items ----
+// The elements are binned by r = |d|^2/s^2 on 64 bins per octave (the bin of r
+// is its exponent and top 6 mantissa bits, so bin b holds r in
+// [r_lo(b), r_hi(b)) with r_hi/r_lo <= 1 + 2^-6; r = 0 has its own exact bin).
+// From the per-bin sums of the weights and multiplicities every grid point gets
+// an interval [G_lo, G_hi] that contains G (sigma is monotone in r); only grid
+// points with G_lo <= min_j G_hi can hold the first minimum or a 1e-12 tie, and
+// only those are evaluated exactly (fd_capi.cu gcv_select_dev).
+constexpr int kHistShift = 46;  // 52 - 6 mantissa bits kept
+
+__device__ __forceinline__ long long hist_key(double r) {
+  return (long long)(__double_as_longlong(r) >> kHistShift);
+}
+
+// min over positive finite r and max over finite r: per-CTA partials
+// mm[2 cta], mm[2 cta + 1] (min / max are order-independent)
+__global__ void __launch_bounds__(256) k_gcv_rrange(GcvData g, double* mm) {
+  __shared__ double red[64];
+  double lo = INFINITY, hi = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < g.N;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double r = gcv_ratio(g, e);
+    if (isinf(r)) continue;
+    if (r > 0.0) lo = fmin(lo, r);
+    hi = fmax(hi, r);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = lo;
+    red[32 + (threadIdx.x >> 5)] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+      lo = fmin(lo, red[w]);
+      hi = fmax(hi, red[32 + w]);
+    }
+    lo = fmin(lo, red[0]);
+    hi = fmax(hi, red[32]);
+    mm[2 * blockIdx.x] = lo;
+    mm[2 * blockIdx.x + 1] = hi;
+  }
+}
+
+
+// per-CTA histogram of (sum W, sum mult) over bins [0, nb) (keys base + b) and
+// the zero bin nb; partial[cta][2 (nb + 1)]
+__global__ void __launch_bounds__(512) k_gcv_hist(GcvData g, long long base, int nb,
+                                                  double* partial) {
+  extern __shared__ double hist[];
+  const int nw = 2 * (nb + 1);
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) hist[i] = 0.0;
+  __syncthreads();
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < g.N;
+       e += (long long)gridDim.x * blockDim.x) {
+    const double r = gcv_ratio(g, e);
+    if (isinf(r)) continue;
+    const int b = r > 0.0 ? (int)(hist_key(r) - base) : nb;
+    atomicAdd(&hist[2 * b], gcv_w(g, 0, e));
+    atomicAdd(&hist[2 * b + 1], gcv_mult(g, e));
+  }
+  __syncthreads();
+  double* out = partial + (long long)blockIdx.x * nw;
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) out[i] = hist[i];
+}
+
+// bounds[k] = (G_lo, G_hi) from the reduced histogram; one CTA per grid point
+__global__ void __launch_bounds__(256) k_gcv_bounds(const double* __restrict__ hist,
+                                                    long long base, int nb, GcvGrid grid,
+                                                    double* bounds) {
+  __shared__ double red[32 * 4];
+  const int k = blockIdx.x;
+  const double mu = grid.mus[k];
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // num_hi, num_lo, den_hi, den_lo
+  for (int b = threadIdx.x; b <= nb; b += blockDim.x) {
+    const double W = hist[2 * b], cnt = hist[2 * b + 1];
+    if (cnt == 0.0 && W == 0.0) continue;
+    double rlo = 0.0, rhi = 0.0;
+    if (b < nb) {
+      rlo = __longlong_as_double((base + b) << kHistShift);
+      rhi = __longlong_as_double((base + b + 1) << kHistShift);
+    }
+    const double shi = 1.0 / (rlo + mu), slo = 1.0 / (rhi + mu);
+    acc[0] = fma(W, shi * shi, acc[0]);
+    acc[1] = fma(W, slo * slo, acc[1]);
+    acc[2] = fma(cnt, shi, acc[2]);
+    acc[3] = fma(cnt, slo, acc[3]);
+  }
+  block_sum<4>(acc, red);
+  if (threadIdx.x == 0) {
+    // widened by 1e-12 for the rounding of these sums and of the exact pass
+    bounds[2 * k] = acc[1] / (acc[2] * acc[2]) * (1.0 - 1e-12);
+    bounds[2 * k + 1] = acc[0] / (acc[3] * acc[3]) * (1.0 + 1e-12);
+  }
+}
+
 // ---- tensor-core screening of the grid (fd_tc.cuh) and exact candidates ----
 // rmin = min over elements of the finite ratios r_e (one CTA)
 __global__ void __launch_bounds__(256) k_gcv_rmin(GcvData g, double* rmin) {
@@ -1880,6 +1979,67 @@ __device__ __forceinline__ double exact_num(const GcvData& g, int item, const do
   for (int i = 1; i < CH; ++i)
     if (lane == i) v = acc[i];
   return v;
+}
+
+// exact num / den of one item at CH explicit grid values (lanes over the
+// elements of a chunk, the CH reciprocals of an element by batch inversion):
+// partial[chunk][2 CH] = (num_0..num_{CH-1}, den_0..den_{CH-1}); padding mu = 1
+template <int CH>
+__global__ void __launch_bounds__(256) k_gcv_cand(GcvData g, const double* __restrict__ mus,
+                                                  int nc, long long chunk, int nch,
+                                                  double* partial) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= nch) return;
+  double mu[CH], num[CH], den[CH];
+#pragma unroll
+  for (int i = 0; i < CH; ++i) {
+    mu[i] = i < nc ? mus[i] : 1.0;
+    num[i] = den[i] = 0.0;
+  }
+  const long long e0 = (long long)warp * chunk, e1 = min(g.N, e0 + chunk);
+  gcv_stream<4>(g, 0, e0, e1, lane, [&](double r, double w) {
+    if (isinf(r)) return;
+    double a[CH], pre[CH];
+#pragma unroll
+    for (int i = 0; i < CH; ++i) a[i] = r + mu[i];
+    pre[0] = a[0];
+#pragma unroll
+    for (int i = 1; i < CH; ++i) pre[i] = pre[i - 1] * a[i];
+    double s[CH];
+    if (pre[CH - 1] < 1e300 && pre[CH - 1] > 1e-300) {
+      double inv = rcp_pos(pre[CH - 1]);
+#pragma unroll
+      for (int i = CH - 1; i >= 1; --i) {
+        s[i] = inv * pre[i - 1];
+        inv *= a[i];
+      }
+      s[0] = inv;
+    } else {
+#pragma unroll
+      for (int i = 0; i < CH; ++i) s[i] = 1.0 / a[i];
+    }
+    const double mult = 1.0;  // 2D / unpaired elements (interval_screen's items)
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      num[i] = fma(w, s[i] * s[i], num[i]);
+      den[i] = fma(mult, s[i], den[i]);
+    }
+  });
+#pragma unroll
+  for (int i = 0; i < CH; ++i)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      num[i] += __shfl_xor_sync(0xffffffffu, num[i], o);
+      den[i] += __shfl_xor_sync(0xffffffffu, den[i], o);
+    }
+  if (lane == 0) {
+    double* out = partial + (long long)warp * 2 * CH;
+#pragma unroll
+    for (int i = 0; i < CH; ++i) {
+      out[i] = num[i];
+      out[CH + i] = den[i];
+    }
+  }
 }
 
 // Exact G(mu_k) = num_k / den_k^2 at the screened candidates of each item

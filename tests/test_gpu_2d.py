@@ -100,3 +100,25 @@ def test_config2_scaled_image():
     w = O.deblur_2d(oop, s, g, True, mu_min=cfg.mu_min, mu_max=cfg.mu_max, count=cfg.count)
     assert int(np_(rep.best_k)) == int(w.best_k)
     assert rel(np_(rep.restored), w.restored) < 1e-10
+
+
+@pytest.mark.parametrize("bc,smoother,search", [("hoc-cosine", "laplacian", (1e-8, 1.0, 512)),
+                                                ("hoc-fourier", "identity", (1e-6, 1.0, 128)),
+                                                ("reflective", "laplacian", (1e-6, 1.0, 7))])
+def test_interval_screen_single_image(bc, smoother, search, monkeypatch):
+    """Single large images (>= 2^20 coefficients) bound G on every grid point
+    from an r-histogram and evaluate exactly only the possible minima: the
+    same best_k, mu and restoration as the full fp64 grid."""
+    import paper_0906_2704_b200 as PP
+    n1, n2 = 1024, 1040
+    psf = W.gaussian_weights(6, 2.0) if bc != "hoc-fourier" else W.onesided_exp_weights(7, 0.25)
+    op = PP.build_operator_2d_separable(psf, psf, n1, n2, bc)
+    L = PP.smoothing_eigenvalues(smoother, op)
+    _, g = W.image_2d(W.config(2), 3, n1, n2)
+    sr = PP.GcvSearch(*search)
+    rep = PP.deblur(op, L, torch.from_numpy(g), PP.MuChoice(True), search=sr)
+    monkeypatch.setenv("FASTDEBLUR_GCV_SCREEN", "0")
+    ref = PP.deblur(op, L, torch.from_numpy(g), PP.MuChoice(True), search=sr)
+    assert int(rep.best_k.cpu()) == int(ref.best_k.cpu())
+    assert abs(float(rep.mu_used.cpu()) / float(ref.mu_used.cpu()) - 1) < 1e-12
+    assert rel(rep.restored.cpu().numpy(), ref.restored.cpu().numpy()) < 1e-12
