@@ -149,59 +149,92 @@ def run_reference_arm(args, cfg, cores):
 
 
 # ----------------------------------------------------------------------------
-# clocks sampler (nvidia-smi during the timed region)
+# clocks sampler (NVML during the timed region; nvidia-smi if NVML is absent)
 # ----------------------------------------------------------------------------
 class Clocks:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap,power.draw")
+    """Samples the SM clock and the clock-event (throttle) reasons every ~2 ms
+    from a background thread.  start() returns only after the first sample, so
+    even a 100 ms timed region is covered; stop() summarises the samples taken
+    between start() and stop()."""
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
 
-    def __init__(self, index):
+    def __init__(self, index, period_s=0.002):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.period = period_s
+        self.sm, self.reasons, self.max_mhz = [], set(), None
+        self.stop_ev = threading.Event()
+        self.first = threading.Event()
+        self.nv = None
+        self.source = "nvml"
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = None
+            try:
+                import torch
+                p = torch.cuda.get_device_properties(index)
+                bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+                h = nv.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:  # noqa: BLE001
+                h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.nv, self.h = nv, h
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self.nv = None
+            self.source = "nvidia-smi"
+
+    def _sample_nvml(self):
+        nv, h = self.nv, self.h
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons",
+                              getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons", None))
+        while not self.stop_ev.is_set():
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+                bits = get_reasons(h) if get_reasons else 0
+                for name, attr in self.REASONS:
+                    if bits & getattr(nv, attr, 0):
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            self.first.set()
+            time.sleep(self.period)
+
+    def _sample_smi(self):
+        fields = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                  "clocks_event_reasons.hw_thermal_slowdown,"
+                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        while not self.stop_ev.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index),
+                                      f"--query-gpu={fields}", "--format=csv,noheader,nounits"],
+                                     capture_output=True, text=True, timeout=5).stdout
+                parts = [p.strip() for p in out.strip().split(",")]
+                self.sm.append(float(parts[0]))
+                self.max_mhz = float(parts[1])
+                for nm, v in zip(names, parts[2:6]):
+                    if v.lower().startswith("active"):
+                        self.reasons.add(nm)
+            except Exception:  # noqa: BLE001
+                pass
+            self.first.set()
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.th = threading.Thread(target=self._read, daemon=True)
-            self.th.start()
-        except OSError:
-            self.proc = None
-
-    def _read(self):
-        for ln in self.proc.stdout:
-            self.lines.append(ln.strip())
+        self.th = threading.Thread(target=self._sample_nvml if self.nv else self._sample_smi,
+                                   daemon=True)
+        self.th.start()
+        self.first.wait(timeout=10)
 
     def stop(self):
-        if not self.proc:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        self.th.join(timeout=2)
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[2:6]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        self.stop_ev.set()
+        self.th.join(timeout=10)
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": self.source}
 
 
 # ----------------------------------------------------------------------------
@@ -220,6 +253,35 @@ def alg_bytes_per_px(name, cfg):
     # 2D: column pass then row pass (each launch covers the whole batch once)
     return {"k_analyze": 0.5 * (8 + c) + 0.5 * (c + c), "k_synth_filter": c + c,
             "k_synth": c + 8, "k_gcv_grid": c, "k_gcv_moments": c}.get(name)
+
+
+NCU_NAMES = {"k_analyze": ("k_ranalyze", "k_analyze"), "k_synth_filter": ("k_rsynth", "k_synth"),
+             "k_synth": ("k_rsynth", "k_synth")}
+
+
+def ncu_traffic(name, cfg):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant
+    kernel from the newest committed `ncu --set full` summary of this config
+    (profiles/*/ncu_full_c<cfg>.txt); (bytes, source) or (None, None)."""
+    import glob
+    import re
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", f"ncu_full_c{cfg.index}.txt")))
+    if not files:
+        return None, None
+    txt = open(files[-1]).read()
+    for blk in txt.split("== ")[1:]:
+        head = blk.split("\n", 1)[0]
+        if not any(re.search(rf"\b{k}\b", head) for k in NCU_NAMES.get(name, (name,))):
+            continue
+        r = re.search(r"dram_read\s+([\d.]+)\s+(\w+)", blk)
+        w = re.search(r"dram_write\s+([\d.]+)\s+(\w+)", blk)
+        if not (r and w):
+            continue
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = float(r.group(1)) * scale.get(r.group(2), 1) + float(w.group(1)) * scale.get(
+            w.group(2), 1)
+        return tot, os.path.relpath(files[-1], ROOT)
+    return None, None
 
 
 def bluestein_flops_per_line(n, bc):
@@ -378,8 +440,10 @@ def main():
         if bpp is not None:
             bytes_launch = bpp * px_rank / launches_per_step
             achieved = bytes_launch / (avg_ms / 1e3) / 1e9
+            traffic, tsrc = ncu_traffic(dom, cfg)
             roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak,
-                    "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                    "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                    "traffic_source": tsrc,
                     "peak_source": peak_src,
                     "share_of_step": (ms_tot / args.steps) / ms_step,
                     "alg_bytes_per_launch": bytes_launch}

@@ -18,6 +18,15 @@ batch), 2D routines on the last two axes (row-major n1 x n2, multidim.hpp:66).
 
 Extensions beyond the reference (flagged where defined):
   * ``first_difference`` smoother, s = sqrt(2 - 2 cos(node)).
+  * higher-order borders ``hoc-fourier-d1`` / ``hoc-fourier-d3`` (degree d = 1
+    and 3 for nonsymmetric PSFs, BASELINE configs 1 and 3): the paper's
+    construction (polynomial columns with eigenvalue
+    1 around an interior trigonometric basis, inverse by Sherman-Morrison-
+    Woodbury, Theorem sec:sherm) generalised to k = d border columns; see
+    ``HoTransform``.  Not in the reference, so pinned by a dense construction
+    (T built entry-wise and solved by LU, as oracle.cpp:102-223 does for the
+    reference's own transforms), polynomial preservation, and equality with the
+    reference's hoc-fourier operator at d = 2 (tests/test_ho_borders.py).
 """
 from __future__ import annotations
 
@@ -30,7 +39,13 @@ PI = math.pi
 
 # BoundaryCondition (operators.hpp:15-21) codes, shared with the C-ABI.
 PERIODIC, REFLECTIVE, ANTIREFLECTIVE, HOC_COSINE, HOC_FOURIER = range(5)
-BC_NAMES = ("periodic", "reflective", "antireflective", "hoc-cosine", "hoc-fourier")
+# extension codes (not in the reference): higher-order Fourier borders
+HOC_FOURIER_D1, HOC_FOURIER_D3 = 5, 6
+BC_NAMES = ("periodic", "reflective", "antireflective", "hoc-cosine", "hoc-fourier",
+            "hoc-fourier-d1", "hoc-fourier-d3")
+# (k_left, k_right, degree) of the generalised borders; the d = 2 member
+# ("ho-2", borders (1, 1)) is the same operator as the reference's hoc-fourier
+HO_BORDERS = {HOC_FOURIER_D1: (1, 0, 1), HOC_FOURIER_D3: (2, 1, 3)}
 # BoundaryBasis (boundary.hpp:18)
 B_AR, B_HC, B_HF = range(3)
 # SmootherKind (regularize.hpp:15) + extension
@@ -49,12 +64,16 @@ def needs_symmetric_psf(bc):  # operators.cpp:205-209
     return bc in (REFLECTIVE, ANTIREFLECTIVE, HOC_COSINE)
 
 
-def is_complex_basis(bc):  # operators.cpp:211-213
-    return bc in (PERIODIC, HOC_FOURIER)
+def is_complex_basis(bc):  # operators.cpp:211-213 (+ extension codes)
+    return bc in (PERIODIC, HOC_FOURIER, HOC_FOURIER_D1, HOC_FOURIER_D3)
 
 
 def is_boundary_corrected(bc):  # operators.cpp:215-219
     return bc in (ANTIREFLECTIVE, HOC_COSINE, HOC_FOURIER)
+
+
+def is_higher_order(bc):  # extension
+    return bc in HO_BORDERS
 
 
 # --------------------------------------------------------------------------
@@ -330,12 +349,129 @@ def transform_apply_inverse(t: StructuredTransform, y):
 
 
 # --------------------------------------------------------------------------
+# Extension: higher-order polynomial borders around a Fourier interior
+# --------------------------------------------------------------------------
+def legendre_columns(n, degree):
+    """Border columns: Legendre polynomials P_1..P_d of t_i = (2i-(n-1))/(n-1),
+    each scaled to unit 2-norm on the n grid points.
+
+    The operator A = T diag(d) T^-1 only depends on span(P u {1}) = P_d (the
+    eigenvalue-1 eigenspace) and on the interior columns, not on the basis
+    chosen for the border columns; this basis is near-orthogonal, which gives
+    the smallest cond(T) of the bases tried (the raw monomials
+    (b-x)^p of the d = 2 construction give cond(T) 20x larger at d = 3)."""
+    t = (2.0 * np.arange(n) - (n - 1)) / (n - 1)
+    p_prev, p = np.ones(n), t.copy()
+    cols = []
+    for k in range(1, degree + 1):
+        if k > 1:  # Bonnet: k P_k = (2k-1) t P_{k-1} - (k-1) P_{k-2}
+            p_prev, p = p, ((2 * k - 1) * t * p - (k - 1) * p_prev) / k
+        cols.append(p / math.sqrt(float(np.sum(p * p))))
+    return np.stack(cols, axis=1)
+
+
+@dataclass
+class HoTransform:
+    """T = [P_L | Phi | P_R] of order n: k_l + k_r = d polynomial columns (unit
+    norm, eigenvalue 1) around the m = n - d interior Fourier columns
+    phi_j(x) = e^{ijx}/sqrt(m) sampled on the grid x_i = (i - k_l) 2 pi / m,
+    i = 0..n-1 (the paper's T_F of PAPER.md:418-431 at d = 2, with k_l = k_r = 1).
+
+    The interior rows of Phi are F^H; every border row is the row of F^H at the
+    2 pi-periodic image of its grid point (wrap), so with E the selection of
+    those rows, Phi_B F = E exactly.  With S = P_B - E P_I (k x k):
+      analyze   a = S^-1 (y_B - E y_I),  b = F (y_I - P_I a)
+      synthesize  y_I = F^H b + P_I a,  y_B = E F^H b + P_B a
+    (Schur complement of the unitary block; the rank-k form of the paper's
+    Theorem th:inv).  Coefficients are ordered [a_left, b, a_right]."""
+    bc: int
+    n: int
+    kl: int
+    kr: int
+    m: int
+    degree: int
+    P: np.ndarray       # (n, k) border columns
+    border: np.ndarray  # (k,) grid rows of the border, top then bottom
+    wrap: np.ndarray    # (k,) interior index (0..m-1) of each border row's image
+    S: np.ndarray
+    Sinv: np.ndarray
+
+    @property
+    def k(self):
+        return self.kl + self.kr
+
+
+def build_ho_transform(bc, n, borders=None) -> HoTransform:
+    """``borders`` = (k_l, k_r, degree) overrides the code's (tests build the
+    d = 2 member (1, 1, 2) to pin the family against the reference)."""
+    kl, kr, deg = borders if borders is not None else HO_BORDERS[bc]
+    k = kl + kr
+    m = n - k
+    if m < 3:
+        raise ValidationError("higher-order borders need n >= degree + 3")
+    P = legendre_columns(n, deg)
+    border = np.array(list(range(kl)) + [kl + m + j for j in range(kr)])
+    wrap = np.array([m - kl + i for i in range(kl)] + list(range(kr)))
+    S = P[border, :] - P[kl + wrap, :]
+    sv = np.linalg.svd(S, compute_uv=False)
+    if sv[-1] <= 0.0 or sv[0] / sv[-1] > 1e12:  # as boundary.cpp:139-150 for k = 2
+        raise DegenerateError("degenerate transform: border capacitance is singular or "
+                              "ill-conditioned")
+    return HoTransform(bc, n, kl, kr, m, deg, P, border, wrap, S, np.linalg.inv(S))
+
+
+def ho_analyze(t: HoTransform, y):
+    """T^-1 y, batched over leading axes."""
+    y = np.asarray(y)
+    kl, m = t.kl, t.m
+    yI = y[..., kl:kl + m]
+    r = y[..., t.border] - yI[..., t.wrap]
+    a = r @ t.Sinv.T
+    b = fourier_apply(yI - a @ t.P[kl:kl + m, :].T, forward=True)
+    out = np.empty(y.shape, dtype=np.complex128)
+    out[..., :kl] = a[..., :kl]
+    out[..., kl:kl + m] = b
+    out[..., kl + m:] = a[..., kl:]
+    return out
+
+
+def ho_synthesize(t: HoTransform, c):
+    """T c, batched over leading axes."""
+    c = np.asarray(c, dtype=np.complex128)
+    kl, m = t.kl, t.m
+    a = np.concatenate([c[..., :kl], c[..., kl + m:]], axis=-1)
+    u = fourier_apply(c[..., kl:kl + m], forward=False)
+    out = np.empty(c.shape, dtype=np.complex128)
+    out[..., kl:kl + m] = u + a @ t.P[kl:kl + m, :].T
+    out[..., t.border] = u[..., t.wrap] + a @ t.P[t.border, :].T
+    return out
+
+
+def ho_dense(t: HoTransform):
+    """T entry-wise: border columns, then e^{i j x_i}/sqrt(m) (test oracle)."""
+    x = (np.arange(t.n) - t.kl) * 2.0 * PI / t.m
+    phi = np.exp(1j * np.outer(x, np.arange(t.m))) / math.sqrt(t.m)
+    return np.hstack([t.P[:, :t.kl], phi, t.P[:, t.kl:]]).astype(np.complex128)
+
+
+def ho_nodes(bc, n):
+    """Symbol nodes: 0 at the border coefficients, 2 pi j / m in the interior."""
+    kl, kr, _ = HO_BORDERS[bc]
+    m = n - kl - kr
+    x = np.zeros(n)
+    x[kl:kl + m] = 2.0 * PI * np.arange(m) / m
+    return x
+
+
+# --------------------------------------------------------------------------
 # Operators (operators.cpp)
 # --------------------------------------------------------------------------
 def eigenvalue_grid(bc, n):
     """Symbol nodes (operators.cpp:241-272)."""
     if is_boundary_corrected(bc) and n < 5:
         raise ValidationError("boundary-corrected grids need n >= 5")
+    if is_higher_order(bc):
+        return ho_nodes(bc, n)
     x = np.zeros(n)
     i = np.arange(n)
     if bc == PERIODIC:
@@ -355,7 +491,13 @@ def validate_build(psf: Psf, n, bc):
     """operators.cpp:173-187."""
     if needs_symmetric_psf(bc) and not psf.symmetric:
         raise ValidationError(f"{BC_NAMES[bc]} boundary conditions require a symmetric psf")
-    if is_boundary_corrected(bc):
+    if is_higher_order(bc):
+        kl, kr, _ = HO_BORDERS[bc]
+        if n < kl + kr + 3:
+            raise ValidationError("higher-order borders need n >= degree + 3")
+        if psf.support() > n - kl - kr:
+            raise ValidationError("psf support 2m+1 must be <= n-d")
+    elif is_boundary_corrected(bc):
         if n < 5:
             raise ValidationError("boundary-corrected operators need n >= 5")
         if psf.support() > n - 2:
@@ -379,6 +521,11 @@ def operator_eigenvalues(psf: Psf, n, bc):
         return symbol_eval(psf, 2.0 * PI * np.arange(n) / n)
     if bc == REFLECTIVE:
         return symbol_eval(psf, np.arange(n) * PI / n).real
+    if is_higher_order(bc):
+        kl, kr, _ = HO_BORDERS[bc]
+        d = np.ones(n, dtype=np.complex128)
+        d[kl:n - kr] = symbol_eval(psf, 2.0 * PI * np.arange(n - kl - kr) / (n - kl - kr))
+        return d
     d = np.ones(n, dtype=np.complex128 if is_complex_basis(bc) else np.float64)
     k = np.arange(n - 2)
     if bc == ANTIREFLECTIVE:
@@ -402,12 +549,15 @@ class SpectralBasis:
             self.t = build_transform(B_HC, n)
         elif bc == HOC_FOURIER:
             self.t = build_transform(B_HF, n)
+        self.ho = build_ho_transform(bc, n) if is_higher_order(bc) else None
 
     @property
     def complex(self):
         return is_complex_basis(self.bc)
 
     def synthesize(self, c):
+        if self.ho is not None:
+            return ho_synthesize(self.ho, c)
         if self.t is not None:
             return transform_apply(self.t, c)
         if self.complex:
@@ -415,6 +565,8 @@ class SpectralBasis:
         return cosine_apply(c, forward=False)
 
     def analyze(self, y):
+        if self.ho is not None:
+            return ho_analyze(self.ho, y)
         if self.t is not None:
             return transform_apply_inverse(self.t, y)
         if self.complex:
@@ -716,6 +868,13 @@ def eigenvalues_2d(p: Psf2D, n1, n2, bc, separable=False):
         d[0, :] = d2
         d[n1 - 1, :] = d2
         d[0, 0] = d[0, n2 - 1] = d[n1 - 1, 0] = d[n1 - 1, n2 - 1] = 1
+    if is_higher_order(bc):  # extension: the same scheme with k_l + k_r border lines
+        kl, kr, _ = HO_BORDERS[bc]
+        b1 = list(range(kl)) + list(range(n1 - kr, n1))
+        b2 = list(range(kl)) + list(range(n2 - kr, n2))
+        d[:, b2] = d1[:, None]
+        d[b1, :] = d2[None, :]
+        d[np.ix_(b1, b2)] = 1
     return d
 
 
@@ -763,6 +922,10 @@ def build_operator_2d(p: Psf2D, n1, n2, bc, separable=False) -> BlurOperator2D:
         raise ValidationError(f"{BC_NAMES[bc]} boundary conditions require a quadrantally "
                               "symmetric 2D psf")
     slack = 2 if is_boundary_corrected(bc) else 0
+    if is_higher_order(bc):
+        slack = HO_BORDERS[bc][0] + HO_BORDERS[bc][1]
+        if min(n1, n2) < slack + 3:
+            raise ValidationError("higher-order borders need n >= degree + 3 per axis")
     if is_boundary_corrected(bc) and (n1 < 5 or n2 < 5):
         raise ValidationError("boundary-corrected 2D operators need n >= 5 per axis")
     if 2 * p.m1 + 1 > n1 - slack or 2 * p.m2 + 1 > n2 - slack:
