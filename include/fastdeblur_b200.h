@@ -43,6 +43,13 @@ extern "C" {
 #define FD_BC_ANTIREFLECTIVE 2
 #define FD_BC_HOC_COSINE 3
 #define FD_BC_HOC_FOURIER 4
+/* Extensions (not in the reference, BASELINE configs 1 and 3):
+ * higher-order borders around the Fourier interior -- degree d = 1 (borders
+ * (1, 0), interior n-1) and d = 3 (borders (2, 1), interior n-3); polynomials
+ * of degree <= d have eigenvalue 1; any PSF.  Oracle: oracle/fdoracle.py
+ * HoTransform, pinned by tests/test_ho_borders.py. */
+#define FD_BC_HOC_FOURIER_D1 5
+#define FD_BC_HOC_FOURIER_D3 6
 
 /* SmootherKind (regularize.hpp:15); FIRST_DIFFERENCE is an extension
  * (s = sqrt(2 - 2 cos node), BASELINE config 1) */
@@ -60,9 +67,11 @@ int fd_version(void);
 int fd_parse_bc(const char* name);
 
 /* BC for a polynomial-preservation degree (north_star "BC degree d"):
- * d=1 -> antireflective (symmetric PSF only, operators.cpp:173-176),
- * d=2 -> hoc-cosine (symmetric) or hoc-fourier (any PSF).
- * Other degrees are not in the reference: ValidationError. */
+ * d=1 -> antireflective (symmetric PSF, operators.cpp:173-176) or the
+ *        hoc-fourier-d1 extension (nonsymmetric PSF),
+ * d=2 -> hoc-cosine (symmetric) or hoc-fourier (any PSF),
+ * d=3 -> the hoc-fourier-d3 extension (any PSF).
+ * Other degrees: ValidationError. */
 int fd_bc_for_degree(int degree, int psf_symmetric, int* bc);
 
 /* build_operator(make_psf(weights, normalize), n, bc)   operators.cpp:404-412,

@@ -359,15 +359,43 @@ def legendre_columns(n, degree):
     eigenvalue-1 eigenspace) and on the interior columns, not on the basis
     chosen for the border columns; this basis is near-orthogonal, which gives
     the smallest cond(T) of the bases tried (the raw monomials
-    (b-x)^p of the d = 2 construction give cond(T) 20x larger at d = 3)."""
+    (b-x)^p of the d = 2 construction give cond(T) 20x larger at d = 3).
+    Operation order as build_ho_axis (fd_capi.cu): Bonnet recurrence per
+    element, sequential sum of squares, so the table is bit-identical."""
     t = (2.0 * np.arange(n) - (n - 1)) / (n - 1)
     p_prev, p = np.ones(n), t.copy()
     cols = []
     for k in range(1, degree + 1):
         if k > 1:  # Bonnet: k P_k = (2k-1) t P_{k-1} - (k-1) P_{k-2}
             p_prev, p = p, ((2 * k - 1) * t * p - (k - 1) * p_prev) / k
-        cols.append(p / math.sqrt(float(np.sum(p * p))))
+        cols.append(p / math.sqrt(float(np.cumsum(p * p)[-1])))
     return np.stack(cols, axis=1)
+
+
+def _gauss_jordan_inverse(S):
+    """Inverse of the k x k border capacitance by Gauss-Jordan elimination with
+    partial pivoting, in the operation order of build_ho_axis (fd_capi.cu):
+    cond(S) reaches ~1e6-1e7 at d = 3 (n = 1024-4096), so two different
+    inversion orders already differ by ~1e-10; restating one order makes the
+    device comparison measure the transforms, not the setup."""
+    k = S.shape[0]
+    W = [[float(S[r][c]) for c in range(k)] + [1.0 if c == r else 0.0 for c in range(k)]
+         for r in range(k)]
+    for c in range(k):
+        piv = c
+        for r in range(c + 1, k):
+            if abs(W[r][c]) > abs(W[piv][c]):
+                piv = r
+        if W[piv][c] == 0.0:
+            raise DegenerateError("degenerate transform: border capacitance is singular")
+        W[c], W[piv] = W[piv], W[c]
+        inv = 1.0 / W[c][c]
+        W[c] = [x * inv for x in W[c]]
+        for r in range(k):
+            if r != c:
+                f = W[r][c]
+                W[r] = [W[r][j] - f * W[c][j] for j in range(2 * k)]
+    return np.array([row[k:] for row in W])
 
 
 @dataclass
@@ -417,7 +445,7 @@ def build_ho_transform(bc, n, borders=None) -> HoTransform:
     if sv[-1] <= 0.0 or sv[0] / sv[-1] > 1e12:  # as boundary.cpp:139-150 for k = 2
         raise DegenerateError("degenerate transform: border capacitance is singular or "
                               "ill-conditioned")
-    return HoTransform(bc, n, kl, kr, m, deg, P, border, wrap, S, np.linalg.inv(S))
+    return HoTransform(bc, n, kl, kr, m, deg, P, border, wrap, S, _gauss_jordan_inverse(S))
 
 
 def ho_analyze(t: HoTransform, y):

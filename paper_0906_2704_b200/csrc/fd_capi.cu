@@ -212,18 +212,20 @@ HostPsf make_psf(const double* w, int len, bool normalize) {
 bool needs_symmetric(int bc) {
   return bc == BC_REFLECTIVE || bc == BC_ANTIREFLECTIVE || bc == BC_HOC_COSINE;
 }
-bool is_complex_bc(int bc) { return bc == BC_PERIODIC || bc == BC_HOC_FOURIER; }
+bool is_complex_bc(int bc) { return bc == BC_PERIODIC || bc == BC_HOC_FOURIER || is_ho_bc(bc); }
 bool is_corrected(int bc) {
   return bc == BC_ANTIREFLECTIVE || bc == BC_HOC_COSINE || bc == BC_HOC_FOURIER;
 }
 const char* bc_name(int bc) {
-  static const char* names[] = {"periodic", "reflective", "antireflective", "hoc-cosine",
-                                "hoc-fourier"};
-  return (bc >= 0 && bc < 5) ? names[bc] : "?";
+  static const char* names[] = {"periodic",    "reflective",     "antireflective", "hoc-cosine",
+                                "hoc-fourier", "hoc-fourier-d1", "hoc-fourier-d3"};
+  return (bc >= 0 && bc < 7) ? names[bc] : "?";
 }
 void check_bc(int bc) {
-  if (bc < 0 || bc > 4) validation("unknown boundary condition");
+  if (bc < 0 || bc > 6) validation("unknown boundary condition");
 }
+// interior slack of an axis: n - m
+int border_slack(int bc) { return is_ho_bc(bc) ? ho_kl(bc) + ho_kr(bc) : is_corrected(bc) ? 2 : 0; }
 
 // validate_build (operators.cpp:173-187)
 void validate_build(const HostPsf& psf, int n, int bc) {
@@ -231,7 +233,11 @@ void validate_build(const HostPsf& psf, int n, int bc) {
   if (needs_symmetric(bc) && !psf.symmetric)
     validation(std::string(bc_name(bc)) + " boundary conditions require a symmetric psf");
   const int support = 2 * psf.m + 1;
-  if (is_corrected(bc)) {
+  if (is_ho_bc(bc)) {  // extension (oracle validate_build)
+    const int k = border_slack(bc);
+    if (n < k + 3) validation("higher-order borders need n >= degree + 3");
+    if (support > n - k) validation("psf support 2m+1 must be <= n-d for higher-order borders");
+  } else if (is_corrected(bc)) {
     if (n < 5) validation("boundary-corrected operators need n >= 5");
     if (support > n - 2)
       validation("psf support 2m+1 must be <= n-2 for boundary-corrected operators");
@@ -402,6 +408,8 @@ AxisDev interior_view(const AxisDev& a) {
   v.n = a.m;
   v.bordered = 0;
   v.correction = 0;
+  v.kl = 0;
+  v.hob = 0;
   return v;
 }
 
@@ -449,14 +457,92 @@ FftTables make_fft_tables(int L, std::vector<std::unique_ptr<DevBuf>>& owner, in
   return T;
 }
 
+// Higher-order borders (extension, oracle/fdoracle.py build_ho_transform):
+// Legendre border columns, wrap/bord rows, S = P_B - P[kl + wrap], S^-1.
+void build_ho_axis(Axis& A, int bc, int n) {
+  AxisDev& d = A.dev;
+  const int kl = ho_kl(bc), kr = ho_kr(bc), k = kl + kr, deg = k;
+  const int m = n - k;
+  d.hob = 1;
+  d.kl = kl;
+  d.kr = kr;
+  d.hk = k;
+  // legendre_columns: P_1..P_d of t_i = (2i-(n-1))/(n-1), unit 2-norm
+  std::vector<double> P((size_t)k * n);
+  {
+    std::vector<double> pprev(n, 1.0), p(n), t(n);
+    for (int i = 0; i < n; ++i) p[i] = t[i] = (2.0 * i - (n - 1)) / (n - 1);
+    for (int l = 1; l <= deg; ++l) {
+      if (l > 1) {
+        for (int i = 0; i < n; ++i) {
+          const double nx = ((2 * l - 1) * t[i] * p[i] - (l - 1) * pprev[i]) / l;
+          pprev[i] = p[i];
+          p[i] = nx;
+        }
+      }
+      double ss = 0.0;
+      for (int i = 0; i < n; ++i) ss += p[i] * p[i];
+      const double nr = std::sqrt(ss);
+      for (int i = 0; i < n; ++i) P[(size_t)(l - 1) * n + i] = p[i] / nr;
+    }
+  }
+  for (int l = 0; l < kl; ++l) {
+    d.bord[l] = l;
+    d.wrap[l] = m - kl + l;
+  }
+  for (int l = 0; l < kr; ++l) {
+    d.bord[kl + l] = kl + m + l;
+    d.wrap[kl + l] = l;
+  }
+  double S[kHoMax][kHoMax] = {}, Si[kHoMax][kHoMax] = {};
+  for (int r = 0; r < k; ++r)
+    for (int c = 0; c < k; ++c)
+      S[r][c] = P[(size_t)c * n + d.bord[r]] - P[(size_t)c * n + kl + d.wrap[r]];
+  // Gauss-Jordan with partial pivoting on [S | I]
+  double Wk[kHoMax][2 * kHoMax] = {};
+  for (int r = 0; r < k; ++r) {
+    for (int c = 0; c < k; ++c) Wk[r][c] = S[r][c];
+    Wk[r][k + r] = 1.0;
+  }
+  for (int c = 0; c < k; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < k; ++r)
+      if (std::abs(Wk[r][c]) > std::abs(Wk[piv][c])) piv = r;
+    if (Wk[piv][c] == 0.0)
+      degenerate("degenerate transform: border capacitance is singular");
+    for (int j = 0; j < 2 * k; ++j) std::swap(Wk[c][j], Wk[piv][j]);
+    const double inv = 1.0 / Wk[c][c];
+    for (int j = 0; j < 2 * k; ++j) Wk[c][j] *= inv;
+    for (int r = 0; r < k; ++r)
+      if (r != c) {
+        const double f = Wk[r][c];
+        for (int j = 0; j < 2 * k; ++j) Wk[r][j] -= f * Wk[c][j];
+      }
+  }
+  double ns = 0.0, ni = 0.0;
+  for (int r = 0; r < k; ++r)
+    for (int c = 0; c < k; ++c) {
+      Si[r][c] = Wk[r][k + c];
+      ns += S[r][c] * S[r][c];
+      ni += Si[r][c] * Si[r][c];
+    }
+  if (!(std::sqrt(ns * ni) <= 1e12))  // Frobenius bound on the 2-norm condition
+    degenerate("degenerate transform: border capacitance is ill-conditioned");
+  for (int r = 0; r < kHoMax; ++r)
+    for (int c = 0; c < kHoMax; ++c) d.sinv[r * kHoMax + c] = (r < k && c < k) ? Si[r][c] : 0.0;
+  d.P = dev_upload(A.bufs, P);
+  (void)m;
+}
+
 std::unique_ptr<Axis> build_axis(int bc, int n) {
   auto A = std::make_unique<Axis>();
   AxisDev& d = A->dev;
   d.n = n;
   d.bordered = is_corrected(bc);
   d.cplx = is_complex_bc(bc);
-  d.m = d.bordered ? n - 2 : n;
-  d.kind = (bc == BC_PERIODIC || bc == BC_HOC_FOURIER) ? IK_FOURIER
+  d.kl = d.bordered ? 1 : 0;
+  d.m = n - border_slack(bc);
+  d.kind = (bc == BC_PERIODIC || bc == BC_HOC_FOURIER || is_ho_bc(bc)) ? IK_FOURIER
            : bc == BC_ANTIREFLECTIVE                  ? IK_SINE
                                                       : IK_COS;
   d.correction = d.bordered && bc != BC_ANTIREFLECTIVE;
@@ -474,8 +560,8 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
     const int M = ceil_pow2(std::max(2LL * L - 1, 2LL), &logM);
     if (M <= kMaxOnChipM) d.fft = make_fft_tables(L, A->bufs, d.kind == IK_COS ? m : 0, dct_tw);
   }
-  // half-length real path (R even)
-  d.rhalf = (L % 2 == 0) && L >= 2;
+  // half-length real path (R even; not for the higher-order borders)
+  d.rhalf = (L % 2 == 0) && L >= 2 && !is_ho_bc(bc);
   if (d.rhalf) {  // split convolution (two halves of M/2) beyond the on-chip size
     int logM = 0;
     const int M = ceil_pow2(std::max((long long)L - 1, 2LL), &logM);
@@ -490,6 +576,11 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
   }
   if (!d.fft.M && !d.rhalf)
     validation("order " + std::to_string(n) + " exceeds this build's on-chip transform limit");
+  if (is_ho_bc(bc)) {
+    build_ho_axis(*A, bc, n);
+    ck(cudaDeviceSynchronize(), "axis tables");
+    return A;
+  }
 
   if (!d.bordered) {
     ck(cudaDeviceSynchronize(), "axis tables");
@@ -1030,14 +1121,14 @@ GcvData gcv_data(const fd_op* op, const fd_smoother* L, const Analyzed& a, long 
 void build_pairs(fd_smoother* L, const fd_op* op) {
   const int n = op->n1;
   std::vector<int2> pairs;
-  const int off = op->bc == BC_HOC_FOURIER ? 1 : 0;
-  const int R = op->bc == BC_HOC_FOURIER ? n - 2 : n;
-  if (off) pairs.push_back(make_int2(0, -1));
+  const int off = op->ax1->dev.kl;
+  const int R = op->ax1->dev.m;
+  for (int k = 0; k < off; ++k) pairs.push_back(make_int2(k, -1));
   for (int k = 0; k <= R / 2; ++k) {
     const int kc = (R - k) % R;
     pairs.push_back(make_int2(off + k, kc == k ? -1 : off + kc));
   }
-  if (off) pairs.push_back(make_int2(n - 1, -1));
+  for (int k = off + R; k < n; ++k) pairs.push_back(make_int2(k, -1));
   std::vector<double> r(n);
   ck(cudaMemcpy(r.data(), L->r, n * sizeof(double), cudaMemcpyDeviceToHost), "r");
   std::vector<double> rr(pairs.size());
@@ -1681,23 +1772,24 @@ int fd_phase_clocks(unsigned long long* out, int reset) {
 int fd_parse_bc(const char* name) {
   if (!name) return -1;
   const std::string s(name);
-  for (int b = 0; b < 5; ++b)
+  for (int b = 0; b < 7; ++b)
     if (s == bc_name(b)) return b;
   return -1;
 }
 
 int fd_bc_for_degree(int degree, int psf_symmetric, int* bc) {
   return guarded([&] {
+    // degree 1: antireflective (reference) for a symmetric psf, the
+    // higher-order Fourier extension otherwise; degree 3: extension only
     if (degree == 1) {
-      if (!psf_symmetric)
-        validation("degree 1 (antireflective) requires a symmetric psf in the reference "
-                   "(operators.cpp:173-176)");
-      *bc = BC_ANTIREFLECTIVE;
+      *bc = psf_symmetric ? BC_ANTIREFLECTIVE : BC_HOC_FOURIER_D1;
     } else if (degree == 2) {
       *bc = psf_symmetric ? BC_HOC_COSINE : BC_HOC_FOURIER;
+    } else if (degree == 3) {
+      *bc = BC_HOC_FOURIER_D3;
     } else {
       validation("boundary-condition degree " + std::to_string(degree) +
-                 " is not provided by the reference (SPEC.md:164)");
+                 " is not provided (degrees 1..3)");
     }
   });
 }
@@ -1765,7 +1857,9 @@ void validate_build_2d(bool symmetric, int rows, int cols, int n1, int n2, int b
     validation(std::string(bc_name(bc)) +
                " boundary conditions require a quadrantally symmetric 2D psf");
   const bool corrected = is_corrected(bc);
-  const int slack = corrected ? 2 : 0;
+  const int slack = border_slack(bc);
+  if (is_ho_bc(bc) && (n1 < slack + 3 || n2 < slack + 3))
+    validation("higher-order borders need n >= degree + 3 per axis");
   if (corrected && (n1 < 5 || n2 < 5))
     validation("boundary-corrected 2D operators need n >= 5 per axis");
   if (rows > n1 - slack || cols > n2 - slack) validation("2D psf support exceeds the per-axis limit");
@@ -1798,6 +1892,10 @@ fd_op* create_2d(const std::vector<double>& w2, int rows, int cols, bool symmetr
     launched("k_eig2d_stage1");
     k_eig2d_stage2<<<2048, 256>>>(T, m1, bc, n1, n2, op->cplx, op->d);
     launched("k_eig2d_stage2");
+    if (is_ho_bc(bc)) {
+      k_eig2d_ho_border<<<1024, 256>>>(op->d1, op->d2, n1, n2, ho_kl(bc), ho_kr(bc), op->d);
+      launched("k_eig2d_ho_border");
+    }
     if (is_corrected(bc)) {
       k_eig2d_edges<<<64, 256>>>(op->d1, op->d2, n1, n2, op->d);
       launched("k_eig2d_edges");
@@ -1974,8 +2072,8 @@ int fd_smoother_create_custom(const fd_op* op, const double* s, fd_smoother** ou
       ck(cudaDeviceSynchronize(), "ratio");
       if (op->cplx) {
         // pairing needs a symmetric custom smoother (s_e = s_{R-e}); check it
-        const int n = op->n1, off = op->bc == BC_HOC_FOURIER ? 1 : 0;
-        const int R = op->bc == BC_HOC_FOURIER ? n - 2 : n;
+        const int off = op->ax1->dev.kl;
+        const int R = op->ax1->dev.m;
         bool sym = true;
         for (int k = 1; k < R && sym; ++k)  // symmetric to rounding
           sym = std::abs(h[off + k] - h[off + R - k]) <= 1e-13 * std::abs(h[off + k]);

@@ -8,8 +8,20 @@
 namespace fdb {
 
 // BoundaryCondition codes (reference operators.hpp:15-21).
+// Extension codes 5, 6: higher-order Fourier borders of degree d = 1 and 3
+// (oracle/fdoracle.py HoTransform), not in the reference.
 enum Bc : int { BC_PERIODIC = 0, BC_REFLECTIVE = 1, BC_ANTIREFLECTIVE = 2, BC_HOC_COSINE = 3,
-                BC_HOC_FOURIER = 4 };
+                BC_HOC_FOURIER = 4, BC_HOC_FOURIER_D1 = 5, BC_HOC_FOURIER_D3 = 6 };
+
+// border widths (k_left, k_right) of the higher-order codes
+__host__ __device__ __forceinline__ int ho_kl(int bc) {
+  return bc == BC_HOC_FOURIER_D1 ? 1 : bc == BC_HOC_FOURIER_D3 ? 2 : 0;
+}
+__host__ __device__ __forceinline__ int ho_kr(int bc) { return bc == BC_HOC_FOURIER_D3 ? 1 : 0; }
+__host__ __device__ __forceinline__ bool is_ho_bc(int bc) {
+  return bc == BC_HOC_FOURIER_D1 || bc == BC_HOC_FOURIER_D3;
+}
+constexpr int kHoMax = 3;  // largest border rank (d = 3)
 // Interior trigonometric transform of an axis (boundary.cpp:120-129, operators.cpp:291-312).
 enum Interior : int { IK_COS = 0, IK_FOURIER = 1, IK_SINE = 2 };
 // Smoother kinds (regularize.hpp:15) + the first-difference extension.
@@ -66,6 +78,19 @@ struct AxisDev {
   // per-axis constants of the trig transforms (trig.cpp:170-234), host-computed
   double inv_sqrt_m, dct_s0, dct_s1, dst_scale;
   double cavr[4], capr[4];
+  // Interior coefficient e = i + kl (kl = 1 for the rank-2 borders).
+  int kl;
+  // Higher-order borders (hob = 1; bordered = correction = 0): k = kl + kr
+  // polynomial columns P (P[l*n + i], unit norm) around the Fourier interior
+  // of length m = n - k (oracle HoTransform).  Border row bord[l] is the
+  // 2 pi-periodic image of interior sample wrap[l], so
+  //   analyze     a = sinv (y[bord] - y[kl + wrap]),  b = F (y_I - P_I a)
+  //   synthesize  y_I = F^H b + P_I a,  y[bord] = (F^H b)[wrap] + P[bord] a
+  // with coefficient l of a stored at element l (l < kl) or m + l (l >= kl).
+  int hob, kr, hk;
+  const double* P;
+  double sinv[kHoMax * kHoMax];
+  int bord[kHoMax], wrap[kHoMax];
 };
 
 // Geometry of a set of lines (rows or columns of a batch of arrays).

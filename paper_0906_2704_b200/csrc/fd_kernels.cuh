@@ -43,9 +43,7 @@ __device__ __forceinline__ void stc(void* base, bool cplx, long long idx, double
 }
 
 // element index of interior coefficient i
-__device__ __forceinline__ int interior_elem(const AxisDev& ax, int i) {
-  return ax.bordered ? i + 1 : i;
-}
+__device__ __forceinline__ int interior_elem(const AxisDev& ax, int i) { return i + ax.kl; }
 
 // spectral values (d, s) of coefficient e of line l
 __device__ __forceinline__ void spectral_at(const Spectral& sp, const Lines& g, int l, int e,
@@ -174,6 +172,11 @@ __device__ __forceinline__ double eig_node(int bc, int n, int i) {
     case BC_REFLECTIVE: return kPi * i / n;
     case BC_ANTIREFLECTIVE: return i < n - 1 ? kPi * i / (n - 1) : 0.0;
     case BC_HOC_COSINE: return (i >= 1 && i < n - 1) ? kPi * (i - 1) / (n - 2) : 0.0;
+    case BC_HOC_FOURIER_D1:
+    case BC_HOC_FOURIER_D3: {  // extension: 2 pi j / m on the interior, 0 on the borders
+      const int kl = ho_kl(bc), m = n - kl - ho_kr(bc);
+      return (i >= kl && i < kl + m) ? 2.0 * kPi * (i - kl) / m : 0.0;
+    }
     default: return (i >= 1 && i < n - 1) ? 2.0 * kPi * (i - 1) / (n - 2) : 0.0;
   }
 }
@@ -197,13 +200,21 @@ __global__ void k_eigenvalues_1d(const double* __restrict__ h, int m, int symmet
         pinned = (i == 0 || i == n - 1);
         t = (i - 1) * kPi / (n - 2);
         break;
+      case BC_HOC_FOURIER_D1:
+      case BC_HOC_FOURIER_D3: {  // extension (oracle operator_eigenvalues)
+        const int kl = ho_kl(bc), m = n - kl - ho_kr(bc);
+        pinned = (i < kl || i >= kl + m);
+        t = 2.0 * kPi * (i - kl) / m;
+        break;
+      }
       default:
         pinned = (i == 0 || i == n - 1);
         t = 2.0 * kPi * (i - 1) / (n - 2);
         break;
     }
     double2 z = pinned ? make_double2(1.0, 0.0) : symbol_eval(h, m, symmetric, t);
-    if (bc != BC_PERIODIC && bc != BC_HOC_FOURIER) z.y = 0.0;  // real bases keep .real()
+    if (bc != BC_PERIODIC && bc != BC_HOC_FOURIER && !is_ho_bc(bc))
+      z.y = 0.0;  // real bases keep .real()
     d[i] = z;
   }
 }
@@ -301,6 +312,23 @@ __global__ void k_eig2d_corners(int n1, int n2, double2* d) {
   }
 }
 
+// higher-order borders (extension): the same scheme with kl + kr border lines
+// per axis -- border columns from d1, border rows from d2, crossings 1
+__global__ void k_eig2d_ho_border(const double2* __restrict__ d1, const double2* __restrict__ d2,
+                                  int n1, int n2, int kl, int kr, double2* d) {
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n1 * n2;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx / n2), j = (int)(idx % n2);
+    const bool bi = i < kl || i >= n1 - kr, bj = j < kl || j >= n2 - kr;
+    if (bi && bj)
+      d[idx] = make_double2(1.0, 0.0);
+    else if (bj)
+      d[idx] = d1[i];
+    else if (bi)
+      d[idx] = d2[j];
+  }
+}
+
 __global__ void k_smoother_2d(int kind, const double* __restrict__ s1,
                               const double* __restrict__ s2, int n1, int n2, double* s) {
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < (long long)n1 * n2;
@@ -315,6 +343,46 @@ __global__ void k_smoother_2d(int kind, const double* __restrict__ s1,
 // boundary.cpp:338-375; plain C / F for reflective / periodic).
 // Real input lines are packed in pairs into one complex FFT.
 // ---------------------------------------------------------------------------
+// ---- higher-order borders (extension; AxisDev::hob) ----
+// a = sinv (y[bord] - y[kl + wrap]) of one line: k <= 3 samples, solved by
+// every thread (no block synchronisation)
+template <class LD>
+__device__ __forceinline__ void ho_amplitudes(const AxisDev& ax, LD ld, double2 (&a)[kHoMax]) {
+  double2 r[kHoMax];
+#pragma unroll
+  for (int l = 0; l < kHoMax; ++l)
+    r[l] = l < ax.hk ? csub(ld(ax.bord[l]), ld(ax.kl + ax.wrap[l])) : czero();
+#pragma unroll
+  for (int l = 0; l < kHoMax; ++l) {
+    double2 v = czero();
+#pragma unroll
+    for (int q = 0; q < kHoMax; ++q) {
+      const double sv = ax.sinv[l * kHoMax + q];
+      v.x += sv * r[q].x;
+      v.y += sv * r[q].y;
+    }
+    a[l] = v;
+  }
+}
+
+// (P a)_e: the border columns' contribution at element e
+__device__ __forceinline__ double2 ho_poly(const AxisDev& ax, const double2 (&a)[kHoMax], int e) {
+  double2 v = czero();
+#pragma unroll
+  for (int l = 0; l < kHoMax; ++l)
+    if (l < ax.hk) {
+      const double p = __ldg(&ax.P[(long long)l * ax.n + e]);
+      v.x += a[l].x * p;
+      v.y += a[l].y * p;
+    }
+  return v;
+}
+
+// element of border coefficient l: [a_0 .. a_{kl-1}, interior, a_kl .. a_{k-1}]
+__device__ __forceinline__ int ho_coef_elem(const AxisDev& ax, int l) {
+  return l < ax.kl ? l : ax.m + l;
+}
+
 struct LineIO {
   const void* in;
   void* out;
@@ -360,6 +428,11 @@ __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
     y01 = ld1(0);
     yn1 = ld1(n - 1);
   }
+  double2 ha0[kHoMax], ha1[kHoMax];
+  if (ax.hob) {
+    ho_amplitudes(ax, ld0, ha0);
+    ho_amplitudes(ax, ld1, ha1);
+  }
 
   // ---- load (with chirp premultiply) + border dot products ----
   double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // ra0, rb0, ra1, rb1 (re, im)
@@ -389,7 +462,11 @@ __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
       if (j < m) {
         const int e = interior_elem(ax, j);
         if (pair) {
-          const double a = ld0(e).x, b = ld1(e).x;
+          double a = ld0(e).x, b = ld1(e).x;
+          if (ax.hob) {  // fold the border: F (y_I - P_I a)
+            a -= ho_poly(ax, ha0, e).x;
+            b -= ho_poly(ax, ha1, e).x;
+          }
           val = cmul(make_double2(a, b), __ldg(&chirp[j]));
           if (dots) {
             const double2 ra = __ldg(&ax.row_a[j]), rb = __ldg(&ax.row_b[j]);
@@ -399,7 +476,8 @@ __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
             acc[6] += rb.x * b, acc[7] += rb.y * b;
           }
         } else {
-          const double2 z = ld0(e);
+          double2 z = ld0(e);
+          if (ax.hob) z = csub(z, ho_poly(ax, ha0, e));
           val = cmul(z, __ldg(&chirp[j]));
           if (dots) {
             const double2 ra = cmul(__ldg(&ax.row_a[j]), z), rb = cmul(__ldg(&ax.row_b[j]), z);
@@ -523,6 +601,13 @@ __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
       if (has1) stc(io.out, io.out_cplx, oo1 + e * eso, xi1);
     }
   }
+  if (ax.hob && threadIdx.x == 0) {
+    for (int l = 0; l < ax.hk; ++l) {
+      const long long el = (long long)ho_coef_elem(ax, l) * eso;
+      stc(io.out, io.out_cplx, oo0 + el, pair ? make_double2(ha0[l].x, 0.0) : ha0[l]);
+      if (has1) stc(io.out, io.out_cplx, oo1 + el, make_double2(ha1[l].x, 0.0));
+    }
+  }
   if (ax.bordered && threadIdx.x == 0) {
     const double al = ax.alpha;
     for (int t = 0; t < (has1 ? 2 : 1); ++t) {
@@ -641,6 +726,14 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
     u01 = c1(0);
     un1 = c1(n - 1);
   }
+  double2 ua0[kHoMax], ua1[kHoMax];  // border amplitudes a (filtered)
+  if (ax.hob) {
+#pragma unroll
+    for (int l = 0; l < kHoMax; ++l) {
+      ua0[l] = l < ax.hk ? c0(ho_coef_elem(ax, l)) : czero();
+      ua1[l] = l < ax.hk ? c1(ho_coef_elem(ax, l)) : czero();
+    }
+  }
   double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // top0, bottom0, top1, bottom1 (re, im)
   const bool dots = ax.bordered && ax.correction;
 
@@ -753,7 +846,34 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
       in0 = cscale(cconj(cmul(x[pidx(p)], __ldg(&chirp[p]))), inv_sqrt_m);
     }
     const int e = interior_elem(ax, p);
-    if (ax.bordered) {
+    if (ax.hob) {
+      // y_I = F^H b + P_I a; border rows whose 2 pi image is p: (F^H b)_p + P_B a
+      if (ax.cplx && !hpack) {
+        const double2 o = cadd(in0, ho_poly(ax, ua0, e));
+        stc(io.out, io.out_cplx, oo0 + e * eso, o);
+        im2 += o.y * o.y;
+        for (int l = 0; l < ax.hk; ++l)
+          if (ax.wrap[l] == p) {
+            const double2 ob = cadd(in0, ho_poly(ax, ua0, ax.bord[l]));
+            stc(io.out, io.out_cplx, oo0 + ax.bord[l] * eso, ob);
+            im2 += ob.y * ob.y;
+          }
+      } else {
+        stc(io.out, io.out_cplx, oo0 + e * eso, make_double2(in0.x + ho_poly(ax, ua0, e).x, 0.0));
+        if (has1)
+          stc(io.out, io.out_cplx, oo1 + e * eso,
+              make_double2(in1.x + ho_poly(ax, ua1, e).x, 0.0));
+        for (int l = 0; l < ax.hk; ++l)
+          if (ax.wrap[l] == p) {
+            const int eb = ax.bord[l];
+            stc(io.out, io.out_cplx, oo0 + eb * eso,
+                make_double2(in0.x + ho_poly(ax, ua0, eb).x, 0.0));
+            if (has1)
+              stc(io.out, io.out_cplx, oo1 + eb * eso,
+                  make_double2(in1.x + ho_poly(ax, ua1, eb).x, 0.0));
+          }
+      }
+    } else if (ax.bordered) {
       const double qi = __ldg(&ax.q[e]), qr = __ldg(&ax.q[n - 1 - e]);
       if (ax.cplx && !hpack) {
         const double2 o = cadd(cadd(cscale(u00, qi), in0), cscale(un0, qr));

@@ -24,7 +24,9 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # FASTDEBLUR_LIB: an alternative in-tree build (e.g. the phase-timing variant)
 LIB_PATH = os.environ.get("FASTDEBLUR_LIB") or os.path.join(_HERE, "libfdb200.so")
 
-BC = {"periodic": 0, "reflective": 1, "antireflective": 2, "hoc-cosine": 3, "hoc-fourier": 4}
+BC = {"periodic": 0, "reflective": 1, "antireflective": 2, "hoc-cosine": 3, "hoc-fourier": 4,
+      # extensions (not in the reference): higher-order Fourier borders, degree 1 and 3
+      "hoc-fourier-d1": 5, "hoc-fourier-d3": 6}
 BC_NAMES = {v: k for k, v in BC.items()}
 SMOOTHER = {"identity": 0, "laplacian": 1, "first-difference": 2}
 

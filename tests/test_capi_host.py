@@ -53,8 +53,10 @@ def test_header_cites_reference_interfaces():
     lambda: P.build_operator([1.0], 16, "no-such-bc"),
     lambda: P.build_operator_2d(np.ones((2, 3)), 16, 16, "periodic"),      # even rows
     lambda: P.build_operator_2d(np.outer([0.1, 0.9, 0.0], [1, 1, 1]), 16, 16, "hoc-cosine"),
-    lambda: P.bc_for_degree(3, True),
-    lambda: P.bc_for_degree(1, False),
+    lambda: P.bc_for_degree(4, True),
+    lambda: P.bc_for_degree(0, False),
+    lambda: P.build_operator([0.1, 0.2, 0.4, 0.2, 0.1], 7, "hoc-fourier-d3"),  # support > n-3
+    lambda: P.build_operator([1.0], 3, "hoc-fourier-d1"),                  # n < d+3
 ])
 def test_validation_errors_match_reference(call):
     """operators.cpp:173-187, psf.cpp:10-38, multidim.cpp:119-130 (status 2)."""
@@ -66,6 +68,9 @@ def test_bc_mapping():
     assert P.bc_for_degree(2, True) == "hoc-cosine"
     assert P.bc_for_degree(2, False) == "hoc-fourier"
     assert P.bc_for_degree(1, True) == "antireflective"
+    assert P.bc_for_degree(1, False) == "hoc-fourier-d1"  # extensions
+    assert P.bc_for_degree(3, False) == "hoc-fourier-d3"
+    assert P.bc_for_degree(3, True) == "hoc-fourier-d3"
     lib = FD.lib()
     for name, code in P.BC.items():
         assert lib.fd_parse_bc(name.encode()) == code
