@@ -44,7 +44,7 @@ from paper_0906_2704_b200 import workloads as W  # noqa: E402
 METRIC = "Mpixels/s per Tikhonov+GCV restoration (fp64) at 1/2/4/8 B200; % HBM roofline"
 SMOOTHER_NAMES = {0: "identity", 1: "laplacian", 2: "first-difference"}
 BC_NAMES = {0: "periodic", 1: "reflective", 2: "antireflective", 3: "hoc-cosine",
-            4: "hoc-fourier"}
+            4: "hoc-fourier", 5: "hoc-fourier-d1", 6: "hoc-fourier-d3"}
 
 
 def parse():
@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--items", type=int, default=0, help="override the per-rank batch")
+    ap.add_argument("--bc", default=None, help="override the config's boundary condition "
+                    "(name, e.g. hoc-fourier-d1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -74,7 +76,11 @@ def first_difference_s(bc, n):
     """s = sqrt(2 - 2 cos node) on the operator's node grid."""
     i = np.arange(n)
     x = np.zeros(n)
-    if bc == W.HOC_FOURIER:
+    if bc in (W.HOC_FOURIER_D1, W.HOC_FOURIER_D3):  # extension: borders (1,0) / (2,1)
+        kl, kr = (1, 0) if bc == W.HOC_FOURIER_D1 else (2, 1)
+        m = n - kl - kr
+        x[kl:kl + m] = 2.0 * np.pi * np.arange(m) / m
+    elif bc == W.HOC_FOURIER:
         x[1:n - 1] = 2.0 * np.pi * (i[1:n - 1] - 1) / (n - 2)
     elif bc == W.HOC_COSINE:
         x[1:n - 1] = np.pi * (i[1:n - 1] - 1) / (n - 2)
@@ -92,7 +98,7 @@ def reference_deblur_sample(cfg, first, count, threads):
         _, g = W.signals_1d(cfg, first, count)
         s_custom = first_difference_s(cfg.bc, cfg.n1) if smoother == 2 else None
         sm = 2 if smoother == 2 else smoother
-        if R.available():
+        if R.available() and cfg.bc <= W.HOC_FOURIER:
             t0 = time.perf_counter()
             R.deblur_1d(cfg.psf, cfg.n1, cfg.bc, sm, g, True, mu_min=cfg.mu_min,
                         mu_max=cfg.mu_max, count=cfg.count, threads=threads, s_custom=s_custom)
@@ -310,6 +316,10 @@ def main():
     from paper_0906_2704_b200 import dist
     rank, world, local = dist.init()
     cfg = W.config(args.config)
+    if args.bc is not None:
+        import dataclasses
+        code = {v: k for k, v in BC_NAMES.items()}[args.bc]
+        cfg = dataclasses.replace(cfg, bc=code, note=f"bc overridden to {args.bc}")
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     # reference threads: batched configs run an outer pool over
     # items with serial inner loops; single-item configs use the library's own

@@ -24,6 +24,7 @@
 #include "fd_gcv_core.h"
 #include "fd_internal.h"
 #include "fd_kernels.cuh"
+#include "fd_pair.cuh"
 
 
 using namespace fdb;
@@ -146,6 +147,11 @@ void set_rline_attrs(int kmax) {
   cudaFuncSetAttribute(k_ranalyze<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
   cudaFuncSetAttribute(k_rsynth<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
 }
+template <int LOGM>
+void set_pair_attrs(int kmax) {
+  cudaFuncSetAttribute(k_panalyze<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+  cudaFuncSetAttribute(k_psynth<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+}
 
 void init_runtime_once() {
   static std::once_flag once;
@@ -169,6 +175,12 @@ void init_runtime_once() {
     set_rline_attrs<11>(kmax);
     set_rline_attrs<12>(kmax);
     set_rline_attrs<13>(kmax);
+    set_pair_attrs<8>(kmax);
+    set_pair_attrs<9>(kmax);
+    set_pair_attrs<10>(kmax);
+    set_pair_attrs<11>(kmax);
+    set_pair_attrs<12>(kmax);
+    set_pair_attrs<13>(kmax);
     ok = true;
   });
   if (!ok) throw FdError(FD_ERR_OTHER, "no CUDA device available (fastdeblur_b200 has no CPU path)");
@@ -310,8 +322,42 @@ int persistent_grid(K kern, int threads, size_t smem, int count) {
   return std::max(1, std::min(count, std::max(1, per_sm) * num_sms()));
 }
 
+// the pair kernels (fd_pair.cuh) carry real lines of the higher-order borders
+// (odd interior length) with Hermitian-packed coefficients (io.pack == 2)
+bool pair_path(const AxisDev& ax) {
+  return ax.hob && (ax.m & 1) && ax.fft.M && ax.fft.logM >= 8 && ax.fft.logM <= 13;
+}
+
+void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaStream_t st) {
+  const size_t smem = (size_t)pair_slots(ax.fft.M, ax.m) * sizeof(double2);
+  const int pairs = (io.gi.count + 1) / 2;
+#define FD_PA(L)                                                                           \
+  if (sa) {                                                                                \
+    k_psynth<L><<<persistent_grid(k_psynth<L>, PairShape<L>::NT, smem, pairs),             \
+                  PairShape<L>::NT, smem, st>>>(ax, io, *sa);                              \
+  } else {                                                                                 \
+    k_panalyze<L><<<persistent_grid(k_panalyze<L>, PairShape<L>::NT, smem, pairs),         \
+                    PairShape<L>::NT, smem, st>>>(ax, io);                                 \
+  }
+  switch (ax.fft.logM) {
+    case 8: FD_PA(8); break;
+    case 9: FD_PA(9); break;
+    case 10: FD_PA(10); break;
+    case 11: FD_PA(11); break;
+    case 12: FD_PA(12); break;
+    default: FD_PA(13); break;
+  }
+#undef FD_PA
+  launched(sa ? "k_psynth" : "k_panalyze");
+}
+
 void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
   if (io.gi.count == 0) return;
+  if (io.pack == 2 && !io.in_cplx && pair_path(ax)) {
+    ProfScope ps("k_analyze", st);
+    launch_pair(ax, io, nullptr, st);
+    return;
+  }
   if (!io.in_cplx && ax.rhalf) {  // one real line per CTA, half-length DFT
     ProfScope ps("k_analyze", st);
     if (ax.hfft.M > kMaxOnChipM) {  // split convolution, persistent CTAs + scratch
@@ -349,6 +395,11 @@ void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
 
 void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cudaStream_t st) {
   if (io.gi.count == 0) return;
+  if (io.pack == 2 && !io.out_cplx && pair_path(ax)) {
+    ProfScope ps(sa.mode == 1 ? "k_synth_filter" : "k_synth", st);
+    launch_pair(ax, io, &sa, st);
+    return;
+  }
   if (!io.out_cplx && ax.rhalf && (!ax.cplx || sa.resid2 == nullptr)) {
     ProfScope ps(sa.mode == 1 ? "k_synth_filter" : "k_synth", st);
     if (ax.hfft.M > kMaxOnChipM) {
@@ -484,7 +535,10 @@ void build_ho_axis(Axis& A, int bc, int n) {
       for (int i = 0; i < n; ++i) ss += p[i] * p[i];
       const double nr = std::sqrt(ss);
       for (int i = 0; i < n; ++i) P[(size_t)(l - 1) * n + i] = p[i] / nr;
+      d.ho_s[l - 1] = 1.0 / nr;
     }
+    d.ho_ta = 2.0 / (n - 1);
+    d.ho_tb = -1.0;
   }
   for (int l = 0; l < kl; ++l) {
     d.bord[l] = l;
@@ -1072,8 +1126,10 @@ struct Analyzed {
 Analyzed analyze_for_gcv(const fd_op* op, const fd_smoother* L, const double* g, long long count,
                          Scratch& S, bool want_full = false, bool want_w32 = false) {
   Analyzed a;
-  const bool use_w = op->dim == 1 && op->ax1->dev.rhalf && (!op->cplx || L->pair);
-  a.pack = use_w && op->cplx && !want_full;
+  const bool pair = op->dim == 1 && pair_path(op->ax1->dev);
+  const bool use_w = op->dim == 1 && (op->ax1->dev.rhalf || (pair && !want_full)) &&
+                     (!op->cplx || L->pair);
+  a.pack = use_w && op->cplx && !want_full ? (pair ? 2 : 1) : 0;
   a.ghat = (op->cplx && !a.pack) ? (void*)S.get<double2>(count * op->N())
                                  : (void*)S.get<double>(count * op->N());
   if (use_w) {

@@ -352,10 +352,12 @@ __device__ __forceinline__ void bluestein_half(double2* x, const FftTables& T, c
 // uses exactly FftShape<LOGM>::NT threads, every pass is unrolled, and every
 // shared-memory address is one per-thread base plus compile-time offsets
 // (pidx(base + q SR) = pidx(base) + q (SR + SR/16) for SR a multiple of 16).
-template <int LOGM>
+// NTH != 0 overrides the thread count (one CTA per SM at large M wants more warps)
+template <int LOGM, int NTH = 0>
 struct FftShape {
   static constexpr int M = 1 << LOGM;
-  static constexpr int NT = M / 16 >= 256 ? 256 : (M / 16 <= 64 ? 64 : M / 16);
+  static constexpr int NT =
+      NTH ? NTH : (M / 16 >= 256 ? 256 : (M / 16 <= 64 ? 64 : M / 16));
   static constexpr int NP = (LOGM + 3) / 4;
   static constexpr int LOB = ((LOGM > 1 ? LOGM - 1 : 0) + 1) / 2;  // load_twiddles' split
 };
@@ -365,9 +367,9 @@ __device__ __forceinline__ double2 tw_t(const TwSm& tw, int j) {
   return cmul(tw.hi[j >> LOB], tw.lo[j & ((1 << LOB) - 1)]);
 }
 
-template <int LOGM, int LR, int S, bool PAD>
+template <int LOGM, int LR, int S, bool PAD, int NTH = 0>
 __device__ __forceinline__ void dif_pass_t(double2* __restrict__ x, const TwSm& tw, int nvalid) {
-  using F = FftShape<LOGM>;
+  using F = FftShape<LOGM, NTH>;
   constexpr int R = 1 << LR, SR = S >> LR, ITEMS = F::M >> LR;
   constexpr int TWSTEP = F::M / S;
   constexpr int QS = SR + SR / 16;
@@ -400,9 +402,9 @@ __device__ __forceinline__ void dif_pass_t(double2* __restrict__ x, const TwSm& 
   }
 }
 
-template <int LOGM, int LR, int S>
+template <int LOGM, int LR, int S, int NTH = 0>
 __device__ __forceinline__ void dit_pass_t(double2* __restrict__ x, const TwSm& tw) {
-  using F = FftShape<LOGM>;
+  using F = FftShape<LOGM, NTH>;
   constexpr int R = 1 << LR, SR = S >> LR, ITEMS = F::M >> LR;
   constexpr int TWSTEP = F::M / S;
   constexpr int QS = SR + SR / 16;
@@ -437,10 +439,10 @@ __device__ __forceinline__ void dit_pass_t(double2* __restrict__ x, const TwSm& 
 }
 
 // innermost radix-16 pass: DIF stages, multiply by bhat, DIT stages
-template <int LOGM, bool PAD>
+template <int LOGM, bool PAD, int NTH = 0>
 __device__ __forceinline__ void mid_pass_t(double2* __restrict__ x,
                                            const double2* __restrict__ bhat, int nvalid) {
-  using F = FftShape<LOGM>;
+  using F = FftShape<LOGM, NTH>;
   constexpr int R = 16, ITEMS = F::M / 16;
 #pragma unroll
   for (int i0 = 0; i0 < ITEMS; i0 += F::NT) {
@@ -486,34 +488,34 @@ __device__ __forceinline__ void mid_pass_t(double2* __restrict__ x,
 }
 
 // pass P of the DIF sequence (block size S), the inner passes, then its DIT mirror
-template <int LOGM, int P, int S>
+template <int LOGM, int P, int S, int NTH = 0>
 __device__ __forceinline__ void bluestein_rec(double2* x, const double2* bhat, const TwSm& tw,
                                               int nvalid) {
-  using F = FftShape<LOGM>;
+  using F = FftShape<LOGM, NTH>;
   if constexpr (P == F::NP - 1) {
     if (P == 0 && nvalid < F::M)
-      mid_pass_t<LOGM, true>(x, bhat, nvalid);
+      mid_pass_t<LOGM, true, NTH>(x, bhat, nvalid);
     else
-      mid_pass_t<LOGM, false>(x, bhat, nvalid);
+      mid_pass_t<LOGM, false, NTH>(x, bhat, nvalid);
     __syncthreads();
   } else {
     constexpr int LR = (P == 0 && LOGM % 4 != 0) ? LOGM % 4 : 4;
     if (P == 0 && nvalid < F::M)
-      dif_pass_t<LOGM, LR, S, true>(x, tw, nvalid);
+      dif_pass_t<LOGM, LR, S, true, NTH>(x, tw, nvalid);
     else
-      dif_pass_t<LOGM, LR, S, false>(x, tw, nvalid);
+      dif_pass_t<LOGM, LR, S, false, NTH>(x, tw, nvalid);
     __syncthreads();
-    bluestein_rec<LOGM, P + 1, (S >> LR)>(x, bhat, tw, nvalid);
-    dit_pass_t<LOGM, LR, S>(x, tw);
+    bluestein_rec<LOGM, P + 1, (S >> LR), NTH>(x, bhat, tw, nvalid);
+    dit_pass_t<LOGM, LR, S, NTH>(x, tw);
     __syncthreads();
   }
 }
 
-// bluestein_core for a compile-time size (LOGM >= 4), blockDim.x == FftShape<LOGM>::NT
-template <int LOGM>
+// bluestein_core for a compile-time size (LOGM >= 4), blockDim.x == FftShape<LOGM, NTH>::NT
+template <int LOGM, int NTH = 0>
 __device__ __forceinline__ void bluestein_t(double2* x, const FftTables& T, const TwSm& tw,
                                             int nvalid) {
-  bluestein_rec<LOGM, 0, (1 << LOGM)>(x, T.bhat, tw, nvalid);
+  bluestein_rec<LOGM, 0, (1 << LOGM), NTH>(x, T.bhat, tw, nvalid);
 }
 
 // ----------------------------------------------------------------------------

@@ -88,6 +88,9 @@ struct AxisDev {
   //   synthesize  y_I = F^H b + P_I a,  y[bord] = (F^H b)[wrap] + P[bord] a
   // with coefficient l of a stored at element l (l < kl) or m + l (l >= kl).
   int hob, kr, hk;
+  // closed form of the border columns for the pair kernels (fd_pair.cuh):
+  //   P[l][e] = L_{l+1}(t_e) ho_s[l],  t_e = ho_ta e + ho_tb  (Legendre)
+  double ho_ta, ho_tb, ho_s[kHoMax];
   const double* P;
   double sinv[kHoMax * kHoMax];
   int bord[kHoMax], wrap[kHoMax];

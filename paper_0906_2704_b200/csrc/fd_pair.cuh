@@ -1,0 +1,318 @@
+// Two real lines per complex Bluestein DFT of the full interior length m:
+// the real-data path of the higher-order borders (AxisDev::hob), whose
+// interior length m = n - d is odd for even n (d = 1, 3), so the half-length
+// R2C split of k_ranalyze / k_rsynth does not apply.
+//
+//   analyze    (oracle ho_analyze):  a = S^-1 (y[bord] - y[kl + wrap]) per line,
+//              z = (y0_I - P_I a0) + i (y1_I - P_I a1),  Z = DFT_m(z),
+//              X0_k = (Z_k + conj Z_{m-k}) / 2,  X1_k = (Z_k - conj Z_{m-k}) / 2i
+//   synthesize (oracle ho_synthesize): v = X0 + i X1 over all m (X_{m-k} = conj X_k),
+//              y0 + i y1 = F^H v,  y_I += P_I a,  y[bord] = y[kl + wrap] + P[bord] a
+//
+// Persistent CTAs (one per SM at m ~ 4096: 139 KB buffer + 64 KB chirp),
+// each streaming line pairs; the next pair's 2n doubles are bulk-copied (TMA
+// engine, mbarrier completion) into the upper half of the FFT buffer, free
+// from the end of the convolution to the next load phase.
+//
+// Coefficients of real data are stored Hermitian-packed, n doubles per line
+// (io.pack == 2):  [a_0 .. a_{k-1}, X_0, Re X_1, Im X_1, .., Re X_h, Im X_h],
+// h = (m-1)/2; the GCV weights |ghat|^2 (Hermitian pairs pre-summed, reduced
+// order of build_pairs) and their TF32 screen tiles are written alongside.
+// The border columns enter as one cubic per line in t_e = ho_ta e + ho_tb
+// (the Legendre closed form of the P table).
+#pragma once
+
+namespace fdb {
+
+template <int LOGM>
+struct PairShape {
+  static constexpr int M = 1 << LOGM;
+  static constexpr int NT = M / 16 >= 512 ? 512 : (M / 16 <= 64 ? 64 : M / 16);
+};
+
+// smem slots (double2) of the pair kernels: buffer, twiddles, chirp, mbarrier
+__host__ __device__ __forceinline__ int pair_slots(int M, int m) {
+  return pidx(M) + 1 + kTwSlots + m + 1;
+}
+
+// sum_l a_l P_l(t) as a cubic in t (P_1 = t, P_2 = (3t^2-1)/2, P_3 = (5t^3-3t)/2)
+struct Cubic {
+  double c0, c1, c2, c3;
+  __device__ __forceinline__ double operator()(double t) const {
+    return fma(fma(fma(c3, t, c2), t, c1), t, c0);
+  }
+};
+__device__ __forceinline__ Cubic ho_cubic(const AxisDev& ax, const double (&a)[kHoMax]) {
+  const double b0 = ax.hk > 0 ? a[0] * ax.ho_s[0] : 0.0;
+  const double b1 = ax.hk > 1 ? a[1] * ax.ho_s[1] : 0.0;
+  const double b2 = ax.hk > 2 ? a[2] * ax.ho_s[2] : 0.0;
+  return Cubic{-0.5 * b1, b0 - 1.5 * b2, 1.5 * b1, 2.5 * b2};
+}
+
+// a = sinv (y[bord] - y[kl + wrap]) of one real line
+template <class LD>
+__device__ __forceinline__ void ho_amps_real(const AxisDev& ax, LD ld, double (&a)[kHoMax]) {
+  double r[kHoMax];
+#pragma unroll
+  for (int l = 0; l < kHoMax; ++l) r[l] = l < ax.hk ? ld(ax.bord[l]) - ld(ax.kl + ax.wrap[l]) : 0.0;
+#pragma unroll
+  for (int l = 0; l < kHoMax; ++l) {
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < kHoMax; ++q) v += ax.sinv[l * kHoMax + q] * r[q];
+    a[l] = v;
+  }
+}
+
+// reduced GCV index of border amplitude l (build_pairs: left singles, interior
+// groups 0..h, right singles)
+__device__ __forceinline__ int ho_wred(const AxisDev& ax, int l, int h) {
+  return l < ax.kl ? l : ax.kl + h + 1 + (l - ax.kl);
+}
+
+struct PairStage {
+  double* buf;
+  uint64_t* bar;
+  bool on;
+  uint32_t phase;
+};
+
+// staging needs contiguous lines (item stride n, unit element stride) and the
+// two lines to fit between the interior and the end of the buffer
+__device__ __forceinline__ PairStage pair_stage_init(double2* x, int M, int m, int n,
+                                                     const Lines& g, uint64_t* bar) {
+  PairStage s;
+  s.buf = reinterpret_cast<double*>(x + pidx(m) + 1);
+  s.bar = bar;
+  s.phase = 0;
+  s.on = g.elem_stride == 1 && g.per_item == 1 && g.item_stride == n &&
+         (long long)(pidx(M) - pidx(m) - 1) >= (long long)n;
+  if (threadIdx.x == 0 && s.on) {
+    mbar_init(s.bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  return s;
+}
+__device__ __forceinline__ bool pair_staged(const PairStage& s, const void* base, const Lines& g,
+                                            int q) {
+  if (!s.on || 2 * q + 1 >= g.count) return false;  // full pairs only
+  const double* src = reinterpret_cast<const double*>(base) + line_offset(g, 2 * q);
+  return (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+}
+__device__ __forceinline__ void pair_issue(PairStage& s, const void* base, const Lines& g, int q,
+                                           int n) {
+  if (!pair_staged(s, base, g, q)) return;
+  const double* src = reinterpret_cast<const double*>(base) + line_offset(g, 2 * q);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_expect_tx(s.bar, (uint32_t)n * 16);
+  bulk_g2s(s.buf, src, (uint32_t)n * 16, s.bar);
+}
+
+template <int LOGM>
+__global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax, LineIO io) {
+  constexpr int NT = PairShape<LOGM>::NT, M = 1 << LOGM;
+  extern __shared__ double2 sm[];
+  const FftTables& T = ax.fft;
+  const int m = ax.m, n = ax.n, kl = ax.kl, hk = ax.hk, h = (m - 1) / 2;
+  double2* x = sm;
+  double2* slots = sm + pidx(M) + 1;
+  const TwSm tw = load_twiddles(slots, T);
+  double2* cs = slots + kTwSlots;
+  for (int j = threadIdx.x; j < m; j += NT) cs[j] = T.chirp[j];
+  PairStage stg = pair_stage_init(x, M, m, n, io.gi,
+                                  reinterpret_cast<uint64_t*>(sm + pair_slots(M, m) - 1));
+  __syncthreads();
+  const int count = io.gi.count, npairs = (count + 1) / 2;
+  if (threadIdx.x == 0) pair_issue(stg, io.in, io.gi, blockIdx.x, n);
+  const double* in = reinterpret_cast<const double*>(io.in);
+  double* out = reinterpret_cast<double*>(io.out);
+  const long long es = io.gi.elem_stride;
+  const double isq = ax.inv_sqrt_m;
+  const long long nkb32 = io.wstride >> 5;
+  for (int q = blockIdx.x; q < npairs; q += gridDim.x) {
+    const int l0 = 2 * q;
+    const bool has1 = l0 + 1 < count;
+    const bool st = pair_staged(stg, io.in, io.gi, q);
+    if (st) {
+      mbar_wait(stg.bar, stg.phase);
+      stg.phase ^= 1;
+    }
+    const double* g0 = in + line_offset(io.gi, l0);
+    const double* g1 = has1 ? in + line_offset(io.gi, l0 + 1) : g0;
+    const double* s0 = stg.buf;
+    const double* s1 = stg.buf + n;
+    double a0[kHoMax], a1[kHoMax];
+    Cubic p0, p1;
+    auto load_phase = [&](auto ld0, auto ld1) {
+      ho_amps_real(ax, ld0, a0);
+      ho_amps_real(ax, ld1, a1);
+      p0 = ho_cubic(ax, a0);
+      p1 = ho_cubic(ax, a1);
+#pragma unroll 4
+      for (int j = threadIdx.x; j < m; j += NT) {
+        const int e = kl + j;
+        const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
+        x[pidx(j)] = cmul(make_double2(ld0(e) - p0(t), ld1(e) - p1(t)), cs[j]);
+      }
+    };
+    if (st)
+      load_phase([&](int e) { return s0[e]; }, [&](int e) { return s1[e]; });
+    else
+      load_phase([&](int e) { return __ldg(g0 + e * es); },
+                 [&](int e) { return has1 ? __ldg(g1 + e * es) : 0.0; });
+    __syncthreads();
+    bluestein_t<LOGM, NT>(x, T, tw, m);
+    // the post phase reads [0, m) only: stage the next pair behind it
+    if (threadIdx.x == 0) pair_issue(stg, io.in, io.gi, q + gridDim.x, n);
+
+    double* o0 = out + line_offset(io.go, l0);
+    double* o1 = has1 ? out + line_offset(io.go, l0 + 1) : nullptr;
+    double* w0 = io.wout ? io.wout + (long long)l0 * io.wstride : nullptr;
+    auto wset = [&](int line, double* wl, long long i, double v) {
+      wl[i] = v;
+      if (io.wout32) {
+        float hi, lo;
+        tf32_split(v, hi, lo);
+        const long long t = tc_tile_index(line, i, kTcBM, nkb32);
+        io.wout32[t] = hi;
+        io.wout32lo[t] = lo;
+      }
+    };
+    double* w1 = (w0 && has1) ? w0 + io.wstride : nullptr;
+    for (int kk = threadIdx.x; kk <= h; kk += NT) {
+      const double2 Zk = cmul(x[pidx(kk)], cs[kk]);
+      const double2 Zc = kk ? cmul(x[pidx(m - kk)], cs[m - kk]) : Zk;
+      const double2 X0 = cscale(cadd(Zk, cconj(Zc)), 0.5 * isq);
+      const double2 D = csub(Zk, cconj(Zc));
+      const double2 X1 = make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
+      if (kk == 0) {
+        o0[hk] = X0.x;
+        if (o1) o1[hk] = X1.x;
+      } else {
+        o0[hk + 2 * kk - 1] = X0.x;
+        o0[hk + 2 * kk] = X0.y;
+        if (o1) {
+          o1[hk + 2 * kk - 1] = X1.x;
+          o1[hk + 2 * kk] = X1.y;
+        }
+      }
+      if (w0) {
+        const double f = kk ? 2.0 : 1.0;  // |X_k|^2 + |X_{m-k}|^2
+        wset(l0, w0, kl + kk, f * (X0.x * X0.x + X0.y * X0.y));
+        if (w1) wset(l0 + 1, w1, kl + kk, f * (X1.x * X1.x + X1.y * X1.y));
+      }
+    }
+    if (threadIdx.x < hk) {
+      const int l = threadIdx.x;
+      o0[l] = a0[l];
+      if (o1) o1[l] = a1[l];
+      if (w0) {
+        wset(l0, w0, ho_wred(ax, l, h), a0[l] * a0[l]);
+        if (w1) wset(l0 + 1, w1, ho_wred(ax, l, h), a1[l] * a1[l]);
+      }
+    }
+    if (w0)
+      for (long long i = io.wn + threadIdx.x; i < io.wstride; i += NT) {
+        wset(l0, w0, i, 0.0);
+        if (w1) wset(l0 + 1, w1, i, 0.0);
+      }
+    __syncthreads();  // x is reused by the next pair
+  }
+}
+
+template <int LOGM>
+__global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_psynth(AxisDev ax, LineIO io,
+                                                                   SynthArgs sa) {
+  constexpr int NT = PairShape<LOGM>::NT, M = 1 << LOGM;
+  extern __shared__ double2 sm[];
+  const FftTables& T = ax.fft;
+  const int m = ax.m, n = ax.n, kl = ax.kl, hk = ax.hk, h = (m - 1) / 2;
+  double2* x = sm;
+  double2* slots = sm + pidx(M) + 1;
+  const TwSm tw = load_twiddles(slots, T);
+  double2* cs = slots + kTwSlots;
+  for (int j = threadIdx.x; j < m; j += NT) cs[j] = T.chirp[j];
+  PairStage stg = pair_stage_init(x, M, m, n, io.gi,
+                                  reinterpret_cast<uint64_t*>(sm + pair_slots(M, m) - 1));
+  __syncthreads();
+  const int count = io.gi.count, npairs = (count + 1) / 2;
+  if (threadIdx.x == 0) pair_issue(stg, io.in, io.gi, blockIdx.x, n);
+  const double* in = reinterpret_cast<const double*>(io.in);
+  double* out = reinterpret_cast<double*>(io.out);
+  const double isq = ax.inv_sqrt_m;
+  for (int q = blockIdx.x; q < npairs; q += gridDim.x) {
+    const int l0 = 2 * q;
+    const bool has1 = l0 + 1 < count;
+    const bool st = pair_staged(stg, io.in, io.gi, q);
+    if (st) {
+      mbar_wait(stg.bar, stg.phase);
+      stg.phase ^= 1;
+    }
+    const double* g0 = in + line_offset(io.gi, l0);
+    const double* g1 = has1 ? in + line_offset(io.gi, l0 + 1) : g0;
+    const double mu0 = line_mu(sa, io.gi, l0);
+    const double mu1 = has1 ? line_mu(sa, io.gi, l0 + 1) : mu0;
+    auto f0 = [&](int e, double2 c) { return coeff_filter_fast(ax, sa, io.gi, l0, e, c, mu0); };
+    auto f1 = [&](int e, double2 c) {
+      return has1 ? coeff_filter_fast(ax, sa, io.gi, l0 + 1, e, c, mu1) : czero();
+    };
+    double ua0[kHoMax], ua1[kHoMax];
+    auto load_phase = [&](auto ld0, auto ld1) {
+#pragma unroll
+      for (int l = 0; l < kHoMax; ++l) {
+        ua0[l] = l < hk ? f0(ho_coef_elem(ax, l), make_double2(ld0(l), 0.0)).x : 0.0;
+        ua1[l] = l < hk ? f1(ho_coef_elem(ax, l), make_double2(ld1(l), 0.0)).x : 0.0;
+      }
+#pragma unroll 2
+      for (int kk = threadIdx.x; kk <= h; kk += NT) {
+        const int e = kl + kk;
+        double2 X0, X1;
+        if (kk == 0) {
+          X0 = make_double2(ld0(hk), 0.0);
+          X1 = make_double2(ld1(hk), 0.0);
+        } else {
+          X0 = make_double2(ld0(hk + 2 * kk - 1), ld0(hk + 2 * kk));
+          X1 = make_double2(ld1(hk + 2 * kk - 1), ld1(hk + 2 * kk));
+        }
+        X0 = f0(e, X0);
+        X1 = f1(e, X1);
+        // F^H v = conj(F conj v): Bluestein input conj(v_k) c_k, v = X0 + i X1
+        x[pidx(kk)] = cmul(make_double2(X0.x - X1.y, -(X0.y + X1.x)), cs[kk]);
+        if (kk) x[pidx(m - kk)] = cmul(make_double2(X0.x + X1.y, X0.y - X1.x), cs[m - kk]);
+      }
+    };
+    if (st)
+      load_phase([&](int i) { return stg.buf[i]; }, [&](int i) { return stg.buf[n + i]; });
+    else
+      load_phase([&](int i) { return __ldg(g0 + i); },
+                 [&](int i) { return has1 ? __ldg(g1 + i) : 0.0; });
+    __syncthreads();
+    bluestein_t<LOGM, NT>(x, T, tw, m);
+    if (threadIdx.x == 0) pair_issue(stg, io.in, io.gi, q + gridDim.x, n);
+
+    const Cubic p0 = ho_cubic(ax, ua0), p1 = ho_cubic(ax, ua1);
+    const long long eso = io.go.elem_stride;
+    double* o0 = out + line_offset(io.go, l0);
+    double* o1 = has1 ? out + line_offset(io.go, l0 + 1) : nullptr;
+#pragma unroll 4
+    for (int p = threadIdx.x; p < m; p += NT) {
+      const double2 z = cmul(x[pidx(p)], cs[p]);  // conj of (F^H v)_p sqrt(m)
+      const double y0 = z.x * isq, y1 = -z.y * isq;
+      const int e = kl + p;
+      const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
+      o0[e * eso] = y0 + p0(t);
+      if (o1) o1[e * eso] = y1 + p1(t);
+#pragma unroll
+      for (int l = 0; l < kHoMax; ++l)
+        if (l < hk && ax.wrap[l] == p) {
+          const int eb = ax.bord[l];
+          const double tb = fma((double)eb, ax.ho_ta, ax.ho_tb);
+          o0[eb * eso] = y0 + p0(tb);
+          if (o1) o1[eb * eso] = y1 + p1(tb);
+        }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace fdb

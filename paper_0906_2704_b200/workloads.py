@@ -29,6 +29,7 @@ from dataclasses import dataclass
 import numpy as np
 
 PERIODIC, REFLECTIVE, ANTIREFLECTIVE, HOC_COSINE, HOC_FOURIER = range(5)
+HOC_FOURIER_D1, HOC_FOURIER_D3 = 5, 6  # extension codes (include/fastdeblur_b200.h)
 IDENTITY, LAPLACIAN, FIRST_DIFFERENCE = range(3)
 
 _GOLD = np.uint64(0x9E3779B97F4A7C15)
