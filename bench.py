@@ -5,10 +5,13 @@
                     [--config 1] [--items B]
 
 Metric (BASELINE.json): Mpixels/s per Tikhonov+GCV restoration (fp64).
-A step is one deblur (GCV select + Tikhonov solve, pipeline.cpp:732-768) of the
-whole batch of the configuration; default workload is config 1 (65,536
-signals of n = 4096 per GPU; hoc-fourier = the reference's degree-2 BC for a
-nonsymmetric PSF; first-difference smoother; 256 lambda in [1e-8, 1]).
+A step restores the whole batch of the configuration (deblur = GCV select +
+Tikhonov solve, pipeline.cpp:732-768) once per (boundary condition, smoother)
+the config names; default workload is config 1 (65,536 signals of n = 4096 per
+GPU, nonsymmetric PSF, BC degrees d = 1 and d = 3 -- the higher-order Fourier
+borders, an extension the reference lacks -- first-difference smoother, 256
+lambda in [1e-8, 1]): two restorations per step.  The reference arm runs its
+own nearest BC (hoc-fourier, d = 2) on the same signals.
 Scaling is weak: every rank restores its own seeded batch (items offset by
 rank), no data-path collective; the step time is the max over ranks.
 
@@ -55,19 +58,20 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--items", type=int, default=0, help="override the per-rank batch")
-    ap.add_argument("--bc", default=None, help="override the config's boundary condition "
-                    "(name, e.g. hoc-fourier-d1)")
+    ap.add_argument("--bc", default=None, help="override the boundary conditions a step "
+                    "restores with (comma-separated names, e.g. hoc-fourier-d1,hoc-fourier-d3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
 
-def workload_name(cfg, batch):
+def workload_name(cfg, batch, bcs=None):
     if cfg.dim == 1:
         shape = f"{batch}x{cfg.n1} 1D"
     else:
         shape = f"{batch}x{cfg.n1}x{cfg.n2} 2D"
-    return (f"config{cfg.index}: {shape} fp64, {BC_NAMES[cfg.bc]}, "
+    bcs = bcs or (cfg.bc,)
+    return (f"config{cfg.index}: {shape} fp64, {' + '.join(BC_NAMES[b] for b in bcs)}, "
             f"{'/'.join(SMOOTHER_NAMES[s] for s in cfg.smoothers)} smoother, GCV {cfg.count} "
             f"lambda in [{cfg.mu_min:g},{cfg.mu_max:g}]")
 
@@ -145,9 +149,12 @@ def run_reference_arm(args, cfg, cores):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, workloads.py)",
-        "config": {"workload": workload_name(cfg, cfg.batch), "sample_items_per_step": per_step},
+        "config": {"workload": workload_name(cfg, cfg.batch, cfg.step_bcs),
+                   "sample_items_per_step": per_step, "reference_bc": BC_NAMES[cfg.bc],
+                   "note": cfg.note},
         "cpu_baseline": {"value": value, "unit": "Mpixels/s", "cores": used, "kind": kind,
-                         "sample": f"{per_step} items of config {cfg.index} per step"},
+                         "sample": f"{per_step} items of config {cfg.index} per step, "
+                                   f"restored at {BC_NAMES[cfg.bc]}"},
         "e2e": {"value": value, "unit": "Mpixels/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -294,6 +301,12 @@ def bluestein_flops_per_line(n, bc):
     """Algorithmic fp64 flops of one real line through the half-length Bluestein
     transform: two complex FFTs of M points (5 M log2 M each), the pointwise
     product with DIF(b)/M (6 M) and the two chirp products (6 h each)."""
+    if bc in (W.HOC_FOURIER_D1, W.HOC_FOURIER_D3):  # pair kernels: full-length DFT per 2 lines
+        m = n - (1 if bc == W.HOC_FOURIER_D1 else 3)
+        M = 1
+        while M < 2 * m - 1:
+            M *= 2
+        return (2 * 5 * M * math.log2(M) + 6 * M + 12 * m) / 2
     m = n if bc in (W.PERIODIC, W.REFLECTIVE) else n - 2
     h = m + 1 if bc == W.ANTIREFLECTIVE else m // 2
     M = 1
@@ -318,8 +331,10 @@ def main():
     cfg = W.config(args.config)
     if args.bc is not None:
         import dataclasses
-        code = {v: k for k, v in BC_NAMES.items()}[args.bc]
-        cfg = dataclasses.replace(cfg, bc=code, note=f"bc overridden to {args.bc}")
+        codes = tuple({v: k for k, v in BC_NAMES.items()}[b] for b in args.bc.split(","))
+        ref_bc = codes[0] if codes[0] <= W.HOC_FOURIER else cfg.bc
+        cfg = dataclasses.replace(cfg, bc=ref_bc, bcs=codes,
+                                  note=f"bc overridden to {args.bc}")
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     # reference threads: batched configs run an outer pool over
     # items with serial inner loops; single-item configs use the library's own
@@ -341,7 +356,6 @@ def main():
 
     batch = args.items or cfg.batch
     first = rank * batch
-    smoother = cfg.smoothers[0]
     dev = torch.device("cuda", local)
     # ---- inputs (host generation, pinned) ----
     if cfg.dim == 1:
@@ -355,7 +369,7 @@ def main():
                                  mp_context=mp.get_context("fork")) as ex:
             for (ci, s0, c), arr in zip(jobs, ex.map(_gen_1d, jobs)):
                 g_host[s0 - first:s0 - first + c] = torch.from_numpy(arr)
-        op = P.build_operator(cfg.psf, cfg.n1, cfg.bc)
+        ops = [P.build_operator(cfg.psf, cfg.n1, b) for b in cfg.step_bcs]
     else:
         shape = (batch, cfg.n1, cfg.n2)
         g_host = torch.empty(shape, dtype=torch.float64).pin_memory()
@@ -370,17 +384,23 @@ def main():
                                  mp_context=mp.get_context("fork")) as ex:
             for (ci, it), arr in zip(jobs, ex.map(_gen_2d, jobs)):
                 g_host[it - first] = torch.from_numpy(arr)
-        op = P.build_operator_2d_separable(cfg.psf, cfg.psf, cfg.n1, cfg.n2, cfg.bc)
-    L = P.smoothing_eigenvalues(SMOOTHER_NAMES[smoother], op)
+        ops = [P.build_operator_2d_separable(cfg.psf, cfg.psf, cfg.n1, cfg.n2, b)
+               for b in cfg.step_bcs]
+    # one restoration per (boundary condition, smoother) of the config
+    rest = [(op, P.smoothing_eigenvalues(SMOOTHER_NAMES[sm], op)) for op in ops
+            for sm in cfg.smoothers]
+    labels = [f"{BC_NAMES[b]}/{SMOOTHER_NAMES[sm]}" for b in cfg.step_bcs for sm in cfg.smoothers]
+    R_ = len(rest)
     g_dev = g_host.to(dev)
-    out_dev = torch.empty_like(g_dev)
+    outs = [torch.empty_like(g_dev) for _ in range(R_)]
     search = P.GcvSearch(cfg.mu_min, cfg.mu_max, cfg.count)
     choice = P.MuChoice(use_gcv=True)
     px_rank = int(np.prod(shape))
     stream = torch.cuda.current_stream()
 
     def step():
-        return P.deblur(op, L, g_dev, choice, search=search, out=out_dev)
+        return [P.deblur(op, L, g_dev, choice, search=search, out=o)
+                for (op, L), o in zip(rest, outs)]
 
     for _ in range(args.warmup):
         rep = step()
@@ -405,18 +425,18 @@ def main():
     launches = FD.kernel_launches() - launches0
     ms_step = dist.max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
     prof = collect_profile(FD)
-    total_px = px_rank * world
+    total_px = px_rank * world * R_  # restored pixels per step (all ranks, all BCs)
     value = total_px / (ms_step / 1e3) / 1e6
 
     # ---- e2e through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
-        out_host = torch.empty(shape, dtype=torch.float64).pin_memory()
-        mu_host = torch.empty(shape[0], dtype=torch.float64).pin_memory()
+        out_hosts = [torch.empty(shape, dtype=torch.float64).pin_memory() for _ in range(R_)]
         e_steps = max(1, min(args.steps, 5))
 
         def e2e_step():  # public host-buffer API: chunked H2D | deblur | D2H pipeline
-            P.deblur_host(op, L, g_host, choice, search=search, out=out_host)
+            for (op, L), o in zip(rest, out_hosts):
+                P.deblur_host(op, L, g_host, choice, search=search, out=o)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -429,8 +449,8 @@ def main():
         torch.cuda.synchronize()
         e_ms = dist.max_over_ranks(a.elapsed_time(b) / e_steps)
         e2e = {"value": total_px / (e_ms / 1e3) / 1e6, "unit": "Mpixels/s",
-               "ms_per_step": e_ms, "h2d_bytes_per_step": px_rank * 8,
-               "d2h_bytes_per_step": px_rank * 8 + shape[0] * 8}
+               "ms_per_step": e_ms, "h2d_bytes_per_step": R_ * px_rank * 8,
+               "d2h_bytes_per_step": R_ * (px_rank * 8 + shape[0] * 8)}
 
     # ---- roofline of the dominant kernel ----
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -448,7 +468,7 @@ def main():
         bpp = alg_bytes_per_px(dom, cfg)
         launches_per_step = cnt / args.steps
         if bpp is not None:
-            bytes_launch = bpp * px_rank / launches_per_step
+            bytes_launch = bpp * px_rank * R_ / launches_per_step
             achieved = bytes_launch / (avg_ms / 1e3) / 1e9
             traffic, tsrc = ncu_traffic(dom, cfg)
             roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak,
@@ -464,19 +484,22 @@ def main():
         fdom = max(fft_kernels, key=lambda k: prof[k][0])
         ms_tot, cnt = prof[fdom]
         # per step: every line of length n1 (1D; 2D column pass) and n2 (2D row pass)
-        fl_step = bluestein_flops_per_line(cfg.n1, cfg.bc) * px_rank / cfg.n1
-        if cfg.dim == 2:
-            fl_step += bluestein_flops_per_line(cfg.n2, cfg.bc) * px_rank / cfg.n2
+        fl_step = 0.0
+        for b in cfg.step_bcs:
+            fl_step += bluestein_flops_per_line(cfg.n1, b) * px_rank / cfg.n1
+            if cfg.dim == 2:
+                fl_step += bluestein_flops_per_line(cfg.n2, b) * px_rank / cfg.n2
         fl = fl_step * args.steps / cnt  # per launch
         tf = fl / (ms_tot / cnt / 1e3) / 1e12
         pk, pks = fp64_peak()
         croof = {"kernel": fdom, "bound": "fp64", "achieved": tf, "peak": pk, "unit": "TFLOP/s",
                  "frac": tf / pk, "peak_source": pks,
                  "alg_flops_per_launch": fl,
-                 "model": "2 x 5 M log2 M + 6 M + 12 h per line (half-length Bluestein)"}
-    pipeline_bytes = 16 * px_rank  # read g + write f
+                 "model": "2 x 5 M log2 M + 6 M + 12 h per line (half-length Bluestein; "
+                          "per pair of lines for the full-length pair kernels)"}
+    pipeline_bytes = 16 * px_rank * R_  # read g + write f
     if cfg.dim == 2 and cfg.batch == 1:
-        pipeline_bytes = 56 * px_rank  # 7-touch out-of-core model (config 2)
+        pipeline_bytes = 56 * px_rank * R_  # 7-touch out-of-core model (config 2)
 
     # ---- CPU baseline (rank 0, N = 1 only) ----
     cpu = None
@@ -487,21 +510,26 @@ def main():
             px = n_items * cfg.n1 * (cfg.n2 if cfg.dim == 2 else 1)
             cpu = {"value": px / dt / 1e6, "unit": "Mpixels/s", "cores": used, "kind": kind,
                    "sample": f"deblur of {n_items} items of config {cfg.index} "
-                             f"({px} pixels), {dt:.2f} s wall"}
+                             f"({px} pixels) at {BC_NAMES[cfg.bc]}, {dt:.2f} s wall"}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "Mpixels/s", "cores": cores, "kind": "unavailable",
                    "sample": f"failed: {e}"}
 
     if rank == 0:
-        mu = rep.mu_used.detach().cpu().numpy()
-        bk = rep.best_k.detach().cpu().numpy()
+        gcv = {}
+        for lab, r in zip(labels, rep):
+            mu = r.mu_used.detach().cpu().numpy()
+            bk = r.best_k.detach().cpu().numpy()
+            gcv[lab] = {"best_k_range": [int(bk.min()), int(bk.max())],
+                                "mu_median": float(np.median(mu))}
         line = {
             "metric": METRIC, "value": value, "unit": "Mpixels/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded SplitMix64 scenes, true-extended blur + add_noise)",
-            "config": {"workload": workload_name(cfg, batch), "items_per_gpu": batch,
-                       "pixels_per_gpu": px_rank,
+            "config": {"workload": workload_name(cfg, batch, cfg.step_bcs),
+                       "items_per_gpu": batch, "pixels_per_gpu": px_rank,
+                       "restorations_per_step": R_,
                        "l2": "inputs larger than L2 (no flush needed)" if px_rank * 8 > 126e6
                        else "inputs L2-resident between steps", "parallelism": f"items x{world}",
                        "note": cfg.note},
@@ -510,8 +538,7 @@ def main():
                              "achieved_gbs": pipeline_bytes / (ms_step / 1e3) / 1e9,
                              "frac": pipeline_bytes / (ms_step / 1e3) / 1e9 / peak},
             "kernels": kernels, "compute_roofline": croof, "cpu_baseline": cpu,
-            "gcv": {"best_k_range": [int(bk.min()), int(bk.max())],
-                    "mu_median": float(np.median(mu))},
+            "gcv": gcv,
         }
         print(json.dumps(line), flush=True)
     dist.finalize()

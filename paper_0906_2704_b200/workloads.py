@@ -140,6 +140,14 @@ class Config:
     blobs: int = 0
     rects: int = 0
     note: str = ""
+    # boundary conditions a bench step restores with (each with every
+    # smoother); () = (bc,).  ``bc`` stays the reference-supported BC (the
+    # reference arm and the golden fixtures use it).
+    bcs: tuple = ()
+
+    @property
+    def step_bcs(self):
+        return self.bcs or (self.bc,)
 
     @property
     def pixels(self):
@@ -158,16 +166,21 @@ def config(index: int) -> Config:
     if index == 1:
         return Config(1, 1, 4096, 1, 65536, onesided_exp_weights(15, 1 / 5), HOC_FOURIER,
                       (FIRST_DIFFERENCE,), 1e-8, 1.0, 256, 0.005,
-                      note="d=1/d=3 with a nonsymmetric PSF are not in the reference; "
-                           "run at d=2 (hoc-fourier)")
+                      bcs=(HOC_FOURIER_D1, HOC_FOURIER_D3),
+                      note="d=1 and d=3 with a nonsymmetric PSF are extensions (not in the "
+                           "reference): a step restores the batch at both degrees; the "
+                           "reference arm runs its nearest BC, hoc-fourier (d=2)")
     if index == 2:
         return Config(2, 2, 4096, 4096, 1, gaussian_weights(12, 2.5), HOC_COSINE, (LAPLACIAN,),
                       1e-6, 1.0, 128, 0.01, blobs=40, rects=10)
     if index == 3:
         return Config(3, 2, 1024, 1024, 512, onesided_exp_weights(11, 1 / 4), HOC_FOURIER,
                       (IDENTITY, LAPLACIAN), 1e-6, 1.0, 128, 0.01, blobs=40, rects=10,
-                      note="d=3 is not in the reference; run at d=2 (hoc-fourier); "
-                           "lambda range unspecified, [1e-6, 1] used")
+                      bcs=(HOC_FOURIER_D3,),
+                      note="d=3 is an extension (not in the reference): a step restores the "
+                           "batch with the identity and the Laplacian smoother; the reference "
+                           "arm runs its nearest BC, hoc-fourier (d=2); lambda range "
+                           "unspecified, [1e-6, 1] used")
     if index == 4:
         return Config(4, 2, 16384, 16384, 1, gaussian_weights(16, 4.0), HOC_COSINE,
                       (LAPLACIAN,), 1e-8, 1.0, 512, 0.01, blobs=80, rects=20)
