@@ -387,20 +387,26 @@ def main():
         ops = [P.build_operator_2d_separable(cfg.psf, cfg.psf, cfg.n1, cfg.n2, b)
                for b in cfg.step_bcs]
     # one restoration per (boundary condition, smoother) of the config
-    rest = [(op, P.smoothing_eigenvalues(SMOOTHER_NAMES[sm], op)) for op in ops
-            for sm in cfg.smoothers]
-    labels = [f"{BC_NAMES[b]}/{SMOOTHER_NAMES[sm]}" for b in cfg.step_bcs for sm in cfg.smoothers]
+    rest = [(op, P.smoothing_eigenvalues(SMOOTHER_NAMES[sm], op), pr) for op in ops
+            for sm in cfg.smoothers for pr in cfg.precisions]
+    labels = [f"{BC_NAMES[b]}/{SMOOTHER_NAMES[sm]}/{pr}" for b in cfg.step_bcs
+              for sm in cfg.smoothers for pr in cfg.precisions]
     R_ = len(rest)
     g_dev = g_host.to(dev)
-    outs = [torch.empty_like(g_dev) for _ in range(R_)]
+    g_src = {"f64": g_dev}
+    g_hosts = {"f64": g_host}
+    if "f32" in cfg.precisions:
+        g_src["f32"] = g_dev.float()
+        g_hosts["f32"] = g_host.float().pin_memory()
+    outs = [torch.empty_like(g_src[pr]) for (_, _, pr) in rest]
     search = P.GcvSearch(cfg.mu_min, cfg.mu_max, cfg.count)
     choice = P.MuChoice(use_gcv=True)
     px_rank = int(np.prod(shape))
     stream = torch.cuda.current_stream()
 
     def step():
-        return [P.deblur(op, L, g_dev, choice, search=search, out=o)
-                for (op, L), o in zip(rest, outs)]
+        return [P.deblur(op, L, g_src[pr], choice, search=search, out=o)
+                for (op, L, pr), o in zip(rest, outs)]
 
     for _ in range(args.warmup):
         rep = step()
@@ -431,12 +437,13 @@ def main():
     # ---- e2e through the public API with host buffers ----
     e2e = None
     if not args.no_e2e:
-        out_hosts = [torch.empty(shape, dtype=torch.float64).pin_memory() for _ in range(R_)]
+        out_hosts = [torch.empty(shape, dtype=g_hosts[pr].dtype).pin_memory()
+                     for (_, _, pr) in rest]
         e_steps = max(1, min(args.steps, 5))
 
         def e2e_step():  # public host-buffer API: chunked H2D | deblur | D2H pipeline
-            for (op, L), o in zip(rest, out_hosts):
-                P.deblur_host(op, L, g_host, choice, search=search, out=o)
+            for (op, L, pr), o in zip(rest, out_hosts):
+                P.deblur_host(op, L, g_hosts[pr], choice, search=search, out=o)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -448,9 +455,10 @@ def main():
         b.record(stream)
         torch.cuda.synchronize()
         e_ms = dist.max_over_ranks(a.elapsed_time(b) / e_steps)
+        esz = sum(4 if pr == "f32" else 8 for (_, _, pr) in rest)
         e2e = {"value": total_px / (e_ms / 1e3) / 1e6, "unit": "Mpixels/s",
-               "ms_per_step": e_ms, "h2d_bytes_per_step": R_ * px_rank * 8,
-               "d2h_bytes_per_step": R_ * (px_rank * 8 + shape[0] * 8)}
+               "ms_per_step": e_ms, "h2d_bytes_per_step": esz * px_rank,
+               "d2h_bytes_per_step": esz * px_rank + R_ * shape[0] * 8}
 
     # ---- roofline of the dominant kernel ----
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -497,9 +505,9 @@ def main():
                  "alg_flops_per_launch": fl,
                  "model": "2 x 5 M log2 M + 6 M + 12 h per line (half-length Bluestein; "
                           "per pair of lines for the full-length pair kernels)"}
-    pipeline_bytes = 16 * px_rank * R_  # read g + write f
-    if cfg.dim == 2 and cfg.batch == 1:
-        pipeline_bytes = 56 * px_rank * R_  # 7-touch out-of-core model (config 2)
+    # read g + write f; 7-touch out-of-core model (config 2)
+    touches = 7 if (cfg.dim == 2 and cfg.batch == 1) else 2
+    pipeline_bytes = sum(touches * (4 if pr == "f32" else 8) for (_, _, pr) in rest) * px_rank
 
     # ---- CPU baseline (rank 0, N = 1 only) ----
     cpu = None
@@ -526,6 +534,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "Mpixels/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "storage": "+".join(cfg.precisions),
             "data": "synthetic (seeded SplitMix64 scenes, true-extended blur + add_noise)",
             "config": {"workload": workload_name(cfg, batch, cfg.step_bcs),
                        "items_per_gpu": batch, "pixels_per_gpu": px_rank,

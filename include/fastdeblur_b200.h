@@ -161,6 +161,26 @@ int fd_deblur_host(const fd_op* op, const fd_smoother* L, const double* g, int u
                    double* restored, double* mu_used, int* best_k, long long count,
                    long long chunk, void* stream);
 
+/* ---- fp32 storage variant (BASELINE config 3 "fp32 and fp64") ----
+ * The reference is double-only (trig.hpp:10).  These take float signals /
+ * images (and return float restorations); every transform, filter and GCV
+ * sum is still computed in fp64 and the coefficients stay fp64 in device
+ * memory, so the result is the fp64 restoration of the fp32 input rounded to
+ * fp32 (north_star fp32 parity bar: 1e-4 relative, identical best_k).  Real-line
+ * 1D fast paths (half-length / pair kernels) are fp64-only; fp32 1D runs the
+ * generic line kernels.  Arguments otherwise as fd_matvec / fd_deblur /
+ * fd_deblur_host. */
+int fd_matvec_f32(const fd_op* op, const float* f, float* out, double* imag_residue,
+                  long long count, void* stream);
+int fd_deblur_f32(const fd_op* op, const fd_smoother* L, const float* g, int use_gcv,
+                  double fixed_mu, double mu_min, double mu_max, int grid_count, float* restored,
+                  double* mu_used, int* best_k, double* curve, double* imag_residue,
+                  long long count, void* stream);
+int fd_deblur_host_f32(const fd_op* op, const fd_smoother* L, const float* g, int use_gcv,
+                       double fixed_mu, double mu_min, double mu_max, int grid_count,
+                       float* restored, double* mu_used, int* best_k, long long count,
+                       long long chunk, void* stream);
+
 /* The same selection logic the kernels run (gcv_minimize, regularize.cpp:281-351),
  * on the host with a caller-supplied G: for the CPU test suite. */
 typedef double (*fd_gcv_fn)(double mu, void* ctx);

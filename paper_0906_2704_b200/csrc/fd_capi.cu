@@ -358,7 +358,7 @@ void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
     launch_pair(ax, io, nullptr, st);
     return;
   }
-  if (!io.in_cplx && ax.rhalf) {  // one real line per CTA, half-length DFT
+  if (!io.in_cplx && ax.rhalf && !io.in_f32) {  // one real line per CTA, half-length DFT
     ProfScope ps("k_analyze", st);
     if (ax.hfft.M > kMaxOnChipM) {  // split convolution, persistent CTAs + scratch
       const int grid = std::min(io.gi.count, 2 * num_sms());
@@ -400,7 +400,7 @@ void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cuda
     launch_pair(ax, io, &sa, st);
     return;
   }
-  if (!io.out_cplx && ax.rhalf && (!ax.cplx || sa.resid2 == nullptr)) {
+  if (!io.out_cplx && ax.rhalf && !io.out_f32 && (!ax.cplx || sa.resid2 == nullptr)) {
     ProfScope ps(sa.mode == 1 ? "k_synth_filter" : "k_synth", st);
     if (ax.hfft.M > kMaxOnChipM) {
       const int grid = std::min(io.gi.count, 2 * num_sms());
@@ -954,10 +954,12 @@ cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 // analyze count items: in (real or complex) -> out (basis type)
 void run_analyze(const fd_op* op, const void* in, int in_cplx, void* out, long long count,
                  Scratch& S, double* wout = nullptr, long long wstride = 0, long long wn = 0,
-                 int pack = 0, float* wout32 = nullptr, float* wout32lo = nullptr) {
+                 int pack = 0, float* wout32 = nullptr, float* wout32lo = nullptr,
+                 int in_f32 = 0) {
   const int oc = op->cplx;
   if (op->dim == 1) {
     LineIO io{};
+    io.in_f32 = in_f32;
     io.pack = pack;
     io.in = in;
     io.out = out;
@@ -989,6 +991,7 @@ void run_analyze(const fd_op* op, const void* in, int in_cplx, void* out, long l
   rows.count = (int)(count * n1);
   LineIO a{};
   a.in = in;
+  a.in_f32 = in_f32;
   a.out = mid;
   a.gi = cols;
   a.go = cols;
@@ -1011,10 +1014,11 @@ void run_analyze(const fd_op* op, const void* in, int in_cplx, void* out, long l
 // one analysis, many mu -- the mu sweep)
 void run_synth(const fd_op* op, const fd_smoother* L, const void* in, void* out, int out_cplx,
                int mode, const double* mu_item, double* resid, long long count, Scratch& S,
-               int pack = 0, bool shared_in = false) {
+               int pack = 0, bool shared_in = false, int out_f32 = 0) {
   const int oc = op->cplx;
   if (op->dim == 1) {
     LineIO io{};
+    io.out_f32 = out_f32;
     io.pack = pack;
     io.in = in;
     io.out = out;
@@ -1075,6 +1079,7 @@ void run_synth(const fd_op* op, const fd_smoother* L, const void* in, void* out,
   LineIO b{};
   b.in = mid;
   b.out = out;
+  b.out_f32 = out_f32;
   b.gi = rows;
   b.go = rows;
   b.in_cplx = oc;
@@ -1123,12 +1128,13 @@ struct Analyzed {
 
 // want_full: keep the full complex coefficients (imaginary residue requested);
 // want_w32: also emit fp32 weights (tensor-core screen, see gcv_select_dev)
-Analyzed analyze_for_gcv(const fd_op* op, const fd_smoother* L, const double* g, long long count,
-                         Scratch& S, bool want_full = false, bool want_w32 = false) {
+Analyzed analyze_for_gcv(const fd_op* op, const fd_smoother* L, const void* g, long long count,
+                         Scratch& S, bool want_full = false, bool want_w32 = false,
+                         int in_f32 = 0) {
   Analyzed a;
   const bool pair = op->dim == 1 && pair_path(op->ax1->dev);
-  const bool use_w = op->dim == 1 && (op->ax1->dev.rhalf || (pair && !want_full)) &&
-                     (!op->cplx || L->pair);
+  const bool use_w = op->dim == 1 && !in_f32 &&
+                     (op->ax1->dev.rhalf || (pair && !want_full)) && (!op->cplx || L->pair);
   a.pack = use_w && op->cplx && !want_full ? (pair ? 2 : 1) : 0;
   a.ghat = (op->cplx && !a.pack) ? (void*)S.get<double2>(count * op->N())
                                  : (void*)S.get<double>(count * op->N());
@@ -1142,7 +1148,7 @@ Analyzed analyze_for_gcv(const fd_op* op, const fd_smoother* L, const double* g,
       a.w32lo = S.get<float>(rows * a.wstride);
     }
   }
-  run_analyze(op, g, 0, a.ghat, count, S, a.w, a.wstride, a.wn, a.pack, a.w32, a.w32lo);
+  run_analyze(op, g, 0, a.ghat, count, S, a.w, a.wstride, a.wn, a.pack, a.w32, a.w32lo, in_f32);
   return a;
 }
 
@@ -1763,12 +1769,13 @@ void check_deblur_args(const fd_op* op, const fd_smoother* L, int use_gcv, doubl
 
 // deblur (pipeline.cpp:732-768) of `count` device-resident items; a GCV
 // degeneracy is flagged in *status (checked by the caller after a sync).
-void deblur_dev(const fd_op* op, const fd_smoother* L, const double* g, int use_gcv,
+// f32: g and restored are float arrays (fp32 storage variant, fp64 arithmetic)
+void deblur_dev(const fd_op* op, const fd_smoother* L, const void* g, int use_gcv,
                 double fixed_mu, double mu_min, double mu_max, const DevGrid* dg,
-                double* restored, double* mu_used, int* best_k, double* curve,
-                double* imag_residue, long long count, int* status, Scratch& S) {
+                void* restored, double* mu_used, int* best_k, double* curve,
+                double* imag_residue, long long count, int* status, Scratch& S, int f32 = 0) {
   const bool w32 = use_gcv && !curve && count >= 32 && dg && dg->d.count <= 256 && screen_enabled();
-  const Analyzed an = analyze_for_gcv(op, L, g, count, S, imag_residue != nullptr, w32);
+  const Analyzed an = analyze_for_gcv(op, L, g, count, S, imag_residue != nullptr, w32, f32);
   if (use_gcv) {
     gcv_select_dev(op, L, an, count, *dg, mu_min, mu_max, mu_used, best_k, curve, status, S);
   } else {
@@ -1782,7 +1789,7 @@ void deblur_dev(const fd_op* op, const fd_smoother* L, const double* g, int use_
   }
   if (!op->cplx && imag_residue)
     ck(cudaMemsetAsync(imag_residue, 0, count * sizeof(double), S.st), "memset");
-  run_synth(op, L, an.ghat, restored, 0, 1, mu_used, imag_residue, count, S, an.pack);
+  run_synth(op, L, an.ghat, restored, 0, 1, mu_used, imag_residue, count, S, an.pack, false, f32);
 }
 
 void check_status(int* status, cudaStream_t st) {
@@ -2213,19 +2220,30 @@ int fd_synthesize(const fd_op* op, const void* in, void* out, int out_complex,
   });
 }
 
-int fd_matvec(const fd_op* op, const double* f, double* out, double* imag_residue, long long count,
-              void* stream) {
+namespace {
+int matvec_impl(const fd_op* op, const void* f, void* out, double* imag_residue, long long count,
+                void* stream, int f32) {
   return guarded([&] {
     check_op(op);
     if (count < 0) validation("negative count");
     if (count == 0) return;
     Scratch S(as_stream(stream));
     void* c = op->cplx ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
-    run_analyze(op, f, 0, c, count, S);
+    run_analyze(op, f, 0, c, count, S, nullptr, 0, 0, 0, nullptr, nullptr, f32);
     if (!op->cplx && imag_residue)
       ck(cudaMemsetAsync(imag_residue, 0, count * sizeof(double), S.st), "memset");
-    run_synth(op, nullptr, c, out, 0, 2, nullptr, imag_residue, count, S);
+    run_synth(op, nullptr, c, out, 0, 2, nullptr, imag_residue, count, S, 0, false, f32);
   });
+}
+}  // namespace
+
+int fd_matvec(const fd_op* op, const double* f, double* out, double* imag_residue, long long count,
+              void* stream) {
+  return matvec_impl(op, f, out, imag_residue, count, stream, 0);
+}
+int fd_matvec_f32(const fd_op* op, const float* f, float* out, double* imag_residue,
+                  long long count, void* stream) {
+  return matvec_impl(op, f, out, imag_residue, count, stream, 1);
 }
 
 int fd_tikhonov(const fd_op* op, const fd_smoother* L, const double* g, const double* mu,
@@ -2286,10 +2304,11 @@ int fd_gcv_select(const fd_op* op, const fd_smoother* L, const double* g, double
   });
 }
 
-int fd_deblur(const fd_op* op, const fd_smoother* L, const double* g, int use_gcv,
-              double fixed_mu, double mu_min, double mu_max, int grid_count, double* restored,
-              double* mu_used, int* best_k, double* curve, double* imag_residue, long long count,
-              void* stream) {
+namespace {
+int deblur_impl(const fd_op* op, const fd_smoother* L, const void* g, int use_gcv,
+                double fixed_mu, double mu_min, double mu_max, int grid_count, void* restored,
+                double* mu_used, int* best_k, double* curve, double* imag_residue,
+                long long count, void* stream, int f32) {
   return guarded([&] {
     check_deblur_args(op, L, use_gcv, fixed_mu, mu_min, mu_max, grid_count, mu_used, curve);
     if (count <= 0) return;
@@ -2299,15 +2318,33 @@ int fd_deblur(const fd_op* op, const fd_smoother* L, const double* g, int use_gc
     std::unique_ptr<DevGrid> dg;
     if (use_gcv || curve) dg = std::make_unique<DevGrid>(mu_min, mu_max, grid_count, S);
     deblur_dev(op, L, g, use_gcv, fixed_mu, mu_min, mu_max, dg.get(), restored, mu_used, best_k,
-               curve, imag_residue, count, status, S);
+               curve, imag_residue, count, status, S, f32);
     if (use_gcv || curve) check_status(status, S.st);
   });
 }
+}  // namespace
 
-int fd_deblur_host(const fd_op* op, const fd_smoother* L, const double* g, int use_gcv,
-                   double fixed_mu, double mu_min, double mu_max, int grid_count,
-                   double* restored, double* mu_used, int* best_k, long long count,
-                   long long chunk, void* stream) {
+int fd_deblur(const fd_op* op, const fd_smoother* L, const double* g, int use_gcv,
+              double fixed_mu, double mu_min, double mu_max, int grid_count, double* restored,
+              double* mu_used, int* best_k, double* curve, double* imag_residue, long long count,
+              void* stream) {
+  return deblur_impl(op, L, g, use_gcv, fixed_mu, mu_min, mu_max, grid_count, restored, mu_used,
+                     best_k, curve, imag_residue, count, stream, 0);
+}
+int fd_deblur_f32(const fd_op* op, const fd_smoother* L, const float* g, int use_gcv,
+                  double fixed_mu, double mu_min, double mu_max, int grid_count, float* restored,
+                  double* mu_used, int* best_k, double* curve, double* imag_residue,
+                  long long count, void* stream) {
+  return deblur_impl(op, L, g, use_gcv, fixed_mu, mu_min, mu_max, grid_count, restored, mu_used,
+                     best_k, curve, imag_residue, count, stream, 1);
+}
+
+namespace {
+int deblur_host_impl(const fd_op* op, const fd_smoother* L, const void* g, int use_gcv,
+                     double fixed_mu, double mu_min, double mu_max, int grid_count,
+                     void* restored, double* mu_used, int* best_k, long long count,
+                     long long chunk, void* stream, int f32) {
+  const size_t esz = f32 ? sizeof(float) : sizeof(double);
   return guarded([&] {
     check_deblur_args(op, L, use_gcv, fixed_mu, mu_min, mu_max, grid_count, mu_used, nullptr);
     if (count <= 0) return;
@@ -2357,9 +2394,9 @@ int fd_deblur_host(const fd_op* op, const fd_smoother* L, const double* g, int u
         for (void* p : regs) cudaHostUnregister(p);
       }
     } pins;
-    pins.pin(g, (size_t)count * N * sizeof(double));
-    pins.pin(restored, (size_t)count * N * sizeof(double));
-    double* slot[2];
+    pins.pin(g, (size_t)count * N * esz);
+    pins.pin(restored, (size_t)count * N * esz);
+    char* slot[2];
     double* dmu = nullptr;
     int* dbk = nullptr;
     int* status = nullptr;
@@ -2368,7 +2405,7 @@ int fd_deblur_host(const fd_op* op, const fd_smoother* L, const double* g, int u
     ck(cudaMallocAsync(&dmu, (size_t)count * sizeof(double), sc), "alloc");
     ck(cudaMallocAsync(&dbk, (size_t)count * sizeof(int), sc), "alloc");
     for (int k = 0; k < 2; ++k)
-      ck(cudaMallocAsync(&slot[k], (size_t)chunk * N * sizeof(double), sc), "alloc");
+      ck(cudaMallocAsync(&slot[k], (size_t)chunk * N * esz, sc), "alloc");
     Scratch SG(sc);
     std::unique_ptr<DevGrid> dg;
     if (use_gcv) dg = std::make_unique<DevGrid>(mu_min, mu_max, grid_count, SG);
@@ -2378,7 +2415,7 @@ int fd_deblur_host(const fd_op* op, const fd_smoother* L, const double* g, int u
       const int k = (int)(i & 1);
       const long long b0 = i * chunk, nb = std::min(chunk, count - b0);
       if (i >= 2) ck(cudaStreamWaitEvent(s_in, ev_out[k], 0), "wait");
-      ck(cudaMemcpyAsync(slot[k], g + b0 * N, (size_t)nb * N * sizeof(double),
+      ck(cudaMemcpyAsync(slot[k], static_cast<const char*>(g) + b0 * N * esz, (size_t)nb * N * esz,
                          cudaMemcpyHostToDevice, s_in),
          "h2d");
       ck(cudaEventRecord(ev_in[k], s_in), "record");
@@ -2386,11 +2423,11 @@ int fd_deblur_host(const fd_op* op, const fd_smoother* L, const double* g, int u
       {
         Scratch S(sc);
         deblur_dev(op, L, slot[k], use_gcv, fixed_mu, mu_min, mu_max, dg.get(), slot[k],
-                   dmu + b0, dbk + b0, nullptr, nullptr, nb, status, S);
+                   dmu + b0, dbk + b0, nullptr, nullptr, nb, status, S, f32);
       }
       ck(cudaEventRecord(ev_comp[k], sc), "record");
       ck(cudaStreamWaitEvent(s_out, ev_comp[k], 0), "wait");
-      ck(cudaMemcpyAsync(restored + b0 * N, slot[k], (size_t)nb * N * sizeof(double),
+      ck(cudaMemcpyAsync(static_cast<char*>(restored) + b0 * N * esz, slot[k], (size_t)nb * N * esz,
                          cudaMemcpyDeviceToHost, s_out),
          "d2h");
       ck(cudaEventRecord(ev_out[k], s_out), "record");
@@ -2408,6 +2445,22 @@ int fd_deblur_host(const fd_op* op, const fd_smoother* L, const double* g, int u
     cudaFreeAsync(status, sc);
     if (h == 3) degenerate("degenerate gcv: all smoother eigenvalues are zero");
   });
+}
+}  // namespace
+
+int fd_deblur_host(const fd_op* op, const fd_smoother* L, const double* g, int use_gcv,
+                   double fixed_mu, double mu_min, double mu_max, int grid_count,
+                   double* restored, double* mu_used, int* best_k, long long count,
+                   long long chunk, void* stream) {
+  return deblur_host_impl(op, L, g, use_gcv, fixed_mu, mu_min, mu_max, grid_count, restored,
+                          mu_used, best_k, count, chunk, stream, 0);
+}
+int fd_deblur_host_f32(const fd_op* op, const fd_smoother* L, const float* g, int use_gcv,
+                       double fixed_mu, double mu_min, double mu_max, int grid_count,
+                       float* restored, double* mu_used, int* best_k, long long count,
+                       long long chunk, void* stream) {
+  return deblur_host_impl(op, L, g, use_gcv, fixed_mu, mu_min, mu_max, grid_count, restored,
+                          mu_used, best_k, count, chunk, stream, 1);
 }
 
 void fd_profile_enable(int on) { g_prof_on.store(on != 0); }

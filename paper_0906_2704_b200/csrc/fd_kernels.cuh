@@ -398,7 +398,32 @@ struct LineIO {
   int chirp_smem;  // real-line kernels: copy the Bluestein chirp to shared memory
   float* wout32;    // optional TF32 split of wout in screen tiles (fd_tc.cuh): hi
   float* wout32lo;  // and lo parts
+  // fp32 storage variant (BASELINE config 3): the analyze input / synthesis
+  // output are float (float2 when complex); arithmetic stays fp64.  Only the
+  // generic kernels k_analyze / k_synth take these (launch_* route them).
+  int in_f32, out_f32;
 };
+
+__device__ __forceinline__ double2 ld_in(const LineIO& io, long long idx) {
+  if (io.in_f32) {
+    if (io.in_cplx) {
+      const float2 v = __ldg(reinterpret_cast<const float2*>(io.in) + idx);
+      return make_double2(v.x, v.y);
+    }
+    return make_double2((double)__ldg(reinterpret_cast<const float*>(io.in) + idx), 0.0);
+  }
+  return ldc(io.in, io.in_cplx, idx);
+}
+__device__ __forceinline__ void st_out(const LineIO& io, long long idx, double2 v) {
+  if (io.out_f32) {
+    if (io.out_cplx)
+      reinterpret_cast<float2*>(io.out)[idx] = make_float2((float)v.x, (float)v.y);
+    else
+      reinterpret_cast<float*>(io.out)[idx] = (float)v.x;
+    return;
+  }
+  stc(io.out, io.out_cplx, idx, v);
+}
 
 __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
   extern __shared__ double2 sm[];
@@ -418,8 +443,8 @@ __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
   const int n = ax.n, m = ax.m, L = ax.fft.L;
   const double2* chirp = ax.fft.chirp;
 
-  auto ld0 = [&](int e) { return ldc(io.in, io.in_cplx, oi0 + e * es); };
-  auto ld1 = [&](int e) { return has1 ? ldc(io.in, io.in_cplx, oi1 + e * es) : czero(); };
+  auto ld0 = [&](int e) { return ld_in(io, oi0 + e * es); };
+  auto ld1 = [&](int e) { return has1 ? ld_in(io, oi1 + e * es) : czero(); };
 
   double2 y00 = czero(), yn0 = czero(), y01 = czero(), yn1 = czero();
   if (ax.bordered) {
@@ -850,26 +875,26 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
       // y_I = F^H b + P_I a; border rows whose 2 pi image is p: (F^H b)_p + P_B a
       if (ax.cplx && !hpack) {
         const double2 o = cadd(in0, ho_poly(ax, ua0, e));
-        stc(io.out, io.out_cplx, oo0 + e * eso, o);
+        st_out(io, oo0 + e * eso, o);
         im2 += o.y * o.y;
         for (int l = 0; l < ax.hk; ++l)
           if (ax.wrap[l] == p) {
             const double2 ob = cadd(in0, ho_poly(ax, ua0, ax.bord[l]));
-            stc(io.out, io.out_cplx, oo0 + ax.bord[l] * eso, ob);
+            st_out(io, oo0 + ax.bord[l] * eso, ob);
             im2 += ob.y * ob.y;
           }
       } else {
-        stc(io.out, io.out_cplx, oo0 + e * eso, make_double2(in0.x + ho_poly(ax, ua0, e).x, 0.0));
+        st_out(io, oo0 + e * eso, make_double2(in0.x + ho_poly(ax, ua0, e).x, 0.0));
         if (has1)
-          stc(io.out, io.out_cplx, oo1 + e * eso,
+          st_out(io, oo1 + e * eso,
               make_double2(in1.x + ho_poly(ax, ua1, e).x, 0.0));
         for (int l = 0; l < ax.hk; ++l)
           if (ax.wrap[l] == p) {
             const int eb = ax.bord[l];
-            stc(io.out, io.out_cplx, oo0 + eb * eso,
+            st_out(io, oo0 + eb * eso,
                 make_double2(in0.x + ho_poly(ax, ua0, eb).x, 0.0));
             if (has1)
-              stc(io.out, io.out_cplx, oo1 + eb * eso,
+              st_out(io, oo1 + eb * eso,
                   make_double2(in1.x + ho_poly(ax, ua1, eb).x, 0.0));
           }
       }
@@ -877,20 +902,20 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
       const double qi = __ldg(&ax.q[e]), qr = __ldg(&ax.q[n - 1 - e]);
       if (ax.cplx && !hpack) {
         const double2 o = cadd(cadd(cscale(u00, qi), in0), cscale(un0, qr));
-        stc(io.out, io.out_cplx, oo0 + e * eso, o);
+        st_out(io, oo0 + e * eso, o);
         im2 += o.y * o.y;
       } else {
         const double o = qi * u00.x + in0.x + qr * un0.x;
-        stc(io.out, io.out_cplx, oo0 + e * eso, make_double2(o, 0.0));
+        st_out(io, oo0 + e * eso, make_double2(o, 0.0));
         if (has1) {
           const double o1 = qi * u01.x + in1.x + qr * un1.x;
-          stc(io.out, io.out_cplx, oo1 + e * eso, make_double2(o1, 0.0));
+          st_out(io, oo1 + e * eso, make_double2(o1, 0.0));
         }
       }
     } else {
-      stc(io.out, io.out_cplx, oo0 + e * eso, in0);
+      st_out(io, oo0 + e * eso, in0);
       if (!hpack) im2 += in0.y * in0.y;
-      if (has1) stc(io.out, io.out_cplx, oo1 + e * eso, in1);
+      if (has1) st_out(io, oo1 + e * eso, in1);
     }
   }
   if (ax.bordered && threadIdx.x == 0) {
@@ -902,8 +927,8 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
       const double2 o0 = cadd(cscale(u0, q0), top);
       const double2 on = cadd(bot, cscale(un, q0));
       const long long oo = t == 0 ? oo0 : oo1;
-      stc(io.out, io.out_cplx, oo, o0);
-      stc(io.out, io.out_cplx, oo + (long long)(n - 1) * eso, on);
+      st_out(io, oo, o0);
+      st_out(io, oo + (long long)(n - 1) * eso, on);
       if (ax.cplx && !hpack) im2 += o0.y * o0.y + on.y * on.y;
     }
   }

@@ -86,6 +86,9 @@ def lib():
                                 vp, vp, vp, ll, vp]
         L.fd_deblur_host.argtypes = [vp, vp, vp, ip, C.c_double, C.c_double, C.c_double, ip,
                                      vp, vp, vp, ll, ll, vp]
+        L.fd_deblur_f32.argtypes = L.fd_deblur.argtypes
+        L.fd_deblur_host_f32.argtypes = L.fd_deblur_host.argtypes
+        L.fd_matvec_f32.argtypes = L.fd_matvec.argtypes
         L.fd_bc_for_degree.argtypes = [ip, ip, C.POINTER(C.c_int)]
         L.fd_parse_bc.argtypes = [C.c_char_p]
         _lib = L
@@ -212,12 +215,15 @@ class BlurOperator:
         return out if complex_out else (out, res)
 
     def apply(self, f):
-        """blur_apply(_2d): (A f, imag_residue)."""
-        f = _dev(f)
+        """blur_apply(_2d): (A f, imag_residue).  A float32 f takes the fp32
+        storage variant (fd_matvec_f32: fp64 arithmetic, float in / out)."""
+        f32 = isinstance(f, torch.Tensor) and f.dtype == torch.float32
+        f = _dev(f, torch.float32 if f32 else torch.float64)
         count, lead = self._count(f)
         out = torch.empty_like(f)
         res = torch.zeros(lead, dtype=torch.float64, device="cuda")
-        check(lib().fd_matvec(self._h, _ptr(f), _ptr(out), _ptr(res), count, _stream()))
+        fn = lib().fd_matvec_f32 if f32 else lib().fd_matvec
+        check(fn(self._h, _ptr(f), _ptr(out), _ptr(res), count, _stream()))
         return out, res
 
 
@@ -371,8 +377,11 @@ def gcv_select(op: BlurOperator, L: Smoother, g, search: GcvSearch = GcvSearch()
 def deblur(op: BlurOperator, L: Smoother, g, mu: MuChoice, want_curve=False,
            search: GcvSearch = GcvSearch(), out=None,
            want_imag_residue=False) -> RestorationReport:
-    """deblur(_2d) (pipeline.cpp:732-778).  imag_residue as in tikhonov_solve."""
-    g = _dev(g)
+    """deblur(_2d) (pipeline.cpp:732-778).  imag_residue as in tikhonov_solve.
+    A float32 g takes the fp32 storage variant (fd_deblur_f32: float in / out,
+    fp64 arithmetic)."""
+    f32 = isinstance(g, torch.Tensor) and g.dtype == torch.float32
+    g = _dev(g, torch.float32 if f32 else torch.float64)
     count, lead = op._count(g)
     restored = torch.empty_like(g) if out is None else out
     mu_used = torch.empty(lead, dtype=torch.float64, device="cuda")
@@ -381,7 +390,8 @@ def deblur(op: BlurOperator, L: Smoother, g, mu: MuChoice, want_curve=False,
         if want_curve else None
     res = torch.zeros(lead, dtype=torch.float64, device="cuda") \
         if (want_imag_residue or not op.complex) else None
-    check(lib().fd_deblur(op._h, L._h, _ptr(g), int(bool(mu.use_gcv)), float(mu.fixed_mu),
+    fn = lib().fd_deblur_f32 if f32 else lib().fd_deblur
+    check(fn(op._h, L._h, _ptr(g), int(bool(mu.use_gcv)), float(mu.fixed_mu),
                           float(search.mu_min), float(search.mu_max), int(search.count),
                           _ptr(restored), _ptr(mu_used), _ptr(bk) if mu.use_gcv else None,
                           _ptr(curve), _ptr(res), count, _stream()))
@@ -434,18 +444,20 @@ def deblur_host(op: BlurOperator, L: Smoother, g, mu: MuChoice, search: GcvSearc
                 out=None, chunk=0):
     """deblur for HOST arrays (the end-to-end entry point): chunks of the batch
     stream through H2D copy -> deblur -> D2H copy on separate CUDA streams
-    (fd_deblur_host).  g: CPU float64 tensor [..., shape] (pinned for overlap).
-    Returns (restored, mu_used, best_k) as CPU tensors."""
+    (fd_deblur_host).  g: CPU float64 (or float32: fd_deblur_host_f32) tensor
+    [..., shape] (pinned for overlap).  Returns (restored, mu_used, best_k) as
+    CPU tensors."""
     if not isinstance(g, torch.Tensor):
         g = torch.from_numpy(np.ascontiguousarray(np.asarray(g, dtype=np.float64)))
-    if g.is_cuda or g.dtype != torch.float64 or not g.is_contiguous():
-        raise ValidationError("deblur_host needs a contiguous CPU float64 tensor")
+    if g.is_cuda or g.dtype not in (torch.float64, torch.float32) or not g.is_contiguous():
+        raise ValidationError("deblur_host needs a contiguous CPU float64 / float32 tensor")
     count, lead = op._count(g)
     pin = g.is_pinned()
-    restored = torch.empty(g.shape, dtype=torch.float64, pin_memory=pin) if out is None else out
+    restored = torch.empty(g.shape, dtype=g.dtype, pin_memory=pin) if out is None else out
     mu_used = torch.empty(lead, dtype=torch.float64, pin_memory=pin)
     bk = torch.full(lead, -1, dtype=torch.int32)
-    check(lib().fd_deblur_host(op._h, L._h, _ptr(g), int(bool(mu.use_gcv)), float(mu.fixed_mu),
+    fn = lib().fd_deblur_host_f32 if g.dtype == torch.float32 else lib().fd_deblur_host
+    check(fn(op._h, L._h, _ptr(g), int(bool(mu.use_gcv)), float(mu.fixed_mu),
                                float(search.mu_min), float(search.mu_max), int(search.count),
                                _ptr(restored), _ptr(mu_used), _ptr(bk), count, int(chunk),
                                _stream()))

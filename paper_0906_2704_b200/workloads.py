@@ -144,6 +144,9 @@ class Config:
     # smoother); () = (bc,).  ``bc`` stays the reference-supported BC (the
     # reference arm and the golden fixtures use it).
     bcs: tuple = ()
+    # storage precisions a step restores in ("f64", and "f32" = the fp32
+    # storage variant, fp64 arithmetic)
+    precisions: tuple = ("f64",)
 
     @property
     def step_bcs(self):
@@ -176,9 +179,10 @@ def config(index: int) -> Config:
     if index == 3:
         return Config(3, 2, 1024, 1024, 512, onesided_exp_weights(11, 1 / 4), HOC_FOURIER,
                       (IDENTITY, LAPLACIAN), 1e-6, 1.0, 128, 0.01, blobs=40, rects=10,
-                      bcs=(HOC_FOURIER_D3,),
+                      bcs=(HOC_FOURIER_D3,), precisions=("f64", "f32"),
                       note="d=3 is an extension (not in the reference): a step restores the "
-                           "batch with the identity and the Laplacian smoother; the reference "
+                           "batch with the identity and the Laplacian smoother, from fp64 and "
+                           "from fp32 storage (fp64 arithmetic in both); the reference "
                            "arm runs its nearest BC, hoc-fourier (d=2); lambda range "
                            "unspecified, [1e-6, 1] used")
     if index == 4:
