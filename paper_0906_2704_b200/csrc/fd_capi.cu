@@ -148,6 +148,11 @@ void set_rline_attrs(int kmax) {
   cudaFuncSetAttribute(k_rsynth<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
 }
 template <int LOGM>
+void set_line_attrs(int kmax) {
+  cudaFuncSetAttribute(k_analyze<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+  cudaFuncSetAttribute(k_synth<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+}
+template <int LOGM>
 void set_pair_attrs(int kmax) {
   cudaFuncSetAttribute(k_panalyze<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
   cudaFuncSetAttribute(k_psynth<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
@@ -167,8 +172,11 @@ void init_runtime_once() {
       cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
     }
     const int kmax = 227 * 1024;
-    cudaFuncSetAttribute(k_analyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
-    cudaFuncSetAttribute(k_synth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+    set_line_attrs<0>(kmax);
+    set_line_attrs<10>(kmax);
+    set_line_attrs<11>(kmax);
+    set_line_attrs<12>(kmax);
+    set_line_attrs<13>(kmax);
     cudaFuncSetAttribute(k_bhat, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
     set_rline_attrs<0>(kmax);
     set_rline_attrs<10>(kmax);
@@ -353,12 +361,14 @@ void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaS
 
 void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
   if (io.gi.count == 0) return;
-  if (io.pack == 2 && !io.in_cplx && pair_path(ax)) {
+  if (io.pack == 2 && !io.in_cplx && !io.half && pair_path(ax)) {
     ProfScope ps("k_analyze", st);
     launch_pair(ax, io, nullptr, st);
     return;
   }
-  if (!io.in_cplx && ax.rhalf && !io.in_f32) {  // one real line per CTA, half-length DFT
+  // one real line per CTA, half-length DFT (k_ranalyze writes every row: not
+  // for the half-spectrum layout)
+  if (!io.in_cplx && ax.rhalf && !io.in_f32 && !io.half) {
     ProfScope ps("k_analyze", st);
     if (ax.hfft.M > kMaxOnChipM) {  // split convolution, persistent CTAs + scratch
       const int grid = std::min(io.gi.count, 2 * num_sms());
@@ -389,18 +399,27 @@ void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
   if (!ax.fft.M) validation("complex lines of this order exceed the on-chip transform limit");
   const int blocks = io.in_cplx ? io.gi.count : (io.gi.count + 1) / 2;
   ProfScope ps("k_analyze", st);
-  k_analyze<<<blocks, line_threads(ax.fft.M), smem_bytes(ax.fft.M), st>>>(ax, io);
+  const int thr = line_threads(ax.fft.M);
+  const size_t sm = smem_bytes(ax.fft.M);
+  switch (ax.fft.logM) {
+    case 10: k_analyze<10><<<blocks, thr, sm, st>>>(ax, io); break;
+    case 11: k_analyze<11><<<blocks, thr, sm, st>>>(ax, io); break;
+    case 12: k_analyze<12><<<blocks, thr, sm, st>>>(ax, io); break;
+    case 13: k_analyze<13><<<blocks, thr, sm, st>>>(ax, io); break;
+    default: k_analyze<0><<<blocks, thr, sm, st>>>(ax, io); break;
+  }
   launched("k_analyze");
 }
 
 void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cudaStream_t st) {
   if (io.gi.count == 0) return;
-  if (io.pack == 2 && !io.out_cplx && pair_path(ax)) {
+  if (io.pack == 2 && !io.out_cplx && !io.half && pair_path(ax)) {
     ProfScope ps(sa.mode == 1 ? "k_synth_filter" : "k_synth", st);
     launch_pair(ax, io, &sa, st);
     return;
   }
-  if (!io.out_cplx && ax.rhalf && !io.out_f32 && (!ax.cplx || sa.resid2 == nullptr)) {
+  if (!io.out_cplx && ax.rhalf && !io.out_f32 && !io.half &&
+      (!ax.cplx || sa.resid2 == nullptr)) {
     ProfScope ps(sa.mode == 1 ? "k_synth_filter" : "k_synth", st);
     if (ax.hfft.M > kMaxOnChipM) {
       const int grid = std::min(io.gi.count, 2 * num_sms());
@@ -433,7 +452,15 @@ void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cuda
   const int blocks = (ax.cplx && !hpack) ? io.gi.count : (io.gi.count + 1) / 2;
   if (blocks == 0) return;
   ProfScope ps(sa.mode == 1 ? "k_synth_filter" : "k_synth", st);
-  k_synth<<<blocks, line_threads(ax.fft.M), smem_bytes(ax.fft.M), st>>>(ax, io, sa);
+  const int thr = line_threads(ax.fft.M);
+  const size_t sm = smem_bytes(ax.fft.M);
+  switch (ax.fft.logM) {
+    case 10: k_synth<10><<<blocks, thr, sm, st>>>(ax, io, sa); break;
+    case 11: k_synth<11><<<blocks, thr, sm, st>>>(ax, io, sa); break;
+    case 12: k_synth<12><<<blocks, thr, sm, st>>>(ax, io, sa); break;
+    case 13: k_synth<13><<<blocks, thr, sm, st>>>(ax, io, sa); break;
+    default: k_synth<0><<<blocks, thr, sm, st>>>(ax, io, sa); break;
+  }
   launched("k_synth");
 }
 
@@ -460,6 +487,7 @@ AxisDev interior_view(const AxisDev& a) {
   v.bordered = 0;
   v.correction = 0;
   v.kl = 0;
+  v.kr = 0;
   v.hob = 0;
   return v;
 }
@@ -594,7 +622,8 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
   d.n = n;
   d.bordered = is_corrected(bc);
   d.cplx = is_complex_bc(bc);
-  d.kl = d.bordered ? 1 : 0;
+  d.kl = d.bordered ? 1 : 0;  // border widths (the higher-order codes reset them)
+  d.kr = d.kl;
   d.m = n - border_slack(bc);
   d.kind = (bc == BC_PERIODIC || bc == BC_HOC_FOURIER || is_ho_bc(bc)) ? IK_FOURIER
            : bc == BC_ANTIREFLECTIVE                  ? IK_SINE
@@ -950,12 +979,44 @@ Spectral spectral_of(const fd_op* op, const fd_smoother* L, bool col_pass) {
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
+// ---- half-spectrum layout (HalfRows, fd_internal.h) ----
+bool half_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FASTDEBLUR_HALF");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+HalfRows half_rows(const fd_op* op) {
+  return make_half_rows(op->n1, op->ax1->dev.kl, op->ax1->dev.kr);
+}
+// columns / rows of `count` items of `rows` x n2 (item stride `istride`)
+Lines cols_of(int rows, int n2, long long istride, long long count) {
+  (void)rows;
+  Lines c{};
+  c.item_stride = istride;
+  c.line_stride = 1;
+  c.elem_stride = n2;
+  c.per_item = n2;
+  c.count = (int)(count * n2);
+  return c;
+}
+Lines rows_of(int rows, int n2, long long istride, long long count) {
+  Lines r{};
+  r.item_stride = istride;
+  r.line_stride = n2;
+  r.elem_stride = 1;
+  r.per_item = rows;
+  r.count = (int)(count * rows);
+  return r;
+}
+
 // ---- transform pipelines (tensor_apply order: columns, then rows) ----
 // analyze count items: in (real or complex) -> out (basis type)
 void run_analyze(const fd_op* op, const void* in, int in_cplx, void* out, long long count,
                  Scratch& S, double* wout = nullptr, long long wstride = 0, long long wn = 0,
                  int pack = 0, float* wout32 = nullptr, float* wout32lo = nullptr,
-                 int in_f32 = 0) {
+                 int in_f32 = 0, int half = 0) {
   const int oc = op->cplx;
   if (op->dim == 1) {
     LineIO io{};
@@ -976,6 +1037,31 @@ void run_analyze(const fd_op* op, const void* in, int in_cplx, void* out, long l
     return;
   }
   const int n1 = op->n1, n2 = op->n2;
+  if (half) {  // real image, complex basis: keep the stored half of the rows
+    const HalfRows hr = half_rows(op);
+    const long long HN = (long long)hr.H * n2;
+    double2* midh = S.get<double2>(count * HN);
+    LineIO a{};
+    a.in = in;
+    a.in_f32 = in_f32;
+    a.out = midh;
+    a.gi = cols_of(n1, n2, (long long)n1 * n2, count);
+    a.go = cols_of(n1, n2, HN, count);
+    a.in_cplx = 0;
+    a.out_cplx = 1;
+    a.half = 1;
+    a.hr = hr;
+    launch_analyze(op->ax1->dev, a, S.st);
+    LineIO b{};
+    b.in = midh;
+    b.out = out;
+    b.gi = rows_of(hr.H, n2, HN, count);
+    b.go = b.gi;
+    b.in_cplx = 1;
+    b.out_cplx = 1;
+    launch_analyze(op->ax2->dev, b, S.st);
+    return;
+  }
   void* mid = oc ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
   Lines cols{};
   cols.item_stride = (long long)n1 * n2;
@@ -1014,7 +1100,7 @@ void run_analyze(const fd_op* op, const void* in, int in_cplx, void* out, long l
 // one analysis, many mu -- the mu sweep)
 void run_synth(const fd_op* op, const fd_smoother* L, const void* in, void* out, int out_cplx,
                int mode, const double* mu_item, double* resid, long long count, Scratch& S,
-               int pack = 0, bool shared_in = false, int out_f32 = 0) {
+               int pack = 0, bool shared_in = false, int out_f32 = 0, int half = 0) {
   const int oc = op->cplx;
   if (op->dim == 1) {
     LineIO io{};
@@ -1050,6 +1136,44 @@ void run_synth(const fd_op* op, const fd_smoother* L, const void* in, void* out,
     return;
   }
   const int n1 = op->n1, n2 = op->n2;
+  if (half) {
+    // half-spectrum input: the row pass first (filter / scale fused) on the
+    // stored rows, then the column pass rebuilds each Hermitian column and
+    // synthesises two real columns per FFT.  Rows-then-columns equals
+    // tensor_apply's order up to rounding.
+    const HalfRows hr = half_rows(op);
+    const long long HN = (long long)hr.H * n2;
+    double2* midh = S.get<double2>(count * HN);
+    LineIO a{};
+    a.in = in;
+    a.out = midh;
+    a.gi = rows_of(hr.H, n2, HN, count);
+    if (shared_in) a.gi.item_stride = 0;
+    a.go = rows_of(hr.H, n2, HN, count);
+    a.in_cplx = 1;
+    a.out_cplx = 1;
+    SynthArgs sa{};
+    sa.mode = mode;
+    sa.sp = spectral_of(op, L, false);
+    sa.sp.hr_split = hr.hs;
+    sa.sp.hr_off = n1 - hr.kr - hr.hs;
+    sa.mu_item = mu_item;
+    launch_synth(op->ax2->dev, a, sa, S.st);
+    LineIO b{};
+    b.in = midh;
+    b.out = out;
+    b.out_f32 = out_f32;
+    b.gi = cols_of(hr.H, n2, HN, count);
+    b.go = cols_of(n1, n2, (long long)n1 * n2, count);
+    b.in_cplx = 1;
+    b.out_cplx = 0;
+    b.half = 1;
+    b.hr = hr;
+    SynthArgs sb{};
+    launch_synth(op->ax1->dev, b, sb, S.st);
+    if (resid) ck(cudaMemsetAsync(resid, 0, count * sizeof(double), S.st), "memset");
+    return;
+  }
   void* mid = oc ? (void*)S.get<double2>(count * op->N()) : (void*)S.get<double>(count * op->N());
   Lines cols{};
   cols.item_stride = (long long)n1 * n2;
@@ -1124,6 +1248,7 @@ struct Analyzed {
   float* w32lo = nullptr;
   long long wn = 0, wstride = 0;
   int pack = 0;  // ghat Hermitian-packed (n doubles per line), see k_ranalyze
+  int half = 0;  // 2D: half-spectrum rows (HalfRows)
 };
 
 // want_full: keep the full complex coefficients (imaginary residue requested);
@@ -1136,8 +1261,12 @@ Analyzed analyze_for_gcv(const fd_op* op, const fd_smoother* L, const void* g, l
   const bool use_w = op->dim == 1 && !in_f32 &&
                      (op->ax1->dev.rhalf || (pair && !want_full)) && (!op->cplx || L->pair);
   a.pack = use_w && op->cplx && !want_full ? (pair ? 2 : 1) : 0;
-  a.ghat = (op->cplx && !a.pack) ? (void*)S.get<double2>(count * op->N())
-                                 : (void*)S.get<double>(count * op->N());
+  a.half = op->dim == 2 && op->cplx && !want_full && half_enabled();
+  if (a.half)
+    a.ghat = S.get<double2>(count * half_rows(op).H * (long long)op->n2);
+  else
+    a.ghat = (op->cplx && !a.pack) ? (void*)S.get<double2>(count * op->N())
+                                   : (void*)S.get<double>(count * op->N());
   if (use_w) {
     a.wn = op->cplx ? L->n_red : op->N();
     a.wstride = (a.wn + 31) / 32 * 32;
@@ -1148,7 +1277,8 @@ Analyzed analyze_for_gcv(const fd_op* op, const fd_smoother* L, const void* g, l
       a.w32lo = S.get<float>(rows * a.wstride);
     }
   }
-  run_analyze(op, g, 0, a.ghat, count, S, a.w, a.wstride, a.wn, a.pack, a.w32, a.w32lo, in_f32);
+  run_analyze(op, g, 0, a.ghat, count, S, a.w, a.wstride, a.wn, a.pack, a.w32, a.w32lo, in_f32,
+              a.half);
   return a;
 }
 
@@ -1171,6 +1301,14 @@ GcvData gcv_data(const fd_op* op, const fd_smoother* L, const void* ghat, long l
 
 GcvData gcv_data(const fd_op* op, const fd_smoother* L, const Analyzed& a, long long count) {
   GcvData g = gcv_data(op, L, a.ghat, count);
+  if (a.half) {  // stored rows; interior pair rows count twice
+    const HalfRows hr = half_rows(op);
+    g.N = g.stride = (long long)hr.H * op->n2;
+    g.sp.hr_split = hr.hs;
+    g.sp.hr_off = op->n1 - hr.kr - hr.hs;
+    g.hm_lo = hr.kl + 1;
+    g.hm_hi = hr.kl + hr.h1 + ((hr.m1 & 1) ? 1 : 0);
+  }
   if (a.w) {
     g.wred = a.w;
     g.wstride = a.wstride;
@@ -1789,7 +1927,8 @@ void deblur_dev(const fd_op* op, const fd_smoother* L, const void* g, int use_gc
   }
   if (!op->cplx && imag_residue)
     ck(cudaMemsetAsync(imag_residue, 0, count * sizeof(double), S.st), "memset");
-  run_synth(op, L, an.ghat, restored, 0, 1, mu_used, imag_residue, count, S, an.pack, false, f32);
+  run_synth(op, L, an.ghat, restored, 0, 1, mu_used, imag_residue, count, S, an.pack, false, f32,
+            an.half);
 }
 
 void check_status(int* status, cudaStream_t st) {
@@ -2579,10 +2718,11 @@ int fd_sweep_mu(const fd_op* op, const fd_smoother* L, const double* g, const do
       double* drre = S.get<double>(K + 1);
       for (int c0 = 0; c0 < K; c0 += ch) {
         const int nk = std::min(ch, K - c0);
-        run_synth(op, L, an.ghat, f, 0, 1, dg.d.mus + c0, nullptr, nk, S, an.pack, true);
+        run_synth(op, L, an.ghat, f, 0, 1, dg.d.mus + c0, nullptr, nk, S, an.pack, true, 0,
+                  an.half);
         rre_dev(f, truth, N, nk, drre + c0, S);
       }
-      run_synth(op, L, an.ghat, f, 0, 1, dmu, nullptr, 1, S, an.pack);
+      run_synth(op, L, an.ghat, f, 0, 1, dmu, nullptr, 1, S, an.pack, false, 0, an.half);
       rre_dev(f, truth, N, 1, drre + K, S);
       std::vector<double> hr(K + 1);
       ck(cudaMemcpyAsync(hr.data(), drre, (K + 1) * sizeof(double), cudaMemcpyDeviceToHost,

@@ -127,7 +127,38 @@ struct Spectral {
   const double2* dB;
   const double* sA;
   const double* sB;
+  // half-spectrum layout of a real image in a complex basis (see HalfRows):
+  // stored row r is full row r (r < hr_split) or r + hr_off
+  int hr_split, hr_off;
 };
+
+// Half-spectrum row layout of the 2D coefficients of a REAL image in a complex
+// (Fourier-interior) basis.  After the column pass the coefficient rows are
+// Hermitian in the row index: row kl + k = conj(row kl + m1 - k) for interior
+// k (the border rows are real), and the row transform preserves the pairing
+// (row kl + m1 - k of the result = conj of row kl + k with the columns
+// reflected).  Only the rows 0 .. hs-1 (borders + interior k <= h1) and the
+// kr right border rows are stored: H = hs + kr rows.
+struct HalfRows {
+  int n1, kl, kr, m1, h1, hs, H;
+  __host__ __device__ int pos(int e) const {  // stored row of full row e, or -1
+    if (e < hs) return e;
+    if (e >= n1 - kr) return e - (n1 - kr) + hs;
+    return -1;
+  }
+  __host__ __device__ int mirror(int e) const { return 2 * kl + m1 - e; }
+};
+__host__ __device__ inline HalfRows make_half_rows(int n1, int kl, int kr) {
+  HalfRows h;
+  h.n1 = n1;
+  h.kl = kl;
+  h.kr = kr;
+  h.m1 = n1 - kl - kr;
+  h.h1 = h.m1 / 2;
+  h.hs = kl + h.h1 + 1;
+  h.H = h.hs + kr;
+  return h;
+}
 
 struct GcvGrid {
   int count;             // K

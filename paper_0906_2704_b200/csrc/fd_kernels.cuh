@@ -54,7 +54,7 @@ __device__ __forceinline__ void spectral_at(const Spectral& sp, const Lines& g, 
     return;
   }
   const int li = l % g.per_item;
-  const int i = sp.col_pass ? e : li;
+  const int i = sp.col_pass ? e : (li < sp.hr_split ? li : li + sp.hr_off);
   const int j = sp.col_pass ? li : e;
   if (sp.mode == 2) {
     d = cmul(__ldg(&sp.dA[i]), __ldg(&sp.dB[j]));
@@ -402,7 +402,12 @@ struct LineIO {
   // output are float (float2 when complex); arithmetic stays fp64.  Only the
   // generic kernels k_analyze / k_synth take these (launch_* route them).
   int in_f32, out_f32;
+  // half-spectrum rows (HalfRows): the column analysis writes only the stored
+  // rows; the column synthesis reads them and mirrors the rest (conj)
+  int half;
+  HalfRows hr;
 };
+
 
 __device__ __forceinline__ double2 ld_in(const LineIO& io, long long idx) {
   if (io.in_f32) {
@@ -414,6 +419,16 @@ __device__ __forceinline__ double2 ld_in(const LineIO& io, long long idx) {
   }
   return ldc(io.in, io.in_cplx, idx);
 }
+// coefficient store of the analysis (element e of the line at `base`); in the
+// half-spectrum layout element e goes to its stored row, or is dropped
+__device__ __forceinline__ void st_coef(const LineIO& io, long long base, int e, double2 v) {
+  if (io.half) {
+    e = io.hr.pos(e);
+    if (e < 0) return;
+  }
+  stc(io.out, io.out_cplx, base + (long long)e * io.go.elem_stride, v);
+}
+
 __device__ __forceinline__ void st_out(const LineIO& io, long long idx, double2 v) {
   if (io.out_f32) {
     if (io.out_cplx)
@@ -425,7 +440,11 @@ __device__ __forceinline__ void st_out(const LineIO& io, long long idx, double2 
   stc(io.out, io.out_cplx, idx, v);
 }
 
-__global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
+// LOGM > 0: size-specialised Bluestein core (bluestein_t; blockDim = line_threads(M))
+template <int LOGM>
+constexpr int kLineNT = (1 << LOGM) / 16 < 64 ? 64 : ((1 << LOGM) / 16 > 512 ? 512 : (1 << LOGM) / 16);
+template <int LOGM>
+__global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512) k_analyze(AxisDev ax, LineIO io) {
   extern __shared__ double2 sm[];
   const int M = ax.fft.M;
   double2* x = sm;
@@ -562,12 +581,14 @@ __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
   }
   __syncthreads();
 
-  bluestein_core(x, ax.fft, tw, ax.fft.M);
+  if constexpr (LOGM > 0)
+    bluestein_t<LOGM, kLineNT<LOGM>>(x, ax.fft, tw, ax.fft.M);
+  else
+    bluestein_core(x, ax.fft, tw, ax.fft.M);
 
   const double2 b00 = bc[0], b10 = bc[1], b01 = bc[2], b11 = bc[3];
   const long long oo0 = line_offset(io.go, l0);
   const long long oo1 = has1 ? line_offset(io.go, l0 + 1) : oo0;
-  const long long eso = io.go.elem_stride;
 
   // ---- post-process, border update, store ----
   const double inv_sqrt_m = 1.0 / sqrt((double)m);
@@ -605,32 +626,32 @@ __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
       if (ax.cplx) {
         double2 o = cadd(cadd(cmul(y00, v), xi0), cmul(yn0, w));
         if (dots) o = csub(o, cadd(cmul(b00, v), cmul(b10, w)));
-        stc(io.out, io.out_cplx, oo0 + e * eso, o);
+        st_coef(io, oo0, e, o);
         if (has1) {
           double2 o1 = cadd(cadd(cmul(y01, v), xi1), cmul(yn1, w));
           if (dots) o1 = csub(o1, cadd(cmul(b01, v), cmul(b11, w)));
-          stc(io.out, io.out_cplx, oo1 + e * eso, o1);
+          st_coef(io, oo1, e, o1);
         }
       } else {
         double o = y00.x * v.x + xi0.x + yn0.x * w.x;
         if (dots) o -= b00.x * v.x + b10.x * w.x;
-        stc(io.out, io.out_cplx, oo0 + e * eso, make_double2(o, 0.0));
+        st_coef(io, oo0, e, make_double2(o, 0.0));
         if (has1) {
           double o1 = y01.x * v.x + xi1.x + yn1.x * w.x;
           if (dots) o1 -= b01.x * v.x + b11.x * w.x;
-          stc(io.out, io.out_cplx, oo1 + e * eso, make_double2(o1, 0.0));
+          st_coef(io, oo1, e, make_double2(o1, 0.0));
         }
       }
     } else {
-      stc(io.out, io.out_cplx, oo0 + e * eso, xi0);
-      if (has1) stc(io.out, io.out_cplx, oo1 + e * eso, xi1);
+      st_coef(io, oo0, e, xi0);
+      if (has1) st_coef(io, oo1, e, xi1);
     }
   }
   if (ax.hob && threadIdx.x == 0) {
     for (int l = 0; l < ax.hk; ++l) {
-      const long long el = (long long)ho_coef_elem(ax, l) * eso;
-      stc(io.out, io.out_cplx, oo0 + el, pair ? make_double2(ha0[l].x, 0.0) : ha0[l]);
-      if (has1) stc(io.out, io.out_cplx, oo1 + el, make_double2(ha1[l].x, 0.0));
+      const int le = ho_coef_elem(ax, l);
+      st_coef(io, oo0, le, pair ? make_double2(ha0[l].x, 0.0) : ha0[l]);
+      if (has1) st_coef(io, oo1, le, make_double2(ha1[l].x, 0.0));
     }
   }
   if (ax.bordered && threadIdx.x == 0) {
@@ -644,8 +665,8 @@ __global__ void __launch_bounds__(512) k_analyze(AxisDev ax, LineIO io) {
         on = csub(on, cscale(b1, al));
       }
       const long long oo = t == 0 ? oo0 : oo1;
-      stc(io.out, io.out_cplx, oo, o0);
-      stc(io.out, io.out_cplx, oo + (long long)(n - 1) * eso, on);
+      st_coef(io, oo, 0, o0);
+      st_coef(io, oo, n - 1, on);
     }
   }
 }
@@ -715,11 +736,21 @@ __device__ __forceinline__ double line_mu(const SynthArgs& sa, const Lines& g, i
 
 __device__ __forceinline__ double2 coeff_at(const AxisDev& ax, const LineIO& io,
                                             const SynthArgs& sa, int l, long long off, int e) {
-  return coeff_filter(ax, sa, io.gi, l, e, ldc(io.in, io.in_cplx, off + e * io.gi.elem_stride),
-                      line_mu(sa, io.gi, l));
+  double2 c;
+  if (io.half) {  // stored row, or the conjugate of the mirrored stored row
+    const int p = io.hr.pos(e);
+    c = p >= 0 ? ldc(io.in, io.in_cplx, off + (long long)p * io.gi.elem_stride)
+               : cconj(ldc(io.in, io.in_cplx,
+                           off + (long long)io.hr.pos(io.hr.mirror(e)) * io.gi.elem_stride));
+  } else {
+    c = ldc(io.in, io.in_cplx, off + e * io.gi.elem_stride);
+  }
+  return coeff_filter(ax, sa, io.gi, l, e, c, line_mu(sa, io.gi, l));
 }
 
-__global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs sa) {
+template <int LOGM>
+__global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512) k_synth(AxisDev ax, LineIO io,
+                                                                        SynthArgs sa) {
   extern __shared__ double2 sm[];
   const int M = ax.fft.M;
   double2* x = sm;
@@ -811,9 +842,12 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
       if (j < m) {
         const int jc = j == 0 ? 0 : m - j;
         const int e = interior_elem(ax, j), ec = interior_elem(ax, jc);
-        const double2 z0 = c0(e), z0c = c0(ec), z1 = c1(e), z1c = c1(ec);
-        const double2 h0 = cscale(cadd(z0, cconj(z0c)), 0.5);
-        const double2 h1 = cscale(cadd(z1, cconj(z1c)), 0.5);
+        const double2 z0 = c0(e), z1 = c1(e);
+        double2 h0 = z0, h1 = z1;
+        if (!io.half) {  // half-spectrum columns are exactly Hermitian already
+          h0 = cscale(cadd(z0, cconj(c0(ec))), 0.5);
+          h1 = cscale(cadd(z1, cconj(c1(ec))), 0.5);
+        }
         const double2 z = make_double2(h0.x - h1.y, h0.y + h1.x);
         val = cmul(cconj(z), __ldg(&chirp[j]));
         if (dots) {
@@ -844,7 +878,10 @@ __global__ void __launch_bounds__(512) k_synth(AxisDev ax, LineIO io, SynthArgs 
   if (dots) block_sum<8>(acc, red);
   __syncthreads();
 
-  bluestein_core(x, ax.fft, tw, ax.fft.M);
+  if constexpr (LOGM > 0)
+    bluestein_t<LOGM, kLineNT<LOGM>>(x, ax.fft, tw, ax.fft.M);
+  else
+    bluestein_core(x, ax.fft, tw, ax.fft.M);
 
   const long long oo0 = line_offset(io.go, l0);
   const long long oo1 = has1 ? line_offset(io.go, l0 + 1) : oo0;
@@ -1607,19 +1644,25 @@ struct GcvData {
   const double* wred;    // optional: precomputed weights w[item * wstride + e] (k_ranalyze wout)
   long long wstride;
   Spectral sp;           // 2D: mode 2 (separable) or 3 (full); sp.n2 = row length
+  // half-spectrum layout (HalfRows): stored rows [hm_lo, hm_hi) stand for
+  // themselves and their conjugate partner rows (multiplicity 2)
+  int hm_lo, hm_hi;
 };
 
 __device__ __forceinline__ double gcv_ratio(const GcvData& g, long long e) {
   if (g.r1d) return __ldg(&g.r1d[e]);
-  const int i = (int)(e / g.sp.n2), j = (int)(e % g.sp.n2);
+  int i = (int)(e / g.sp.n2);
+  const int j = (int)(e % g.sp.n2);
+  if (i >= g.sp.hr_split) i += g.sp.hr_off;
   double2 d;
   double s;
   if (g.sp.mode == 2) {
     d = cmul(__ldg(&g.sp.dA[i]), __ldg(&g.sp.dB[j]));
     s = g.sp.smooth_sum ? __ldg(&g.sp.sA[i]) + __ldg(&g.sp.sB[j]) : 1.0;
   } else {
-    d = __ldg(&g.sp.dA[e]);
-    s = __ldg(&g.sp.sA[e]);
+    const long long idx = (long long)i * g.sp.n2 + j;
+    d = __ldg(&g.sp.dA[idx]);
+    s = __ldg(&g.sp.sA[idx]);
   }
   if (s == 0.0) return INFINITY;
   return (d.x * d.x + d.y * d.y) / (s * s);
@@ -1639,6 +1682,10 @@ __device__ __forceinline__ double gcv_w1(const GcvData& g, long long idx) {
 // s_{R-e} = s_e), so sigma^2 w summed over the pair is one term.
 // multiplicity of element e in sum_e sigma_e (2 for a Hermitian pair)
 __device__ __forceinline__ double gcv_mult(const GcvData& g, long long e) {
+  if (g.hm_hi > g.hm_lo) {
+    const int r = (int)(e / g.sp.n2);
+    return (r >= g.hm_lo && r < g.hm_hi) ? 2.0 : 1.0;
+  }
   return (g.pair && __ldg(&g.pair[e]).y >= 0) ? 2.0 : 1.0;
 }
 
@@ -1650,6 +1697,7 @@ __device__ __forceinline__ double gcv_w(const GcvData& g, int item, long long e)
     const double w = gcv_w1(g, base + p.x);
     return p.y >= 0 ? w + gcv_w1(g, base + p.y) : w;
   }
+  if (g.hm_hi > g.hm_lo) return gcv_mult(g, e) * gcv_w1(g, base + e);
   return gcv_w1(g, base + e);
 }
 
