@@ -1299,7 +1299,8 @@ GcvData gcv_data(const fd_op* op, const fd_smoother* L, const void* ghat, long l
   return g;
 }
 
-GcvData gcv_data(const fd_op* op, const fd_smoother* L, const Analyzed& a, long long count) {
+GcvData gcv_data(const fd_op* op, const fd_smoother* L, const Analyzed& a, long long count,
+                 Scratch* S = nullptr) {
   GcvData g = gcv_data(op, L, a.ghat, count);
   if (a.half) {  // stored rows; interior pair rows count twice
     const HalfRows hr = half_rows(op);
@@ -1308,6 +1309,15 @@ GcvData gcv_data(const fd_op* op, const fd_smoother* L, const Analyzed& a, long 
     g.sp.hr_off = op->n1 - hr.kr - hr.hs;
     g.hm_lo = hr.kl + 1;
     g.hm_hi = hr.kl + hr.h1 + ((hr.m1 & 1) ? 1 : 0);
+  }
+  if (op->dim == 2 && S && count >= 2 && !g.r1d) {
+    // batches of images sharing the operator: one r_e = |d_e|^2 / s_e^2 table
+    // (item-independent, L2-resident) instead of d1 d2, s1 + s2 and a division
+    // per element in every GCV pass
+    double* rt = S->get<double>(g.N);
+    k_gcv_rtab<<<(int)std::min<long long>(4096, (g.N + 255) / 256), 256, 0, S->st>>>(g, rt);
+    launched("k_gcv_rtab");
+    g.r1d = rt;
   }
   if (a.w) {
     g.wred = a.w;
@@ -1718,7 +1728,7 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
   const GridHost& gh = dg.h;
   const int K = dg.d.count;
   GcvGrid grid = dg.d;
-  const GcvData g = gcv_data(op, L, an, count);
+  const GcvData g = gcv_data(op, L, an, count, &S);
   const int items = (int)count;
 
   int nch;

@@ -444,7 +444,7 @@ __device__ __forceinline__ void st_out(const LineIO& io, long long idx, double2 
 template <int LOGM>
 constexpr int kLineNT = (1 << LOGM) / 16 < 64 ? 64 : ((1 << LOGM) / 16 > 512 ? 512 : (1 << LOGM) / 16);
 template <int LOGM>
-__global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512) k_analyze(AxisDev ax, LineIO io) {
+__global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512 / kLineNT<LOGM> : 1) k_analyze(AxisDev ax, LineIO io) {
   extern __shared__ double2 sm[];
   const int M = ax.fft.M;
   double2* x = sm;
@@ -749,7 +749,7 @@ __device__ __forceinline__ double2 coeff_at(const AxisDev& ax, const LineIO& io,
 }
 
 template <int LOGM>
-__global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512) k_synth(AxisDev ax, LineIO io,
+__global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512 / kLineNT<LOGM> : 1) k_synth(AxisDev ax, LineIO io,
                                                                         SynthArgs sa) {
   extern __shared__ double2 sm[];
   const int M = ax.fft.M;
@@ -2052,6 +2052,13 @@ __global__ void __launch_bounds__(256) k_gcv_bounds(const double* __restrict__ h
 
 // ---- tensor-core screening of the grid (fd_tc.cuh) and exact candidates ----
 // rmin = min over elements of the finite ratios r_e (one CTA)
+// r table of a batch sharing one 2D operator (gcv_ratio for every element)
+__global__ void k_gcv_rtab(GcvData g, double* r) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < g.N;
+       e += (long long)gridDim.x * blockDim.x)
+    r[e] = gcv_ratio(g, e);
+}
+
 __global__ void __launch_bounds__(256) k_gcv_rmin(GcvData g, double* rmin) {
   __shared__ double red[32];
   double v = INFINITY;
