@@ -25,6 +25,7 @@
 #include "fd_internal.h"
 #include "fd_kernels.cuh"
 #include "fd_pair.cuh"
+#include "fd_mixed.cuh"
 
 
 using namespace fdb;
@@ -189,6 +190,18 @@ void init_runtime_once() {
     set_pair_attrs<11>(kmax);
     set_pair_attrs<12>(kmax);
     set_pair_attrs<13>(kmax);
+    {  // cos / sin (2 pi t / r) of the mixed-radix codelets
+      double cs[14][7] = {}, sn[14][7] = {};
+      for (int r = 3; r < 14; ++r)
+        for (int t = 0; t < 7; ++t) {
+          cs[r][t] = std::cos(2.0 * kPi * t / r);
+          sn[r][t] = std::sin(2.0 * kPi * t / r);
+        }
+      cudaMemcpyToSymbol(c_mix_cos, cs, sizeof(cs));
+      cudaMemcpyToSymbol(c_mix_sin, sn, sizeof(sn));
+      cudaFuncSetAttribute(k_manalyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+      cudaFuncSetAttribute(k_msynth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+    }
     ok = true;
   });
   if (!ok) throw FdError(FD_ERR_OTHER, "no CUDA device available (fastdeblur_b200 has no CPU path)");
@@ -333,12 +346,23 @@ int persistent_grid(K kern, int threads, size_t smem, int count) {
 // the pair kernels (fd_pair.cuh) carry real lines of the higher-order borders
 // (odd interior length) with Hermitian-packed coefficients (io.pack == 2)
 bool pair_path(const AxisDev& ax) {
-  return ax.hob && (ax.m & 1) && ax.fft.M && ax.fft.logM >= 8 && ax.fft.logM <= 13;
+  return ax.hob && (ax.m & 1) &&
+         (ax.mstages > 0 || (ax.fft.M && ax.fft.logM >= 8 && ax.fft.logM <= 13));
 }
 
 void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaStream_t st) {
-  const size_t smem = (size_t)pair_slots(ax.fft.M, ax.m) * sizeof(double2);
   const int pairs = (io.gi.count + 1) / 2;
+  if (ax.mstages > 0) {  // direct mixed-radix DFT (fd_mixed.cuh)
+    const size_t sm = (size_t)ax.m * sizeof(double2);
+    if (sa) {
+      k_msynth<<<persistent_grid(k_msynth, kMixNT, sm, pairs), kMixNT, sm, st>>>(ax, io, *sa);
+    } else {
+      k_manalyze<<<persistent_grid(k_manalyze, kMixNT, sm, pairs), kMixNT, sm, st>>>(ax, io);
+    }
+    launched(sa ? "k_msynth" : "k_manalyze");
+    return;
+  }
+  const size_t smem = (size_t)pair_slots(ax.fft.M, ax.m) * sizeof(double2);
 #define FD_PA(L)                                                                           \
   if (sa) {                                                                                \
     k_psynth<L><<<persistent_grid(k_psynth<L>, PairShape<L>::NT, smem, pairs),             \
@@ -536,6 +560,49 @@ FftTables make_fft_tables(int L, std::vector<std::unique_ptr<DevBuf>>& owner, in
   return T;
 }
 
+bool mixed_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FASTDEBLUR_MIXED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// direct mixed-radix DFT plan (fd_mixed.cuh) for an odd interior length that
+// factors into 13, 11, 9, 7, 5, 3 (largest radix first)
+void build_mixed_plan(Axis& A, int m) {
+  AxisDev& d = A.dev;
+  d.mstages = 0;
+  if (!mixed_enabled() || m < 9 || !(m & 1)) return;
+  int rest = m, ns = 0, rad[8];
+  for (int r : {13, 11, 9, 7, 5, 3})
+    while (rest % r == 0 && ns < kMixMaxStages) {
+      rad[ns++] = r;
+      rest /= r;
+    }
+  if (rest != 1) return;
+  std::vector<double2> tw(m);
+  for (int t = 0; t < m; ++t) {
+    const double ang = -2.0 * kPi * (double)t / (double)m;
+    tw[t] = make_double2(std::cos(ang), std::sin(ang));
+  }
+  // frequency k = d0 + r0 (d1 + r1 (d2 + ...)) sits at sum_s d_s m / (r0 .. r_s)
+  std::vector<int> perm(m);
+  for (int k = 0; k < m; ++k) {
+    int kk = k, span = m, pos = 0;
+    for (int s = 0; s < ns; ++s) {
+      span /= rad[s];
+      pos += (kk % rad[s]) * span;
+      kk /= rad[s];
+    }
+    perm[k] = pos;
+  }
+  for (int s = 0; s < ns; ++s) d.mrad[s] = rad[s];
+  d.mtw = dev_upload(A.bufs, tw);
+  d.mperm = dev_upload(A.bufs, perm);
+  d.mstages = ns;
+}
+
 // Higher-order borders (extension, oracle/fdoracle.py build_ho_transform):
 // Legendre border columns, wrap/bord rows, S = P_B - P[kl + wrap], S^-1.
 void build_ho_axis(Axis& A, int bc, int n) {
@@ -613,7 +680,7 @@ void build_ho_axis(Axis& A, int bc, int n) {
   for (int r = 0; r < kHoMax; ++r)
     for (int c = 0; c < kHoMax; ++c) d.sinv[r * kHoMax + c] = (r < k && c < k) ? Si[r][c] : 0.0;
   d.P = dev_upload(A.bufs, P);
-  (void)m;
+  build_mixed_plan(A, m);
 }
 
 std::unique_ptr<Axis> build_axis(int bc, int n) {

@@ -92,6 +92,12 @@ struct AxisDev {
   //   P[l][e] = L_{l+1}(t_e) ho_s[l],  t_e = ho_ta e + ho_tb  (Legendre)
   double ho_ta, ho_tb, ho_s[kHoMax];
   const double* P;
+  // direct mixed-radix DFT of the interior (fd_mixed.cuh) when m is a product
+  // of 3, 5, 7, 9, 11, 13 (mstages > 0): radices in stage order, the twiddle
+  // table e^{-2 pi i t/m} (t < m) and the output permutation
+  int mstages, mrad[6];
+  const double2* mtw;
+  const int* mperm;
   double sinv[kHoMax * kHoMax];
   int bord[kHoMax], wrap[kHoMax];
 };

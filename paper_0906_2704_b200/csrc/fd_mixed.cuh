@@ -1,0 +1,262 @@
+// Direct mixed-radix DFT for the pair kernels when the interior length m is
+// a product of small odd radices (3, 5, 7, 9, 11, 13): m = 4095 = 13*9*7*5 at
+// n = 4096, d = 1.  Bluestein (fd_pair.cuh) spends two 8192-point FFTs per
+// pair of lines; the direct in-place decimation-in-frequency transform of
+// length m needs ~45 fp64 instructions per point and four shared-memory
+// passes over 64 KB instead of seven over 139 KB.
+//
+// Stage s (radix r, block size S, stride L = S/r) applies, for every block and
+// j < L, the r-point DFT to x[blk S + j + q L] (q < r) and multiplies output p
+// by w_S^{jp} = w_m^{jp m/S}; after the last stage frequency k sits at
+// mperm[k] (mixed-radix digit reversal, a host-built table).  The r-point
+// DFTs use the symmetric split (x_j +- x_{r-j}) with constant-memory cos/sin.
+// Everything else -- border fold, Hermitian split of the two lines, packed
+// coefficients, GCV weights, TF32 tiles, filtered synthesis -- is the pair
+// kernels' (fd_pair.cuh), without the chirp.
+#pragma once
+
+namespace fdb {
+
+constexpr int kMixMaxStages = 6;
+// cos / sin (2 pi t / r) for t = 0 .. 6, radix r = 3 .. 13 (row r)
+__constant__ double c_mix_cos[14][7];
+__constant__ double c_mix_sin[14][7];
+
+// forward r-point DFT in registers: v[p] <- sum_q v[q] e^{-2 pi i pq / r}, r odd
+template <int R>
+__device__ __forceinline__ void mix_codelet(double2 (&v)[R]) {
+  constexpr int H = R / 2;
+  double2 s[H], d[H];
+#pragma unroll
+  for (int j = 1; j <= H; ++j) {
+    s[j - 1] = cadd(v[j], v[R - j]);
+    d[j - 1] = csub(v[j], v[R - j]);
+  }
+  double2 x0 = v[0];
+#pragma unroll
+  for (int j = 0; j < H; ++j) x0 = cadd(x0, s[j]);
+  double2 out[R];
+  out[0] = x0;
+#pragma unroll
+  for (int k = 1; k <= H; ++k) {
+    double2 A = v[0], B = czero();
+#pragma unroll
+    for (int j = 1; j <= H; ++j) {
+      const int t = (j * k) % R;
+      const double cv = c_mix_cos[R][t <= H ? t : R - t];
+      const double sv = t <= H ? c_mix_sin[R][t] : -c_mix_sin[R][R - t];
+      A.x = fma(s[j - 1].x, cv, A.x);
+      A.y = fma(s[j - 1].y, cv, A.y);
+      B.x = fma(d[j - 1].x, sv, B.x);
+      B.y = fma(d[j - 1].y, sv, B.y);
+    }
+    out[k] = make_double2(A.x + B.y, A.y - B.x);      // A - iB
+    out[R - k] = make_double2(A.x - B.y, A.y + B.x);  // A + iB
+  }
+#pragma unroll
+  for (int p = 0; p < R; ++p) v[p] = out[p];
+}
+
+template <int R>
+__device__ __forceinline__ void mix_stage(double2* __restrict__ x, int N, int S,
+                                          const double2* __restrict__ tw, int nt) {
+  const int L = S / R, items = N / R, tstep = N / S;
+  for (int it = threadIdx.x; it < items; it += nt) {
+    const int blk = it / L, j = it - blk * L;
+    double2* xb = x + blk * S + j;
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = xb[q * L];
+    mix_codelet<R>(v);
+    if (L > 1) {
+      const int t1 = j * tstep;
+#pragma unroll
+      for (int p = 1; p < R; ++p) v[p] = cmul(v[p], __ldg(&tw[t1 * p]));
+    }
+#pragma unroll
+    for (int p = 0; p < R; ++p) xb[p * L] = v[p];
+  }
+}
+
+// in-place DIF DFT of length ax.m (natural order in, mperm order out)
+__device__ __forceinline__ void mix_dft(double2* x, const AxisDev& ax, int nt) {
+  int S = ax.m;
+  for (int s = 0; s < ax.mstages; ++s) {
+    const int r = ax.mrad[s];
+    switch (r) {
+      case 3: mix_stage<3>(x, ax.m, S, ax.mtw, nt); break;
+      case 5: mix_stage<5>(x, ax.m, S, ax.mtw, nt); break;
+      case 7: mix_stage<7>(x, ax.m, S, ax.mtw, nt); break;
+      case 9: mix_stage<9>(x, ax.m, S, ax.mtw, nt); break;
+      case 11: mix_stage<11>(x, ax.m, S, ax.mtw, nt); break;
+      default: mix_stage<13>(x, ax.m, S, ax.mtw, nt); break;
+    }
+    S /= r;
+    __syncthreads();
+  }
+}
+
+constexpr int kMixNT = 256;
+
+// analyze, two real lines per direct DFT (see k_panalyze)
+__global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
+  extern __shared__ double2 sm[];
+  const int m = ax.m, n = ax.n, kl = ax.kl, hk = ax.hk, h = (m - 1) / 2;
+  double2* x = sm;
+  const int* perm = ax.mperm;
+  const int count = io.gi.count, npairs = (count + 1) / 2;
+  const double* in = reinterpret_cast<const double*>(io.in);
+  double* out = reinterpret_cast<double*>(io.out);
+  const long long es = io.gi.elem_stride;
+  const double isq = ax.inv_sqrt_m;
+  const long long nkb32 = io.wstride >> 5;
+  for (int q = blockIdx.x; q < npairs; q += gridDim.x) {
+    const int l0 = 2 * q;
+    const bool has1 = l0 + 1 < count;
+    const double* g0 = in + line_offset(io.gi, l0);
+    const double* g1 = has1 ? in + line_offset(io.gi, l0 + 1) : g0;
+    auto ld0 = [&](int e) { return __ldg(g0 + e * es); };
+    auto ld1 = [&](int e) { return has1 ? __ldg(g1 + e * es) : 0.0; };
+    double a0[kHoMax], a1[kHoMax];
+    ho_amps_real(ax, ld0, a0);
+    ho_amps_real(ax, ld1, a1);
+    const Cubic p0 = ho_cubic(ax, a0), p1 = ho_cubic(ax, a1);
+#pragma unroll 4
+    for (int j = threadIdx.x; j < m; j += kMixNT) {
+      const int e = kl + j;
+      const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
+      x[j] = make_double2(ld0(e) - p0(t), ld1(e) - p1(t));
+    }
+    __syncthreads();
+    mix_dft(x, ax, kMixNT);
+
+    double* o0 = out + line_offset(io.go, l0);
+    double* o1 = has1 ? out + line_offset(io.go, l0 + 1) : nullptr;
+    double* w0 = io.wout ? io.wout + (long long)l0 * io.wstride : nullptr;
+    double* w1 = (w0 && has1) ? w0 + io.wstride : nullptr;
+    auto wset = [&](int line, double* wl, long long i, double v) {
+      wl[i] = v;
+      if (io.wout32) {
+        float hi, lo;
+        tf32_split(v, hi, lo);
+        const long long t = tc_tile_index(line, i, kTcBM, nkb32);
+        io.wout32[t] = hi;
+        io.wout32lo[t] = lo;
+      }
+    };
+    for (int kk = threadIdx.x; kk <= h; kk += kMixNT) {
+      const double2 Zk = x[__ldg(&perm[kk])];
+      const double2 Zc = kk ? x[__ldg(&perm[m - kk])] : Zk;
+      const double2 X0 = cscale(cadd(Zk, cconj(Zc)), 0.5 * isq);
+      const double2 D = csub(Zk, cconj(Zc));
+      const double2 X1 = make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
+      if (kk == 0) {
+        o0[hk] = X0.x;
+        if (o1) o1[hk] = X1.x;
+      } else {
+        o0[hk + 2 * kk - 1] = X0.x;
+        o0[hk + 2 * kk] = X0.y;
+        if (o1) {
+          o1[hk + 2 * kk - 1] = X1.x;
+          o1[hk + 2 * kk] = X1.y;
+        }
+      }
+      if (w0) {
+        const double f = kk ? 2.0 : 1.0;
+        wset(l0, w0, kl + kk, f * (X0.x * X0.x + X0.y * X0.y));
+        if (w1) wset(l0 + 1, w1, kl + kk, f * (X1.x * X1.x + X1.y * X1.y));
+      }
+    }
+    if (threadIdx.x < hk) {
+      const int l = threadIdx.x;
+      o0[l] = a0[l];
+      if (o1) o1[l] = a1[l];
+      if (w0) {
+        wset(l0, w0, ho_wred(ax, l, h), a0[l] * a0[l]);
+        if (w1) wset(l0 + 1, w1, ho_wred(ax, l, h), a1[l] * a1[l]);
+      }
+    }
+    if (w0)
+      for (long long i = io.wn + threadIdx.x; i < io.wstride; i += kMixNT) {
+        wset(l0, w0, i, 0.0);
+        if (w1) wset(l0 + 1, w1, i, 0.0);
+      }
+    __syncthreads();
+  }
+}
+
+// synthesis with the filter fused, two lines per direct DFT (see k_psynth)
+__global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, SynthArgs sa) {
+  extern __shared__ double2 sm[];
+  const int m = ax.m, kl = ax.kl, hk = ax.hk, h = (m - 1) / 2;
+  double2* x = sm;
+  const int* perm = ax.mperm;
+  const int count = io.gi.count, npairs = (count + 1) / 2;
+  const double* in = reinterpret_cast<const double*>(io.in);
+  double* out = reinterpret_cast<double*>(io.out);
+  const double isq = ax.inv_sqrt_m;
+  for (int q = blockIdx.x; q < npairs; q += gridDim.x) {
+    const int l0 = 2 * q;
+    const bool has1 = l0 + 1 < count;
+    const double* g0 = in + line_offset(io.gi, l0);
+    const double* g1 = has1 ? in + line_offset(io.gi, l0 + 1) : g0;
+    const double mu0 = line_mu(sa, io.gi, l0);
+    const double mu1 = has1 ? line_mu(sa, io.gi, l0 + 1) : mu0;
+    auto f0 = [&](int e, double2 c) { return coeff_filter_fast(ax, sa, io.gi, l0, e, c, mu0); };
+    auto f1 = [&](int e, double2 c) {
+      return has1 ? coeff_filter_fast(ax, sa, io.gi, l0 + 1, e, c, mu1) : czero();
+    };
+    auto ld0 = [&](int i) { return __ldg(g0 + i); };
+    auto ld1 = [&](int i) { return has1 ? __ldg(g1 + i) : 0.0; };
+    double ua0[kHoMax], ua1[kHoMax];
+#pragma unroll
+    for (int l = 0; l < kHoMax; ++l) {
+      ua0[l] = l < hk ? f0(ho_coef_elem(ax, l), make_double2(ld0(l), 0.0)).x : 0.0;
+      ua1[l] = l < hk ? f1(ho_coef_elem(ax, l), make_double2(ld1(l), 0.0)).x : 0.0;
+    }
+#pragma unroll 2
+    for (int kk = threadIdx.x; kk <= h; kk += kMixNT) {
+      const int e = kl + kk;
+      double2 X0, X1;
+      if (kk == 0) {
+        X0 = make_double2(ld0(hk), 0.0);
+        X1 = make_double2(ld1(hk), 0.0);
+      } else {
+        X0 = make_double2(ld0(hk + 2 * kk - 1), ld0(hk + 2 * kk));
+        X1 = make_double2(ld1(hk + 2 * kk - 1), ld1(hk + 2 * kk));
+      }
+      X0 = f0(e, X0);
+      X1 = f1(e, X1);
+      // F^H v = conj(F conj v), v = X0 + i X1 (natural order input)
+      x[kk] = make_double2(X0.x - X1.y, -(X0.y + X1.x));
+      if (kk) x[m - kk] = make_double2(X0.x + X1.y, X0.y - X1.x);
+    }
+    __syncthreads();
+    mix_dft(x, ax, kMixNT);
+
+    const Cubic p0 = ho_cubic(ax, ua0), p1 = ho_cubic(ax, ua1);
+    const long long eso = io.go.elem_stride;
+    double* o0 = out + line_offset(io.go, l0);
+    double* o1 = has1 ? out + line_offset(io.go, l0 + 1) : nullptr;
+#pragma unroll 4
+    for (int p = threadIdx.x; p < m; p += kMixNT) {
+      const double2 z = x[__ldg(&perm[p])];
+      const double y0 = z.x * isq, y1 = -z.y * isq;
+      const int e = kl + p;
+      const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
+      o0[e * eso] = y0 + p0(t);
+      if (o1) o1[e * eso] = y1 + p1(t);
+#pragma unroll
+      for (int l = 0; l < kHoMax; ++l)
+        if (l < hk && ax.wrap[l] == p) {
+          const int eb = ax.bord[l];
+          const double tb = fma((double)eb, ax.ho_ta, ax.ho_tb);
+          o0[eb * eso] = y0 + p0(tb);
+          if (o1) o1[eb * eso] = y1 + p1(tb);
+        }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace fdb

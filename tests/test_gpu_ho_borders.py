@@ -130,3 +130,24 @@ def test_2d(bc, separable, rng):
         assert np.array_equal(np_(rep.best_k), want.best_k)
         assert np.max(np.abs(np_(rep.mu_used) / want.mu_used - 1)) < 1e-10
         assert rel(np_(rep.restored), want.restored) < 1e-10
+
+
+@pytest.mark.parametrize("n", [64, 1366, 4096])
+@pytest.mark.parametrize("smoother", [0, 2])
+def test_mixed_radix_pair_path(n, smoother):
+    """d = 1 interiors m = 63, 1365, 4095 factor into 3..13: the pair kernels
+    run the direct mixed-radix DFT (fd_mixed.cuh) instead of Bluestein."""
+    bc = O.HOC_FOURIER_D1
+    psf = onesided(15, 0.2)
+    op = P.build_operator(psf, n, bc)
+    L = P.smoothing_eigenvalues(smoother, op)
+    oop = O.build_operator(O.make_psf(psf, normalize=True), n, bc)
+    s = O.smoothing_eigenvalues(SM[smoother], bc, n, oop.eigenvalues)
+    g = scenes(n, psf, 37, 7 + n)
+    rep = P.deblur(op, L, torch.from_numpy(g), P.MuChoice(True), want_curve=True,
+                   search=P.GcvSearch(1e-8, 1.0, 256))
+    want = O.deblur(oop, s, g, True, mu_min=1e-8, mu_max=1.0, count=256, want_curve=True)
+    assert np.array_equal(np_(rep.best_k), want.best_k)
+    assert np.max(np.abs(np_(rep.gcv_curve) / want.curves - 1)) < 1e-10
+    assert np.max(np.abs(np_(rep.mu_used) / want.mu_used - 1)) < 1e-10
+    assert rel(np_(rep.restored), want.restored) < 1e-10
