@@ -353,7 +353,7 @@ bool pair_path(const AxisDev& ax) {
 void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaStream_t st) {
   const int pairs = (io.gi.count + 1) / 2;
   if (ax.mstages > 0) {  // direct mixed-radix DFT (fd_mixed.cuh)
-    const size_t sm = (size_t)ax.m * sizeof(double2);
+    const size_t sm = mix_smem_bytes(ax.m);
     if (sa) {
       k_msynth<<<persistent_grid(k_msynth, kMixNT, sm, pairs), kMixNT, sm, st>>>(ax, io, *sa);
     } else {

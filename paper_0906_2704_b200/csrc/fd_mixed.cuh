@@ -57,9 +57,16 @@ __device__ __forceinline__ void mix_codelet(double2 (&v)[R]) {
   for (int p = 0; p < R; ++p) v[p] = out[p];
 }
 
+// twiddles w_m^t from two shared-memory tables: hi[t >> 6] * lo[t & 63]
+struct MixTw {
+  const double2* lo;
+  const double2* hi;
+  __device__ __forceinline__ double2 operator()(int t) const { return cmul(hi[t >> 6], lo[t & 63]); }
+};
+
 template <int R>
-__device__ __forceinline__ void mix_stage(double2* __restrict__ x, int N, int S,
-                                          const double2* __restrict__ tw, int nt) {
+__device__ __forceinline__ void mix_stage(double2* __restrict__ x, int N, int S, const MixTw& tw,
+                                          int nt) {
   const int L = S / R, items = N / R, tstep = N / S;
   for (int it = threadIdx.x; it < items; it += nt) {
     const int blk = it / L, j = it - blk * L;
@@ -71,7 +78,7 @@ __device__ __forceinline__ void mix_stage(double2* __restrict__ x, int N, int S,
     if (L > 1) {
       const int t1 = j * tstep;
 #pragma unroll
-      for (int p = 1; p < R; ++p) v[p] = cmul(v[p], __ldg(&tw[t1 * p]));
+      for (int p = 1; p < R; ++p) v[p] = cmul(v[p], tw(t1 * p));
     }
 #pragma unroll
     for (int p = 0; p < R; ++p) xb[p * L] = v[p];
@@ -79,17 +86,17 @@ __device__ __forceinline__ void mix_stage(double2* __restrict__ x, int N, int S,
 }
 
 // in-place DIF DFT of length ax.m (natural order in, mperm order out)
-__device__ __forceinline__ void mix_dft(double2* x, const AxisDev& ax, int nt) {
+__device__ __forceinline__ void mix_dft(double2* x, const AxisDev& ax, const MixTw& tw, int nt) {
   int S = ax.m;
   for (int s = 0; s < ax.mstages; ++s) {
     const int r = ax.mrad[s];
     switch (r) {
-      case 3: mix_stage<3>(x, ax.m, S, ax.mtw, nt); break;
-      case 5: mix_stage<5>(x, ax.m, S, ax.mtw, nt); break;
-      case 7: mix_stage<7>(x, ax.m, S, ax.mtw, nt); break;
-      case 9: mix_stage<9>(x, ax.m, S, ax.mtw, nt); break;
-      case 11: mix_stage<11>(x, ax.m, S, ax.mtw, nt); break;
-      default: mix_stage<13>(x, ax.m, S, ax.mtw, nt); break;
+      case 3: mix_stage<3>(x, ax.m, S, tw, nt); break;
+      case 5: mix_stage<5>(x, ax.m, S, tw, nt); break;
+      case 7: mix_stage<7>(x, ax.m, S, tw, nt); break;
+      case 9: mix_stage<9>(x, ax.m, S, tw, nt); break;
+      case 11: mix_stage<11>(x, ax.m, S, tw, nt); break;
+      default: mix_stage<13>(x, ax.m, S, tw, nt); break;
     }
     S /= r;
     __syncthreads();
@@ -98,12 +105,31 @@ __device__ __forceinline__ void mix_dft(double2* x, const AxisDev& ax, int nt) {
 
 constexpr int kMixNT = 256;
 
+// smem: DFT buffer (m complex), twiddle hi / lo tables, output permutation
+__host__ __device__ __forceinline__ size_t mix_smem_bytes(int m) {
+  return (size_t)m * 16 + (size_t)(64 + ((m + 63) >> 6)) * 16 + (size_t)m * 4;
+}
+// twiddle tables and permutation into shared memory (before the first barrier)
+__device__ __forceinline__ MixTw mix_setup(double2* sm, const AxisDev& ax, const int** perm) {
+  const int m = ax.m, nhi = (m + 63) >> 6;
+  double2* lo = sm + m;
+  double2* hi = lo + 64;
+  int* ps = reinterpret_cast<int*>(hi + nhi);
+  for (int i = threadIdx.x; i < 64; i += blockDim.x) lo[i] = i < m ? ax.mtw[i] : czero();
+  for (int i = threadIdx.x; i < nhi; i += blockDim.x) hi[i] = ax.mtw[i << 6];
+  for (int i = threadIdx.x; i < m; i += blockDim.x) ps[i] = ax.mperm[i];
+  *perm = ps;
+  return MixTw{lo, hi};
+}
+
 // analyze, two real lines per direct DFT (see k_panalyze)
 __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
   extern __shared__ double2 sm[];
   const int m = ax.m, n = ax.n, kl = ax.kl, hk = ax.hk, h = (m - 1) / 2;
   double2* x = sm;
-  const int* perm = ax.mperm;
+  const int* perm = nullptr;
+  const MixTw tw = mix_setup(sm, ax, &perm);
+  __syncthreads();
   const int count = io.gi.count, npairs = (count + 1) / 2;
   const double* in = reinterpret_cast<const double*>(io.in);
   double* out = reinterpret_cast<double*>(io.out);
@@ -121,14 +147,14 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
     ho_amps_real(ax, ld0, a0);
     ho_amps_real(ax, ld1, a1);
     const Cubic p0 = ho_cubic(ax, a0), p1 = ho_cubic(ax, a1);
-#pragma unroll 4
+#pragma unroll 8
     for (int j = threadIdx.x; j < m; j += kMixNT) {
       const int e = kl + j;
       const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
       x[j] = make_double2(ld0(e) - p0(t), ld1(e) - p1(t));
     }
     __syncthreads();
-    mix_dft(x, ax, kMixNT);
+    mix_dft(x, ax, tw, kMixNT);
 
     double* o0 = out + line_offset(io.go, l0);
     double* o1 = has1 ? out + line_offset(io.go, l0 + 1) : nullptr;
@@ -145,8 +171,8 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
       }
     };
     for (int kk = threadIdx.x; kk <= h; kk += kMixNT) {
-      const double2 Zk = x[__ldg(&perm[kk])];
-      const double2 Zc = kk ? x[__ldg(&perm[m - kk])] : Zk;
+      const double2 Zk = x[perm[kk]];
+      const double2 Zc = kk ? x[perm[m - kk]] : Zk;
       const double2 X0 = cscale(cadd(Zk, cconj(Zc)), 0.5 * isq);
       const double2 D = csub(Zk, cconj(Zc));
       const double2 X1 = make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
@@ -190,7 +216,9 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
   extern __shared__ double2 sm[];
   const int m = ax.m, kl = ax.kl, hk = ax.hk, h = (m - 1) / 2;
   double2* x = sm;
-  const int* perm = ax.mperm;
+  const int* perm = nullptr;
+  const MixTw tw = mix_setup(sm, ax, &perm);
+  __syncthreads();
   const int count = io.gi.count, npairs = (count + 1) / 2;
   const double* in = reinterpret_cast<const double*>(io.in);
   double* out = reinterpret_cast<double*>(io.out);
@@ -214,7 +242,7 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
       ua0[l] = l < hk ? f0(ho_coef_elem(ax, l), make_double2(ld0(l), 0.0)).x : 0.0;
       ua1[l] = l < hk ? f1(ho_coef_elem(ax, l), make_double2(ld1(l), 0.0)).x : 0.0;
     }
-#pragma unroll 2
+#pragma unroll 4
     for (int kk = threadIdx.x; kk <= h; kk += kMixNT) {
       const int e = kl + kk;
       double2 X0, X1;
@@ -232,7 +260,7 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
       if (kk) x[m - kk] = make_double2(X0.x + X1.y, X0.y - X1.x);
     }
     __syncthreads();
-    mix_dft(x, ax, kMixNT);
+    mix_dft(x, ax, tw, kMixNT);
 
     const Cubic p0 = ho_cubic(ax, ua0), p1 = ho_cubic(ax, ua1);
     const long long eso = io.go.elem_stride;
@@ -240,7 +268,7 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
     double* o1 = has1 ? out + line_offset(io.go, l0 + 1) : nullptr;
 #pragma unroll 4
     for (int p = threadIdx.x; p < m; p += kMixNT) {
-      const double2 z = x[__ldg(&perm[p])];
+      const double2 z = x[perm[p]];
       const double y0 = z.x * isq, y1 = -z.y * isq;
       const int e = kl + p;
       const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
