@@ -181,6 +181,16 @@ int fd_deblur_host_f32(const fd_op* op, const fd_smoother* L, const float* g, in
                        float* restored, double* mu_used, int* best_k, long long count,
                        long long chunk, void* stream);
 
+/* deblur of ONE host batch under several operators of the same shape (e.g.
+ * BC degrees d = 1 and d = 3, or two smoothers): as fd_deblur_host, but each
+ * chunk is uploaded once and restored by every (ops[o], Ls[o]); restored[o]
+ * (host, count*N of double, or float when g_f32), mu_used[o*count + i],
+ * best_k[o*count + i] (or NULL). */
+int fd_deblur_host_multi(int nops, const fd_op* const* ops, const fd_smoother* const* Ls,
+                         const void* g, int g_f32, int use_gcv, double fixed_mu, double mu_min,
+                         double mu_max, int grid_count, void* const* restored, double* mu_used,
+                         int* best_k, long long count, long long chunk, void* stream);
+
 /* The same selection logic the kernels run (gcv_minimize, regularize.cpp:281-351),
  * on the host with a caller-supplied G: for the CPU test suite. */
 typedef double (*fd_gcv_fn)(double mu, void* ctx);

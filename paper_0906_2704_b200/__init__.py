@@ -5,6 +5,6 @@ operator API over it."""
 from .fastdeblur import (  # noqa: F401
     BC, SMOOTHER, BlurOperator, DegenerateError, FastDeblurError, GcvResult, GcvSearch,
     MuChoice, RestorationReport, Smoother, ValidationError, bc_for_degree, blur_apply, deblur_host,
-    build_operator, build_operator_2d, build_operator_2d_separable, deblur, gcv_select,
+    build_operator, build_operator_2d, deblur_host_multi, build_operator_2d_separable, deblur, gcv_select,
     gcv_value, kernel_launches, lib, smoother_from_eigenvalues, smoothing_eigenvalues,
     tikhonov_solve, sweep_mu, BcSweep, SweepPoint)

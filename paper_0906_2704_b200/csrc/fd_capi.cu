@@ -2556,16 +2556,24 @@ int fd_deblur_f32(const fd_op* op, const fd_smoother* L, const float* g, int use
 }
 
 namespace {
-int deblur_host_impl(const fd_op* op, const fd_smoother* L, const void* g, int use_gcv,
-                     double fixed_mu, double mu_min, double mu_max, int grid_count,
-                     void* restored, double* mu_used, int* best_k, long long count,
-                     long long chunk, void* stream, int f32) {
+// nops operators restore the same host batch g (uploaded once per chunk):
+// restored[o], mu_used + o*count, best_k + o*count per operator
+int deblur_host_impl(int nops, const fd_op* const* ops, const fd_smoother* const* Ls,
+                     const void* g, int use_gcv, double fixed_mu, double mu_min, double mu_max,
+                     int grid_count, void* const* restored, double* mu_used, int* best_k,
+                     long long count, long long chunk, void* stream, int f32) {
   const size_t esz = f32 ? sizeof(float) : sizeof(double);
   return guarded([&] {
-    check_deblur_args(op, L, use_gcv, fixed_mu, mu_min, mu_max, grid_count, mu_used, nullptr);
+    if (nops < 1 || !ops || !Ls || !restored) validation("null operator list");
+    for (int o = 0; o < nops; ++o) {
+      check_deblur_args(ops[o], Ls[o], use_gcv, fixed_mu, mu_min, mu_max, grid_count, mu_used,
+                        nullptr);
+      if (ops[o]->N() != ops[0]->N()) validation("operators must have the same shape");
+      if (!restored[o]) validation("null host buffer");
+    }
     if (count <= 0) return;
-    if (!g || !restored) validation("null host buffer");
-    const long long N = op->N();
+    if (!g) validation("null host buffer");
+    const long long N = ops[0]->N();
     if (chunk <= 0) chunk = std::max(std::min(count, 256LL), (count + 15) / 16);
     chunk = std::min(chunk, count);
     const long long nchunks = (count + chunk - 1) / chunk;
@@ -2611,17 +2619,24 @@ int deblur_host_impl(const fd_op* op, const fd_smoother* L, const void* g, int u
       }
     } pins;
     pins.pin(g, (size_t)count * N * esz);
-    pins.pin(restored, (size_t)count * N * esz);
+    for (int o = 0; o < nops; ++o) pins.pin(restored[o], (size_t)count * N * esz);
     char* slot[2];
+    std::vector<char*> oslot((size_t)2 * nops);
     double* dmu = nullptr;
     int* dbk = nullptr;
     int* status = nullptr;
     ck(cudaMallocAsync(&status, sizeof(int), sc), "alloc");
     ck(cudaMemsetAsync(status, 0, sizeof(int), sc), "memset");
-    ck(cudaMallocAsync(&dmu, (size_t)count * sizeof(double), sc), "alloc");
-    ck(cudaMallocAsync(&dbk, (size_t)count * sizeof(int), sc), "alloc");
-    for (int k = 0; k < 2; ++k)
+    ck(cudaMallocAsync(&dmu, (size_t)nops * count * sizeof(double), sc), "alloc");
+    ck(cudaMallocAsync(&dbk, (size_t)nops * count * sizeof(int), sc), "alloc");
+    for (int k = 0; k < 2; ++k) {
       ck(cudaMallocAsync(&slot[k], (size_t)chunk * N * esz, sc), "alloc");
+      // the last operator restores in place; the others need their own outputs
+      for (int o = 0; o < nops; ++o)
+        oslot[(size_t)k * nops + o] = slot[k];
+      for (int o = 0; o + 1 < nops; ++o)
+        ck(cudaMallocAsync(&oslot[(size_t)k * nops + o], (size_t)chunk * N * esz, sc), "alloc");
+    }
     Scratch SG(sc);
     std::unique_ptr<DevGrid> dg;
     if (use_gcv) dg = std::make_unique<DevGrid>(mu_min, mu_max, grid_count, SG);
@@ -2636,26 +2651,34 @@ int deblur_host_impl(const fd_op* op, const fd_smoother* L, const void* g, int u
          "h2d");
       ck(cudaEventRecord(ev_in[k], s_in), "record");
       ck(cudaStreamWaitEvent(sc, ev_in[k], 0), "wait");
-      {
+      for (int o = 0; o < nops; ++o) {
         Scratch S(sc);
-        deblur_dev(op, L, slot[k], use_gcv, fixed_mu, mu_min, mu_max, dg.get(), slot[k],
-                   dmu + b0, dbk + b0, nullptr, nullptr, nb, status, S, f32);
+        deblur_dev(ops[o], Ls[o], slot[k], use_gcv, fixed_mu, mu_min, mu_max, dg.get(),
+                   oslot[(size_t)k * nops + o], dmu + o * count + b0, dbk + o * count + b0,
+                   nullptr, nullptr, nb, status, S, f32);
       }
       ck(cudaEventRecord(ev_comp[k], sc), "record");
       ck(cudaStreamWaitEvent(s_out, ev_comp[k], 0), "wait");
-      ck(cudaMemcpyAsync(static_cast<char*>(restored) + b0 * N * esz, slot[k], (size_t)nb * N * esz,
-                         cudaMemcpyDeviceToHost, s_out),
-         "d2h");
+      for (int o = 0; o < nops; ++o)
+        ck(cudaMemcpyAsync(static_cast<char*>(restored[o]) + b0 * N * esz,
+                           oslot[(size_t)k * nops + o], (size_t)nb * N * esz,
+                           cudaMemcpyDeviceToHost, s_out),
+           "d2h");
       ck(cudaEventRecord(ev_out[k], s_out), "record");
     }
     ck(cudaStreamSynchronize(s_out), "sync");
     ck(cudaStreamSynchronize(sc), "sync");
     int h = 0;
     ck(cudaMemcpy(&h, status, sizeof(int), cudaMemcpyDeviceToHost), "status");
-    ck(cudaMemcpy(mu_used, dmu, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost), "mu");
+    ck(cudaMemcpy(mu_used, dmu, (size_t)nops * count * sizeof(double), cudaMemcpyDeviceToHost),
+       "mu");
     if (best_k && use_gcv)
-      ck(cudaMemcpy(best_k, dbk, (size_t)count * sizeof(int), cudaMemcpyDeviceToHost), "best_k");
-    for (int k = 0; k < 2; ++k) cudaFreeAsync(slot[k], sc);
+      ck(cudaMemcpy(best_k, dbk, (size_t)nops * count * sizeof(int), cudaMemcpyDeviceToHost),
+         "best_k");
+    for (int k = 0; k < 2; ++k) {
+      for (int o = 0; o + 1 < nops; ++o) cudaFreeAsync(oslot[(size_t)k * nops + o], sc);
+      cudaFreeAsync(slot[k], sc);
+    }
     cudaFreeAsync(dmu, sc);
     cudaFreeAsync(dbk, sc);
     cudaFreeAsync(status, sc);
@@ -2668,14 +2691,23 @@ int fd_deblur_host(const fd_op* op, const fd_smoother* L, const double* g, int u
                    double fixed_mu, double mu_min, double mu_max, int grid_count,
                    double* restored, double* mu_used, int* best_k, long long count,
                    long long chunk, void* stream) {
-  return deblur_host_impl(op, L, g, use_gcv, fixed_mu, mu_min, mu_max, grid_count, restored,
+  void* r[1] = {restored};
+  return deblur_host_impl(1, &op, &L, g, use_gcv, fixed_mu, mu_min, mu_max, grid_count, r,
                           mu_used, best_k, count, chunk, stream, 0);
+}
+int fd_deblur_host_multi(int nops, const fd_op* const* ops, const fd_smoother* const* Ls,
+                         const void* g, int g_f32, int use_gcv, double fixed_mu, double mu_min,
+                         double mu_max, int grid_count, void* const* restored, double* mu_used,
+                         int* best_k, long long count, long long chunk, void* stream) {
+  return deblur_host_impl(nops, ops, Ls, g, use_gcv, fixed_mu, mu_min, mu_max, grid_count,
+                          restored, mu_used, best_k, count, chunk, stream, g_f32 ? 1 : 0);
 }
 int fd_deblur_host_f32(const fd_op* op, const fd_smoother* L, const float* g, int use_gcv,
                        double fixed_mu, double mu_min, double mu_max, int grid_count,
                        float* restored, double* mu_used, int* best_k, long long count,
                        long long chunk, void* stream) {
-  return deblur_host_impl(op, L, g, use_gcv, fixed_mu, mu_min, mu_max, grid_count, restored,
+  void* r[1] = {restored};
+  return deblur_host_impl(1, &op, &L, g, use_gcv, fixed_mu, mu_min, mu_max, grid_count, r,
                           mu_used, best_k, count, chunk, stream, 1);
 }
 

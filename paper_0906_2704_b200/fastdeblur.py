@@ -88,6 +88,8 @@ def lib():
                                      vp, vp, vp, ll, ll, vp]
         L.fd_deblur_f32.argtypes = L.fd_deblur.argtypes
         L.fd_deblur_host_f32.argtypes = L.fd_deblur_host.argtypes
+        L.fd_deblur_host_multi.argtypes = [ip, vp, vp, vp, ip, ip, C.c_double, C.c_double,
+                                           C.c_double, ip, vp, vp, vp, ll, ll, vp]
         L.fd_matvec_f32.argtypes = L.fd_matvec.argtypes
         L.fd_bc_for_degree.argtypes = [ip, ip, C.POINTER(C.c_int)]
         L.fd_parse_bc.argtypes = [C.c_char_p]
@@ -462,3 +464,31 @@ def deblur_host(op: BlurOperator, L: Smoother, g, mu: MuChoice, search: GcvSearc
                                _ptr(restored), _ptr(mu_used), _ptr(bk), count, int(chunk),
                                _stream()))
     return restored, mu_used, bk
+
+
+def deblur_host_multi(ops, Ls, g, mu: MuChoice, search: GcvSearch = GcvSearch(), outs=None,
+                      chunk=0):
+    """One host batch restored under several operators of the same shape
+    (fd_deblur_host_multi: each chunk is uploaded once).  Returns a list of
+    (restored, mu_used, best_k) CPU tensors, one per operator."""
+    if not isinstance(g, torch.Tensor):
+        g = torch.from_numpy(np.ascontiguousarray(np.asarray(g, dtype=np.float64)))
+    if g.is_cuda or g.dtype not in (torch.float64, torch.float32) or not g.is_contiguous():
+        raise ValidationError("deblur_host_multi needs a contiguous CPU float64 / float32 tensor")
+    k = len(ops)
+    if k == 0 or len(Ls) != k:
+        raise ValidationError("one smoother per operator")
+    count, lead = ops[0]._count(g)
+    pin = g.is_pinned()
+    outs = outs or [torch.empty(g.shape, dtype=g.dtype, pin_memory=pin) for _ in range(k)]
+    mu_used = torch.empty((k,) + tuple(lead), dtype=torch.float64, pin_memory=pin)
+    bk = torch.full((k,) + tuple(lead), -1, dtype=torch.int32)
+    hops = (C.c_void_p * k)(*[op._h for op in ops])
+    hls = (C.c_void_p * k)(*[L._h for L in Ls])
+    houts = (C.c_void_p * k)(*[_ptr(o) for o in outs])
+    check(lib().fd_deblur_host_multi(k, hops, hls, _ptr(g), int(g.dtype == torch.float32),
+                                     int(bool(mu.use_gcv)), float(mu.fixed_mu),
+                                     float(search.mu_min), float(search.mu_max),
+                                     int(search.count), houts, _ptr(mu_used), _ptr(bk), count,
+                                     int(chunk), _stream()))
+    return [(outs[i], mu_used[i], bk[i]) for i in range(k)]

@@ -151,3 +151,21 @@ def test_mixed_radix_pair_path(n, smoother):
     assert np.max(np.abs(np_(rep.gcv_curve) / want.curves - 1)) < 1e-10
     assert np.max(np.abs(np_(rep.mu_used) / want.mu_used - 1)) < 1e-10
     assert rel(np_(rep.restored), want.restored) < 1e-10
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_deblur_host_multi_matches_device(dtype):
+    """fd_deblur_host_multi: one upload per chunk, every operator restores it."""
+    n, B = 1024, 70
+    psf = onesided(15, 0.2)
+    g = torch.from_numpy(scenes(n, psf, B, 3)).to(dtype)
+    ops = [P.build_operator(psf, n, bc) for bc in HO]
+    Ls = [P.smoothing_eigenvalues(2, op) for op in ops]
+    search = P.GcvSearch(1e-8, 1.0, 256)
+    res = P.deblur_host_multi(ops, Ls, g, P.MuChoice(True), search=search, chunk=16)
+    for op, L, (f, mu, bk) in zip(ops, Ls, res):
+        rep = P.deblur(op, L, g.cuda(), P.MuChoice(True), search=search)
+        assert f.dtype == dtype
+        assert np.array_equal(bk.numpy(), np_(rep.best_k))
+        assert np.array_equal(mu.numpy(), np_(rep.mu_used))
+        assert np.array_equal(f.numpy(), np_(rep.restored))
