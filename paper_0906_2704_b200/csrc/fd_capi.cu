@@ -26,6 +26,7 @@
 #include "fd_kernels.cuh"
 #include "fd_pair.cuh"
 #include "fd_mixed.cuh"
+#include "fd_rader.cuh"
 
 
 using namespace fdb;
@@ -191,8 +192,8 @@ void init_runtime_once() {
     set_pair_attrs<12>(kmax);
     set_pair_attrs<13>(kmax);
     {  // cos / sin (2 pi t / r) of the mixed-radix codelets
-      double cs[14][7] = {}, sn[14][7] = {};
-      for (int r = 3; r < 14; ++r)
+      double cs[kMixMaxR + 1][7] = {}, sn[kMixMaxR + 1][7] = {};
+      for (int r = 3; r <= kMixMaxR; ++r)
         for (int t = 0; t < 7; ++t) {
           cs[r][t] = std::cos(2.0 * kPi * t / r);
           sn[r][t] = std::sin(2.0 * kPi * t / r);
@@ -201,6 +202,8 @@ void init_runtime_once() {
       cudaMemcpyToSymbol(c_mix_sin, sn, sizeof(sn));
       cudaFuncSetAttribute(k_manalyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
       cudaFuncSetAttribute(k_msynth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+      cudaFuncSetAttribute(k_qanalyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+      cudaFuncSetAttribute(k_qsynth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
     }
     ok = true;
   });
@@ -352,6 +355,16 @@ bool pair_path(const AxisDev& ax) {
 
 void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaStream_t st) {
   const int pairs = (io.gi.count + 1) / 2;
+  if (ax.rader) {  // Rader (fd_rader.cuh)
+    const size_t sm = rad_smem_bytes(ax.m);
+    if (sa) {
+      k_qsynth<<<persistent_grid(k_qsynth, kRadNT, sm, pairs), kRadNT, sm, st>>>(ax, io, *sa);
+    } else {
+      k_qanalyze<<<persistent_grid(k_qanalyze, kRadNT, sm, pairs), kRadNT, sm, st>>>(ax, io);
+    }
+    launched(sa ? "k_qsynth" : "k_qanalyze");
+    return;
+  }
   if (ax.mstages > 0) {  // direct mixed-radix DFT (fd_mixed.cuh)
     const size_t sm = mix_smem_bytes(ax.m);
     if (sa) {
@@ -568,39 +581,121 @@ bool mixed_enabled() {
   return on;
 }
 
-// direct mixed-radix DFT plan (fd_mixed.cuh) for an odd interior length that
-// factors into 13, 11, 9, 7, 5, 3 (largest radix first)
-void build_mixed_plan(Axis& A, int m) {
-  AxisDev& d = A.dev;
-  d.mstages = 0;
-  if (!mixed_enabled() || m < 9 || !(m & 1)) return;
-  int rest = m, ns = 0, rad[8];
-  for (int r : {13, 11, 9, 7, 5, 3})
-    while (rest % r == 0 && ns < kMixMaxStages) {
-      rad[ns++] = r;
+// radices of a mixed-radix plan of length N from `allowed` (largest first;
+// powers of two as 4s and at most one 2); empty when N does not factor
+std::vector<int> mixed_radices(int N, std::initializer_list<int> allowed) {
+  std::vector<int> rad;
+  int rest = N;
+  for (int r : allowed)
+    while (rest % r == 0 && (int)rad.size() < kMixMaxStages) {
+      rad.push_back(r);
       rest /= r;
     }
-  if (rest != 1) return;
-  std::vector<double2> tw(m);
-  for (int t = 0; t < m; ++t) {
-    const double ang = -2.0 * kPi * (double)t / (double)m;
+  if (rest != 1) rad.clear();
+  return rad;
+}
+
+// twiddles w_N^t and the DIF output permutation of a plan
+void upload_plan(Axis& A, int N, const std::vector<int>& rad, std::vector<int>* perm_out) {
+  AxisDev& d = A.dev;
+  std::vector<double2> tw(N);
+  for (int t = 0; t < N; ++t) {
+    const double ang = -2.0 * kPi * (double)t / (double)N;
     tw[t] = make_double2(std::cos(ang), std::sin(ang));
   }
-  // frequency k = d0 + r0 (d1 + r1 (d2 + ...)) sits at sum_s d_s m / (r0 .. r_s)
-  std::vector<int> perm(m);
-  for (int k = 0; k < m; ++k) {
-    int kk = k, span = m, pos = 0;
-    for (int s = 0; s < ns; ++s) {
+  // frequency k = d0 + r0 (d1 + r1 (d2 + ...)) sits at sum_s d_s N / (r0 .. r_s)
+  std::vector<int> perm(N);
+  for (int k = 0; k < N; ++k) {
+    int kk = k, span = N, pos = 0;
+    for (size_t s = 0; s < rad.size(); ++s) {
       span /= rad[s];
       pos += (kk % rad[s]) * span;
       kk /= rad[s];
     }
     perm[k] = pos;
   }
-  for (int s = 0; s < ns; ++s) d.mrad[s] = rad[s];
+  for (size_t s = 0; s < rad.size(); ++s) d.mrad[s] = rad[s];
   d.mtw = dev_upload(A.bufs, tw);
   d.mperm = dev_upload(A.bufs, perm);
-  d.mstages = ns;
+  d.mstages = (int)rad.size();
+  if (perm_out) *perm_out = perm;
+}
+
+long long powmod(long long b, long long e, long long p) {
+  long long r = 1;
+  b %= p;
+  while (e) {
+    if (e & 1) r = r * b % p;
+    b = b * b % p;
+    e >>= 1;
+  }
+  return r;
+}
+
+// direct DFT plans for the pair kernels' odd interior length m:
+//  * m factors into 13, 11, 9, 7, 5, 3: direct mixed radix (fd_mixed.cuh);
+//  * m an odd prime with m - 1 factoring into 2..13: Rader (fd_rader.cuh)
+void build_mixed_plan(Axis& A, int m) {
+  AxisDev& d = A.dev;
+  d.mstages = 0;
+  d.rader = 0;
+  if (!mixed_enabled() || m < 9 || !(m & 1)) return;
+  const std::vector<int> rad = mixed_radices(m, {13, 11, 9, 7, 5, 3});
+  if (!rad.empty()) {
+    upload_plan(A, m, rad, nullptr);
+    return;
+  }
+  bool prime = true;
+  for (int q = 3; (long long)q * q <= m && prime; q += 2) prime = m % q != 0;
+  const int N = m - 1;
+  if (!prime || N > kRadPer * kRadNT) return;
+  const std::vector<int> rr =
+      mixed_radices(N, {13, 11, 9, 7, 5, 3, 4, 2});
+  if (rr.empty()) return;
+  // smallest primitive root g: g^(N/f) != 1 for every prime factor f of N
+  std::vector<int> pf;
+  for (int f = 2, t = N; t > 1; ++f)
+    if (t % f == 0) {
+      pf.push_back(f);
+      while (t % f == 0) t /= f;
+    }
+  int g = 2;
+  for (;; ++g) {
+    bool ok = true;
+    for (int f : pf) ok = ok && powmod(g, N / f, m) != 1;
+    if (ok) break;
+  }
+  std::vector<int> perm;
+  upload_plan(A, N, rr, &perm);
+  std::vector<int> gidx(N), opos(m, 0);
+  const long long ginv = powmod(g, m - 2, m);
+  long long gp = 1, gi = 1;
+  std::vector<double2> b(N);
+  for (int n = 0; n < N; ++n) {
+    gidx[n] = (int)gp;   // g^n
+    opos[gi] = n;        // g^-n sits at convolution index n
+    const double ang = -2.0 * kPi * (double)gi / (double)m;
+    b[n] = make_double2(std::cos(ang), std::sin(ang));  // w_m^{g^-n}
+    gp = gp * g % m;
+    gi = gi * ginv % m;
+  }
+  // DFT_N(b) / N in the DIF output order (host O(N^2) in long double: setup only)
+  std::vector<double2> bh(N);
+  for (int k = 0; k < N; ++k) {
+    long double re = 0.0L, im = 0.0L;
+    for (int n = 0; n < N; ++n) {
+      const long long t = (long long)n * k % N;
+      const long double ang = -2.0L * 3.141592653589793238462643383279502884L * t / N;
+      const long double c = cosl(ang), s = sinl(ang);
+      re += b[n].x * c - b[n].y * s;
+      im += b[n].x * s + b[n].y * c;
+    }
+    bh[perm[k]] = make_double2((double)(re / N), (double)(im / N));
+  }
+  d.rgidx = dev_upload(A.bufs, gidx);
+  d.ropos = dev_upload(A.bufs, opos);
+  d.rbhat = dev_upload(A.bufs, bh);
+  d.rader = 1;
 }
 
 // Higher-order borders (extension, oracle/fdoracle.py build_ho_transform):

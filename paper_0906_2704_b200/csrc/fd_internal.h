@@ -98,6 +98,13 @@ struct AxisDev {
   int mstages, mrad[6];
   const double2* mtw;
   const int* mperm;
+  // Rader (fd_rader.cuh) when m is an odd prime and m - 1 factors into 2..31:
+  // the mixed-radix plan above is for length m - 1; g^n table, output
+  // positions, DFT(b)/(m-1) in the DIF output order
+  int rader;
+  const int* rgidx;
+  const int* ropos;
+  const double2* rbhat;
   double sinv[kHoMax * kHoMax];
   int bord[kHoMax], wrap[kHoMax];
 };

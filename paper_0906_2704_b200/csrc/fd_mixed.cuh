@@ -19,8 +19,9 @@ namespace fdb {
 
 constexpr int kMixMaxStages = 6;
 // cos / sin (2 pi t / r) for t = 0 .. 6, radix r = 3 .. 13 (row r)
-__constant__ double c_mix_cos[14][7];
-__constant__ double c_mix_sin[14][7];
+constexpr int kMixMaxR = 13;
+__constant__ double c_mix_cos[kMixMaxR + 1][7];
+__constant__ double c_mix_sin[kMixMaxR + 1][7];
 
 // forward r-point DFT in registers: v[p] <- sum_q v[q] e^{-2 pi i pq / r}, r odd
 template <int R>

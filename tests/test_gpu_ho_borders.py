@@ -132,12 +132,14 @@ def test_2d(bc, separable, rng):
         assert rel(np_(rep.restored), want.restored) < 1e-10
 
 
-@pytest.mark.parametrize("n", [64, 1366, 4096])
+@pytest.mark.parametrize("bc,n", [(O.HOC_FOURIER_D1, 64), (O.HOC_FOURIER_D1, 1366),
+                                  (O.HOC_FOURIER_D1, 4096), (O.HOC_FOURIER_D3, 64),
+                                  (O.HOC_FOURIER_D3, 2314)])
 @pytest.mark.parametrize("smoother", [0, 2])
-def test_mixed_radix_pair_path(n, smoother):
+def test_mixed_radix_pair_path(bc, n, smoother):
     """d = 1 interiors m = 63, 1365, 4095 factor into 3..13: the pair kernels
-    run the direct mixed-radix DFT (fd_mixed.cuh) instead of Bluestein."""
-    bc = O.HOC_FOURIER_D1
+    run the direct mixed-radix DFT (fd_mixed.cuh); d = 3 interiors m = 61 and
+    2311 are primes with m - 1 = 4*3*5, 2*3*5*7*11: Rader (fd_rader.cuh)."""
     psf = onesided(15, 0.2)
     op = P.build_operator(psf, n, bc)
     L = P.smoothing_eigenvalues(smoother, op)
