@@ -28,7 +28,31 @@ template <int LOGM>
 struct PairShape {
   static constexpr int M = 1 << LOGM;
   static constexpr int NT = M / 16 >= 512 ? 512 : (M / 16 <= 64 ? 64 : M / 16);
+  // LOGM = 1 (mod 4): the Bluestein pass sequence starts with a radix-2 DIF
+  // stage whose upper input half is zero padding (m <= M/2), i.e. the stage is
+  // (v, v W^j): the load phase writes both halves itself, and the matching
+  // last DIT stage is only needed on the lower half, so it is folded into the
+  // post phase -- two full shared-memory passes saved per line pair.
+  static constexpr bool FOLD = (LOGM % 4 == 1) && LOGM >= 9;
+  static constexpr int HM = M / 2;
+  static constexpr int JS = (HM + NT - 1) / NT;  // register slots per thread (j < HM)
 };
+
+// the Bluestein convolution of the pair kernels; with FOLD the buffer must
+// hold both halves of the first DIF stage already, and on return the lower
+// half [0, m) holds the result
+template <int LOGM, int NT>
+__device__ __forceinline__ void pair_conv(double2* x, const FftTables& T, const TwSm& tw, int m) {
+  using S = PairShape<LOGM>;
+  if constexpr (S::FOLD) {
+    bluestein_rec<LOGM, 1, S::HM, NT>(x, T.bhat, tw, S::M);
+    for (int k = threadIdx.x; k < m; k += NT)
+      x[pidx(k)] = cadd(x[pidx(k)], cmulc(x[pidx(k + S::HM)], tw(k)));
+    __syncthreads();
+  } else {
+    bluestein_t<LOGM, NT>(x, T, tw, m);
+  }
+}
 
 // smem slots (double2) of the pair kernels: buffer, twiddles, chirp, mbarrier
 __host__ __device__ __forceinline__ int pair_slots(int M, int m) {
@@ -143,16 +167,27 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
     const double* s1 = stg.buf + n;
     double a0[kHoMax], a1[kHoMax];
     Cubic p0, p1;
+    using PS = PairShape<LOGM>;
+    double2 vr[PS::FOLD ? PS::JS : 1];
     auto load_phase = [&](auto ld0, auto ld1) {
       ho_amps_real(ax, ld0, a0);
       ho_amps_real(ax, ld1, a1);
       p0 = ho_cubic(ax, a0);
       p1 = ho_cubic(ax, a1);
-#pragma unroll 4
-      for (int j = threadIdx.x; j < m; j += NT) {
+      auto val = [&](int j) {
         const int e = kl + j;
         const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
-        x[pidx(j)] = cmul(make_double2(ld0(e) - p0(t), ld1(e) - p1(t)), cs[j]);
+        return cmul(make_double2(ld0(e) - p0(t), ld1(e) - p1(t)), cs[j]);
+      };
+      if constexpr (PS::FOLD) {
+#pragma unroll
+        for (int t = 0; t < PS::JS; ++t) {
+          const int j = threadIdx.x + t * NT;
+          vr[t] = j < m ? val(j) : czero();
+        }
+      } else {
+#pragma unroll 4
+        for (int j = threadIdx.x; j < m; j += NT) x[pidx(j)] = val(j);
       }
     };
     if (st)
@@ -161,7 +196,18 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
       load_phase([&](int e) { return __ldg(g0 + e * es); },
                  [&](int e) { return has1 ? __ldg(g1 + e * es) : 0.0; });
     __syncthreads();
-    bluestein_t<LOGM, NT>(x, T, tw, m);
+    if constexpr (PS::FOLD) {  // first DIF stage (v, v W^j), staged input consumed
+#pragma unroll
+      for (int t = 0; t < PS::JS; ++t) {
+        const int j = threadIdx.x + t * NT;
+        if (j < PS::HM) {
+          x[pidx(j)] = vr[t];
+          x[pidx(j + PS::HM)] = cmul(vr[t], tw(j));
+        }
+      }
+      __syncthreads();
+    }
+    pair_conv<LOGM, NT>(x, T, tw, m);
     // the post phase reads [0, m) only: stage the next pair behind it
     if (threadIdx.x == 0) pair_issue(stg, io.in, io.gi, q + gridDim.x, n);
 
@@ -257,14 +303,18 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_psynth(AxisDev ax, L
       return has1 ? coeff_filter_fast(ax, sa, io.gi, l0 + 1, e, c, mu1) : czero();
     };
     double ua0[kHoMax], ua1[kHoMax];
+    using PS = PairShape<LOGM>;
+    constexpr int KS = PS::FOLD ? (PS::HM / 2 + NT) / NT : 1;  // kk slots (kk <= h < HM/2+1)
+    double2 vk[KS], vc[KS];
     auto load_phase = [&](auto ld0, auto ld1) {
 #pragma unroll
       for (int l = 0; l < kHoMax; ++l) {
         ua0[l] = l < hk ? f0(ho_coef_elem(ax, l), make_double2(ld0(l), 0.0)).x : 0.0;
         ua1[l] = l < hk ? f1(ho_coef_elem(ax, l), make_double2(ld1(l), 0.0)).x : 0.0;
       }
-#pragma unroll 2
-      for (int kk = threadIdx.x; kk <= h; kk += NT) {
+      // Bluestein inputs of index kk and m - kk (F^H v = conj(F conj v):
+      // conj(v_k) c_k, v = X0 + i X1)
+      auto one = [&](int kk, double2& a, double2& b) {
         const int e = kl + kk;
         double2 X0, X1;
         if (kk == 0) {
@@ -276,9 +326,24 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_psynth(AxisDev ax, L
         }
         X0 = f0(e, X0);
         X1 = f1(e, X1);
-        // F^H v = conj(F conj v): Bluestein input conj(v_k) c_k, v = X0 + i X1
-        x[pidx(kk)] = cmul(make_double2(X0.x - X1.y, -(X0.y + X1.x)), cs[kk]);
-        if (kk) x[pidx(m - kk)] = cmul(make_double2(X0.x + X1.y, X0.y - X1.x), cs[m - kk]);
+        a = cmul(make_double2(X0.x - X1.y, -(X0.y + X1.x)), cs[kk]);
+        b = kk ? cmul(make_double2(X0.x + X1.y, X0.y - X1.x), cs[m - kk]) : czero();
+      };
+      if constexpr (PS::FOLD) {
+#pragma unroll
+        for (int t = 0; t < KS; ++t) {
+          const int kk = threadIdx.x + t * NT;
+          vk[t] = vc[t] = czero();
+          if (kk <= h) one(kk, vk[t], vc[t]);
+        }
+      } else {
+#pragma unroll 2
+        for (int kk = threadIdx.x; kk <= h; kk += NT) {
+          double2 a, b;
+          one(kk, a, b);
+          x[pidx(kk)] = a;
+          if (kk) x[pidx(m - kk)] = b;
+        }
       }
     };
     if (st)
@@ -287,7 +352,26 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_psynth(AxisDev ax, L
       load_phase([&](int i) { return __ldg(g0 + i); },
                  [&](int i) { return has1 ? __ldg(g1 + i) : 0.0; });
     __syncthreads();
-    bluestein_t<LOGM, NT>(x, T, tw, m);
+    if constexpr (PS::FOLD) {  // first DIF stage (v, v W^j); zero padding written explicitly
+#pragma unroll
+      for (int t = 0; t < KS; ++t) {
+        const int kk = threadIdx.x + t * NT;
+        if (kk <= h) {
+          x[pidx(kk)] = vk[t];
+          x[pidx(kk + PS::HM)] = cmul(vk[t], tw(kk));
+          if (kk) {
+            x[pidx(m - kk)] = vc[t];
+            x[pidx(m - kk + PS::HM)] = cmul(vc[t], tw(m - kk));
+          }
+        }
+      }
+      for (int j = m + threadIdx.x; j < PS::HM; j += NT) {
+        x[pidx(j)] = czero();
+        x[pidx(j + PS::HM)] = czero();
+      }
+      __syncthreads();
+    }
+    pair_conv<LOGM, NT>(x, T, tw, m);
     if (threadIdx.x == 0) pair_issue(stg, io.in, io.gi, q + gridDim.x, n);
 
     const Cubic p0 = ho_cubic(ax, ua0), p1 = ho_cubic(ax, ua1);
