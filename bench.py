@@ -253,10 +253,20 @@ class Clocks:
 # ----------------------------------------------------------------------------
 # our arm
 # ----------------------------------------------------------------------------
+# pair kernels of the 1D higher-order borders (one launch per restoration at
+# that degree, covering the whole batch): mixed-radix (k_m*), Bluestein (k_p*),
+# Rader (k_q*); the BC each one runs and its textbook flop model per line
+PAIR_KERNELS = {"k_manalyze": W.HOC_FOURIER_D1, "k_msynth": W.HOC_FOURIER_D1,
+                "k_panalyze": W.HOC_FOURIER_D3, "k_psynth": W.HOC_FOURIER_D3,
+                "k_qanalyze": None, "k_qsynth": None}
+
+
 def alg_bytes_per_px(name, cfg):
     """Algorithmic HBM bytes per pixel of one launch of each hot kernel
     (SURVEY 8d model): what the kernel must read + write at minimum."""
     c = 16 if cfg.bc in (W.PERIODIC, W.HOC_FOURIER) else 8  # coefficient bytes
+    if name in PAIR_KERNELS:  # read 8 B/px, write 8 B/px (Hermitian-packed coefficients)
+        return 8 + 8
     if cfg.dim == 1:
         # real data: the coefficients are n reals (Hermitian-packed in a complex
         # basis); GCV streams one weight per Hermitian pair (n/2) or per coefficient
@@ -268,8 +278,18 @@ def alg_bytes_per_px(name, cfg):
             "k_synth": c + 8, "k_gcv_grid": c, "k_gcv_moments": c}.get(name)
 
 
+def launch_pixels(name, cfg, px_rank, restorations, launches_per_step):
+    """Pixels one launch of `name` covers: a pair kernel runs once per
+    restoration at its degree over the whole batch; the grouped names average
+    over the launches of a step."""
+    if name in PAIR_KERNELS:
+        return px_rank
+    return px_rank * restorations / launches_per_step
+
+
 NCU_NAMES = {"k_analyze": ("k_ranalyze", "k_analyze"), "k_synth_filter": ("k_rsynth", "k_synth"),
              "k_synth": ("k_rsynth", "k_synth")}
+NCU_NAMES.update({k: (k,) for k in PAIR_KERNELS})
 
 
 def ncu_traffic(name, cfg):
@@ -313,6 +333,15 @@ def bluestein_flops_per_line(n, bc):
     while M < max(2 * h - 1, 2):
         M *= 2
     return 2 * 5 * M * math.log2(M) + 6 * M + 12 * h
+
+
+def kernel_flops_per_line(name, n):
+    """Textbook fp64 flops per real line of one pair-kernel launch."""
+    bc = PAIR_KERNELS[name]
+    if name[2] == "m":  # direct mixed-radix DFT of length m, one per pair
+        m = n - 1
+        return 5 * m * math.log2(m) / 2
+    return bluestein_flops_per_line(n, bc if bc is not None else W.HOC_FOURIER_D3)
 
 
 def fp64_peak():
@@ -484,7 +513,7 @@ def main():
         bpp = alg_bytes_per_px(dom, cfg)
         launches_per_step = cnt / args.steps
         if bpp is not None:
-            bytes_launch = bpp * px_rank * R_ / launches_per_step
+            bytes_launch = bpp * launch_pixels(dom, cfg, px_rank, R_, launches_per_step)
             achieved = bytes_launch / (avg_ms / 1e3) / 1e9
             traffic, tsrc = ncu_traffic(dom, cfg)
             roof = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak,
@@ -495,24 +524,30 @@ def main():
                     "alg_bytes_per_launch": bytes_launch}
     # fp64 roofline of the transform kernels: Bluestein FFTs are fp64-bound on B200
     croof = None
-    fft_kernels = [k for k in prof if k in ("k_analyze", "k_synth_filter", "k_synth")]
+    fft_kernels = [k for k in prof if k in ("k_analyze", "k_synth_filter", "k_synth")
+                   or k in PAIR_KERNELS]
     if fft_kernels:
         fdom = max(fft_kernels, key=lambda k: prof[k][0])
         ms_tot, cnt = prof[fdom]
-        # per step: every line of length n1 (1D; 2D column pass) and n2 (2D row pass)
-        fl_step = 0.0
-        for b in cfg.step_bcs:
-            fl_step += bluestein_flops_per_line(cfg.n1, b) * px_rank / cfg.n1
-            if cfg.dim == 2:
-                fl_step += bluestein_flops_per_line(cfg.n2, b) * px_rank / cfg.n2
-        fl = fl_step * args.steps / cnt  # per launch
+        if fdom in PAIR_KERNELS:  # one launch per restoration at its degree
+            fl = kernel_flops_per_line(fdom, cfg.n1) * px_rank / cfg.n1
+            model = ("Bluestein pair kernel: (2 x 5 M log2 M + 6 M + 12 m) / 2 per line"
+                     if fdom[2] == "p" else "direct DFT: 5 m log2 m / 2 per line (one complex "
+                     "DFT of length m per pair of lines)")
+        else:
+            # per step: every line of length n1 (1D; 2D column pass) and n2 (2D row pass)
+            fl_step = 0.0
+            for b in cfg.step_bcs:
+                fl_step += bluestein_flops_per_line(cfg.n1, b) * px_rank / cfg.n1
+                if cfg.dim == 2:
+                    fl_step += bluestein_flops_per_line(cfg.n2, b) * px_rank / cfg.n2
+            fl = fl_step * args.steps / cnt  # per launch
+            model = "2 x 5 M log2 M + 6 M + 12 h per line (half-length Bluestein)"
         tf = fl / (ms_tot / cnt / 1e3) / 1e12
         pk, pks = fp64_peak()
         croof = {"kernel": fdom, "bound": "fp64", "achieved": tf, "peak": pk, "unit": "TFLOP/s",
                  "frac": tf / pk, "peak_source": pks,
-                 "alg_flops_per_launch": fl,
-                 "model": "2 x 5 M log2 M + 6 M + 12 h per line (half-length Bluestein; "
-                          "per pair of lines for the full-length pair kernels)"}
+                 "alg_flops_per_launch": fl, "model": model}
     # read g + write f; 7-touch out-of-core model (config 2)
     touches = 7 if (cfg.dim == 2 and cfg.batch == 1) else 2
     pipeline_bytes = sum(touches * (4 if pr == "f32" else 8) for (_, _, pr) in rest) * px_rank

@@ -355,6 +355,11 @@ bool pair_path(const AxisDev& ax) {
 
 void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaStream_t st) {
   const int pairs = (io.gi.count + 1) / 2;
+  // per-kernel timing names (bench.py maps them to their algorithmic bytes)
+  ProfScope ps(ax.rader ? (sa ? "k_qsynth" : "k_qanalyze")
+               : ax.mstages > 0 ? (sa ? "k_msynth" : "k_manalyze")
+                                : (sa ? "k_psynth" : "k_panalyze"),
+               st);
   if (ax.rader) {  // Rader (fd_rader.cuh)
     const size_t sm = rad_smem_bytes(ax.m);
     if (sa) {
@@ -399,7 +404,6 @@ void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaS
 void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
   if (io.gi.count == 0) return;
   if (io.pack == 2 && !io.in_cplx && !io.half && pair_path(ax)) {
-    ProfScope ps("k_analyze", st);
     launch_pair(ax, io, nullptr, st);
     return;
   }
@@ -451,7 +455,6 @@ void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
 void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cudaStream_t st) {
   if (io.gi.count == 0) return;
   if (io.pack == 2 && !io.out_cplx && !io.half && pair_path(ax)) {
-    ProfScope ps(sa.mode == 1 ? "k_synth_filter" : "k_synth", st);
     launch_pair(ax, io, &sa, st);
     return;
   }

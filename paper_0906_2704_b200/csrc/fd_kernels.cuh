@@ -1023,6 +1023,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// bulk prefetch of [src, src + bytes) into L2 (TMA engine, no completion);
+// src and bytes 16-byte aligned
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
   mbar_wait(bar, parity);
 }

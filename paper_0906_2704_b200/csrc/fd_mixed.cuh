@@ -106,6 +106,18 @@ __device__ __forceinline__ void mix_dft(double2* x, const AxisDev& ax, const Mix
 
 constexpr int kMixNT = 256;
 
+// L2 prefetch of the line pair q (contiguous lines only), issued one pair
+// ahead so the load phase of the persistent loop hits L2 instead of HBM
+__device__ __forceinline__ void mix_prefetch_pair(const void* base, const Lines& g, int q, int n) {
+  if (threadIdx.x != 0 || g.elem_stride != 1 || 2 * q >= g.count || (n & 1)) return;
+#pragma unroll
+  for (int l = 2 * q; l < 2 * q + 2; ++l) {
+    if (l >= g.count) break;
+    const double* src = reinterpret_cast<const double*>(base) + line_offset(g, l);
+    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) bulk_prefetch_l2(src, (uint32_t)n * 8);
+  }
+}
+
 // smem: DFT buffer (m complex), twiddle hi / lo tables, output permutation
 __host__ __device__ __forceinline__ size_t mix_smem_bytes(int m) {
   return (size_t)m * 16 + (size_t)(64 + ((m + 63) >> 6)) * 16 + (size_t)m * 4;
@@ -138,6 +150,7 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
   const double isq = ax.inv_sqrt_m;
   const long long nkb32 = io.wstride >> 5;
   for (int q = blockIdx.x; q < npairs; q += gridDim.x) {
+    mix_prefetch_pair(io.in, io.gi, q + gridDim.x, n);
     const int l0 = 2 * q;
     const bool has1 = l0 + 1 < count;
     const double* g0 = in + line_offset(io.gi, l0);
@@ -225,6 +238,7 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
   double* out = reinterpret_cast<double*>(io.out);
   const double isq = ax.inv_sqrt_m;
   for (int q = blockIdx.x; q < npairs; q += gridDim.x) {
+    mix_prefetch_pair(io.in, io.gi, q + gridDim.x, ax.n);
     const int l0 = 2 * q;
     const bool has1 = l0 + 1 < count;
     const double* g0 = in + line_offset(io.gi, l0);
