@@ -150,7 +150,6 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
   const double isq = ax.inv_sqrt_m;
   const long long nkb32 = io.wstride >> 5;
   for (int q = blockIdx.x; q < npairs; q += gridDim.x) {
-    mix_prefetch_pair(io.in, io.gi, q + gridDim.x, n);
     const int l0 = 2 * q;
     const bool has1 = l0 + 1 < count;
     const double* g0 = in + line_offset(io.gi, l0);
@@ -169,6 +168,8 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
     }
     __syncthreads();
     mix_dft(x, ax, tw, kMixNT);
+    // the next pair into L2 while the outputs stream out (written evict-first)
+    mix_prefetch_pair(io.in, io.gi, q + gridDim.x, n);
 
     double* o0 = out + line_offset(io.go, l0);
     double* o1 = has1 ? out + line_offset(io.go, l0 + 1) : nullptr;
@@ -191,14 +192,14 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
       const double2 D = csub(Zk, cconj(Zc));
       const double2 X1 = make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
       if (kk == 0) {
-        o0[hk] = X0.x;
-        if (o1) o1[hk] = X1.x;
+        __stcs(o0 + hk, X0.x);
+        if (o1) __stcs(o1 + hk, X1.x);
       } else {
-        o0[hk + 2 * kk - 1] = X0.x;
-        o0[hk + 2 * kk] = X0.y;
+        __stcs(o0 + hk + 2 * kk - 1, X0.x);
+        __stcs(o0 + hk + 2 * kk, X0.y);
         if (o1) {
-          o1[hk + 2 * kk - 1] = X1.x;
-          o1[hk + 2 * kk] = X1.y;
+          __stcs(o1 + hk + 2 * kk - 1, X1.x);
+          __stcs(o1 + hk + 2 * kk, X1.y);
         }
       }
       if (w0) {

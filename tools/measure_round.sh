@@ -15,6 +15,6 @@ echo "reference rc $?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_c1.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > $O/ncu_launch.log 2>&1
 echo "launch list rc $?"
-timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"k_rsynth|k_ranalyze|k_gcv_screen" \
-  -s 4 -c 3 -o $O/full_c1 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > $O/ncu_full.log 2>&1
+timeout 1200 ncu --set full --import-source on --clock-control none -k regex:"k_psynth|k_panalyze|k_msynth|k_manalyze|k_gcv_exact|k_gcv_moments" \
+  -s 6 -c 6 -o $O/full_c1 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > $O/ncu_full.log 2>&1
 echo "full capture rc $?"
