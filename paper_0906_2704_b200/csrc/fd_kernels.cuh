@@ -1695,6 +1695,14 @@ __device__ __forceinline__ double gcv_mult(const GcvData& g, long long e) {
   return (g.pair && __ldg(&g.pair[e]).y >= 0) ? 2.0 : 1.0;
 }
 
+// L2 bulk prefetch of one item's compact weight row (wstride doubles, a
+// multiple of 32: 16-byte aligned and sized)
+__device__ __forceinline__ void gcv_prefetch_row(const GcvData& g, int item) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g.wred + (long long)item * g.wstride),
+               "r"((uint32_t)(g.wstride * 8))
+               : "memory");
+}
+
 __device__ __forceinline__ double gcv_w(const GcvData& g, int item, long long e) {
   if (g.wred) return __ldg(&g.wred[(long long)item * g.wstride + e]);
   const long long base = (long long)item * g.stride;
@@ -2268,6 +2276,9 @@ __global__ void __launch_bounds__(256) k_gcv_exact(GcvData g, GcvGrid grid,
   const int K = grid.count;
   int* list = lists[wib];
   double* val = vals[wib];
+  // the item's weight row into L2 while the candidate list is built (the
+  // warp then streams it at L2 latency)
+  if (lane == 0 && g.wred) gcv_prefetch_row(g, item);
   const bool all = flag[item] != 0;
   // candidate list (ascending k) in shared memory
   int nc = 0;
@@ -2502,6 +2513,7 @@ __global__ void __launch_bounds__(256) k_gcv_moments(GcvData g, const double* __
   if (warp_global >= g.items * nchunks) return;
   const int item = warp_global / nchunks, ch = warp_global % nchunks;
   if (!need[item]) return;
+  if (lane == 0 && g.wred && nchunks == 1) gcv_prefetch_row(g, item);
   const double mc = center[item];
   constexpr int NB = WITH_B ? J : 1;
   double A[J], B[NB];

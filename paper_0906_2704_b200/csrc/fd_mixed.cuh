@@ -239,7 +239,6 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
   double* out = reinterpret_cast<double*>(io.out);
   const double isq = ax.inv_sqrt_m;
   for (int q = blockIdx.x; q < npairs; q += gridDim.x) {
-    mix_prefetch_pair(io.in, io.gi, q + gridDim.x, ax.n);
     const int l0 = 2 * q;
     const bool has1 = l0 + 1 < count;
     const double* g0 = in + line_offset(io.gi, l0);
@@ -277,6 +276,7 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
     }
     __syncthreads();
     mix_dft(x, ax, tw, kMixNT);
+    mix_prefetch_pair(io.in, io.gi, q + gridDim.x, ax.n);
 
     const Cubic p0 = ho_cubic(ax, ua0), p1 = ho_cubic(ax, ua1);
     const long long eso = io.go.elem_stride;
@@ -288,8 +288,8 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
       const double y0 = z.x * isq, y1 = -z.y * isq;
       const int e = kl + p;
       const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
-      o0[e * eso] = y0 + p0(t);
-      if (o1) o1[e * eso] = y1 + p1(t);
+      __stcs(o0 + e * eso, y0 + p0(t));
+      if (o1) __stcs(o1 + e * eso, y1 + p1(t));
 #pragma unroll
       for (int l = 0; l < kHoMax; ++l)
         if (l < hk && ax.wrap[l] == p) {
