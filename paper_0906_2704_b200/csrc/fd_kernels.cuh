@@ -2262,7 +2262,7 @@ __global__ void __launch_bounds__(256) k_gcv_cand(GcvData g, const double* __res
 // the first minimum, the 1e-12 ties and the bracket are those of the full
 // grid.  One warp per item; candidates in groups of up to 8 (exact_num).
 // Fixed lane order + shuffle tree: deterministic.
-__global__ void __launch_bounds__(256, 3) k_gcv_exact(GcvData g, GcvGrid grid,
+__global__ void __launch_bounds__(256, 4) k_gcv_exact(GcvData g, GcvGrid grid,
                                                    const uint32_t* __restrict__ mask,
                                                    const int* __restrict__ flag,
                                                    const double* __restrict__ den, double* mu_out,
