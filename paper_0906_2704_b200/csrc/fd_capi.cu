@@ -383,8 +383,8 @@ void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaS
   const size_t smem = (size_t)pair_slots(ax.fft.M, ax.m) * sizeof(double2);
 #define FD_PA(L)                                                                           \
   if (sa) {                                                                                \
-    k_psynth<L><<<persistent_grid(k_psynth<L>, PairShape<L>::NT, smem, pairs),             \
-                  PairShape<L>::NT, smem, st>>>(ax, io, *sa);                              \
+    k_psynth<L><<<persistent_grid(k_psynth<L>, PairShape<L, true>::NT, smem, pairs),       \
+                  PairShape<L, true>::NT, smem, st>>>(ax, io, *sa);                        \
   } else {                                                                                 \
     k_panalyze<L><<<persistent_grid(k_panalyze<L>, PairShape<L>::NT, smem, pairs),         \
                     PairShape<L>::NT, smem, st>>>(ax, io);                                 \

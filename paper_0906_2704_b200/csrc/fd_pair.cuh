@@ -24,10 +24,15 @@
 
 namespace fdb {
 
-template <int LOGM>
+// SYN: the synthesis kernel (filter fused into its load phase) runs 512
+// threads at M = 8192; the analysis kernel runs 256 threads with up to 255
+// registers (two radix-16 items per thread per pass) -- measured faster for
+// analyze (4.45 -> 4.31 ms at config 1), much slower for synthesize
+template <int LOGM, bool SYN = false>
 struct PairShape {
   static constexpr int M = 1 << LOGM;
-  static constexpr int NT = M / 16 >= 512 ? 512 : (M / 16 <= 64 ? 64 : M / 16);
+  static constexpr int NT = M / 16 >= (SYN ? 512 : 256) ? (SYN ? 512 : 256)
+                                                         : (M / 16 <= 64 ? 64 : M / 16);
   // LOGM = 1 (mod 4): the Bluestein pass sequence starts with a radix-2 DIF
   // stage whose upper input half is zero padding (m <= M/2), i.e. the stage is
   // (v, v W^j): the load phase writes both halves itself, and the matching
@@ -267,9 +272,9 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
 }
 
 template <int LOGM>
-__global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_psynth(AxisDev ax, LineIO io,
+__global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev ax, LineIO io,
                                                                    SynthArgs sa) {
-  constexpr int NT = PairShape<LOGM>::NT, M = 1 << LOGM;
+  constexpr int NT = PairShape<LOGM, true>::NT, M = 1 << LOGM;
   extern __shared__ double2 sm[];
   const FftTables& T = ax.fft;
   const int m = ax.m, n = ax.n, kl = ax.kl, hk = ax.hk, h = (m - 1) / 2;
@@ -303,7 +308,7 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_psynth(AxisDev ax, L
       return has1 ? coeff_filter_fast(ax, sa, io.gi, l0 + 1, e, c, mu1) : czero();
     };
     double ua0[kHoMax], ua1[kHoMax];
-    using PS = PairShape<LOGM>;
+    using PS = PairShape<LOGM, true>;
     constexpr int KS = PS::FOLD ? (PS::HM / 2 + NT) / NT : 1;  // kk slots (kk <= h < HM/2+1)
     double2 vk[KS], vc[KS];
     auto load_phase = [&](auto ld0, auto ld1) {
