@@ -2504,7 +2504,7 @@ __global__ void k_gcv_pick(const double* __restrict__ G, int items, GcvGrid grid
 // WITH_B: also accumulate B per item (few large items: a B table over all K
 // grid points would cost K passes over the elements); partial holds [A | B].
 template <int J, bool WITH_B>
-__global__ void __launch_bounds__(256, 3) k_gcv_moments(GcvData g, const double* __restrict__ center,
+__global__ void __launch_bounds__(256, WITH_B ? 2 : 3) k_gcv_moments(GcvData g, const double* __restrict__ center,
                                                      const int* __restrict__ need, long long chunk,
                                                      int nchunks, double* partial) {
   // one warp per (item, chunk); lanes stride over elements
