@@ -86,10 +86,49 @@ __device__ __forceinline__ void mix_stage(double2* __restrict__ x, int N, int S,
   }
 }
 
-// in-place DIF DFT of length ax.m (natural order in, mperm order out)
-__device__ __forceinline__ void mix_dft(double2* x, const AxisDev& ax, const MixTw& tw, int nt) {
+// first stage (S = N) reading its inputs through ld(j) instead of x: the
+// analysis computes them from global memory (border fold included), which
+// saves the load phase's shared-memory pass and barrier
+template <int R, class LD>
+__device__ __forceinline__ void mix_stage_first(double2* __restrict__ x, int N, const MixTw& tw,
+                                                int nt, LD&& ld) {
+  const int L = N / R;
+  for (int j = threadIdx.x; j < L; j += nt) {
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = ld(j + q * L);
+    mix_codelet<R>(v);
+    if (L > 1) {
+#pragma unroll
+      for (int p = 1; p < R; ++p) v[p] = cmul(v[p], tw(j * p));
+    }
+#pragma unroll
+    for (int p = 0; p < R; ++p) x[j + p * L] = v[p];
+  }
+}
+
+// in-place DIF DFT of length ax.m (natural order in, mperm order out); with a
+// loader the first stage reads x_j = ld(j) (FIRST_LD)
+template <bool FIRST_LD = false, class LD = int>
+__device__ __forceinline__ void mix_dft(double2* x, const AxisDev& ax, const MixTw& tw, int nt,
+                                        LD&& ld = 0) {
   int S = ax.m;
-  for (int s = 0; s < ax.mstages; ++s) {
+  int s0 = 0;
+  if constexpr (FIRST_LD) {
+    const int r = ax.mrad[0];
+    switch (r) {
+      case 3: mix_stage_first<3>(x, ax.m, tw, nt, ld); break;
+      case 5: mix_stage_first<5>(x, ax.m, tw, nt, ld); break;
+      case 7: mix_stage_first<7>(x, ax.m, tw, nt, ld); break;
+      case 9: mix_stage_first<9>(x, ax.m, tw, nt, ld); break;
+      case 11: mix_stage_first<11>(x, ax.m, tw, nt, ld); break;
+      default: mix_stage_first<13>(x, ax.m, tw, nt, ld); break;
+    }
+    S /= r;
+    s0 = 1;
+    __syncthreads();
+  }
+  for (int s = s0; s < ax.mstages; ++s) {
     const int r = ax.mrad[s];
     switch (r) {
       case 3: mix_stage<3>(x, ax.m, S, tw, nt); break;
@@ -160,14 +199,11 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
     ho_amps_real(ax, ld0, a0);
     ho_amps_real(ax, ld1, a1);
     const Cubic p0 = ho_cubic(ax, a0), p1 = ho_cubic(ax, a1);
-#pragma unroll 8
-    for (int j = threadIdx.x; j < m; j += kMixNT) {
+    mix_dft<true>(x, ax, tw, kMixNT, [&](int j) {
       const int e = kl + j;
       const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
-      x[j] = make_double2(ld0(e) - p0(t), ld1(e) - p1(t));
-    }
-    __syncthreads();
-    mix_dft(x, ax, tw, kMixNT);
+      return make_double2(ld0(e) - p0(t), ld1(e) - p1(t));
+    });
     // the next pair into L2 while the outputs stream out (written evict-first)
     mix_prefetch_pair(io.in, io.gi, q + gridDim.x, n);
 
