@@ -2071,11 +2071,11 @@ void gcv_select_dev(const fd_op* op, const fd_smoother* L, const Analyzed& an, l
 
 void check_deblur_args(const fd_op* op, const fd_smoother* L, int use_gcv, double fixed_mu,
                        double mu_min, double mu_max, int grid_count, const double* mu_used,
-                       const double* curve) {
+                       const double* curve, long long count = 1) {
   if (!op) validation("null operator");
   if (!L) validation("null smoother");
   if (L->op != op) validation("smoother was built for a different operator");
-  if (!mu_used) validation("mu_used output is required");
+  if (!mu_used && count > 0) validation("mu_used output is required");  // empty batches: no outputs
   if (use_gcv || curve) make_grid(mu_min, mu_max, grid_count);  // pipeline.cpp:737-750
   if (!use_gcv && !(fixed_mu > 0.0)) validation("mu must be positive");
 }
@@ -2624,7 +2624,7 @@ int deblur_impl(const fd_op* op, const fd_smoother* L, const void* g, int use_gc
                 double* mu_used, int* best_k, double* curve, double* imag_residue,
                 long long count, void* stream, int f32) {
   return guarded([&] {
-    check_deblur_args(op, L, use_gcv, fixed_mu, mu_min, mu_max, grid_count, mu_used, curve);
+    check_deblur_args(op, L, use_gcv, fixed_mu, mu_min, mu_max, grid_count, mu_used, curve, count);
     if (count <= 0) return;
     Scratch S(as_stream(stream));
     int* status = S.get<int>(1);

@@ -109,9 +109,9 @@ __device__ __forceinline__ void mix_stage_first(double2* __restrict__ x, int N, 
 
 // in-place DIF DFT of length ax.m (natural order in, mperm order out); with a
 // loader the first stage reads x_j = ld(j) (FIRST_LD)
-template <bool FIRST_LD = false, class LD = int>
+template <bool FIRST_LD = false, class LD = int, class AF = int>
 __device__ __forceinline__ void mix_dft(double2* x, const AxisDev& ax, const MixTw& tw, int nt,
-                                        LD&& ld = 0) {
+                                        LD&& ld = 0, AF&& after_first = 0) {
   int S = ax.m;
   int s0 = 0;
   if constexpr (FIRST_LD) {
@@ -124,6 +124,7 @@ __device__ __forceinline__ void mix_dft(double2* x, const AxisDev& ax, const Mix
       case 11: mix_stage_first<11>(x, ax.m, tw, nt, ld); break;
       default: mix_stage_first<13>(x, ax.m, tw, nt, ld); break;
     }
+    after_first();  // before the stage barrier
     S /= r;
     s0 = 1;
     __syncthreads();
@@ -157,9 +158,10 @@ __device__ __forceinline__ void mix_prefetch_pair(const void* base, const Lines&
   }
 }
 
-// smem: DFT buffer (m complex), twiddle hi / lo tables, output permutation
+// smem: DFT buffer (m complex), twiddle hi / lo tables, output permutation,
+// the two zero-line flag words (zf_add / zf_take)
 __host__ __device__ __forceinline__ size_t mix_smem_bytes(int m) {
-  return (size_t)m * 16 + (size_t)(64 + ((m + 63) >> 6)) * 16 + (size_t)m * 4;
+  return (size_t)m * 16 + (size_t)(64 + ((m + 63) >> 6)) * 16 + (size_t)m * 4 + 8;
 }
 // twiddle tables and permutation into shared memory (before the first barrier)
 __device__ __forceinline__ MixTw mix_setup(double2* sm, const AxisDev& ax, const int** perm) {
@@ -170,6 +172,7 @@ __device__ __forceinline__ MixTw mix_setup(double2* sm, const AxisDev& ax, const
   for (int i = threadIdx.x; i < 64; i += blockDim.x) lo[i] = i < m ? ax.mtw[i] : czero();
   for (int i = threadIdx.x; i < nhi; i += blockDim.x) hi[i] = ax.mtw[i << 6];
   for (int i = threadIdx.x; i < m; i += blockDim.x) ps[i] = ax.mperm[i];
+  if (threadIdx.x < 2) ps[m + threadIdx.x] = 0;  // zero-line flags
   *perm = ps;
   return MixTw{lo, hi};
 }
@@ -188,7 +191,8 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
   const long long es = io.gi.elem_stride;
   const double isq = ax.inv_sqrt_m;
   const long long nkb32 = io.wstride >> 5;
-  for (int q = blockIdx.x; q < npairs; q += gridDim.x) {
+  int* zf = const_cast<int*>(perm) + m;
+  for (int q = blockIdx.x, it = 0; q < npairs; q += gridDim.x, ++it) {
     const int l0 = 2 * q;
     const bool has1 = l0 + 1 < count;
     const double* g0 = in + line_offset(io.gi, l0);
@@ -199,11 +203,15 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
     ho_amps_real(ax, ld0, a0);
     ho_amps_real(ax, ld1, a1);
     const Cubic p0 = ho_cubic(ax, a0), p1 = ho_cubic(ax, a1);
+    long long nzb0 = 0, nzb1 = 0;  // OR of the bit patterns of line 0 / 1 (-0.0 counts as nonzero)
     mix_dft<true>(x, ax, tw, kMixNT, [&](int j) {
       const int e = kl + j;
       const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
-      return make_double2(ld0(e) - p0(t), ld1(e) - p1(t));
-    });
+      const double y0 = ld0(e), y1 = ld1(e);
+      nzb0 |= __double_as_longlong(y0);  // integer pipe: the fp64 pipe is the bound
+      nzb1 |= __double_as_longlong(y1);
+      return make_double2(y0 - p0(t), y1 - p1(t));
+    }, [&] { zf_add(zf, it, (nzb0 != 0 ? 1 : 0) | (nzb1 != 0 ? 2 : 0)); });
     // the next pair into L2 while the outputs stream out (written evict-first)
     mix_prefetch_pair(io.in, io.gi, q + gridDim.x, n);
 
@@ -211,6 +219,10 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
     double* o1 = has1 ? out + line_offset(io.go, l0 + 1) : nullptr;
     double* w0 = io.wout ? io.wout + (long long)l0 * io.wstride : nullptr;
     double* w1 = (w0 && has1) ? w0 + io.wstride : nullptr;
+    // an all-zero line gets exactly zero coefficients (its partner's DFT
+    // round-off would otherwise leak into it through the Hermitian split)
+    const int nz = zf_take(zf, it);
+    const bool z0 = !(nz & 1) && ho_zero(a0), z1 = !(nz & 2) && ho_zero(a1);
     auto wset = [&](int line, double* wl, long long i, double v) {
       wl[i] = v;
       if (io.wout32) {
@@ -224,9 +236,9 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
     for (int kk = threadIdx.x; kk <= h; kk += kMixNT) {
       const double2 Zk = x[perm[kk]];
       const double2 Zc = kk ? x[perm[m - kk]] : Zk;
-      const double2 X0 = cscale(cadd(Zk, cconj(Zc)), 0.5 * isq);
       const double2 D = csub(Zk, cconj(Zc));
-      const double2 X1 = make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
+      const double2 X0 = z0 ? czero() : cscale(cadd(Zk, cconj(Zc)), 0.5 * isq);
+      const double2 X1 = z1 ? czero() : make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
       if (kk == 0) {
         __stcs(o0 + hk, X0.x);
         if (o1) __stcs(o1 + hk, X1.x);

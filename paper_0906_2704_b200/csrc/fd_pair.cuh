@@ -60,6 +60,7 @@ __device__ __forceinline__ void pair_conv(double2* x, const FftTables& T, const 
 }
 
 // smem slots (double2) of the pair kernels: buffer, twiddles, chirp, mbarrier
+// (+ the two zero-line flag words in the same slot)
 __host__ __device__ __forceinline__ int pair_slots(int M, int m) {
   return pidx(M) + 1 + kTwSlots + m + 1;
 }
@@ -91,6 +92,29 @@ __device__ __forceinline__ void ho_amps_real(const AxisDev& ax, LD ld, double (&
     for (int q = 0; q < kHoMax; ++q) v += ax.sinv[l * kHoMax + q] * r[q];
     a[l] = v;
   }
+}
+
+// Zero-line flags of the line-pair kernels: two ints in shared memory, one per
+// parity of the CTA's pair counter.  Warps OR their "line l has a nonzero
+// input" bits in during the load phase (before an existing barrier); the post
+// phase reads them and thread 0 clears the other parity's word for the next
+// pair (the end-of-pair barrier orders that against its writers).
+__device__ __forceinline__ void zf_add(int* zf, int it, int nzl) {
+  nzl = (int)__reduce_or_sync(0xffffffffu, (unsigned)nzl);
+  if ((threadIdx.x & 31) == 0 && nzl) atomicOr(&zf[it & 1], nzl);
+}
+__device__ __forceinline__ int zf_take(int* zf, int it) {
+  const int v = zf[it & 1];
+  if (threadIdx.x == 0) zf[(it + 1) & 1] = 0;
+  return v;
+}
+
+// all border amplitudes of a line exactly zero
+__device__ __forceinline__ bool ho_zero(const double (&a)[kHoMax]) {
+  bool z = true;
+#pragma unroll
+  for (int l = 0; l < kHoMax; ++l) z = z && a[l] == 0.0;
+  return z;
 }
 
 // reduced GCV index of border amplitude l (build_pairs: left singles, interior
@@ -150,6 +174,8 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
   for (int j = threadIdx.x; j < m; j += NT) cs[j] = T.chirp[j];
   PairStage stg = pair_stage_init(x, M, m, n, io.gi,
                                   reinterpret_cast<uint64_t*>(sm + pair_slots(M, m) - 1));
+  int* zf = reinterpret_cast<int*>(sm + pair_slots(M, m) - 1) + 2;
+  if (threadIdx.x < 2) zf[threadIdx.x] = 0;
   __syncthreads();
   const int count = io.gi.count, npairs = (count + 1) / 2;
   if (threadIdx.x == 0) pair_issue(stg, io.in, io.gi, blockIdx.x, n);
@@ -158,7 +184,7 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
   const long long es = io.gi.elem_stride;
   const double isq = ax.inv_sqrt_m;
   const long long nkb32 = io.wstride >> 5;
-  for (int q = blockIdx.x; q < npairs; q += gridDim.x) {
+  for (int q = blockIdx.x, it = 0; q < npairs; q += gridDim.x, ++it) {
     const int l0 = 2 * q;
     const bool has1 = l0 + 1 < count;
     const bool st = pair_staged(stg, io.in, io.gi, q);
@@ -174,6 +200,7 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
     Cubic p0, p1;
     using PS = PairShape<LOGM>;
     double2 vr[PS::FOLD ? PS::JS : 1];
+    long long nzb0 = 0, nzb1 = 0;  // OR of the bit patterns of line 0 / 1 (-0.0 counts as nonzero)
     auto load_phase = [&](auto ld0, auto ld1) {
       ho_amps_real(ax, ld0, a0);
       ho_amps_real(ax, ld1, a1);
@@ -182,7 +209,10 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
       auto val = [&](int j) {
         const int e = kl + j;
         const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
-        return cmul(make_double2(ld0(e) - p0(t), ld1(e) - p1(t)), cs[j]);
+        const double y0 = ld0(e), y1 = ld1(e);
+        nzb0 |= __double_as_longlong(y0);  // integer pipe: the fp64 pipe is the bound
+      nzb1 |= __double_as_longlong(y1);
+        return cmul(make_double2(y0 - p0(t), y1 - p1(t)), cs[j]);
       };
       if constexpr (PS::FOLD) {
 #pragma unroll
@@ -200,6 +230,9 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
     else
       load_phase([&](int e) { return __ldg(g0 + e * es); },
                  [&](int e) { return has1 ? __ldg(g1 + e * es) : 0.0; });
+    // an all-zero line gets exactly zero coefficients (its partner's DFT
+    // round-off would otherwise leak into it through the Hermitian split)
+    zf_add(zf, it, (nzb0 != 0 ? 1 : 0) | (nzb1 != 0 ? 2 : 0));
     __syncthreads();
     if constexpr (PS::FOLD) {  // first DIF stage (v, v W^j), staged input consumed
 #pragma unroll
@@ -230,12 +263,14 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
       }
     };
     double* w1 = (w0 && has1) ? w0 + io.wstride : nullptr;
+    const int nz = zf_take(zf, it);
+    const bool z0 = !(nz & 1) && ho_zero(a0), z1 = !(nz & 2) && ho_zero(a1);
     for (int kk = threadIdx.x; kk <= h; kk += NT) {
       const double2 Zk = cmul(x[pidx(kk)], cs[kk]);
       const double2 Zc = kk ? cmul(x[pidx(m - kk)], cs[m - kk]) : Zk;
-      const double2 X0 = cscale(cadd(Zk, cconj(Zc)), 0.5 * isq);
       const double2 D = csub(Zk, cconj(Zc));
-      const double2 X1 = make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
+      const double2 X0 = z0 ? czero() : cscale(cadd(Zk, cconj(Zc)), 0.5 * isq);
+      const double2 X1 = z1 ? czero() : make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
       if (kk == 0) {
         o0[hk] = X0.x;
         if (o1) o1[hk] = X1.x;
