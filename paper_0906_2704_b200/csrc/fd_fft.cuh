@@ -220,7 +220,7 @@ __device__ __forceinline__ void mid_pass(double2* __restrict__ x, int M,
     const int base = it * R;  // S = R: SR = 1, j0 = 0
     double2 v[R], bh[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) bh[q] = __ldg(&bhat[q * items + it]);
+    for (int q = 0; q < R; ++q) bh[q] = __ldcg(&bhat[q * items + it]);  // L2 only: keep L1 for the filter tables
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = (!PAD || base + q < nvalid) ? x[pidx(base + q)] : czero();
     (void)twstep;
@@ -452,7 +452,7 @@ __device__ __forceinline__ void mid_pass_t(double2* __restrict__ x,
     double2* xb = x + pidx(base);
     double2 v[R], bh[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) bh[q] = __ldg(&bhat[q * ITEMS + it]);
+    for (int q = 0; q < R; ++q) bh[q] = __ldcg(&bhat[q * ITEMS + it]);  // L2 only: keep L1 for the filter tables
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = (!PAD || base + q < nvalid) ? xb[q] : czero();
 #pragma unroll
