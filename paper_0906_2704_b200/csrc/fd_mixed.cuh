@@ -65,6 +65,19 @@ struct MixTw {
   __device__ __forceinline__ double2 operator()(int t) const { return cmul(hi[t >> 6], lo[t & 63]); }
 };
 
+// v[p] *= w1^p for p = 1 .. R-1, the powers by a squaring tree (depth
+// log2 R, <= 4 roundings): two shared-memory loads per item instead of
+// 2 (R - 1) scattered twiddle-table reads
+template <int R>
+__device__ __forceinline__ void mix_twiddle(double2 (&v)[R], double2 w1) {
+  double2 w[R];
+  w[1] = w1;
+#pragma unroll
+  for (int p = 2; p < R; ++p) w[p] = (p & 1) ? cmul(w[p - 1], w1) : cmul(w[p / 2], w[p / 2]);
+#pragma unroll
+  for (int p = 1; p < R; ++p) v[p] = cmul(v[p], w[p]);
+}
+
 template <int R>
 __device__ __forceinline__ void mix_stage(double2* __restrict__ x, int N, int S, const MixTw& tw,
                                           int nt) {
@@ -76,11 +89,7 @@ __device__ __forceinline__ void mix_stage(double2* __restrict__ x, int N, int S,
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = xb[q * L];
     mix_codelet<R>(v);
-    if (L > 1) {
-      const int t1 = j * tstep;
-#pragma unroll
-      for (int p = 1; p < R; ++p) v[p] = cmul(v[p], tw(t1 * p));
-    }
+    if (L > 1) mix_twiddle<R>(v, tw(j * tstep));
 #pragma unroll
     for (int p = 0; p < R; ++p) xb[p * L] = v[p];
   }
@@ -98,10 +107,7 @@ __device__ __forceinline__ void mix_stage_first(double2* __restrict__ x, int N, 
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = ld(j + q * L);
     mix_codelet<R>(v);
-    if (L > 1) {
-#pragma unroll
-      for (int p = 1; p < R; ++p) v[p] = cmul(v[p], tw(j * p));
-    }
+    if (L > 1) mix_twiddle<R>(v, tw(j));
 #pragma unroll
     for (int p = 0; p < R; ++p) x[j + p * L] = v[p];
   }
