@@ -367,6 +367,18 @@ __device__ __forceinline__ double2 tw_t(const TwSm& tw, int j) {
   return cmul(tw.hi[j >> LOB], tw.lo[j & ((1 << LOB) - 1)]);
 }
 
+// ws[st] = w^(2^st): the twiddles of the LR radix-2 stages of one item from
+// one table lookup and LR-1 squarings (relative error <= ~2^LR ulp)
+template <int LR>
+__device__ __forceinline__ void tw_pow2(double2 (&ws)[LR], double2 w) {
+  ws[0] = w;
+#pragma unroll
+  for (int st = 1; st < LR; ++st) {
+    const double2 a = ws[st - 1];
+    ws[st] = make_double2(fma(a.x, a.x, -a.y * a.y), 2.0 * a.x * a.y);
+  }
+}
+
 template <int LOGM, int LR, int S, bool PAD, int NTH = 0>
 __device__ __forceinline__ void dif_pass_t(double2* __restrict__ x, const TwSm& tw, int nvalid) {
   using F = FftShape<LOGM, NTH>;
@@ -384,10 +396,12 @@ __device__ __forceinline__ void dif_pass_t(double2* __restrict__ x, const TwSm& 
     double2 v[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = (!PAD || base + q * SR < nvalid) ? xb[q * QS] : czero();
+    double2 ws[LR];
+    tw_pow2<LR>(ws, tw_t<F::LOB>(tw, j0 * TWSTEP));
 #pragma unroll
     for (int st = 0; st < LR; ++st) {
       const int half = R >> (st + 1);
-      const double2 w = tw_t<F::LOB>(tw, (j0 * TWSTEP) << st);
+      const double2 w = ws[st];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         if (q & half) continue;
@@ -419,10 +433,12 @@ __device__ __forceinline__ void dit_pass_t(double2* __restrict__ x, const TwSm& 
     double2 v[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = xb[q * QS];
+    double2 ws[LR];
+    tw_pow2<LR>(ws, tw_t<F::LOB>(tw, j0 * TWSTEP));
 #pragma unroll
     for (int st = LR - 1; st >= 0; --st) {
       const int half = R >> (st + 1);
-      const double2 w = tw_t<F::LOB>(tw, (j0 * TWSTEP) << st);
+      const double2 w = ws[st];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         if (q & half) continue;

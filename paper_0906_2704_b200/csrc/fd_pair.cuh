@@ -320,13 +320,15 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
   for (int j = threadIdx.x; j < m; j += NT) cs[j] = T.chirp[j];
   PairStage stg = pair_stage_init(x, M, m, n, io.gi,
                                   reinterpret_cast<uint64_t*>(sm + pair_slots(M, m) - 1));
+  int* zf = reinterpret_cast<int*>(sm + pair_slots(M, m) - 1) + 2;
+  if (threadIdx.x < 2) zf[threadIdx.x] = 0;
   __syncthreads();
   const int count = io.gi.count, npairs = (count + 1) / 2;
   if (threadIdx.x == 0) pair_issue(stg, io.in, io.gi, blockIdx.x, n);
   const double* in = reinterpret_cast<const double*>(io.in);
   double* out = reinterpret_cast<double*>(io.out);
   const double isq = ax.inv_sqrt_m;
-  for (int q = blockIdx.x; q < npairs; q += gridDim.x) {
+  for (int q = blockIdx.x, it = 0; q < npairs; q += gridDim.x, ++it) {
     const int l0 = 2 * q;
     const bool has1 = l0 + 1 < count;
     const bool st = pair_staged(stg, io.in, io.gi, q);
@@ -346,6 +348,10 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
     using PS = PairShape<LOGM, true>;
     constexpr int KS = PS::FOLD ? (PS::HM / 2 + NT) / NT : 1;  // kk slots (kk <= h < HM/2+1)
     double2 vk[KS], vc[KS];
+    // OR of the filtered coefficients' bit patterns: a line whose filtered
+    // coefficients are all zero is written as exact zeros (its partner's
+    // inverse-DFT round-off would otherwise leak into it)
+    long long nzb0 = 0, nzb1 = 0;
     auto load_phase = [&](auto ld0, auto ld1) {
 #pragma unroll
       for (int l = 0; l < kHoMax; ++l) {
@@ -366,6 +372,8 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
         }
         X0 = f0(e, X0);
         X1 = f1(e, X1);
+        nzb0 |= __double_as_longlong(X0.x) | __double_as_longlong(X0.y);
+        nzb1 |= __double_as_longlong(X1.x) | __double_as_longlong(X1.y);
         a = cmul(make_double2(X0.x - X1.y, -(X0.y + X1.x)), cs[kk]);
         b = kk ? cmul(make_double2(X0.x + X1.y, X0.y - X1.x), cs[m - kk]) : czero();
       };
@@ -391,6 +399,7 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
     else
       load_phase([&](int i) { return __ldg(g0 + i); },
                  [&](int i) { return has1 ? __ldg(g1 + i) : 0.0; });
+    zf_add(zf, it, (nzb0 != 0 ? 1 : 0) | (nzb1 != 0 ? 2 : 0));
     __syncthreads();
     if constexpr (PS::FOLD) {  // first DIF stage (v, v W^j); zero padding written explicitly
 #pragma unroll
@@ -418,10 +427,12 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
     const long long eso = io.go.elem_stride;
     double* o0 = out + line_offset(io.go, l0);
     double* o1 = has1 ? out + line_offset(io.go, l0 + 1) : nullptr;
+    const int nz = zf_take(zf, it);
+    const double s0 = (nz & 1) ? isq : 0.0, s1 = (nz & 2) ? -isq : 0.0;
 #pragma unroll 4
     for (int p = threadIdx.x; p < m; p += NT) {
       const double2 z = cmul(x[pidx(p)], cs[p]);  // conj of (F^H v)_p sqrt(m)
-      const double y0 = z.x * isq, y1 = -z.y * isq;
+      const double y0 = z.x * s0, y1 = z.y * s1;
       const int e = kl + p;
       const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
       o0[e * eso] = y0 + p0(t);
