@@ -90,6 +90,18 @@ __device__ __forceinline__ TwSm load_twiddles(double2* slots, const FftTables& T
   return TwSm{lo, hi, lob};
 }
 
+// ws[st] = w^(2^st): the twiddles of the LR radix-2 stages of one item from
+// one table lookup and LR-1 squarings (relative error <= ~2^LR ulp)
+template <int LR>
+__device__ __forceinline__ void tw_pow2(double2 (&ws)[LR], double2 w) {
+  ws[0] = w;
+#pragma unroll
+  for (int st = 1; st < LR; ++st) {
+    const double2 a = ws[st - 1];
+    ws[st] = make_double2(fma(a.x, a.x, -a.y * a.y), 2.0 * a.x * a.y);
+  }
+}
+
 // One fused pass of LOGR radix-2 decimation-in-frequency stages on blocks of
 // size S (S >= 2^LOGR).  Items are disjoint element sets, so the pass is
 // in-place with no barrier inside.
@@ -109,10 +121,12 @@ __device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S, 
 #pragma unroll
     for (int q = 0; q < R; ++q)
       v[q] = (!PAD || base + q * SR < nvalid) ? x[pidx(base + q * SR)] : czero();
+    double2 ws[LOGR];
+    tw_pow2<LOGR>(ws, tw(j0 * twstep));
 #pragma unroll
     for (int st = 0; st < LOGR; ++st) {
       const int half = R >> (st + 1);
-      const double2 w = tw((j0 * twstep) << st);
+      const double2 w = ws[st];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         if (q & half) continue;
@@ -143,10 +157,12 @@ __device__ __forceinline__ void dit_pass(double2* __restrict__ x, int M, int S, 
     double2 v[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = x[pidx(base + q * SR)];
+    double2 ws[LOGR];
+    tw_pow2<LOGR>(ws, tw(j0 * twstep));
 #pragma unroll
     for (int st = LOGR - 1; st >= 0; --st) {
       const int half = R >> (st + 1);
-      const double2 w = tw((j0 * twstep) << st);
+      const double2 w = ws[st];
 #pragma unroll
       for (int q = 0; q < R; ++q) {
         if (q & half) continue;
@@ -365,18 +381,6 @@ struct FftShape {
 template <int LOB>
 __device__ __forceinline__ double2 tw_t(const TwSm& tw, int j) {
   return cmul(tw.hi[j >> LOB], tw.lo[j & ((1 << LOB) - 1)]);
-}
-
-// ws[st] = w^(2^st): the twiddles of the LR radix-2 stages of one item from
-// one table lookup and LR-1 squarings (relative error <= ~2^LR ulp)
-template <int LR>
-__device__ __forceinline__ void tw_pow2(double2 (&ws)[LR], double2 w) {
-  ws[0] = w;
-#pragma unroll
-  for (int st = 1; st < LR; ++st) {
-    const double2 a = ws[st - 1];
-    ws[st] = make_double2(fma(a.x, a.x, -a.y * a.y), 2.0 * a.x * a.y);
-  }
 }
 
 template <int LOGM, int LR, int S, bool PAD, int NTH = 0>
