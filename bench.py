@@ -302,19 +302,26 @@ def ncu_traffic(name, cfg):
     if not files:
         return None, None
     txt = open(files[-1]).read()
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "us": 1e-3, "ms": 1.0,
+             "s": 1e3}
+    best = None  # the longest matching launch: setup launches of the same kernel are tiny
     for blk in txt.split("== ")[1:]:
         head = blk.split("\n", 1)[0]
         if not any(re.search(rf"\b{k}\b", head) for k in NCU_NAMES.get(name, (name,))):
             continue
         r = re.search(r"dram_read\s+([\d.]+)\s+(\w+)", blk)
         w = re.search(r"dram_write\s+([\d.]+)\s+(\w+)", blk)
-        if not (r and w):
+        d = re.search(r"duration\s+([\d.]+)\s+(\w+)", blk)
+        if not (r and w and d):
             continue
-        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        dur = float(d.group(1)) * scale.get(d.group(2), 1)
         tot = float(r.group(1)) * scale.get(r.group(2), 1) + float(w.group(1)) * scale.get(
             w.group(2), 1)
-        return tot, os.path.relpath(files[-1], ROOT)
-    return None, None
+        if best is None or dur > best[0]:
+            best = (dur, tot)
+    if best is None:
+        return None, None
+    return best[1], os.path.relpath(files[-1], ROOT)
 
 
 def bluestein_flops_per_line(n, bc):

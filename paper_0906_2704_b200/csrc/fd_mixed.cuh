@@ -292,7 +292,8 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
   const double* in = reinterpret_cast<const double*>(io.in);
   double* out = reinterpret_cast<double*>(io.out);
   const double isq = ax.inv_sqrt_m;
-  for (int q = blockIdx.x; q < npairs; q += gridDim.x) {
+  int* zf = const_cast<int*>(perm) + m;
+  for (int q = blockIdx.x, it = 0; q < npairs; q += gridDim.x, ++it) {
     const int l0 = 2 * q;
     const bool has1 = l0 + 1 < count;
     const double* g0 = in + line_offset(io.gi, l0);
@@ -311,6 +312,7 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
       ua0[l] = l < hk ? f0(ho_coef_elem(ax, l), make_double2(ld0(l), 0.0)).x : 0.0;
       ua1[l] = l < hk ? f1(ho_coef_elem(ax, l), make_double2(ld1(l), 0.0)).x : 0.0;
     }
+    long long nzb0 = 0, nzb1 = 0;  // all-zero filtered lines are written as exact zeros
 #pragma unroll 4
     for (int kk = threadIdx.x; kk <= h; kk += kMixNT) {
       const int e = kl + kk;
@@ -324,10 +326,13 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
       }
       X0 = f0(e, X0);
       X1 = f1(e, X1);
+      nzb0 |= __double_as_longlong(X0.x) | __double_as_longlong(X0.y);
+      nzb1 |= __double_as_longlong(X1.x) | __double_as_longlong(X1.y);
       // F^H v = conj(F conj v), v = X0 + i X1 (natural order input)
       x[kk] = make_double2(X0.x - X1.y, -(X0.y + X1.x));
       if (kk) x[m - kk] = make_double2(X0.x + X1.y, X0.y - X1.x);
     }
+    zf_add(zf, it, (nzb0 != 0 ? 1 : 0) | (nzb1 != 0 ? 2 : 0));
     __syncthreads();
     mix_dft(x, ax, tw, kMixNT);
     mix_prefetch_pair(io.in, io.gi, q + gridDim.x, ax.n);
@@ -336,10 +341,12 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
     const long long eso = io.go.elem_stride;
     double* o0 = out + line_offset(io.go, l0);
     double* o1 = has1 ? out + line_offset(io.go, l0 + 1) : nullptr;
+    const int nz = zf_take(zf, it);
+    const double s0 = (nz & 1) ? isq : 0.0, s1 = (nz & 2) ? -isq : 0.0;
 #pragma unroll 4
     for (int p = threadIdx.x; p < m; p += kMixNT) {
       const double2 z = x[perm[p]];
-      const double y0 = z.x * isq, y1 = -z.y * isq;
+      const double y0 = z.x * s0, y1 = z.y * s1;
       const int e = kl + p;
       const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
       __stcs(o0 + e * eso, y0 + p0(t));

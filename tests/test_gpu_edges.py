@@ -96,7 +96,7 @@ def test_constant_and_zero_items_in_batch(bc):
     gives an identically zero curve: ties everywhere, the geometric mean of the
     grid (regularize.cpp:180-190), best_k 0 -- the pair analysis kernels flag
     all-zero lines so their partner's DFT round-off does not leak into them --
-    and a restoration at round-off level.  Both sit among
+    and an exactly zero restoration.  Both sit among
     ordinary items of a batch large enough for the tensor-core screen."""
     n, B = 512, 200
     psf = onesided(15, 0.2) if bc != O.HOC_COSINE else gauss(10, 3.0)
@@ -115,8 +115,9 @@ def test_constant_and_zero_items_in_batch(bc):
     curve = np_(rep.gcv_curve)
     assert np.max(curve[5]) < 1e-20 * np.min(curve[4])
     assert np.max(np.abs(np_(rep.restored)[5] - 0.75)) < 1e-12
-    # the zero item's restoration is exact zero up to its pair partner's
-    # synthesis round-off (two real lines share one complex inverse DFT)
+    # the zero item's restoration is exactly zero, as the reference's (its
+    # pair partner's inverse-DFT round-off must not leak into it: the pair
+    # synthesis kernels flag all-zero filtered lines)
     f = np_(rep.restored)
-    assert np.max(np.abs(f[6])) <= 1e-14 * np.max(np.abs(f[7]))
+    assert np.max(np.abs(f[6])) == 0.0
     assert abs(np_(rep.mu_used)[6] - np.sqrt(search[0] * search[1])) < 1e-12
