@@ -43,6 +43,19 @@ struct PairShape {
   static constexpr int JS = (HM + NT - 1) / NT;  // register slots per thread (j < HM)
 };
 
+// tw(j) at j = j0 + t NT for the FOLD phases: with NT a multiple of the lo
+// table's length the lo factor is the same for every t, so each thread loads
+// it once and the per-element lookup is one (warp-broadcast) hi entry
+template <int LOGM>
+struct FoldTw {
+  static constexpr int LOB = FftShape<LOGM>::LOB;
+  const double2* hi;
+  double2 lo;
+  __device__ __forceinline__ FoldTw(const TwSm& tw, int j0)
+      : hi(tw.hi), lo(tw.lo[j0 & ((1 << LOB) - 1)]) {}
+  __device__ __forceinline__ double2 operator()(int j) const { return cmul(hi[j >> LOB], lo); }
+};
+
 // the Bluestein convolution of the pair kernels; with FOLD the buffer must
 // hold both halves of the first DIF stage already, and on return the lower
 // half [0, m) holds the result
@@ -50,9 +63,11 @@ template <int LOGM, int NT>
 __device__ __forceinline__ void pair_conv(double2* x, const FftTables& T, const TwSm& tw, int m) {
   using S = PairShape<LOGM>;
   if constexpr (S::FOLD) {
+    static_assert(NT % (1 << FoldTw<LOGM>::LOB) == 0, "FoldTw needs NT % lo length == 0");
     bluestein_rec<LOGM, 1, S::HM, NT>(x, T.bhat, tw, S::M);
+    const FoldTw<LOGM> ft(tw, threadIdx.x);
     for (int k = threadIdx.x; k < m; k += NT)
-      x[pidx(k)] = cadd(x[pidx(k)], cmulc(x[pidx(k + S::HM)], tw(k)));
+      x[pidx(k)] = cadd(x[pidx(k)], cmulc(x[pidx(k + S::HM)], ft(k)));
     __syncthreads();
   } else {
     bluestein_t<LOGM, NT>(x, T, tw, m);
@@ -235,12 +250,13 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
     zf_add(zf, it, (nzb0 != 0 ? 1 : 0) | (nzb1 != 0 ? 2 : 0));
     __syncthreads();
     if constexpr (PS::FOLD) {  // first DIF stage (v, v W^j), staged input consumed
+      const FoldTw<LOGM> ft(tw, threadIdx.x);
 #pragma unroll
       for (int t = 0; t < PS::JS; ++t) {
         const int j = threadIdx.x + t * NT;
         if (j < PS::HM) {
           x[pidx(j)] = vr[t];
-          x[pidx(j + PS::HM)] = cmul(vr[t], tw(j));
+          x[pidx(j + PS::HM)] = cmul(vr[t], ft(j));
         }
       }
       __syncthreads();
@@ -402,15 +418,16 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
     zf_add(zf, it, (nzb0 != 0 ? 1 : 0) | (nzb1 != 0 ? 2 : 0));
     __syncthreads();
     if constexpr (PS::FOLD) {  // first DIF stage (v, v W^j); zero padding written explicitly
+      const FoldTw<LOGM> fk(tw, threadIdx.x), fc(tw, m - threadIdx.x);
 #pragma unroll
       for (int t = 0; t < KS; ++t) {
         const int kk = threadIdx.x + t * NT;
         if (kk <= h) {
           x[pidx(kk)] = vk[t];
-          x[pidx(kk + PS::HM)] = cmul(vk[t], tw(kk));
+          x[pidx(kk + PS::HM)] = cmul(vk[t], fk(kk));
           if (kk) {
             x[pidx(m - kk)] = vc[t];
-            x[pidx(m - kk + PS::HM)] = cmul(vc[t], tw(m - kk));
+            x[pidx(m - kk + PS::HM)] = cmul(vc[t], fc(m - kk));
           }
         }
       }
