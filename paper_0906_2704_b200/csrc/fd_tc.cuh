@@ -25,7 +25,13 @@
 namespace fdb {
 
 constexpr int kTcBM = 128;     // items per CTA (UMMA M)
-constexpr int kTcBK = 32;      // elements per pipeline stage (4 MMAs of K = 8)
+constexpr int kTcBK = 32;      // elements per tile (the K extent of one stored tile)
+// elements per pipeline stage: half a tile.  The tile is chunk-major (16-byte
+// chunks of 4 elements for all rows, see tc_tile_index), so each half is one
+// contiguous block and the stage is still one bulk copy per operand; halving
+// the stage doubles the number of stages that fit (4 instead of 2 at BN = 256
+// with the hi/lo split), so the producer refills at a finer grain.
+constexpr int kTcSK = 16;
 // candidate tolerance tau (screen_tau): a relative error bound eps of num~,
 //   single TF32 pass: 2 * 2^-10 (input truncation) + accumulation,
 //   3xTF32 split:     3 * 2^-21 (hi/lo products)  + accumulation,
@@ -111,7 +117,7 @@ __host__ __device__ constexpr int tc_tmem_cols(int n) {
   return n <= 32 ? 32 : n <= 64 ? 64 : n <= 128 ? 128 : n <= 256 ? 256 : 512;
 }
 __host__ __device__ constexpr int tc_stage_bytes(int BN, bool split) {
-  return (split ? 2 : 1) * (kTcBM + BN) * kTcBK * 4;
+  return (split ? 2 : 1) * (kTcBM + BN) * kTcSK * 4;
 }
 // as many stages as fit next to the barriers in 227 KB (at least 2)
 __host__ __device__ constexpr int tc_stages(int BN, bool split) {
@@ -160,8 +166,10 @@ __global__ void __launch_bounds__(128, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   constexpr int NA = SPLIT ? 2 : 1, NB = SPLIT ? 2 : 1;
-  constexpr int ABYTES = kTcBM * kTcBK * 4;
-  constexpr int BBYTES = BN * kTcBK * 4;
+  constexpr int ABYTES = kTcBM * kTcSK * 4;
+  constexpr int BBYTES = BN * kTcSK * 4;
+  constexpr int NSUB = kTcBK / kTcSK;  // stages per stored tile
+  const int nsb = nkb * NSUB;
   constexpr int STAGE = NA * ABYTES + NB * BBYTES;
   constexpr int NST = tc_stages(BN, SPLIT);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + NST * STAGE);
@@ -193,13 +201,14 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
 
   if (warp == 0 && lane == 0) {  // producer
-    for (int kb = 0; kb < nkb; ++kb) {
+    for (int kb = 0; kb < nsb; ++kb) {
       const int s = kb % NST;
       mbar_wait(&empty[s], (uint32_t)(((kb / NST) & 1) ^ 1));
       mbar_expect_tx(&full[s], STAGE);
       uint8_t* dst = smem + s * STAGE;
-      const long long ta = ((long long)rb * nkb + kb) * (kTcBM * kTcBK);
-      const long long tb = (long long)kb * (BN * kTcBK);
+      const int t = kb / NSUB, half = kb % NSUB;
+      const long long ta = ((long long)rb * nkb + t) * (kTcBM * kTcBK) + half * (kTcBM * kTcSK);
+      const long long tb = (long long)t * (BN * kTcBK) + half * (BN * kTcSK);
       bulk_g2s(dst, Ah + ta, ABYTES, &full[s]);
       if (SPLIT) bulk_g2s(dst + ABYTES, Al + ta, ABYTES, &full[s]);
       bulk_g2s(dst + NA * ABYTES, Bh + tb, BBYTES, &full[s]);
@@ -207,14 +216,14 @@ __global__ void __launch_bounds__(128, 1)
     }
   } else if (warp == 1 && lane == 0) {  // MMA issuer
     constexpr uint32_t IDESC = idesc_tf32(kTcBM, BN);
-    for (int kb = 0; kb < nkb; ++kb) {
+    for (int kb = 0; kb < nsb; ++kb) {
       const int s = kb % NST;
       mbar_wait(&full[s], (uint32_t)((kb / NST) & 1));
       tc_fence_after();
       const uint32_t a_h = sbase + s * STAGE, a_l = a_h + ABYTES;
       const uint32_t b_h = a_h + NA * ABYTES, b_l = b_h + BBYTES;
 #pragma unroll
-      for (int kk = 0; kk < kTcBK / 8; ++kk) {  // MMA K = 8 tf32 = two 16-byte chunks
+      for (int kk = 0; kk < kTcSK / 8; ++kk) {  // MMA K = 8 tf32 = two 16-byte chunks
         const uint32_t ao = 2 * kk * (kTcBM * 16), bo = 2 * kk * (BN * 16);
         const uint64_t dah = umma_desc(a_h + ao, kTcBM * 16, 128);
         const uint64_t dbh = umma_desc(b_h + bo, BN * 16, 128);
