@@ -1639,7 +1639,8 @@ void launch_moments(int J, const GcvData& g, const GcvGrid& grid, const double* 
     }                                                                                       \
     break;
   switch (J) {
-    FD_MOM(4) FD_MOM(8) FD_MOM(12) FD_MOM(16) FD_MOM(20) FD_MOM(24) FD_MOM(28) FD_MOM(32)
+    FD_MOM(4) FD_MOM(8) FD_MOM(12) FD_MOM(13) FD_MOM(14) FD_MOM(15) FD_MOM(16) FD_MOM(17)
+    FD_MOM(18) FD_MOM(19) FD_MOM(20) FD_MOM(24) FD_MOM(28) FD_MOM(32)
     FD_MOM(36) FD_MOM(40) FD_MOM(44) FD_MOM(48)
     default: throw FdError(FD_ERR_OTHER, "unsupported moment count");
   }

@@ -93,7 +93,10 @@ FD_HD inline int gcv_moment_terms(double mu_min, double mu_max, int count) {
   const double delta = (log(mu_max) - log(mu_min)) / (double)(count - 1);
   const double ratio = exp(delta) - 1.0;
   if (!(ratio < 0.45)) return 0;
-  for (int J = 4; J <= 48; J += 4)
+  // every J in 12..20 (the configs' grids land there: 13 at 512 points over
+  // 1e-8..1, 17 at 256, 20 at 128 over 1e-6..1), multiples of 4 elsewhere --
+  // the moment kernels are instantiated for exactly these counts
+  for (int J = 4; J <= 48; J += (J >= 12 && J < 20) ? 1 : 4)
     if ((J + 1) * pow(ratio, (double)J) < 1e-17) return J;
   return 0;
 }
