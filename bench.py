@@ -6,7 +6,7 @@
 
 Metric (BASELINE.json): Mpixels/s per Tikhonov+GCV restoration (fp64).
 A step restores the whole batch of the configuration (deblur = GCV select +
-Tikhonov solve, pipeline.cpp:732-768) once per (boundary condition, smoother)
+Tikhonov solve, pipeline.cpp:120-155) once per (boundary condition, smoother)
 the config names; default workload is config 1 (65,536 signals of n = 4096 per
 GPU, nonsymmetric PSF, BC degrees d = 1 and d = 3 -- the higher-order Fourier
 borders, an extension the reference lacks -- first-difference smoother, 256

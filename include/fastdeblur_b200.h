@@ -63,28 +63,28 @@ typedef struct fd_smoother fd_smoother;
 const char* fd_last_error(void);
 int fd_version(void);
 
-/* parse_boundary_condition (operators.cpp:232-239); -1 if unknown */
+/* parse_boundary_condition (operators.cpp:121-128); -1 if unknown */
 int fd_parse_bc(const char* name);
 
 /* BC for a polynomial-preservation degree (north_star "BC degree d"):
- * d=1 -> antireflective (symmetric PSF, operators.cpp:173-176) or the
+ * d=1 -> antireflective (symmetric PSF, operators.cpp:94-98) or the
  *        hoc-fourier-d1 extension (nonsymmetric PSF),
  * d=2 -> hoc-cosine (symmetric) or hoc-fourier (any PSF),
  * d=3 -> the hoc-fourier-d3 extension (any PSF).
  * Other degrees: ValidationError. */
 int fd_bc_for_degree(int degree, int psf_symmetric, int* bc);
 
-/* build_operator(make_psf(weights, normalize), n, bc)   operators.cpp:404-412,
- * psf.cpp:10-38.  Validation errors as validate_build (operators.cpp:173-187). */
+/* build_operator(make_psf(weights, normalize), n, bc)   operators.cpp:293-301,
+ * psf.cpp:10-37.  Validation errors as validate_build (operators.cpp:62-76). */
 int fd_op_create_1d(const double* psf, int len, int normalize, int n, int bc, fd_op** op);
 
 /* build_operator_2d(make_psf2d(weights, rows, cols, normalize), n1, n2, bc)
- * multidim.cpp:413-426; eigenvalues by the three-step scheme (311-376). */
+ * multidim.cpp:309-322; eigenvalues by the three-step scheme (311-376). */
 int fd_op_create_2d(const double* psf, int rows, int cols, int normalize, int n1, int n2, int bc,
                     fd_op** op);
 
 /* build_operator_2d for the separable mask separable_psf2d(a, b)
- * (multidim.cpp:226-233): eigenvalues are kept as the outer product of the
+ * (multidim.cpp:122-129): eigenvalues are kept as the outer product of the
  * marginal 1D eigenvalue vectors (equal to eigenvalues_2d for separable
  * masks, test_multidim.cpp:106-123), so no n1*n2 eigenvalue array is stored. */
 int fd_op_create_2d_separable(const double* psf_a, int len_a, const double* psf_b, int len_b,
@@ -99,7 +99,7 @@ int fd_op_info(const fd_op* op, int* dim, int* n1, int* n2, int* bc, int* is_com
  * writes N complex values (interleaved) to the device array d. */
 int fd_op_eigenvalues(const fd_op* op, double* d, void* stream);
 
-/* smoothing_eigenvalues(_2d) (regularize.cpp:155-175, multidim.cpp:433-460);
+/* smoothing_eigenvalues(_2d) (regularize.cpp:19-38, multidim.cpp:329-356);
  * ValidationError on a joint null space with the operator. */
 int fd_smoother_create(const fd_op* op, int kind, fd_smoother** L);
 /* SmoothingOperator{kind, eigenvalues} aggregate with caller-supplied
@@ -109,41 +109,41 @@ int fd_smoother_destroy(fd_smoother* L);
 /* writes the N smoother eigenvalues to the device array s */
 int fd_smoother_eigenvalues(const fd_smoother* L, double* s, void* stream);
 
-/* SpectralBasis::analyze = T_X^{-1} (operators.cpp:303-312, boundary.cpp:338-375)
- * and tensor_apply(..., Direction::inverse) for 2D (multidim.cpp:275-302).
+/* SpectralBasis::analyze = T_X^{-1} (operators.cpp:193-201, boundary.cpp:253-289)
+ * and tensor_apply(..., Direction::inverse) for 2D (multidim.cpp:172-198).
  * in: real (in_complex = 0) or complex; out: complex for complex bases
  * (periodic, hoc-fourier), real otherwise. */
 int fd_analyze(const fd_op* op, const void* in, int in_complex, void* out, long long count,
                void* stream);
 
-/* SpectralBasis::synthesize = T_X (operators.cpp:291-301, boundary.cpp:310-336);
+/* SpectralBasis::synthesize = T_X (operators.cpp:181-190, boundary.cpp:225-250);
  * in: complex for complex bases, real otherwise.  out_complex = 0 keeps the
  * real part and, if imag_residue != NULL, writes ||Im||_2 per item. */
 int fd_synthesize(const fd_op* op, const void* in, void* out, int out_complex,
                   double* imag_residue, long long count, void* stream);
 
-/* blur_apply(_2d) (operators.cpp:317-343, multidim.cpp:381-408): real f -> real A f */
+/* blur_apply(_2d) (operators.cpp:207-232, multidim.cpp:278-304): real f -> real A f */
 int fd_matvec(const fd_op* op, const double* f, double* out, double* imag_residue,
               long long count, void* stream);
 
-/* tikhonov_solve(_2d) (regularize.cpp:209-239, multidim.cpp:462-499) with one
+/* tikhonov_solve(_2d) (regularize.cpp:73-116, multidim.cpp:358-395) with one
  * mu per item (device array mu, each > 0: ParameterError otherwise). */
 int fd_tikhonov(const fd_op* op, const fd_smoother* L, const double* g, const double* mu,
                 double* out, double* imag_residue, long long count, void* stream);
 
-/* gcv_value(_2d) (regularize.cpp:255-269, multidim.cpp:501-519): G per item */
+/* gcv_value(_2d) (regularize.cpp:119-142, multidim.cpp:397-415): G per item */
 int fd_gcv_value(const fd_op* op, const fd_smoother* L, const double* g, double mu, double* G,
                  long long count, void* stream);
 
-/* gcv_select(_2d) (regularize.cpp:353-374, multidim.cpp:521-546) with the
- * gcv_minimize semantics (regularize.cpp:281-351) per item: mu (device, per
+/* gcv_select(_2d) (regularize.cpp:217-247, multidim.cpp:417-442) with the
+ * gcv_minimize semantics (regularize.cpp:144-214) per item: mu (device, per
  * item), best_k (device int, per item; -1 never), curve (device
  * count x grid_count G values, or NULL). */
 int fd_gcv_select(const fd_op* op, const fd_smoother* L, const double* g, double mu_min,
                   double mu_max, int grid_count, double* mu, int* best_k, double* curve,
                   long long count, void* stream);
 
-/* deblur(_2d) (pipeline.cpp:732-778): GCV-selected (use_gcv = 1) or fixed mu,
+/* deblur(_2d) (pipeline.cpp:120-165): GCV-selected (use_gcv = 1) or fixed mu,
  * then the Tikhonov solve.  Outputs per item: restored (device, N each),
  * mu_used, best_k (or NULL), curve (or NULL), imag_residue (or NULL). */
 int fd_deblur(const fd_op* op, const fd_smoother* L, const double* g, int use_gcv,
@@ -191,7 +191,7 @@ int fd_deblur_host_multi(int nops, const fd_op* const* ops, const fd_smoother* c
                          double mu_max, int grid_count, void* const* restored, double* mu_used,
                          int* best_k, long long count, long long chunk, void* stream);
 
-/* The same selection logic the kernels run (gcv_minimize, regularize.cpp:281-351),
+/* The same selection logic the kernels run (gcv_minimize, regularize.cpp:144-214),
  * on the host with a caller-supplied G: for the CPU test suite. */
 typedef double (*fd_gcv_fn)(double mu, void* ctx);
 int fd_gcv_minimize_host(fd_gcv_fn G, void* ctx, double mu_min, double mu_max, int grid_count,
@@ -242,7 +242,7 @@ int fd_slab_gcv_partials(const fd_op* op, const fd_smoother* L, const void* ghat
  * (the golden-section series of k_gcv_moments).  Synchronous. */
 int fd_slab_gcv_moments(const fd_op* op, const fd_smoother* L, const void* ghat, long long ncols,
                         long long col0, double center, int J, double* moments, void* stream);
-/* gcv_minimize (regularize.cpp:281-351) on summed partials, host only:
+/* gcv_minimize (regularize.cpp:144-214) on summed partials, host only:
  * moment count J (0: coarse grid, refine with direct evaluations), grid pick
  * (first minimum, 1e-12 ties, bracket centre), golden section on the moments. */
 int fd_gcv_moment_terms(double mu_min, double mu_max, int grid_count, int* J);

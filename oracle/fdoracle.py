@@ -60,15 +60,15 @@ class DegenerateError(ArithmeticError):
     """errors.hpp:38-41 (CLI exit code 3)."""
 
 
-def needs_symmetric_psf(bc):  # operators.cpp:205-209
+def needs_symmetric_psf(bc):  # operators.cpp:94-98
     return bc in (REFLECTIVE, ANTIREFLECTIVE, HOC_COSINE)
 
 
-def is_complex_basis(bc):  # operators.cpp:211-213 (+ extension codes)
+def is_complex_basis(bc):  # operators.cpp:100-102 (+ extension codes)
     return bc in (PERIODIC, HOC_FOURIER, HOC_FOURIER_D1, HOC_FOURIER_D3)
 
 
-def is_boundary_corrected(bc):  # operators.cpp:215-219
+def is_boundary_corrected(bc):  # operators.cpp:104-108
     return bc in (ANTIREFLECTIVE, HOC_COSINE, HOC_FOURIER)
 
 
@@ -93,7 +93,7 @@ class Psf:
 
 
 def make_psf(weights, normalize=False) -> Psf:
-    """psf.cpp:10-38."""
+    """psf.cpp:10-37."""
     w = np.asarray(weights, dtype=np.float64).copy()
     if w.size == 0 or w.size % 2 == 0:
         raise ValidationError("psf must have odd length 2m+1")
@@ -135,10 +135,10 @@ def symbol_eval(psf: Psf, t):
 
 
 # --------------------------------------------------------------------------
-# Trig transforms (trig.cpp:170-234)
+# Trig transforms (trig.cpp:116-180)
 # --------------------------------------------------------------------------
 def fourier_apply(v, forward=True):
-    """Unitary DFT F v / F^H v (trig.cpp:170-178)."""
+    """Unitary DFT F v / F^H v (trig.cpp:116-124)."""
     v = np.asarray(v, dtype=np.complex128)
     m = v.shape[-1]
     y = np.fft.fft(v, axis=-1) if forward else np.fft.ifft(v, axis=-1) * m
@@ -146,12 +146,12 @@ def fourier_apply(v, forward=True):
 
 
 def _dct_tw(m):
-    ang = -0.5 * PI * np.arange(m, dtype=np.float64) / m  # trig.cpp:134-136
+    ang = -0.5 * PI * np.arange(m, dtype=np.float64) / m  # trig.cpp:73-87
     return np.cos(ang) + 1j * np.sin(ang)
 
 
 def cosine_apply(v, forward=True):
-    """Orthogonal DCT-II C v (forward) / C^T v (inverse), trig.cpp:180-214."""
+    """Orthogonal DCT-II C v (forward) / C^T v (inverse), trig.cpp:126-160."""
     v = np.asarray(v, dtype=np.float64)
     m = v.shape[-1]
     if m == 1:
@@ -177,7 +177,7 @@ def cosine_apply(v, forward=True):
 
 
 def sine_apply(v):
-    """DST-I Q v via the odd extension of length 2(m+1), trig.cpp:216-234."""
+    """DST-I Q v via the odd extension of length 2(m+1), trig.cpp:162-180."""
     v = np.asarray(v, dtype=np.float64)
     m = v.shape[-1]
     ln = 2 * (m + 1)
@@ -212,7 +212,7 @@ class StructuredTransform:
 
 
 def extended_grid(basis, n):
-    """boundary.cpp:218-246 -> (a, b, points)."""
+    """boundary.cpp:132-160 -> (a, b, points)."""
     if n < 5:
         raise ValidationError("boundary transform needs order n >= 5")
     i = np.arange(n)
@@ -225,7 +225,7 @@ def extended_grid(basis, n):
 
 
 def _interior_apply(basis, x, forward):
-    """boundary.cpp:120-129."""
+    """boundary.cpp:35-43."""
     if basis == B_HF:
         return fourier_apply(x, forward)
     if basis == B_AR:
@@ -234,7 +234,7 @@ def _interior_apply(basis, x, forward):
 
 
 def _check_capacitance(mm):
-    """boundary.cpp:139-150 (2-norm condition <= 1e12)."""
+    """boundary.cpp:54-64 (2-norm condition <= 1e12)."""
     a2 = np.abs(np.asarray(mm)) ** 2
     t = float(a2.sum())
     det = mm[0] * mm[3] - mm[1] * mm[2]
@@ -248,7 +248,7 @@ def _check_capacitance(mm):
 
 
 def _assemble(basis, n, q, c_a, c_b, grid):
-    """boundary.cpp:153-214."""
+    """boundary.cpp:132-160."""
     cplx = basis == B_HF
     q = np.asarray(q, dtype=np.float64)
     norm = math.sqrt(sum(float(x) * float(x) for x in q))
@@ -281,7 +281,7 @@ def _assemble(basis, n, q, c_a, c_b, grid):
 
 
 def build_transform(basis, n) -> StructuredTransform:
-    """build_real_transform / build_fourier_transform (boundary.cpp:248-303)."""
+    """build_real_transform / build_fourier_transform (boundary.cpp:162-217)."""
     grid = extended_grid(basis, n)
     a, b, pts = grid
     m = n - 2
@@ -304,7 +304,7 @@ def build_transform(basis, n) -> StructuredTransform:
 
 
 def transform_apply(t: StructuredTransform, u):
-    """y = T_X u (boundary.cpp:310-336); batched over leading axes."""
+    """y = T_X u (boundary.cpp:225-250); batched over leading axes."""
     u = np.asarray(u)
     n = t.n
     if u.shape[-1] != n:
@@ -322,7 +322,7 @@ def transform_apply(t: StructuredTransform, u):
 
 
 def transform_apply_inverse(t: StructuredTransform, y):
-    """v = T_X^-1 y (boundary.cpp:338-375); batched over leading axes."""
+    """v = T_X^-1 y (boundary.cpp:253-289); batched over leading axes."""
     y = np.asarray(y)
     n = t.n
     if y.shape[-1] != n:
@@ -442,7 +442,7 @@ def build_ho_transform(bc, n, borders=None) -> HoTransform:
     wrap = np.array([m - kl + i for i in range(kl)] + list(range(kr)))
     S = P[border, :] - P[kl + wrap, :]
     sv = np.linalg.svd(S, compute_uv=False)
-    if sv[-1] <= 0.0 or sv[0] / sv[-1] > 1e12:  # as boundary.cpp:139-150 for k = 2
+    if sv[-1] <= 0.0 or sv[0] / sv[-1] > 1e12:  # as boundary.cpp:54-64 for k = 2
         raise DegenerateError("degenerate transform: border capacitance is singular or "
                               "ill-conditioned")
     return HoTransform(bc, n, kl, kr, m, deg, P, border, wrap, S, _gauss_jordan_inverse(S))
@@ -495,7 +495,7 @@ def ho_nodes(bc, n):
 # Operators (operators.cpp)
 # --------------------------------------------------------------------------
 def eigenvalue_grid(bc, n):
-    """Symbol nodes (operators.cpp:241-272)."""
+    """Symbol nodes (operators.cpp:130-161)."""
     if is_boundary_corrected(bc) and n < 5:
         raise ValidationError("boundary-corrected grids need n >= 5")
     if is_higher_order(bc):
@@ -516,7 +516,7 @@ def eigenvalue_grid(bc, n):
 
 
 def validate_build(psf: Psf, n, bc):
-    """operators.cpp:173-187."""
+    """operators.cpp:62-76."""
     if needs_symmetric_psf(bc) and not psf.symmetric:
         raise ValidationError(f"{BC_NAMES[bc]} boundary conditions require a symmetric psf")
     if is_higher_order(bc):
@@ -538,10 +538,10 @@ def validate_build(psf: Psf, n, bc):
 
 
 def operator_eigenvalues(psf: Psf, n, bc):
-    """d = z(node) with pinned boundary eigenvalues 1 (operators.cpp:348-397).
+    """d = z(node) with pinned boundary eigenvalues 1 (operators.cpp:238-286).
 
     The reference sums the symbol directly for support <= 64 and uses a wrapped
-    FFT otherwise (operators.cpp:130-171); both give z(node) to rounding, and
+    FFT otherwise (operators.cpp:23-33); both give z(node) to rounding, and
     this restatement always sums directly.  Real bases return float64.
     """
     validate_build(psf, n, bc)
@@ -566,7 +566,7 @@ def operator_eigenvalues(psf: Psf, n, bc):
 
 
 class SpectralBasis:
-    """operators.cpp:274-312: synthesize = T_X, analyze = T_X^-1."""
+    """operators.cpp:164-201: synthesize = T_X, analyze = T_X^-1."""
 
     def __init__(self, bc, n):
         self.bc, self.n = bc, n
@@ -611,7 +611,7 @@ class BlurOperator:
     basis: SpectralBasis
 
     def apply(self, f):
-        """Matvec A f (operators.cpp:317-343) -> (out, imag_residue)."""
+        """Matvec A f (operators.cpp:207-232) -> (out, imag_residue)."""
         f = np.asarray(f, dtype=np.float64)
         if f.shape[-1] != self.n:
             raise ValidationError("blur apply: signal length != operator order")
@@ -623,7 +623,7 @@ class BlurOperator:
 
 
 def build_operator(psf: Psf, n, bc) -> BlurOperator:
-    """operators.cpp:404-412."""
+    """operators.cpp:293-301."""
     validate_build(psf, n, bc)
     return BlurOperator(bc, n, operator_eigenvalues(psf, n, bc), psf, SpectralBasis(bc, n))
 
@@ -632,7 +632,7 @@ def build_operator(psf: Psf, n, bc) -> BlurOperator:
 # Regularisation (regularize.hpp / regularize.cpp)
 # --------------------------------------------------------------------------
 def smoothing_eigenvalues(kind, bc, n, d=None):
-    """regularize.cpp:155-175; FIRST_DIFFERENCE is an extension."""
+    """regularize.cpp:19-38; FIRST_DIFFERENCE is an extension."""
     if kind == IDENTITY:
         return np.ones(n)
     nodes = eigenvalue_grid(bc, n)
@@ -677,7 +677,7 @@ class GcvResult:
 
 
 def gcv_grid(mu_min, mu_max, count):
-    """Log-spaced grid (regularize.cpp:286-293)."""
+    """Log-spaced grid (regularize.cpp:149-156)."""
     if not (mu_min > 0.0) or not (mu_max > mu_min) or count < 2:
         raise ValidationError("gcv search needs 0 < mu_min < mu_max and count >= 2")
     llo, lhi = math.log(mu_min), math.log(mu_max)
@@ -685,7 +685,7 @@ def gcv_grid(mu_min, mu_max, count):
 
 
 def gcv_minimize(G, mu_min, mu_max, count, grid_vals=None) -> GcvResult:
-    """gcv_minimize restated verbatim (regularize.cpp:281-351).
+    """gcv_minimize restated verbatim (regularize.cpp:144-214).
 
     ``G`` maps a scalar mu to G(mu); ``grid_vals`` optionally supplies the grid
     values (vectorised evaluation).  First minimum, 1e-12 relative tie test with
@@ -735,7 +735,7 @@ def gcv_minimize(G, mu_min, mu_max, count, grid_vals=None) -> GcvResult:
 
 
 def _coeffs(op, g):
-    """analyze real data in the operator's basis (regularize.cpp:220-228)."""
+    """analyze real data in the operator's basis (regularize.cpp:84-89)."""
     g = np.asarray(g, dtype=np.float64)
     return op.basis.analyze(g.astype(np.complex128) if op.basis.complex else g)
 
@@ -748,21 +748,21 @@ def _solve_from_coeffs(op, s, ghat, mu):
 
 
 def tikhonov_solve(op: BlurOperator, s, g, mu):
-    """regularize.cpp:209-239 -> (f_reg, imag_residue); batched."""
+    """regularize.cpp:73-116 -> (f_reg, imag_residue); batched."""
     if mu <= 0.0:
         raise ValidationError("mu must be positive")
     return _solve_from_coeffs(op, s, _coeffs(op, g), mu)
 
 
 def gcv_value(op: BlurOperator, s, g, mu):
-    """regularize.cpp:255-269."""
+    """regularize.cpp:119-142."""
     if mu <= 0.0:
         raise ValidationError("mu must be positive")
     return gcv_from_coeffs(op.eigenvalues, s, _coeffs(op, g), mu)
 
 
 def gcv_select(op: BlurOperator, s, g, mu_min, mu_max, count) -> GcvResult:
-    """regularize.cpp:353-374 for one signal."""
+    """regularize.cpp:217-247 for one signal."""
     ghat = _coeffs(op, g)
     return _select_from_coeffs(op.eigenvalues, s, ghat, mu_min, mu_max, count)
 
@@ -798,9 +798,9 @@ class Restoration:
 
 def deblur(op: BlurOperator, s, g, use_gcv=True, fixed_mu=0.0, mu_min=1e-12, mu_max=10.0,
            count=200, want_curve=False) -> Restoration:
-    """deblur / deblur_impl (pipeline.cpp:732-768), batched over leading axes.
+    """deblur / deblur_impl (pipeline.cpp:120-155), batched over leading axes.
 
-    Like the reference, the solve re-analyses g (pipeline.cpp:752)."""
+    Like the reference, the solve re-analyses g (pipeline.cpp:139-140)."""
     g = np.asarray(g, dtype=np.float64)
     flat = g.reshape(-1, op.n)
     B = flat.shape[0]
@@ -840,7 +840,7 @@ class Psf2D:
 
 
 def make_psf2d(weights, normalize=False) -> Psf2D:
-    """multidim.cpp:185-213."""
+    """multidim.cpp:81-109."""
     w = np.array(weights, dtype=np.float64)
     r, c = w.shape
     if r % 2 == 0 or c % 2 == 0:
@@ -857,21 +857,21 @@ def make_psf2d(weights, normalize=False) -> Psf2D:
 
 
 def separable_psf2d(a: Psf, b: Psf) -> Psf2D:
-    """multidim.cpp:226-233."""
+    """multidim.cpp:122-129."""
     return make_psf2d(np.outer(a.weights, b.weights), normalize=True)
 
 
-def marginal_sum_columns(p: Psf2D) -> Psf:  # multidim.cpp:247-254
+def marginal_sum_columns(p: Psf2D) -> Psf:  # multidim.cpp:143-150
     return make_psf(np.array([sum(float(x) for x in row) for row in p.weights]), normalize=True)
 
 
-def marginal_sum_rows(p: Psf2D) -> Psf:  # multidim.cpp:256-263
+def marginal_sum_rows(p: Psf2D) -> Psf:  # multidim.cpp:152-159
     return make_psf(np.array([sum(float(x) for x in col) for col in p.weights.T]),
                     normalize=True)
 
 
 def eigenvalues_2d(p: Psf2D, n1, n2, bc, separable=False):
-    """Three-step eigenvalue scheme (multidim.cpp:311-376).
+    """Three-step eigenvalue scheme (multidim.cpp:208-272).
 
     Interior: z2(x1_i, x2_j) by direct summation (real part for real bases);
     the separable factorisation e^{i(j t1 + k t2)} = e^{ij t1} e^{ik t2} turns
@@ -907,7 +907,7 @@ def eigenvalues_2d(p: Psf2D, n1, n2, bc, separable=False):
 
 
 def tensor_apply(rows: SpectralBasis, cols: SpectralBasis, arr, forward):
-    """Columns first, then rows (multidim.cpp:275-302).  forward = synthesize."""
+    """Columns first, then rows (multidim.cpp:172-198).  forward = synthesize."""
     arr = np.asarray(arr)
     t = np.swapaxes(arr, -1, -2)
     t = rows.synthesize(t) if forward else rows.analyze(t)
@@ -940,12 +940,12 @@ class BlurOperator2D:
         return yc, np.zeros(yc.shape[:-2])
 
     def apply(self, f):
-        """multidim.cpp:381-408."""
+        """multidim.cpp:278-304."""
         return self.synthesize(self.analyze(f) * self.eigenvalues)
 
 
 def build_operator_2d(p: Psf2D, n1, n2, bc, separable=False) -> BlurOperator2D:
-    """multidim.cpp:413-426 (validate_build_2d, multidim.cpp:119-130)."""
+    """multidim.cpp:309-322 (validate_build_2d, multidim.cpp:15-26)."""
     if needs_symmetric_psf(bc) and not p.symmetric:
         raise ValidationError(f"{BC_NAMES[bc]} boundary conditions require a quadrantally "
                               "symmetric 2D psf")
@@ -963,7 +963,7 @@ def build_operator_2d(p: Psf2D, n1, n2, bc, separable=False) -> BlurOperator2D:
 
 
 def smoothing_eigenvalues_2d(kind, bc, n1, n2, d=None):
-    """multidim.cpp:433-460: identity -> 1, laplacian -> s(x1_i) + s(x2_j)."""
+    """multidim.cpp:329-356: identity -> 1, laplacian -> s(x1_i) + s(x2_j)."""
     if kind == IDENTITY:
         return np.ones((n1, n2))
     x1, x2 = eigenvalue_grid(bc, n1), eigenvalue_grid(bc, n2)
@@ -975,7 +975,7 @@ def smoothing_eigenvalues_2d(kind, bc, n1, n2, d=None):
 
 def deblur_2d(op: BlurOperator2D, s, g, use_gcv=True, fixed_mu=0.0, mu_min=1e-12,
               mu_max=10.0, count=200, want_curve=False) -> Restoration:
-    """deblur_2d (pipeline.cpp:770-778); batched over a leading axis."""
+    """deblur_2d (pipeline.cpp:157-165); batched over a leading axis."""
     g = np.asarray(g, dtype=np.float64)
     flat = g.reshape(-1, op.n1, op.n2)
     B = flat.shape[0]
@@ -1001,13 +1001,13 @@ def deblur_2d(op: BlurOperator2D, s, g, use_gcv=True, fixed_mu=0.0, mu_min=1e-12
 
 
 # --------------------------------------------------------------------------
-# Input generation (operators.cpp:189-201, 443-469; pipeline.cpp:628-664)
+# Input generation (operators.cpp:78-90, 443-469; pipeline.cpp:15-51)
 # --------------------------------------------------------------------------
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
 
 
 def splitmix64(x):
-    """operators.cpp:189-196, vectorised over uint64 arrays."""
+    """operators.cpp:78-85, vectorised over uint64 arrays."""
     x = np.asarray(x, dtype=np.uint64)
     with np.errstate(over="ignore"):
         x = x ^ (x >> np.uint64(30))
@@ -1019,13 +1019,13 @@ def splitmix64(x):
 
 
 def bits_to_u01(bits):
-    """(0, 1] (operators.cpp:198-201)."""
+    """(0, 1] (operators.cpp:88-90)."""
     return ((np.asarray(bits, dtype=np.uint64) >> np.uint64(11)).astype(np.float64) + 1.0) \
         * (2.0 ** -53)
 
 
 def add_noise(g, level, seed):
-    """g + eta, ||eta|| = level ||g|| (operators.cpp:443-469).  Last axis = signal;
+    """g + eta, ||eta|| = level ||g|| (operators.cpp:332-358).  Last axis = signal;
     ``seed`` is a scalar or an array broadcast against the leading axes."""
     g = np.asarray(g, dtype=np.float64)
     if level < 0.0:
@@ -1053,7 +1053,7 @@ def add_noise(g, level, seed):
 
 
 def convolve_valid(ext, psf: Psf):
-    """g_i = sum_j h_j f_{i+j} (pipeline.cpp:628-642); last axis."""
+    """g_i = sum_j h_j f_{i+j} (pipeline.cpp:15-29); last axis."""
     ext = np.asarray(ext, dtype=np.float64)
     m = psf.m
     n = ext.shape[-1] - 2 * m
@@ -1066,7 +1066,7 @@ def convolve_valid(ext, psf: Psf):
 
 
 def convolve_valid_2d(ext, p: Psf2D):
-    """pipeline.cpp:644-664; last two axes."""
+    """pipeline.cpp:31-51; last two axes."""
     ext = np.asarray(ext, dtype=np.float64)
     rows, cols = ext.shape[-2:]
     n1, n2 = rows - 2 * p.m1, cols - 2 * p.m2
@@ -1101,7 +1101,7 @@ def sweep_mu(op: BlurOperator, s, g, truth=None, mu_min=1e-12, mu_max=10.0, coun
 
 
 def rre(truth, restored):
-    """regularize.cpp:386-397."""
+    """regularize.cpp:249-260."""
     truth, restored = np.asarray(truth), np.asarray(restored)
     tn = np.sum(truth * truth, axis=-1)
     return np.sqrt(np.sum((truth - restored) ** 2, axis=-1) / tn)

@@ -2,7 +2,7 @@
  * TEST INFRASTRUCTURE ONLY (oracle/). Never linked into the product library.
  *
  * O(n log n) stand-in for the three FFTW3 calls the reference makes
- * (reference: proj/core/src/trig.cpp:107-124 plan cache, 159-166 execute).
+ * (reference: proj/core/src/trig.cpp:53-70 plan cache, 105-112 execute).
  * FFTW 3.x (unpinned: found via find_library, core/CMakeLists.txt:1-2) is
  * absent from this image; this file restates its published contract:
  *
@@ -18,7 +18,7 @@
  *
  * Thread safety: plans are immutable after creation; every execute allocates
  * its own scratch, so concurrent executes on one plan are safe (the reference
- * relies on this, trig.cpp:81-83).
+ * relies on this, trig.cpp:95-112).
  */
 #include "fftw3.h"
 

@@ -4,8 +4,8 @@
  * Minimal FFTW3 API stand-in so the UNMODIFIED reference core
  * (/root/reference/proj/core/src/*.cpp) compiles into oracle/_ref/.
  * The reference uses exactly three FFTW entry points and four macros
- * (trig.cpp:116-120 plan creation, trig.cpp:163-165 new-array execute,
- * trig.cpp:92 destroy). FFTW itself is a third-party dependency that is
+ * (trig.cpp:53-70 plan creation, trig.cpp:105-112 new-array execute,
+ * trig.cpp:38 destroy). FFTW itself is a third-party dependency that is
  * neither vendored nor installed here (core/CMakeLists.txt:1-2); this file
  * restates its published contract: unnormalised complex DFT
  *     out_k = sum_j in_j exp(sign * 2 pi i j k / n),  sign = FFTW_FORWARD (-1)

@@ -4,16 +4,16 @@
 // /root/reference/proj/core/src/*.cpp (see oracle/Makefile). It lets the
 // Python tests, the golden-vector generator and bench.py's reference arm call
 // the reference's own public API through ctypes:
-//   build_operator / build_operator_2d     operators.cpp:404-412, multidim.cpp:413-426
-//   SpectralBasis::analyze / synthesize    operators.cpp:291-312
-//   tensor_apply                           multidim.cpp:275-302
-//   blur_apply(_2d)                        operators.cpp:430-433, multidim.cpp:428-431
-//   smoothing_eigenvalues(_2d)             regularize.cpp:155-184, multidim.cpp:433-460
-//   tikhonov_solve(_2d), gcv_value(_2d)    regularize.cpp:209-279, multidim.cpp:462-519
-//   gcv_minimize, gcv_select(_2d)          regularize.cpp:281-384, multidim.cpp:521-546
-//   deblur(_2d)                            pipeline.cpp:760-778
+//   build_operator / build_operator_2d     operators.cpp:293-301, multidim.cpp:309-322
+//   SpectralBasis::analyze / synthesize    operators.cpp:181-201
+//   tensor_apply                           multidim.cpp:172-198
+//   blur_apply(_2d)                        operators.cpp:319-322, multidim.cpp:324-327
+//   smoothing_eigenvalues(_2d)             regularize.cpp:19-47, multidim.cpp:329-356
+//   tikhonov_solve(_2d), gcv_value(_2d)    regularize.cpp:73-142, multidim.cpp:358-415
+//   gcv_minimize, gcv_select(_2d)          regularize.cpp:144-247, multidim.cpp:417-442
+//   deblur(_2d)                            pipeline.cpp:147-165
 //   sweep_mu                               pipeline.cpp:55-115
-//   add_noise, convolve_valid(_2d)         operators.cpp:443-469, pipeline.cpp:628-664
+//   add_noise, convolve_valid(_2d)         operators.cpp:332-358, pipeline.cpp:15-51
 // Status codes follow the CLI mapping (fastdeblur.cpp:442-451):
 // 0 ok, 2 ValidationError, 3 DegenerateError, 1 anything else.
 #include <atomic>
@@ -263,7 +263,7 @@ int ref_gcv_value_1d(const double* psf, int len, int n, int bc, int smoother,
   });
 }
 
-// deblur (pipeline.cpp:760-768) for `batch` independent signals sharing one
+// deblur (pipeline.cpp:147-155) for `batch` independent signals sharing one
 // operator; `threads` > 1 runs an outer pool over signals (a harness
 // addition; the reference itself has no batch entry point).
 // curve_G (optional) receives batch*count grid values of G.
@@ -314,7 +314,7 @@ int ref_deblur_1d(const double* psf, int len, int n, int bc, int smoother,
 
 typedef double (*ref_gcv_fn)(double mu, void* ctx);
 
-// gcv_minimize (regularize.cpp:281-351) driven by an arbitrary G callback;
+// gcv_minimize (regularize.cpp:144-214) driven by an arbitrary G callback;
 // used to pin the product's host-side selection logic.
 int ref_gcv_minimize(ref_gcv_fn G, void* ctx, double mu_min, double mu_max, int count,
                      double* mu, double* curve_G) {
@@ -368,7 +368,7 @@ int ref_eigenvalues_2d(const double* psf2, int rows, int cols, int n1, int n2, i
   });
 }
 
-// tensor_apply (multidim.cpp:275-302): dir 0 = analyze, 1 = synthesize.
+// tensor_apply (multidim.cpp:172-198): dir 0 = analyze, 1 = synthesize.
 int ref_tensor_apply(int bc, int n1, int n2, int dir, const double* in_re, const double* in_im,
                      double* out_re, double* out_im) {
   return guarded([&] {
@@ -411,7 +411,7 @@ int ref_gcv_value_2d(const double* psf2, int rows, int cols, int n1, int n2, int
   });
 }
 
-// deblur_2d (pipeline.cpp:770-778) for `batch` images sharing one operator.
+// deblur_2d (pipeline.cpp:157-165) for `batch` images sharing one operator.
 int ref_deblur_2d(const double* psf2, int rows, int cols, int n1, int n2, int bc, int eig_mode,
                   int smoother, const double* s_custom, int use_gcv, double fixed_mu,
                   double mu_min, double mu_max, int count, long batch, const double* g,

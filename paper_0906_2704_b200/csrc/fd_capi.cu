@@ -1,7 +1,7 @@
 // C ABI (include/fastdeblur_b200.h) and host orchestration of the sm_100a
 // kernels in fd_kernels.cu.  Host code only builds O(n) operator metadata
 // exactly as the reference does (boundary column q, boundary rows c_a/c_b,
-// capacitance check: boundary.cpp:139-303) and validates arguments; every
+// capacitance check: boundary.cpp:54-217) and validates arguments; every
 // transform, filter, eigenvalue and GCV evaluation runs on the GPU.  There is
 // no CPU fallback: without a CUDA device every call fails with status 1.
 #include <cuda_runtime.h>
@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -160,10 +161,27 @@ void set_pair_attrs(int kmax) {
   cudaFuncSetAttribute(k_psynth<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
 }
 
+// One-time setup per DEVICE (a process may drive several GPUs: the constant
+// codelet tables, the dynamic shared-memory opt-ins and the mempool threshold
+// are per-device state).  `once_per_device(mask, f)` runs f the first time
+// the current device reaches it.
+bool once_per_device(std::atomic<uint64_t>& mask, const std::function<void()>& f) {
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  const uint64_t bit = dev < 64 ? (1ull << dev) : 0;
+  if (bit && (mask.load(std::memory_order_acquire) & bit)) return true;
+  std::lock_guard<std::mutex> lk(mu);
+  if (bit && (mask.load(std::memory_order_relaxed) & bit)) return true;
+  f();
+  mask.fetch_or(bit, std::memory_order_release);
+  return true;
+}
+
 void init_runtime_once() {
-  static std::once_flag once;
-  static bool ok = false;
-  std::call_once(once, [] {
+  static std::atomic<uint64_t> done{0};
+  bool ok = false;
+  once_per_device(done, [&ok] {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return;
     int dev = 0;
@@ -207,7 +225,9 @@ void init_runtime_once() {
     }
     ok = true;
   });
-  if (!ok) throw FdError(FD_ERR_OTHER, "no CUDA device available (fastdeblur_b200 has no CPU path)");
+  int ndev = 0;
+  if (!ok && (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0))
+    throw FdError(FD_ERR_OTHER, "no CUDA device available (fastdeblur_b200 has no CPU path)");
 }
 
 // ---------------------------------------------------------------------------
@@ -219,7 +239,7 @@ struct HostPsf {
   bool symmetric = false;
 };
 
-// make_psf (psf.cpp:10-38)
+// make_psf (psf.cpp:10-37)
 HostPsf make_psf(const double* w, int len, bool normalize) {
   if (len < 1 || len % 2 == 0) validation("psf must have odd length 2m+1");
   HostPsf p;
@@ -263,7 +283,7 @@ void check_bc(int bc) {
 // interior slack of an axis: n - m
 int border_slack(int bc) { return is_ho_bc(bc) ? ho_kl(bc) + ho_kr(bc) : is_corrected(bc) ? 2 : 0; }
 
-// validate_build (operators.cpp:173-187)
+// validate_build (operators.cpp:62-76)
 void validate_build(const HostPsf& psf, int n, int bc) {
   check_bc(bc);
   if (needs_symmetric(bc) && !psf.symmetric)
@@ -532,7 +552,7 @@ AxisDev interior_view(const AxisDev& a) {
   return v;
 }
 
-void check_capacitance(const cplx m[4]) {  // boundary.cpp:139-150
+void check_capacitance(const cplx m[4]) {  // boundary.cpp:54-64
   const double t = std::norm(m[0]) + std::norm(m[1]) + std::norm(m[2]) + std::norm(m[3]);
   const cplx det = m[0] * m[3] - m[1] * m[2];
   const double d = std::norm(det);
@@ -834,7 +854,7 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
     ck(cudaDeviceSynchronize(), "axis tables");
     return A;
   }
-  // ---- boundary column and rows (boundary.cpp:218-303) ----
+  // ---- boundary column and rows (boundary.cpp:162-217) ----
   double ga, gb;
   std::vector<double> pts(n), q(n);
   if (bc == BC_ANTIREFLECTIVE) {
@@ -863,7 +883,7 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
   double norm = 0.0;
   for (double x : q) norm += x * x;
   norm = std::sqrt(norm);
-  for (double& x : q) x /= norm;  // boundary.cpp:153-160
+  for (double& x : q) x /= norm;  // boundary.cpp:77-83
   q.back() = 0.0;
   const double alpha = 1.0 / q[0];
   d.alpha = alpha;
@@ -1389,7 +1409,7 @@ struct GridHost {
   std::vector<double> mus, logmus;
 };
 
-GridHost make_grid(double mu_min, double mu_max, int count) {  // regularize.cpp:283-293
+GridHost make_grid(double mu_min, double mu_max, int count) {  // regularize.cpp:149-156
   if (!(mu_min > 0.0) || !(mu_max > mu_min) || count < 2)
     validation("gcv search needs 0 < mu_min < mu_max and count >= 2");
   GridHost g;
@@ -1556,13 +1576,12 @@ size_t gemm_smem(int nj) {
 template <int NJ>
 void launch_gemm_t(const GcvData& g, const GcvGrid& grid, long long echunk, int nch,
                    double* partial, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
     ck(cudaFuncSetAttribute(k_gcv_gemm<NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)gemm_smem(NJ)),
        "gemm attr");
-    attr = true;
-  }
+  });
   const dim3 blocks((g.items + 63) / 64, nch);
   for (int kb = 0; kb < grid.count; kb += 32 * NJ) {
     ProfScope ps("k_gcv_grid", st);
@@ -1589,13 +1608,12 @@ size_t gemm2_smem(int nj) { return (size_t)2 * (64 * 32 + 32 * 32 * nj) * 8 + 16
 template <int NJ>
 void launch_gemm2_t(const GcvData& g, const GcvGrid& grid, int nch, long long echunk,
                     double* partial, Scratch& S) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
     ck(cudaFuncSetAttribute(k_gcv_gemm2<NJ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)gemm2_smem(NJ)),
        "gemm2 attr");
-    attr = true;
-  }
+  });
   constexpr int BK = 32 * NJ;
   const int K = grid.count;
   const int Kp = (K + BK - 1) / BK * BK;
@@ -1638,6 +1656,7 @@ void launch_moments(int J, const GcvData& g, const GcvGrid& grid, const double* 
       k_gcv_moments<JV, true><<<blocks, 256, 0, st>>>(g, center, need, chunk, nch, partial);  \
     }                                                                                       \
     break;
+  if (!gcv_moment_count_supported(J)) throw FdError(FD_ERR_OTHER, "unsupported moment count");
   switch (J) {
     FD_MOM(4) FD_MOM(8) FD_MOM(12) FD_MOM(13) FD_MOM(14) FD_MOM(15) FD_MOM(16) FD_MOM(17)
     FD_MOM(18) FD_MOM(19) FD_MOM(20) FD_MOM(24) FD_MOM(28) FD_MOM(32)
@@ -1671,7 +1690,7 @@ void gcv_direct(const GcvData& g, const double* mu_item, double* G, int* status,
 }
 
 // gcv_minimize per item on the GPU.  ghat: analyzed coefficients.
-// the log-spaced grid (regularize.cpp:283-293) on the host with the
+// the log-spaced grid (regularize.cpp:149-156) on the host with the
 // reference's libm, uploaded once per API call (a pageable upload would
 // synchronise the stream, so it must not sit inside a pipelined loop)
 struct DevGrid {
@@ -1698,13 +1717,12 @@ template <int BN>
 void launch_screen(const Analyzed& an, int items, const float* Sh, const float* Sl, int nkb, int K,
                    const double* gscale, uint32_t* mask, int* flag, cudaStream_t st) {
   constexpr bool SPLIT = true;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
     ck(cudaFuncSetAttribute(k_gcv_screen<BN, SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)tc_smem_bytes(BN, SPLIT)),
        "screen attr");
-    attr = true;
-  }
+  });
   ProfScope ps("k_gcv_screen", st);
   k_gcv_screen<BN, SPLIT><<<(items + kTcBM - 1) / kTcBM, 128, tc_smem_bytes(BN, SPLIT), st>>>(
       an.w32, an.w32lo, items, Sh, Sl, nkb, K, gscale, (float)screen_tau(32LL * nkb, SPLIT), mask,
@@ -1807,12 +1825,11 @@ double* interval_screen(const GcvData& g, const GcvGrid& grid, const GridHost& g
   const long long nb = any_pos ? top - base + 1 : 0;
   const size_t hbytes = (size_t)2 * (nb + 1) * sizeof(double);
   if (hbytes > 200 * 1024) return nullptr;  // r spans too many octaves for one SMEM histogram
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  once_per_device(attr, [&] {
     ck(cudaFuncSetAttribute(k_gcv_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
        "hist attr");
-    attr = true;
-  }
+  });
   const int ctas = num_sms();
   const int nw = (int)(2 * (nb + 1));
   double* part = S.get<double>((size_t)ctas * nw);
@@ -1824,7 +1841,8 @@ double* interval_screen(const GcvData& g, const GcvGrid& grid, const GridHost& g
     launched("k_gcv_hist");
     k_reduce_partials<<<dim3(1, (nw + 31) / 32), 256, 0, S.st>>>(part, ctas, nw, hist);
     launched("k_reduce_partials");
-    k_gcv_bounds<<<K, 256, 0, S.st>>>(hist, base, (int)nb, grid, bounds);
+    const double widen = 4.0 * ((double)g.N + (double)nb + ctas + 8.0) * 0x1p-53 + 1e-12;
+    k_gcv_bounds<<<K, 256, 0, S.st>>>(hist, base, (int)nb, grid, widen, bounds);
     launched("k_gcv_bounds");
   }
   std::vector<double> hb(2 * (size_t)K);
@@ -2077,11 +2095,11 @@ void check_deblur_args(const fd_op* op, const fd_smoother* L, int use_gcv, doubl
   if (!L) validation("null smoother");
   if (L->op != op) validation("smoother was built for a different operator");
   if (!mu_used && count > 0) validation("mu_used output is required");  // empty batches: no outputs
-  if (use_gcv || curve) make_grid(mu_min, mu_max, grid_count);  // pipeline.cpp:737-750
+  if (use_gcv || curve) make_grid(mu_min, mu_max, grid_count);  // pipeline.cpp:124-136
   if (!use_gcv && !(fixed_mu > 0.0)) validation("mu must be positive");
 }
 
-// deblur (pipeline.cpp:732-768) of `count` device-resident items; a GCV
+// deblur (pipeline.cpp:120-155) of `count` device-resident items; a GCV
 // degeneracy is flagged in *status (checked by the caller after a sync).
 // f32: g and restored are float arrays (fp32 storage variant, fp64 arithmetic)
 void deblur_dev(const fd_op* op, const fd_smoother* L, const void* g, int use_gcv,
@@ -2193,7 +2211,7 @@ int fd_op_create_1d(const double* psf, int len, int normalize, int n, int bc, fd
 
 namespace {
 HostPsf marginal(const std::vector<double>& w2, int rows, int cols, bool sum_columns) {
-  // marginal_sum_columns / _rows (multidim.cpp:247-263), then make_psf(normalize)
+  // marginal_sum_columns / _rows (multidim.cpp:143-159), then make_psf(normalize)
   std::vector<double> w(sum_columns ? rows : cols, 0.0);
   for (int j = 0; j < rows; ++j)
     for (int k = 0; k < cols; ++k) w[sum_columns ? j : k] += w2[(size_t)j * cols + k];
@@ -2201,7 +2219,7 @@ HostPsf marginal(const std::vector<double>& w2, int rows, int cols, bool sum_col
 }
 
 std::vector<double> make_psf2d(const double* w, int rows, int cols, bool normalize,
-                               bool* symmetric) {  // multidim.cpp:185-213
+                               bool* symmetric) {  // multidim.cpp:81-109
   if (rows < 1 || cols < 1 || rows % 2 == 0 || cols % 2 == 0)
     validation("2D psf needs odd rows and cols");
   std::vector<double> v(w, w + (size_t)rows * cols);
@@ -2304,7 +2322,7 @@ int fd_op_create_2d_separable(const double* psf_a, int len_a, const double* psf_
     *out = nullptr;
     const HostPsf a = make_psf(psf_a, len_a, normalize != 0);
     const HostPsf b = make_psf(psf_b, len_b, normalize != 0);
-    // separable_psf2d (multidim.cpp:226-233): outer product, normalised
+    // separable_psf2d (multidim.cpp:122-129): outer product, normalised
     std::vector<double> w((size_t)len_a * len_b);
     for (int j = 0; j < len_a; ++j)
       for (int k = 0; k < len_b; ++k) w[(size_t)j * len_b + k] = a.w[j] * b.w[k];
@@ -2676,28 +2694,6 @@ int deblur_host_impl(int nops, const fd_op* const* ops, const fd_smoother* const
     if (chunk <= 0) chunk = std::max(std::min(count, 256LL), (count + 15) / 16);
     chunk = std::min(chunk, count);
     const long long nchunks = (count + chunk - 1) / chunk;
-    const cudaStream_t sc = as_stream(stream);
-    cudaStream_t s_in = nullptr, s_out = nullptr;
-    cudaEvent_t ev_in[2], ev_comp[2], ev_out[2];
-    ck(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "stream");
-    ck(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "stream");
-    for (int k = 0; k < 2; ++k) {
-      ck(cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming), "event");
-      ck(cudaEventCreateWithFlags(&ev_comp[k], cudaEventDisableTiming), "event");
-      ck(cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming), "event");
-    }
-    struct Cleanup {
-      cudaStream_t a, b;
-      cudaEvent_t* e[3];
-      ~Cleanup() {
-        cudaStreamSynchronize(a);
-        cudaStreamSynchronize(b);
-        for (auto* ev : e)
-          for (int k = 0; k < 2; ++k) cudaEventDestroy(ev[k]);
-        cudaStreamDestroy(a);
-        cudaStreamDestroy(b);
-      }
-    } cleanup{s_in, s_out, {ev_in, ev_comp, ev_out}};
     // Async copies need page-locked host memory; pageable g / restored are
     // registered for the duration of the call (a copy into pageable memory
     // would block the issuing thread and serialise the pipeline).
@@ -2716,25 +2712,60 @@ int deblur_host_impl(int nops, const fd_op* const* ops, const fd_smoother* const
       ~HostPin() {
         for (void* p : regs) cudaHostUnregister(p);
       }
-    } pins;
+    } pins;  // declared first: unregistered only after the streams below are drained
+    // device buffers of the pipeline, released on sc after every stream is drained
+    struct DevAllocs {
+      cudaStream_t st;
+      std::vector<void*> ptrs;
+      void* get(size_t bytes) {
+        void* p = nullptr;
+        ck(cudaMallocAsync(&p, bytes, st), "alloc");
+        ptrs.push_back(p);
+        return p;
+      }
+      ~DevAllocs() {
+        for (void* p : ptrs) cudaFreeAsync(p, st);
+      }
+    } allocs{as_stream(stream), {}};
+    const cudaStream_t sc = as_stream(stream);
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev_in[2], ev_comp[2], ev_out[2];
+    ck(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking), "stream");
+    for (int k = 0; k < 2; ++k) {
+      ck(cudaEventCreateWithFlags(&ev_in[k], cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&ev_comp[k], cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&ev_out[k], cudaEventDisableTiming), "event");
+    }
+    struct Cleanup {
+      cudaStream_t a, b;
+      cudaEvent_t* e[3];
+      cudaStream_t c;
+      ~Cleanup() {
+        cudaStreamSynchronize(a);
+        cudaStreamSynchronize(b);
+        cudaStreamSynchronize(c);
+        for (auto* ev : e)
+          for (int k = 0; k < 2; ++k) cudaEventDestroy(ev[k]);
+        cudaStreamDestroy(a);
+        cudaStreamDestroy(b);
+      }
+    } cleanup{s_in, s_out, {ev_in, ev_comp, ev_out}, sc};
     pins.pin(g, (size_t)count * N * esz);
     for (int o = 0; o < nops; ++o) pins.pin(restored[o], (size_t)count * N * esz);
     char* slot[2];
     std::vector<char*> oslot((size_t)2 * nops);
-    double* dmu = nullptr;
-    int* dbk = nullptr;
-    int* status = nullptr;
-    ck(cudaMallocAsync(&status, sizeof(int), sc), "alloc");
+    int* status = static_cast<int*>(allocs.get(sizeof(int)));
     ck(cudaMemsetAsync(status, 0, sizeof(int), sc), "memset");
-    ck(cudaMallocAsync(&dmu, (size_t)nops * count * sizeof(double), sc), "alloc");
-    ck(cudaMallocAsync(&dbk, (size_t)nops * count * sizeof(int), sc), "alloc");
+    double* dmu = static_cast<double*>(allocs.get((size_t)nops * count * sizeof(double)));
+    int* dbk = static_cast<int*>(allocs.get((size_t)nops * count * sizeof(int)));
     for (int k = 0; k < 2; ++k) {
-      ck(cudaMallocAsync(&slot[k], (size_t)chunk * N * esz, sc), "alloc");
+      slot[k] = static_cast<char*>(allocs.get((size_t)chunk * N * esz));
       // the last operator restores in place; the others need their own outputs
       for (int o = 0; o < nops; ++o)
         oslot[(size_t)k * nops + o] = slot[k];
       for (int o = 0; o + 1 < nops; ++o)
-        ck(cudaMallocAsync(&oslot[(size_t)k * nops + o], (size_t)chunk * N * esz, sc), "alloc");
+        oslot[(size_t)k * nops + o] = static_cast<char*>(allocs.get((size_t)chunk * N * esz));
     }
     Scratch SG(sc);
     std::unique_ptr<DevGrid> dg;
@@ -2774,13 +2805,6 @@ int deblur_host_impl(int nops, const fd_op* const* ops, const fd_smoother* const
     if (best_k && use_gcv)
       ck(cudaMemcpy(best_k, dbk, (size_t)nops * count * sizeof(int), cudaMemcpyDeviceToHost),
          "best_k");
-    for (int k = 0; k < 2; ++k) {
-      for (int o = 0; o + 1 < nops; ++o) cudaFreeAsync(oslot[(size_t)k * nops + o], sc);
-      cudaFreeAsync(slot[k], sc);
-    }
-    cudaFreeAsync(dmu, sc);
-    cudaFreeAsync(dbk, sc);
-    cudaFreeAsync(status, sc);
     if (h == 3) degenerate("degenerate gcv: all smoother eigenvalues are zero");
   });
 }
@@ -2940,7 +2964,7 @@ int fd_sweep_mu(const fd_op* op, const fd_smoother* L, const double* g, const do
       if (std::isnan(hr[K])) validation("rre: zero ground truth");  // regularize.cpp:258
       double best = INFINITY;
       mu_opt = dg.h.mus[0];
-      for (int k = 0; k < K; ++k) {  // first strict minimum (pipeline.cpp:70-81)
+      for (int k = 0; k < K; ++k) {  // first strict minimum (pipeline.cpp:69-82)
         curve_rre[k] = hr[k];
         if (hr[k] < best) {
           best = hr[k];
@@ -3110,7 +3134,8 @@ int fd_slab_gcv_moments(const fd_op* op, const fd_smoother* L, const void* ghat,
   return guarded([&] {
     check_slab(op, L, 1);
     if (!moments) validation("null output");
-    if (J < 4 || J > 48 || J % 4) validation("moment count must be 4..48 in steps of 4");
+    if (!gcv_moment_count_supported(J))
+      validation("moment count must be 4, 8, 12..20 or 24..48 in steps of 4");
     if (ncols <= 0) {
       std::fill(moments, moments + 2 * J, 0.0);
       return;
@@ -3139,7 +3164,7 @@ int fd_slab_gcv_moments(const fd_op* op, const fd_smoother* L, const void* ghat,
   });
 }
 
-// ---- selection from all-reduced sums (host; gcv_minimize, regularize.cpp:281-351) ----
+// ---- selection from all-reduced sums (host; gcv_minimize, regularize.cpp:144-214) ----
 int fd_gcv_moment_terms(double mu_min, double mu_max, int grid_count, int* J) {
   return guarded([&] {
     make_grid(mu_min, mu_max, grid_count);

@@ -1,4 +1,4 @@
-// gcv_minimize's selection logic (reference src/regularize.cpp:281-351),
+// gcv_minimize's selection logic (reference src/regularize.cpp:144-214),
 // written once as __host__ __device__ code: the sm_100a kernels run it per
 // item on the GPU, and the C-ABI exports the same code on the host
 // (fd_gcv_minimize_host) so the CPU test suite pins it against the reference.
@@ -22,7 +22,7 @@ struct GcvPick {
 };
 
 // First minimum (std::min_element), 1e-12 relative tie test with the
-// geometric midpoint of the tied grid values (regularize.cpp:305-322), and the
+// geometric midpoint of the tied grid values (regularize.cpp:172-185), and the
 // golden-section bracket [mu_{k-1}, mu_{k+1}] clamped at the ends (325-326).
 FD_HD inline GcvPick gcv_pick(const double* mus, const double* logmus, const double* vals,
                               int count) {
@@ -51,7 +51,7 @@ FD_HD inline GcvPick gcv_pick(const double* mus, const double* logmus, const dou
   return p;
 }
 
-// Golden-section refinement in log(mu) (regularize.cpp:324-350), verbatim.
+// Golden-section refinement in log(mu) (regularize.cpp:187-213), verbatim.
 #ifdef __CUDACC__
 #pragma nv_exec_check_disable
 #endif
@@ -89,6 +89,12 @@ FD_HD inline double gcv_golden(const double* mus, int count, int best_k, double 
 // ratio = sqrt(hi/lo) - 1 = e^{Delta} - 1, Delta the grid's log spacing;
 // need (J+1) ratio^J < 1e-17.  Returns 0 when the series would need > 48
 // terms (very coarse grids), in which case the caller evaluates directly.
+// the term counts the moment kernels are instantiated for (launch_moments):
+// 4, 8, every J in 12..20, then 24..48 in steps of 4
+FD_HD inline bool gcv_moment_count_supported(int J) {
+  return J >= 4 && J <= 48 && ((J >= 12 && J <= 20) || J % 4 == 0);
+}
+
 FD_HD inline int gcv_moment_terms(double mu_min, double mu_max, int count) {
   const double delta = (log(mu_max) - log(mu_min)) / (double)(count - 1);
   const double ratio = exp(delta) - 1.0;

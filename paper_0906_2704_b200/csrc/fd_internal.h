@@ -22,7 +22,7 @@ __host__ __device__ __forceinline__ bool is_ho_bc(int bc) {
   return bc == BC_HOC_FOURIER_D1 || bc == BC_HOC_FOURIER_D3;
 }
 constexpr int kHoMax = 3;  // largest border rank (d = 3)
-// Interior trigonometric transform of an axis (boundary.cpp:120-129, operators.cpp:291-312).
+// Interior trigonometric transform of an axis (boundary.cpp:35-43, operators.cpp:181-201).
 enum Interior : int { IK_COS = 0, IK_FOURIER = 1, IK_SINE = 2 };
 // Smoother kinds (regularize.hpp:15) + the first-difference extension.
 enum Smoother : int { SM_IDENTITY = 0, SM_LAPLACIAN = 1, SM_FIRST_DIFFERENCE = 2, SM_CUSTOM = 3 };
@@ -75,7 +75,7 @@ struct AxisDev {
   //   or 1 (qmode 0), so a border combination a q[s+1] + b q[n-2-s] is one
   //   quadratic per line (border_poly).
   double qa1, qa2;
-  // per-axis constants of the trig transforms (trig.cpp:170-234), host-computed
+  // per-axis constants of the trig transforms (trig.cpp:116-180), host-computed
   double inv_sqrt_m, dct_s0, dct_s1, dst_scale;
   double cavr[4], capr[4];
   // Interior coefficient e = i + kl (kl = 1 for the rank-2 borders).
@@ -175,7 +175,7 @@ __host__ __device__ inline HalfRows make_half_rows(int n1, int kl, int kr) {
 
 struct GcvGrid {
   int count;             // K
-  const double* mus;     // K grid values (host std::exp, regularize.cpp:291-293)
+  const double* mus;     // K grid values (host std::exp, regularize.cpp:154-156)
   const double* logmus;  // log of each grid value (tie geometric mean)
 };
 

@@ -1,16 +1,16 @@
 // sm_100a kernels of the transform + filter + GCV restoration path.
 //
 // Reference functions restated here (paths under /root/reference/proj/core):
-//   transform_apply_inverse (analyze)       src/boundary.cpp:338-375
-//   transform_apply (synthesize)            src/boundary.cpp:310-336
-//   cosine_apply / fourier_apply / sine_apply  src/trig.cpp:170-234
-//   SpectralBasis::analyze / synthesize     src/operators.cpp:291-312
-//   tensor_apply (2D: column pass, row pass) src/multidim.cpp:275-302
+//   transform_apply_inverse (analyze)       src/boundary.cpp:253-289
+//   transform_apply (synthesize)            src/boundary.cpp:225-250
+//   cosine_apply / fourier_apply / sine_apply  src/trig.cpp:116-180
+//   SpectralBasis::analyze / synthesize     src/operators.cpp:181-201
+//   tensor_apply (2D: column pass, row pass) src/multidim.cpp:172-198
 //   apply_tikhonov_filter                   include/fastdeblur/regularize.hpp:42-58
 //   gcv_from_coeffs                         include/fastdeblur/regularize.hpp:63-81
-//   gcv_minimize                            src/regularize.cpp:281-351
-//   operator_eigenvalues / eigenvalues_2d   src/operators.cpp:348-397, src/multidim.cpp:311-376
-//   smoothing_eigenvalues(_2d)              src/regularize.cpp:155-175, src/multidim.cpp:433-460
+//   gcv_minimize                            src/regularize.cpp:144-214
+//   operator_eigenvalues / eigenvalues_2d   src/operators.cpp:238-286, src/multidim.cpp:208-272
+//   smoothing_eigenvalues(_2d)              src/regularize.cpp:19-38, src/multidim.cpp:329-356
 //
 // Every line transform is one CTA: the interior trigonometric transform runs
 // in shared memory (fd_fft.cuh), two real lines share one complex FFT, and the
@@ -70,7 +70,7 @@ __device__ __forceinline__ void spectral_at(const Spectral& sp, const Lines& g, 
 // setup kernels
 // ---------------------------------------------------------------------------
 // chirp c_j = e^{-i pi j^2/L}, twiddles e^{-2 pi i j/M}, Bluestein kernel b,
-// DCT quarter-wave twiddles e^{-i pi k/(2m)} (trig.cpp:126-141).
+// DCT quarter-wave twiddles e^{-i pi k/(2m)} (trig.cpp:73-87).
 __global__ void k_init_tables(int L, int M, double2* chirp, double2* tw, double2* b, int mdct,
                               double2* dct_tw) {
   const long long stride = (long long)gridDim.x * blockDim.x;
@@ -164,7 +164,7 @@ __device__ double2 symbol_eval(const double* __restrict__ h, int m, int symmetri
   return make_double2(zr, zi);
 }
 
-// node_i of eigenvalue_grid (operators.cpp:241-272), operation order mirrored
+// node_i of eigenvalue_grid (operators.cpp:130-161), operation order mirrored
 __device__ __forceinline__ double eig_node(int bc, int n, int i) {
   const double kPi = 3.14159265358979323846;
   switch (bc) {
@@ -181,7 +181,7 @@ __device__ __forceinline__ double eig_node(int bc, int n, int i) {
   }
 }
 
-// 1D eigenvalues d (operators.cpp:348-397): symbol at the interior nodes,
+// 1D eigenvalues d (operators.cpp:238-286): symbol at the interior nodes,
 // boundary eigenvalues of corrected operators pinned to exactly 1.
 __global__ void k_eigenvalues_1d(const double* __restrict__ h, int m, int symmetric, int bc,
                                  int n, double2* d) {
@@ -219,7 +219,7 @@ __global__ void k_eigenvalues_1d(const double* __restrict__ h, int m, int symmet
   }
 }
 
-// smoother eigenvalues on the node grid (regularize.cpp:155-175)
+// smoother eigenvalues on the node grid (regularize.cpp:19-38)
 __global__ void k_smoother_1d(int kind, int bc, int n, double* s) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     if (kind == SM_IDENTITY) {
@@ -282,7 +282,7 @@ __global__ void k_eig2d_stage2(const double2* __restrict__ T, int m1, int bc, in
   }
 }
 
-// edges from the marginal 1D eigenvalues, corners 1 (multidim.cpp:352-374)
+// edges from the marginal 1D eigenvalues, corners 1 (multidim.cpp:248-271)
 __global__ void k_eig2d_edges(const double2* __restrict__ d1, const double2* __restrict__ d2,
                               int n1, int n2, double2* d) {
   const int tot = 2 * n1 + 2 * n2;
@@ -340,7 +340,7 @@ __global__ void k_smoother_2d(int kind, const double* __restrict__ s1,
 
 // ---------------------------------------------------------------------------
 // analyze: out = T_X^{-1} in along each line (transform_apply_inverse,
-// boundary.cpp:338-375; plain C / F for reflective / periodic).
+// boundary.cpp:253-289; plain C / F for reflective / periodic).
 // Real input lines are packed in pairs into one complex FFT.
 // ---------------------------------------------------------------------------
 // ---- higher-order borders (extension; AxisDev::hob) ----
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512
     for (int j = threadIdx.x; j < M; j += blockDim.x) {
       double2 val = czero();
       if (j < m) {
-        const int src = j < half ? 2 * j : 2 * (m - 1 - j) + 1;  // trig.cpp:194-195
+        const int src = j < half ? 2 * j : 2 * (m - 1 - j) + 1;  // trig.cpp:139-141
         const int e = interior_elem(ax, src);
         const double a = ld0(e).x, b = ld1(e).x;
         val = cmul(make_double2(a, b), __ldg(&chirp[j]));
@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512
       }
       x[pidx(j)] = val;
     }
-  } else {  // IK_SINE: odd extension (0, u, 0, -rev u) of length 2(m+1) (trig.cpp:219-228)
+  } else {  // IK_SINE: odd extension (0, u, 0, -rev u) of length 2(m+1) (trig.cpp:165-174)
     for (int p = threadIdx.x; p < M; p += blockDim.x) {
       double2 val = czero();
       if (p < L && p != 0 && p != m + 1) {
@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512
   }
   if (dots) block_sum<8>(acc, red);
 
-  // ---- SMW capacitance solve (boundary.cpp:357-368) ----
+  // ---- SMW capacitance solve (boundary.cpp:278-286) ----
   if (threadIdx.x == 0) {
     double2 beta[4] = {czero(), czero(), czero(), czero()};
     if (dots) {
@@ -672,11 +672,11 @@ __global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512
 }
 
 // ---------------------------------------------------------------------------
-// synthesize: out = T_X c (transform_apply, boundary.cpp:310-336), optionally
+// synthesize: out = T_X c (transform_apply, boundary.cpp:225-250), optionally
 // with the Tikhonov filter (mode 1, regularize.hpp:42-58) or the eigenvalue
-// scale of the matvec (mode 2, operators.cpp:317-343) fused into the load.
+// scale of the matvec (mode 2, operators.cpp:207-232) fused into the load.
 // Real bases: pairs of real lines.  Complex bases: one complex line per CTA;
-// real outputs keep Re and report sum(Im^2) per line (operators.cpp:334-340).
+// real outputs keep Re and report sum(Im^2) per line (operators.cpp:222-229).
 // ---------------------------------------------------------------------------
 struct SynthArgs {
   int mode;              // 0 plain, 1 filter, 2 scale by d
@@ -794,7 +794,7 @@ __global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512
   const bool dots = ax.bordered && ax.correction;
 
   if (ax.kind == IK_COS) {
-    // C^T u (trig.cpp:201-212): buf_k = s_k u_k tw_k, Re FFT(buf) reordered.
+    // C^T u (trig.cpp:147-158): buf_k = s_k u_k tw_k, Re FFT(buf) reordered.
     // Two lines: Re FFT(buf) = FFT(herm(buf)), herm(b)_k = (b_k + conj b_{-k})/2.
     const double s0 = sqrt(1.0 / (double)m), s = sqrt(2.0 / (double)m);
     for (int j = threadIdx.x; j < M; j += blockDim.x) {
@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512
       }
       x[pidx(j)] = val;
     }
-  } else if (ax.kind == IK_SINE) {  // Q is an involution (boundary.cpp:124)
+  } else if (ax.kind == IK_SINE) {  // Q is an involution (boundary.cpp:35-43)
     for (int p = threadIdx.x; p < M; p += blockDim.x) {
       double2 val = czero();
       if (p < L && p != 0 && p != m + 1) {
@@ -860,7 +860,7 @@ __global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512
       }
       x[pidx(j)] = val;
     }
-  } else {  // IK_FOURIER: F^H v = conj(F conj(v)) (trig.cpp:170-178)
+  } else {  // IK_FOURIER: F^H v = conj(F conj(v)) (trig.cpp:116-124)
     for (int j = threadIdx.x; j < M; j += blockDim.x) {
       double2 val = czero();
       if (j < m) {
@@ -891,7 +891,7 @@ __global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512
   for (int p = threadIdx.x; p < m; p += blockDim.x) {
     double2 in0, in1 = czero();
     if (ax.kind == IK_COS) {
-      const int idx = (p & 1) ? m - 1 - (p >> 1) : (p >> 1);  // trig.cpp:209-211
+      const int idx = (p & 1) ? m - 1 - (p >> 1) : (p >> 1);  // trig.cpp:154-157
       const double2 Z = cmul(x[pidx(idx)], __ldg(&chirp[idx]));
       in0 = make_double2(Z.x, 0.0);
       in1 = make_double2(Z.y, 0.0);
@@ -988,10 +988,10 @@ __global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512
 // A real line of even length is exactly the interleaved complex buffer z, so
 // the Bluestein size drops from M >= 2R-1 to M >= R-1 (4096 at n = 4096): a
 // 70 KB buffer, several CTAs per SM.  The interior kinds map on this as
-//   cosine (DCT-II / III, trig.cpp:180-214): Makhoul reorder + quarter-wave twiddle,
+//   cosine (DCT-II / III, trig.cpp:126-160): Makhoul reorder + quarter-wave twiddle,
 //     DCT-III via Re DFT(buf) = C2R(herm(conj buf));
 //   Fourier (F / F^H, real data): R2C / C2R of length m (Re F^H c = F^H herm(c));
-//   sine (DST-I, trig.cpp:216-234): R2C of the odd extension, R = 2(m+1).
+//   sine (DST-I, trig.cpp:162-180): R2C of the odd extension, R = 2(m+1).
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -1037,7 +1037,7 @@ __device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity)
 namespace fdb {
 
 __device__ __forceinline__ int makhoul_src(int p, int m, int half) {
-  return p < half ? 2 * p : 2 * (m - 1 - p) + 1;  // trig.cpp:194-195
+  return p < half ? 2 * p : 2 * (m - 1 - p) + 1;  // trig.cpp:139-141
 }
 
 // Two-level table of a twiddle sequence t_k (k < len) in shared memory:
@@ -1060,7 +1060,7 @@ __device__ __forceinline__ Tw2 load_tw2(double2* slots, const double2* tab, int 
   return Tw2{slots, slots + 64};
 }
 
-// boundary column q_e (boundary.cpp:218-303) in registers
+// boundary column q_e (boundary.cpp:162-217) in registers
 __device__ __forceinline__ double q_at(const AxisDev& ax, int e) {
   if (ax.qmode == 0) return (1.0 - e * ax.q_s) * ax.q_inv;
   const double t = ax.q_gb - fma((double)e, ax.q_s, ax.q_o);
@@ -1091,7 +1091,7 @@ __device__ __forceinline__ BorderPoly border_poly(const AxisDev& ax, double a, d
 }
 
 // Border terms of T_X^{-1} y for a real line (transform_apply_inverse,
-// boundary.cpp:338-375).  row_a / row_b are unit impulses, so the two dot
+// boundary.cpp:253-289).  row_a / row_b are unit impulses, so the two dot
 // products are two samples and every thread solves the 2x2 system itself; and
 //   y0 v + xi + yn w - (b0 v + b1 w) = X (x - o0 qhat - on J qhat),
 //   o0 = alpha y0 - alpha b0,  on = alpha yn - alpha b1  (v = -alpha X qhat,
@@ -1409,7 +1409,7 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   }
 }
 
-// Real output of T_X c (transform_apply, boundary.cpp:310-336) with the
+// Real output of T_X c (transform_apply, boundary.cpp:225-250) with the
 // filter of the restoration fused into the coefficient loads.  The two border
 // dots c_a . c_mid, c_b . c_mid are samples of the interior synthesis
 // (top_i, bot_i), written by the thread that produces them.
@@ -1488,7 +1488,7 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
       x[pidx(j)] = cmul(make_double2(ext(2 * j), ext(2 * j + 1)), chirp_at(j));
     }
   } else {
-    // cosine works on conj(buf_i) = s_i c_i conj(tw_i) (DCT-III, trig.cpp:201-212)
+    // cosine works on conj(buf_i) = s_i c_i conj(tw_i) (DCT-III, trig.cpp:147-158)
     const double s0 = ax.dct_s0, s1 = ax.dct_s1;
     auto val_at = [&](int i) {
       const double2 c = cf(interior_elem(ax, i));
@@ -2035,9 +2035,15 @@ __global__ void __launch_bounds__(512) k_gcv_hist(GcvData g, long long base, int
 }
 
 // bounds[k] = (G_lo, G_hi) from the reduced histogram; one CTA per grid point
+// `widen` is the relative rounding allowance of the bounds: every histogram
+// sum is a sum of positive terms in no fixed order (shared atomics, then the
+// cross-CTA reduction), so its relative error is below (terms)*2^-53; G is a
+// ratio num/den^2 of such sums, and the exact pass that later decides among the
+// candidates rounds the same way.  The caller passes
+// 4*(N + bins + CTAs + 8)*2^-53 + 1e-12.
 __global__ void __launch_bounds__(256) k_gcv_bounds(const double* __restrict__ hist,
                                                     long long base, int nb, GcvGrid grid,
-                                                    double* bounds) {
+                                                    double widen, double* bounds) {
   __shared__ double red[32 * 4];
   const int k = blockIdx.x;
   const double mu = grid.mus[k];
@@ -2058,9 +2064,9 @@ __global__ void __launch_bounds__(256) k_gcv_bounds(const double* __restrict__ h
   }
   block_sum<4>(acc, red);
   if (threadIdx.x == 0) {
-    // widened by 1e-12 for the rounding of these sums and of the exact pass
-    bounds[2 * k] = acc[1] / (acc[2] * acc[2]) * (1.0 - 1e-12);
-    bounds[2 * k + 1] = acc[0] / (acc[3] * acc[3]) * (1.0 + 1e-12);
+    // widened for the rounding of these sums and of the exact pass
+    bounds[2 * k] = acc[1] / (acc[2] * acc[2]) * (1.0 - widen);
+    bounds[2 * k + 1] = acc[0] / (acc[3] * acc[3]) * (1.0 + widen);
   }
 }
 
@@ -2424,7 +2430,7 @@ __global__ void __launch_bounds__(256) k_gcv_gemm2(const double* __restrict__ W,
 }
 
 // ---------------------------------------------------------------------------
-// GCV selection (gcv_minimize, regularize.cpp:281-351), one thread per item:
+// GCV selection (gcv_minimize, regularize.cpp:144-214), one thread per item:
 // reduce the grid partials in chunk order, G_k = num/den^2, first minimum,
 // 1e-12 tie test, and the golden-section refinement evaluated from Taylor
 // moments about mu_c = sqrt(lo*hi):
@@ -2651,7 +2657,7 @@ __global__ void k_gcv_golden(const double* __restrict__ partial, int items, int 
   mu_out[item] = gcv_golden(grid.mus, grid.count, k, best, f);
 }
 
-// direct G(mu_item) for every item (gcv_value, regularize.cpp:255-269)
+// direct G(mu_item) for every item (gcv_value, regularize.cpp:119-142)
 __global__ void __launch_bounds__(256) k_gcv_direct(GcvData g, const double* __restrict__ mu_item,
                                                     long long chunk, int nchunks,
                                                     double* partial) {
@@ -2699,7 +2705,7 @@ __global__ void k_gcv_direct_reduce(const double* __restrict__ partial, int item
   G[item] = num / (den * den);
 }
 
-// per-item residue: sqrt of the summed per-line Im^2 (operators.cpp:334-340)
+// per-item residue: sqrt of the summed per-line Im^2 (operators.cpp:222-229)
 // rre (regularize.cpp:249-260) partial sums of `items` restorations against
 // one truth: partial[item][chunk] = (sum t^2, sum (t - f)^2) over the chunk
 __global__ void __launch_bounds__(256) k_rre_partials(const double* __restrict__ f,

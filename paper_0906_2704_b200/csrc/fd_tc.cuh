@@ -1,6 +1,6 @@
 // GCV grid screening on the 5th-generation tensor cores (tcgen05, sm_100a).
 //
-// gcv_minimize (reference src/regularize.cpp:281-351) needs, per item, the
+// gcv_minimize (reference src/regularize.cpp:144-214) needs, per item, the
 // first minimum of G(mu_k) = num_k / den_k^2 over the log grid, with
 //   num_k = sum_e W_e sigma_e(mu_k)^2,  den_k = sum_e mult_e sigma_e(mu_k),
 // W_e = |ghat_e|^2 (Hermitian pairs summed), sigma_e = 1/(r_e + mu_k).  den is
@@ -29,8 +29,10 @@ constexpr int kTcBK = 32;      // elements per tile (the K extent of one stored 
 // elements per pipeline stage: half a tile.  The tile is chunk-major (16-byte
 // chunks of 4 elements for all rows, see tc_tile_index), so each half is one
 // contiguous block and the stage is still one bulk copy per operand; halving
-// the stage doubles the number of stages that fit (4 instead of 2 at BN = 256
-// with the hi/lo split), so the producer refills at a finer grain.
+// the stage doubles the number of stages that fit, so the producer refills at
+// a finer grain.  tc_stages() sizes them for two CTAs per SM (2 stages per CTA
+// at BN = 256 with the hi/lo split), so one CTA's epilogue overlaps the other's
+// copies.
 constexpr int kTcSK = 16;
 // candidate tolerance tau (screen_tau): a relative error bound eps of num~,
 //   single TF32 pass: 2 * 2^-10 (input truncation) + accumulation,

@@ -239,13 +239,13 @@ def _new_op(create, *args):
 
 
 def build_operator(psf, n, bc, normalize=True) -> BlurOperator:
-    """build_operator(make_psf(psf, normalize), n, bc) (operators.cpp:404-412)."""
+    """build_operator(make_psf(psf, normalize), n, bc) (operators.cpp:293-301)."""
     a, p = _host(psf)
     return _new_op(lib().fd_op_create_1d, p, len(a), int(normalize), int(n), _bc(bc))
 
 
 def build_operator_2d(psf2d, n1, n2, bc, normalize=True) -> BlurOperator:
-    """build_operator_2d(make_psf2d(...), n1, n2, bc) (multidim.cpp:413-426)."""
+    """build_operator_2d(make_psf2d(...), n1, n2, bc) (multidim.cpp:309-322)."""
     a, p = _host(psf2d)
     if a.ndim != 2:
         raise ValidationError("2D psf must be a 2D array")
@@ -283,7 +283,7 @@ class Smoother:
 
 
 def smoothing_eigenvalues(kind, op: BlurOperator) -> Smoother:
-    """smoothing_eigenvalues(_2d) (regularize.cpp:155-175, multidim.cpp:433-460)."""
+    """smoothing_eigenvalues(_2d) (regularize.cpp:19-38, multidim.cpp:329-356)."""
     k = SMOOTHER[kind] if isinstance(kind, str) else int(kind)
     h = C.c_void_p()
     check(lib().fd_smoother_create(op._h, k, C.byref(h)))
@@ -339,7 +339,7 @@ class RestorationReport:
 def tikhonov_solve(op: BlurOperator, L: Smoother, g, mu, want_imag_residue=False):
     """tikhonov_solve(_2d) -> (f_reg, imag_residue); mu scalar or per item.
 
-    The imaginary residue of complex bases is a diagnostic (operators.cpp:334-340);
+    The imaginary residue of complex bases is a diagnostic (operators.cpp:222-229);
     requesting it runs the exact one-line-per-FFT synthesis, otherwise two real
     lines share each FFT and imag_residue is None."""
     g = _dev(g)
@@ -379,7 +379,7 @@ def gcv_select(op: BlurOperator, L: Smoother, g, search: GcvSearch = GcvSearch()
 def deblur(op: BlurOperator, L: Smoother, g, mu: MuChoice, want_curve=False,
            search: GcvSearch = GcvSearch(), out=None,
            want_imag_residue=False) -> RestorationReport:
-    """deblur(_2d) (pipeline.cpp:732-778).  imag_residue as in tikhonov_solve.
+    """deblur(_2d) (pipeline.cpp:120-165).  imag_residue as in tikhonov_solve.
     A float32 g takes the fp32 storage variant (fd_deblur_f32: float in / out,
     fp64 arithmetic)."""
     f32 = isinstance(g, torch.Tensor) and g.dtype == torch.float32

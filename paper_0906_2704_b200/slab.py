@@ -1,7 +1,7 @@
 """One 2D image split into row slabs across ranks.
 
 A rank holds rows [r0, r0 + R) of an n1 x n2 image (R = n1 / P).  The
-restoration is the reference's deblur_2d (pipeline.cpp:770-778: gcv_select_2d +
+restoration is the reference's deblur_2d (pipeline.cpp:157-165: gcv_select_2d +
 tikhonov_solve_2d, multidim.cpp:358-442) with the data movement of SURVEY 8e:
 
     rows analyze (local, axis 2)
@@ -185,7 +185,7 @@ def golden_from_moments(mom, J, center, best_G, best_k, search):
 
 def golden_direct(G_of, best_k, best_G, search):
     """Coarse grids (no moment series): the golden section of gcv_minimize
-    (regularize.cpp:324-350, fd_gcv_core.h gcv_golden) with G evaluated on the
+    (regularize.cpp:187-213, fd_gcv_core.h gcv_golden) with G evaluated on the
     reduced partial sums."""
     mus = np.exp(np.log(search.mu_min) + (np.log(search.mu_max) - np.log(search.mu_min)) *
                  np.arange(search.count) / (search.count - 1))
@@ -219,7 +219,7 @@ class SlabResult:
 
 
 def deblur_2d_slabs(backend, comm, g_rows, n1, n2, search) -> SlabResult:
-    """deblur_2d with GCV (pipeline.cpp:770-778) of one image whose rows are
+    """deblur_2d with GCV (pipeline.cpp:157-165) of one image whose rows are
     spread over `comm`; g_rows = this rank's rows [n1/P, n2]."""
     Pw = comm.world
     if n1 % Pw or n2 % Pw:

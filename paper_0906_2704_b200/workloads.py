@@ -5,9 +5,9 @@ paper's unpublished test signals with the shapes, sizes and value
 distributions BASELINE.json names.  Generation follows the reference's
 "true-extended" observation model: the scene is sampled on the extended grid
 (n + 2m per axis, t = (i - m)/n as in acceptance_main.cpp:387-398), blurred
-with ``convolve_valid`` (g_i = sum_j h_j f_{i+j}, pipeline.cpp:628-664) and
+with ``convolve_valid`` (g_i = sum_j h_j f_{i+j}, pipeline.cpp:15-51) and
 perturbed with the reference's ``add_noise`` (SplitMix64 + Box-Muller,
-rescaled so ||eta|| = level ||g||, operators.cpp:443-469).
+rescaled so ||eta|| = level ||g||, operators.cpp:332-358).
 
 Random parameters come from a counter-based SplitMix64 keyed by
 (config, item, draw), so every item is reproducible independently of batch
@@ -36,7 +36,7 @@ _GOLD = np.uint64(0x9E3779B97F4A7C15)
 
 
 def splitmix64(x):
-    """operators.cpp:189-196."""
+    """operators.cpp:78-85."""
     x = np.asarray(x, dtype=np.uint64)
     with np.errstate(over="ignore"):
         x = x ^ (x >> np.uint64(30))
@@ -48,7 +48,7 @@ def splitmix64(x):
 
 
 def bits_to_u01(bits):
-    """(0, 1], operators.cpp:198-201."""
+    """(0, 1], operators.cpp:88-90."""
     return ((np.asarray(bits, dtype=np.uint64) >> np.uint64(11)).astype(np.float64) + 1.0) \
         * (2.0 ** -53)
 
@@ -67,7 +67,7 @@ def draw(key, k):
 
 
 def add_noise(g, level, seed):
-    """Reference add_noise (operators.cpp:443-469) over the last axis; ``seed``
+    """Reference add_noise (operators.cpp:332-358) over the last axis; ``seed``
     broadcasts against the leading axes."""
     g = np.asarray(g, dtype=np.float64)
     if level == 0.0:
@@ -91,7 +91,7 @@ def add_noise(g, level, seed):
 
 
 def convolve_valid(ext, w):
-    """g_i = sum_j h_j f_{i+j} over the last axis (pipeline.cpp:628-642)."""
+    """g_i = sum_j h_j f_{i+j} over the last axis (pipeline.cpp:15-29)."""
     m = (len(w) - 1) // 2
     n = ext.shape[-1] - 2 * m
     g = np.zeros(ext.shape[:-1] + (n,))

@@ -35,8 +35,8 @@ def test_exports_every_declared_symbol():
 
 def test_header_cites_reference_interfaces():
     src = open(HDR).read()
-    for ref in ("operators.cpp:404-412", "boundary.cpp:338-375", "regularize.cpp:281-351",
-                "pipeline.cpp:732-778", "multidim.cpp:413-426"):
+    for ref in ("operators.cpp:293-301", "boundary.cpp:253-289", "regularize.cpp:144-214",
+                "pipeline.cpp:120-165", "multidim.cpp:309-322"):
         assert ref in src
 
 
@@ -59,7 +59,7 @@ def test_header_cites_reference_interfaces():
     lambda: P.build_operator([1.0], 3, "hoc-fourier-d1"),                  # n < d+3
 ])
 def test_validation_errors_match_reference(call):
-    """operators.cpp:173-187, psf.cpp:10-38, multidim.cpp:119-130 (status 2)."""
+    """operators.cpp:62-76, psf.cpp:10-37, multidim.cpp:15-26 (status 2)."""
     with pytest.raises(P.ValidationError):
         call()
 

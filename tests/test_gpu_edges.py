@@ -94,7 +94,7 @@ def test_constant_and_zero_items_in_batch(bc):
     argmin is not a parity quantity -- the compiled reference, numpy and cuFFT
     each pick a different one; only the restoration is compared.  A zero item
     gives an identically zero curve: ties everywhere, the geometric mean of the
-    grid (regularize.cpp:180-190), best_k 0 -- the pair analysis kernels flag
+    grid (regularize.cpp:172-185), best_k 0 -- the pair analysis kernels flag
     all-zero lines so their partner's DFT round-off does not leak into them --
     and an exactly zero restoration.  Both sit among
     ordinary items of a batch large enough for the tensor-core screen."""

@@ -1,5 +1,5 @@
 """GPU parity of the filter + GCV path (regularize.hpp:42-81,
-regularize.cpp:209-374, pipeline.cpp:732-768) against the numpy restatement:
+regularize.cpp:73-247, pipeline.cpp:120-155) against the numpy restatement:
 restorations within 1e-10 relative, identical GCV grid index best_k, refined
 mu within 1e-10 relative (north_star parity contract)."""
 import numpy as np

@@ -27,6 +27,10 @@ def image(n1, n2, item=0):
     ("hoc-cosine", gauss(4, 1.5), "identity", (1e-8, 1.0, 64), 4),
     ("hoc-fourier", onesided(7, 0.25), "laplacian", (1e-6, 1.0, 128), 2),
     ("reflective", gauss(4, 1.5), "laplacian", (1e-6, 1.0, 7), 2),
+    # config 4's grid (moment count J = 13) and config 1's (J = 17): the slab
+    # moment entry point must accept every count the kernels are built for
+    ("hoc-cosine", gauss(6, 2.0), "laplacian", (1e-8, 1.0, 512), 2),
+    ("hoc-cosine", gauss(6, 2.0), "laplacian", (1e-8, 1.0, 256), 2),
 ])
 def test_slab_deblur_matches_single_gpu(bc, psf, smoother, search, world):
     n1, n2 = 192, 256

@@ -1,7 +1,7 @@
 """Row-slab restoration of one 2D image over a real torch.distributed group
 (gloo, world 2, CPU) with the numpy oracle as the per-rank compute:
 the transposes, the summed GCV partials and moments and the selection on the
-sums give the oracle's whole-image deblur_2d (pipeline.cpp:770-778)."""
+sums give the oracle's whole-image deblur_2d (pipeline.cpp:157-165)."""
 import os
 import socket
 import sys

@@ -38,7 +38,7 @@ def test_items_are_independent_of_batching():
 
 
 def test_noise_matches_reference_add_noise():
-    """operators.cpp:443-469 (SplitMix64 + Box-Muller, ||eta|| = level ||g||)."""
+    """operators.cpp:332-358 (SplitMix64 + Box-Muller, ||eta|| = level ||g||)."""
     rng = np.random.default_rng(3)
     for n in (1, 2, 7, 1024, 4097):
         g = rng.uniform(-1, 1, n)
