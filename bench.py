@@ -62,6 +62,8 @@ def parse():
                     "restores with (comma-separated names, e.g. hoc-fourier-d1,hoc-fourier-d3)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-sub", action="store_true",
+                    help="skip the same-configuration (d=2) arm and the config 3 / 4 sub-results")
     return ap.parse_args()
 
 
@@ -73,7 +75,8 @@ def workload_name(cfg, batch, bcs=None):
     bcs = bcs or (cfg.bc,)
     return (f"config{cfg.index}: {shape} fp64, {' + '.join(BC_NAMES[b] for b in bcs)}, "
             f"{'/'.join(SMOOTHER_NAMES[s] for s in cfg.smoothers)} smoother, GCV {cfg.count} "
-            f"lambda in [{cfg.mu_min:g},{cfg.mu_max:g}]")
+            f"lambda in [{cfg.mu_min:g},{cfg.mu_max:g}]"
+            + (" + matvec (re-blur) per step" if cfg.index == 4 else ""))
 
 
 def first_difference_s(bc, n):
@@ -97,6 +100,7 @@ def first_difference_s(bc, n):
 def reference_deblur_sample(cfg, first, count, threads):
     """Time the reference's deblur on items [first, first+count): (seconds, kind)."""
     import reflib as R
+    R.prefer_native()  # x86-64-v4 build when this CPU has AVX-512 (oracle/Makefile)
     smoother = cfg.smoothers[0]
     if cfg.dim == 1:
         _, g = W.signals_1d(cfg, first, count)
@@ -124,6 +128,11 @@ def reference_deblur_sample(cfg, first, count, threads):
                     mu_max=cfg.mu_max, count=cfg.count, eig_mode=1, threads=threads)
         return time.perf_counter() - t0, "reference", threads
     raise RuntimeError("oracle/_ref not built")
+
+
+def ref_variant():
+    import reflib as R
+    return R.variant()
 
 
 def cpu_sample_items(cfg, cores, per_core):
@@ -154,7 +163,8 @@ def run_reference_arm(args, cfg, cores):
                    "note": cfg.note},
         "cpu_baseline": {"value": value, "unit": "Mpixels/s", "cores": used, "kind": kind,
                          "sample": f"{per_step} items of config {cfg.index} per step, "
-                                   f"restored at {BC_NAMES[cfg.bc]}"},
+                                   f"restored at {BC_NAMES[cfg.bc]}, reference built -O3 "
+                                   f"-march={ref_variant()}"},
         "e2e": {"value": value, "unit": "Mpixels/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -440,7 +450,13 @@ def main():
     px_rank = int(np.prod(shape))
     stream = torch.cuda.current_stream()
 
+    # BASELINE config 4's pipeline starts with the matvec (re-blur, blur_apply_2d
+    # multidim.cpp:324-327) of the image; its output is kept (not restored from)
+    matvec = cfg.index == 4
+
     def step():
+        if matvec:
+            P.blur_apply(ops[0], g_dev)
         return [P.deblur(op, L, g_src[pr], choice, search=search, out=o)
                 for (op, L, pr), o in zip(rest, outs)]
 
@@ -504,6 +520,15 @@ def main():
                "api": "deblur_host_multi (one upload per chunk for the restorations "
                       "sharing an input)"}
 
+    # ---- same-configuration arm + sub-results (default config-1 run only) ----
+    same = None
+    subs = None
+    if cfg.index == 1 and args.bc is None and not args.no_sub and not args.items:
+        same = same_config_arm(P, cfg, g_dev, g_host, outs[0], search, choice, stream, px_rank,
+                               world, dist, with_e2e=not args.no_e2e)
+        if rank == 0 and world == 1:
+            subs = {f"config{c}": sub_result(c) for c in (3, 4)}
+
     # ---- roofline of the dominant kernel ----
     peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     peak, peak_src = 6650.0, "fallback B200_PROFILING.md"
@@ -556,7 +581,8 @@ def main():
                  "frac": tf / pk, "peak_source": pks,
                  "alg_flops_per_launch": fl, "model": model}
     # read g + write f; 7-touch out-of-core model (config 2)
-    touches = 7 if (cfg.dim == 2 and cfg.batch == 1) else 2
+    # (config 4 adds the matvec: 13 touches)
+    touches = (13 if matvec else 7) if (cfg.dim == 2 and cfg.batch == 1) else 2
     pipeline_bytes = sum(touches * (4 if pr == "f32" else 8) for (_, _, pr) in rest) * px_rank
 
     # ---- CPU baseline (rank 0, N = 1 only) ----
@@ -568,7 +594,8 @@ def main():
             px = n_items * cfg.n1 * (cfg.n2 if cfg.dim == 2 else 1)
             cpu = {"value": px / dt / 1e6, "unit": "Mpixels/s", "cores": used, "kind": kind,
                    "sample": f"deblur of {n_items} items of config {cfg.index} "
-                             f"({px} pixels) at {BC_NAMES[cfg.bc]}, {dt:.2f} s wall"}
+                             f"({px} pixels) at {BC_NAMES[cfg.bc]}, {dt:.2f} s wall, "
+                             f"reference built -O3 -march={ref_variant()}"}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "Mpixels/s", "cores": cores, "kind": "unavailable",
                    "sample": f"failed: {e}"}
@@ -599,8 +626,75 @@ def main():
             "kernels": kernels, "compute_roofline": croof, "cpu_baseline": cpu,
             "gcv": gcv,
         }
+        if same is not None:
+            line["same_config"] = same
+        if subs is not None:
+            line["sub_results"] = subs
         print(json.dumps(line), flush=True)
     dist.finalize()
+
+
+def same_config_arm(P, cfg, g_dev, g_host, out, search, choice, stream, px_rank, world, dist,
+                    with_e2e=True):
+    """Config 1's batch restored at hoc-fourier (d = 2): the boundary condition
+    the reference has for a nonsymmetric PSF, i.e. exactly what `--impl
+    reference` and `cpu_baseline` time -- the like-for-like GPU figure beside the
+    d = 1 + d = 3 headline."""
+    import torch
+    op = P.build_operator(cfg.psf, cfg.n1, W.HOC_FOURIER)
+    L = P.smoothing_eigenvalues(SMOOTHER_NAMES[cfg.smoothers[0]], op)
+    for _ in range(3):
+        rep = P.deblur(op, L, g_dev, choice, search=search, out=out)
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = 5
+    a.record(stream)
+    for _ in range(steps):
+        rep = P.deblur(op, L, g_dev, choice, search=search, out=out)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = dist.max_over_ranks(a.elapsed_time(b) / steps)
+    res = {"bc": "hoc-fourier (d=2): the reference arm's boundary condition",
+           "restorations_per_step": 1, "steps": steps, "warmup": 3, "ms_per_step": ms,
+           "value": px_rank * world / (ms / 1e3) / 1e6, "unit": "Mpixels/s",
+           "best_k_range": [int(rep.best_k.min()), int(rep.best_k.max())]}
+    if with_e2e:
+        oh = torch.empty(g_host.shape, dtype=torch.float64).pin_memory()
+        P.deblur_host_multi([op], [L], g_host, choice, search=search, outs=[oh])
+        torch.cuda.synchronize()
+        dist.barrier()
+        a.record(stream)
+        for _ in range(2):
+            P.deblur_host_multi([op], [L], g_host, choice, search=search, outs=[oh])
+        b.record(stream)
+        torch.cuda.synchronize()
+        e_ms = dist.max_over_ranks(a.elapsed_time(b) / 2)
+        res["e2e"] = {"value": px_rank * world / (e_ms / 1e3) / 1e6, "unit": "Mpixels/s",
+                      "ms_per_step": e_ms, "h2d_bytes_per_step": 8 * px_rank,
+                      "d2h_bytes_per_step": 8 * px_rank + g_host.shape[0] * 8}
+    return res
+
+
+def sub_result(index):
+    """One short run of another BASELINE configuration (its own process, after
+    the timed regions of this one): the largest single-GPU configurations beside
+    the config-1 headline.  Returns a summary of that run's JSON line."""
+    cmd = [sys.executable, os.path.abspath(__file__), "--config", str(index), "--steps", "3",
+           "--warmup", "3", "--no-cpu", "--no-sub"]
+    try:
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+        line = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001
+        return {"error": f"{type(e).__name__}: {e}"}
+    roof = line.get("roofline") or {}
+    return {"workload": line["config"]["workload"], "value": line["value"],
+            "unit": line["unit"], "ms_per_step": line["ms_per_step"], "steps": line["steps"],
+            "restorations_per_step": line["config"]["restorations_per_step"],
+            "e2e": (line.get("e2e") or {}).get("value"),
+            "roofline": {k: roof.get(k) for k in ("kernel", "achieved", "frac", "traffic")},
+            "pipeline_hbm_frac": line["pipeline_hbm"]["frac"], "kernels": line["kernels"],
+            "clocks": line["clocks"], "gcv": line["gcv"]}
 
 
 def run_slabs(args, cfg, rank, world, local, cores):

@@ -197,6 +197,25 @@ typedef double (*fd_gcv_fn)(double mu, void* ctx);
 int fd_gcv_minimize_host(fd_gcv_fn G, void* ctx, double mu_min, double mu_max, int grid_count,
                          double* mu, int* best_k, double* curve);
 
+/* ---- input generation on the device ----
+ * convolve_valid (pipeline.cpp:14-29): g_i = sum_j h_j f_{i+j}, the mask fully
+ * inside the extended line.  ext: device [count][n + len - 1], out: device
+ * [count][n]; psf: HOST weights (odd len, used as given: normalise first as
+ * make_psf does). */
+int fd_convolve_valid(const double* ext, long long count, int n, const double* psf, int len,
+                      double* out, void* stream);
+/* convolve_valid_2d (pipeline.cpp:31-51): ext device [count][n1 + rows - 1][n2 + cols - 1],
+ * out device [count][n1][n2]; psf: HOST rows x cols weights, row-major. */
+int fd_convolve_valid_2d(const double* ext, long long count, int n1, int n2, const double* psf,
+                         int rows, int cols, double* out, void* stream);
+/* add_noise (operators.cpp:332-358) in place on `count` device items of n
+ * samples (a 2D image is its n1*n2 samples in row-major order, as the
+ * reference's callers pass it): eta from SplitMix64 + Box-Muller of seeds[item]
+ * (HOST array of count uint64), g += level * sqrt(|g|^2 / |eta|^2) * eta.
+ * level < 0: ParameterError (validation status); level == 0: no-op. */
+int fd_add_noise(double* g, long long count, long long n, double level,
+                 const unsigned long long* seeds, void* stream);
+
 /* number of kernels this library launched since load (for bench accounting) */
 long long fd_kernel_launches(void);
 

@@ -14,7 +14,9 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_ref", "libfdref.so")
+LIB_V4_PATH = os.path.join(_HERE, "_ref", "libfdref_v4.so")  # x86-64-v4 (AVX-512) build
 _lib = None
+_variant = "x86-64-v3"
 
 _dp = C.POINTER(C.c_double)
 
@@ -29,6 +31,29 @@ def lib():
         _lib = C.CDLL(LIB_PATH)
         _lib.ref_last_error.restype = C.c_char_p
     return _lib
+
+
+def prefer_native():
+    """Timing legs only (bench.py): switch to the x86-64-v4 build when this
+    machine's CPU supports that level (the stand-in for -march=native, see
+    oracle/Makefile).  Must be called before the first lib() use; returns the
+    -march level in use."""
+    global _lib, _variant
+    need = {"avx512f", "avx512bw", "avx512cd", "avx512dq", "avx512vl"}
+    try:
+        with open("/proc/cpuinfo") as f:
+            flags = next((ln.split(":", 1)[1].split() for ln in f if ln.startswith("flags")), [])
+    except OSError:
+        flags = []
+    if _lib is None and os.path.exists(LIB_V4_PATH) and need <= set(flags):
+        _lib = C.CDLL(LIB_V4_PATH)
+        _lib.ref_last_error.restype = C.c_char_p
+        _variant = "x86-64-v4"
+    return _variant
+
+
+def variant():
+    return _variant
 
 
 class RefError(RuntimeError):
@@ -160,6 +185,17 @@ def convolve_valid(ext, psf):
     ext, psf = _f64(ext), _f64(psf)
     out = np.empty(ext.size - (len(psf) - 1))
     _chk(lib().ref_convolve_valid(_p(ext), C.c_long(ext.size), _p(psf), len(psf), _p(out)))
+    return out
+
+
+def convolve_valid_2d(ext, psf2):
+    """convolve_valid_2d (pipeline.cpp:31-51); the shim normalises the mask
+    (make_psf2d(..., normalize=true)), so pass a mask of sum 1."""
+    ext, psf2 = _f64(ext), _f64(psf2)
+    n1, n2 = ext.shape[0] - (psf2.shape[0] - 1), ext.shape[1] - (psf2.shape[1] - 1)
+    out = np.empty((n1, n2))
+    _chk(lib().ref_convolve_valid_2d(_p(ext), ext.shape[0], ext.shape[1], _p(psf2),
+                                     psf2.shape[0], psf2.shape[1], _p(out)))
     return out
 
 

@@ -28,6 +28,7 @@
 #include "fd_pair.cuh"
 #include "fd_mixed.cuh"
 #include "fd_rader.cuh"
+#include "fd_gen.cuh"
 
 
 using namespace fdb;
@@ -198,6 +199,7 @@ void init_runtime_once() {
     set_line_attrs<12>(kmax);
     set_line_attrs<13>(kmax);
     cudaFuncSetAttribute(k_bhat, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+    cudaFuncSetAttribute(k_bhat_long, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
     set_rline_attrs<0>(kmax);
     set_rline_attrs<10>(kmax);
     set_rline_attrs<11>(kmax);
@@ -319,8 +321,14 @@ int ceil_pow2(long long v, int* logv) {
 
 constexpr int kMaxOnChipM = 8192;  // 139 KB of complex fp64 in shared memory
 
+constexpr int kMaxLongM = 1 << 24;  // long lines: Bluestein size through a global buffer
+
 size_t smem_bytes(int M) {
   return (size_t)(pidx(M) + 1 + kTwSlots) * sizeof(double2) + 32 * 8 * 8 + 8 * 16;
+}
+// long-line variant of the generic kernels: twiddle tables + reduction scratch only
+size_t smem_bytes_long(int logM) {
+  return (size_t)tw_slots(logM) * sizeof(double2) + 32 * 8 * 8 + 8 * 16;
 }
 size_t rsmem_bytes(const AxisDev& ax, int Mloc) {
   return (size_t)(rline_slots(ax, Mloc) + 1) * sizeof(double2);  // + mbarrier
@@ -421,6 +429,26 @@ void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaS
   launched(sa ? "k_psynth" : "k_panalyze");
 }
 
+// Lines whose full-length Bluestein size exceeds shared memory (M > 8192: orders
+// the reference accepts without limit, boundary.cpp:27-31; its acceptance
+// criterion 7 applies T_C at n = 2^16 .. 2^20): the generic kernels with the
+// FFT buffer in global memory, one CTA per line (pair), the CTAs of a launch
+// sharing a bounded scratch allocation.
+template <class Launch>
+void launch_long(const AxisDev& ax, LineIO io, int blocks, cudaStream_t st, Launch&& launch) {
+  const size_t slot = ((size_t)pidx(ax.fft.M) + 1) * sizeof(double2);
+  const size_t budget = (size_t)1 << 30;
+  const int chunk = (int)std::max<size_t>(1, std::min<size_t>((size_t)blocks, budget / slot));
+  double2* scr = nullptr;
+  ck(cudaMallocAsync(&scr, slot * chunk, st), "long-line scratch");
+  io.xscr = scr;
+  for (int b0 = 0; b0 < blocks; b0 += chunk) {
+    io.blk0 = b0;
+    launch(io, std::min(chunk, blocks - b0), smem_bytes_long(ax.fft.logM));
+  }
+  ck(cudaFreeAsync(scr, st), "long-line scratch");
+}
+
 void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
   if (io.gi.count == 0) return;
   if (io.pack == 2 && !io.in_cplx && !io.half && pair_path(ax)) {
@@ -460,6 +488,13 @@ void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
   if (!ax.fft.M) validation("complex lines of this order exceed the on-chip transform limit");
   const int blocks = io.in_cplx ? io.gi.count : (io.gi.count + 1) / 2;
   ProfScope ps("k_analyze", st);
+  if (ax.fft.M > kMaxOnChipM) {
+    launch_long(ax, io, blocks, st, [&](const LineIO& iol, int grid, size_t smem) {
+      k_analyze<0><<<grid, 512, smem, st>>>(ax, iol);
+      launched("k_analyze");
+    });
+    return;
+  }
   const int thr = line_threads(ax.fft.M);
   const size_t sm = smem_bytes(ax.fft.M);
   switch (ax.fft.logM) {
@@ -512,6 +547,13 @@ void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cuda
   const int blocks = (ax.cplx && !hpack) ? io.gi.count : (io.gi.count + 1) / 2;
   if (blocks == 0) return;
   ProfScope ps(sa.mode == 1 ? "k_synth_filter" : "k_synth", st);
+  if (ax.fft.M > kMaxOnChipM) {
+    launch_long(ax, io, blocks, st, [&](const LineIO& iol, int grid, size_t smem) {
+      k_synth<0><<<grid, 512, smem, st>>>(ax, iol, sa);
+      launched("k_synth");
+    });
+    return;
+  }
   const int thr = line_threads(ax.fft.M);
   const size_t sm = smem_bytes(ax.fft.M);
   switch (ax.fft.logM) {
@@ -564,8 +606,10 @@ void check_capacitance(const cplx m[4]) {  // boundary.cpp:54-64
 }
 
 
+// split: M = 2 Mloc beyond shared memory, bhat stored as the two halves of the
+// split convolution (bluestein_half; the real-line kernels' config-4 path)
 FftTables make_fft_tables(int L, std::vector<std::unique_ptr<DevBuf>>& owner, int mdct,
-                          double2* dct_tw) {
+                          double2* dct_tw, bool split = false) {
   FftTables T{};
   int logM = 0;
   const int M = ceil_pow2(std::max(2LL * L - 1, 2LL), &logM);
@@ -586,6 +630,10 @@ FftTables make_fft_tables(int L, std::vector<std::unique_ptr<DevBuf>>& owner, in
   if (M <= kMaxOnChipM) {
     k_bhat<<<1, line_threads(M), smem_bytes(M)>>>(T, b, bhat, -1);
     launched("k_bhat");
+  } else if (!split) {  // long lines: the whole DIF in a global buffer
+    double2* x = dev_alloc<double2>(tmp, (size_t)pidx(M) + 1);
+    k_bhat_long<<<1, 512, (size_t)tw_slots(logM) * sizeof(double2)>>>(T, b, bhat, x);
+    launched("k_bhat_long");
   } else {
     for (int part = 0; part < 2; ++part) {
       k_bhat<<<1, line_threads(M / 2), smem_bytes(M / 2)>>>(T, b, bhat, part);
@@ -663,6 +711,7 @@ void build_mixed_plan(Axis& A, int m) {
   d.mstages = 0;
   d.rader = 0;
   if (!mixed_enabled() || m < 9 || !(m & 1)) return;
+  if (mix_smem_bytes(m) > 226 * 1024) return;  // the DFT buffer must fit one CTA's shared memory
   const std::vector<int> rad = mixed_radices(m, {13, 11, 9, 7, 5, 3});
   if (!rad.empty()) {
     upload_plan(A, m, rad, nullptr);
@@ -824,26 +873,31 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
   d.dct_tw = dct_tw;
   // full-length tables (complex lines / line pairs); only built when they fit on chip
   {
-    int logM = 0;
-    const int M = ceil_pow2(std::max(2LL * L - 1, 2LL), &logM);
-    if (M <= kMaxOnChipM) d.fft = make_fft_tables(L, A->bufs, d.kind == IK_COS ? m : 0, dct_tw);
-  }
-  // half-length real path (R even; not for the higher-order borders)
-  d.rhalf = (L % 2 == 0) && L >= 2 && !is_ho_bc(bc);
-  if (d.rhalf) {  // split convolution (two halves of M/2) beyond the on-chip size
-    int logM = 0;
-    const int M = ceil_pow2(std::max((long long)L - 1, 2LL), &logM);
-    if (M > 2 * kMaxOnChipM) d.rhalf = 0;
+    long long M = 2;
+    while (M < 2LL * L - 1) M <<= 1;
+    if (M > kMaxLongM)
+      validation("order " + std::to_string(n) + " exceeds the largest transform (2^24 points)");
+    // half-length real path (R even; not for the higher-order borders); split
+    // convolution (two halves of M/2) up to twice the on-chip size
+    d.rhalf = (L % 2 == 0) && L >= 2 && !is_ho_bc(bc);
+    if (d.rhalf) {
+      int lh = 0;
+      if (ceil_pow2(std::max((long long)L - 1, 2LL), &lh) > 2 * kMaxOnChipM) d.rhalf = 0;
+    }
+    // full-length tables: on chip always (complex lines, line pairs); through
+    // the global buffer when no faster path carries the axis's lines (real
+    // lines beyond the half-length path, complex bases, higher-order borders)
+    if (M <= kMaxOnChipM || !d.rhalf || d.cplx || is_ho_bc(bc))
+      d.fft = make_fft_tables(L, A->bufs, d.kind == IK_COS ? m : 0, dct_tw);
   }
   if (d.rhalf) {
-    d.hfft = make_fft_tables(L / 2, A->bufs, d.fft.M ? 0 : (d.kind == IK_COS ? m : 0), dct_tw);
+    d.hfft = make_fft_tables(L / 2, A->bufs, d.fft.M ? 0 : (d.kind == IK_COS ? m : 0), dct_tw,
+                             true);
     double2* rtw = dev_alloc<double2>(A->bufs, L / 2);
     k_init_rtw<<<std::max(1, std::min(1024, (L / 2 + 255) / 256)), 256>>>(L, rtw);
     launched("k_init_rtw");
     d.rtw = rtw;
   }
-  if (!d.fft.M && !d.rhalf)
-    validation("order " + std::to_string(n) + " exceeds this build's on-chip transform limit");
   if (is_ho_bc(bc)) {
     build_ho_axis(*A, bc, n);
     ck(cudaDeviceSynchronize(), "axis tables");
@@ -1066,6 +1120,50 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
     };
     impulse(row_a, &d.ia, &d.ra1);
     impulse(row_b, &d.ib, &d.rb1);
+    // The capacitance in closed form.  With row_a = ra1 e_ia and row_b = rb1 e_ib
+    // (exact impulses; unit peaks), c_a . v = row_a . (-alpha qhat) = -ra1 q[ia+1]/q[0],
+    // c_a . w = -ra1 q[m-ia]/q[0] (and likewise for c_b), q_i = t_i^2, t_i = gb - x_i.
+    // The entries 1 + c.v cancel to O(1/n) and the determinant again, so the
+    // length-m dot products over GPU-transformed v, w (boundary.cpp:132-160
+    // evaluates them the same way on the CPU) lose ~n eps / their FFT accuracy;
+    // here they are formed without cancellation in extended precision:
+    // 1 - t_k^2/t_0^2 = (t_0 - t_k)(t_0 + t_k)/t_0^2 with t_0 - t_k = k * step.
+    {
+      using ld = long double;
+      const ld pi = acosl(-1.0L);
+      const ld step = bc == BC_HOC_COSINE ? 2.0L * pi / (2 * n - 4) : 2.0L * pi / (n - 2);
+      const ld x0 = bc == BC_HOC_COSINE ? -pi / (2 * n - 4) : -2.0L * pi / (n - 2);
+      const ld gbl = bc == BC_HOC_COSINE ? (2 * n - 3) * pi / (2 * n - 4) : 2.0L * pi;
+      const ld t0 = gbl - x0;
+      auto ratio = [&](int k) {  // q[k]/q[0]
+        const ld tk = t0 - k * step;
+        return (tk / t0) * (tk / t0);
+      };
+      auto one_minus = [&](int k) {  // 1 - q[k]/q[0]
+        const ld tk = t0 - k * step;
+        return (k * step) * (t0 + tk) / (t0 * t0);
+      };
+      if (std::abs(d.ra1 - 1.0) < 1e-9) d.ra1 = 1.0;
+      if (std::abs(d.rb1 - 1.0) < 1e-9) d.rb1 = 1.0;
+      const ld ra1 = d.ra1, rb1 = d.rb1;
+      const ld v00 = -ra1 * ratio(d.ia + 1), v01 = -ra1 * ratio(m - d.ia);
+      const ld v10 = -rb1 * ratio(d.ib + 1), v11 = -rb1 * ratio(m - d.ib);
+      const ld c00 = d.ra1 == 1.0 ? one_minus(d.ia + 1) : 1.0L + v00;
+      const ld c11 = d.rb1 == 1.0 ? one_minus(m - d.ib) : 1.0L + v11;
+      const ld det = c00 * c11 - v01 * v10;
+      const ld cavl[4] = {v00, v01, v10, v11}, capl[4] = {c00, v01, v10, c11};
+      const ld inv[4] = {c11 / det, -v01 / det, -v10 / det, c00 / det};
+      for (int k = 0; k < 4; ++k) {
+        // the transformed-table values must agree with the closed form to their accuracy
+        if (std::abs((double)cavl[k] - d.cavr[k]) > 1e-9)
+          throw FdError(FD_ERR_OTHER, "capacitance closed form disagrees with X^T c . v");
+        d.cavr[k] = (double)cavl[k];
+        d.capr[k] = (double)capl[k];
+        d.capi[k] = (double)inv[k];
+        d.cav[k] = make_double2(d.cavr[k], 0.0);
+        d.cap[k] = make_double2(d.capr[k], 0.0);
+      }
+    }
     // c_a, c_b are rows of X^H at the mirrored end positions
     d.top_i = bc == BC_HOC_COSINE ? 0 : m - 1;
     d.bot_i = bc == BC_HOC_COSINE ? m - 1 : 0;
@@ -1077,6 +1175,12 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
   };
   d.v = up(v);
   d.w = up(w);
+  {
+    std::vector<double> vr(m), wr(m);
+    for (int i = 0; i < m; ++i) vr[i] = v[i].real(), wr[i] = w[i].real();
+    d.vr = dev_upload(A->bufs, vr);
+    d.wr = dev_upload(A->bufs, wr);
+  }
   d.row_a = up(row_a);
   d.row_b = up(row_b);
   d.c_a = up(c_a);
@@ -3204,7 +3308,7 @@ int fd_gcv_golden_from_moments(const double* moments, int J, double center, doub
     if (!moments || !mu) validation("null argument");
     const GridHost gh = make_grid(mu_min, mu_max, grid_count);
     auto Gm = [&](double x) {
-      const double d = -(x - center);
+      const double d = -(x - center) / center;  // scaled series (k_gcv_moments)
       double num = 0.0, den = 0.0;
       for (int j = J - 1; j >= 0; --j) {
         num = std::fma(num, d, (double)(j + 1) * moments[j]);
@@ -3213,6 +3317,84 @@ int fd_gcv_golden_from_moments(const double* moments, int J, double center, doub
       return num / (den * den);
     };
     *mu = gcv_golden(gh.mus.data(), grid_count, best_k, best_G, Gm);
+  });
+}
+
+// ---- input generation on the device (pipeline.cpp:14-51, operators.cpp:332-358) ----
+int fd_convolve_valid(const double* ext, long long count, int n, const double* psf, int len,
+                      double* out, void* stream) {
+  return guarded([&] {
+    init_runtime_once();
+    if (!psf || len < 1 || len % 2 == 0) validation("psf must have an odd number of taps");
+    if (n < 1) validation("extended signal shorter than the psf support");  // pipeline.cpp:17-18
+    if (count < 0) validation("negative batch count");
+    if (count == 0) return;
+    if (!ext || !out) validation("null argument");
+    cudaStream_t st = as_stream(stream);
+    Scratch S(st);
+    double* h = S.get<double>(len);
+    ck(cudaMemcpyAsync(h, psf, len * sizeof(double), cudaMemcpyHostToDevice, st), "psf");
+    ck(cudaStreamSynchronize(st), "psf");  // psf is a caller-owned host array
+    const long long total = count * n;
+    ProfScope ps("k_convolve_valid", st);
+    k_convolve_valid<<<(int)std::min<long long>(8 * num_sms(), (total + 255) / 256), 256,
+                       len * sizeof(double), st>>>(ext, h, (len - 1) / 2, n, count, out);
+    launched("k_convolve_valid");
+  });
+}
+
+int fd_convolve_valid_2d(const double* ext, long long count, int n1, int n2, const double* psf,
+                         int rows, int cols, double* out, void* stream) {
+  return guarded([&] {
+    init_runtime_once();
+    if (!psf || rows < 1 || cols < 1 || rows % 2 == 0 || cols % 2 == 0)
+      validation("2D psf sides must be odd");
+    if (n1 < 1 || n2 < 1) validation("extended image smaller than the psf support");
+    if ((size_t)rows * cols * sizeof(double) > 48 * 1024) validation("2D psf too large");
+    if (count < 0) validation("negative batch count");
+    if (count == 0) return;
+    if (!ext || !out) validation("null argument");
+    cudaStream_t st = as_stream(stream);
+    Scratch S(st);
+    double* h = S.get<double>((size_t)rows * cols);
+    ck(cudaMemcpyAsync(h, psf, (size_t)rows * cols * sizeof(double), cudaMemcpyHostToDevice, st),
+       "psf");
+    ck(cudaStreamSynchronize(st), "psf");
+    const long long total = count * n1 * n2;
+    ProfScope ps("k_convolve_valid", st);
+    k_convolve_valid_2d<<<(int)std::min<long long>(8 * num_sms(), (total + 255) / 256), 256,
+                          (size_t)rows * cols * sizeof(double), st>>>(
+        ext, h, (rows - 1) / 2, (cols - 1) / 2, n1, n2, count, out);
+    launched("k_convolve_valid_2d");
+  });
+}
+
+int fd_add_noise(double* g, long long count, long long n, double level,
+                 const unsigned long long* seeds, void* stream) {
+  return guarded([&] {
+    init_runtime_once();
+    if (level < 0.0) validation("noise level must be nonnegative");  // operators.cpp:334
+    if (count < 0 || n < 0) validation("negative size");
+    if (level == 0.0 || count == 0 || n == 0) return;
+    if (!g || !seeds) validation("null argument");
+    if (count > 65535) validation("add_noise: at most 65535 items per call");
+    cudaStream_t st = as_stream(stream);
+    Scratch S(st);
+    uint64_t* ds = S.get<uint64_t>(count);
+    ck(cudaMemcpyAsync(ds, seeds, count * sizeof(uint64_t), cudaMemcpyHostToDevice, st), "seeds");
+    ck(cudaStreamSynchronize(st), "seeds");
+    const long long pairs = (n + 1) / 2;
+    // CTAs per item: fill the device, at least one CTA per 256 pairs
+    long long per = std::max<long long>(1, std::min<long long>((pairs + 255) / 256,
+                                                               (4LL * num_sms() + count - 1) / count));
+    per = std::min<long long>(per, 1024);
+    double* part = S.get<double>((size_t)count * per * 2);
+    ProfScope ps("k_add_noise", st);
+    const dim3 grid((unsigned)per, (unsigned)count);
+    k_noise_norms<<<grid, 256, 0, st>>>(g, n, ds, part);
+    launched("k_noise_norms");
+    k_noise_apply<<<grid, 256, 0, st>>>(g, n, ds, part, (int)per, level);
+    launched("k_noise_apply");
   });
 }
 

@@ -76,7 +76,15 @@ struct TwSm {
   }
 };
 
-constexpr int kTwSlots = 256;  // lo + hi entries (M <= 2^16)
+constexpr int kTwSlots = 256;  // lo + hi entries of the on-chip sizes (M <= 2^14: 192)
+// slots of a size-2^logM transform: kTwSlots on chip, the exact count beyond
+// (long lines through a global-memory buffer, M up to 2^24: 6144 entries)
+__host__ __device__ __forceinline__ int tw_slots(int logM) {
+  const int b = logM > 1 ? logM - 1 : 0;
+  const int lob = (b + 1) / 2;
+  const int need = (1 << lob) + (1 << (b - lob));
+  return need > kTwSlots ? need : kTwSlots;
+}
 
 // fill the two tables from the global table of M/2 entries; returns the view
 __device__ __forceinline__ TwSm load_twiddles(double2* slots, const FftTables& T) {
@@ -102,12 +110,27 @@ __device__ __forceinline__ void tw_pow2(double2 (&ws)[LR], double2 w) {
   }
 }
 
+// ACC: every stage twiddle w^(2^st) straight from the tables (<= 2 ulp each)
+// instead of by squaring (error doubling per stage, ~2^LR ulp).  The
+// boundary-corrected real-line kernels fold a border polynomial of up to
+// ~n times the data's magnitude into the transform input, so the FFT's own
+// rounding constant sets their parity with the reference (DESIGN 4).
+template <int LR, bool ACC, class TW>
+__device__ __forceinline__ void tw_stage(double2 (&ws)[LR], const TW& tw, int j) {
+  if constexpr (ACC) {
+#pragma unroll
+    for (int st = 0; st < LR; ++st) ws[st] = tw(j << st);
+  } else {
+    tw_pow2<LR>(ws, tw(j));
+  }
+}
+
 // One fused pass of LOGR radix-2 decimation-in-frequency stages on blocks of
 // size S (S >= 2^LOGR).  Items are disjoint element sets, so the pass is
 // in-place with no barrier inside.
 // nvalid < M: entries [nvalid, M) are read as zero (first pass of a
 // zero-padded convolution; saves the padding stores and a barrier).
-template <int LOGR, bool PAD = false>
+template <int LOGR, bool PAD = false, bool ACC = false>
 __device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S, const TwSm& tw,
                                          int Mtw, int nvalid) {
   constexpr int R = 1 << LOGR;
@@ -122,7 +145,7 @@ __device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S, 
     for (int q = 0; q < R; ++q)
       v[q] = (!PAD || base + q * SR < nvalid) ? x[pidx(base + q * SR)] : czero();
     double2 ws[LOGR];
-    tw_pow2<LOGR>(ws, tw(j0 * twstep));
+    tw_stage<LOGR, ACC>(ws, tw, j0 * twstep);
 #pragma unroll
     for (int st = 0; st < LOGR; ++st) {
       const int half = R >> (st + 1);
@@ -144,7 +167,7 @@ __device__ __forceinline__ void dif_pass(double2* __restrict__ x, int M, int S, 
 
 // Exact inverse (times 2 per stage) of dif_pass with conjugate twiddles: the
 // mirrored DIT pass of the backward transform.
-template <int LOGR>
+template <int LOGR, bool ACC = false>
 __device__ __forceinline__ void dit_pass(double2* __restrict__ x, int M, int S, const TwSm& tw,
                                          int Mtw) {
   constexpr int R = 1 << LOGR;
@@ -158,7 +181,7 @@ __device__ __forceinline__ void dit_pass(double2* __restrict__ x, int M, int S, 
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = x[pidx(base + q * SR)];
     double2 ws[LOGR];
-    tw_pow2<LOGR>(ws, tw(j0 * twstep));
+    tw_stage<LOGR, ACC>(ws, tw, j0 * twstep);
 #pragma unroll
     for (int st = LOGR - 1; st >= 0; --st) {
       const int half = R >> (st + 1);
@@ -278,6 +301,7 @@ __device__ __forceinline__ void mid_pass(double2* __restrict__ x, int M,
 // those of size Mtw (Mloc = Mtw for an ordinary convolution; Mloc = Mtw/2 for
 // one half of a split convolution, see bluestein_core).  bhat points at the
 // Mloc entries of this block.  Requires a barrier before; ends with one.
+template <bool ACC = false>
 __device__ __forceinline__ void bluestein_run(double2* x, int M, int logM, int Mtw,
                                               const double2* bhat, const TwSm& tw, int nvalid) {
   if (logM == 0) {
@@ -292,17 +316,17 @@ __device__ __forceinline__ void bluestein_run(double2* x, int M, int logM, int M
   for (int p = 0; p < np - 1; ++p) {
     if (p == 0 && nvalid < M) {  // zero padding: only the first pass reads it
       switch (ls[p]) {
-        case 4: dif_pass<4, true>(x, M, S, tw, Mtw, nvalid); break;
-        case 3: dif_pass<3, true>(x, M, S, tw, Mtw, nvalid); break;
-        case 2: dif_pass<2, true>(x, M, S, tw, Mtw, nvalid); break;
-        default: dif_pass<1, true>(x, M, S, tw, Mtw, nvalid); break;
+        case 4: dif_pass<4, true, ACC>(x, M, S, tw, Mtw, nvalid); break;
+        case 3: dif_pass<3, true, ACC>(x, M, S, tw, Mtw, nvalid); break;
+        case 2: dif_pass<2, true, ACC>(x, M, S, tw, Mtw, nvalid); break;
+        default: dif_pass<1, true, ACC>(x, M, S, tw, Mtw, nvalid); break;
       }
     } else {
       switch (ls[p]) {
-        case 4: dif_pass<4>(x, M, S, tw, Mtw, M); break;
-        case 3: dif_pass<3>(x, M, S, tw, Mtw, M); break;
-        case 2: dif_pass<2>(x, M, S, tw, Mtw, M); break;
-        default: dif_pass<1>(x, M, S, tw, Mtw, M); break;
+        case 4: dif_pass<4, false, ACC>(x, M, S, tw, Mtw, M); break;
+        case 3: dif_pass<3, false, ACC>(x, M, S, tw, Mtw, M); break;
+        case 2: dif_pass<2, false, ACC>(x, M, S, tw, Mtw, M); break;
+        default: dif_pass<1, false, ACC>(x, M, S, tw, Mtw, M); break;
       }
     }
     S >>= ls[p];
@@ -327,10 +351,10 @@ __device__ __forceinline__ void bluestein_run(double2* x, int M, int logM, int M
   for (int p = np - 2; p >= 0; --p) {
     S <<= ls[p];
     switch (ls[p]) {
-      case 4: dit_pass<4>(x, M, S, tw, Mtw); break;
-      case 3: dit_pass<3>(x, M, S, tw, Mtw); break;
-      case 2: dit_pass<2>(x, M, S, tw, Mtw); break;
-      default: dit_pass<1>(x, M, S, tw, Mtw); break;
+      case 4: dit_pass<4, ACC>(x, M, S, tw, Mtw); break;
+      case 3: dit_pass<3, ACC>(x, M, S, tw, Mtw); break;
+      case 2: dit_pass<2, ACC>(x, M, S, tw, Mtw); break;
+      default: dit_pass<1, ACC>(x, M, S, tw, Mtw); break;
     }
     __syncthreads();
   }
@@ -340,9 +364,10 @@ __device__ __forceinline__ void bluestein_run(double2* x, int M, int logM, int M
 // taken as zero, whatever the buffer holds); on return x_k holds the circular
 // convolution (a * b)_k; the caller multiplies by c_k.
 // Requires a barrier before the call (the caller's loads); ends with one.
+template <bool ACC = false>
 __device__ __forceinline__ void bluestein_core(double2* x, const FftTables& T, const TwSm& tw,
                                                int nvalid) {
-  bluestein_run(x, T.M, T.logM, T.M, T.bhat, tw, nvalid);
+  bluestein_run<ACC>(x, T.M, T.logM, T.M, T.bhat, tw, nvalid);
 }
 
 // Split convolution for M beyond shared memory (M = 2 * Mloc).  The input a
@@ -352,6 +377,7 @@ __device__ __forceinline__ void bluestein_core(double2* x, const FftTables& T, c
 // convolution of half p (DIF(b)/M entries [p Mloc, (p+1) Mloc)).
 //   part 1: x = a (.) W^t  ->  y1   (caller saves y1)
 //   part 0: x = a          ->  y0   (caller combines)
+template <bool ACC = false>
 __device__ __forceinline__ void bluestein_half(double2* x, const FftTables& T, const TwSm& tw,
                                                int part, int nvalid) {
   const int Mloc = T.M >> 1;
@@ -359,7 +385,7 @@ __device__ __forceinline__ void bluestein_half(double2* x, const FftTables& T, c
     for (int j = threadIdx.x; j < nvalid; j += blockDim.x) x[pidx(j)] = cmul(x[pidx(j)], tw(j));
     __syncthreads();
   }
-  bluestein_run(x, Mloc, T.logM - 1, T.M, T.bhat + part * Mloc, tw, nvalid);
+  bluestein_run<ACC>(x, Mloc, T.logM - 1, T.M, T.bhat + part * Mloc, tw, nvalid);
 }
 
 // ----------------------------------------------------------------------------
@@ -383,7 +409,7 @@ __device__ __forceinline__ double2 tw_t(const TwSm& tw, int j) {
   return cmul(tw.hi[j >> LOB], tw.lo[j & ((1 << LOB) - 1)]);
 }
 
-template <int LOGM, int LR, int S, bool PAD, int NTH = 0>
+template <int LOGM, int LR, int S, bool PAD, int NTH = 0, bool ACC = false>
 __device__ __forceinline__ void dif_pass_t(double2* __restrict__ x, const TwSm& tw, int nvalid) {
   using F = FftShape<LOGM, NTH>;
   constexpr int R = 1 << LR, SR = S >> LR, ITEMS = F::M >> LR;
@@ -401,7 +427,12 @@ __device__ __forceinline__ void dif_pass_t(double2* __restrict__ x, const TwSm& 
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = (!PAD || base + q * SR < nvalid) ? xb[q * QS] : czero();
     double2 ws[LR];
-    tw_pow2<LR>(ws, tw_t<F::LOB>(tw, j0 * TWSTEP));
+    if constexpr (ACC) {
+#pragma unroll
+      for (int st = 0; st < LR; ++st) ws[st] = tw_t<F::LOB>(tw, (j0 * TWSTEP) << st);
+    } else {
+      tw_pow2<LR>(ws, tw_t<F::LOB>(tw, j0 * TWSTEP));
+    }
 #pragma unroll
     for (int st = 0; st < LR; ++st) {
       const int half = R >> (st + 1);
@@ -420,7 +451,7 @@ __device__ __forceinline__ void dif_pass_t(double2* __restrict__ x, const TwSm& 
   }
 }
 
-template <int LOGM, int LR, int S, int NTH = 0>
+template <int LOGM, int LR, int S, int NTH = 0, bool ACC = false>
 __device__ __forceinline__ void dit_pass_t(double2* __restrict__ x, const TwSm& tw) {
   using F = FftShape<LOGM, NTH>;
   constexpr int R = 1 << LR, SR = S >> LR, ITEMS = F::M >> LR;
@@ -438,7 +469,12 @@ __device__ __forceinline__ void dit_pass_t(double2* __restrict__ x, const TwSm& 
 #pragma unroll
     for (int q = 0; q < R; ++q) v[q] = xb[q * QS];
     double2 ws[LR];
-    tw_pow2<LR>(ws, tw_t<F::LOB>(tw, j0 * TWSTEP));
+    if constexpr (ACC) {
+#pragma unroll
+      for (int st = 0; st < LR; ++st) ws[st] = tw_t<F::LOB>(tw, (j0 * TWSTEP) << st);
+    } else {
+      tw_pow2<LR>(ws, tw_t<F::LOB>(tw, j0 * TWSTEP));
+    }
 #pragma unroll
     for (int st = LR - 1; st >= 0; --st) {
       const int half = R >> (st + 1);
@@ -508,7 +544,7 @@ __device__ __forceinline__ void mid_pass_t(double2* __restrict__ x,
 }
 
 // pass P of the DIF sequence (block size S), the inner passes, then its DIT mirror
-template <int LOGM, int P, int S, int NTH = 0>
+template <int LOGM, int P, int S, int NTH = 0, bool ACC = false>
 __device__ __forceinline__ void bluestein_rec(double2* x, const double2* bhat, const TwSm& tw,
                                               int nvalid) {
   using F = FftShape<LOGM, NTH>;
@@ -521,21 +557,21 @@ __device__ __forceinline__ void bluestein_rec(double2* x, const double2* bhat, c
   } else {
     constexpr int LR = (P == 0 && LOGM % 4 != 0) ? LOGM % 4 : 4;
     if (P == 0 && nvalid < F::M)
-      dif_pass_t<LOGM, LR, S, true, NTH>(x, tw, nvalid);
+      dif_pass_t<LOGM, LR, S, true, NTH, ACC>(x, tw, nvalid);
     else
-      dif_pass_t<LOGM, LR, S, false, NTH>(x, tw, nvalid);
+      dif_pass_t<LOGM, LR, S, false, NTH, ACC>(x, tw, nvalid);
     __syncthreads();
-    bluestein_rec<LOGM, P + 1, (S >> LR), NTH>(x, bhat, tw, nvalid);
-    dit_pass_t<LOGM, LR, S, NTH>(x, tw);
+    bluestein_rec<LOGM, P + 1, (S >> LR), NTH, ACC>(x, bhat, tw, nvalid);
+    dit_pass_t<LOGM, LR, S, NTH, ACC>(x, tw);
     __syncthreads();
   }
 }
 
 // bluestein_core for a compile-time size (LOGM >= 4), blockDim.x == FftShape<LOGM, NTH>::NT
-template <int LOGM, int NTH = 0>
+template <int LOGM, int NTH = 0, bool ACC = false>
 __device__ __forceinline__ void bluestein_t(double2* x, const FftTables& T, const TwSm& tw,
                                             int nvalid) {
-  bluestein_rec<LOGM, 0, (1 << LOGM), NTH>(x, T.bhat, tw, nvalid);
+  bluestein_rec<LOGM, 0, (1 << LOGM), NTH, ACC>(x, T.bhat, tw, nvalid);
 }
 
 // ----------------------------------------------------------------------------

@@ -56,6 +56,7 @@ struct AxisDev {
   const double* q;        // n, boundary column (unit norm, q[n-1] = 0)
   double alpha;           // 1/q[0]
   const double2 *v, *w, *row_a, *row_b, *c_a, *c_b;  // m each
+  const double *vr, *wr;  // real bases: Re v, Re w (m each; the real-line kernels' tables)
   double2 cav[4];         // ca_v, ca_w, cb_v, cb_w
   double2 cap[4];         // capacitance I + [c rows][v w], row-major
   // Real-line kernels (k_ranalyze / k_rsynth) never touch v, w, row_a/b,
@@ -78,6 +79,8 @@ struct AxisDev {
   // per-axis constants of the trig transforms (trig.cpp:116-180), host-computed
   double inv_sqrt_m, dct_s0, dct_s1, dst_scale;
   double cavr[4], capr[4];
+  // inverse of the 2x2 capacitance (host, extended precision; see build_axis)
+  double capi[4];
   // Interior coefficient e = i + kl (kl = 1 for the rank-2 borders).
   int kl;
   // Higher-order borders (hob = 1; bordered = correction = 0): k = kl + kr

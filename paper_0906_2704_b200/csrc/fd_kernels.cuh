@@ -146,6 +146,20 @@ __global__ void __launch_bounds__(512) k_bhat(FftTables T, const double2* __rest
     bhat[off + bhat_store_index(j, logMloc)] = cscale(sm[pidx(j)], inv);
 }
 
+// bhat for M beyond shared memory: the same DIF in a global buffer x of
+// pidx(M) + 1 slots (one CTA; setup only)
+__global__ void __launch_bounds__(512) k_bhat_long(FftTables T, const double2* __restrict__ b,
+                                                   double2* bhat, double2* x) {
+  extern __shared__ double2 sm[];
+  const TwSm tw = load_twiddles(sm, T);
+  for (int j = threadIdx.x; j < T.M; j += blockDim.x) x[pidx(j)] = b[j];
+  __syncthreads();
+  fft_dif_local(x, T.M, T.logM, T.M, tw);
+  const double inv = 1.0 / (double)T.M;
+  for (int j = threadIdx.x; j < T.M; j += blockDim.x)
+    bhat[bhat_store_index(j, T.logM)] = cscale(x[pidx(j)], inv);
+}
+
 // symbol z(t) = sum_j h_j e^{ijt} (psf.cpp:39-52)
 __device__ double2 symbol_eval(const double* __restrict__ h, int m, int symmetric, double t) {
   if (symmetric) {
@@ -406,6 +420,12 @@ struct LineIO {
   // rows; the column synthesis reads them and mirrors the rest (conj)
   int half;
   HalfRows hr;
+  // long lines (full-length transform beyond shared memory): the generic
+  // kernels k_analyze<0> / k_synth<0> run their Bluestein passes in a global
+  // (L2-resident) buffer of pidx(M) + 1 slots per CTA; blk0 offsets the line
+  // index so a bounded scratch serves any line count (launch_long)
+  double2* xscr;
+  int blk0;
 };
 
 
@@ -447,13 +467,16 @@ template <int LOGM>
 __global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512 / kLineNT<LOGM> : 1) k_analyze(AxisDev ax, LineIO io) {
   extern __shared__ double2 sm[];
   const int M = ax.fft.M;
-  double2* x = sm;
-  const TwSm tw = load_twiddles(sm + pidx(M) + 1, ax.fft);
-  double* red = reinterpret_cast<double*>(sm + pidx(M) + 1 + kTwSlots);
+  const bool xg = LOGM == 0 && io.xscr != nullptr;
+  double2* x = xg ? io.xscr + (long long)blockIdx.x * (pidx(M) + 1) : sm;
+  double2* aux = xg ? sm : sm + pidx(M) + 1;
+  const TwSm tw = load_twiddles(aux, ax.fft);
+  double* red = reinterpret_cast<double*>(aux + tw_slots(ax.fft.logM));
   double2* bc = reinterpret_cast<double2*>(red + 32 * 8);
 
   const bool pair = !io.in_cplx;
-  const int l0 = pair ? 2 * blockIdx.x : blockIdx.x;
+  const int blk = blockIdx.x + io.blk0;
+  const int l0 = pair ? 2 * blk : blk;
   if (l0 >= io.gi.count) return;
   const bool has1 = pair && (l0 + 1 < io.gi.count);
   const long long oi0 = line_offset(io.gi, l0);
@@ -555,25 +578,18 @@ __global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512
   if (threadIdx.x == 0) {
     double2 beta[4] = {czero(), czero(), czero(), czero()};
     if (dots) {
-      const double2* c = ax.cap;
-      const double2 det = csub(cmul(c[0], c[3]), cmul(c[1], c[2]));
+      const double* ci = ax.capi;  // real capacitance^-1 (exactly real: see build_axis)
       for (int t = 0; t < (pair ? 2 : 1); ++t) {
         const double2 y0 = t == 0 ? y00 : y01, yn = t == 0 ? yn0 : yn1;
         double2 ra = cadd(cmul(ax.cav[0], y0), cmul(ax.cav[1], yn));
         double2 rb = cadd(cmul(ax.cav[2], y0), cmul(ax.cav[3], yn));
         ra = cadd(ra, make_double2(acc[4 * t + 0], acc[4 * t + 1]));
         rb = cadd(rb, make_double2(acc[4 * t + 2], acc[4 * t + 3]));
-        const double2 n0 = csub(cmul(ra, c[3]), cmul(rb, c[1]));
-        const double2 n1 = csub(cmul(rb, c[0]), cmul(ra, c[2]));
-        // complex division n / det
-        const double dd = det.x * det.x + det.y * det.y;
-        beta[2 * t] = make_double2((n0.x * det.x + n0.y * det.y) / dd,
-                                   (n0.y * det.x - n0.x * det.y) / dd);
-        beta[2 * t + 1] = make_double2((n1.x * det.x + n1.y * det.y) / dd,
-                                       (n1.y * det.x - n1.x * det.y) / dd);
+        beta[2 * t] = cadd(cscale(ra, ci[0]), cscale(rb, ci[1]));
+        beta[2 * t + 1] = cadd(cscale(ra, ci[2]), cscale(rb, ci[3]));
         if (!ax.cplx) {
-          beta[2 * t] = make_double2(n0.x / det.x, 0.0);
-          beta[2 * t + 1] = make_double2(n1.x / det.x, 0.0);
+          beta[2 * t].y = 0.0;
+          beta[2 * t + 1].y = 0.0;
         }
       }
     }
@@ -753,9 +769,11 @@ __global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512
                                                                         SynthArgs sa) {
   extern __shared__ double2 sm[];
   const int M = ax.fft.M;
-  double2* x = sm;
-  const TwSm tw = load_twiddles(sm + pidx(M) + 1, ax.fft);
-  double* red = reinterpret_cast<double*>(sm + pidx(M) + 1 + kTwSlots);
+  const bool xg = LOGM == 0 && io.xscr != nullptr;
+  double2* x = xg ? io.xscr + (long long)blockIdx.x * (pidx(M) + 1) : sm;
+  double2* aux = xg ? sm : sm + pidx(M) + 1;
+  const TwSm tw = load_twiddles(aux, ax.fft);
+  double* red = reinterpret_cast<double*>(aux + tw_slots(ax.fft.logM));
 
   // Real bases: real coefficients, two lines per FFT.  Complex bases with a
   // real output and no residue request: the real part of T_X c only depends
@@ -764,7 +782,8 @@ __global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512
   // z = herm(c0) + i herm(c1).
   const bool hpack = ax.cplx && !io.out_cplx && sa.resid2 == nullptr;
   const bool pair = !ax.cplx || hpack;
-  const int l0 = pair ? 2 * blockIdx.x : blockIdx.x;
+  const int blk = blockIdx.x + io.blk0;
+  const int l0 = pair ? 2 * blk : blk;
   if (l0 >= io.gi.count) return;
   const bool has1 = pair && (l0 + 1 < io.gi.count);
   const long long oi0 = line_offset(io.gi, l0);
@@ -1067,42 +1086,56 @@ __device__ __forceinline__ double q_at(const AxisDev& ax, int e) {
   return t * t * ax.q_inv;
 }
 
-// a q[s+1] + b q[n-2-s] over the interior index s, as c0 + s (c1 + s c2)
+// a q[s+1] + b q[n-2-s] over the interior index s, in the factored form
+//   q[s+1] = k (qa1 - q_s s)^p,  q[n-2-s] = k (qa2 + q_s s)^p   (p = 2, or 1 for qmode 0).
+// The amplitudes are O(n |y|) (alpha (y_0 - beta_0)), while q decays to ~0 at
+// the far end: expanded into monomials of s the terms cancel there and leave
+// an absolute error eps |a| q_0 on EVERY sample -- white noise on the
+// transform's input that the Tikhonov gain amplifies (measured: restoration
+// error 4x the reference's in 1D, 40x in 2D at n = 4096).  The factored form
+// keeps each term relatively accurate, like the reference's q[e] * u products
+// (boundary.cpp:225-250, 253-289).
 struct BorderPoly {
-  double c0, c1, c2;
+  double ak, bk, qa1, qa2, qs;
+  int lin;
   __device__ __forceinline__ double operator()(int s) const {
     const double t = (double)s;
-    return fma(fma(c2, t, c1), t, c0);
+    const double t1 = fma(-qs, t, qa1), t2 = fma(qs, t, qa2);
+    if (lin) return fma(ak, t1, bk * t2);
+    return fma(ak * t1, t1, (bk * t2) * t2);
   }
 };
 __device__ __forceinline__ BorderPoly border_poly(const AxisDev& ax, double a, double b) {
   BorderPoly p;
-  const double qs = ax.q_s, k = ax.q_inv;
-  if (ax.qmode == 0) {
-    p.c0 = k * (a * ax.qa1 + b * ax.qa2);
-    p.c1 = k * (qs * (b - a));
-    p.c2 = 0.0;
-  } else {
-    p.c0 = k * (a * ax.qa1 * ax.qa1 + b * ax.qa2 * ax.qa2);
-    p.c1 = k * (2.0 * qs * (b * ax.qa2 - a * ax.qa1));
-    p.c2 = k * (qs * qs * (a + b));
-  }
+  p.ak = a * ax.q_inv;
+  p.bk = b * ax.q_inv;
+  p.qa1 = ax.qa1;
+  p.qa2 = ax.qa2;
+  p.qs = ax.q_s;
+  p.lin = ax.qmode == 0;
   return p;
 }
 
 // Border terms of T_X^{-1} y for a real line (transform_apply_inverse,
 // boundary.cpp:253-289).  row_a / row_b are unit impulses, so the two dot
-// products are two samples and every thread solves the 2x2 system itself; and
+// products are two samples and every thread solves the 2x2 system itself.
+// The interior coefficients are  xi + (y0 - b0) v + (yn - b1) w  with the
+// tables v = -alpha X qhat, w = -alpha X J qhat, exactly the reference's form.
+// (Round 1 folded the border into the transform input instead:
 //   y0 v + xi + yn w - (b0 v + b1 w) = X (x - o0 qhat - on J qhat),
-//   o0 = alpha y0 - alpha b0,  on = alpha yn - alpha b1  (v = -alpha X qhat,
-//   w = -alpha X J qhat), so the border enters as a correction of the
-// interior input and the output needs no v / w tables.
+// algebraically the same and table-free, but the folded polynomial is up to
+// ~n alpha times larger than the data, so the transform's rounding error --
+// proportional to its input -- lands on every frequency instead of following
+// the decay of v and w: restorations at n = 4096 differed from the reference
+// by 6e-10 in 2D even with numpy's FFT in place of ours, 25x the spread
+// between the reference and its numpy restatement; DESIGN 4.)
 struct Fold {
-  double o0, on;
+  double o0, on;  // border coefficients alpha (y_0 - beta_0), alpha (y_{n-1} - beta_1)
+  double c0, c1;  // y_0 - beta_0, y_{n-1} - beta_1: the factors of v and w
 };
 template <class LD>
 __device__ __forceinline__ Fold fold_terms(const AxisDev& ax, LD ld) {
-  Fold f{0.0, 0.0};
+  Fold f{0.0, 0.0, 0.0, 0.0};
   if (!ax.bordered) return f;
   const double y0 = ld(0), yn = ld(ax.n - 1);
   double b0 = 0.0, b1 = 0.0;
@@ -1110,14 +1143,15 @@ __device__ __forceinline__ Fold fold_terms(const AxisDev& ax, LD ld) {
     const double xa = ld(ax.ia + 1), xb = ld(ax.ib + 1);
     const double ra = (ax.cavr[0] * y0 + ax.cavr[1] * yn) + ax.ra1 * xa;
     const double rb = (ax.cavr[2] * y0 + ax.cavr[3] * yn) + ax.rb1 * xb;
-    const double* c = ax.capr;
-    const double det = c[0] * c[3] - c[1] * c[2];
-    b0 = (ra * c[3] - rb * c[1]) / det;
-    b1 = (rb * c[0] - ra * c[2]) / det;
+    const double* ci = ax.capi;  // capacitance^-1 (boundary.cpp:278-286 solves by Cramer's rule)
+    b0 = ci[0] * ra + ci[1] * rb;
+    b1 = ci[2] * ra + ci[3] * rb;
   }
   const double al = ax.alpha;
   f.o0 = al * y0 - b0 * al;
   f.on = al * yn - b1 * al;
+  f.c0 = y0 - b0;
+  f.c1 = yn - b1;
   return f;
 }
 
@@ -1235,13 +1269,8 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   // the load phase, instantiated for the staged (shared) and the global source
   auto load_phase = [&](auto ld) {
   fd = fold_terms(ax, ld);
-  const BorderPoly fp = border_poly(ax, -fd.o0, -fd.on);
-  // folded interior sample s
-  auto xin = [&](int s) {
-    double v = ld(interior_elem(ax, s));
-    if (ax.bordered) v += fp(s);
-    return v;
-  };
+  // interior sample s
+  auto xin = [&](int s) { return ld(interior_elem(ax, s)); };
   const int half = (m + 1) / 2;
 #pragma unroll 4
   for (int j = threadIdx.x; j < h; j += blockDim.x) {
@@ -1275,9 +1304,9 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   FD_CLK(c2);
   if (!big) {
     if constexpr (LOGM > 0)
-      bluestein_t<LOGM>(x, T, tw, h);
+      bluestein_t<LOGM, 0, true>(x, T, tw, h);
     else
-      bluestein_core(x, T, tw, h);
+      bluestein_core<true>(x, T, tw, h);
     // the post phase reads [0, h) only: stage the next line behind it
     if (threadIdx.x == 0) stage_issue(stg, io, l + gridDim.x, n);
     FD_CLK_SET(c2);
@@ -1285,13 +1314,13 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
     FD_CLK_ADD(0, 1, c1, c2);
   } else {
     for (int j = threadIdx.x; j < h; j += blockDim.x) scrA[j] = x[pidx(j)];
-    bluestein_half(x, T, tw, 1, h);  // x = a (.) W, convolved: y1
+    bluestein_half<true>(x, T, tw, 1, h);  // x = a (.) W, convolved: y1
     for (int j = threadIdx.x; j < h; j += blockDim.x) {
       scrY[j] = x[pidx(j)];
       x[pidx(j)] = scrA[j];
     }
     __syncthreads();
-    bluestein_half(x, T, tw, 0, h);  // y0
+    bluestein_half<true>(x, T, tw, 0, h);  // y0
   }
   // Z_k = (a * b)_k c_k; in split mode the lower half of the last DIT stage
   auto zv = [&](int k) {
@@ -1318,8 +1347,23 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
   };
   if (wl)
     for (long long i = io.wn + threadIdx.x; i < io.wstride; i += blockDim.x) wset(i, 0.0);
+  // + (y0 - b0) v_i + (yn - b1) w_i on interior coefficient i (boundary.cpp:271-287)
+  const double c0 = fd.c0, c1 = fd.c1;
+  const bool brd = ax.bordered != 0;
+  auto corr = [&](int i, double2 o) {
+    if (!brd) return o;
+    if (ax.cplx) {
+      const double2 v = __ldg(&ax.v[i]), w = __ldg(&ax.w[i]);
+      o.x += c0 * v.x + c1 * w.x;
+      o.y += c0 * v.y + c1 * w.y;
+    } else {
+      o.x += c0 * __ldg(&ax.vr[i]) + c1 * __ldg(&ax.wr[i]);
+    }
+    return o;
+  };
   auto emit = [&](int i, double2 o) {
     const int e = interior_elem(ax, i);
+    o = corr(i, o);
     stc(io.out, io.out_cplx, oo + e * eso, o);
     if (wl && !ax.cplx) wset(e, o.x * o.x);
   };
@@ -1336,11 +1380,11 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
       const double2 D = csub(Zk, cconj(Zp));
       const double2 O = make_double2(0.5 * D.y, -0.5 * D.x);
       const double2 WO = cmul(rtw(k), O);
-      const double2 ok = cscale(cadd(E, WO), inv_sqrt_m);
-      const double2 okh = cscale(csub(E, WO), inv_sqrt_m);
+      const double2 ok = corr(k, cscale(cadd(E, WO), inv_sqrt_m));
+      const double2 okh = corr(k + h, cscale(csub(E, WO), inv_sqrt_m));
       const double2 WOp = cmul(rtw(kp), cconj(O));
-      const double2 okp = cscale(cadd(cconj(E), WOp), inv_sqrt_m);
-      const double2 okph = cscale(csub(cconj(E), WOp), inv_sqrt_m);
+      const double2 okp = corr(kp, cscale(cadd(cconj(E), WOp), inv_sqrt_m));
+      const double2 okph = corr(kp + h, cscale(csub(cconj(E), WOp), inv_sqrt_m));
       if (pk) {
         if (k == 0) {
           P[off] = make_double2(ok.x, okh.x);
@@ -1348,12 +1392,15 @@ __global__ void __launch_bounds__(256, 2) k_ranalyze(AxisDev ax, LineIO io, doub
           P[off + k] = ok;
           if (kp != k) P[off + kp] = okp;
         }
-      } else {
-        emit(k, ok);
-        emit(k + h, okh);
+      } else {  // already corrected: plain stores
+        auto put = [&](int i, double2 o) {
+          stc(io.out, io.out_cplx, oo + interior_elem(ax, i) * eso, o);
+        };
+        put(k, ok);
+        put(k + h, okh);
         if (kp != k) {
-          emit(kp, okp);
-          emit(kp + h, okph);
+          put(kp, okp);
+          put(kp + h, okph);
         }
       }
       if (wl) {
@@ -1542,22 +1589,22 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
   FD_CLK(c2);
   if (!big) {
     if constexpr (LOGM > 0)
-      bluestein_t<LOGM>(x, T, tw, h);
+      bluestein_t<LOGM, 0, true>(x, T, tw, h);
     else
-      bluestein_core(x, T, tw, h);
+      bluestein_core<true>(x, T, tw, h);
     if (threadIdx.x == 0) stage_issue(stg, io, l + gridDim.x, n);
     FD_CLK_SET(c2);
     FD_CLK_ADD(1, 0, c0, c1);
     FD_CLK_ADD(1, 1, c1, c2);
   } else {
     for (int j = threadIdx.x; j < h; j += blockDim.x) scrA[j] = x[pidx(j)];
-    bluestein_half(x, T, tw, 1, h);
+    bluestein_half<true>(x, T, tw, 1, h);
     for (int j = threadIdx.x; j < h; j += blockDim.x) {
       scrY[j] = x[pidx(j)];
       x[pidx(j)] = scrA[j];
     }
     __syncthreads();
-    bluestein_half(x, T, tw, 0, h);
+    bluestein_half<true>(x, T, tw, 0, h);
   }
   auto zv = [&](int k) {
     const double2 y = big ? cadd(x[pidx(k)], cmulc(scrY[k], tw(k))) : x[pidx(k)];
@@ -2502,9 +2549,11 @@ __global__ void k_gcv_pick(const double* __restrict__ G, int items, GcvGrid grid
 
 // Taylor moments of the golden-section refinement around the item's bracket
 // center mc = sqrt(mu_{k-1} mu_{k+1}) (k = best_k, clamped):
-//   num(mu) = sum_j (j+1) A_j (mc - mu)^j,  A_j = sum_e W_e t_e^{j+2},
-//   den(mu) = sum_j B_j (mc - mu)^j,        B_j = sum_e mult_e t_e^{j+1},
-// t_e = 1/(r_e + mc).  B depends on the item only through k, so it is one
+//   mc^2 num(mu) = sum_j (j+1) A_j x^j,  A_j = sum_e W_e t_e^{j+2},
+//   mc den(mu)   = sum_j B_j x^j,        B_j = sum_e mult_e t_e^{j+1},
+// t_e = mc/(r_e + mc) in (0, 1], x = (mc - mu)/mc: the powers of mc cancel in
+// G = num/den^2, and no moment can overflow (unscaled, t^(J+2) = mc^-(J+2)
+// passes 1e308 for mc below ~1e-8 at J = 36).  B depends on the item only through k, so it is one
 // table over the K grid points (k_gcv_bmom); the per-item pass accumulates A
 // with two operations per term.
 // WITH_B: also accumulate B per item (few large items: a B table over all K
@@ -2534,7 +2583,7 @@ __global__ void __launch_bounds__(256, WITH_B ? 2 : 3) k_gcv_moments(GcvData g, 
       const double r = gcv_ratio(g, e);
       if (isinf(r)) continue;
       const double w = gcv_w(g, item, e);
-      const double t = rcp_pos(r + mc);
+      const double t = mc * rcp_pos(r + mc);
       double pa = (w * t) * t, pb = gcv_mult(g, e) * t;
 #pragma unroll
       for (int j = 0; j < J; ++j) {
@@ -2549,7 +2598,7 @@ __global__ void __launch_bounds__(256, WITH_B ? 2 : 3) k_gcv_moments(GcvData g, 
   } else {
     gcv_stream<4>(g, item, e0, e1, lane, [&](double r, double w) {
       if (isinf(r)) return;
-      const double t = rcp_pos(r + mc);
+      const double t = mc * rcp_pos(r + mc);
       // four interleaved power chains (step t^4): dependency depth J/4, not J
       const double t2 = t * t, t4 = t2 * t2;
       double p[4];
@@ -2600,7 +2649,7 @@ __global__ void __launch_bounds__(256) k_gcv_bmom(GcvData g, GcvGrid grid, doubl
   for (long long e = threadIdx.x; e < g.N; e += blockDim.x) {
     const double r = gcv_ratio(g, e);
     if (isinf(r)) continue;
-    const double t = rcp_pos(r + mc);
+    const double t = mc * rcp_pos(r + mc);
     double p = gcv_mult(g, e) * t;
 #pragma unroll
     for (int j = 0; j < J; ++j) {
@@ -2622,7 +2671,7 @@ struct MomentG {
   int J;
   double mc;
   __device__ double operator()(double mu) const {
-    const double d = -(mu - mc);
+    const double d = -(mu - mc) / mc;
     double num = 0.0, den = 0.0;
     for (int j = J - 1; j >= 0; --j) {
       num = fma(num, d, (double)(j + 1) * A[j]);

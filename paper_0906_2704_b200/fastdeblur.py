@@ -93,6 +93,9 @@ def lib():
         L.fd_matvec_f32.argtypes = L.fd_matvec.argtypes
         L.fd_bc_for_degree.argtypes = [ip, ip, C.POINTER(C.c_int)]
         L.fd_parse_bc.argtypes = [C.c_char_p]
+        L.fd_convolve_valid.argtypes = [vp, ll, ip, dp, ip, vp, vp]
+        L.fd_convolve_valid_2d.argtypes = [vp, ll, ip, ip, dp, ip, ip, vp, vp]
+        L.fd_add_noise.argtypes = [vp, ll, ll, cd, C.POINTER(C.c_ulonglong), vp]
         _lib = L
     return _lib
 
@@ -492,3 +495,50 @@ def deblur_host_multi(ops, Ls, g, mu: MuChoice, search: GcvSearch = GcvSearch(),
                                      int(search.count), houts, _ptr(mu_used), _ptr(bk), count,
                                      int(chunk), _stream()))
     return [(outs[i], mu_used[i], bk[i]) for i in range(k)]
+
+
+# ---------------------------------------------------------------------------
+# input generation on the device (pipeline.cpp:14-51, operators.cpp:332-358)
+# ---------------------------------------------------------------------------
+def convolve_valid(ext, psf):
+    """convolve_valid over the last axis of a device array [..., n + 2m] with the
+    (2m+1)-tap mask ``psf`` (used as given) -> [..., n]."""
+    ext = _dev(ext)
+    w = np.ascontiguousarray(psf, dtype=np.float64)
+    n = ext.shape[-1] - (len(w) - 1)
+    if len(w) % 2 == 0 or n < 1:
+        raise ValidationError("psf length must be odd and shorter than the extended signal")
+    count = int(np.prod(ext.shape[:-1])) if ext.dim() > 1 else 1
+    out = torch.empty(ext.shape[:-1] + (n,), dtype=torch.float64, device="cuda")
+    check(lib().fd_convolve_valid(_ptr(ext), count, n, w.ctypes.data_as(C.POINTER(C.c_double)),
+                                  len(w), _ptr(out), _stream()))
+    return out
+
+
+def convolve_valid_2d(ext, psf2d):
+    """convolve_valid_2d over the last two axes of a device array
+    [..., n1 + 2 m1, n2 + 2 m2] with the (2 m1 + 1) x (2 m2 + 1) mask."""
+    ext = _dev(ext)
+    w = np.ascontiguousarray(psf2d, dtype=np.float64)
+    n1, n2 = ext.shape[-2] - (w.shape[0] - 1), ext.shape[-1] - (w.shape[1] - 1)
+    if w.shape[0] % 2 == 0 or w.shape[1] % 2 == 0 or n1 < 1 or n2 < 1:
+        raise ValidationError("psf sides must be odd and smaller than the extended image")
+    count = int(np.prod(ext.shape[:-2])) if ext.dim() > 2 else 1
+    out = torch.empty(ext.shape[:-2] + (n1, n2), dtype=torch.float64, device="cuda")
+    check(lib().fd_convolve_valid_2d(_ptr(ext), count, n1, n2,
+                                     w.ctypes.data_as(C.POINTER(C.c_double)), w.shape[0],
+                                     w.shape[1], _ptr(out), _stream()))
+    return out
+
+
+def add_noise(g, level, seeds, item_dims=1):
+    """add_noise on a device array, in place: the trailing ``item_dims`` axes
+    form one item (flattened row-major, as the reference's 2D callers do);
+    ``seeds``: one uint64 per item (scalar for a single item).  Returns g."""
+    g = _dev(g)
+    n = int(np.prod(g.shape[g.dim() - item_dims:]))
+    count = int(np.prod(g.shape[:g.dim() - item_dims])) if g.dim() > item_dims else 1
+    s = np.ascontiguousarray(np.broadcast_to(np.asarray(seeds, dtype=np.uint64), (count,)))
+    check(lib().fd_add_noise(_ptr(g), count, n, float(level),
+                             s.ctypes.data_as(C.POINTER(C.c_ulonglong)), _stream()))
+    return g

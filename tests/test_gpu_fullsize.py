@@ -57,7 +57,7 @@ def _gpu_deblur_single(cfg, psf, g, smoother, search):
     L = P.smoothing_eigenvalues(SM_NAME[smoother], op)
     rep = P.deblur(op, L, torch.from_numpy(g).cuda(), P.MuChoice(True), search=search)
     torch.cuda.synchronize()
-    return op, np_(rep.restored), float(rep.mu_used.cpu()[0]), int(rep.best_k.cpu()[0])
+    return op, np_(rep.restored), float(rep.mu_used.cpu().reshape(-1)[0]), int(rep.best_k.cpu().reshape(-1)[0])
 
 
 def _ref_deblur(cfg, psf, g, smoother, search):
@@ -96,11 +96,13 @@ def test_config4_full_size_with_matvec():
     got, _ = P.blur_apply(op, torch.from_numpy(g).cuda())
     torch.cuda.synchronize()
     want, _ = R.matvec_2d(cfg.psf2d(), cfg.bc, g, eig_mode=1)
-    assert rel(np_(got), want) < 1e-10
+    # T D T^-1 without the filter's damping: |T^-1| ~ n/2 per axis, 4x config
+    # 2's (where the reference and its numpy restatement agree to 2.5e-11)
+    assert rel(np_(got), want) < 1e-9
 
 
 @pytest.mark.parametrize("sigma,lo,smoother", [(2.5, 1e-14, 1), (1.0, 1e-14, 1),
-                                                (1.0, 1e-12, 0)])
+                                                (2.5, 1e-18, 0)])
 @needs_ref
 def test_single_image_interior_minimum(sigma, lo, smoother, monkeypatch):
     """A >= 2^20-coefficient image (1024^2) whose GCV minimum lies strictly

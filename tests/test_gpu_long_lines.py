@@ -1,0 +1,150 @@
+"""Orders beyond the on-chip transform sizes (VERDICT r1 Missing #1).
+
+The reference accepts any n >= 5 (boundary.cpp:27-31) and its acceptance
+criterion 7 applies T_C at n = 2^16 .. 2^20 (acceptance_main.cpp:575-614).
+Lines whose full-length Bluestein transform does not fit in shared memory run
+the generic kernels with the FFT buffer in global memory (launch_long,
+fd_capi.cu).  Checked against the numpy restatement of boundary.cpp /
+trig.cpp; tolerances as tests/test_gpu_transforms.py (analyze through the
+2x2 SMW solve at 1e-9, synthesize and round trips at 1e-10) with the
+conditioning of the d = 3 borders (cond(T) ~ n^2.5) for the higher-order code."""
+import numpy as np
+import pytest
+import torch
+
+import fdoracle as O
+import paper_0906_2704_b200 as P
+from paper_0906_2704_b200 import workloads as W
+from util import np_, rel, gauss, onesided
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("bc,n", [
+    (O.HOC_COSINE, 16391),      # odd interior, beyond the half-length real path
+    (O.HOC_COSINE, 1 << 17),    # acceptance c7 sizes
+    (O.HOC_COSINE, 1 << 20),
+    (O.ANTIREFLECTIVE, 16384),  # DST-I odd extension 2(m+1) = 32766
+    (O.ANTIREFLECTIVE, 8195),
+    (O.REFLECTIVE, 40001),
+    (O.PERIODIC, 5000),         # complex basis: full-length complex lines
+    (O.PERIODIC, 70001),
+    (O.HOC_FOURIER, 16384),
+    (O.HOC_FOURIER, 100003),
+])
+def test_long_analyze_synthesize(bc, n, rng):
+    op = P.build_operator([1.0], n, bc)
+    b = O.SpectralBasis(bc, n)
+    x = rng.standard_normal((3, n))
+    got = np_(op.analyze(torch.from_numpy(x)))
+    want = b.analyze(x.astype(complex) if b.complex else x)
+    assert rel(got, want) < 1e-9, (bc, n, rel(got, want))
+    c = rng.standard_normal((3, n)) + (1j * rng.standard_normal((3, n)) if b.complex else 0)
+    got_s = op.synthesize(torch.from_numpy(c))
+    got_s = np_(got_s if b.complex else got_s[0])
+    assert rel(got_s, b.synthesize(c)) < 1e-11, (bc, n, rel(got_s, b.synthesize(c)))
+    back = op.synthesize(op.analyze(torch.from_numpy(x)))
+    back = np_(back).real if b.complex else np_(back[0])
+    # |T^-1| grows like n/2 on white noise (the border coefficients carry
+    # alpha (y_1 - y_0) n/4): the numpy restatement's own round trip is 5.5e-11
+    # at n = 2^17 and 3.4e-10 at 2^20, so the bar scales with n beyond 2^16
+    assert rel(back, x) < max(1e-10, 2e-15 * n)
+
+
+@pytest.mark.parametrize("bc,n", [(O.PERIODIC, 8192), (O.HOC_FOURIER, 16384)])
+def test_long_complex_input(bc, n, rng):
+    op = P.build_operator([1.0], n, bc)
+    b = O.SpectralBasis(bc, n)
+    x = rng.standard_normal((2, n)) + 1j * rng.standard_normal((2, n))
+    got = np_(op.analyze(torch.from_numpy(x)))
+    assert rel(got, b.analyze(x)) < 1e-9
+
+
+@pytest.mark.parametrize("bc", [W.HOC_FOURIER_D1, W.HOC_FOURIER_D3])
+def test_long_higher_order_borders(bc, rng):
+    """d = 1 / d = 3 at n = 16384 (interior 16383 / 16381: beyond the pair
+    kernels): transforms against HoTransform, restoration against the oracle."""
+    n = 16384
+    psf = onesided(15, 0.2)
+    op = P.build_operator(psf, n, bc)
+    t = O.build_ho_transform(bc, n)
+    x = np.cumsum(rng.standard_normal((3, n)), axis=1) / 50.0  # smooth-ish lines
+    got = np_(op.analyze(torch.from_numpy(x)))
+    want = O.ho_analyze(t, x)
+    cond = 1e3 if bc == W.HOC_FOURIER_D1 else 2e9  # cond(T) ~ n^2.5 at d = 3
+    assert rel(got, want) < 1e-15 * cond, rel(got, want)
+    c = want
+    got_s = np_(op.synthesize(torch.from_numpy(c)))
+    # the d = 3 border amplitudes of these lines reach 1e6 x the samples
+    assert rel(got_s, O.ho_synthesize(t, c)) < (1e-11 if bc == W.HOC_FOURIER_D1 else 1e-9)
+    # restoration (fixed mu and GCV) against the oracle
+    cfg = W.config(1)
+    _, g = W.signals_1d(cfg, 0, 3, n=n)
+    oop = O.build_operator(O.make_psf(cfg.psf, True), n, bc)
+    op = P.build_operator(cfg.psf, n, bc)
+    L = P.smoothing_eigenvalues("first-difference", op)
+    s = O.smoothing_eigenvalues(O.FIRST_DIFFERENCE, bc, n, oop.eigenvalues)
+    rep = P.deblur(op, L, torch.from_numpy(g).cuda(), P.MuChoice(True),
+                   search=P.GcvSearch(1e-8, 1.0, 64))
+    w = O.deblur(oop, s, g, True, mu_min=1e-8, mu_max=1.0, count=64)
+    assert np.array_equal(np_(rep.best_k), w.best_k)
+    assert np.max(np.abs(np_(rep.mu_used) / w.mu_used - 1)) < 1e-9
+    assert rel(np_(rep.restored), w.restored) < 1e-9
+
+
+def test_long_deblur_1d_against_reference(rng):
+    """GCV restoration of a 1D hoc-cosine signal of n = 2^17 (the reference's
+    own BC at an acceptance-c7 size), against the compiled reference."""
+    import reflib as R
+    if not R.available():
+        pytest.skip("oracle/_ref not built")
+    n = 1 << 17
+    cfg = W.config(0)
+    _, g = W.signals_1d(cfg, 0, 2, n=n)
+    op = P.build_operator(cfg.psf, n, "hoc-cosine")
+    L = P.smoothing_eigenvalues("identity", op)
+    rep = P.deblur(op, L, torch.from_numpy(g).cuda(), P.MuChoice(True),
+                   search=P.GcvSearch(1e-6, 1.0, 64))
+    out, mu, curve, _ = R.deblur_1d(cfg.psf, n, O.HOC_COSINE, 0, g, True, mu_min=1e-6,
+                                    mu_max=1.0, count=64, want_curve=True)
+    assert np.array_equal(np_(rep.best_k), np.argmin(curve, axis=1))
+    assert np.max(np.abs(np_(rep.mu_used) / mu - 1)) < 1e-9
+    assert rel(np_(rep.restored), out) < 1e-9
+
+
+def test_acceptance_c7_apply_inverse_time(rng):
+    """Acceptance criterion 7 (acceptance_main.cpp:575-614): T_C apply + inverse
+    at n = 2^20 in under a second (here: device time of synthesize + analyze)."""
+    n = 1 << 20
+    op = P.build_operator([1.0], n, "hoc-cosine")
+    v = torch.from_numpy(rng.standard_normal((1, n))).cuda()
+    for _ in range(2):
+        y = op.synthesize(v)[0]
+        x = op.analyze(y)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    y = op.synthesize(v)[0]
+    x = op.analyze(y)
+    b.record()
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b)
+    print(f"T_C apply + inverse at n = 2^20: {ms:.1f} ms")
+    assert ms < 1000.0
+    assert rel(np_(x), np_(v)) < 2e-15 * n
+
+
+def test_long_axis_2d(rng):
+    """A 2D image with one long axis (24 x 20001 hoc-cosine): the row pass runs
+    the long-line path, the column pass the on-chip kernels."""
+    n1, n2 = 24, 20001
+    psf = gauss(3, 1.2)
+    op = P.build_operator_2d_separable(psf, psf, n1, n2, "hoc-cosine")
+    p = O.make_psf(psf, True)
+    oop = O.build_operator_2d(O.separable_psf2d(p, p), n1, n2, O.HOC_COSINE, separable=True)
+    x = rng.standard_normal((n1, n2))
+    got = np_(op.analyze(torch.from_numpy(x)))
+    assert rel(got, oop.analyze(x)) < 1e-9
+    back = op.synthesize(op.analyze(torch.from_numpy(x)))
+    back = np_(back[0] if isinstance(back, tuple) else back)
+    assert rel(np.real(back), x) < 1e-10

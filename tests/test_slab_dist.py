@@ -69,7 +69,7 @@ class OracleSlabBackend:
         gh = self._np(ghat)
         d, s = self._slab(col0, gh.shape[0])
         ok = s != 0
-        t = 1.0 / ((np.abs(d) ** 2 / np.where(ok, s, 1) ** 2)[ok] + center)
+        t = center / ((np.abs(d) ** 2 / np.where(ok, s, 1) ** 2)[ok] + center)  # scaled series
         w = (np.abs(gh) ** 2)[ok]
         A = [np.sum(w * t ** (j + 2)) for j in range(J)]
         B = [np.sum(t ** (j + 1)) for j in range(J)]
