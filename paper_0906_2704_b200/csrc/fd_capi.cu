@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -29,6 +30,7 @@
 #include "fd_mixed.cuh"
 #include "fd_rader.cuh"
 #include "fd_gen.cuh"
+#include "fd_cdirect.cuh"
 
 
 using namespace fdb;
@@ -224,6 +226,8 @@ void init_runtime_once() {
       cudaFuncSetAttribute(k_msynth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
       cudaFuncSetAttribute(k_qanalyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
       cudaFuncSetAttribute(k_qsynth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+      cudaFuncSetAttribute(k_canalyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+      cudaFuncSetAttribute(k_csynth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
     }
     ok = true;
   });
@@ -459,6 +463,12 @@ void launch_analyze(const AxisDev& ax, const LineIO& io, cudaStream_t st) {
   // for the half-spectrum layout)
   if (!io.in_cplx && ax.rhalf && !io.in_f32 && !io.half) {
     ProfScope ps("k_analyze", st);
+    if (ax.cdir) {  // Rader over h - 1 in shared memory (fd_cdirect.cuh)
+      const size_t sm = cd_smem_bytes(ax.hfft.L, ax.m);
+      k_canalyze<<<std::min(io.gi.count, num_sms()), kCdNT, sm, st>>>(ax, io);
+      launched("k_canalyze");
+      return;
+    }
     if (ax.hfft.M > kMaxOnChipM) {  // split convolution, persistent CTAs + scratch
       const int grid = std::min(io.gi.count, 2 * num_sms());
       double2* scr = nullptr;
@@ -516,6 +526,12 @@ void launch_synth(const AxisDev& ax, const LineIO& io, const SynthArgs& sa, cuda
   if (!io.out_cplx && ax.rhalf && !io.out_f32 && !io.half &&
       (!ax.cplx || sa.resid2 == nullptr)) {
     ProfScope ps(sa.mode == 1 ? "k_synth_filter" : "k_synth", st);
+    if (ax.cdir && !io.pack) {
+      const size_t sm = cd_smem_bytes(ax.hfft.L, ax.m);
+      k_csynth<<<std::min(io.gi.count, num_sms()), kCdNT, sm, st>>>(ax, io, sa);
+      launched("k_csynth");
+      return;
+    }
     if (ax.hfft.M > kMaxOnChipM) {
       const int grid = std::min(io.gi.count, 2 * num_sms());
       double2* scr = nullptr;
@@ -772,6 +788,95 @@ void build_mixed_plan(Axis& A, int m) {
 
 // Higher-order borders (extension, oracle/fdoracle.py build_ho_transform):
 // Legendre border columns, wrap/bord rows, S = P_B - P[kl + wrap], S^-1.
+bool cdirect_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FASTDEBLUR_CDIRECT");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// Rader plan for the cosine real-line kernels (fd_cdirect.cuh): h = m/2 an odd
+// prime, N = h - 1 a product of 13, 11, 9, 7, 5, 3, 4, 2, everything in one
+// CTA's shared memory
+void build_cdirect(Axis& A) {
+  AxisDev& d = A.dev;
+  d.cdir = 0;
+  if (!cdirect_enabled() || d.kind != IK_COS || !d.rhalf) return;
+  const int h = d.hfft.L, N = h - 1;
+  if (h < 64 || h > 65535 || !(h & 1)) return;
+  if (cd_smem_bytes(h, d.m) > 226 * 1024) return;
+  for (int q = 3; (long long)q * q <= h; q += 2)
+    if (h % q == 0) return;
+  const std::vector<int> rr = mixed_radices(N, {13, 11, 9, 7, 5, 3, 4, 2});
+  if (rr.empty()) return;
+  std::vector<int> pf;
+  for (int f = 2, t = N; t > 1; ++f)
+    if (t % f == 0) {
+      pf.push_back(f);
+      while (t % f == 0) t /= f;
+    }
+  int g = 2;
+  for (;; ++g) {
+    bool ok = true;
+    for (int f : pf) ok = ok && powmod(g, N / f, h) != 1;
+    if (ok) break;
+  }
+  std::vector<int> perm;
+  upload_plan(A, N, rr, &perm);
+  std::vector<int> ilog(h, 0), opos(h, 0);
+  const long long ginv = powmod(g, h - 2, h);
+  long long gp = 1, gi = 1;
+  std::vector<long double> br(N), bi(N);
+  const long double two_pi = 2.0L * acosl(-1.0L);
+  for (int nn = 0; nn < N; ++nn) {
+    ilog[gp] = nn;  // a_n = z_{g^n}: sample g^n goes to slot n
+    opos[gi] = nn;  // frequency g^-n comes from slot n
+    const long double ang = -two_pi * (long double)gi / (long double)h;
+    br[nn] = cosl(ang);  // b_n = w_h^{g^-n}
+    bi[nn] = sinl(ang);
+    gp = gp * g % h;
+    gi = gi * ginv % h;
+  }
+  // DFT_N(b)/N in the DIF output order, O(N^2) in long double over a root table (setup only)
+  std::vector<long double> cr(N), ci(N);
+  for (int t = 0; t < N; ++t) {
+    const long double ang = -two_pi * (long double)t / (long double)N;
+    cr[t] = cosl(ang);
+    ci[t] = sinl(ang);
+  }
+  // (cached per h: the two axes of a square image share it)
+  static std::mutex cache_mu;
+  static std::map<int, std::vector<double2>> cache;
+  std::vector<double2> bh;
+  {
+    std::lock_guard<std::mutex> lk(cache_mu);
+    auto it = cache.find(h);
+    if (it != cache.end()) bh = it->second;
+  }
+  if (bh.empty()) {
+    bh.resize(N);
+    for (int k = 0; k < N; ++k) {
+      long double re = 0.0L, im = 0.0L;
+      int t = 0;
+      for (int nn = 0; nn < N; ++nn) {
+        re += br[nn] * cr[t] - bi[nn] * ci[t];
+        im += br[nn] * ci[t] + bi[nn] * cr[t];
+        t += k;
+        if (t >= N) t -= N;
+      }
+      bh[perm[k]] = make_double2((double)(re / N), (double)(im / N));
+    }
+    std::lock_guard<std::mutex> lk(cache_mu);
+    if (cache.size() > 8) cache.clear();
+    cache[h] = bh;
+  }
+  d.cd_ilog = dev_upload(A.bufs, ilog);
+  d.cd_opos = dev_upload(A.bufs, opos);
+  d.cd_bhat = dev_upload(A.bufs, bh);
+  d.cdir = 1;
+}
+
 void build_ho_axis(Axis& A, int bc, int n) {
   AxisDev& d = A.dev;
   const int kl = ho_kl(bc), kr = ho_kr(bc), k = kl + kr, deg = k;
@@ -884,11 +989,10 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
       int lh = 0;
       if (ceil_pow2(std::max((long long)L - 1, 2LL), &lh) > 2 * kMaxOnChipM) d.rhalf = 0;
     }
-    // full-length tables: on chip always (complex lines, line pairs); through
-    // the global buffer when no faster path carries the axis's lines (real
-    // lines beyond the half-length path, complex bases, higher-order borders)
-    if (M <= kMaxOnChipM || !d.rhalf || d.cplx || is_ho_bc(bc))
-      d.fft = make_fft_tables(L, A->bufs, d.kind == IK_COS ? m : 0, dct_tw);
+    // full-length tables (complex lines, line pairs, fp32-storage and
+    // half-spectrum lines): on chip up to M = 8192, through the global
+    // buffer beyond (launch_long)
+    d.fft = make_fft_tables(L, A->bufs, d.kind == IK_COS ? m : 0, dct_tw);
   }
   if (d.rhalf) {
     d.hfft = make_fft_tables(L / 2, A->bufs, d.fft.M ? 0 : (d.kind == IK_COS ? m : 0), dct_tw,
@@ -897,6 +1001,8 @@ std::unique_ptr<Axis> build_axis(int bc, int n) {
     k_init_rtw<<<std::max(1, std::min(1024, (L / 2 + 255) / 256)), 256>>>(L, rtw);
     launched("k_init_rtw");
     d.rtw = rtw;
+    ck(cudaDeviceSynchronize(), "axis tables");
+    build_cdirect(*A);
   }
   if (is_ho_bc(bc)) {
     build_ho_axis(*A, bc, n);

@@ -108,6 +108,13 @@ struct AxisDev {
   const int* rgidx;
   const int* ropos;
   const double2* rbhat;
+  // cosine lines whose half length h is a prime with smooth h - 1 (fd_cdirect.cuh):
+  // Rader over N = h - 1 with the plan in mrad / mtw; sample j -> slot
+  // cd_ilog[j], frequency k -> slot cd_opos[k] (h entries each), DFT(b)/N
+  int cdir;
+  const int* cd_ilog;
+  const int* cd_opos;
+  const double2* cd_bhat;
   double sinv[kHoMax * kHoMax];
   int bord[kHoMax], wrap[kHoMax];
 };

@@ -109,6 +109,25 @@ __device__ __forceinline__ void rad_stage_any(int r, double2* x, int N, int S, c
 
 // cyclic convolution of x (length N = m - 1, natural order) with b:
 // DIF forward, pointwise DFT(b)/N, DIT inverse -> natural order
+// (length N, DFT(b)/N table `bhat` in the DIF output order; plan in ax.mrad)
+__device__ __forceinline__ void rader_conv_n(double2* x, int N, const AxisDev& ax,
+                                             const double2* __restrict__ bhat, const MixTw& tw,
+                                             int nt) {
+  int S = N;
+  for (int s = 0; s < ax.mstages; ++s) {
+    rad_stage_any<false>(ax.mrad[s], x, N, S, tw, nt);
+    S /= ax.mrad[s];
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < N; i += nt) x[i] = cmul(x[i], __ldg(&bhat[i]));
+  __syncthreads();
+  for (int s = ax.mstages - 1; s >= 0; --s) {
+    S *= ax.mrad[s];
+    rad_stage_any<true>(ax.mrad[s], x, N, S, tw, nt);
+    __syncthreads();
+  }
+}
+
 __device__ __forceinline__ void rader_conv(double2* x, const AxisDev& ax, const MixTw& tw, int nt) {
   const int N = ax.m - 1;
   int S = N;
