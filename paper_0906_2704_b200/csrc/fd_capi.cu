@@ -1694,6 +1694,14 @@ GcvData gcv_data(const fd_op* op, const fd_smoother* L, const void* ghat, long l
   return g;
 }
 
+bool wbuild_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("FASTDEBLUR_GCV_WBUILD");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 GcvData gcv_data(const fd_op* op, const fd_smoother* L, const Analyzed& a, long long count,
                  Scratch* S = nullptr) {
   GcvData g = gcv_data(op, L, a.ghat, count);
@@ -1717,6 +1725,17 @@ GcvData gcv_data(const fd_op* op, const fd_smoother* L, const Analyzed& a, long 
   if (a.w) {
     g.wred = a.w;
     g.wstride = a.wstride;
+  } else if (op->dim == 2 && S && count >= 32 && g.r1d && wbuild_enabled()) {
+    // batched 2D GCV: compact weights, so the grid is the
+    // W . S2 product and the refinement passes stream 8 B per element
+    const long long ws = (g.N + 31) / 32 * 32;
+    double* W = S->get<double>((size_t)count * ws);
+    ProfScope ps("k_gcv_tables", S->st);
+    k_gcv_wbuild<<<(int)std::min<long long>(16 * num_sms(), (count * ws + 255) / 256), 256, 0,
+                   S->st>>>(g, ws, W);
+    launched("k_gcv_wbuild");
+    g.wred = W;
+    g.wstride = ws;
   }
   return g;
 }

@@ -2120,6 +2120,20 @@ __global__ void __launch_bounds__(256) k_gcv_bounds(const double* __restrict__ h
 // ---- tensor-core screening of the grid (fd_tc.cuh) and exact candidates ----
 // rmin = min over elements of the finite ratios r_e (one CTA)
 // r table of a batch sharing one 2D operator (gcv_ratio for every element)
+// compact GCV weights of a batch sharing one 2D operator: W[item][e] =
+// mult_e |ghat_e|^2 (the half-spectrum pair rows counted twice), rows padded
+// with zeros to wstride -- the batched grid then runs as the W . S2 product
+// (k_gcv_gemm2) and every later pass streams 8 B per element instead of the
+// 16 B complex coefficient plus the index arithmetic of the 2D ratio
+__global__ void __launch_bounds__(256) k_gcv_wbuild(GcvData g, long long wstride, double* W) {
+  const long long tot = (long long)g.items * wstride;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long item = t / wstride, e = t - item * wstride;
+    W[t] = e < g.N ? gcv_w(g, (int)item, e) : 0.0;
+  }
+}
+
 __global__ void k_gcv_rtab(GcvData g, double* r) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < g.N;
        e += (long long)gridDim.x * blockDim.x)
