@@ -181,6 +181,18 @@ int fd_deblur_host_f32(const fd_op* op, const fd_smoother* L, const float* g, in
                        float* restored, double* mu_used, int* best_k, long long count,
                        long long chunk, void* stream);
 
+/* deblur of one DEVICE batch under several smoothing norms of the same operator
+ * (e.g. identity and Laplacian, BASELINE config 3): the batch is analyzed once
+ * (the coefficients do not depend on the norm); each norm runs its own GCV
+ * selection and filtered synthesis -- the results are those of nL separate
+ * fd_deblur calls (deblur(_2d), pipeline.cpp:120-165).  restored[l]: device,
+ * count*N of double (float when g_f32); mu_used[l*count + i], best_k[l*count + i]
+ * (or NULL). */
+int fd_deblur_smoothers(const fd_op* op, int nL, const fd_smoother* const* Ls, const void* g,
+                        int g_f32, int use_gcv, double fixed_mu, double mu_min, double mu_max,
+                        int grid_count, void* const* restored, double* mu_used, int* best_k,
+                        long long count, void* stream);
+
 /* deblur of ONE host batch under several operators of the same shape (e.g.
  * BC degrees d = 1 and d = 3, or two smoothers): as fd_deblur_host, but each
  * chunk is uploaded once and restored by every (ops[o], Ls[o]); restored[o]

@@ -7,4 +7,5 @@ from .fastdeblur import (  # noqa: F401
     MuChoice, RestorationReport, Smoother, ValidationError, bc_for_degree, blur_apply, deblur_host,
     build_operator, build_operator_2d, deblur_host_multi, build_operator_2d_separable, deblur, gcv_select,
     gcv_value, kernel_launches, lib, smoother_from_eigenvalues, smoothing_eigenvalues,
-    tikhonov_solve, sweep_mu, BcSweep, SweepPoint, convolve_valid, convolve_valid_2d, add_noise)
+    tikhonov_solve, sweep_mu, BcSweep, SweepPoint, convolve_valid, convolve_valid_2d, add_noise,
+    deblur_smoothers)

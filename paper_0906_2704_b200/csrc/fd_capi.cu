@@ -1834,6 +1834,22 @@ void launch_gemm(const GcvData& g, const GcvGrid& grid, long long echunk, int nc
 
 size_t gemm2_smem(int nj) { return (size_t)2 * (64 * 32 + 32 * 32 * nj) * 8 + 16; }
 
+// den_k = sum_e mult_e / (r_e + mu_k): item-independent, one table per grid
+void launch_den(const GcvData& g, const GcvGrid& grid, double* den, Scratch& S) {
+  const int K = grid.count;
+  const int nsplit = (int)std::max<long long>(1, std::min<long long>(32, g.N / 32768));
+  if (nsplit == 1) {
+    k_gcv_den<<<K, 256, 0, S.st>>>(g, grid, den);
+    launched("k_gcv_den");
+    return;
+  }
+  double* part = S.get<double>((size_t)K * nsplit);
+  k_gcv_den<<<dim3(K, nsplit), 256, 0, S.st>>>(g, grid, part);
+  launched("k_gcv_den");
+  k_reduce_partials<<<dim3(K, 1), 256, 0, S.st>>>(part, nsplit, 1, den);
+  launched("k_reduce_partials");
+}
+
 template <int NJ>
 void launch_gemm2_t(const GcvData& g, const GcvGrid& grid, int nch, long long echunk,
                     double* partial, Scratch& S) {
@@ -1857,8 +1873,7 @@ void launch_gemm2_t(const GcvData& g, const GcvGrid& grid, int nch, long long ec
   }
   {
     ProfScope ps("k_gcv_den", S.st);
-    k_gcv_den<<<K, 256, 0, S.st>>>(g, grid, den);
-    launched("k_gcv_den");
+    launch_den(g, grid, den, S);
   }
   const dim3 blocks((g.items + 63) / 64, nch);
   for (int kb = 0; kb < K; kb += BK) {
@@ -1978,8 +1993,7 @@ void gcv_screen_exact(const GcvData& g, const GcvGrid& grid, const Analyzed& an,
     ProfScope ps("k_gcv_tables", S.st);
     k_gcv_rmin<<<1, 256, 0, S.st>>>(g, rmin);
     launched("k_gcv_rmin");
-    k_gcv_den<<<K, 256, 0, S.st>>>(g, grid, den);
-    launched("k_gcv_den");
+    launch_den(g, grid, den, S);
     k_gcv_s32<<<(int)std::min<long long>(4096, (BN * Ep + 255) / 256), 256, 0, S.st>>>(
         g, grid, BN, Ep, rmin, Sh, Sl);
     launched("k_gcv_s32");
@@ -2885,6 +2899,49 @@ int deblur_impl(const fd_op* op, const fd_smoother* L, const void* g, int use_gc
   });
 }
 }  // namespace
+
+// One observation batch restored under several smoothing norms of the same
+// operator (BASELINE config 3: identity and Laplacian): the spectral
+// coefficients do not depend on the norm, so the batch is analyzed once and
+// each norm runs its own GCV selection and filtered synthesis
+// (deblur(_2d), pipeline.cpp:120-165, called once per norm by the reference).
+int fd_deblur_smoothers(const fd_op* op, int nL, const fd_smoother* const* Ls, const void* g,
+                        int g_f32, int use_gcv, double fixed_mu, double mu_min, double mu_max,
+                        int grid_count, void* const* restored, double* mu_used, int* best_k,
+                        long long count, void* stream) {
+  return guarded([&] {
+    if (nL < 1 || !Ls || !restored) validation("at least one smoother and output are required");
+    for (int l = 0; l < nL; ++l) {
+      check_deblur_args(op, Ls[l], use_gcv, fixed_mu, mu_min, mu_max, grid_count, mu_used, nullptr,
+                        count);
+      if ((Ls[l]->pair != nullptr) != (Ls[0]->pair != nullptr))
+        validation("smoothers of one call must share the operator's coefficient layout");
+      if (count > 0 && !restored[l]) validation("null output");
+    }
+    if (count <= 0) return;
+    Scratch S(as_stream(stream));
+    int* status = S.get<int>(1);
+    ck(cudaMemsetAsync(status, 0, sizeof(int), S.st), "memset");
+    std::unique_ptr<DevGrid> dg;
+    if (use_gcv) dg = std::make_unique<DevGrid>(mu_min, mu_max, grid_count, S);
+    const bool w32 = use_gcv && count >= 32 && dg && dg->d.count <= 256 && screen_enabled();
+    const Analyzed an = analyze_for_gcv(op, Ls[0], g, count, S, false, w32, g_f32);
+    for (int l = 0; l < nL; ++l) {
+      double* mu_l = mu_used + (long long)l * count;
+      if (use_gcv) {
+        gcv_select_dev(op, Ls[l], an, count, *dg, mu_min, mu_max, mu_l,
+                       best_k ? best_k + (long long)l * count : nullptr, nullptr, status, S);
+      } else {
+        k_fill<<<(int)std::min<long long>(1024, (count + 255) / 256), 256, 0, S.st>>>(mu_l, count,
+                                                                                    fixed_mu);
+        launched("k_fill");
+      }
+      run_synth(op, Ls[l], an.ghat, restored[l], 0, 1, mu_l, nullptr, count, S, an.pack, false,
+                g_f32, an.half);
+    }
+    if (use_gcv) check_status(status, S.st);
+  });
+}
 
 int fd_deblur(const fd_op* op, const fd_smoother* L, const double* g, int use_gcv,
               double fixed_mu, double mu_min, double mu_max, int grid_count, double* restored,

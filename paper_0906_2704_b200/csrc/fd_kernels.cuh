@@ -461,10 +461,16 @@ __device__ __forceinline__ void st_out(const LineIO& io, long long idx, double2 
 }
 
 // LOGM > 0: size-specialised Bluestein core (bluestein_t; blockDim = line_threads(M))
+// resident threads per SM the generic line kernels are compiled for (register cap 65536 / kLineOcc);
+// 768 (80 registers, 1.5 KB of spills) measured 15 % slower on config 3 (r02)
+#ifndef FD_LINE_OCC
+#define FD_LINE_OCC 512
+#endif
+constexpr int kLineOcc = FD_LINE_OCC;
 template <int LOGM>
 constexpr int kLineNT = (1 << LOGM) / 16 < 64 ? 64 : ((1 << LOGM) / 16 > 512 ? 512 : (1 << LOGM) / 16);
 template <int LOGM>
-__global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512 / kLineNT<LOGM> : 1) k_analyze(AxisDev ax, LineIO io) {
+__global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? kLineOcc / kLineNT<LOGM> : 1) k_analyze(AxisDev ax, LineIO io) {
   extern __shared__ double2 sm[];
   const int M = ax.fft.M;
   const bool xg = LOGM == 0 && io.xscr != nullptr;
@@ -765,7 +771,7 @@ __device__ __forceinline__ double2 coeff_at(const AxisDev& ax, const LineIO& io,
 }
 
 template <int LOGM>
-__global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? 512 / kLineNT<LOGM> : 1) k_synth(AxisDev ax, LineIO io,
+__global__ void __launch_bounds__(LOGM > 0 ? kLineNT<LOGM> : 512, LOGM > 0 ? kLineOcc / kLineNT<LOGM> : 1) k_synth(AxisDev ax, LineIO io,
                                                                         SynthArgs sa) {
   extern __shared__ double2 sm[];
   const int M = ax.fft.M;
@@ -1999,17 +2005,21 @@ __global__ void k_gcv_s2(GcvData g, GcvGrid grid, long long Np, int Kp, double* 
   }
 }
 
-__global__ void __launch_bounds__(256) k_gcv_den(GcvData g, GcvGrid grid, double* den) {
+// grid (K, nsplit): CTA (k, y) sums the elements of split y; nsplit == 1 writes
+// den[k], otherwise out[k * nsplit + y] (reduced in split order afterwards)
+__global__ void __launch_bounds__(256) k_gcv_den(GcvData g, GcvGrid grid, double* out) {
   __shared__ double red[32];
   const int kk = blockIdx.x;
   const double mu = grid.mus[kk];
+  const long long chunk = (g.N + gridDim.y - 1) / gridDim.y;
+  const long long e0 = (long long)blockIdx.y * chunk, e1 = min(g.N, e0 + chunk);
   double acc[1] = {0.0};
-  for (long long e = threadIdx.x; e < g.N; e += blockDim.x) {
+  for (long long e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
     const double r = gcv_ratio(g, e);
     if (!isinf(r)) acc[0] = fma(gcv_mult(g, e), 1.0 / (r + mu), acc[0]);
   }
   block_sum<1>(acc, red);
-  if (threadIdx.x == 0) den[kk] = acc[0];
+  if (threadIdx.x == 0) out[(long long)kk * gridDim.y + blockIdx.y] = acc[0];
 }
 
 // ---- interval screen of the grid for single large items ----

@@ -93,6 +93,7 @@ def lib():
         L.fd_matvec_f32.argtypes = L.fd_matvec.argtypes
         L.fd_bc_for_degree.argtypes = [ip, ip, C.POINTER(C.c_int)]
         L.fd_parse_bc.argtypes = [C.c_char_p]
+        L.fd_deblur_smoothers.argtypes = [vp, ip, vp, vp, ip, ip, cd, cd, cd, ip, vp, vp, vp, ll, vp]
         L.fd_convolve_valid.argtypes = [vp, ll, ip, dp, ip, vp, vp]
         L.fd_convolve_valid_2d.argtypes = [vp, ll, ip, ip, dp, ip, ip, vp, vp]
         L.fd_add_noise.argtypes = [vp, ll, ll, cd, C.POINTER(C.c_ulonglong), vp]
@@ -401,6 +402,30 @@ def deblur(op: BlurOperator, L: Smoother, g, mu: MuChoice, want_curve=False,
                           _ptr(restored), _ptr(mu_used), _ptr(bk) if mu.use_gcv else None,
                           _ptr(curve), _ptr(res), count, _stream()))
     return RestorationReport(restored, mu_used, bk if mu.use_gcv else None, curve, res)
+
+
+def deblur_smoothers(op: BlurOperator, Ls, g, mu: MuChoice, search: GcvSearch = GcvSearch(),
+                     outs=None):
+    """deblur(_2d) of one batch under several smoothing norms of the same
+    operator (fd_deblur_smoothers: one analysis, a GCV selection and a filtered
+    synthesis per norm).  Returns one RestorationReport per norm, equal to
+    separate ``deblur`` calls."""
+    f32 = isinstance(g, torch.Tensor) and g.dtype == torch.float32
+    g = _dev(g, torch.float32 if f32 else torch.float64)
+    count, lead = op._count(g)
+    nL = len(Ls)
+    outs = [torch.empty_like(g) for _ in range(nL)] if outs is None else list(outs)
+    mu_used = torch.empty((nL,) + tuple(lead), dtype=torch.float64, device="cuda")
+    bk = torch.full((nL,) + tuple(lead), -1, dtype=torch.int32, device="cuda")
+    hs = (C.c_void_p * nL)(*[L._h for L in Ls])
+    ps = (C.c_void_p * nL)(*[o.data_ptr() for o in outs])
+    check(lib().fd_deblur_smoothers(op._h, nL, hs, _ptr(g), int(f32), int(bool(mu.use_gcv)),
+                                    float(mu.fixed_mu), float(search.mu_min),
+                                    float(search.mu_max), int(search.count), ps, _ptr(mu_used),
+                                    _ptr(bk) if mu.use_gcv else None, count, _stream()))
+    zero = torch.zeros(lead, dtype=torch.float64, device="cuda")
+    return [RestorationReport(outs[l], mu_used[l], bk[l] if mu.use_gcv else None, None, zero)
+            for l in range(nL)]
 
 
 @dataclass

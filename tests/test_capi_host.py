@@ -140,3 +140,16 @@ def test_no_cpu_fallback():
     with pytest.raises(P.FastDeblurError) as e:
         P.build_operator([0.25, 0.5, 0.25], 64, "hoc-cosine")
     assert "no CUDA device" in str(e.value)
+
+
+def test_cli_front_end_parses_without_a_gpu():
+    """tools/fastdeblur_b200 (reference tools/fastdeblur.cpp:349-453): --help exits 0,
+    parse errors exit 2 before any device work."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools",
+                       "fastdeblur_b200")
+    if not os.path.exists(exe):
+        pytest.skip("tools/fastdeblur_b200 not built")
+    assert subprocess.run([exe, "--help"], capture_output=True).returncode == 0
+    assert subprocess.run([exe], capture_output=True).returncode == 2
+    assert subprocess.run([exe, "deblur", "--bogus", "1"], capture_output=True).returncode == 2

@@ -122,3 +122,32 @@ def test_interval_screen_single_image(bc, smoother, search, monkeypatch):
     assert int(rep.best_k.cpu()) == int(ref.best_k.cpu())
     assert abs(float(rep.mu_used.cpu()) / float(ref.mu_used.cpu()) - 1) < 1e-12
     assert rel(rep.restored.cpu().numpy(), ref.restored.cpu().numpy()) < 1e-12
+
+
+def test_deblur_smoothers_equals_separate_calls(rng):
+    """fd_deblur_smoothers (one analysis, several smoothing norms) returns exactly
+    what separate deblur calls return: 2D d = 3 batch (config-3 shape, fp64 and
+    fp32 storage), a 1D hoc-fourier batch and a fixed mu."""
+    from paper_0906_2704_b200 import workloads as W
+    cfg = W.config(3)
+    n, B = 96, 40
+    g = np.stack([W.image_2d(cfg, i, n, n)[1] for i in range(B)])
+    op = P.build_operator_2d_separable(cfg.psf, cfg.psf, n, n, W.HOC_FOURIER_D3)
+    Ls = [P.smoothing_eigenvalues(k, op) for k in ("identity", "laplacian")]
+    search = P.GcvSearch(1e-6, 1.0, 64)
+    for dt in (torch.float64, torch.float32):
+        gd = torch.from_numpy(g).to("cuda", dt)
+        got = P.deblur_smoothers(op, Ls, gd, P.MuChoice(True), search=search)
+        for L, r in zip(Ls, got):
+            w = P.deblur(op, L, gd, P.MuChoice(True), search=search)
+            assert torch.equal(r.best_k, w.best_k)
+            assert torch.equal(r.mu_used, w.mu_used)
+            assert torch.equal(r.restored, w.restored)
+    op1 = P.build_operator(onesided(9, 0.3), 512, "hoc-fourier")
+    L1 = [P.smoothing_eigenvalues(k, op1) for k in ("laplacian", "identity")]
+    g1 = torch.from_numpy(rng.standard_normal((50, 512)) + 3.0).cuda()
+    for mu in (P.MuChoice(True), P.MuChoice(False, 1e-3)):
+        got = P.deblur_smoothers(op1, L1, g1, mu, search=search)
+        for L, r in zip(L1, got):
+            w = P.deblur(op1, L, g1, mu, search=search)
+            assert torch.equal(r.mu_used, w.mu_used) and torch.equal(r.restored, w.restored)
