@@ -1708,10 +1708,25 @@ struct GcvData {
   int hm_lo, hm_hi;
 };
 
+// (row, column) of 2D element e; 32-bit division whenever the item has fewer
+// than 2^31 elements (the 64-bit one is ~5x the instructions, and every GCV
+// pass over a single large image pays it per element)
+__device__ __forceinline__ void gcv_row_col(const GcvData& g, long long e, int& i, int& j) {
+  if (g.N <= 0x7fffffffLL) {
+    const unsigned ee = (unsigned)e, n2 = (unsigned)g.sp.n2;
+    const unsigned q = ee / n2;
+    i = (int)q;
+    j = (int)(ee - q * n2);
+  } else {
+    i = (int)(e / g.sp.n2);
+    j = (int)(e % g.sp.n2);
+  }
+}
+
 __device__ __forceinline__ double gcv_ratio(const GcvData& g, long long e) {
   if (g.r1d) return __ldg(&g.r1d[e]);
-  int i = (int)(e / g.sp.n2);
-  const int j = (int)(e % g.sp.n2);
+  int i, j;
+  gcv_row_col(g, e, i, j);
   if (i >= g.sp.hr_split) i += g.sp.hr_off;
   double2 d;
   double s;
@@ -1742,7 +1757,8 @@ __device__ __forceinline__ double gcv_w1(const GcvData& g, long long idx) {
 // multiplicity of element e in sum_e sigma_e (2 for a Hermitian pair)
 __device__ __forceinline__ double gcv_mult(const GcvData& g, long long e) {
   if (g.hm_hi > g.hm_lo) {
-    const int r = (int)(e / g.sp.n2);
+    int r, c;
+    gcv_row_col(g, e, r, c);
     return (r >= g.hm_lo && r < g.hm_hi) ? 2.0 : 1.0;
   }
   return (g.pair && __ldg(&g.pair[e]).y >= 0) ? 2.0 : 1.0;
@@ -2078,13 +2094,43 @@ __global__ void __launch_bounds__(512) k_gcv_hist(GcvData g, long long base, int
   const int nw = 2 * (nb + 1);
   for (int i = threadIdx.x; i < nw; i += blockDim.x) hist[i] = 0.0;
   __syncthreads();
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < g.N;
-       e += (long long)gridDim.x * blockDim.x) {
-    const double r = gcv_ratio(g, e);
-    if (isinf(r)) continue;
-    const int b = r > 0.0 ? (int)(hist_key(r) - base) : nb;
-    atomicAdd(&hist[2 * b], gcv_w(g, 0, e));
-    atomicAdd(&hist[2 * b + 1], gcv_mult(g, e));
+  // Neighbouring elements have nearly equal r at low frequencies: when a whole
+  // warp adds into one bin its 64 shared-memory atomics serialise, so that case
+  // is reduced by shuffles into one pair of atomics.  (Walking the distinct bins
+  // of every warp instead measured 3.7x slower: at high frequencies the 32
+  // lanes hit ~32 bins.)
+  const unsigned full = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long e0 = blockIdx.x * (long long)blockDim.x + (threadIdx.x & ~31); e0 < g.N;
+       e0 += stride) {
+    const long long e = e0 + lane;
+    double w = 0.0, mlt = 0.0;
+    int b = -1;  // -1: nothing to add (past the end, or s_e = 0)
+    if (e < g.N) {
+      const double r = gcv_ratio(g, e);
+      if (!isinf(r)) {
+        b = r > 0.0 ? (int)(hist_key(r) - base) : nb;
+        w = gcv_w(g, 0, e);
+        mlt = gcv_mult(g, e);
+      }
+    }
+    const int b0 = __shfl_sync(full, b, 0);
+    if (__all_sync(full, b == b0)) {
+      if (b0 < 0) continue;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        w += __shfl_xor_sync(full, w, o);
+        mlt += __shfl_xor_sync(full, mlt, o);
+      }
+      if (lane == 0) {
+        atomicAdd(&hist[2 * b0], w);
+        atomicAdd(&hist[2 * b0 + 1], mlt);
+      }
+    } else if (b >= 0) {
+      atomicAdd(&hist[2 * b], w);
+      atomicAdd(&hist[2 * b + 1], mlt);
+    }
   }
   __syncthreads();
   double* out = partial + (long long)blockIdx.x * nw;

@@ -150,7 +150,12 @@ __device__ __forceinline__ void mix_dft(double2* x, const AxisDev& ax, const Mix
   }
 }
 
-constexpr int kMixNT = 256;
+// threads per CTA (two CTAs per SM).  320 threads (98 / 71 / 91 / 85 % full stage rounds at m = 4095
+// instead of 61 / 89 / 76 / 80 %) at 96 registers measured no faster (k_msynth 2.27 -> 2.36 ms, r02)
+#ifndef FD_MIX_NT
+#define FD_MIX_NT 256
+#endif
+constexpr int kMixNT = FD_MIX_NT;
 
 // L2 prefetch of the line pair q (contiguous lines only), issued one pair
 // ahead so the load phase of the persistent loop hits L2 instead of HBM
