@@ -27,6 +27,7 @@
 #include "fd_internal.h"
 #include "fd_kernels.cuh"
 #include "fd_pair.cuh"
+#include "fd_pair_edge.cuh"
 #include "fd_mixed.cuh"
 #include "fd_rader.cuh"
 #include "fd_gen.cuh"
@@ -162,6 +163,10 @@ template <int LOGM>
 void set_pair_attrs(int kmax) {
   cudaFuncSetAttribute(k_panalyze<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
   cudaFuncSetAttribute(k_psynth<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+  if constexpr (LOGM == 13) {
+    cudaFuncSetAttribute(k_panalyze_e<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+    cudaFuncSetAttribute(k_psynth_e<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+  }
 }
 
 // One-time setup per DEVICE (a process may drive several GPUs: the constant
@@ -420,6 +425,22 @@ void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaS
   } else {                                                                                 \
     k_panalyze<L><<<persistent_grid(k_panalyze<L>, PairShape<L>::NT, smem, pairs),         \
                     PairShape<L>::NT, smem, st>>>(ax, io);                                 \
+  }
+  // M = 8192: outermost radix-16 passes in registers (fd_pair_edge.cuh);
+  // FASTDEBLUR_PAIR_EDGE=0 selects the all-shared-memory kernels (A/B timing)
+  static const bool edge = [] {
+    const char* e = std::getenv("FASTDEBLUR_PAIR_EDGE");
+    return !(e && e[0] == '0');
+  }();
+  if (ax.fft.logM == 13 && edge) {
+    constexpr int NT = EdgeShape<13>::NT;
+    if (sa) {
+      k_psynth_e<13><<<persistent_grid(k_psynth_e<13>, NT, smem, pairs), NT, smem, st>>>(ax, io, *sa);
+    } else {
+      k_panalyze_e<13><<<persistent_grid(k_panalyze_e<13>, NT, smem, pairs), NT, smem, st>>>(ax, io);
+    }
+    launched(sa ? "k_psynth" : "k_panalyze");
+    return;
   }
   switch (ax.fft.logM) {
     case 8: FD_PA(8); break;
@@ -2403,6 +2424,16 @@ int fd_phase_clocks(unsigned long long* out, int reset) {
     if (reset) {
       unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
       ck(cudaMemcpyToSymbol(fdb::g_phase_clocks, z, sizeof(z)), "clk");
+    }
+  });
+}
+// pair kernels (fd_pair.cuh / fd_pair_edge.cuh): [kernel 0..3][phase 0..11]
+int fd_pair_clocks(unsigned long long* out, int reset) {
+  return guarded([&] {
+    ck(cudaMemcpyFromSymbol(out, fdb::g_pair_clocks, sizeof(unsigned long long) * 48), "clk");
+    if (reset) {
+      unsigned long long z[48] = {};
+      ck(cudaMemcpyToSymbol(fdb::g_pair_clocks, z, sizeof(z)), "clk");
     }
   });
 }

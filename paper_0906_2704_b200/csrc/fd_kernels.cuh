@@ -1220,10 +1220,11 @@ __device__ __forceinline__ Stage stage_init(double2* x, int h, int Mloc, double2
 // staging wait at the line start, per kernel.
 #ifdef FD_PHASE_CLOCKS
 __device__ unsigned long long g_phase_clocks[2][4];
-#define FD_CLK(v) long long v = clock64()
-#define FD_CLK_SET(v) v = clock64()
+#define FD_CLK(v) long long clk_##v = clock64()
+#define FD_CLK_SET(v) clk_##v = clock64()
 #define FD_CLK_ADD(k, i, a, b) \
-  if (threadIdx.x == 0) atomicAdd(&g_phase_clocks[k][i], (unsigned long long)((b) - (a)))
+  if (threadIdx.x == 0) \
+  atomicAdd(&g_phase_clocks[k][i], (unsigned long long)((clk_##b) - (clk_##a)))
 #else
 #define FD_CLK(v)
 #define FD_CLK_SET(v)

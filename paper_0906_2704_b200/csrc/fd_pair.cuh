@@ -59,9 +59,60 @@ struct FoldTw {
 // the Bluestein convolution of the pair kernels; with FOLD the buffer must
 // hold both halves of the first DIF stage already, and on return the lower
 // half [0, m) holds the result
-template <int LOGM, int NT>
-__device__ __forceinline__ void pair_conv(double2* x, const FftTables& T, const TwSm& tw, int m) {
+// Optional phase timing of the pair kernels (-DFD_PHASE_CLOCKS): thread 0 of
+// every CTA adds the SM clocks between phase marks, g_pair_clocks[kernel][phase]
+// (kernel: 0 k_panalyze, 1 k_psynth, 2 k_panalyze_e, 3 k_psynth_e)
+#ifdef FD_PHASE_CLOCKS
+__device__ unsigned long long g_pair_clocks[4][12];
+#define FD_PCLK_INIT() long long pclk_ = clock64()
+#define FD_PCLK(k, i)                                                                 \
+  do {                                                                                \
+    const long long now_ = clock64();                                                 \
+    if (threadIdx.x == 0) atomicAdd(&g_pair_clocks[k][i], (unsigned long long)(now_ - pclk_)); \
+    pclk_ = now_;                                                                     \
+  } while (0)
+#else
+#define FD_PCLK_INIT()
+#define FD_PCLK(k, i)
+#endif
+
+// bluestein_rec<LOGM, P, S, NT> with phase marks after every pass (marks base + 0 ..)
+template <int LOGM, int P, int S, int NT, int KERN, int BASE>
+__device__ __forceinline__ void bluestein_rec_clk(double2* x, const double2* bhat, const TwSm& tw,
+                                                  int nvalid, long long& pclk_) {
+#ifdef FD_PHASE_CLOCKS
+  using F = FftShape<LOGM, NT>;
+  if constexpr (P == F::NP - 1) {
+    mid_pass_t<LOGM, false, NT>(x, bhat, nvalid);
+    __syncthreads();
+    FD_PCLK(KERN, BASE);
+  } else {
+    dif_pass_t<LOGM, 4, S, false, NT, false>(x, tw, nvalid);
+    __syncthreads();
+    FD_PCLK(KERN, BASE);
+    bluestein_rec_clk<LOGM, P + 1, (S >> 4), NT, KERN, BASE + 1>(x, bhat, tw, nvalid, pclk_);
+    dit_pass_t<LOGM, 4, S, NT, false>(x, tw);
+    __syncthreads();
+    FD_PCLK(KERN, BASE + 2 * (F::NP - 1 - P));
+  }
+#endif
+}
+
+template <int LOGM, int NT, int KERN = 0>
+__device__ __forceinline__ void pair_conv(double2* x, const FftTables& T, const TwSm& tw, int m,
+                                          long long& pclk_) {
   using S = PairShape<LOGM>;
+#ifdef FD_PHASE_CLOCKS
+  if constexpr (LOGM == 13) {
+    bluestein_rec_clk<LOGM, 1, S::HM, NT, KERN, 2>(x, T.bhat, tw, S::M, pclk_);
+    const FoldTw<LOGM> ft(tw, threadIdx.x);
+    for (int k = threadIdx.x; k < m; k += NT)
+      x[pidx(k)] = cadd(x[pidx(k)], cmulc(x[pidx(k + S::HM)], ft(k)));
+    __syncthreads();
+    FD_PCLK(KERN, 7);
+    return;
+  }
+#endif
   if constexpr (S::FOLD) {
     static_assert(NT % (1 << FoldTw<LOGM>::LOB) == 0, "FoldTw needs NT % lo length == 0");
     bluestein_rec<LOGM, 1, S::HM, NT>(x, T.bhat, tw, S::M);
@@ -199,6 +250,11 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
   const long long es = io.gi.elem_stride;
   const double isq = ax.inv_sqrt_m;
   const long long nkb32 = io.wstride >> 5;
+#ifdef FD_PHASE_CLOCKS
+  long long pclk_ = clock64();
+#else
+  long long pclk_ = 0;
+#endif
   for (int q = blockIdx.x, it = 0; q < npairs; q += gridDim.x, ++it) {
     const int l0 = 2 * q;
     const bool has1 = l0 + 1 < count;
@@ -249,6 +305,7 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
     // round-off would otherwise leak into it through the Hermitian split)
     zf_add(zf, it, (nzb0 != 0 ? 1 : 0) | (nzb1 != 0 ? 2 : 0));
     __syncthreads();
+    FD_PCLK(0, 0);
     if constexpr (PS::FOLD) {  // first DIF stage (v, v W^j), staged input consumed
       const FoldTw<LOGM> ft(tw, threadIdx.x);
 #pragma unroll
@@ -260,8 +317,9 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
         }
       }
       __syncthreads();
+      FD_PCLK(0, 1);
     }
-    pair_conv<LOGM, NT>(x, T, tw, m);
+    pair_conv<LOGM, NT, 0>(x, T, tw, m, pclk_);
     // the post phase reads [0, m) only: stage the next pair behind it
     if (threadIdx.x == 0) pair_issue(stg, io.in, io.gi, q + gridDim.x, n);
 
@@ -319,6 +377,7 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
         if (w1) wset(l0 + 1, w1, i, 0.0);
       }
     __syncthreads();  // x is reused by the next pair
+    FD_PCLK(0, 8);
   }
 }
 
@@ -344,6 +403,11 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
   const double* in = reinterpret_cast<const double*>(io.in);
   double* out = reinterpret_cast<double*>(io.out);
   const double isq = ax.inv_sqrt_m;
+#ifdef FD_PHASE_CLOCKS
+  long long pclk_ = clock64();
+#else
+  long long pclk_ = 0;
+#endif
   for (int q = blockIdx.x, it = 0; q < npairs; q += gridDim.x, ++it) {
     const int l0 = 2 * q;
     const bool has1 = l0 + 1 < count;
@@ -417,6 +481,7 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
                  [&](int i) { return has1 ? __ldg(g1 + i) : 0.0; });
     zf_add(zf, it, (nzb0 != 0 ? 1 : 0) | (nzb1 != 0 ? 2 : 0));
     __syncthreads();
+    FD_PCLK(1, 0);
     if constexpr (PS::FOLD) {  // first DIF stage (v, v W^j); zero padding written explicitly
       const FoldTw<LOGM> fk(tw, threadIdx.x), fc(tw, m - threadIdx.x);
 #pragma unroll
@@ -436,8 +501,9 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
         x[pidx(j + PS::HM)] = czero();
       }
       __syncthreads();
+      FD_PCLK(1, 1);
     }
-    pair_conv<LOGM, NT>(x, T, tw, m);
+    pair_conv<LOGM, NT, 1>(x, T, tw, m, pclk_);
     if (threadIdx.x == 0) pair_issue(stg, io.in, io.gi, q + gridDim.x, n);
 
     const Cubic p0 = ho_cubic(ax, ua0), p1 = ho_cubic(ax, ua1);
@@ -464,6 +530,7 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
         }
     }
     __syncthreads();
+    FD_PCLK(1, 8);
   }
 }
 
