@@ -164,6 +164,7 @@ void set_pair_attrs(int kmax) {
   cudaFuncSetAttribute(k_panalyze<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
   cudaFuncSetAttribute(k_psynth<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
   if constexpr (LOGM == 13) {
+    cudaFuncSetAttribute(k_panalyze<LOGM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
     cudaFuncSetAttribute(k_panalyze_e<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
     cudaFuncSetAttribute(k_psynth_e<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
   }
@@ -426,12 +427,19 @@ void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaS
     k_panalyze<L><<<persistent_grid(k_panalyze<L>, PairShape<L>::NT, smem, pairs),         \
                     PairShape<L>::NT, smem, st>>>(ax, io);                                 \
   }
-  // M = 8192: outermost radix-16 passes in registers (fd_pair_edge.cuh);
-  // FASTDEBLUR_PAIR_EDGE=0 selects the all-shared-memory kernels (A/B timing)
+  // M = 8192: outermost radix-16 passes in registers (fd_pair_edge.cuh), an
+  // experiment that measured slower (FASTDEBLUR_PAIR_EDGE=1 selects it)
   static const bool edge = [] {
     const char* e = std::getenv("FASTDEBLUR_PAIR_EDGE");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
   }();
+  static std::atomic<uint64_t> skew_mask{0};
+  once_per_device(skew_mask, [] {
+    if (const char* e = std::getenv("FASTDEBLUR_PAIR_SKEW")) {
+      const int v = std::atoi(e);
+      cudaMemcpyToSymbol(g_pair_skew, &v, sizeof(int));
+    }
+  });
   if (ax.fft.logM == 13 && edge) {
     constexpr int NT = EdgeShape<13>::NT;
     if (sa) {
@@ -440,6 +448,16 @@ void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaS
       k_panalyze_e<13><<<persistent_grid(k_panalyze_e<13>, NT, smem, pairs), NT, smem, st>>>(ax, io);
     }
     launched(sa ? "k_psynth" : "k_panalyze");
+    return;
+  }
+  static const bool wide = [] {
+    const char* e = std::getenv("FASTDEBLUR_PAIR_WIDE");
+    return !(e && e[0] == '0');
+  }();
+  if (ax.fft.logM == 13 && wide && !sa) {
+    constexpr int NT = PairShape<13, true>::NT;
+    k_panalyze<13, true><<<persistent_grid(k_panalyze<13, true>, NT, smem, pairs), NT, smem, st>>>(ax, io);
+    launched("k_panalyze");
     return;
   }
   switch (ax.fft.logM) {

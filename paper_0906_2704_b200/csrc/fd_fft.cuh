@@ -543,8 +543,23 @@ __device__ __forceinline__ void mid_pass_t(double2* __restrict__ x,
   }
 }
 
+// Barrier between passes.  GRP == 0: the whole CTA.  GRP > 0: the threads
+// [g GRP, (g+1) GRP) only (named barrier 1 + g) -- for pass sequences whose
+// items split into independent element sets per thread group (the two halves
+// of a folded convolution at NT = M/16: thread group g owns half g in every
+// pass), so the groups drift out of phase and one group's shared-memory
+// traffic overlaps the other's arithmetic.
+template <int GRP>
+__device__ __forceinline__ void pass_sync() {
+  if constexpr (GRP == 0) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)(threadIdx.x / GRP)), "n"(GRP) : "memory");
+  }
+}
+
 // pass P of the DIF sequence (block size S), the inner passes, then its DIT mirror
-template <int LOGM, int P, int S, int NTH = 0, bool ACC = false>
+template <int LOGM, int P, int S, int NTH = 0, bool ACC = false, int GRP = 0>
 __device__ __forceinline__ void bluestein_rec(double2* x, const double2* bhat, const TwSm& tw,
                                               int nvalid) {
   using F = FftShape<LOGM, NTH>;
@@ -553,17 +568,17 @@ __device__ __forceinline__ void bluestein_rec(double2* x, const double2* bhat, c
       mid_pass_t<LOGM, true, NTH>(x, bhat, nvalid);
     else
       mid_pass_t<LOGM, false, NTH>(x, bhat, nvalid);
-    __syncthreads();
+    pass_sync<GRP>();
   } else {
     constexpr int LR = (P == 0 && LOGM % 4 != 0) ? LOGM % 4 : 4;
     if (P == 0 && nvalid < F::M)
       dif_pass_t<LOGM, LR, S, true, NTH, ACC>(x, tw, nvalid);
     else
       dif_pass_t<LOGM, LR, S, false, NTH, ACC>(x, tw, nvalid);
-    __syncthreads();
-    bluestein_rec<LOGM, P + 1, (S >> LR), NTH, ACC>(x, bhat, tw, nvalid);
+    pass_sync<GRP>();
+    bluestein_rec<LOGM, P + 1, (S >> LR), NTH, ACC, GRP>(x, bhat, tw, nvalid);
     dit_pass_t<LOGM, LR, S, NTH, ACC>(x, tw);
-    __syncthreads();
+    pass_sync<GRP>();
   }
 }
 

@@ -77,26 +77,30 @@ __device__ unsigned long long g_pair_clocks[4][12];
 #endif
 
 // bluestein_rec<LOGM, P, S, NT> with phase marks after every pass (marks base + 0 ..)
-template <int LOGM, int P, int S, int NT, int KERN, int BASE>
+template <int LOGM, int P, int S, int NT, int KERN, int BASE, int GRP = 0>
 __device__ __forceinline__ void bluestein_rec_clk(double2* x, const double2* bhat, const TwSm& tw,
                                                   int nvalid, long long& pclk_) {
 #ifdef FD_PHASE_CLOCKS
   using F = FftShape<LOGM, NT>;
   if constexpr (P == F::NP - 1) {
     mid_pass_t<LOGM, false, NT>(x, bhat, nvalid);
-    __syncthreads();
+    pass_sync<GRP>();
     FD_PCLK(KERN, BASE);
   } else {
     dif_pass_t<LOGM, 4, S, false, NT, false>(x, tw, nvalid);
-    __syncthreads();
+    pass_sync<GRP>();
     FD_PCLK(KERN, BASE);
-    bluestein_rec_clk<LOGM, P + 1, (S >> 4), NT, KERN, BASE + 1>(x, bhat, tw, nvalid, pclk_);
+    bluestein_rec_clk<LOGM, P + 1, (S >> 4), NT, KERN, BASE + 1, GRP>(x, bhat, tw, nvalid, pclk_);
     dit_pass_t<LOGM, 4, S, NT, false>(x, tw);
-    __syncthreads();
+    pass_sync<GRP>();
     FD_PCLK(KERN, BASE + 2 * (F::NP - 1 - P));
   }
 #endif
 }
+
+// experiment knob: SM clocks the upper-half thread group waits before its
+// passes (FASTDEBLUR_PAIR_SKEW), to start the two groups out of phase
+__device__ int g_pair_skew = 1200;
 
 template <int LOGM, int NT, int KERN = 0>
 __device__ __forceinline__ void pair_conv(double2* x, const FftTables& T, const TwSm& tw, int m,
@@ -104,7 +108,16 @@ __device__ __forceinline__ void pair_conv(double2* x, const FftTables& T, const 
   using S = PairShape<LOGM>;
 #ifdef FD_PHASE_CLOCKS
   if constexpr (LOGM == 13) {
-    bluestein_rec_clk<LOGM, 1, S::HM, NT, KERN, 2>(x, T.bhat, tw, S::M, pclk_);
+    constexpr int GRPC = (NT == S::M / 16) ? NT / 2 : 0;
+    if constexpr (GRPC != 0) {
+      if (threadIdx.x >= GRPC) {
+        const long long t0 = clock64();
+        const int skew = g_pair_skew;
+        while (clock64() - t0 < skew) {}
+      }
+    }
+    bluestein_rec_clk<LOGM, 1, S::HM, NT, KERN, 2, GRPC>(x, T.bhat, tw, S::M, pclk_);
+    if constexpr (GRPC != 0) __syncthreads();
     const FoldTw<LOGM> ft(tw, threadIdx.x);
     for (int k = threadIdx.x; k < m; k += NT)
       x[pidx(k)] = cadd(x[pidx(k)], cmulc(x[pidx(k + S::HM)], ft(k)));
@@ -115,7 +128,18 @@ __device__ __forceinline__ void pair_conv(double2* x, const FftTables& T, const 
 #endif
   if constexpr (S::FOLD) {
     static_assert(NT % (1 << FoldTw<LOGM>::LOB) == 0, "FoldTw needs NT % lo length == 0");
-    bluestein_rec<LOGM, 1, S::HM, NT>(x, T.bhat, tw, S::M);
+    // NT == M/16: threads [0, NT/2) own the lower half's items in every pass,
+    // [NT/2, NT) the upper half's -- the halves synchronise separately
+    constexpr int GRP = (NT == S::M / 16 && NT >= 64) ? NT / 2 : 0;
+    if constexpr (GRP != 0) {
+      if (threadIdx.x >= GRP) {
+        const long long t0 = clock64();
+        const int skew = g_pair_skew;
+        while (clock64() - t0 < skew) {}
+      }
+    }
+    bluestein_rec<LOGM, 1, S::HM, NT, false, GRP>(x, T.bhat, tw, S::M);
+    if constexpr (GRP != 0) __syncthreads();
     const FoldTw<LOGM> ft(tw, threadIdx.x);
     for (int k = threadIdx.x; k < m; k += NT)
       x[pidx(k)] = cadd(x[pidx(k)], cmulc(x[pidx(k + S::HM)], ft(k)));
@@ -189,6 +213,30 @@ __device__ __forceinline__ int ho_wred(const AxisDev& ax, int l, int h) {
   return l < ax.kl ? l : ax.kl + h + 1 + (l - ax.kl);
 }
 
+// Output lines leave through the bulk-copy engine (shared -> global): an SM's
+// own store path sustains only ~14 B/clock (measured: the direct stores of the
+// post phases took 24 % of k_panalyze, 13 % of k_psynth), while a bulk store
+// drains in the background of the next pair's load phase.
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"((uint32_t)__cvta_generic_to_shared(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// all committed bulk stores have finished READING shared memory
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// the staged output lines (2 n doubles at the start of the FFT buffer) need
+// 16-byte aligned, unit-stride global lines of even length
+__device__ __forceinline__ bool pair_out_staged(const double* o0, const double* o1, int n,
+                                                long long eso) {
+  return eso == 1 && !(n & 1) && (reinterpret_cast<uintptr_t>(o0) & 15) == 0 &&
+         (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
+}
+
 struct PairStage {
   double* buf;
   uint64_t* bar;
@@ -227,9 +275,12 @@ __device__ __forceinline__ void pair_issue(PairStage& s, const void* base, const
   bulk_g2s(s.buf, src, (uint32_t)n * 16, s.bar);
 }
 
-template <int LOGM>
-__global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax, LineIO io) {
-  constexpr int NT = PairShape<LOGM>::NT, M = 1 << LOGM;
+// WIDE: 512 threads x 128 registers at M = 8192 (one radix-16 item per thread
+// per pass, the two halves' thread groups synchronising separately) instead of
+// 256 x 255
+template <int LOGM, bool WIDE = false>
+__global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisDev ax, LineIO io) {
+  constexpr int NT = PairShape<LOGM, WIDE>::NT, M = 1 << LOGM;
   extern __shared__ double2 sm[];
   const FftTables& T = ax.fft;
   const int m = ax.m, n = ax.n, kl = ax.kl, hk = ax.hk, h = (m - 1) / 2;
@@ -269,7 +320,7 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
     const double* s1 = stg.buf + n;
     double a0[kHoMax], a1[kHoMax];
     Cubic p0, p1;
-    using PS = PairShape<LOGM>;
+    using PS = PairShape<LOGM, WIDE>;
     double2 vr[PS::FOLD ? PS::JS : 1];
     long long nzb0 = 0, nzb1 = 0;  // OR of the bit patterns of line 0 / 1 (-0.0 counts as nonzero)
     auto load_phase = [&](auto ld0, auto ld1) {
@@ -304,6 +355,7 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
     // an all-zero line gets exactly zero coefficients (its partner's DFT
     // round-off would otherwise leak into it through the Hermitian split)
     zf_add(zf, it, (nzb0 != 0 ? 1 : 0) | (nzb1 != 0 ? 2 : 0));
+    if (PS::FOLD && threadIdx.x == 0) bulk_wait_read();  // the previous pair's output lines
     __syncthreads();
     FD_PCLK(0, 0);
     if constexpr (PS::FOLD) {  // first DIF stage (v, v W^j), staged input consumed
@@ -339,6 +391,52 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
     double* w1 = (w0 && has1) ? w0 + io.wstride : nullptr;
     const int nz = zf_take(zf, it);
     const bool z0 = !(nz & 1) && ho_zero(a0), z1 = !(nz & 2) && ho_zero(a1);
+    // FOLD sizes: the packed coefficient lines are assembled in shared memory
+    // (the buffer's lower part, free once every thread has read its Z_k) and
+    // leave as two bulk stores; only the GCV weights take the store path
+    constexpr int KSA = PS::FOLD ? (PS::HM / 2 + NT) / NT : 1;
+    const bool tout = PS::FOLD && pair_out_staged(o0, o1, n, io.go.elem_stride) && (hk & 1);
+    if (tout) {
+      double2 X0r[KSA], X1r[KSA];
+#pragma unroll
+      for (int t = 0; t < KSA; ++t) {
+        const int kk = threadIdx.x + t * NT;
+        X0r[t] = X1r[t] = czero();
+        if (kk > h) continue;
+        const double2 Zk = cmul(x[pidx(kk)], cs[kk]);
+        const double2 Zc = kk ? cmul(x[pidx(m - kk)], cs[m - kk]) : Zk;
+        const double2 D = csub(Zk, cconj(Zc));
+        const double2 X0 = z0 ? czero() : cscale(cadd(Zk, cconj(Zc)), 0.5 * isq);
+        const double2 X1 = z1 ? czero() : make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
+        X0r[t] = X0;
+        X1r[t] = X1;
+        if (w0) {
+          const double f = kk ? 2.0 : 1.0;  // |X_k|^2 + |X_{m-k}|^2
+          wset(l0, w0, kl + kk, f * (X0.x * X0.x + X0.y * X0.y));
+          if (w1) wset(l0 + 1, w1, kl + kk, f * (X1.x * X1.x + X1.y * X1.y));
+        }
+      }
+      __syncthreads();  // every Z_k has been read
+      double* lineA = reinterpret_cast<double*>(x);
+      double* lineB = lineA + n;
+#pragma unroll
+      for (int t = 0; t < KSA; ++t) {
+        const int kk = threadIdx.x + t * NT;
+        if (kk > h) continue;
+        if (kk == 0) {
+          lineA[hk] = X0r[t].x;
+          lineB[hk] = X1r[t].x;
+        } else {  // hk odd: (Re, Im) 16-byte aligned
+          *reinterpret_cast<double2*>(lineA + hk + 2 * kk - 1) = X0r[t];
+          *reinterpret_cast<double2*>(lineB + hk + 2 * kk - 1) = X1r[t];
+        }
+      }
+      if (threadIdx.x < hk) {
+        lineA[threadIdx.x] = a0[threadIdx.x];
+        lineB[threadIdx.x] = a1[threadIdx.x];
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    } else
     for (int kk = threadIdx.x; kk <= h; kk += NT) {
       const double2 Zk = cmul(x[pidx(kk)], cs[kk]);
       const double2 Zc = kk ? cmul(x[pidx(m - kk)], cs[m - kk]) : Zk;
@@ -364,8 +462,10 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
     }
     if (threadIdx.x < hk) {
       const int l = threadIdx.x;
-      o0[l] = a0[l];
-      if (o1) o1[l] = a1[l];
+      if (!tout) {
+        o0[l] = a0[l];
+        if (o1) o1[l] = a1[l];
+      }
       if (w0) {
         wset(l0, w0, ho_wred(ax, l, h), a0[l] * a0[l]);
         if (w1) wset(l0 + 1, w1, ho_wred(ax, l, h), a1[l] * a1[l]);
@@ -377,8 +477,14 @@ __global__ void __launch_bounds__(PairShape<LOGM>::NT, 1) k_panalyze(AxisDev ax,
         if (w1) wset(l0 + 1, w1, i, 0.0);
       }
     __syncthreads();  // x is reused by the next pair
+    if (tout && threadIdx.x == 0) {
+      bulk_s2g(o0, x, (uint32_t)n * 8);
+      if (o1) bulk_s2g(o1, reinterpret_cast<double*>(x) + n, (uint32_t)n * 8);
+      bulk_commit();
+    }
     FD_PCLK(0, 8);
   }
+  if (threadIdx.x == 0) bulk_wait_read();  // shared memory stays valid until the last lines are read
 }
 
 template <int LOGM>
@@ -403,6 +509,29 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
   const double* in = reinterpret_cast<const double*>(io.in);
   double* out = reinterpret_cast<double*>(io.out);
   const double isq = ax.inv_sqrt_m;
+  using PS = PairShape<LOGM, true>;
+  constexpr int KS = PS::FOLD ? (PS::HM / 2 + NT) / NT : 1;  // kk slots (kk <= h < HM/2+1)
+  // 1D filter (one spectral table for every line): the values of this thread's
+  // kk slots are the same for every pair -- read once, kept in registers (the
+  // per-pair table reads were latency bound: 27 % of the kernel at config 1)
+  const bool spreg = PS::FOLD && sa.mode == 1 && sa.sp.mode == 1 && ax.cplx;
+  double2 spd[KS];
+  double sps[KS];
+  if (spreg) {
+#pragma unroll
+    for (int t = 0; t < KS; ++t) {
+      const int kk = threadIdx.x + t * NT;
+      const int e = kl + (kk <= h ? kk : h);
+      spd[t] = __ldg(&sa.sp.dA[e]);
+      sps[t] = sa.sp.sA ? __ldg(&sa.sp.sA[e]) : 1.0;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < KS; ++t) {
+      spd[t] = czero();
+      sps[t] = 0.0;
+    }
+  }
 #ifdef FD_PHASE_CLOCKS
   long long pclk_ = clock64();
 #else
@@ -425,14 +554,12 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
       return has1 ? coeff_filter_fast(ax, sa, io.gi, l0 + 1, e, c, mu1) : czero();
     };
     double ua0[kHoMax], ua1[kHoMax];
-    using PS = PairShape<LOGM, true>;
-    constexpr int KS = PS::FOLD ? (PS::HM / 2 + NT) / NT : 1;  // kk slots (kk <= h < HM/2+1)
     double2 vk[KS], vc[KS];
     // OR of the filtered coefficients' bit patterns: a line whose filtered
     // coefficients are all zero is written as exact zeros (its partner's
     // inverse-DFT round-off would otherwise leak into it)
     long long nzb0 = 0, nzb1 = 0;
-    auto load_phase = [&](auto ld0, auto ld1) {
+    auto load_phase = [&](auto ld0, auto ld1, auto ldp0, auto ldp1) {
 #pragma unroll
       for (int l = 0; l < kHoMax; ++l) {
         ua0[l] = l < hk ? f0(ho_coef_elem(ax, l), make_double2(ld0(l), 0.0)).x : 0.0;
@@ -440,18 +567,26 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
       }
       // Bluestein inputs of index kk and m - kk (F^H v = conj(F conj v):
       // conj(v_k) c_k, v = X0 + i X1)
-      auto one = [&](int kk, double2& a, double2& b) {
+      auto one = [&](int kk, int t, double2& a, double2& b) {
         const int e = kl + kk;
         double2 X0, X1;
         if (kk == 0) {
           X0 = make_double2(ld0(hk), 0.0);
           X1 = make_double2(ld1(hk), 0.0);
         } else {
-          X0 = make_double2(ld0(hk + 2 * kk - 1), ld0(hk + 2 * kk));
-          X1 = make_double2(ld1(hk + 2 * kk - 1), ld1(hk + 2 * kk));
+          X0 = ldp0(hk + 2 * kk - 1);
+          X1 = ldp1(hk + 2 * kk - 1);
         }
-        X0 = f0(e, X0);
-        X1 = f1(e, X1);
+        if (spreg) {  // coeff_filter_fast on the register copy of (d, s)
+          const double2 d = spd[t];
+          const double dd = d.x * d.x + d.y * d.y, ss = sps[t] * sps[t];
+          const double r0 = rcp_pos(dd + mu0 * ss), r1 = rcp_pos(dd + mu1 * ss);
+          X0 = cmul(X0, make_double2(d.x * r0, -d.y * r0));
+          X1 = has1 ? cmul(X1, make_double2(d.x * r1, -d.y * r1)) : czero();
+        } else {
+          X0 = f0(e, X0);
+          X1 = f1(e, X1);
+        }
         nzb0 |= __double_as_longlong(X0.x) | __double_as_longlong(X0.y);
         nzb1 |= __double_as_longlong(X1.x) | __double_as_longlong(X1.y);
         a = cmul(make_double2(X0.x - X1.y, -(X0.y + X1.x)), cs[kk]);
@@ -462,24 +597,35 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
         for (int t = 0; t < KS; ++t) {
           const int kk = threadIdx.x + t * NT;
           vk[t] = vc[t] = czero();
-          if (kk <= h) one(kk, vk[t], vc[t]);
+          if (kk <= h) one(kk, t, vk[t], vc[t]);
         }
       } else {
 #pragma unroll 2
         for (int kk = threadIdx.x; kk <= h; kk += NT) {
           double2 a, b;
-          one(kk, a, b);
+          one(kk, 0, a, b);
           x[pidx(kk)] = a;
           if (kk) x[pidx(m - kk)] = b;
         }
       }
     };
-    if (st)
-      load_phase([&](int i) { return stg.buf[i]; }, [&](int i) { return stg.buf[n + i]; });
+    if (st && (hk & 1) && !(n & 1))  // (Re, Im) pairs 16-byte aligned in the staged lines
+      load_phase([&](int i) { return stg.buf[i]; }, [&](int i) { return stg.buf[n + i]; },
+                 [&](int i) { return *reinterpret_cast<const double2*>(stg.buf + i); },
+                 [&](int i) { return *reinterpret_cast<const double2*>(stg.buf + n + i); });
+    else if (st)
+      load_phase([&](int i) { return stg.buf[i]; }, [&](int i) { return stg.buf[n + i]; },
+                 [&](int i) { return make_double2(stg.buf[i], stg.buf[i + 1]); },
+                 [&](int i) { return make_double2(stg.buf[n + i], stg.buf[n + i + 1]); });
     else
       load_phase([&](int i) { return __ldg(g0 + i); },
-                 [&](int i) { return has1 ? __ldg(g1 + i) : 0.0; });
+                 [&](int i) { return has1 ? __ldg(g1 + i) : 0.0; },
+                 [&](int i) { return make_double2(__ldg(g0 + i), __ldg(g0 + i + 1)); },
+                 [&](int i) {
+                   return has1 ? make_double2(__ldg(g1 + i), __ldg(g1 + i + 1)) : czero();
+                 });
     zf_add(zf, it, (nzb0 != 0 ? 1 : 0) | (nzb1 != 0 ? 2 : 0));
+    if (PS::FOLD && threadIdx.x == 0) bulk_wait_read();  // the previous pair's output lines
     __syncthreads();
     FD_PCLK(1, 0);
     if constexpr (PS::FOLD) {  // first DIF stage (v, v W^j); zero padding written explicitly
@@ -512,6 +658,74 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
     double* o1 = has1 ? out + line_offset(io.go, l0 + 1) : nullptr;
     const int nz = zf_take(zf, it);
     const double s0 = (nz & 1) ? isq : 0.0, s1 = (nz & 2) ? -isq : 0.0;
+    const bool vec = eso == 1 && (reinterpret_cast<uintptr_t>(o0) & 15) == 0 &&
+                     (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
+    // FOLD sizes: the restored lines are assembled in shared memory (the
+    // buffer's lower part, free once every thread has read its samples) and
+    // leave as two bulk stores
+    constexpr int PSN = PS::FOLD ? (PS::HM + NT - 1) / NT : 1;
+    const bool tout = PS::FOLD && pair_out_staged(o0, o1, n, eso);
+    if (tout) {
+      double y0r[PSN], y1r[PSN];
+#pragma unroll
+      for (int t = 0; t < PSN; ++t) {
+        const int p = threadIdx.x + t * NT;
+        y0r[t] = y1r[t] = 0.0;
+        if (p < m) {
+          const double2 z = cmul(x[pidx(p)], cs[p]);  // conj of (F^H v)_p sqrt(m)
+          y0r[t] = z.x * s0;
+          y1r[t] = z.y * s1;
+        }
+      }
+      __syncthreads();  // every sample has been read
+      double* lineA = reinterpret_cast<double*>(x);
+      double* lineB = lineA + n;
+#pragma unroll
+      for (int t = 0; t < PSN; ++t) {
+        const int p = threadIdx.x + t * NT;
+        if (p >= m) continue;
+        const int e = kl + p;
+        const double tt = fma((double)e, ax.ho_ta, ax.ho_tb);
+        lineA[e] = y0r[t] + p0(tt);
+        lineB[e] = y1r[t] + p1(tt);
+#pragma unroll
+        for (int l = 0; l < kHoMax; ++l)
+          if (l < hk && ax.wrap[l] == p) {
+            const int eb = ax.bord[l];
+            const double tb = fma((double)eb, ax.ho_ta, ax.ho_tb);
+            lineA[eb] = y0r[t] + p0(tb);
+            lineB[eb] = y1r[t] + p1(tb);
+          }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    } else if (vec) {
+      // element pairs (2u, 2u + 1) as 16-byte stores; a border element takes
+      // the interior sample it wraps to (ax.wrap) with the cubic at its own t
+      for (int u = threadIdx.x; 2 * u < n; u += NT) {
+        double r0[2] = {0.0, 0.0}, r1[2] = {0.0, 0.0};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int e = 2 * u + c;
+          if (e >= n) continue;
+          int p = e - kl;
+          if (p < 0)
+            p = ax.wrap[e];
+          else if (p >= m)
+            p = ax.wrap[kl + (p - m)];
+          const double2 z = cmul(x[pidx(p)], cs[p]);  // conj of (F^H v)_p sqrt(m)
+          const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
+          r0[c] = z.x * s0 + p0(t);
+          r1[c] = z.y * s1 + p1(t);
+        }
+        if (2 * u + 1 < n) {
+          *reinterpret_cast<double2*>(o0 + 2 * u) = make_double2(r0[0], r0[1]);
+          if (o1) *reinterpret_cast<double2*>(o1 + 2 * u) = make_double2(r1[0], r1[1]);
+        } else {
+          o0[2 * u] = r0[0];
+          if (o1) o1[2 * u] = r1[0];
+        }
+      }
+    } else
 #pragma unroll 4
     for (int p = threadIdx.x; p < m; p += NT) {
       const double2 z = cmul(x[pidx(p)], cs[p]);  // conj of (F^H v)_p sqrt(m)
@@ -530,8 +744,14 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
         }
     }
     __syncthreads();
+    if (tout && threadIdx.x == 0) {
+      bulk_s2g(o0, x, (uint32_t)n * 8);
+      if (o1) bulk_s2g(o1, reinterpret_cast<double*>(x) + n, (uint32_t)n * 8);
+      bulk_commit();
+    }
     FD_PCLK(1, 8);
   }
+  if (threadIdx.x == 0) bulk_wait_read();  // shared memory stays valid until the last lines are read
 }
 
 }  // namespace fdb
