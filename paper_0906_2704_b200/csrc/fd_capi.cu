@@ -27,7 +27,6 @@
 #include "fd_internal.h"
 #include "fd_kernels.cuh"
 #include "fd_pair.cuh"
-#include "fd_pair_edge.cuh"
 #include "fd_mixed.cuh"
 #include "fd_rader.cuh"
 #include "fd_gen.cuh"
@@ -165,8 +164,6 @@ void set_pair_attrs(int kmax) {
   cudaFuncSetAttribute(k_psynth<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
   if constexpr (LOGM == 13) {
     cudaFuncSetAttribute(k_panalyze<LOGM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
-    cudaFuncSetAttribute(k_panalyze_e<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
-    cudaFuncSetAttribute(k_psynth_e<LOGM>, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
   }
 }
 
@@ -418,7 +415,7 @@ void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaS
     launched(sa ? "k_msynth" : "k_manalyze");
     return;
   }
-  const size_t smem = (size_t)pair_slots(ax.fft.M, ax.m) * sizeof(double2);
+  const size_t smem = (size_t)pair_smem_slots(ax.fft.M, ax.m) * sizeof(double2);
 #define FD_PA(L)                                                                           \
   if (sa) {                                                                                \
     k_psynth<L><<<persistent_grid(k_psynth<L>, PairShape<L, true>::NT, smem, pairs),       \
@@ -427,29 +424,13 @@ void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaS
     k_panalyze<L><<<persistent_grid(k_panalyze<L>, PairShape<L>::NT, smem, pairs),         \
                     PairShape<L>::NT, smem, st>>>(ax, io);                                 \
   }
-  // M = 8192: outermost radix-16 passes in registers (fd_pair_edge.cuh), an
-  // experiment that measured slower (FASTDEBLUR_PAIR_EDGE=1 selects it)
-  static const bool edge = [] {
-    const char* e = std::getenv("FASTDEBLUR_PAIR_EDGE");
-    return e && e[0] == '1';
-  }();
   static std::atomic<uint64_t> skew_mask{0};
-  once_per_device(skew_mask, [] {
+  once_per_device(skew_mask, [] {  // experiment knob, see g_pair_skew
     if (const char* e = std::getenv("FASTDEBLUR_PAIR_SKEW")) {
       const int v = std::atoi(e);
       cudaMemcpyToSymbol(g_pair_skew, &v, sizeof(int));
     }
   });
-  if (ax.fft.logM == 13 && edge) {
-    constexpr int NT = EdgeShape<13>::NT;
-    if (sa) {
-      k_psynth_e<13><<<persistent_grid(k_psynth_e<13>, NT, smem, pairs), NT, smem, st>>>(ax, io, *sa);
-    } else {
-      k_panalyze_e<13><<<persistent_grid(k_panalyze_e<13>, NT, smem, pairs), NT, smem, st>>>(ax, io);
-    }
-    launched(sa ? "k_psynth" : "k_panalyze");
-    return;
-  }
   static const bool wide = [] {
     const char* e = std::getenv("FASTDEBLUR_PAIR_WIDE");
     return !(e && e[0] == '0');

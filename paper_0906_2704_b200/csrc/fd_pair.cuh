@@ -149,11 +149,27 @@ __device__ __forceinline__ void pair_conv(double2* x, const FftTables& T, const 
   }
 }
 
-// smem slots (double2) of the pair kernels: buffer, twiddles, chirp, mbarrier
-// (+ the two zero-line flag words in the same slot)
+// Shared-memory slots (double2) of the pair kernels:
+//   FFT buffer | twiddles | chirp c_0 .. c_h | mbarrier + zero-line flags |
+//   border spectral values (8) | synthesis filter table: d (h + 1), s ((h + 2) / 2)
+// Only half the chirp is stored: c_{m-j} = e^{-i pi (m-j)^2/m} = (-1)^m c_j = -c_j
+// for the odd m of this path.  The freed space holds the 1D filter's spectral
+// table (k_psynth), which was re-read from L2 for every line pair.
+__host__ __device__ __forceinline__ int pair_cs_slots(int m) { return (m - 1) / 2 + 1; }
 __host__ __device__ __forceinline__ int pair_slots(int M, int m) {
-  return pidx(M) + 1 + kTwSlots + m + 1;
+  return pidx(M) + 1 + kTwSlots + pair_cs_slots(m) + 1;
 }
+__host__ __device__ __forceinline__ int pair_smem_slots(int M, int m) {
+  return pair_slots(M, m) + 8 + pair_cs_slots(m) + (pair_cs_slots(m) + 1) / 2;
+}
+struct HalfChirp {
+  const double2* cs;
+  int m, h;
+  __device__ __forceinline__ double2 operator()(int j) const {
+    const double2 c = cs[j <= h ? j : m - j];
+    return j <= h ? c : make_double2(-c.x, -c.y);
+  }
+};
 
 // sum_l a_l P_l(t) as a cubic in t (P_1 = t, P_2 = (3t^2-1)/2, P_3 = (5t^3-3t)/2)
 struct Cubic {
@@ -288,7 +304,8 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
   double2* slots = sm + pidx(M) + 1;
   const TwSm tw = load_twiddles(slots, T);
   double2* cs = slots + kTwSlots;
-  for (int j = threadIdx.x; j < m; j += NT) cs[j] = T.chirp[j];
+  for (int j = threadIdx.x; j <= h; j += NT) cs[j] = T.chirp[j];
+  const HalfChirp chirp{cs, m, h};
   PairStage stg = pair_stage_init(x, M, m, n, io.gi,
                                   reinterpret_cast<uint64_t*>(sm + pair_slots(M, m) - 1));
   int* zf = reinterpret_cast<int*>(sm + pair_slots(M, m) - 1) + 2;
@@ -301,6 +318,8 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
   const long long es = io.gi.elem_stride;
   const double isq = ax.inv_sqrt_m;
   const long long nkb32 = io.wstride >> 5;
+  // t_e = ho_ta e + ho_tb at this thread's first element; slot t adds t NT ho_ta
+  const double tt0 = fma((double)(kl + (int)threadIdx.x), ax.ho_ta, ax.ho_tb);
 #ifdef FD_PHASE_CLOCKS
   long long pclk_ = clock64();
 #else
@@ -328,23 +347,23 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
       ho_amps_real(ax, ld1, a1);
       p0 = ho_cubic(ax, a0);
       p1 = ho_cubic(ax, a1);
-      auto val = [&](int j) {
+      auto val = [&](int j, double t) {
         const int e = kl + j;
-        const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
         const double y0 = ld0(e), y1 = ld1(e);
         nzb0 |= __double_as_longlong(y0);  // integer pipe: the fp64 pipe is the bound
-      nzb1 |= __double_as_longlong(y1);
-        return cmul(make_double2(y0 - p0(t), y1 - p1(t)), cs[j]);
+        nzb1 |= __double_as_longlong(y1);
+        return cmul(make_double2(y0 - p0(t), y1 - p1(t)), chirp(j));
       };
       if constexpr (PS::FOLD) {
 #pragma unroll
         for (int t = 0; t < PS::JS; ++t) {
           const int j = threadIdx.x + t * NT;
-          vr[t] = j < m ? val(j) : czero();
+          vr[t] = j < m ? val(j, fma((double)(t * NT), ax.ho_ta, tt0)) : czero();
         }
       } else {
 #pragma unroll 4
-        for (int j = threadIdx.x; j < m; j += NT) x[pidx(j)] = val(j);
+        for (int j = threadIdx.x; j < m; j += NT)
+          x[pidx(j)] = val(j, fma((double)(kl + j), ax.ho_ta, ax.ho_tb));
       }
     };
     if (st)
@@ -378,17 +397,27 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
     double* o0 = out + line_offset(io.go, l0);
     double* o1 = has1 ? out + line_offset(io.go, l0 + 1) : nullptr;
     double* w0 = io.wout ? io.wout + (long long)l0 * io.wstride : nullptr;
-    auto wset = [&](int line, double* wl, long long i, double v) {
-      wl[i] = v;
-      if (io.wout32) {
+    // weight i of both lines: fp64 rows, and their TF32 split in the screen's
+    // tile layout (tc_tile_index = row part + element part; the pair's rows
+    // l0, l0 + 1 are adjacent 16-byte chunks, 4 floats apart)
+    float* t32h = io.wout32 ? io.wout32 + tc_tile_index(l0, 0, kTcBM, nkb32) : nullptr;
+    float* t32l = io.wout32 ? io.wout32lo + tc_tile_index(l0, 0, kTcBM, nkb32) : nullptr;
+    auto wset2 = [&](int i, double v0, double v1) {
+      w0[i] = v0;
+      if (has1) w0[io.wstride + i] = v1;
+      if (t32h) {
+        const int eo = (i >> 5) * (kTcBM * 32) + ((i & 31) >> 2) * (kTcBM * 4) + (i & 3);
         float hi, lo;
-        tf32_split(v, hi, lo);
-        const long long t = tc_tile_index(line, i, kTcBM, nkb32);
-        io.wout32[t] = hi;
-        io.wout32lo[t] = lo;
+        tf32_split(v0, hi, lo);
+        t32h[eo] = hi;
+        t32l[eo] = lo;
+        if (has1) {
+          tf32_split(v1, hi, lo);
+          t32h[eo + 4] = hi;
+          t32l[eo + 4] = lo;
+        }
       }
     };
-    double* w1 = (w0 && has1) ? w0 + io.wstride : nullptr;
     const int nz = zf_take(zf, it);
     const bool z0 = !(nz & 1) && ho_zero(a0), z1 = !(nz & 2) && ho_zero(a1);
     // FOLD sizes: the packed coefficient lines are assembled in shared memory
@@ -403,8 +432,9 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
         const int kk = threadIdx.x + t * NT;
         X0r[t] = X1r[t] = czero();
         if (kk > h) continue;
-        const double2 Zk = cmul(x[pidx(kk)], cs[kk]);
-        const double2 Zc = kk ? cmul(x[pidx(m - kk)], cs[m - kk]) : Zk;
+        const double2 ck = cs[kk];  // c_{m-kk} = -c_kk
+        const double2 Zk = cmul(x[pidx(kk)], ck);
+        const double2 Zc = kk ? cmul(x[pidx(m - kk)], make_double2(-ck.x, -ck.y)) : Zk;
         const double2 D = csub(Zk, cconj(Zc));
         const double2 X0 = z0 ? czero() : cscale(cadd(Zk, cconj(Zc)), 0.5 * isq);
         const double2 X1 = z1 ? czero() : make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
@@ -412,8 +442,7 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
         X1r[t] = X1;
         if (w0) {
           const double f = kk ? 2.0 : 1.0;  // |X_k|^2 + |X_{m-k}|^2
-          wset(l0, w0, kl + kk, f * (X0.x * X0.x + X0.y * X0.y));
-          if (w1) wset(l0 + 1, w1, kl + kk, f * (X1.x * X1.x + X1.y * X1.y));
+          wset2(kl + kk, f * (X0.x * X0.x + X0.y * X0.y), f * (X1.x * X1.x + X1.y * X1.y));
         }
       }
       __syncthreads();  // every Z_k has been read
@@ -438,8 +467,9 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     } else
     for (int kk = threadIdx.x; kk <= h; kk += NT) {
-      const double2 Zk = cmul(x[pidx(kk)], cs[kk]);
-      const double2 Zc = kk ? cmul(x[pidx(m - kk)], cs[m - kk]) : Zk;
+      const double2 ck = cs[kk];  // c_{m-kk} = -c_kk
+      const double2 Zk = cmul(x[pidx(kk)], ck);
+      const double2 Zc = kk ? cmul(x[pidx(m - kk)], make_double2(-ck.x, -ck.y)) : Zk;
       const double2 D = csub(Zk, cconj(Zc));
       const double2 X0 = z0 ? czero() : cscale(cadd(Zk, cconj(Zc)), 0.5 * isq);
       const double2 X1 = z1 ? czero() : make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
@@ -456,8 +486,7 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
       }
       if (w0) {
         const double f = kk ? 2.0 : 1.0;  // |X_k|^2 + |X_{m-k}|^2
-        wset(l0, w0, kl + kk, f * (X0.x * X0.x + X0.y * X0.y));
-        if (w1) wset(l0 + 1, w1, kl + kk, f * (X1.x * X1.x + X1.y * X1.y));
+        wset2(kl + kk, f * (X0.x * X0.x + X0.y * X0.y), f * (X1.x * X1.x + X1.y * X1.y));
       }
     }
     if (threadIdx.x < hk) {
@@ -466,16 +495,10 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
         o0[l] = a0[l];
         if (o1) o1[l] = a1[l];
       }
-      if (w0) {
-        wset(l0, w0, ho_wred(ax, l, h), a0[l] * a0[l]);
-        if (w1) wset(l0 + 1, w1, ho_wred(ax, l, h), a1[l] * a1[l]);
-      }
+      if (w0) wset2(ho_wred(ax, l, h), a0[l] * a0[l], a1[l] * a1[l]);
     }
     if (w0)
-      for (long long i = io.wn + threadIdx.x; i < io.wstride; i += NT) {
-        wset(l0, w0, i, 0.0);
-        if (w1) wset(l0 + 1, w1, i, 0.0);
-      }
+      for (int i = (int)io.wn + threadIdx.x; i < (int)io.wstride; i += NT) wset2(i, 0.0, 0.0);
     __syncthreads();  // x is reused by the next pair
     if (tout && threadIdx.x == 0) {
       bulk_s2g(o0, x, (uint32_t)n * 8);
@@ -498,7 +521,8 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
   double2* slots = sm + pidx(M) + 1;
   const TwSm tw = load_twiddles(slots, T);
   double2* cs = slots + kTwSlots;
-  for (int j = threadIdx.x; j < m; j += NT) cs[j] = T.chirp[j];
+  for (int j = threadIdx.x; j <= h; j += NT) cs[j] = T.chirp[j];
+  const HalfChirp chirp{cs, m, h};
   PairStage stg = pair_stage_init(x, M, m, n, io.gi,
                                   reinterpret_cast<uint64_t*>(sm + pair_slots(M, m) - 1));
   int* zf = reinterpret_cast<int*>(sm + pair_slots(M, m) - 1) + 2;
@@ -511,27 +535,36 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
   const double isq = ax.inv_sqrt_m;
   using PS = PairShape<LOGM, true>;
   constexpr int KS = PS::FOLD ? (PS::HM / 2 + NT) / NT : 1;  // kk slots (kk <= h < HM/2+1)
-  // 1D filter (one spectral table for every line): the values of this thread's
-  // kk slots are the same for every pair -- read once, kept in registers (the
-  // per-pair table reads were latency bound: 27 % of the kernel at config 1)
-  const bool spreg = PS::FOLD && sa.mode == 1 && sa.sp.mode == 1 && ax.cplx;
-  double2 spd[KS];
-  double sps[KS];
-  if (spreg) {
-#pragma unroll
-    for (int t = 0; t < KS; ++t) {
-      const int kk = threadIdx.x + t * NT;
-      const int e = kl + (kk <= h ? kk : h);
-      spd[t] = __ldg(&sa.sp.dA[e]);
-      sps[t] = sa.sp.sA ? __ldg(&sa.sp.sA[e]) : 1.0;
+  // 1D filter (one spectral table for every line): the table lives in shared
+  // memory -- the per-pair reads from L2 were latency bound (27 % of the kernel
+  // at config 1); the border coefficients' entries sit in the extras slots
+  const bool spsm = sa.mode == 1 && sa.sp.mode == 1 && ax.cplx;
+  double2* bsp = sm + pair_slots(M, m);        // [l] = d of border coefficient l, [4 + l].x = s
+  double2* spd = bsp + 8;                      // d of interior coefficient kk
+  double* sps = reinterpret_cast<double*>(spd + pair_cs_slots(m));
+  if (spsm) {
+    for (int kk = threadIdx.x; kk <= h; kk += NT) {
+      spd[kk] = __ldg(&sa.sp.dA[kl + kk]);
+      sps[kk] = sa.sp.sA ? __ldg(&sa.sp.sA[kl + kk]) : 1.0;
     }
-  } else {
-#pragma unroll
-    for (int t = 0; t < KS; ++t) {
-      spd[t] = czero();
-      sps[t] = 0.0;
+    if (threadIdx.x < hk) {
+      const int e = ho_coef_elem(ax, threadIdx.x);
+      bsp[threadIdx.x] = __ldg(&sa.sp.dA[e]);
+      bsp[4 + threadIdx.x].x = sa.sp.sA ? __ldg(&sa.sp.sA[e]) : 1.0;
     }
+    __syncthreads();
   }
+  const double tt0 = fma((double)(kl + (int)threadIdx.x), ax.ho_ta, ax.ho_tb);
+  // regularisation parameters of the next pair, read one pair ahead
+  auto pair_mu = [&](int q, double& m0, double& m1) {
+    m0 = m1 = 0.0;
+    if (q < npairs) {
+      m0 = line_mu(sa, io.gi, 2 * q);
+      m1 = 2 * q + 1 < count ? line_mu(sa, io.gi, 2 * q + 1) : m0;
+    }
+  };
+  double mu0n, mu1n;
+  pair_mu(blockIdx.x, mu0n, mu1n);
 #ifdef FD_PHASE_CLOCKS
   long long pclk_ = clock64();
 #else
@@ -547,8 +580,8 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
     }
     const double* g0 = in + line_offset(io.gi, l0);
     const double* g1 = has1 ? in + line_offset(io.gi, l0 + 1) : g0;
-    const double mu0 = line_mu(sa, io.gi, l0);
-    const double mu1 = has1 ? line_mu(sa, io.gi, l0 + 1) : mu0;
+    const double mu0 = mu0n, mu1 = mu1n;
+    pair_mu(q + gridDim.x, mu0n, mu1n);
     auto f0 = [&](int e, double2 c) { return coeff_filter_fast(ax, sa, io.gi, l0, e, c, mu0); };
     auto f1 = [&](int e, double2 c) {
       return has1 ? coeff_filter_fast(ax, sa, io.gi, l0 + 1, e, c, mu1) : czero();
@@ -562,8 +595,16 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
     auto load_phase = [&](auto ld0, auto ld1, auto ldp0, auto ldp1) {
 #pragma unroll
       for (int l = 0; l < kHoMax; ++l) {
-        ua0[l] = l < hk ? f0(ho_coef_elem(ax, l), make_double2(ld0(l), 0.0)).x : 0.0;
-        ua1[l] = l < hk ? f1(ho_coef_elem(ax, l), make_double2(ld1(l), 0.0)).x : 0.0;
+        if (spsm) {  // Re(c conj(d) / den) of a real border coefficient c
+          const double2 d = bsp[l];
+          const double sv = bsp[4 + l].x;
+          const double dd = d.x * d.x + d.y * d.y, ss = sv * sv;
+          ua0[l] = l < hk ? ld0(l) * (d.x * rcp_pos(dd + mu0 * ss)) : 0.0;
+          ua1[l] = (l < hk && has1) ? ld1(l) * (d.x * rcp_pos(dd + mu1 * ss)) : 0.0;
+        } else {
+          ua0[l] = l < hk ? f0(ho_coef_elem(ax, l), make_double2(ld0(l), 0.0)).x : 0.0;
+          ua1[l] = l < hk ? f1(ho_coef_elem(ax, l), make_double2(ld1(l), 0.0)).x : 0.0;
+        }
       }
       // Bluestein inputs of index kk and m - kk (F^H v = conj(F conj v):
       // conj(v_k) c_k, v = X0 + i X1)
@@ -577,9 +618,10 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
           X0 = ldp0(hk + 2 * kk - 1);
           X1 = ldp1(hk + 2 * kk - 1);
         }
-        if (spreg) {  // coeff_filter_fast on the register copy of (d, s)
-          const double2 d = spd[t];
-          const double dd = d.x * d.x + d.y * d.y, ss = sps[t] * sps[t];
+        if (spsm) {  // coeff_filter_fast on the shared-memory copy of (d, s)
+          const double2 d = spd[kk];
+          const double sv = sps[kk];
+          const double dd = d.x * d.x + d.y * d.y, ss = sv * sv;
           const double r0 = rcp_pos(dd + mu0 * ss), r1 = rcp_pos(dd + mu1 * ss);
           X0 = cmul(X0, make_double2(d.x * r0, -d.y * r0));
           X1 = has1 ? cmul(X1, make_double2(d.x * r1, -d.y * r1)) : czero();
@@ -589,8 +631,9 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
         }
         nzb0 |= __double_as_longlong(X0.x) | __double_as_longlong(X0.y);
         nzb1 |= __double_as_longlong(X1.x) | __double_as_longlong(X1.y);
-        a = cmul(make_double2(X0.x - X1.y, -(X0.y + X1.x)), cs[kk]);
-        b = kk ? cmul(make_double2(X0.x + X1.y, X0.y - X1.x), cs[m - kk]) : czero();
+        const double2 ck = cs[kk];  // c_{m-kk} = -c_kk
+        a = cmul(make_double2(X0.x - X1.y, -(X0.y + X1.x)), ck);
+        b = kk ? cmul(make_double2(-(X0.x + X1.y), X1.x - X0.y), ck) : czero();
       };
       if constexpr (PS::FOLD) {
 #pragma unroll
@@ -672,7 +715,7 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
         const int p = threadIdx.x + t * NT;
         y0r[t] = y1r[t] = 0.0;
         if (p < m) {
-          const double2 z = cmul(x[pidx(p)], cs[p]);  // conj of (F^H v)_p sqrt(m)
+          const double2 z = cmul(x[pidx(p)], chirp(p));  // conj of (F^H v)_p sqrt(m)
           y0r[t] = z.x * s0;
           y1r[t] = z.y * s1;
         }
@@ -685,7 +728,7 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
         const int p = threadIdx.x + t * NT;
         if (p >= m) continue;
         const int e = kl + p;
-        const double tt = fma((double)e, ax.ho_ta, ax.ho_tb);
+        const double tt = fma((double)(t * NT), ax.ho_ta, tt0);
         lineA[e] = y0r[t] + p0(tt);
         lineB[e] = y1r[t] + p1(tt);
 #pragma unroll
@@ -712,7 +755,7 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
             p = ax.wrap[e];
           else if (p >= m)
             p = ax.wrap[kl + (p - m)];
-          const double2 z = cmul(x[pidx(p)], cs[p]);  // conj of (F^H v)_p sqrt(m)
+          const double2 z = cmul(x[pidx(p)], chirp(p));  // conj of (F^H v)_p sqrt(m)
           const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
           r0[c] = z.x * s0 + p0(t);
           r1[c] = z.y * s1 + p1(t);
@@ -728,7 +771,7 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
     } else
 #pragma unroll 4
     for (int p = threadIdx.x; p < m; p += NT) {
-      const double2 z = cmul(x[pidx(p)], cs[p]);  // conj of (F^H v)_p sqrt(m)
+      const double2 z = cmul(x[pidx(p)], chirp(p));  // conj of (F^H v)_p sqrt(m)
       const double y0 = z.x * s0, y1 = z.y * s1;
       const int e = kl + p;
       const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
