@@ -357,8 +357,11 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
       if constexpr (PS::FOLD) {
 #pragma unroll
         for (int t = 0; t < PS::JS; ++t) {
+          // branch-free (index clamped, result selected): the slots' loads
+          // and arithmetic interleave instead of running slot after slot
           const int j = threadIdx.x + t * NT;
-          vr[t] = j < m ? val(j, fma((double)(t * NT), ax.ho_ta, tt0)) : czero();
+          const double2 vj = val(j < m ? j : m - 1, fma((double)(t * NT), ax.ho_ta, tt0));
+          vr[t] = j < m ? vj : czero();
         }
       } else {
 #pragma unroll 4
@@ -425,27 +428,51 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
     // leave as two bulk stores; only the GCV weights take the store path
     constexpr int KSA = PS::FOLD ? (PS::HM / 2 + NT) / NT : 1;
     const bool tout = PS::FOLD && pair_out_staged(o0, o1, n, io.go.elem_stride) && (hk & 1);
+    // ... and so do the fp64 weight rows (staged in the area the synthesis
+    // kernel keeps its spectral table in); their TF32 tiles are then written
+    // chunk-wise from the staged rows: one lane per (16-byte chunk, line), so a
+    // store instruction touches 16 lines instead of the 32 that per-element
+    // 4-byte stores did (~2 clocks per line touched: 11 % of the kernel)
+    double* wA = reinterpret_cast<double*>(sm + pair_slots(M, m) + 8);
+    double* wB = wA + io.wstride;
+    const bool wst = tout && w0 && (io.wstride & 3) == 0 &&
+                     (reinterpret_cast<uintptr_t>(w0) & 15) == 0 &&
+                     2 * io.wstride <= 2 * (pair_cs_slots(m) + (pair_cs_slots(m) + 1) / 2);
     if (tout) {
       double2 X0r[KSA], X1r[KSA];
 #pragma unroll
       for (int t = 0; t < KSA; ++t) {
-        const int kk = threadIdx.x + t * NT;
-        X0r[t] = X1r[t] = czero();
-        if (kk > h) continue;
+        const int kq = threadIdx.x + t * NT;
+        const int kk = kq <= h ? kq : h;  // clamped: branch-free slots interleave
         const double2 ck = cs[kk];  // c_{m-kk} = -c_kk
         const double2 Zk = cmul(x[pidx(kk)], ck);
-        const double2 Zc = kk ? cmul(x[pidx(m - kk)], make_double2(-ck.x, -ck.y)) : Zk;
+        const double2 Zm = cmul(x[pidx(m - kk)], make_double2(-ck.x, -ck.y));
+        const double2 Zc = kk ? Zm : Zk;
         const double2 D = csub(Zk, cconj(Zc));
         const double2 X0 = z0 ? czero() : cscale(cadd(Zk, cconj(Zc)), 0.5 * isq);
         const double2 X1 = z1 ? czero() : make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
         X0r[t] = X0;
         X1r[t] = X1;
-        if (w0) {
+        if (w0 && kq <= h) {
           const double f = kk ? 2.0 : 1.0;  // |X_k|^2 + |X_{m-k}|^2
-          wset2(kl + kk, f * (X0.x * X0.x + X0.y * X0.y), f * (X1.x * X1.x + X1.y * X1.y));
+          const double v0 = f * (X0.x * X0.x + X0.y * X0.y), v1 = f * (X1.x * X1.x + X1.y * X1.y);
+          if (wst) {
+            wA[kl + kk] = v0;
+            wB[kl + kk] = v1;
+          } else {
+            wset2(kl + kk, v0, v1);
+          }
         }
       }
-      __syncthreads();  // every Z_k has been read
+      if (wst) {
+        if (threadIdx.x < hk) {
+          const int l = threadIdx.x, i = ho_wred(ax, l, h);
+          wA[i] = a0[l] * a0[l];
+          wB[i] = a1[l] * a1[l];
+        }
+        for (int i = (int)io.wn + threadIdx.x; i < (int)io.wstride; i += NT) wA[i] = wB[i] = 0.0;
+      }
+      __syncthreads();  // every Z_k has been read; the weight rows are complete
       double* lineA = reinterpret_cast<double*>(x);
       double* lineB = lineA + n;
 #pragma unroll
@@ -465,6 +492,24 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
         lineB[threadIdx.x] = a1[threadIdx.x];
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (wst && t32h) {
+        // task c: chunk c >> 1 (4 elements) of line l0 + (c & 1)
+        const int ntask = (int)(io.wstride >> 1);
+        for (int c = threadIdx.x; c < ntask; c += NT) {
+          const int row = c & 1, i = (c >> 1) * 4;
+          if (row && !has1) continue;
+          const double2* src = reinterpret_cast<const double2*>((row ? wB : wA) + i);
+          const double2 u0 = src[0], u1 = src[1];
+          float4 hi, lo;
+          tf32_split(u0.x, hi.x, lo.x);
+          tf32_split(u0.y, hi.y, lo.y);
+          tf32_split(u1.x, hi.z, lo.z);
+          tf32_split(u1.y, hi.w, lo.w);
+          const int eo = (i >> 5) * (kTcBM * 32) + ((i & 31) >> 2) * (kTcBM * 4) + row * 4;
+          *reinterpret_cast<float4*>(t32h + eo) = hi;
+          *reinterpret_cast<float4*>(t32l + eo) = lo;
+        }
+      }
     } else
     for (int kk = threadIdx.x; kk <= h; kk += NT) {
       const double2 ck = cs[kk];  // c_{m-kk} = -c_kk
@@ -495,14 +540,18 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
         o0[l] = a0[l];
         if (o1) o1[l] = a1[l];
       }
-      if (w0) wset2(ho_wred(ax, l, h), a0[l] * a0[l], a1[l] * a1[l]);
+      if (w0 && !wst) wset2(ho_wred(ax, l, h), a0[l] * a0[l], a1[l] * a1[l]);
     }
-    if (w0)
+    if (w0 && !wst)
       for (int i = (int)io.wn + threadIdx.x; i < (int)io.wstride; i += NT) wset2(i, 0.0, 0.0);
     __syncthreads();  // x is reused by the next pair
     if (tout && threadIdx.x == 0) {
       bulk_s2g(o0, x, (uint32_t)n * 8);
       if (o1) bulk_s2g(o1, reinterpret_cast<double*>(x) + n, (uint32_t)n * 8);
+      if (wst) {
+        bulk_s2g(w0, wA, (uint32_t)io.wstride * 8);
+        if (has1) bulk_s2g(w0 + io.wstride, wB, (uint32_t)io.wstride * 8);
+      }
       bulk_commit();
     }
     FD_PCLK(0, 8);
@@ -640,7 +689,7 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
         for (int t = 0; t < KS; ++t) {
           const int kk = threadIdx.x + t * NT;
           vk[t] = vc[t] = czero();
-          if (kk <= h) one(kk, t, vk[t], vc[t]);
+          if (kk <= h) one(kk, t, vk[t], vc[t]);  // (branch-free slots spill at 128 registers)
         }
       } else {
 #pragma unroll 2
@@ -711,14 +760,20 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
     if (tout) {
       double y0r[PSN], y1r[PSN];
 #pragma unroll
-      for (int t = 0; t < PSN; ++t) {
+      for (int t = 0; t < PSN; ++t) {  // branch-free: the slots interleave
         const int p = threadIdx.x + t * NT;
-        y0r[t] = y1r[t] = 0.0;
-        if (p < m) {
-          const double2 z = cmul(x[pidx(p)], chirp(p));  // conj of (F^H v)_p sqrt(m)
-          y0r[t] = z.x * s0;
-          y1r[t] = z.y * s1;
-        }
+        const int pc = p < m ? p : m - 1;
+        const double2 z = cmul(x[pidx(pc)], chirp(pc));  // conj of (F^H v)_p sqrt(m)
+        y0r[t] = z.x * s0;
+        y1r[t] = z.y * s1;
+      }
+      // border element bord[l] repeats the interior sample wrap[l] (thread l)
+      double yb0 = 0.0, yb1 = 0.0;
+      if (threadIdx.x < hk) {
+        const int pb = ax.wrap[threadIdx.x];
+        const double2 z = cmul(x[pidx(pb)], chirp(pb));
+        yb0 = z.x * s0;
+        yb1 = z.y * s1;
       }
       __syncthreads();  // every sample has been read
       double* lineA = reinterpret_cast<double*>(x);
@@ -726,19 +781,18 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
 #pragma unroll
       for (int t = 0; t < PSN; ++t) {
         const int p = threadIdx.x + t * NT;
-        if (p >= m) continue;
-        const int e = kl + p;
         const double tt = fma((double)(t * NT), ax.ho_ta, tt0);
-        lineA[e] = y0r[t] + p0(tt);
-        lineB[e] = y1r[t] + p1(tt);
-#pragma unroll
-        for (int l = 0; l < kHoMax; ++l)
-          if (l < hk && ax.wrap[l] == p) {
-            const int eb = ax.bord[l];
-            const double tb = fma((double)eb, ax.ho_ta, ax.ho_tb);
-            lineA[eb] = y0r[t] + p0(tb);
-            lineB[eb] = y1r[t] + p1(tb);
-          }
+        const double r0 = y0r[t] + p0(tt), r1 = y1r[t] + p1(tt);
+        if (p < m) {
+          lineA[kl + p] = r0;
+          lineB[kl + p] = r1;
+        }
+      }
+      if (threadIdx.x < hk) {
+        const int eb = ax.bord[threadIdx.x];
+        const double tb = fma((double)eb, ax.ho_ta, ax.ho_tb);
+        lineA[eb] = yb0 + p0(tb);
+        lineB[eb] = yb1 + p1(tb);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     } else if (vec) {
