@@ -102,48 +102,57 @@ __device__ __forceinline__ void bluestein_rec_clk(double2* x, const double2* bha
 // passes (FASTDEBLUR_PAIR_SKEW), to start the two groups out of phase
 __device__ int g_pair_skew = 1200;
 
-template <int LOGM, int NT, int KERN = 0>
-__device__ __forceinline__ void pair_conv(double2* x, const FftTables& T, const TwSm& tw, int m,
-                                          long long& pclk_) {
+// the folded convolution's last step: lower half += conj(W^k) upper half, k < m
+template <int LOGM, int NT>
+__device__ __forceinline__ void pair_combine(double2* x, const TwSm& tw, int m) {
   using S = PairShape<LOGM>;
-#ifdef FD_PHASE_CLOCKS
-  if constexpr (LOGM == 13) {
-    constexpr int GRPC = (NT == S::M / 16) ? NT / 2 : 0;
-    if constexpr (GRPC != 0) {
-      if (threadIdx.x >= GRPC) {
-        const long long t0 = clock64();
-        const int skew = g_pair_skew;
-        while (clock64() - t0 < skew) {}
-      }
-    }
-    bluestein_rec_clk<LOGM, 1, S::HM, NT, KERN, 2, GRPC>(x, T.bhat, tw, S::M, pclk_);
-    if constexpr (GRPC != 0) __syncthreads();
-    const FoldTw<LOGM> ft(tw, threadIdx.x);
-    for (int k = threadIdx.x; k < m; k += NT)
-      x[pidx(k)] = cadd(x[pidx(k)], cmulc(x[pidx(k + S::HM)], ft(k)));
-    __syncthreads();
-    FD_PCLK(KERN, 7);
-    return;
+  const FoldTw<LOGM> ft(tw, threadIdx.x);
+  constexpr int JS = (S::HM + NT - 1) / NT;
+#pragma unroll
+  for (int t = 0; t < JS; ++t) {  // clamped, branch-free: the slots' loads batch
+    const int k = threadIdx.x + t * NT;
+    const int kc = k < m ? k : m - 1;
+    const double2 r = cadd(x[pidx(kc)], cmulc(x[pidx(kc + S::HM)], ft(kc)));
+    if (k < m) x[pidx(k)] = r;
   }
-#endif
+  __syncthreads();
+}
+
+// SKEW: what the upper half's thread group does before its passes while the
+// lower half's group starts -- work worth ~1200 SM clocks (deferred stores of
+// the previous pair), or a spin of g_pair_skew clocks
+struct SkewSpin {
+  __device__ __forceinline__ void operator()() const {
+    const long long t0 = clock64();
+    const int skew = g_pair_skew;
+    while (clock64() - t0 < skew) {}
+  }
+};
+
+template <int LOGM, int NT, int KERN = 0, class SKEW = SkewSpin>
+__device__ __forceinline__ void pair_conv(double2* x, const FftTables& T, const TwSm& tw, int m,
+                                          long long& pclk_, SKEW skew = SKEW()) {
+  using S = PairShape<LOGM>;
   if constexpr (S::FOLD) {
     static_assert(NT % (1 << FoldTw<LOGM>::LOB) == 0, "FoldTw needs NT % lo length == 0");
     // NT == M/16: threads [0, NT/2) own the lower half's items in every pass,
     // [NT/2, NT) the upper half's -- the halves synchronise separately
     constexpr int GRP = (NT == S::M / 16 && NT >= 64) ? NT / 2 : 0;
     if constexpr (GRP != 0) {
-      if (threadIdx.x >= GRP) {
-        const long long t0 = clock64();
-        const int skew = g_pair_skew;
-        while (clock64() - t0 < skew) {}
-      }
+      if (threadIdx.x >= GRP) skew();
     }
+#ifdef FD_PHASE_CLOCKS
+    if constexpr (LOGM == 13) {
+      bluestein_rec_clk<LOGM, 1, S::HM, NT, KERN, 2, GRP>(x, T.bhat, tw, S::M, pclk_);
+      if constexpr (GRP != 0) __syncthreads();
+      pair_combine<LOGM, NT>(x, tw, m);
+      FD_PCLK(KERN, 7);
+      return;
+    }
+#endif
     bluestein_rec<LOGM, 1, S::HM, NT, false, GRP>(x, T.bhat, tw, S::M);
     if constexpr (GRP != 0) __syncthreads();
-    const FoldTw<LOGM> ft(tw, threadIdx.x);
-    for (int k = threadIdx.x; k < m; k += NT)
-      x[pidx(k)] = cadd(x[pidx(k)], cmulc(x[pidx(k + S::HM)], ft(k)));
-    __syncthreads();
+    pair_combine<LOGM, NT>(x, tw, m);
   } else {
     bluestein_t<LOGM, NT>(x, T, tw, m);
   }
@@ -325,6 +334,32 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
 #else
   long long pclk_ = 0;
 #endif
+  // TF32 tiles of a pair's weight rows, from the rows staged in shared memory
+  // (wA, wB below): task c = chunk c >> 1 (4 elements) of line l0 + (c & 1)
+  using PSK = PairShape<LOGM, WIDE>;
+  constexpr int GRPK = (PSK::FOLD && NT == M / 16 && NT >= 64) ? NT / 2 : 0;  // pair_conv's groups
+  auto tf32_rows = [&](int l0p, int first, int step, int c0, int c1) {
+    const double* wa = reinterpret_cast<const double*>(sm + pair_slots(M, m) + 8);
+    const double* wb = wa + io.wstride;
+    float* th = io.wout32 + tc_tile_index(l0p, 0, kTcBM, nkb32);
+    float* tl = io.wout32lo + tc_tile_index(l0p, 0, kTcBM, nkb32);
+    const bool two = l0p + 1 < count;
+    for (int c = c0 + first; c < c1; c += step) {
+      const int row = c & 1, i = (c >> 1) * 4;
+      if (row && !two) continue;
+      const double2* src = reinterpret_cast<const double2*>((row ? wb : wa) + i);
+      const double2 u0 = src[0], u1 = src[1];
+      float4 hi, lo;
+      tf32_split(u0.x, hi.x, lo.x);
+      tf32_split(u0.y, hi.y, lo.y);
+      tf32_split(u1.x, hi.z, lo.z);
+      tf32_split(u1.y, hi.w, lo.w);
+      const int eo = (i >> 5) * (kTcBM * 32) + ((i & 31) >> 2) * (kTcBM * 4) + row * 4;
+      *reinterpret_cast<float4*>(th + eo) = hi;
+      *reinterpret_cast<float4*>(tl + eo) = lo;
+    }
+  };
+  int tf_l0 = -1;  // pair whose tiles are still to be written
   for (int q = blockIdx.x, it = 0; q < npairs; q += gridDim.x, ++it) {
     const int l0 = 2 * q;
     const bool has1 = l0 + 1 < count;
@@ -393,7 +428,15 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
       __syncthreads();
       FD_PCLK(0, 1);
     }
-    pair_conv<LOGM, NT, 0>(x, T, tw, m, pclk_);
+    pair_conv<LOGM, NT, 0>(x, T, tw, m, pclk_, [&] {
+      if (tf_l0 >= 0) {
+        const int ntask = (int)(io.wstride >> 1);
+        tf32_rows(tf_l0, (int)threadIdx.x - GRPK, GRPK, (ntask / 2) & ~1, ntask);
+      } else {
+        SkewSpin()();
+      }
+    });
+    tf_l0 = -1;
     // the post phase reads [0, m) only: stage the next pair behind it
     if (threadIdx.x == 0) pair_issue(stg, io.in, io.gi, q + gridDim.x, n);
 
@@ -493,22 +536,13 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       if (wst && t32h) {
-        // task c: chunk c >> 1 (4 elements) of line l0 + (c & 1)
+        // with thread groups, the upper group writes the second half of the
+        // tiles in the next pair's skew slot (~1200 clocks of store work
+        // instead of a spin)
         const int ntask = (int)(io.wstride >> 1);
-        for (int c = threadIdx.x; c < ntask; c += NT) {
-          const int row = c & 1, i = (c >> 1) * 4;
-          if (row && !has1) continue;
-          const double2* src = reinterpret_cast<const double2*>((row ? wB : wA) + i);
-          const double2 u0 = src[0], u1 = src[1];
-          float4 hi, lo;
-          tf32_split(u0.x, hi.x, lo.x);
-          tf32_split(u0.y, hi.y, lo.y);
-          tf32_split(u1.x, hi.z, lo.z);
-          tf32_split(u1.y, hi.w, lo.w);
-          const int eo = (i >> 5) * (kTcBM * 32) + ((i & 31) >> 2) * (kTcBM * 4) + row * 4;
-          *reinterpret_cast<float4*>(t32h + eo) = hi;
-          *reinterpret_cast<float4*>(t32l + eo) = lo;
-        }
+        const int nnow = GRPK != 0 ? (ntask / 2) & ~1 : ntask;
+        tf32_rows(l0, threadIdx.x, NT, 0, nnow);
+        if constexpr (GRPK != 0) tf_l0 = l0;
       }
     } else
     for (int kk = threadIdx.x; kk <= h; kk += NT) {
@@ -555,6 +589,10 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
       bulk_commit();
     }
     FD_PCLK(0, 8);
+  }
+  if (tf_l0 >= 0) {  // the last pair's deferred tiles
+    const int ntask = (int)(io.wstride >> 1);
+    tf32_rows(tf_l0, threadIdx.x, NT, (ntask / 2) & ~1, ntask);
   }
   if (threadIdx.x == 0) bulk_wait_read();  // shared memory stays valid until the last lines are read
 }
