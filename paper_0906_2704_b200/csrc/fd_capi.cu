@@ -28,6 +28,7 @@
 #include "fd_kernels.cuh"
 #include "fd_pair.cuh"
 #include "fd_mixed.cuh"
+#include "fd_mixed_staged.cuh"
 #include "fd_rader.cuh"
 #include "fd_gen.cuh"
 #include "fd_cdirect.cuh"
@@ -227,6 +228,8 @@ void init_runtime_once() {
       cudaMemcpyToSymbol(c_mix_sin, sn, sizeof(sn));
       cudaFuncSetAttribute(k_manalyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
       cudaFuncSetAttribute(k_msynth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+      cudaFuncSetAttribute(k_manalyze_s, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
+      cudaFuncSetAttribute(k_msynth_s, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
       cudaFuncSetAttribute(k_qanalyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
       cudaFuncSetAttribute(k_qsynth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
       cudaFuncSetAttribute(k_canalyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
@@ -406,11 +409,45 @@ void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaS
     return;
   }
   if (ax.mstages > 0) {  // direct mixed-radix DFT (fd_mixed.cuh)
-    const size_t sm = mix_smem_bytes(ax.m);
+    // FASTDEBLUR_MIXED_STAGED=1: the one-CTA-per-SM staged kernels
+    // (fd_mixed_staged.cuh) -- measured slower than two CTAs per SM (k_manalyze
+    // 3.3 vs 2.2 ms: the stages' uneven item counts idle a lone CTA at every
+    // barrier), kept for A/B timing
+    static const bool staged_on = [] {
+      const char* e = std::getenv("FASTDEBLUR_MIXED_STAGED");
+      return e && e[0] == '1';
+    }();
+    auto contiguous = [&](const Lines& g, const void* p) {
+      return g.elem_stride == 1 && g.per_item == 1 && g.item_stride == ax.n &&
+             (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+    };
+    const size_t sms = mixs_smem_bytes(ax.m, ax.n, io.wout ? io.wstride : 0);
+    const bool staged =
+        staged_on && mixs_shape_ok(ax.m, ax.n, ax.mrad[0]) && sms <= 227 * 1024 &&
+        contiguous(io.gi, io.in) && contiguous(io.go, io.out) && !io.in_f32 && !io.out_f32 &&
+        (!io.wout || ((io.wstride & 31) == 0 && (reinterpret_cast<uintptr_t>(io.wout) & 15) == 0 &&
+                      (!io.wout32 || ((reinterpret_cast<uintptr_t>(io.wout32) & 15) == 0 &&
+                                      (reinterpret_cast<uintptr_t>(io.wout32lo) & 15) == 0)))) &&
+        (!sa || sa->mode == 0 || (sa->mode == 1 && sa->sp.mode == 1 && ax.cplx));
+    if (staged) {
+      const int grid = std::max(1, std::min(pairs, num_sms()));
+      if (sa) {
+        k_msynth_s<<<grid, kMixSNT, sms, st>>>(ax, io, *sa);
+      } else {
+        k_manalyze_s<<<grid, kMixSNT, sms, st>>>(ax, io);
+      }
+      launched(sa ? "k_msynth" : "k_manalyze");
+      return;
+    }
+    // the analysis stages the pair's GCV weight rows when two CTAs still fit an SM
+    int wslots = 0;
+    if (!sa && io.wout && 2 * (mix_smem_bytes(ax.m, ax.n, io.wstride) + 1024) <= 227 * 1024)
+      wslots = (int)io.wstride;
+    const size_t sm = mix_smem_bytes(ax.m, ax.n, wslots);
     if (sa) {
       k_msynth<<<persistent_grid(k_msynth, kMixNT, sm, pairs), kMixNT, sm, st>>>(ax, io, *sa);
     } else {
-      k_manalyze<<<persistent_grid(k_manalyze, kMixNT, sm, pairs), kMixNT, sm, st>>>(ax, io);
+      k_manalyze<<<persistent_grid(k_manalyze, kMixNT, sm, pairs), kMixNT, sm, st>>>(ax, io, wslots);
     }
     launched(sa ? "k_msynth" : "k_manalyze");
     return;
@@ -747,7 +784,7 @@ void build_mixed_plan(Axis& A, int m) {
   d.mstages = 0;
   d.rader = 0;
   if (!mixed_enabled() || m < 9 || !(m & 1)) return;
-  if (mix_smem_bytes(m) > 226 * 1024) return;  // the DFT buffer must fit one CTA's shared memory
+  if (mix_smem_bytes(m, m + 4, 0) > 226 * 1024) return;  // the DFT buffer must fit one CTA's shared memory
   const std::vector<int> rad = mixed_radices(m, {13, 11, 9, 7, 5, 3});
   if (!rad.empty()) {
     upload_plan(A, m, rad, nullptr);

@@ -169,32 +169,51 @@ __device__ __forceinline__ void mix_prefetch_pair(const void* base, const Lines&
   }
 }
 
-// smem: DFT buffer (m complex), twiddle hi / lo tables, output permutation,
-// the two zero-line flag words (zf_add / zf_take)
-__host__ __device__ __forceinline__ size_t mix_smem_bytes(int m) {
-  return (size_t)m * 16 + (size_t)(64 + ((m + 63) >> 6)) * 16 + (size_t)m * 4 + 8;
+// smem (double2 slots): DFT buffer (max(m + 1, n): the two output lines of n
+// doubles are assembled in it) | twiddle lo (64), hi | weight rows of the pair
+// (wslots = wstride of the analysis with GCV weights, else 0) | output
+// permutation (u16) | the two zero-line flag words (zf_add / zf_take)
+constexpr int kMixK = 8;   // Hermitian slots per thread of the staged-output path: h + 1 <= 8 NT
+constexpr int kMixP = 16;  // sample slots per thread: m <= 16 NT
+__host__ __device__ __forceinline__ int mix_x_slots(int m, int n) { return m + 1 > n ? m + 1 : n; }
+__host__ __device__ __forceinline__ size_t mix_smem_bytes(int m, int n, long long wslots) {
+  return ((size_t)mix_x_slots(m, n) + 64 + ((m + 63) >> 6) + (size_t)wslots + (m + 7) / 8 + 1) * 16;
 }
+struct MixLay {
+  MixTw tw;
+  double* wrows;
+  const unsigned short* perm;
+  int* zf;
+};
 // twiddle tables and permutation into shared memory (before the first barrier)
-__device__ __forceinline__ MixTw mix_setup(double2* sm, const AxisDev& ax, const int** perm) {
+__device__ __forceinline__ MixLay mix_setup(double2* sm, const AxisDev& ax, long long wslots) {
   const int m = ax.m, nhi = (m + 63) >> 6;
-  double2* lo = sm + m;
+  double2* lo = sm + mix_x_slots(m, ax.n);
   double2* hi = lo + 64;
-  int* ps = reinterpret_cast<int*>(hi + nhi);
+  double2* wr = hi + nhi;
+  unsigned short* ps = reinterpret_cast<unsigned short*>(wr + wslots);
+  int* zf = reinterpret_cast<int*>(reinterpret_cast<double2*>(ps) + (m + 7) / 8);
   for (int i = threadIdx.x; i < 64; i += blockDim.x) lo[i] = i < m ? ax.mtw[i] : czero();
   for (int i = threadIdx.x; i < nhi; i += blockDim.x) hi[i] = ax.mtw[i << 6];
-  for (int i = threadIdx.x; i < m; i += blockDim.x) ps[i] = ax.mperm[i];
-  if (threadIdx.x < 2) ps[m + threadIdx.x] = 0;  // zero-line flags
-  *perm = ps;
-  return MixTw{lo, hi};
+  for (int i = threadIdx.x; i < m; i += blockDim.x) ps[i] = (unsigned short)ax.mperm[i];
+  if (threadIdx.x < 2) zf[threadIdx.x] = 0;  // zero-line flags
+  return MixLay{MixTw{lo, hi}, reinterpret_cast<double*>(wr), ps, zf};
+}
+// the output lines can be assembled in the buffer and bulk-stored
+__device__ __forceinline__ bool mix_out_staged(const AxisDev& ax, const double* o0,
+                                               const double* o1, long long eso) {
+  return pair_out_staged(o0, o1, ax.n, eso) && (ax.m - 1) / 2 < kMixK * kMixNT &&
+         ax.m <= kMixP * kMixNT;
 }
 
 // analyze, two real lines per direct DFT (see k_panalyze)
-__global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
+__global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io, int wslots) {
   extern __shared__ double2 sm[];
   const int m = ax.m, n = ax.n, kl = ax.kl, hk = ax.hk, h = (m - 1) / 2;
   double2* x = sm;
-  const int* perm = nullptr;
-  const MixTw tw = mix_setup(sm, ax, &perm);
+  const MixLay lay = mix_setup(sm, ax, wslots);
+  const MixTw tw = lay.tw;
+  const unsigned short* perm = lay.perm;
   __syncthreads();
   const int count = io.gi.count, npairs = (count + 1) / 2;
   const double* in = reinterpret_cast<const double*>(io.in);
@@ -202,19 +221,26 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
   const long long es = io.gi.elem_stride;
   const double isq = ax.inv_sqrt_m;
   const long long nkb32 = io.wstride >> 5;
-  int* zf = const_cast<int*>(perm) + m;
+  int* zf = lay.zf;
+  double* wA = lay.wrows;
+  double* wB = wA + io.wstride;
   for (int q = blockIdx.x, it = 0; q < npairs; q += gridDim.x, ++it) {
     const int l0 = 2 * q;
     const bool has1 = l0 + 1 < count;
     const double* g0 = in + line_offset(io.gi, l0);
     const double* g1 = has1 ? in + line_offset(io.gi, l0 + 1) : g0;
-    auto ld0 = [&](int e) { return __ldg(g0 + e * es); };
-    auto ld1 = [&](int e) { return has1 ? __ldg(g1 + e * es) : 0.0; };
+    // streaming loads (the pair was prefetched into L2; nothing re-reads it)
+    auto ld0 = [&](int e) { return __ldcs(g0 + e * es); };
+    auto ld1 = [&](int e) { return has1 ? __ldcs(g1 + e * es) : 0.0; };
     double a0[kHoMax], a1[kHoMax];
     ho_amps_real(ax, ld0, a0);
     ho_amps_real(ax, ld1, a1);
     const Cubic p0 = ho_cubic(ax, a0), p1 = ho_cubic(ax, a1);
     long long nzb0 = 0, nzb1 = 0;  // OR of the bit patterns of line 0 / 1 (-0.0 counts as nonzero)
+    // the previous pair's output lines must have left x (and the weight rows);
+    // the SM's other CTA computes meanwhile
+    if (threadIdx.x == 0) bulk_wait_read();
+    __syncthreads();
     mix_dft<true>(x, ax, tw, kMixNT, [&](int j) {
       const int e = kl + j;
       const double t = fma((double)e, ax.ho_ta, ax.ho_tb);
@@ -223,7 +249,7 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
       nzb1 |= __double_as_longlong(y1);
       return make_double2(y0 - p0(t), y1 - p1(t));
     }, [&] { zf_add(zf, it, (nzb0 != 0 ? 1 : 0) | (nzb1 != 0 ? 2 : 0)); });
-    // the next pair into L2 while the outputs stream out (written evict-first)
+    // the next pair into L2 while the outputs stream out
     mix_prefetch_pair(io.in, io.gi, q + gridDim.x, n);
 
     double* o0 = out + line_offset(io.go, l0);
@@ -234,6 +260,12 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
     // round-off would otherwise leak into it through the Hermitian split)
     const int nz = zf_take(zf, it);
     const bool z0 = !(nz & 1) && ho_zero(a0), z1 = !(nz & 2) && ho_zero(a1);
+    // Staged output (see k_panalyze): the packed coefficient lines are
+    // assembled in x and the weight rows in their staging area, both leave by
+    // bulk stores; the TF32 tiles are written chunk-wise from the staged rows
+    const bool tout = mix_out_staged(ax, o0, o1, io.go.elem_stride) && (hk & 1);
+    const bool wst = tout && w0 && wslots >= io.wstride && (io.wstride & 3) == 0 &&
+                     (reinterpret_cast<uintptr_t>(w0) & 15) == 0;
     auto wset = [&](int line, double* wl, long long i, double v) {
       wl[i] = v;
       if (io.wout32) {
@@ -244,73 +276,185 @@ __global__ void __launch_bounds__(kMixNT, 2) k_manalyze(AxisDev ax, LineIO io) {
         io.wout32lo[t] = lo;
       }
     };
-    for (int kk = threadIdx.x; kk <= h; kk += kMixNT) {
-      const double2 Zk = x[perm[kk]];
-      const double2 Zc = kk ? x[perm[m - kk]] : Zk;
-      const double2 D = csub(Zk, cconj(Zc));
-      const double2 X0 = z0 ? czero() : cscale(cadd(Zk, cconj(Zc)), 0.5 * isq);
-      const double2 X1 = z1 ? czero() : make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
-      if (kk == 0) {
-        __stcs(o0 + hk, X0.x);
-        if (o1) __stcs(o1 + hk, X1.x);
-      } else {
-        __stcs(o0 + hk + 2 * kk - 1, X0.x);
-        __stcs(o0 + hk + 2 * kk, X0.y);
-        if (o1) {
-          __stcs(o1 + hk + 2 * kk - 1, X1.x);
-          __stcs(o1 + hk + 2 * kk, X1.y);
+    if (tout) {
+      double2 X0r[kMixK], X1r[kMixK];
+#pragma unroll
+      for (int t = 0; t < kMixK; ++t) {
+        const int kq = threadIdx.x + t * kMixNT;
+        const int kk = kq <= h ? kq : h;  // clamped: branch-free slots interleave
+        const double2 Zk = x[perm[kk]];
+        const double2 Zm = x[perm[kk ? m - kk : 0]];
+        const double2 Zc = kk ? Zm : Zk;
+        const double2 D = csub(Zk, cconj(Zc));
+        const double2 X0 = z0 ? czero() : cscale(cadd(Zk, cconj(Zc)), 0.5 * isq);
+        const double2 X1 = z1 ? czero() : make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
+        X0r[t] = X0;
+        X1r[t] = X1;
+        if (w0 && kq <= h) {
+          const double f = kk ? 2.0 : 1.0;  // |X_k|^2 + |X_{m-k}|^2
+          const double v0 = f * (X0.x * X0.x + X0.y * X0.y), v1 = f * (X1.x * X1.x + X1.y * X1.y);
+          if (wst) {
+            wA[kl + kk] = v0;
+            wB[kl + kk] = v1;
+          } else {
+            wset(l0, w0, kl + kk, v0);
+            if (w1) wset(l0 + 1, w1, kl + kk, v1);
+          }
         }
       }
-      if (w0) {
-        const double f = kk ? 2.0 : 1.0;
-        wset(l0, w0, kl + kk, f * (X0.x * X0.x + X0.y * X0.y));
-        if (w1) wset(l0 + 1, w1, kl + kk, f * (X1.x * X1.x + X1.y * X1.y));
+      if (wst) {
+        if (threadIdx.x < hk) {
+          const int l = threadIdx.x, i = ho_wred(ax, l, h);
+          wA[i] = a0[l] * a0[l];
+          wB[i] = a1[l] * a1[l];
+        }
+        for (int i = (int)io.wn + threadIdx.x; i < (int)io.wstride; i += kMixNT) wA[i] = wB[i] = 0.0;
+      }
+      __syncthreads();  // every Z_k has been read; the weight rows are complete
+      double* lineA = reinterpret_cast<double*>(x);
+      double* lineB = lineA + n;
+#pragma unroll
+      for (int t = 0; t < kMixK; ++t) {
+        const int kk = threadIdx.x + t * kMixNT;
+        if (kk > h) continue;
+        if (kk == 0) {
+          lineA[hk] = X0r[t].x;
+          lineB[hk] = X1r[t].x;
+        } else {  // hk odd: (Re, Im) 16-byte aligned
+          *reinterpret_cast<double2*>(lineA + hk + 2 * kk - 1) = X0r[t];
+          *reinterpret_cast<double2*>(lineB + hk + 2 * kk - 1) = X1r[t];
+        }
+      }
+      if (threadIdx.x < hk) {
+        lineA[threadIdx.x] = a0[threadIdx.x];
+        lineB[threadIdx.x] = a1[threadIdx.x];
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (wst && io.wout32) {  // task c: chunk c >> 1 (4 elements) of line l0 + (c & 1)
+        float* th = io.wout32 + tc_tile_index(l0, 0, kTcBM, nkb32);
+        float* tl = io.wout32lo + tc_tile_index(l0, 0, kTcBM, nkb32);
+        const int ntask = (int)(io.wstride >> 1);
+        for (int c = threadIdx.x; c < ntask; c += kMixNT) {
+          const int row = c & 1, i = (c >> 1) * 4;
+          if (row && !has1) continue;
+          const double2* src = reinterpret_cast<const double2*>((row ? wB : wA) + i);
+          const double2 u0 = src[0], u1 = src[1];
+          float4 hi, lo;
+          tf32_split(u0.x, hi.x, lo.x);
+          tf32_split(u0.y, hi.y, lo.y);
+          tf32_split(u1.x, hi.z, lo.z);
+          tf32_split(u1.y, hi.w, lo.w);
+          const int eo = (i >> 5) * (kTcBM * 32) + ((i & 31) >> 2) * (kTcBM * 4) + row * 4;
+          *reinterpret_cast<float4*>(th + eo) = hi;
+          *reinterpret_cast<float4*>(tl + eo) = lo;
+        }
+      }
+    } else {
+      for (int kk = threadIdx.x; kk <= h; kk += kMixNT) {
+        const double2 Zk = x[perm[kk]];
+        const double2 Zc = kk ? x[perm[m - kk]] : Zk;
+        const double2 D = csub(Zk, cconj(Zc));
+        const double2 X0 = z0 ? czero() : cscale(cadd(Zk, cconj(Zc)), 0.5 * isq);
+        const double2 X1 = z1 ? czero() : make_double2(0.5 * isq * D.y, -0.5 * isq * D.x);
+        if (kk == 0) {
+          __stcs(o0 + hk, X0.x);
+          if (o1) __stcs(o1 + hk, X1.x);
+        } else {
+          __stcs(o0 + hk + 2 * kk - 1, X0.x);
+          __stcs(o0 + hk + 2 * kk, X0.y);
+          if (o1) {
+            __stcs(o1 + hk + 2 * kk - 1, X1.x);
+            __stcs(o1 + hk + 2 * kk, X1.y);
+          }
+        }
+        if (w0) {
+          const double f = kk ? 2.0 : 1.0;
+          wset(l0, w0, kl + kk, f * (X0.x * X0.x + X0.y * X0.y));
+          if (w1) wset(l0 + 1, w1, kl + kk, f * (X1.x * X1.x + X1.y * X1.y));
+        }
       }
     }
     if (threadIdx.x < hk) {
       const int l = threadIdx.x;
-      o0[l] = a0[l];
-      if (o1) o1[l] = a1[l];
-      if (w0) {
+      if (!tout) {
+        o0[l] = a0[l];
+        if (o1) o1[l] = a1[l];
+      }
+      if (w0 && !wst) {
         wset(l0, w0, ho_wred(ax, l, h), a0[l] * a0[l]);
         if (w1) wset(l0 + 1, w1, ho_wred(ax, l, h), a1[l] * a1[l]);
       }
     }
-    if (w0)
+    if (w0 && !wst)
       for (long long i = io.wn + threadIdx.x; i < io.wstride; i += kMixNT) {
         wset(l0, w0, i, 0.0);
         if (w1) wset(l0 + 1, w1, i, 0.0);
       }
     __syncthreads();
+    if (tout && threadIdx.x == 0) {
+      bulk_s2g(o0, x, (uint32_t)n * 8);
+      if (o1) bulk_s2g(o1, reinterpret_cast<double*>(x) + n, (uint32_t)n * 8);
+      if (wst) {
+        bulk_s2g(w0, wA, (uint32_t)io.wstride * 8);
+        if (has1) bulk_s2g(w0 + io.wstride, wB, (uint32_t)io.wstride * 8);
+      }
+      bulk_commit();
+    }
   }
+  if (threadIdx.x == 0) bulk_wait_read();  // shared memory stays valid until the last lines are read
 }
 
 // synthesis with the filter fused, two lines per direct DFT (see k_psynth)
 __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, SynthArgs sa) {
   extern __shared__ double2 sm[];
-  const int m = ax.m, kl = ax.kl, hk = ax.hk, h = (m - 1) / 2;
+  const int m = ax.m, n = ax.n, kl = ax.kl, hk = ax.hk, h = (m - 1) / 2;
   double2* x = sm;
-  const int* perm = nullptr;
-  const MixTw tw = mix_setup(sm, ax, &perm);
+  const MixLay lay = mix_setup(sm, ax, 0);
+  const MixTw tw = lay.tw;
+  const unsigned short* perm = lay.perm;
   __syncthreads();
   const int count = io.gi.count, npairs = (count + 1) / 2;
   const double* in = reinterpret_cast<const double*>(io.in);
   double* out = reinterpret_cast<double*>(io.out);
   const double isq = ax.inv_sqrt_m;
-  int* zf = const_cast<int*>(perm) + m;
+  int* zf = lay.zf;
+  const double tt0 = fma((double)(kl + (int)threadIdx.x), ax.ho_ta, ax.ho_tb);
+  auto pair_mu = [&](int q, double& m0, double& m1) {  // read one pair ahead
+    m0 = m1 = 0.0;
+    if (q < npairs) {
+      m0 = line_mu(sa, io.gi, 2 * q);
+      m1 = 2 * q + 1 < count ? line_mu(sa, io.gi, 2 * q + 1) : m0;
+    }
+  };
+  double mu0n, mu1n;
+  pair_mu(blockIdx.x, mu0n, mu1n);
   for (int q = blockIdx.x, it = 0; q < npairs; q += gridDim.x, ++it) {
     const int l0 = 2 * q;
     const bool has1 = l0 + 1 < count;
     const double* g0 = in + line_offset(io.gi, l0);
     const double* g1 = has1 ? in + line_offset(io.gi, l0 + 1) : g0;
-    const double mu0 = line_mu(sa, io.gi, l0);
-    const double mu1 = has1 ? line_mu(sa, io.gi, l0 + 1) : mu0;
+    const double mu0 = mu0n, mu1 = mu1n;
+    pair_mu(q + gridDim.x, mu0n, mu1n);
     auto f0 = [&](int e, double2 c) { return coeff_filter_fast(ax, sa, io.gi, l0, e, c, mu0); };
     auto f1 = [&](int e, double2 c) {
       return has1 ? coeff_filter_fast(ax, sa, io.gi, l0 + 1, e, c, mu1) : czero();
     };
-    auto ld0 = [&](int i) { return __ldg(g0 + i); };
-    auto ld1 = [&](int i) { return has1 ? __ldg(g1 + i) : 0.0; };
+    // streaming loads: the pair was prefetched into L2 and is read once, so
+    // L1 keeps the filter's spectral table
+    auto ld0 = [&](int i) { return __ldcs(g0 + i); };
+    auto ld1 = [&](int i) { return has1 ? __ldcs(g1 + i) : 0.0; };
+    // (Re, Im) of coefficient kk >= 1 at [hk + 2 kk - 1]: one 16-byte load when aligned
+    const bool v2 = (hk & 1) && ((reinterpret_cast<uintptr_t>(g0) | reinterpret_cast<uintptr_t>(g1)) & 15) == 0;
+    auto ldp0 = [&](int i) {
+      return v2 ? __ldcs(reinterpret_cast<const double2*>(g0 + i)) : make_double2(ld0(i), ld0(i + 1));
+    };
+    auto ldp1 = [&](int i) {
+      if (!has1) return czero();
+      return v2 ? __ldcs(reinterpret_cast<const double2*>(g1 + i)) : make_double2(ld1(i), ld1(i + 1));
+    };
+    // the previous pair's output lines must have left x
+    if (threadIdx.x == 0) bulk_wait_read();
+    __syncthreads();
     double ua0[kHoMax], ua1[kHoMax];
 #pragma unroll
     for (int l = 0; l < kHoMax; ++l) {
@@ -326,8 +470,8 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
         X0 = make_double2(ld0(hk), 0.0);
         X1 = make_double2(ld1(hk), 0.0);
       } else {
-        X0 = make_double2(ld0(hk + 2 * kk - 1), ld0(hk + 2 * kk));
-        X1 = make_double2(ld1(hk + 2 * kk - 1), ld1(hk + 2 * kk));
+        X0 = ldp0(hk + 2 * kk - 1);
+        X1 = ldp1(hk + 2 * kk - 1);
       }
       X0 = f0(e, X0);
       X1 = f1(e, X1);
@@ -348,6 +492,44 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
     double* o1 = has1 ? out + line_offset(io.go, l0 + 1) : nullptr;
     const int nz = zf_take(zf, it);
     const double s0 = (nz & 1) ? isq : 0.0, s1 = (nz & 2) ? -isq : 0.0;
+    const bool tout = mix_out_staged(ax, o0, o1, eso);
+    if (tout) {  // lines assembled in x, two bulk stores (see k_psynth)
+      double y0r[kMixP], y1r[kMixP];
+#pragma unroll
+      for (int t = 0; t < kMixP; ++t) {  // branch-free: the slots interleave
+        const int p = threadIdx.x + t * kMixNT;
+        const double2 z = x[perm[p < m ? p : m - 1]];
+        y0r[t] = z.x * s0;
+        y1r[t] = z.y * s1;
+      }
+      // border element bord[l] repeats the interior sample wrap[l] (thread l)
+      double yb0 = 0.0, yb1 = 0.0;
+      if (threadIdx.x < hk) {
+        const double2 z = x[perm[ax.wrap[threadIdx.x]]];
+        yb0 = z.x * s0;
+        yb1 = z.y * s1;
+      }
+      __syncthreads();  // every sample has been read
+      double* lineA = reinterpret_cast<double*>(x);
+      double* lineB = lineA + n;
+#pragma unroll
+      for (int t = 0; t < kMixP; ++t) {
+        const int p = threadIdx.x + t * kMixNT;
+        const double tt = fma((double)(t * kMixNT), ax.ho_ta, tt0);
+        const double r0 = y0r[t] + p0(tt), r1 = y1r[t] + p1(tt);
+        if (p < m) {
+          lineA[kl + p] = r0;
+          lineB[kl + p] = r1;
+        }
+      }
+      if (threadIdx.x < hk) {
+        const int eb = ax.bord[threadIdx.x];
+        const double tb = fma((double)eb, ax.ho_ta, ax.ho_tb);
+        lineA[eb] = yb0 + p0(tb);
+        lineB[eb] = yb1 + p1(tb);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    } else
 #pragma unroll 4
     for (int p = threadIdx.x; p < m; p += kMixNT) {
       const double2 z = x[perm[p]];
@@ -366,7 +548,13 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
         }
     }
     __syncthreads();
+    if (tout && threadIdx.x == 0) {
+      bulk_s2g(o0, x, (uint32_t)n * 8);
+      if (o1) bulk_s2g(o1, reinterpret_cast<double*>(x) + n, (uint32_t)n * 8);
+      bulk_commit();
+    }
   }
+  if (threadIdx.x == 0) bulk_wait_read();  // shared memory stays valid until the last lines are read
 }
 
 }  // namespace fdb
