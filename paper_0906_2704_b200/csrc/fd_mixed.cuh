@@ -456,30 +456,96 @@ __global__ void __launch_bounds__(kMixNT, 2) k_msynth(AxisDev ax, LineIO io, Syn
     if (threadIdx.x == 0) bulk_wait_read();
     __syncthreads();
     double ua0[kHoMax], ua1[kHoMax];
-#pragma unroll
-    for (int l = 0; l < kHoMax; ++l) {
-      ua0[l] = l < hk ? f0(ho_coef_elem(ax, l), make_double2(ld0(l), 0.0)).x : 0.0;
-      ua1[l] = l < hk ? f1(ho_coef_elem(ax, l), make_double2(ld1(l), 0.0)).x : 0.0;
-    }
     long long nzb0 = 0, nzb1 = 0;  // all-zero filtered lines are written as exact zeros
-#pragma unroll 4
-    for (int kk = threadIdx.x; kk <= h; kk += kMixNT) {
-      const int e = kl + kk;
-      double2 X0, X1;
-      if (kk == 0) {
-        X0 = make_double2(ld0(hk), 0.0);
-        X1 = make_double2(ld1(hk), 0.0);
-      } else {
-        X0 = ldp0(hk + 2 * kk - 1);
-        X1 = ldp1(hk + 2 * kk - 1);
+    // Fast path (1D filter of a complex basis, aligned lines, h + 1 <= 8 NT):
+    // straight-line batches of four slots, every load of a batch -- coefficient
+    // pairs and spectral values -- issued before its first use.  The generic
+    // loop below runs slot after slot behind the filter's mode branches, one
+    // L2 round trip each (39 % of the kernel, 40 % long-scoreboard stalls).
+    const bool fast = sa.mode == 1 && sa.sp.mode == 1 && ax.cplx && v2 && h < kMixK * kMixNT;
+    if (fast) {
+      const double2* dA = sa.sp.dA;
+      const double* sA = sa.sp.sA;
+      const double* gz = has1 ? g1 : g0;  // a valid address for the absent partner line
+      auto fil = [&](double2 d, double sv, double mu) {  // conj(d) / (|d|^2 + mu s^2)
+        const double r = rcp_pos((d.x * d.x + d.y * d.y) + mu * sv * sv);
+        return make_double2(d.x * r, -d.y * r);
+      };
+      {
+        double2 bd[kHoMax];
+        double bs[kHoMax], c0[kHoMax], c1[kHoMax];
+#pragma unroll
+        for (int l = 0; l < kHoMax; ++l) {
+          const int lc = l < hk ? l : 0, e = ho_coef_elem(ax, lc);
+          bd[l] = __ldg(dA + e);
+          bs[l] = sA ? __ldg(sA + e) : 1.0;
+          c0[l] = __ldcs(g0 + lc);
+          c1[l] = __ldcs(gz + lc);
+        }
+#pragma unroll
+        for (int l = 0; l < kHoMax; ++l) {
+          ua0[l] = l < hk ? c0[l] * fil(bd[l], bs[l], mu0).x : 0.0;
+          ua1[l] = (l < hk && has1) ? c1[l] * fil(bd[l], bs[l], mu1).x : 0.0;
+        }
       }
-      X0 = f0(e, X0);
-      X1 = f1(e, X1);
-      nzb0 |= __double_as_longlong(X0.x) | __double_as_longlong(X0.y);
-      nzb1 |= __double_as_longlong(X1.x) | __double_as_longlong(X1.y);
-      // F^H v = conj(F conj v), v = X0 + i X1 (natural order input)
-      x[kk] = make_double2(X0.x - X1.y, -(X0.y + X1.x));
-      if (kk) x[m - kk] = make_double2(X0.x + X1.y, X0.y - X1.x);
+#pragma unroll
+      for (int b = 0; b < kMixK / 4; ++b) {
+        double2 c0[4], c1[4], d[4];
+        double sv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int kq = threadIdx.x + (4 * b + u) * kMixNT;
+          const int kk = kq <= h ? kq : h;
+          // (Re, Im) at [hk - 1 + 2 kk, hk + 2 kk] (16-byte aligned); X_0 is real, at [hk]
+          c0[u] = __ldcs(reinterpret_cast<const double2*>(g0 + hk - 1 + 2 * kk));
+          c1[u] = __ldcs(reinterpret_cast<const double2*>(gz + hk - 1 + 2 * kk));
+          d[u] = __ldg(dA + kl + kk);
+          sv[u] = sA ? __ldg(sA + kl + kk) : 1.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int kq = threadIdx.x + (4 * b + u) * kMixNT;
+          double2 X0 = c0[u], X1 = has1 ? c1[u] : czero();
+          if (kq == 0) {
+            X0 = make_double2(X0.y, 0.0);
+            X1 = make_double2(X1.y, 0.0);
+          }
+          X0 = cmul(X0, fil(d[u], sv[u], mu0));
+          X1 = cmul(X1, fil(d[u], sv[u], mu1));
+          if (kq <= h) {
+            nzb0 |= __double_as_longlong(X0.x) | __double_as_longlong(X0.y);
+            nzb1 |= __double_as_longlong(X1.x) | __double_as_longlong(X1.y);
+            // F^H v = conj(F conj v), v = X0 + i X1 (natural order input)
+            x[kq] = make_double2(X0.x - X1.y, -(X0.y + X1.x));
+            if (kq) x[m - kq] = make_double2(X0.x + X1.y, X0.y - X1.x);
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int l = 0; l < kHoMax; ++l) {
+        ua0[l] = l < hk ? f0(ho_coef_elem(ax, l), make_double2(ld0(l), 0.0)).x : 0.0;
+        ua1[l] = l < hk ? f1(ho_coef_elem(ax, l), make_double2(ld1(l), 0.0)).x : 0.0;
+      }
+#pragma unroll 4
+      for (int kk = threadIdx.x; kk <= h; kk += kMixNT) {
+        const int e = kl + kk;
+        double2 X0, X1;
+        if (kk == 0) {
+          X0 = make_double2(ld0(hk), 0.0);
+          X1 = make_double2(ld1(hk), 0.0);
+        } else {
+          X0 = ldp0(hk + 2 * kk - 1);
+          X1 = ldp1(hk + 2 * kk - 1);
+        }
+        X0 = f0(e, X0);
+        X1 = f1(e, X1);
+        nzb0 |= __double_as_longlong(X0.x) | __double_as_longlong(X0.y);
+        nzb1 |= __double_as_longlong(X1.x) | __double_as_longlong(X1.y);
+        // F^H v = conj(F conj v), v = X0 + i X1 (natural order input)
+        x[kk] = make_double2(X0.x - X1.y, -(X0.y + X1.x));
+        if (kk) x[m - kk] = make_double2(X0.x + X1.y, X0.y - X1.x);
+      }
     }
     zf_add(zf, it, (nzb0 != 0 ? 1 : 0) | (nzb1 != 0 ? 2 : 0));
     __syncthreads();
