@@ -18,6 +18,10 @@
 namespace fdb {
 
 constexpr int kMixMaxStages = 6;
+#ifndef FD_MIX_NT
+#define FD_MIX_NT 256
+#endif
+constexpr int kMixNTc = FD_MIX_NT;  // threads per CTA of k_manalyze / k_msynth (kMixNT below)
 // cos / sin (2 pi t / r) for t = 0 .. 6, radix r = 3 .. 13 (row r)
 constexpr int kMixMaxR = 13;
 __constant__ double c_mix_cos[kMixMaxR + 1][7];
@@ -113,11 +117,69 @@ __device__ __forceinline__ void mix_stage_first(double2* __restrict__ x, int N, 
   }
 }
 
+// Compile-time stage sequences (BASELINE config 1, d = 1: m = 4095 = 13 9 7 5):
+// block sizes, strides and item counts are constants, so the item -> (block,
+// j) split is a multiply-shift and every shared-memory offset an immediate --
+// the generic stages spend two of three issued instructions on that arithmetic.
+template <int N, int S, int R, int NT>
+__device__ __forceinline__ void mix_stage_c(double2* __restrict__ x, const MixTw& tw) {
+  constexpr int L = S / R, ITEMS = N / R, TSTEP = N / S;
+#pragma unroll 1
+  for (int it = threadIdx.x; it < ITEMS; it += NT) {
+    const int blk = it / L, j = it - blk * L;
+    double2* xb = x + blk * S + j;
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = xb[q * L];
+    mix_codelet<R>(v);
+    if constexpr (L > 1) mix_twiddle<R>(v, tw(j * TSTEP));
+#pragma unroll
+    for (int p = 0; p < R; ++p) xb[p * L] = v[p];
+  }
+}
+template <int N, int S, int NT, int R, int... REST>
+__device__ __forceinline__ void mix_stages_c(double2* x, const MixTw& tw) {
+  mix_stage_c<N, S, R, NT>(x, tw);
+  __syncthreads();
+  if constexpr (sizeof...(REST) > 0) mix_stages_c<N, S / R, NT, REST...>(x, tw);
+}
+template <int N, int R, int NT, class LD>
+__device__ __forceinline__ void mix_stage_first_c(double2* __restrict__ x, const MixTw& tw,
+                                                  LD&& ld) {
+  constexpr int L = N / R;
+#pragma unroll 1
+  for (int j = threadIdx.x; j < L; j += NT) {
+    double2 v[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) v[q] = ld(j + q * L);
+    mix_codelet<R>(v);
+    mix_twiddle<R>(v, tw(j));
+#pragma unroll
+    for (int p = 0; p < R; ++p) x[j + p * L] = v[p];
+  }
+}
+// the plan is the compile-time sequence 13 9 7 5
+__device__ __forceinline__ bool mix_plan_4095(const AxisDev& ax) {
+  return ax.m == 4095 && ax.mstages == 4 && ax.mrad[0] == 13 && ax.mrad[1] == 9 &&
+         ax.mrad[2] == 7 && ax.mrad[3] == 5;
+}
+
 // in-place DIF DFT of length ax.m (natural order in, mperm order out); with a
 // loader the first stage reads x_j = ld(j) (FIRST_LD)
 template <bool FIRST_LD = false, class LD = int, class AF = int>
 __device__ __forceinline__ void mix_dft(double2* x, const AxisDev& ax, const MixTw& tw, int nt,
                                         LD&& ld = 0, AF&& after_first = 0) {
+  if (mix_plan_4095(ax) && nt == kMixNTc) {
+    if constexpr (FIRST_LD) {
+      mix_stage_first_c<4095, 13, kMixNTc>(x, tw, ld);
+      after_first();  // before the stage barrier
+      __syncthreads();
+      mix_stages_c<4095, 315, kMixNTc, 9, 7, 5>(x, tw);
+    } else {
+      mix_stages_c<4095, 4095, kMixNTc, 13, 9, 7, 5>(x, tw);
+    }
+    return;
+  }
   int S = ax.m;
   int s0 = 0;
   if constexpr (FIRST_LD) {
