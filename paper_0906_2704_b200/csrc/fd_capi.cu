@@ -785,8 +785,13 @@ void build_mixed_plan(Axis& A, int m) {
   d.rader = 0;
   if (!mixed_enabled() || m < 9 || !(m & 1)) return;
   if (mix_smem_bytes(m, m + 4, 0) > 226 * 1024) return;  // the DFT buffer must fit one CTA's shared memory
-  const std::vector<int> rad = mixed_radices(m, {13, 11, 9, 7, 5, 3});
+  std::vector<int> rad = mixed_radices(m, {13, 11, 9, 7, 5, 3});
   if (!rad.empty()) {
+    // the smallest radix first: the analysis' first stage reads global memory,
+    // and its partial last round of items (315 items of radix 13 on 256
+    // threads: 59 threads with a second L2 round trip) kept the others at the
+    // stage barrier for 14 % of k_manalyze; radix-5 items are short
+    if (rad.size() > 1) std::rotate(rad.begin(), rad.end() - 1, rad.end());
     upload_plan(A, m, rad, nullptr);
     return;
   }

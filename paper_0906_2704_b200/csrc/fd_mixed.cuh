@@ -117,7 +117,7 @@ __device__ __forceinline__ void mix_stage_first(double2* __restrict__ x, int N, 
   }
 }
 
-// Compile-time stage sequences (BASELINE config 1, d = 1: m = 4095 = 13 9 7 5):
+// Compile-time stage sequences (BASELINE config 1, d = 1: m = 4095 = 5 13 9 7):
 // block sizes, strides and item counts are constants, so the item -> (block,
 // j) split is a multiply-shift and every shared-memory offset an immediate --
 // the generic stages spend two of three issued instructions on that arithmetic.
@@ -147,7 +147,7 @@ template <int N, int R, int NT, class LD>
 __device__ __forceinline__ void mix_stage_first_c(double2* __restrict__ x, const MixTw& tw,
                                                   LD&& ld) {
   constexpr int L = N / R;
-#pragma unroll 1
+#pragma unroll 2
   for (int j = threadIdx.x; j < L; j += NT) {
     double2 v[R];
 #pragma unroll
@@ -158,10 +158,10 @@ __device__ __forceinline__ void mix_stage_first_c(double2* __restrict__ x, const
     for (int p = 0; p < R; ++p) x[j + p * L] = v[p];
   }
 }
-// the plan is the compile-time sequence 13 9 7 5
+// the plan is the compile-time sequence 5 13 9 7 (build_mixed_plan's order)
 __device__ __forceinline__ bool mix_plan_4095(const AxisDev& ax) {
-  return ax.m == 4095 && ax.mstages == 4 && ax.mrad[0] == 13 && ax.mrad[1] == 9 &&
-         ax.mrad[2] == 7 && ax.mrad[3] == 5;
+  return ax.m == 4095 && ax.mstages == 4 && ax.mrad[0] == 5 && ax.mrad[1] == 13 &&
+         ax.mrad[2] == 9 && ax.mrad[3] == 7;
 }
 
 // in-place DIF DFT of length ax.m (natural order in, mperm order out); with a
@@ -171,12 +171,12 @@ __device__ __forceinline__ void mix_dft(double2* x, const AxisDev& ax, const Mix
                                         LD&& ld = 0, AF&& after_first = 0) {
   if (mix_plan_4095(ax) && nt == kMixNTc) {
     if constexpr (FIRST_LD) {
-      mix_stage_first_c<4095, 13, kMixNTc>(x, tw, ld);
+      mix_stage_first_c<4095, 5, kMixNTc>(x, tw, ld);
       after_first();  // before the stage barrier
       __syncthreads();
-      mix_stages_c<4095, 315, kMixNTc, 9, 7, 5>(x, tw);
+      mix_stages_c<4095, 819, kMixNTc, 13, 9, 7>(x, tw);
     } else {
-      mix_stages_c<4095, 4095, kMixNTc, 13, 9, 7, 5>(x, tw);
+      mix_stages_c<4095, 4095, kMixNTc, 5, 13, 9, 7>(x, tw);
     }
     return;
   }
