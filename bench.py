@@ -297,8 +297,9 @@ def launch_pixels(name, cfg, px_rank, restorations, launches_per_step):
     return px_rank * restorations / launches_per_step
 
 
-NCU_NAMES = {"k_analyze": ("k_ranalyze", "k_analyze"), "k_synth_filter": ("k_rsynth", "k_synth"),
-             "k_synth": ("k_rsynth", "k_synth")}
+NCU_NAMES = {"k_analyze": ("k_ranalyze", "k_canalyze", "k_analyze"),
+             "k_synth_filter": ("k_rsynth", "k_csynth", "k_synth"),
+             "k_synth": ("k_rsynth", "k_csynth", "k_synth")}
 NCU_NAMES.update({k: (k,) for k in PAIR_KERNELS})
 
 

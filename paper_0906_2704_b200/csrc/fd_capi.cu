@@ -28,7 +28,6 @@
 #include "fd_kernels.cuh"
 #include "fd_pair.cuh"
 #include "fd_mixed.cuh"
-#include "fd_mixed_staged.cuh"
 #include "fd_rader.cuh"
 #include "fd_gen.cuh"
 #include "fd_cdirect.cuh"
@@ -228,8 +227,6 @@ void init_runtime_once() {
       cudaMemcpyToSymbol(c_mix_sin, sn, sizeof(sn));
       cudaFuncSetAttribute(k_manalyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
       cudaFuncSetAttribute(k_msynth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
-      cudaFuncSetAttribute(k_manalyze_s, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
-      cudaFuncSetAttribute(k_msynth_s, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
       cudaFuncSetAttribute(k_qanalyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
       cudaFuncSetAttribute(k_qsynth, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
       cudaFuncSetAttribute(k_canalyze, cudaFuncAttributeMaxDynamicSharedMemorySize, kmax);
@@ -409,36 +406,6 @@ void launch_pair(const AxisDev& ax, const LineIO& io, const SynthArgs* sa, cudaS
     return;
   }
   if (ax.mstages > 0) {  // direct mixed-radix DFT (fd_mixed.cuh)
-    // FASTDEBLUR_MIXED_STAGED=1: the one-CTA-per-SM staged kernels
-    // (fd_mixed_staged.cuh) -- measured slower than two CTAs per SM (k_manalyze
-    // 3.3 vs 2.2 ms: the stages' uneven item counts idle a lone CTA at every
-    // barrier), kept for A/B timing
-    static const bool staged_on = [] {
-      const char* e = std::getenv("FASTDEBLUR_MIXED_STAGED");
-      return e && e[0] == '1';
-    }();
-    auto contiguous = [&](const Lines& g, const void* p) {
-      return g.elem_stride == 1 && g.per_item == 1 && g.item_stride == ax.n &&
-             (reinterpret_cast<uintptr_t>(p) & 15) == 0;
-    };
-    const size_t sms = mixs_smem_bytes(ax.m, ax.n, io.wout ? io.wstride : 0);
-    const bool staged =
-        staged_on && mixs_shape_ok(ax.m, ax.n, ax.mrad[0]) && sms <= 227 * 1024 &&
-        contiguous(io.gi, io.in) && contiguous(io.go, io.out) && !io.in_f32 && !io.out_f32 &&
-        (!io.wout || ((io.wstride & 31) == 0 && (reinterpret_cast<uintptr_t>(io.wout) & 15) == 0 &&
-                      (!io.wout32 || ((reinterpret_cast<uintptr_t>(io.wout32) & 15) == 0 &&
-                                      (reinterpret_cast<uintptr_t>(io.wout32lo) & 15) == 0)))) &&
-        (!sa || sa->mode == 0 || (sa->mode == 1 && sa->sp.mode == 1 && ax.cplx));
-    if (staged) {
-      const int grid = std::max(1, std::min(pairs, num_sms()));
-      if (sa) {
-        k_msynth_s<<<grid, kMixSNT, sms, st>>>(ax, io, *sa);
-      } else {
-        k_manalyze_s<<<grid, kMixSNT, sms, st>>>(ax, io);
-      }
-      launched(sa ? "k_msynth" : "k_manalyze");
-      return;
-    }
     // the analysis stages the pair's GCV weight rows when two CTAs still fit an SM
     int wslots = 0;
     if (!sa && io.wout && 2 * (mix_smem_bytes(ax.m, ax.n, io.wstride) + 1024) <= 227 * 1024)

@@ -51,7 +51,8 @@ def test_empty_batch(bc):
 
 
 @pytest.mark.parametrize("bc,n", [(O.HOC_FOURIER_D1, 1024), (O.HOC_FOURIER_D3, 1024),
-                                  (O.HOC_FOURIER_D1, 4096), (O.HOC_FOURIER, 1024)])
+                                  (O.HOC_FOURIER_D1, 4096), (O.HOC_FOURIER_D3, 4096),
+                                  (O.HOC_FOURIER, 1024)])
 @pytest.mark.parametrize("B", [1, 2, 127, 129, 257])
 def test_ragged_batches(bc, n, B):
     psf = onesided(15, 0.2)
@@ -121,3 +122,30 @@ def test_constant_and_zero_items_in_batch(bc):
     f = np_(rep.restored)
     assert np.max(np.abs(f[6])) == 0.0
     assert abs(np_(rep.mu_used)[6] - np.sqrt(search[0] * search[1])) < 1e-12
+
+
+@pytest.mark.parametrize("bc", [O.HOC_FOURIER_D1, O.HOC_FOURIER_D3])
+def test_pair_kernels_unaligned_input(bc):
+    """The n = 4096 line-pair kernels stage their input lines with bulk copies
+    and bulk-store their outputs when the lines are 16-byte aligned; a batch
+    that starts 8 bytes off takes their direct-access loads instead.  Both must
+    agree with the oracle, and a zero line among the items stays exactly zero
+    (zero-line flags of the staged and the direct path)."""
+    n, B = 4096, 5
+    psf = onesided(15, 0.2)
+    op, L, oop, s = _setup(bc, psf, n, 2)
+    g = _scenes(n, psf, B, 77)
+    g[3] = 0.0
+    big = torch.zeros(B * n + 1, dtype=torch.float64, device="cuda")
+    view = big[1:].view(B, n)
+    view.copy_(torch.from_numpy(g))
+    assert view.data_ptr() % 16 == 8
+    search = (1e-8, 1.0, 256)
+    want = O.deblur(oop, s, g, True, mu_min=search[0], mu_max=search[1], count=search[2])
+    for src in (view, torch.from_numpy(g).cuda()):
+        rep = P.deblur(op, L, src, P.MuChoice(True), search=P.GcvSearch(*search))
+        keep = [0, 1, 2, 4]
+        assert np.array_equal(np_(rep.best_k)[keep], want.best_k[keep])
+        assert np.max(np.abs(np_(rep.mu_used)[keep] / want.mu_used[keep] - 1)) < 1e-10
+        assert rel(np_(rep.restored)[keep], want.restored[keep]) < 1e-10
+        assert np.all(np_(rep.restored)[3] == 0.0)
