@@ -149,3 +149,22 @@ def test_pair_kernels_unaligned_input(bc):
         assert np.max(np.abs(np_(rep.mu_used)[keep] / want.mu_used[keep] - 1)) < 1e-10
         assert rel(np_(rep.restored)[keep], want.restored[keep]) < 1e-10
         assert np.all(np_(rep.restored)[3] == 0.0)
+
+
+@pytest.mark.parametrize("bc,n", [(O.HOC_FOURIER_D3, 250), (O.HOC_FOURIER_D3, 3000),
+                                  (O.HOC_FOURIER_D1, 3000), (O.HOC_FOURIER_D3, 2052)])
+def test_pair_kernels_other_fold_sizes(bc, n):
+    """Bluestein line-pair kernels at sizes other than config 1's: M = 512 (the
+    folded radix-2 stage without thread groups), and M = 8192 with m = 2997,
+    2999 (d = 1: one border column) and 2049 (the smallest m of that size) --
+    the staged output lines, weight rows and spectral table are sized by m."""
+    B = 7
+    psf = onesided(9, 0.25)
+    op, L, oop, s = _setup(bc, psf, n, 2)
+    g = _scenes(n, psf, B, 55 + n)
+    search = (1e-8, 1.0, 64)
+    rep = P.deblur(op, L, torch.from_numpy(g), P.MuChoice(True), search=P.GcvSearch(*search))
+    want = O.deblur(oop, s, g, True, mu_min=search[0], mu_max=search[1], count=search[2])
+    assert np.array_equal(np_(rep.best_k), want.best_k)
+    assert np.max(np.abs(np_(rep.mu_used) / want.mu_used - 1)) < 1e-9
+    assert rel(np_(rep.restored), want.restored) < 1e-9
