@@ -168,3 +168,30 @@ def test_pair_kernels_other_fold_sizes(bc, n):
     assert np.array_equal(np_(rep.best_k), want.best_k)
     assert np.max(np.abs(np_(rep.mu_used) / want.mu_used - 1)) < 1e-9
     assert rel(np_(rep.restored), want.restored) < 1e-9
+
+
+@pytest.mark.parametrize("bc", [O.HOC_FOURIER_D1, O.HOC_FOURIER_D3])
+def test_pair_kernels_run_to_run_identical(bc):
+    """The line-pair kernels hand data between thread groups, the bulk-copy
+    engine and the generic proxy through shared memory (staged input, output
+    lines assembled in the FFT buffer, skewed thread groups on named
+    barriers).  A missing barrier or fence shows up as run-to-run differences:
+    three restorations of the same 2,049-item batch (persistent CTAs with
+    several pairs each, odd count) must agree bit for bit."""
+    n, B = 4096, 2049
+    cfg = W.config(1)
+    _, g = W.signals_1d(cfg, 3, B)
+    op = P.build_operator(cfg.psf, n, bc)
+    L = P.smoothing_eigenvalues(2, op)
+    gd = torch.from_numpy(g).cuda()
+    outs = []
+    for _ in range(3):
+        rep = P.deblur(op, L, gd, P.MuChoice(True),
+                       search=P.GcvSearch(cfg.mu_min, cfg.mu_max, cfg.count))
+        torch.cuda.synchronize()
+        outs.append((rep.restored.clone(), rep.mu_used.clone(), rep.best_k.clone()))
+    for f, mu, k in outs[1:]:
+        assert torch.equal(f, outs[0][0])
+        assert torch.equal(mu, outs[0][1])
+        assert torch.equal(k, outs[0][2])
+    assert torch.isfinite(outs[0][0]).all()
