@@ -129,9 +129,15 @@ struct SkewSpin {
   }
 };
 
-template <int LOGM, int NT, int KERN = 0, class SKEW = SkewSpin>
+struct SkewNone {
+  __device__ __forceinline__ void operator()() const {}
+};
+// TAIL: what the lower half's group does after its passes, while the (late)
+// upper group finishes
+template <int LOGM, int NT, int KERN = 0, class SKEW = SkewSpin, class TAIL = SkewNone>
 __device__ __forceinline__ void pair_conv(double2* x, const FftTables& T, const TwSm& tw, int m,
-                                          long long& pclk_, SKEW skew = SKEW()) {
+                                          long long& pclk_, SKEW skew = SKEW(),
+                                          TAIL tail = TAIL()) {
   using S = PairShape<LOGM>;
   if constexpr (S::FOLD) {
     static_assert(NT % (1 << FoldTw<LOGM>::LOB) == 0, "FoldTw needs NT % lo length == 0");
@@ -144,14 +150,20 @@ __device__ __forceinline__ void pair_conv(double2* x, const FftTables& T, const 
 #ifdef FD_PHASE_CLOCKS
     if constexpr (LOGM == 13) {
       bluestein_rec_clk<LOGM, 1, S::HM, NT, KERN, 2, GRP>(x, T.bhat, tw, S::M, pclk_);
-      if constexpr (GRP != 0) __syncthreads();
+      if constexpr (GRP != 0) {
+        if (threadIdx.x < GRP) tail();
+        __syncthreads();
+      }
       pair_combine<LOGM, NT>(x, tw, m);
       FD_PCLK(KERN, 7);
       return;
     }
 #endif
     bluestein_rec<LOGM, 1, S::HM, NT, false, GRP>(x, T.bhat, tw, S::M);
-    if constexpr (GRP != 0) __syncthreads();
+    if constexpr (GRP != 0) {
+      if (threadIdx.x < GRP) tail();
+      __syncthreads();
+    }
     pair_combine<LOGM, NT>(x, tw, m);
   } else {
     bluestein_t<LOGM, NT>(x, T, tw, m);
@@ -435,6 +447,11 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
       } else {
         SkewSpin()();
       }
+    }, [&] {
+      if (tf_l0 >= 0) {
+        const int ntask = (int)(io.wstride >> 1);
+        tf32_rows(tf_l0, (int)threadIdx.x, GRPK, 0, (ntask / 2) & ~1);
+      }
     });
     tf_l0 = -1;
     // the post phase reads [0, m) only: stage the next pair behind it
@@ -472,7 +489,7 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
     constexpr int KSA = PS::FOLD ? (PS::HM / 2 + NT) / NT : 1;
     const bool tout = PS::FOLD && pair_out_staged(o0, o1, n, io.go.elem_stride) && (hk & 1);
     // ... and so do the fp64 weight rows (staged in the area the synthesis
-    // kernel keeps its spectral table in); their TF32 tiles are then written
+    // kernel keeps its spectral table in); their TF32 tiles are written
     // chunk-wise from the staged rows: one lane per (16-byte chunk, line), so a
     // store instruction touches 16 lines instead of the 32 that per-element
     // 4-byte stores did (~2 clocks per line touched: 11 % of the kernel)
@@ -539,10 +556,15 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
         // with thread groups, the upper group writes the second half of the
         // tiles in the next pair's skew slot (~1200 clocks of store work
         // instead of a spin)
-        const int ntask = (int)(io.wstride >> 1);
-        const int nnow = GRPK != 0 ? (ntask / 2) & ~1 : ntask;
-        tf32_rows(l0, threadIdx.x, NT, 0, nnow);
-        if constexpr (GRPK != 0) tf_l0 = l0;
+        // with thread groups the tiles are written during the NEXT pair's
+        // convolution: the second half by the upper group in its skew slot
+        // (work instead of a spin), the first half by the lower group while it
+        // waits for the upper one to finish
+        if constexpr (GRPK != 0) {
+          tf_l0 = l0;
+        } else {
+          tf32_rows(l0, threadIdx.x, NT, 0, (int)(io.wstride >> 1));
+        }
       }
     } else
     for (int kk = threadIdx.x; kk <= h; kk += NT) {
@@ -590,10 +612,8 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
     }
     FD_PCLK(0, 8);
   }
-  if (tf_l0 >= 0) {  // the last pair's deferred tiles
-    const int ntask = (int)(io.wstride >> 1);
-    tf32_rows(tf_l0, threadIdx.x, NT, (ntask / 2) & ~1, ntask);
-  }
+  if (tf_l0 >= 0)  // the last pair's deferred tiles
+    tf32_rows(tf_l0, threadIdx.x, NT, 0, (int)(io.wstride >> 1));
   if (threadIdx.x == 0) bulk_wait_read();  // shared memory stays valid until the last lines are read
 }
 
