@@ -1556,6 +1556,66 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
     // C2R pre-pass over the closed index groups {k, h-k}: X = herm(c),
     // Zin_k = (X_k + X_{k+h}) + i (X_k - X_{k+h}) W^{-k}; Bluestein input conj(Zin) c_k.
     // Each coefficient is read exactly once, straight from global memory.
+    auto zin = [&](int kk, double2 Xa, double2 Xb) {
+      const double2 Od = cmulc(csub(Xa, Xb), rtw(kk));
+      const double2 Ev = cadd(Xa, Xb);
+      return make_double2(Ev.x - Od.y, Ev.y + Od.x);
+    };
+    // Fast path (packed Fourier line, 1D filter of a complex basis, h / 2 < 4
+    // blockDim): straight-line batches of two groups, the coefficient pairs and
+    // the spectral values of a batch all requested before the first is used.
+    // The generic loop below runs group after group behind the filter's mode
+    // branches, one cache round trip each (see k_msynth).
+    const bool fastpk = pk && sa.mode == 1 && sa.sp.mode == 1 && ax.cplx &&
+                        h / 2 < 4 * (int)blockDim.x;
+    if (fastpk) {
+      const double2* dA = sa.sp.dA;
+      const double* sA = sa.sp.sA;
+      const int kl = ax.kl;
+      auto fil = [&](double2 d, double sv) {  // conj(d) / (|d|^2 + mu s^2)
+        const double r = rcp_pos((d.x * d.x + d.y * d.y) + mu * sv * sv);
+        return make_double2(d.x * r, -d.y * r);
+      };
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        double2 ck[2], cp[2], dk[2], dp[2];
+        double sk[2], sp[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int kq = threadIdx.x + (2 * b + u) * blockDim.x;
+          const int k = kq <= h / 2 ? kq : h / 2;
+          const int kp = k == 0 ? 0 : h - k;
+          // k = 0: the packed pair (X_0, X_h), two real coefficients at e = kl, kl + h
+          ck[u] = ldp(off + k);
+          cp[u] = ldp(off + kp);
+          dk[u] = __ldg(dA + kl + k);
+          sk[u] = sA ? __ldg(sA + kl + k) : 1.0;
+          const int ep = k == 0 ? kl + h : kl + kp;
+          dp[u] = __ldg(dA + ep);
+          sp[u] = sA ? __ldg(sA + ep) : 1.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int k = threadIdx.x + (2 * b + u) * blockDim.x;
+          if (k > h / 2) continue;
+          const int kp = k == 0 ? 0 : h - k;
+          double2 Xk, Xkh, Xp, Xph;
+          if (k == 0) {
+            Xk = Xp = cmul(make_double2(ck[u].x, 0.0), fil(dk[u], sk[u]));
+            Xkh = Xph = cmul(make_double2(ck[u].y, 0.0), fil(dp[u], sp[u]));
+          } else {
+            const double2 fk = cmul(ck[u], fil(dk[u], sk[u]));
+            const double2 fp = kp != k ? cmul(cp[u], fil(dp[u], sp[u])) : fk;
+            Xk = fk;
+            Xp = fp;
+            Xkh = cconj(fp);  // m - (k+h) = kp
+            Xph = cconj(fk);
+          }
+          x[pidx(k)] = cmul(cconj(zin(k, Xk, Xkh)), chirp_at(k));
+          if (kp != k) x[pidx(kp)] = cmul(cconj(zin(kp, Xp, Xph)), chirp_at(kp));
+        }
+      }
+    } else
     for (int k = threadIdx.x; k <= h / 2; k += blockDim.x) {
       const int kp = k == 0 ? 0 : h - k;
       double2 Xk, Xkh, Xp, Xph;  // X at k, k+h, kp, kp+h
@@ -1581,11 +1641,6 @@ __global__ void __launch_bounds__(256, 2) k_rsynth(AxisDev ax, LineIO io, SynthA
         Xp = cscale(cadd(vp, cconj(k == 0 ? vp : vkh)), 0.5);
         Xph = cscale(cadd(vph, cconj(k == 0 ? vph : vk)), 0.5);
       }
-      auto zin = [&](int kk, double2 Xa, double2 Xb) {
-        const double2 Od = cmulc(csub(Xa, Xb), rtw(kk));
-        const double2 Ev = cadd(Xa, Xb);
-        return make_double2(Ev.x - Od.y, Ev.y + Od.x);
-      };
       x[pidx(k)] = cmul(cconj(zin(k, Xk, Xkh)), chirp_at(k));
       if (kp != k) x[pidx(kp)] = cmul(cconj(zin(kp, Xp, Xph)), chirp_at(kp));
     }
