@@ -767,7 +767,8 @@ __device__ __forceinline__ double2 coeff_at(const AxisDev& ax, const LineIO& io,
   } else {
     c = ldc(io.in, io.in_cplx, off + e * io.gi.elem_stride);
   }
-  return coeff_filter(ax, sa, io.gi, l, e, c, line_mu(sa, io.gi, l));
+  // one reciprocal instead of the filter's two divisions (<= 1 ulp, as the real-line kernels)
+  return coeff_filter_fast(ax, sa, io.gi, l, e, c, line_mu(sa, io.gi, l));
 }
 
 template <int LOGM>
