@@ -486,7 +486,8 @@ __global__ void __launch_bounds__(PairShape<LOGM, WIDE>::NT, 1) k_panalyze(AxisD
     // FOLD sizes: the packed coefficient lines are assembled in shared memory
     // (the buffer's lower part, free once every thread has read its Z_k) and
     // leave as two bulk stores; only the GCV weights take the store path
-    constexpr int KSA = PS::FOLD ? (PS::HM / 2 + NT) / NT : 1;
+    // kk <= h slots: M >= 2 m - 1 and m odd give h = (m - 1) / 2 <= HM / 2 - 1
+    constexpr int KSA = PS::FOLD ? (PS::HM / 2 + NT - 1) / NT : 1;
     const bool tout = PS::FOLD && pair_out_staged(o0, o1, n, io.go.elem_stride) && (hk & 1);
     // ... and so do the fp64 weight rows (staged in the area the synthesis
     // kernel keeps its spectral table in); their TF32 tiles are written
@@ -641,7 +642,8 @@ __global__ void __launch_bounds__(PairShape<LOGM, true>::NT, 1) k_psynth(AxisDev
   double* out = reinterpret_cast<double*>(io.out);
   const double isq = ax.inv_sqrt_m;
   using PS = PairShape<LOGM, true>;
-  constexpr int KS = PS::FOLD ? (PS::HM / 2 + NT) / NT : 1;  // kk slots (kk <= h < HM/2+1)
+  // kk slots: M >= 2 m - 1 and m odd give h = (m - 1) / 2 <= HM / 2 - 1
+  constexpr int KS = PS::FOLD ? (PS::HM / 2 + NT - 1) / NT : 1;
   // 1D filter (one spectral table for every line): the table lives in shared
   // memory -- the per-pair reads from L2 were latency bound (27 % of the kernel
   // at config 1); the border coefficients' entries sit in the extras slots
